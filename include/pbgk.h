@@ -1,0 +1,124 @@
+/*
+ * pbgk.h — C ABI of the B200 fine kinetic propagator (libpbgk.so).
+ *
+ * Drop-in boundary for the hot path of arXiv 2502.02704's reference package
+ * `parabgk` (Python/numpy; /root/reference/pkg/src/parabgk, "ref/" below).
+ * The reference has no FFI of its own: its boundary is the Python API
+ * re-exported at ref/__init__.py:8-31.  Each entry point here replaces the
+ * numpy body of one reference function; the Python host package
+ * `paper_2502_02704_b200` keeps the reference signatures and calls these
+ * through ctypes (see INTEGRATION.md for the binding a parabgk maintainer
+ * would add).
+ *
+ * Conventions
+ *  - All array arguments are DEVICE pointers (cudaMalloc / torch CUDA
+ *    storage) unless named h_*; fp64 only; C order.
+ *  - Distribution f: double[nx][nvx][nvy][nvz] (ref/lifting.py:16-23).
+ *  - Moments: double[5][nx] = rho, u_x, u_y, u_z, theta (ref/moments.py:29-34).
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).
+ *  - Return value: 0 on success, negative on an API/CUDA failure (message in
+ *    pbgk_last_error()).  Numerical failures are NOT return codes: when
+ *    `h_code` is non-NULL the call synchronises `stream` and stores the
+ *    solver status there: -1 = clean, otherwise the key
+ *        (unit << 40) | (step << 8) | kind
+ *    (unit = window / slice index where it applies, else 0) with
+ *      kind 0  rho <= 0 in a projection        -> DegenerateStateError
+ *      kind 1  degenerate state in lift or in
+ *              conserved->primitive            -> DegenerateStateError
+ *      kind 2  non-finite state after `step`    -> BlowUpError(step)
+ *      kind 3  rho or p <= 0 in G after `step`  -> BlowUpError(step)
+ *      kind 4  correction overshoot             -> CorrectionOvershootError(unit)
+ *    Keys are min-reduced: lowest unit, then earliest step, then the
+ *    reference's raise order within a step (ref/moments.py:102-104,
+ *    ref/lifting.py:44-45, ref/kinetic.py:157-159, ref/fluid.py:117-122).
+ */
+#ifndef PBGK_H
+#define PBGK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pbgk_ctx pbgk_ctx;
+
+/* Phase grid + boundary (ref/grid.py:39-87, :89-116). */
+typedef struct pbgk_grid_desc {
+  int32_t nx, nvx, nvy, nvz;
+  double x_min, x_max, v_max;
+  int32_t periodic; /* 1: BoundaryKind.PERIODIC, 0: BoundaryKind.ABSORBING */
+  int32_t device;   /* CUDA device ordinal the context (and every call on it) uses */
+} pbgk_grid_desc;
+
+/* Library identification. */
+int pbgk_version(void);
+const char* pbgk_last_error(void);
+
+/* Context: grid constants, tiling, device workspace (tables, partials). */
+int pbgk_ctx_create(const pbgk_grid_desc* grid, pbgk_ctx** out);
+void pbgk_ctx_destroy(pbgk_ctx* ctx);
+/* Workspace bytes held by a context (diagnostics). */
+size_t pbgk_ctx_workspace_bytes(const pbgk_ctx* ctx);
+
+/* lift(U, grid, normalize_mass) — replaces ref/lifting.py:36-58. */
+int pbgk_lift(pbgk_ctx* ctx, const double* mom, int normalize_mass, double* f_out, void* stream,
+              long long* h_code);
+
+/* project(f, grid) — replaces ref/moments.py:91-113. */
+int pbgk_project(pbgk_ctx* ctx, const double* f, double* mom_out, void* stream, long long* h_code);
+
+/* transport_update(f, dt, grid, params, bc) — replaces ref/kinetic.py:86-124.
+ * E: per-cell field (nx) or NULL; e_max = max|E| (field term only if > 0). */
+int pbgk_transport(pbgk_ctx* ctx, const double* f, double* f_out, double dt, const double* E,
+                   double e_max, void* stream);
+
+/* bgk_relax(f, dt, grid, params) — replaces ref/kinetic.py:127-134.
+ * lambda = dt*tau/eps with tau = tau_cells[i] when tau_cells != NULL. */
+int pbgk_relax(pbgk_ctx* ctx, const double* f, double* f_out, double dt, double eps, double tau,
+               const double* tau_cells, void* stream, long long* h_code);
+
+/* Finiteness guard of ref/kinetic.py:157-159 on a distribution: status key
+ * (0 << 40) | (step << 8) | 2 if any value of f is NaN/Inf. */
+int pbgk_check_finite(pbgk_ctx* ctx, const double* f, int step, void* stream, long long* h_code);
+
+/* The fine propagator loop of propagate_kinetic (ref/kinetic.py:137-161) for a
+ * given step schedule h_dts[0..nsteps) (computed by the caller exactly as the
+ * reference does, ref/kinetic.py:146-156).
+ * Start: f0 (distribution) or, when f0 == NULL, mom0 (the window lift
+ *   L(U) of ref/parareal.py:129, never materialised).
+ * End:   f_out receives f_S when write_final != 0; mom_out (may be NULL)
+ *   receives P(f_S) (ref/parareal.py:136).  f_tmp is a second f-sized buffer
+ *   (ping-pong); f0 must not alias f_out or f_tmp. */
+int pbgk_propagate(pbgk_ctx* ctx, const double* f0, const double* mom0, double* f_out,
+                   double* f_tmp, int write_final, double* mom_out, int nsteps,
+                   const double* h_dts, double eps, double tau, const double* E, double e_max,
+                   void* stream, long long* h_code);
+
+/* Coarse Euler propagator G (ref/fluid.py:91-125) on one GPU: advance
+ * `nwin` independent primitive states mom_in[w] (double[nwin][5][nx]) over
+ * [h_t0[w], h_t1[w]] into mom_out[w]; when `minuend` is non-NULL the output
+ * is minuend[w] - G(mom_in[w]) (the parareal jump, ref/parareal.py:142).
+ * dt_max <= 0 means no cap.  force: per-cell E or NULL.  Failure keys carry
+ * the window index (0-based) as unit. */
+int pbgk_fluid_propagate(pbgk_ctx* ctx, int nwin, const double* mom_in, double* mom_out,
+                         const double* minuend, const double* h_t0, const double* h_t1,
+                         double dt_max, double cfl, const double* force, void* stream,
+                         long long* h_code);
+
+/* Sequential parareal correction (ref/parareal.py:217-248) on one GPU:
+ *   U_n = G(U_{n-1}) + jump_n   for n = start..n_g  (primitive variables),
+ * snaps: double[n_g+1][5][nx] (updated in place from index start),
+ * old:   double[n_g+1][5][nx] (iterate before the correction),
+ * jumps: double[n_g][5][nx];  h_times: coarse times (n_g+1).
+ * h_err receives the successive-iterate sup error; failure keys carry the
+ * 1-based slice index as unit (kind 4: CorrectionOvershootError). */
+int pbgk_parareal_correct(pbgk_ctx* ctx, int n_g, int start, double* snaps, const double* old,
+                          const double* jumps, const double* h_times, double dt_max, double cfl,
+                          const double* force, void* stream, double* h_err, long long* h_code);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PBGK_H */

@@ -1,0 +1,482 @@
+"""Numpy restatement of the reference hot path (TEST INFRASTRUCTURE ONLY).
+
+This module is the CPU checker for the CUDA path in ``paper_2502_02704_b200``.
+It restates, operation for operation, the arithmetic of the reference package
+``parabgk`` (``/root/reference/pkg/src/parabgk``; abbreviated ``ref/`` below)
+so that on the same inputs it reproduces the reference bit for bit.  The pin is
+``tests/test_oracle.py`` (reference imported where present, golden vectors in
+``tests/golden/`` everywhere else).
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU legs may
+use it.  The product never imports it and has no CPU fallback.
+
+Conventions: a distribution is an ``(nx, nvx, nvy, nvz)`` float64 C-order
+array; a moment state is the triple ``(rho (nx,), u (nx, 3), theta (nx,))``.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+GUARD = 1e-12  # ref/kinetic.py:39 and ref/fluid.py:30 (span guard)
+
+
+class OracleError(Exception):
+    """Base of the oracle's failure signals (mirrors ref/errors.py:4-29)."""
+
+
+class OracleConfigError(OracleError):
+    pass
+
+
+class OracleDegenerate(OracleError):
+    pass
+
+
+class OracleBlowUp(OracleError):
+    def __init__(self, msg, step=None):
+        super().__init__(msg)
+        self.step = step
+
+
+class OracleOvershoot(OracleError):
+    def __init__(self, msg, slice_index=None):
+        super().__init__(msg)
+        self.slice_index = slice_index
+
+
+# --------------------------------------------------------------------------
+# meshes (ref/grid.py:89-127)
+# --------------------------------------------------------------------------
+
+@dataclass
+class Mesh:
+    """Phase-space mesh: x cells plus a per-axis velocity cube."""
+
+    x_min: float
+    x_max: float
+    nx: int
+    v_max: float
+    nv: tuple
+
+    def __post_init__(self):
+        self.nv = tuple(int(n) for n in self.nv)
+        # ref/grid.py:95-96
+        self.dx = (self.x_max - self.x_min) / self.nx
+        self.xc = self.x_min + (np.arange(self.nx) + 0.5) * self.dx
+        # ref/grid.py:100-103, 114-115
+        self.dv = tuple(2.0 * self.v_max / n for n in self.nv)
+        self.vc = tuple((np.arange(n) - (n - 1) / 2.0) * (2.0 * self.v_max / n)
+                        for n in self.nv)
+        # ref/grid.py:57-59
+        self.dvol = self.dv[0] * self.dv[1] * self.dv[2]
+
+
+def coarse_grid(t_final: float, n_g: int, n_f: int):
+    """(times, dt_g, dt_f) of ref/grid.py:119-127."""
+    return np.linspace(0.0, t_final, n_g + 1), t_final / n_g, t_final / n_f
+
+
+# --------------------------------------------------------------------------
+# moments: P (ref/moments.py:80-129)
+# --------------------------------------------------------------------------
+
+def marginals(f: np.ndarray):
+    """Three per-cell velocity marginals (ref/moments.py:100)."""
+    return (np.add.reduce(f, axis=(2, 3)), np.add.reduce(f, axis=(1, 3)),
+            np.add.reduce(f, axis=(1, 2)))
+
+
+def _mirror_weighted(m: np.ndarray, c: np.ndarray) -> np.ndarray:
+    # ref/moments.py:80-88: mirrored pairs are differenced before weighting.
+    n = c.size
+    k = n // 2
+    return np.matmul(m[:, :k] - m[:, : n - k - 1: -1], c[:k])
+
+
+def moments_of(margs, mesh: Mesh):
+    """(rho, u, theta) from marginals (ref/moments.py:101-113)."""
+    w = mesh.dvol
+    rho = np.add.reduce(margs[0], axis=1) * w
+    if np.any(rho <= 0.0):
+        raise OracleDegenerate("rho <= 0 in projection at cell %d"
+                               % int(np.argmax(rho <= 0.0)))
+    ru = np.stack([_mirror_weighted(margs[a], mesh.vc[a]) for a in range(3)],
+                  axis=1) * w
+    u = ru / rho[:, None]
+    acc = np.zeros_like(rho)
+    for a in range(3):
+        d = mesh.vc[a][None, :] - u[:, a, None]
+        acc += np.einsum("ij,ij->i", d * d, margs[a])
+    theta = acc * w / (3.0 * rho)
+    return rho, u, theta
+
+
+def project(f: np.ndarray, mesh: Mesh):
+    """P: ref/moments.py:91-113."""
+    return moments_of(marginals(f), mesh)
+
+
+# --------------------------------------------------------------------------
+# lifting: L (ref/lifting.py:36-58)
+# --------------------------------------------------------------------------
+
+def maxwell_factors(rho, u, theta, mesh: Mesh):
+    """Separable Maxwellian factors (gx*amp, gy, gz) of ref/lifting.py:44-50."""
+    if np.any(rho <= 0.0) or np.any(theta <= 0.0):
+        raise OracleDegenerate("lift needs rho > 0 and theta > 0")
+    h = 1.0 / (2.0 * theta)
+    g = []
+    for a in range(3):
+        d = mesh.vc[a][None, :] - u[:, a, None]
+        g.append(np.exp(-(d * d) * h[:, None]))
+    amp = rho / (2.0 * np.pi * theta) ** 1.5
+    return g[0] * amp[:, None], g[1], g[2]
+
+
+def lift(rho, u, theta, mesh: Mesh, normalize: bool = False) -> np.ndarray:
+    """L: ref/lifting.py:36-58 (outer product, optional per-cell mass fix)."""
+    gxa, gy, gz = maxwell_factors(rho, u, theta, mesh)
+    f = gxa[:, :, None, None] * gy[:, None, :, None] * gz[:, None, None, :]
+    if normalize:
+        mass = np.add.reduce(f, axis=(1, 2, 3)) * mesh.dvol
+        f *= (rho / mass)[:, None, None, None]
+    return f
+
+
+def maxwellian_point(rho, u, theta, v):
+    """Scalar Maxwellian (ref/lifting.py:26-33)."""
+    if theta <= 0.0:
+        raise OracleDegenerate("theta <= 0")
+    q = np.sum((np.asarray(v, float) - np.asarray(u, float)) ** 2)
+    return float(rho / (2.0 * np.pi * theta) ** 1.5 * np.exp(-q / (2.0 * theta)))
+
+
+# --------------------------------------------------------------------------
+# fine propagator F (ref/kinetic.py:77-161)
+# --------------------------------------------------------------------------
+
+def field_bound(force) -> float:
+    """max |E| (ref/kinetic.py:71-74)."""
+    return 0.0 if force is None else float(np.max(np.abs(force)))
+
+
+def fine_cap(mesh: Mesh, cfl: float, force=None) -> float:
+    """CFL cap of ref/kinetic.py:77-83 (cube bound v_max, not the last centre)."""
+    rate = mesh.v_max / mesh.dx
+    e = field_bound(force)
+    if e > 0.0:
+        rate += e / mesh.dv[0]
+    return cfl / rate
+
+
+def transport(f: np.ndarray, dt: float, mesh: Mesh, periodic: bool,
+              force=None) -> np.ndarray:
+    """Explicit upwind-x + Rusanov-v_x step (ref/kinetic.py:86-124)."""
+    nx = f.shape[0]
+    c = mesh.vc[0]
+    cpos = np.maximum(c, 0.0)[None, :, None, None]
+    cneg = np.minimum(c, 0.0)[None, :, None, None]
+    g = np.empty((nx + 2,) + f.shape[1:])
+    g[1:-1] = f
+    if periodic:
+        g[0], g[-1] = f[-1], f[0]
+    else:
+        g[0], g[-1] = 0.0, 0.0
+    fl = cpos * g[:-1] + cneg * g[1:]
+    out = f - (dt / mesh.dx) * (fl[1:] - fl[:-1])
+    e = field_bound(force)
+    if e > 0.0:
+        E = force[:, None, None, None]
+        a, b = f[:, :-1], f[:, 1:]
+        G = 0.5 * E * (a + b) - 0.5 * e * (b - a)
+        r = dt / mesh.dv[0]
+        out[:, 0] -= r * G[:, 0]
+        out[:, 1:-1] -= r * (G[:, 1:] - G[:, :-1])
+        out[:, -1] -= r * (-G[:, -1])
+    return out
+
+
+def unit_tau(rho, theta):
+    """Default collision frequency (ref/kinetic.py:42-44)."""
+    return 1.0
+
+
+def relax(fs: np.ndarray, dt: float, mesh: Mesh, eps: float,
+          tau: Callable = unit_tau) -> np.ndarray:
+    """Implicit BGK blend (ref/kinetic.py:127-134)."""
+    rho, u, theta = project(fs, mesh)
+    lam = dt * np.asarray(tau(rho, theta), dtype=float) / eps
+    lam = np.broadcast_to(lam, rho.shape)[:, None, None, None]
+    M = lift(rho, u, theta, mesh, normalize=True)
+    return (fs + lam * M) / (1.0 + lam)
+
+
+def fine_schedule(t0: float, t1: float, cap: float) -> list:
+    """The dt sequence of ref/kinetic.py:146-160 (Python-float arithmetic)."""
+    span = t1 - t0
+    out = []
+    done = 0.0
+    while span - done > GUARD * span:
+        d = min(cap, span - done)
+        out.append(d)
+        done += d
+    return out
+
+
+def fine_propagate(f0: np.ndarray, t0: float, t1: float, mesh: Mesh,
+                   eps: float, periodic: bool, force=None, dt_max=None,
+                   cfl: float = 0.5, tau: Callable = unit_tau) -> np.ndarray:
+    """F over [t0, t1] (ref/kinetic.py:137-161)."""
+    if t1 < t0:
+        raise OracleConfigError("t1 < t0")
+    if t1 - t0 == 0.0:
+        return f0
+    cap = fine_cap(mesh, cfl, force)
+    if dt_max is not None:
+        cap = min(cap, dt_max)
+    f = f0
+    for s, d in enumerate(fine_schedule(t0, t1, cap), start=1):
+        f = transport(f, d, mesh, periodic, force)
+        f = relax(f, d, mesh, eps, tau)
+        if not np.all(np.isfinite(f)):
+            raise OracleBlowUp("non-finite at step %d" % s, step=s)
+    return f
+
+
+# --------------------------------------------------------------------------
+# coarse propagator G (ref/fluid.py:39-125, ref/moments.py:116-129)
+# --------------------------------------------------------------------------
+
+def to_conserved(rho, u, theta) -> np.ndarray:
+    """Packed (nx, 5) conserved state (ref/moments.py:116-119, 59-72)."""
+    out = np.empty((rho.shape[0], 5))
+    out[:, 0] = rho
+    out[:, 1:4] = rho[:, None] * u
+    out[:, 4] = 0.5 * rho * np.einsum("ij,ij->i", u, u) + 1.5 * rho * theta
+    return out
+
+
+def to_primitive(v: np.ndarray):
+    """ref/moments.py:122-129 on a packed state."""
+    rho = v[:, 0].copy()
+    mom = v[:, 1:4].copy()
+    en = v[:, 4].copy()
+    if np.any(rho <= 0.0):
+        raise OracleDegenerate("rho <= 0 in conserved state")
+    u = mom / rho[:, None]
+    eint = en - 0.5 * np.einsum("ij,ij->i", mom, u)
+    if np.any(eint <= 0.0):
+        raise OracleDegenerate("internal energy <= 0")
+    return rho, u, eint / (1.5 * rho)
+
+
+def pressure(v: np.ndarray) -> np.ndarray:
+    """ref/fluid.py:39-42."""
+    ke = 0.5 * (v[..., 1] ** 2 + v[..., 2] ** 2 + v[..., 3] ** 2) / v[..., 0]
+    return (v[..., 4] - ke) / 1.5
+
+
+def euler_flux(v: np.ndarray) -> np.ndarray:
+    """ref/fluid.py:45-56."""
+    v = np.asarray(v, dtype=float)
+    ux = v[..., 1] / v[..., 0]
+    p = pressure(v)
+    h = np.empty_like(v)
+    h[..., 0] = v[..., 1]
+    h[..., 1] = v[..., 1] * ux + p
+    h[..., 2] = v[..., 2] * ux
+    h[..., 3] = v[..., 3] * ux
+    h[..., 4] = ux * (v[..., 4] + p)
+    return h
+
+
+def rusanov(vl: np.ndarray, vr: np.ndarray) -> np.ndarray:
+    """ref/fluid.py:59-66."""
+    vl = np.asarray(vl, dtype=float)
+    vr = np.asarray(vr, dtype=float)
+    sl = np.abs(vl[..., 1] / vl[..., 0]) + np.sqrt(pressure(vl) / vl[..., 0])
+    sr = np.abs(vr[..., 1] / vr[..., 0]) + np.sqrt(pressure(vr) / vr[..., 0])
+    s = np.maximum(sl, sr)
+    return 0.5 * (euler_flux(vl) + euler_flux(vr)) - 0.5 * s[..., None] * (vr - vl)
+
+
+def coarse_cap(v: np.ndarray, dx: float, cfl: float) -> float:
+    """ref/fluid.py:69-75 on a packed state."""
+    ux = v[:, 1] / v[:, 0]
+    th = pressure(v) / v[:, 0]
+    return cfl * dx / float(np.max(np.abs(ux) + np.sqrt(th)))
+
+
+def coarse_propagate(rho, u, theta, t0, t1, mesh: Mesh, periodic: bool,
+                     force=None, dt_max=None, cfl: float = 0.9):
+    """G over [t0, t1] (ref/fluid.py:91-125); returns (rho, u, theta)."""
+    if t1 < t0:
+        raise OracleConfigError("t1 < t0")
+    span = t1 - t0
+    if span == 0.0:
+        return rho, u, theta
+    v = to_conserved(rho, u, theta)
+    done = 0.0
+    step = 0
+    while span - done > GUARD * span:
+        d = coarse_cap(v, mesh.dx, cfl)
+        if dt_max is not None:
+            d = min(d, dt_max)
+        d = min(d, span - done)
+        g = np.empty((v.shape[0] + 2, 5))
+        g[1:-1] = v
+        if periodic:
+            g[0], g[-1] = v[-1], v[0]
+        else:  # transmissive copy (ref/fluid.py:84-87)
+            g[0], g[-1] = v[0], v[-1]
+        H = rusanov(g[:-1], g[1:])
+        nv = v - (d / mesh.dx) * (H[1:] - H[:-1])
+        if force is not None:
+            nv[:, 1] += d * v[:, 0] * force
+            nv[:, 4] += d * v[:, 1] * force
+        step += 1
+        if not np.all(np.isfinite(nv)):
+            raise OracleBlowUp("fluid non-finite at step %d" % step, step=step)
+        if np.any(nv[:, 0] <= 0.0) or np.any(pressure(nv) <= 0.0):
+            raise OracleBlowUp("fluid unphysical at step %d" % step, step=step)
+        v = nv
+        done += d
+    return to_primitive(v)
+
+
+# --------------------------------------------------------------------------
+# parareal slice loop (ref/parareal.py:109-314)
+# --------------------------------------------------------------------------
+
+@dataclass
+class Problem:
+    """Everything one parareal run fixes (mesh, time grid, physics)."""
+
+    mesh: Mesh
+    t_final: float
+    n_g: int
+    n_f: int
+    eps: float
+    periodic: bool
+    force: Optional[np.ndarray] = None
+    cfl_kin: float = 0.5
+    cfl_fluid: float = 0.9
+    tau: Callable = unit_tau
+
+    @property
+    def times(self):
+        return coarse_grid(self.t_final, self.n_g, self.n_f)[0]
+
+    @property
+    def dt_g(self):
+        return self.t_final / self.n_g
+
+    @property
+    def dt_f(self):
+        return self.t_final / self.n_f
+
+
+def G(prob: Problem, U, n: int):
+    """Coarse solve over window n (1-based)."""
+    t = prob.times
+    return coarse_propagate(*U, float(t[n - 1]), float(t[n]), prob.mesh,
+                            prob.periodic, prob.force, prob.dt_g, prob.cfl_fluid)
+
+
+def PFL(prob: Problem, U, n: int):
+    """Fine solve of window n from moments U: P(F(L(U))) (ref/parareal.py:123-142)."""
+    t = prob.times
+    f = lift(*U, prob.mesh, normalize=False)
+    f = fine_propagate(f, float(t[n - 1]), float(t[n]), prob.mesh, prob.eps,
+                       prob.periodic, prob.force, prob.dt_f, prob.cfl_kin,
+                       prob.tau)
+    return project(f, prob.mesh)
+
+
+def _sub(a, b):
+    return tuple(x - y for x, y in zip(a, b))
+
+
+def _add(a, b):
+    return tuple(x + y for x, y in zip(a, b))
+
+
+def sup_gap(a, b) -> float:
+    """ref/moments.py:48-52."""
+    return max(float(np.max(np.abs(x - y))) for x, y in zip(a, b))
+
+
+def window_jump(prob: Problem, U, n: int):
+    """Delta^n = P F L (U) - G (U) (ref/parareal.py:123-142)."""
+    return _sub(PFL(prob, U, n), G(prob, U, n))
+
+
+def parareal(prob: Problem, U0, k_max: int, tol: float, frozen: bool = True,
+             jump_fn=None):
+    """Outer iteration (ref/parareal.py:109-120, 179-278).
+
+    Returns (snapshots, errors).  ``jump_fn(prob, U, n)`` may replace the
+    serial window jump (tests use it to inject distributed variants).
+    """
+    jump_fn = jump_fn or window_jump
+    snaps = [tuple(np.array(x, copy=True) for x in U0)]
+    for n in range(1, prob.n_g + 1):
+        snaps.append(G(prob, snaps[-1], n))
+    jumps = [None] * prob.n_g
+    errors = []
+    for k in range(1, k_max + 1):
+        start = k if frozen else 1
+        for n in range(start, prob.n_g + 1):
+            jumps[n - 1] = jump_fn(prob, snaps[n - 1], n)
+        new = list(snaps)
+        err = 0.0
+        for n in range(start, prob.n_g + 1):
+            cor = _add(G(prob, new[n - 1], n), jumps[n - 1])
+            ok = all(np.all(np.isfinite(x)) for x in cor)
+            if not ok or np.any(cor[0] <= 0.0) or np.any(cor[2] <= 0.0):
+                raise OracleOvershoot("overshoot in window %d" % n, slice_index=n)
+            err = max(err, sup_gap(cor, snaps[n]))
+            new[n] = cor
+        snaps = new
+        errors.append(err)
+        if err < tol:
+            break
+    return snaps, errors
+
+
+def fine_chain(prob: Problem, U0):
+    """Window-wise serial fine reference (ref/parareal.py:281-295)."""
+    out = [tuple(np.array(x, copy=True) for x in U0)]
+    for n in range(1, prob.n_g + 1):
+        out.append(PFL(prob, out[-1], n))
+    return out
+
+
+def work_range(work: int, n_p: int, rank: int):
+    """(start, end, end-start, size) of ref/parareal.py:298-314."""
+    if n_p < 1 or not 0 <= rank < n_p or work < 0:
+        raise OracleConfigError("bad partition request")
+    q, r = divmod(work, n_p)
+    s = rank * q + min(r, rank) + 1
+    e = (rank + 1) * q + min(r, rank + 1)
+    return s, e, e - s, max(0, e - s + 1)
+
+
+# --------------------------------------------------------------------------
+# synthetic problem builders for the BASELINE.json configs
+# --------------------------------------------------------------------------
+
+def two_state(mesh: Mesh, edge: float, left, right):
+    """Piecewise (rho, u_x, theta) classified by cell centre (ref/cases.py:29-42)."""
+    x = mesh.xc
+    m = x < edge
+    rho = np.where(m, left[0], right[0]).astype(float)
+    u = np.zeros((mesh.nx, 3))
+    u[:, 0] = np.where(m, left[1], right[1])
+    theta = np.where(m, left[2], right[2]).astype(float)
+    return rho, u, theta

@@ -1,0 +1,573 @@
+// extern "C" boundary of libpbgk.so (declared in include/pbgk.h).
+//
+// Host orchestration of the fine propagator: context (grid constants, tiling,
+// device workspace, TMA descriptors), the skewed sweep/finalize sequence of
+// propagate_kinetic, and the single-GPU coarse solver / correction launches.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/pbgk.h"
+#include "common.cuh"
+
+namespace pbgk {
+cudaError_t launch_sweep(int cfg_id, const CUtensorMap& map, const SweepArgs& a, bool synth,
+                         bool field, int grid, int ns, size_t smem, cudaStream_t st);
+size_t sweep_smem_bytes(const SweepArgs& a, int V, int LZ, int NTHR, bool synth, bool tma, int ns);
+cudaError_t launch_finalize(const FinalArgs& a, cudaStream_t st);
+cudaError_t launch_set_key(ErrKey* p, ErrKey v, cudaStream_t st);
+struct FluidArgs {
+  int nx;
+  double dx;
+  int periodic;
+  double dt_max;
+  double cfl;
+  const double* force;
+  ErrKey* err;
+};
+cudaError_t launch_fluid_batch(const FluidArgs& a, int nwin, const double* in, double* out,
+                               const double* minuend, const double* t0, const double* t1,
+                               cudaStream_t st);
+cudaError_t launch_correct(const FluidArgs& a, int n_g, int start, double* snaps, const double* old,
+                           const double* jumps, const double* times, double* err_out,
+                           cudaStream_t st);
+}  // namespace pbgk
+
+using namespace pbgk;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(const std::string& msg) {
+  g_last_error = msg;
+  return -1;
+}
+
+#define CK(expr)                                                                   \
+  do {                                                                             \
+    cudaError_t e_ = (expr);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      return fail(std::string(#expr) + ": " + cudaGetErrorString(e_));            \
+  } while (0)
+
+// compile-time tile shapes of sweep.cu (index = cfg id)
+struct CfgShape {
+  int V, LZ, K, NTHR;
+  bool tma;
+};
+const CfgShape kCfg[] = {
+    {2, 32, 8, 512, true},  // 0: nvz % 64 == 0
+    {2, 16, 8, 512, true},  // 1: nvz % 32 == 0
+    {2, 16, 4, 512, true},  // 2: nvz % 32 == 0 (field / small)
+    {3, 16, 4, 512, true},  // 3: nvz % 48 == 0
+    {2, 8, 4, 256, true},   // 4: nvz % 16 == 0
+    {2, 4, 4, 256, true},   // 5: nvz % 8 == 0
+    {1, 32, 4, 256, false}, // 6: anything (no TMA)
+};
+
+struct Plan {
+  int cfg;
+  Tiling t;
+  int grid;
+  int ns;
+};
+
+struct MapEntry {
+  const void* ptr;
+  int rows_load, By, Bz;
+  CUtensorMap map;
+};
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+}  // namespace
+
+struct pbgk_ctx {
+  pbgk_grid_desc g;
+  double dx, dv[3], dvol;
+  int dev, nsm;
+  size_t smem_optin;
+  double* d_c[3] = {nullptr, nullptr, nullptr};
+  Plan plan[2];  // [0] no field, [1] v_x field term
+  int TL, gxo, gyo, gzo;
+  double* d_part = nullptr;
+  size_t part_elems = 0;
+  double* d_tab[2] = {nullptr, nullptr};
+  double* d_scratch = nullptr;  // 5*nx moments / small host-visible staging
+  ErrKey* d_err = nullptr;
+  ErrKey* h_err = nullptr;  // pinned
+  double* h_dbl = nullptr;  // pinned small
+  double* d_times = nullptr;
+  size_t times_cap = 0;
+  std::vector<MapEntry> maps;
+  size_t ws_bytes = 0;
+};
+
+namespace {
+
+// Tile choice for one configuration of the sweep.
+bool make_plan(pbgk_ctx* c, bool field, Plan& out) {
+  const int nvx = c->g.nvx, nvy = c->g.nvy, nvz = c->g.nvz;
+  const int nneg = nvx / 2;  // centres (j - (n-1)/2) dv are < 0 exactly for j < n/2
+  const int npos = nvx - nneg;
+  std::vector<int> cands;
+  const bool even = (nvz % 2 == 0);
+  if (even && nvz % 64 == 0) cands.push_back(field ? 2 : 0);
+  if (even && nvz % 48 == 0) cands.push_back(3);
+  if (even && nvz % 32 == 0) cands.push_back(field ? 2 : 1);
+  if (even && nvz % 16 == 0) cands.push_back(4);
+  if (even && nvz % 8 == 0) cands.push_back(5);
+  cands.push_back(6);
+  if (const char* force = getenv("PBGK_FORCE_CFG")) {  // development knob
+    cands.assign(1, atoi(force));
+  }
+  double best = 1e300;
+  bool found = false;
+  for (int id : cands) {
+    const CfgShape& s = kCfg[id];
+    const int Bz = s.V * s.LZ;
+    const int lines = s.K * (s.NTHR / s.LZ);
+    for (int A = 1; A <= lines; A *= 2) {
+      if (A > std::max(nneg, npos) && A > 1) break;
+      int By = lines / A;
+      if (By > nvy) By = nvy;
+      if (By < 1 || By > 256 || A + (field ? 2 : 0) > 256) continue;
+      if (A + By + Bz > s.NTHR) continue;
+      Tiling t;
+      t.A = A;
+      t.By = By;
+      t.Bz = Bz;
+      t.rows_load = A + (field ? 2 : 0);
+      t.nneg = nneg;
+      t.ntn = (nneg + A - 1) / A;
+      t.ntp = (npos + A - 1) / A;
+      t.nty = (nvy + By - 1) / By;
+      t.ntz = (nvz + Bz - 1) / Bz;
+      t.NT = (t.ntn + t.ntp) * t.nty * t.ntz;
+      t.PS = A + By + Bz;
+      // loaded elements per useful element, plus marginal-partial traffic
+      const double loaded = (double)t.NT * t.rows_load * By * Bz;
+      const double useful = (double)nvx * nvy * nvz;
+      const double part = 2.0 * t.NT * t.PS;
+      // shared memory for 2 stages at least
+      SweepArgs dummy{};
+      dummy.t = t;
+      dummy.TL = c->TL;
+      const size_t sm2 = sweep_smem_bytes(dummy, s.V, s.LZ, s.NTHR, false, s.tma, 2);
+      if (sm2 > c->smem_optin) continue;
+      // halo overhead: one extra plane per tile run per CTA segment
+      const double items = (double)t.NT * c->g.nx;
+      const double runs = std::min<double>(c->nsm, items) + t.NT;
+      const double halo = runs / items;
+      const double penalty = (s.tma ? 1.0 : 4.0);
+      const double util = (double)(A * By) / lines;  // busy fraction of the thread lines
+      const double score = penalty * ((loaded + part) / useful) * (1.0 + halo) * (1.5 - 0.5 * util) +
+                           (id == 6 ? 1.0 : 0.0);
+      if (score < best) {
+        best = score;
+        out.cfg = id;
+        out.t = t;
+        found = true;
+      }
+    }
+  }
+  if (!found) return false;
+  const CfgShape& s = kCfg[out.cfg];
+  SweepArgs dummy{};
+  dummy.t = out.t;
+  dummy.TL = c->TL;
+  int ns = 4;
+  while (ns > 2 && sweep_smem_bytes(dummy, s.V, s.LZ, s.NTHR, false, s.tma, ns) > c->smem_optin) --ns;
+  out.ns = s.tma ? ns : 1;
+  const long long items = (long long)out.t.NT * c->g.nx;
+  long long grid = c->nsm;
+  if (grid > items) grid = items;
+  out.grid = (int)std::max<long long>(grid, 1);
+  return true;
+}
+
+const CUtensorMap* tensor_map(pbgk_ctx* c, const double* ptr, const Tiling& t, int cfg) {
+  static CUtensorMap dummy;
+  if (!kCfg[cfg].tma || ptr == nullptr) return &dummy;
+  for (auto& m : c->maps)
+    if (m.ptr == ptr && m.rows_load == t.rows_load && m.By == t.By && m.Bz == t.Bz) return &m.map;
+  auto enc = get_encode();
+  if (!enc) return nullptr;
+  MapEntry e;
+  e.ptr = ptr;
+  e.rows_load = t.rows_load;
+  e.By = t.By;
+  e.Bz = t.Bz;
+  const cuuint64_t dims[4] = {(cuuint64_t)c->g.nvz, (cuuint64_t)c->g.nvy, (cuuint64_t)c->g.nvx,
+                              (cuuint64_t)c->g.nx};
+  const cuuint64_t strides[3] = {(cuuint64_t)c->g.nvz * 8, (cuuint64_t)c->g.nvy * c->g.nvz * 8,
+                                 (cuuint64_t)c->g.nvx * c->g.nvy * c->g.nvz * 8};
+  const cuuint32_t box[4] = {(cuuint32_t)t.Bz, (cuuint32_t)t.By, (cuuint32_t)t.rows_load, 1};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(&e.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(ptr), dims,
+                   strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[128];
+    snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    g_last_error = buf;
+    return nullptr;
+  }
+  if (c->maps.size() > 64) c->maps.erase(c->maps.begin());
+  c->maps.push_back(e);
+  return &c->maps.back().map;
+}
+
+SweepArgs base_args(pbgk_ctx* c, const Plan& p) {
+  SweepArgs a{};
+  a.nx = c->g.nx;
+  a.nvx = c->g.nvx;
+  a.nvy = c->g.nvy;
+  a.nvz = c->g.nvz;
+  a.plane = (long long)c->g.nvx * c->g.nvy * c->g.nvz;
+  a.t = p.t;
+  a.total = (long long)p.t.NT * c->g.nx;
+  a.tab = c->d_tab[0];
+  a.TL = c->TL;
+  a.gxo = c->gxo;
+  a.gyo = c->gyo;
+  a.gzo = c->gzo;
+  a.cx = c->d_c[0];
+  a.periodic = c->g.periodic;
+  a.part = c->d_part;
+  a.err = c->d_err;
+  return a;
+}
+
+FinalArgs fin_args(pbgk_ctx* c, const Plan& p) {
+  FinalArgs f{};
+  f.nx = c->g.nx;
+  f.nvx = c->g.nvx;
+  f.nvy = c->g.nvy;
+  f.nvz = c->g.nvz;
+  f.t = p.t;
+  f.part = c->d_part;
+  f.cx = c->d_c[0];
+  f.cy = c->d_c[1];
+  f.cz = c->d_c[2];
+  f.dvol = c->dvol;
+  f.TL = c->TL;
+  f.gxo = c->gxo;
+  f.gyo = c->gyo;
+  f.gzo = c->gzo;
+  f.err = c->d_err;
+  f.tau = 1.0;
+  f.eps = 1.0;
+  return f;
+}
+
+// One sweep over f (see sweep.cu).  `in` null => SYNTH from `tab`.
+int run_sweep(pbgk_ctx* c, int pid, bool field, const double* in, const double* tab, double* out,
+              double dtdx, const double* E, double half_emax, double dtdv, int check_step,
+              cudaStream_t st) {
+  const Plan& p = c->plan[pid];
+  const CfgShape& s = kCfg[p.cfg];
+  SweepArgs a = base_args(c, p);
+  a.fin = in;
+  a.fout = out;
+  a.tab = tab;
+  a.dtdx = dtdx;
+  a.E = field ? E : nullptr;
+  a.half_emax = half_emax;
+  a.dtdv = dtdv;
+  a.check_step = check_step;
+  const bool synth = (in == nullptr);
+  const CUtensorMap* map = tensor_map(c, synth ? nullptr : in, p.t, p.cfg);
+  if (!map) return fail("tensor map: " + g_last_error);
+  const size_t smem = sweep_smem_bytes(a, s.V, s.LZ, s.NTHR, synth, s.tma, p.ns);
+  CK(launch_sweep(p.cfg, *map, a, synth, field, p.grid, p.ns, smem, st));
+  return 0;
+}
+
+int run_final(pbgk_ctx* c, int pid, int mode, const double* mom_in, double* mom_out,
+              double* tab, double dt, double eps, double tau, const double* tau_cells, int step,
+              cudaStream_t st) {
+  FinalArgs f = fin_args(c, c->plan[pid]);
+  f.mode = mode;
+  f.mom_in = mom_in;
+  f.mom_out = mom_out;
+  f.tab = tab;
+  f.dt = dt;
+  f.eps = eps;
+  f.tau = tau;
+  f.tau_arr = tau_cells;
+  f.step = step;
+  CK(launch_finalize(f, st));
+  return 0;
+}
+
+int reset_err(pbgk_ctx* c, cudaStream_t st) {
+  CK(launch_set_key(c->d_err, kNoError, st));
+  return 0;
+}
+
+int fetch_err(pbgk_ctx* c, cudaStream_t st, long long* code) {
+  if (!code) return 0;
+  CK(cudaMemcpyAsync(c->h_err, c->d_err, sizeof(ErrKey), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  *code = (*c->h_err == kNoError) ? -1 : (long long)*c->h_err;
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pbgk_version(void) { return 1; }
+
+const char* pbgk_last_error(void) { return g_last_error.c_str(); }
+
+int pbgk_ctx_create(const pbgk_grid_desc* g, pbgk_ctx** out) {
+  if (!g || !out) return fail("null argument");
+  if (g->nx < 1 || g->nvx < 1 || g->nvy < 1 || g->nvz < 1) return fail("bad grid sizes");
+  if (g->nvx > 4096 || g->nvy > 4096 || g->nvz > 4096) return fail("velocity axis too long");
+  pbgk_ctx* c = new pbgk_ctx();
+  c->g = *g;
+  c->dx = (g->x_max - g->x_min) / g->nx;  // ref/grid.py:95
+  const int nv[3] = {g->nvx, g->nvy, g->nvz};
+  for (int a = 0; a < 3; ++a) c->dv[a] = 2.0 * g->v_max / nv[a];  // ref/grid.py:114
+  c->dvol = c->dv[0] * c->dv[1] * c->dv[2];
+  auto bail = [&](int rc) {
+    pbgk_ctx_destroy(c);
+    return rc;
+  };
+  c->dev = g->device;
+  if (cudaSetDevice(c->dev) != cudaSuccess) return bail(fail("cannot select CUDA device"));
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, c->dev) != cudaSuccess) return bail(fail("device query failed"));
+  c->nsm = prop.multiProcessorCount;
+  c->smem_optin = prop.sharedMemPerBlockOptin;
+  // table row: [r, ls, gx(nvx), gy(nvy), gz(nvz)] padded to 16 bytes
+  c->gxo = 2;
+  c->gyo = c->gxo + g->nvx;
+  c->gzo = c->gyo + g->nvy;
+  c->TL = (c->gzo + g->nvz + 1) & ~1;
+  if (!make_plan(c, false, c->plan[0]) || !make_plan(c, true, c->plan[1]))
+    return bail(fail("no tiling fits this velocity grid"));
+  for (int a = 0; a < 3; ++a) {
+    std::vector<double> h(nv[a]);
+    for (int j = 0; j < nv[a]; ++j) h[j] = ((double)j - (nv[a] - 1) / 2.0) * c->dv[a];  // ref/grid.py:100-103
+    if (cudaMalloc(&c->d_c[a], nv[a] * sizeof(double)) != cudaSuccess) return bail(fail("cudaMalloc"));
+    cudaMemcpy(c->d_c[a], h.data(), nv[a] * sizeof(double), cudaMemcpyHostToDevice);
+  }
+  c->part_elems = 0;
+  for (int f = 0; f < 2; ++f)
+    c->part_elems = std::max(c->part_elems, (size_t)g->nx * c->plan[f].t.NT * c->plan[f].t.PS);
+  size_t bytes = c->part_elems * 8 + 2 * (size_t)g->nx * c->TL * 8 + (size_t)5 * g->nx * 8 + 64;
+  if (cudaMalloc(&c->d_part, c->part_elems * 8) != cudaSuccess ||
+      cudaMalloc(&c->d_tab[0], (size_t)g->nx * c->TL * 8) != cudaSuccess ||
+      cudaMalloc(&c->d_tab[1], (size_t)g->nx * c->TL * 8) != cudaSuccess ||
+      cudaMalloc(&c->d_scratch, (size_t)5 * g->nx * 8) != cudaSuccess ||
+      cudaMalloc(&c->d_err, 64) != cudaSuccess)
+    return bail(fail("cudaMalloc workspace"));
+  if (cudaMallocHost(&c->h_err, 64) != cudaSuccess || cudaMallocHost(&c->h_dbl, 64) != cudaSuccess)
+    return bail(fail("cudaMallocHost"));
+  c->ws_bytes = bytes;
+  *out = c;
+  return 0;
+}
+
+void pbgk_ctx_destroy(pbgk_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->dev);
+  for (int a = 0; a < 3; ++a) cudaFree(c->d_c[a]);
+  cudaFree(c->d_part);
+  cudaFree(c->d_tab[0]);
+  cudaFree(c->d_tab[1]);
+  cudaFree(c->d_scratch);
+  cudaFree(c->d_err);
+  cudaFree(c->d_times);
+  if (c->h_err) cudaFreeHost(c->h_err);
+  if (c->h_dbl) cudaFreeHost(c->h_dbl);
+  delete c;
+}
+
+size_t pbgk_ctx_workspace_bytes(const pbgk_ctx* c) { return c ? c->ws_bytes : 0; }
+
+int pbgk_lift(pbgk_ctx* c, const double* mom, int normalize, double* f_out, void* stream,
+              long long* h_code) {
+  if (!c || !mom || !f_out) return fail("pbgk_lift: null argument");
+  if (cudaSetDevice(c->dev) != cudaSuccess) return fail("cudaSetDevice");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (reset_err(c, st)) return -1;
+  if (run_final(c, 0, normalize ? kFinSynthNorm : kFinSynthRaw, mom, nullptr, c->d_tab[0], 0, 1,
+                1, nullptr, 0, st))
+    return -1;
+  if (run_sweep(c, 0, false, nullptr, c->d_tab[0], f_out, 0.0, nullptr, 0.0, 0.0, 0, st)) return -1;
+  return fetch_err(c, st, h_code);
+}
+
+int pbgk_project(pbgk_ctx* c, const double* f, double* mom_out, void* stream, long long* h_code) {
+  if (!c || !f || !mom_out) return fail("pbgk_project: null argument");
+  if (cudaSetDevice(c->dev) != cudaSuccess) return fail("cudaSetDevice");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (reset_err(c, st)) return -1;
+  if (run_final(c, 0, kFinIdentity, nullptr, nullptr, c->d_tab[0], 0, 1, 1, nullptr, 0, st)) return -1;
+  if (run_sweep(c, 0, false, f, c->d_tab[0], nullptr, 0.0, nullptr, 0.0, 0.0, 0, st)) return -1;
+  if (run_final(c, 0, kFinProject, nullptr, mom_out, nullptr, 0, 1, 1, nullptr, 0, st)) return -1;
+  return fetch_err(c, st, h_code);
+}
+
+int pbgk_transport(pbgk_ctx* c, const double* f, double* f_out, double dt, const double* E,
+                   double e_max, void* stream) {
+  if (!c || !f || !f_out) return fail("pbgk_transport: null argument");
+  if (cudaSetDevice(c->dev) != cudaSuccess) return fail("cudaSetDevice");
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool field = (E != nullptr && e_max > 0.0);
+  const int pid = field ? 1 : 0;
+  if (run_final(c, pid, kFinIdentity, nullptr, nullptr, c->d_tab[0], 0, 1, 1, nullptr, 0, st)) return -1;
+  return run_sweep(c, pid, field, f, c->d_tab[0], f_out, dt / c->dx, E, 0.5 * e_max, dt / c->dv[0], 0,
+                   st);
+}
+
+int pbgk_relax(pbgk_ctx* c, const double* f, double* f_out, double dt, double eps, double tau,
+               const double* tau_cells, void* stream, long long* h_code) {
+  if (!c || !f || !f_out) return fail("pbgk_relax: null argument");
+  if (cudaSetDevice(c->dev) != cudaSuccess) return fail("cudaSetDevice");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (reset_err(c, st)) return -1;
+  if (run_final(c, 0, kFinIdentity, nullptr, nullptr, c->d_tab[0], 0, 1, 1, nullptr, 0, st)) return -1;
+  if (run_sweep(c, 0, false, f, c->d_tab[0], nullptr, 0.0, nullptr, 0.0, 0.0, 0, st)) return -1;
+  if (run_final(c, 0, kFinRelax, nullptr, nullptr, c->d_tab[1], dt, eps, tau, tau_cells, 1, st))
+    return -1;
+  if (run_sweep(c, 0, false, f, c->d_tab[1], f_out, 0.0, nullptr, 0.0, 0.0, 0, st)) return -1;
+  return fetch_err(c, st, h_code);
+}
+
+int pbgk_check_finite(pbgk_ctx* c, const double* f, int step, void* stream, long long* h_code) {
+  if (!c || !f) return fail("pbgk_check_finite: null argument");
+  if (cudaSetDevice(c->dev) != cudaSuccess) return fail("cudaSetDevice");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (reset_err(c, st)) return -1;
+  if (run_final(c, 0, kFinIdentity, nullptr, nullptr, c->d_tab[0], 0, 1, 1, nullptr, 0, st)) return -1;
+  if (run_sweep(c, 0, false, f, c->d_tab[0], nullptr, 0.0, nullptr, 0.0, 0.0, step, st)) return -1;
+  return fetch_err(c, st, h_code);
+}
+
+int pbgk_propagate(pbgk_ctx* c, const double* f0, const double* mom0, double* f_out, double* f_tmp,
+                   int write_final, double* mom_out, int nsteps, const double* h_dts, double eps,
+                   double tau, const double* E, double e_max, void* stream, long long* h_code) {
+  if (!c || (!f0 && !mom0) || !f_out || !f_tmp || (nsteps > 0 && !h_dts))
+    return fail("pbgk_propagate: null argument");
+  if (cudaSetDevice(c->dev) != cudaSuccess) return fail("cudaSetDevice");
+  if (f_out == f_tmp || (f0 && (f0 == f_out || f0 == f_tmp)))
+    return fail("pbgk_propagate: buffers alias");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (reset_err(c, st)) return -1;
+  const bool field = (E != nullptr && e_max > 0.0);
+  const int pid = field ? 1 : 0;
+  const int S = nsteps;
+  const int W = S + (write_final ? 1 : 0);
+  auto buf = [&](int w) { return ((W - w) % 2 == 0) ? f_out : f_tmp; };
+  // f_0: the given distribution (identity tables) or the raw lift of mom0
+  if (f0) {
+    if (run_final(c, pid, kFinIdentity, nullptr, nullptr, c->d_tab[0], 0, 1, 1, nullptr, 0, st)) return -1;
+  } else {
+    if (run_final(c, pid, kFinSynthRaw, mom0, nullptr, c->d_tab[0], 0, 1, 1, nullptr, 0, st)) return -1;
+  }
+  for (int s = 1; s <= S; ++s) {
+    const double dt = h_dts[s - 1];
+    const double* in = (s == 1) ? f0 : buf(s - 1);
+    if (run_sweep(c, pid, field, in, c->d_tab[(s - 1) & 1], buf(s), dt / c->dx, E, 0.5 * e_max,
+                  dt / c->dv[0], s == 1 ? 0 : s - 1, st))
+      return -1;
+    if (run_final(c, pid, kFinRelax, nullptr, nullptr, c->d_tab[s & 1], dt, eps, tau, nullptr, s, st))
+      return -1;
+  }
+  if (S > 0) {
+    if (run_sweep(c, pid, false, buf(S), c->d_tab[S & 1], write_final ? f_out : nullptr, 0.0, nullptr,
+                  0.0, 0.0, S, st))
+      return -1;
+    if (mom_out &&
+        run_final(c, pid, kFinProject, nullptr, mom_out, nullptr, 0, 1, 1, nullptr, S + 1, st))
+      return -1;
+  }
+  return fetch_err(c, st, h_code);
+}
+
+namespace {
+int upload_times(pbgk_ctx* c, const double* h, size_t n, cudaStream_t st) {
+  if (n > c->times_cap) {
+    if (c->d_times) {
+      CK(cudaStreamSynchronize(st));
+      CK(cudaFree(c->d_times));
+      c->d_times = nullptr;
+    }
+    size_t cap = 256;
+    while (cap < n) cap *= 2;
+    CK(cudaMalloc(&c->d_times, cap * sizeof(double)));
+    c->times_cap = cap;
+  }
+  CK(cudaMemcpyAsync(c->d_times, h, n * sizeof(double), cudaMemcpyHostToDevice, st));
+  return 0;
+}
+}  // namespace
+
+int pbgk_fluid_propagate(pbgk_ctx* c, int nwin, const double* mom_in, double* mom_out,
+                         const double* minuend, const double* h_t0, const double* h_t1,
+                         double dt_max, double cfl, const double* force, void* stream,
+                         long long* h_code) {
+  if (!c || !mom_in || !mom_out || !h_t0 || !h_t1) return fail("pbgk_fluid_propagate: null argument");
+  if (cudaSetDevice(c->dev) != cudaSuccess) return fail("cudaSetDevice");
+  if (nwin <= 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<double> t(2 * (size_t)nwin);
+  for (int w = 0; w < nwin; ++w) {
+    t[w] = h_t0[w];
+    t[nwin + w] = h_t1[w];
+  }
+  if (upload_times(c, t.data(), t.size(), st)) return -1;
+  if (reset_err(c, st)) return -1;
+  FluidArgs a{c->g.nx, c->dx, c->g.periodic, dt_max, cfl, force, c->d_err};
+  CK(launch_fluid_batch(a, nwin, mom_in, mom_out, minuend, c->d_times, c->d_times + nwin, st));
+  return fetch_err(c, st, h_code);
+}
+
+int pbgk_parareal_correct(pbgk_ctx* c, int n_g, int start, double* snaps, const double* old,
+                          const double* jumps, const double* h_times, double dt_max, double cfl,
+                          const double* force, void* stream, double* h_err, long long* h_code) {
+  if (!c || !snaps || !old || !jumps || !h_times) return fail("pbgk_parareal_correct: null argument");
+  if (cudaSetDevice(c->dev) != cudaSuccess) return fail("cudaSetDevice");
+  if (start < 1) return fail("pbgk_parareal_correct: start < 1");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (upload_times(c, h_times, (size_t)n_g + 1, st)) return -1;
+  if (reset_err(c, st)) return -1;
+  FluidArgs a{c->g.nx, c->dx, c->g.periodic, dt_max, cfl, force, c->d_err};
+  double* d_e = c->d_scratch;
+  CK(cudaMemsetAsync(d_e, 0, sizeof(double), st));
+  if (start <= n_g) CK(launch_correct(a, n_g, start, snaps, old, jumps, c->d_times, d_e, st));
+  CK(cudaMemcpyAsync(c->h_dbl, d_e, sizeof(double), cudaMemcpyDeviceToHost, st));
+  long long code = -1;
+  if (fetch_err(c, st, &code)) return -1;
+  if (h_code) *h_code = code;
+  if (h_err) *h_err = c->h_dbl[0];
+  return 0;
+}
+
+}  // extern "C"

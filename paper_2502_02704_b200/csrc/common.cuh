@@ -1,0 +1,92 @@
+// Shared definitions of the fine-propagator kernels.
+//
+// Data layout in HBM (fp64, C order, identical to the reference's numpy array,
+// ref/lifting.py:16-23):  f[i][jx][jy][jz],  i = x cell, jz fastest.
+// Per-cell side tables (one row of TL doubles per x cell):
+//   [0] r    relax: 1/(1+lambda)             synth: unused
+//   [1] ls   relax: lambda*rho/mass           synth: 1 (raw lift) or rho/mass
+//   [gxo .. gxo+nvx)  gx*amp      (ref/lifting.py:47-50)
+//   [gyo .. gyo+nvy)  gy
+//   [gzo .. gzo+nvz)  gz
+// Moments (SoA, 5*nx): rho, u_x, u_y, u_z, theta.
+// Partial marginals: part[(i*NT + tile)*PS + {0..A) m_x rows, A..A+By) m_y, A+By..) m_z].
+#pragma once
+#include <cstdint>
+
+namespace pbgk {
+
+// Error codes are 64-bit keys (unit << 40) | (step << 8) | kind, reduced with
+// atomicMin: the lowest unit (window / slice) wins, then the earliest step,
+// then the lowest kind, which is the reference's raise order inside one step
+// (SURVEY 8(b) Errors).  All ones = clean.
+typedef unsigned long long ErrKey;
+enum ErrKind : int {
+  kErrProjectRho = 0,   // DegenerateStateError in project (ref/moments.py:102-104)
+  kErrLiftState = 1,    // DegenerateStateError in lift / conserved->primitive
+  kErrNonFinite = 2,    // BlowUpError(step)
+  kErrUnphysical = 3,   // BlowUpError(step) from G's positivity guard
+  kErrOvershoot = 4,    // CorrectionOvershootError(slice_index)
+};
+constexpr ErrKey kNoError = ~0ull;
+__host__ __device__ constexpr ErrKey err_key(unsigned long long unit, unsigned long long step,
+                                             int kind) {
+  return (unit << 40) | (step << 8) | (unsigned long long)kind;
+}
+
+struct Tiling {
+  int A, By, Bz;     // velocity box of one tile (rows, jy, jz)
+  int rows_load;     // A, or A+2 when the v_x field term needs neighbour rows
+  int nneg;          // rows [0,nneg) have c_x < 0 and march downward in x
+  int ntn, ntp;      // row tiles in the negative / non-negative group
+  int nty, ntz, NT;  // y / z tiles, total tiles
+  int PS;            // stride of one tile's partial record (doubles)
+};
+
+struct SweepArgs {
+  int nx, nvx, nvy, nvz;
+  long long plane;   // nvx*nvy*nvz
+  Tiling t;
+  long long total;   // NT*nx plane items (halos excluded)
+  const double* fin;
+  double* fout;      // nullptr: marginals only
+  const double* tab;
+  int TL, gxo, gyo, gzo;
+  const double* cx;  // x-velocity centres
+  double dtdx;       // 0: no transport (pure relax/copy pass)
+  int periodic;
+  const double* E;   // per-cell field or nullptr
+  double half_emax;  // 0.5*max|E|
+  double dtdv;       // dt / dv_x
+  double* part;
+  ErrKey* err;
+  int check_step;    // >0: flag non-finite f_pre as step `check_step`
+};
+
+enum FinalMode : int {
+  kFinRelax = 0,      // tables of the normalised Maxwellian + lambda (bgk_relax)
+  kFinSynthRaw = 1,   // tables of the un-normalised lift (window start)
+  kFinSynthNorm = 2,  // tables of the mass-normalised lift
+  kFinIdentity = 3,   // r=1, ls=0: f_pre = f (a loaded distribution as is)
+  kFinProject = 4,    // moments only
+};
+
+struct FinalArgs {
+  int nx, nvx, nvy, nvz;
+  Tiling t;
+  const double* part;
+  const double* mom_in;  // non-null: moments given (lift), partials ignored
+  const double* cx;
+  const double* cy;
+  const double* cz;
+  double dvol;
+  double* mom_out;       // may be null
+  double* tab;           // may be null
+  int TL, gxo, gyo, gzo;
+  int mode;
+  double dt, eps, tau;   // lambda = dt*tau/eps (ref/kinetic.py:131)
+  const double* tau_arr; // optional per-cell tau values
+  ErrKey* err;
+  int step;
+};
+
+}  // namespace pbgk

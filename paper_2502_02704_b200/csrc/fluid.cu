@@ -1,0 +1,328 @@
+// Coarse propagator G: first-order Rusanov Euler solver (ref/fluid.py:39-125)
+// and the sequential parareal correction (ref/parareal.py:217-248), on one GPU.
+//
+// One CTA owns one window's state (conserved variables of all nx cells in
+// shared memory).  Every expression is evaluated in the reference's operation
+// order with explicitly rounded fp64 intrinsics (no FMA contraction), so the
+// result is bitwise that of numpy for the same input; the CFL max is
+// order-independent.  Each thread recomputes both faces of its cells (no face
+// buffer), which keeps the smem footprint at 40*nx bytes.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace pbgk {
+
+struct FluidArgs {
+  int nx;
+  double dx;
+  int periodic;
+  double dt_max;  // <= 0: none
+  double cfl;
+  const double* force;  // nx or null
+  ErrKey* err;
+};
+
+#define DM __dmul_rn
+#define DA __dadd_rn
+#define DS __dsub_rn
+#define DD __ddiv_rn
+
+// ref/fluid.py:39-42
+__device__ __forceinline__ double press(double v0, double v1, double v2, double v3, double v4) {
+  const double ke = DD(DM(0.5, DA(DA(DM(v1, v1), DM(v2, v2)), DM(v3, v3))), v0);
+  return DD(DS(v4, ke), 1.5);
+}
+
+struct St {
+  double v[5];
+};
+
+// ref/fluid.py:45-56
+__device__ __forceinline__ void eflux(const St& s, double h[5]) {
+  const double ux = DD(s.v[1], s.v[0]);
+  const double p = press(s.v[0], s.v[1], s.v[2], s.v[3], s.v[4]);
+  h[0] = s.v[1];
+  h[1] = DA(DM(s.v[1], ux), p);
+  h[2] = DM(s.v[2], ux);
+  h[3] = DM(s.v[3], ux);
+  h[4] = DM(ux, DA(s.v[4], p));
+}
+
+__device__ __forceinline__ double wave(const St& s) {
+  const double p = press(s.v[0], s.v[1], s.v[2], s.v[3], s.v[4]);
+  return DA(fabs(DD(s.v[1], s.v[0])), sqrt(DD(p, s.v[0])));
+}
+
+// ref/fluid.py:59-66
+__device__ __forceinline__ void rusanov(const St& l, const St& r, double H[5]) {
+  const double s = fmax(wave(l), wave(r));
+  double hl[5], hr[5];
+  eflux(l, hl);
+  eflux(r, hr);
+  const double hs = DM(0.5, s);
+#pragma unroll
+  for (int c = 0; c < 5; ++c) H[c] = DS(DM(0.5, DA(hl[c], hr[c])), DM(hs, DS(r.v[c], l.v[c])));
+}
+
+__device__ __forceinline__ St load_state(const double* V, int nx, int i) {
+  St s;
+#pragma unroll
+  for (int c = 0; c < 5; ++c) s.v[c] = V[c * nx + i];
+  return s;
+}
+
+__device__ __forceinline__ St ghost_state(const double* V, int nx, int i, int periodic) {
+  // ref/fluid.py:78-88: periodic wrap or transmissive copy
+  if (i < 0) return load_state(V, nx, periodic ? nx - 1 : 0);
+  if (i >= nx) return load_state(V, nx, periodic ? 0 : nx - 1);
+  return load_state(V, nx, i);
+}
+
+__device__ double block_max(double x, double* red) {
+  for (int w = 16; w >= 1; w >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, w));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[warp] = x;
+  __syncthreads();
+  double m = red[0];
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
+  return m;
+}
+
+// prim -> conserved (ref/moments.py:116-119; einsum('ij,ij->i') over 3
+// components evaluates as (a0 b0 + a2 b2) + a1 b1 in numpy 2.x)
+__device__ __forceinline__ void to_cons(double rho, double u0, double u1, double u2, double th,
+                                        double v[5]) {
+  v[0] = rho;
+  v[1] = DM(rho, u0);
+  v[2] = DM(rho, u1);
+  v[3] = DM(rho, u2);
+  const double uu = DA(DA(DM(u0, u0), DM(u2, u2)), DM(u1, u1));
+  v[4] = DA(DM(DM(0.5, rho), uu), DM(DM(1.5, rho), th));
+}
+
+// Advances the state held in smem V (5 x nx, conserved) over `span`.
+// Returns 0 or (step << 8) | kind (kErrNonFinite / kErrUnphysical).
+constexpr int kMaxCellsPerThread = 4;
+
+__device__ ErrKey g_advance(double* V, double* red, int* flag, const FluidArgs& a, double span) {
+  const int nx = a.nx;
+  const double guard = 1e-12;  // ref/fluid.py:30
+  double done = 0.0;
+  unsigned long long step = 0;
+  while (DS(span, done) > DM(guard, span)) {
+    double rate = 0.0;
+    for (int i = threadIdx.x; i < nx; i += blockDim.x) rate = fmax(rate, wave(load_state(V, nx, i)));
+    rate = block_max(rate, red);
+    // ref/fluid.py:75, :106-109
+    double dt = DD(DM(a.cfl, a.dx), rate);
+    if (a.dt_max > 0.0) dt = fmin(dt, a.dt_max);
+    dt = fmin(dt, DS(span, done));
+    const double dtdx = DD(dt, a.dx);
+    ++step;
+    double nv[kMaxCellsPerThread][5];
+    int bad = 0;
+#pragma unroll
+    for (int k = 0; k < kMaxCellsPerThread; ++k) {
+      const int i = threadIdx.x + k * blockDim.x;
+      if (i >= nx) break;
+      const St c = load_state(V, nx, i);
+      const St l = ghost_state(V, nx, i - 1, a.periodic);
+      const St r = ghost_state(V, nx, i + 1, a.periodic);
+      double HL[5], HR[5];
+      rusanov(l, c, HL);
+      rusanov(c, r, HR);
+      double* w = nv[k];
+#pragma unroll
+      for (int q = 0; q < 5; ++q) w[q] = DS(c.v[q], DM(dtdx, DS(HR[q], HL[q])));
+      if (a.force != nullptr) {  // ref/fluid.py:113-115 (old state)
+        const double E = a.force[i];
+        w[1] = DA(w[1], DM(DM(dt, c.v[0]), E));
+        w[4] = DA(w[4], DM(DM(dt, c.v[1]), E));
+      }
+      bool fin = true;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) fin = fin && isfinite(w[q]);
+      if (!fin) bad |= 1;
+      else if (w[0] <= 0.0 || press(w[0], w[1], w[2], w[3], w[4]) <= 0.0) bad |= 2;
+    }
+    if (bad) atomicOr(flag, bad);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kMaxCellsPerThread; ++k) {
+      const int i = threadIdx.x + k * blockDim.x;
+      if (i >= nx) break;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) V[q * nx + i] = nv[k][q];
+    }
+    __syncthreads();
+    const int f = *flag;
+    // ref/fluid.py:117-122: the finiteness guard is tested first
+    if (f) return (step << 8) | (unsigned long long)((f & 1) ? kErrNonFinite : kErrUnphysical);
+    done = DA(done, dt);
+  }
+  return 0;
+}
+
+// conserved -> primitive (ref/moments.py:122-129); returns false if degenerate.
+__device__ bool to_prim(const double* V, int nx, int i, double out[5]) {
+  const double rho = V[i], m0 = V[nx + i], m1 = V[2 * nx + i], m2 = V[3 * nx + i],
+               en = V[4 * nx + i];
+  const double u0 = DD(m0, rho), u1 = DD(m1, rho), u2 = DD(m2, rho);
+  const double mu = DA(DA(DM(m0, u0), DM(m2, u2)), DM(m1, u1));
+  const double eint = DS(en, DM(0.5, mu));
+  out[0] = rho;
+  out[1] = u0;
+  out[2] = u1;
+  out[3] = u2;
+  out[4] = DD(eint, DM(1.5, rho));
+  return !(rho <= 0.0) && !(eint <= 0.0);
+}
+
+// Batched independent G solves: blockIdx.x = window.  out = minuend - G(in)
+// when minuend != null (the parareal jump, ref/parareal.py:142).
+__global__ void __launch_bounds__(1024) fluid_batch_kernel(FluidArgs a, const double* in, double* out,
+                                                           const double* minuend, const double* t0,
+                                                           const double* t1) {
+  extern __shared__ double V[];
+  __shared__ double red[32];
+  __shared__ int flag;
+  const int w = blockIdx.x, nx = a.nx;
+  const double* src = in + (size_t)w * 5 * nx;
+  if (threadIdx.x == 0) flag = 0;
+  for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+    double v[5];
+    to_cons(src[i], src[nx + i], src[2 * nx + i], src[3 * nx + i], src[4 * nx + i], v);
+#pragma unroll
+    for (int q = 0; q < 5; ++q) V[q * nx + i] = v[q];
+  }
+  __syncthreads();
+  const double span = DS(t1[w], t0[w]);
+  double* dst = out + (size_t)w * 5 * nx;
+  const double* mn = minuend ? minuend + (size_t)w * 5 * nx : nullptr;
+  if (span == 0.0) {  // ref/fluid.py:98-99: the input itself
+    for (int i = threadIdx.x; i < 5 * nx; i += blockDim.x)
+      dst[i] = mn ? DS(mn[i], src[i]) : src[i];
+    return;
+  }
+  const ErrKey code = g_advance(V, red, &flag, a, span);
+  if (code) {
+    if (threadIdx.x == 0) atomicMin(a.err, ((ErrKey)w << 40) | code);
+    return;
+  }
+  bool ok = true;
+  for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+    double p[5];
+    ok = to_prim(V, nx, i, p) && ok;
+#pragma unroll
+    for (int q = 0; q < 5; ++q) dst[q * nx + i] = mn ? DS(mn[q * nx + i], p[q]) : p[q];
+  }
+  if (!ok) atomicMin(a.err, err_key(w, 0, kErrLiftState));
+}
+
+// Sequential correction sweep (one CTA): U_n = G(U_{n-1}) + jump_n for
+// n = start..n_g, overshoot guard, sup error (ref/parareal.py:226-248).
+__global__ void __launch_bounds__(1024) correct_kernel(FluidArgs a, int n_g, int start, double* snaps,
+                                                       const double* old, const double* jumps,
+                                                       const double* times, double* err_out) {
+  extern __shared__ double V[];
+  __shared__ double red[32];
+  __shared__ int flag;
+  __shared__ int over;
+  const int nx = a.nx;
+  double emax = 0.0;
+  if (threadIdx.x == 0) {
+    flag = 0;
+    over = 0;
+  }
+  __syncthreads();
+  for (int n = start; n <= n_g; ++n) {
+    const double* src = snaps + (size_t)(n - 1) * 5 * nx;
+    for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+      double v[5];
+      to_cons(src[i], src[nx + i], src[2 * nx + i], src[3 * nx + i], src[4 * nx + i], v);
+#pragma unroll
+      for (int q = 0; q < 5; ++q) V[q * nx + i] = v[q];
+    }
+    __syncthreads();
+    const double span = DS(times[n], times[n - 1]);
+    double* dst = snaps + (size_t)n * 5 * nx;
+    const double* jp = jumps + (size_t)(n - 1) * 5 * nx;
+    const double* od = old + (size_t)n * 5 * nx;
+    ErrKey code = 0;
+    if (span != 0.0) code = g_advance(V, red, &flag, a, span);
+    if (code) {
+      if (threadIdx.x == 0) atomicMin(a.err, ((ErrKey)n << 40) | code);
+      return;
+    }
+    bool bad = false;
+    bool degen = false;
+    for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+      double p[5];
+      if (span != 0.0) {
+        if (!to_prim(V, nx, i, p)) degen = true;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 5; ++q) p[q] = src[q * nx + i];
+      }
+      double c[5];
+#pragma unroll
+      for (int q = 0; q < 5; ++q) c[q] = DA(p[q], jp[q * nx + i]);
+      bool fin = true;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) fin = fin && isfinite(c[q]);
+      if (!fin || c[0] <= 0.0 || c[4] <= 0.0) bad = true;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) {
+        emax = fmax(emax, fabs(DS(c[q], od[q * nx + i])));
+        dst[q * nx + i] = c[q];
+      }
+    }
+    if (bad) atomicOr(&over, 1);
+    if (degen) atomicOr(&over, 2);
+    __syncthreads();
+    if (over) {
+      // a degenerate G result raises inside propagate_fluid, before the guard
+      if (threadIdx.x == 0)
+        atomicMin(a.err, err_key(n, 0, (over & 2) ? kErrLiftState : kErrOvershoot));
+      return;
+    }
+  }
+  emax = block_max(emax, red);
+  if (threadIdx.x == 0) *err_out = emax;
+}
+
+static int fluid_threads(int nx) {
+  int t = 32;
+  while (t < nx && t < 1024) t <<= 1;
+  return t;
+}
+
+cudaError_t launch_fluid_batch(const FluidArgs& a, int nwin, const double* in, double* out,
+                               const double* minuend, const double* t0, const double* t1,
+                               cudaStream_t st) {
+  const int thr = fluid_threads(a.nx);
+  if ((size_t)thr * kMaxCellsPerThread < (size_t)a.nx) return cudaErrorInvalidValue;
+  const size_t smem = (size_t)5 * a.nx * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(fluid_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  fluid_batch_kernel<<<nwin, thr, smem, st>>>(a, in, out, minuend, t0, t1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_correct(const FluidArgs& a, int n_g, int start, double* snaps, const double* old,
+                           const double* jumps, const double* times, double* err_out,
+                           cudaStream_t st) {
+  const int thr = fluid_threads(a.nx);
+  if ((size_t)thr * kMaxCellsPerThread < (size_t)a.nx) return cudaErrorInvalidValue;
+  const size_t smem = (size_t)5 * a.nx * sizeof(double);
+  cudaError_t e =
+      cudaFuncSetAttribute(correct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  correct_kernel<<<1, thr, smem, st>>>(a, n_g, start, snaps, old, jumps, times, err_out);
+  return cudaGetLastError();
+}
+
+}  // namespace pbgk

@@ -1,0 +1,177 @@
+"""Device plumbing between the reference-shaped Python API and libpbgk.so.
+
+* ``Ctx``: one ``pbgk_ctx`` (grid constants, tiling, device workspace) per
+  (grid, boundary, device); cached.
+* moment packing: a ``MomentField`` travels as a ``(5, nx)`` fp64 tensor
+  (rho, u_x, u_y, u_z, theta) — the layout of include/pbgk.h.
+* error keys from the C ABI are turned back into the reference's exceptions
+  with the reference's context fields (``step``, ``slice_index``).
+
+torch is used for device memory and streams only; every numeric operation on
+the path runs in the kernels of libpbgk.so.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import BlowUpError, CorrectionOvershootError, DegenerateStateError
+from .grid import is_periodic
+
+KIND_PROJECT, KIND_LIFT, KIND_NONFINITE, KIND_UNPHYSICAL, KIND_OVERSHOOT = range(5)
+
+_lock = threading.Lock()
+_ctx_cache: dict = {}
+
+
+def require_cuda() -> None:
+    if not torch.cuda.is_available():
+        raise RuntimeError("no CUDA device visible: this package runs its solver on the GPU "
+                           "only (there is no CPU fallback)")
+
+
+def current_device() -> torch.device:
+    require_cuda()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_handle(device: torch.device | None = None) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def ptr(t: torch.Tensor | None) -> ctypes.c_void_p:
+    return ctypes.c_void_p(0 if t is None else t.data_ptr())
+
+
+class Ctx:
+    """A libpbgk context bound to one grid, one x boundary and one device."""
+
+    def __init__(self, shape, x_min, x_max, v_max, periodic: bool, device: torch.device):
+        self.lib = _lib.load()
+        self.shape = tuple(int(n) for n in shape)
+        self.device = device
+        self.periodic = bool(periodic)
+        nx, nvx, nvy, nvz = self.shape
+        self.dx = (x_max - x_min) / nx
+        self.dv = tuple(2.0 * v_max / n for n in (nvx, nvy, nvz))
+        desc = _lib.GridDesc(nx, nvx, nvy, nvz, float(x_min), float(x_max), float(v_max),
+                             1 if periodic else 0, device.index)
+        h = ctypes.c_void_p()
+        _lib.check(self.lib.pbgk_ctx_create(ctypes.byref(desc), ctypes.byref(h)),
+                   "pbgk_ctx_create")
+        self.h = h
+        # f-sized scratch buffers reused across calls (allocated lazily)
+        self._f_tmp = [None, None]
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self.lib.pbgk_ctx_destroy(self.h)
+        except Exception:
+            pass
+
+    @property
+    def nx(self):
+        return self.shape[0]
+
+    def empty_f(self) -> torch.Tensor:
+        return torch.empty(self.shape, dtype=torch.float64, device=self.device)
+
+    def f_scratch(self, k: int = 0) -> torch.Tensor:
+        if self._f_tmp[k] is None:
+            self._f_tmp[k] = self.empty_f()
+        return self._f_tmp[k]
+
+    def empty_moments(self, n: int | None = None) -> torch.Tensor:
+        shape = (5, self.nx) if n is None else (n, 5, self.nx)
+        return torch.empty(shape, dtype=torch.float64, device=self.device)
+
+
+def ctx_for(grid, bc, device: torch.device | None = None) -> Ctx:
+    """Cached context for a (phase grid, boundary, device) triple."""
+    device = device or current_device()
+    sp, vel = grid.space, grid.velocity
+    nv = tuple(int(n) for n in vel.n_v)
+    key = (float(sp.x_min), float(sp.x_max), int(sp.n_x), float(vel.v_max), nv,
+           is_periodic(bc), device.index)
+    with _lock:
+        c = _ctx_cache.get(key)
+        if c is None:
+            c = Ctx((sp.n_x,) + nv, sp.x_min, sp.x_max, vel.v_max, is_periodic(bc), device)
+            _ctx_cache[key] = c
+        return c
+
+
+# ---------------------------------------------------------------------------
+# moments <-> (5, nx) device tensors
+# ---------------------------------------------------------------------------
+
+def pack_moments_np(rho, u, theta) -> np.ndarray:
+    nx = np.shape(rho)[0]
+    out = np.empty((5, nx))
+    out[0] = rho
+    out[1:4] = np.asarray(u, dtype=float).T
+    out[4] = theta
+    return out
+
+
+def to_device_moments(U, device: torch.device) -> torch.Tensor:
+    return torch.from_numpy(pack_moments_np(U.rho, U.u, U.theta)).to(device)
+
+
+def unpack_moments_np(m: np.ndarray):
+    return m[0].copy(), np.ascontiguousarray(m[1:4].T), m[4].copy()
+
+
+def to_device_field(force, device: torch.device, nx: int):
+    if force is None:
+        return None, 0.0
+    E = np.array(np.broadcast_to(np.asarray(force, dtype=float), (nx,)), dtype=float)
+    e_max = float(np.max(np.abs(force)))
+    return torch.from_numpy(E).to(device), e_max
+
+
+# ---------------------------------------------------------------------------
+# solver status keys -> reference exceptions
+# ---------------------------------------------------------------------------
+
+def decode(code: int):
+    """(unit, step, kind) of a status key (include/pbgk.h)."""
+    return code >> 40, (code >> 8) & 0xFFFFFFFF, code & 0xFF
+
+
+def raise_kinetic(code: int) -> None:
+    """Kinetic-path status: same exception and step as the reference raises."""
+    if code < 0:
+        return
+    _, step, kind = decode(code)
+    if kind == KIND_PROJECT:
+        raise DegenerateStateError("nonpositive density in projection")
+    if kind == KIND_LIFT:
+        raise DegenerateStateError("lift requires rho > 0 and theta > 0 in every cell")
+    if kind == KIND_NONFINITE:
+        raise BlowUpError("kinetic propagation lost finiteness at step %d" % step, step=step)
+    raise RuntimeError("unexpected kinetic status key %#x" % code)
+
+
+def raise_fluid(code: int) -> None:
+    """Coarse-path status (batched G or the correction sweep)."""
+    if code < 0:
+        return
+    unit, step, kind = decode(code)
+    if kind == KIND_OVERSHOOT:
+        raise CorrectionOvershootError(
+            "correction left the physical regime in window %d" % unit, slice_index=unit)
+    if kind == KIND_LIFT:
+        raise DegenerateStateError("nonpositive density or internal energy in conserved state")
+    if kind == KIND_NONFINITE:
+        raise BlowUpError("fluid propagation lost finiteness at step %d" % step, step=step)
+    if kind == KIND_UNPHYSICAL:
+        raise BlowUpError("fluid propagation left the physical regime at step %d" % step,
+                          step=step)
+    raise RuntimeError("unexpected fluid status key %#x" % code)
