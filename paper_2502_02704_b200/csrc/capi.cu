@@ -65,10 +65,10 @@ struct CfgShape {
   bool tma;
 };
 const CfgShape kCfg[] = {
-    {2, 32, 8, 512, true},  // 0: nvz % 64 == 0
-    {2, 16, 8, 512, true},  // 1: nvz % 32 == 0
-    {2, 16, 4, 512, true},  // 2: nvz % 32 == 0 (field / small)
-    {3, 16, 4, 512, true},  // 3: nvz % 48 == 0
+    {4, 16, 4, 256, true},  // 0: nvz % 64 == 0
+    {4, 8, 4, 256, true},   // 1: nvz % 32 == 0
+    {2, 16, 4, 256, true},  // 2: nvz % 32 == 0 (alternative)
+    {3, 16, 4, 256, true},  // 3: nvz % 48 == 0
     {2, 8, 4, 256, true},   // 4: nvz % 16 == 0
     {2, 4, 4, 256, true},   // 5: nvz % 8 == 0
     {1, 32, 4, 256, false}, // 6: anything (no TMA)
@@ -107,7 +107,7 @@ struct pbgk_ctx {
   pbgk_grid_desc g;
   double dx, dv[3], dvol;
   int dev, nsm;
-  size_t smem_optin;
+  size_t smem_optin, smem_per_sm;
   double* d_c[3] = {nullptr, nullptr, nullptr};
   Plan plan[2];  // [0] no field, [1] v_x field term
   int TL, gxo, gyo, gzo;
@@ -133,9 +133,9 @@ bool make_plan(pbgk_ctx* c, bool field, Plan& out) {
   const int npos = nvx - nneg;
   std::vector<int> cands;
   const bool even = (nvz % 2 == 0);
-  if (even && nvz % 64 == 0) cands.push_back(field ? 2 : 0);
+  if (even && nvz % 64 == 0) cands.push_back(0);
   if (even && nvz % 48 == 0) cands.push_back(3);
-  if (even && nvz % 32 == 0) cands.push_back(field ? 2 : 1);
+  if (even && nvz % 32 == 0) cands.push_back(2);
   if (even && nvz % 16 == 0) cands.push_back(4);
   if (even && nvz % 8 == 0) cands.push_back(5);
   cands.push_back(6);
@@ -151,7 +151,7 @@ bool make_plan(pbgk_ctx* c, bool field, Plan& out) {
     for (int A = 1; A <= lines; A *= 2) {
       if (A > std::max(nneg, npos) && A > 1) break;
       int By = lines / A;
-      if (By > nvy) By = nvy;
+      while (By > nvy && By > 1) By >>= 1;  // power of two (the kernel shifts by log2 By)
       if (By < 1 || By > 256 || A + (field ? 2 : 0) > 256) continue;
       if (A + By + Bz > s.NTHR) continue;
       Tiling t;
@@ -172,6 +172,7 @@ bool make_plan(pbgk_ctx* c, bool field, Plan& out) {
       const double part = 2.0 * t.NT * t.PS;
       // shared memory for 2 stages at least
       SweepArgs dummy{};
+      dummy.nvx = nvx;
       dummy.t = t;
       dummy.TL = c->TL;
       const size_t sm2 = sweep_smem_bytes(dummy, s.V, s.LZ, s.NTHR, false, s.tma, 2);
@@ -195,13 +196,22 @@ bool make_plan(pbgk_ctx* c, bool field, Plan& out) {
   if (!found) return false;
   const CfgShape& s = kCfg[out.cfg];
   SweepArgs dummy{};
+  dummy.nvx = nvx;
   dummy.t = out.t;
   dummy.TL = c->TL;
+  // two CTAs per SM when the ring fits in half the shared memory, else one
+  const size_t half = (c->smem_per_sm / 2) - 2048;
   int ns = 4;
-  while (ns > 2 && sweep_smem_bytes(dummy, s.V, s.LZ, s.NTHR, false, s.tma, ns) > c->smem_optin) --ns;
+  while (ns > 2 && sweep_smem_bytes(dummy, s.V, s.LZ, s.NTHR, false, s.tma, ns) > half) --ns;
+  int per_sm = 2;
+  if (sweep_smem_bytes(dummy, s.V, s.LZ, s.NTHR, false, s.tma, ns) > half) {
+    per_sm = 1;
+    ns = 4;
+    while (ns > 2 && sweep_smem_bytes(dummy, s.V, s.LZ, s.NTHR, false, s.tma, ns) > c->smem_optin) --ns;
+  }
   out.ns = s.tma ? ns : 1;
   const long long items = (long long)out.t.NT * c->g.nx;
-  long long grid = c->nsm;
+  long long grid = (long long)c->nsm * per_sm;
   if (grid > items) grid = items;
   out.grid = (int)std::max<long long>(grid, 1);
   return true;
@@ -307,8 +317,9 @@ int run_sweep(pbgk_ctx* c, int pid, bool field, const double* in, const double* 
 
 int run_final(pbgk_ctx* c, int pid, int mode, const double* mom_in, double* mom_out,
               double* tab, double dt, double eps, double tau, const double* tau_cells, int step,
-              cudaStream_t st) {
+              cudaStream_t st, int check_finite = 0) {
   FinalArgs f = fin_args(c, c->plan[pid]);
+  f.check_finite = check_finite;
   f.mode = mode;
   f.mom_in = mom_in;
   f.mom_out = mom_out;
@@ -363,10 +374,11 @@ int pbgk_ctx_create(const pbgk_grid_desc* g, pbgk_ctx** out) {
   if (cudaGetDeviceProperties(&prop, c->dev) != cudaSuccess) return bail(fail("device query failed"));
   c->nsm = prop.multiProcessorCount;
   c->smem_optin = prop.sharedMemPerBlockOptin;
+  c->smem_per_sm = prop.sharedMemPerMultiprocessor;
   // table row: [r, ls, gx(nvx), gy(nvy), gz(nvz)] padded to 16 bytes
   c->gxo = 2;
   c->gyo = c->gxo + g->nvx;
-  c->gzo = c->gyo + g->nvy;
+  c->gzo = (c->gyo + g->nvy + 1) & ~1;  // 16-byte aligned for vector reads
   c->TL = (c->gzo + g->nvz + 1) & ~1;
   if (!make_plan(c, false, c->plan[0]) || !make_plan(c, true, c->plan[1]))
     return bail(fail("no tiling fits this velocity grid"));
@@ -467,6 +479,7 @@ int pbgk_check_finite(pbgk_ctx* c, const double* f, int step, void* stream, long
   if (reset_err(c, st)) return -1;
   if (run_final(c, 0, kFinIdentity, nullptr, nullptr, c->d_tab[0], 0, 1, 1, nullptr, 0, st)) return -1;
   if (run_sweep(c, 0, false, f, c->d_tab[0], nullptr, 0.0, nullptr, 0.0, 0.0, step, st)) return -1;
+  if (run_final(c, 0, kFinProject, nullptr, nullptr, nullptr, 0, 1, 1, nullptr, step, st, 1)) return -1;
   return fetch_err(c, st, h_code);
 }
 

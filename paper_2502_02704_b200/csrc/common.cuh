@@ -87,6 +87,7 @@ struct FinalArgs {
   const double* tau_arr; // optional per-cell tau values
   ErrKey* err;
   int step;
+  int check_finite;      // kFinProject: flag non-finite marginals as BlowUpError(step)
 };
 
 }  // namespace pbgk

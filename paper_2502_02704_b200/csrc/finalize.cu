@@ -49,6 +49,7 @@ __global__ void __launch_bounds__(128) finalize_kernel(const FinalArgs a) {
   }
 
   double rho, u0, u1, u2, th;
+  int nonfinite = 0;
   if (a.mom_in != nullptr) {
     rho = a.mom_in[i];
     u0 = a.mom_in[a.nx + i];
@@ -91,7 +92,11 @@ __global__ void __launch_bounds__(128) finalize_kernel(const FinalArgs a) {
         mz[jz] = s;
       }
     }
-    __syncthreads();
+    // finiteness of f* (all its values feed these sums; a NaN/Inf anywhere
+    // leaves a non-finite marginal) -- the guard of ref/kinetic.py:157-159
+    int bad = 0;
+    for (int j = tid; j < nvx + nvy + nvz; j += blockDim.x) bad |= !isfinite(sm[j]);
+    nonfinite = __syncthreads_or(bad);
     if (warp == 0) {
       double s = 0.0;
       for (int j = lane; j < nvx; j += 32) s += mx[j];
@@ -137,7 +142,10 @@ __global__ void __launch_bounds__(128) finalize_kernel(const FinalArgs a) {
     a.mom_out[3 * a.nx + i] = u2;
     a.mom_out[4 * a.nx + i] = th;
   }
-  if (a.mode == kFinProject) return;
+  if (a.mode == kFinProject) {
+    if (a.check_finite && nonfinite && tid == 0) atomicMin(a.err, err_key(0, a.step, kErrNonFinite));
+    return;
+  }
 
   if (tid == 0 && (rho <= 0.0 || th <= 0.0)) atomicMin(a.err, err_key(0, a.step, kErrLiftState));
   const double inv2t = 1.0 / (2.0 * th);
@@ -172,6 +180,11 @@ __global__ void __launch_bounds__(128) finalize_kernel(const FinalArgs a) {
       ls = scale;
     }
   }
+  // f_s = R_s(f*_s) is finite iff f*_s and the table row are (BlowUpError(step))
+  if (a.mode == kFinRelax && tid == 0 &&
+      (nonfinite || !isfinite(r) || !isfinite(ls) || !isfinite(amp) || !isfinite(u0) ||
+       !isfinite(u1) || !isfinite(u2) || !isfinite(th)))
+    atomicMin(a.err, err_key(0, a.step, kErrNonFinite));
   double* row = a.tab + (size_t)i * a.TL;
   for (int j = tid; j < a.TL; j += blockDim.x) {
     double v = 0.0;

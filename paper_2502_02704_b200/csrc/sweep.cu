@@ -11,19 +11,22 @@
 // of reading it (SYNTH); the last pass applies R_S only (dtdx == 0) and may
 // skip the write (the window only needs P(f_S)).
 //
-// Work decomposition (persistent, 1 CTA per SM):
+// Work decomposition (persistent CTAs, 2 per SM):
 //   velocity box "tile" (A rows of v_x, By of v_y, Bz of v_z) x all x cells.
 //   Every tile has one sign of c_x, so its upwind neighbour plane is on one
-//   side: c_x >= 0 tiles march upward in x, c_x < 0 tiles march downward and
-//   a register sliding window holds f_pre of the previous plane.  The
-//   (tile, plane) sequence is cut into gridDim.x contiguous segments; a
-//   segment pays one halo plane per tile it touches.
+//   side: c_x >= 0 tiles march upward in x, c_x < 0 tiles march downward, and
+//   each thread keeps f_pre of the previous plane for its elements in
+//   registers.  The (tile, plane) sequence is cut into gridDim.x contiguous
+//   segments; a segment pays one halo plane per tile run it touches.
 //   Each plane's box arrives by one 4-D TMA copy (plus a 1-D bulk copy of the
 //   cell's table row) into a ring of `ns` shared-memory stages.
+//   Thread layout: LZ lanes x V consecutive v_z per box line (a line is one
+//   (v_x, v_y) pair of the box), K lines per thread.
 //
-// Reductions are deterministic and mirror-symmetric (same tree for every
+// Reductions are deterministic and mirror-symmetric (the same tree for every
 // marginal index), so even data keeps an exactly-zero folded first moment
-// (ref/moments.py:80-88).
+// (ref/moments.py:80-88).  Non-finite values are not tested per element here:
+// they propagate into the marginals and the finalize kernel flags the step.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -35,7 +38,7 @@ namespace pbgk {
 constexpr unsigned FULL = 0xffffffffu;
 
 // Reduce-scatter of C per-lane line values over the W..1 lane bits of an
-// aligned lane group.  After the split levels each lane holds C' = max(C/LZ,1)
+// aligned lane group.  After the split levels each lane holds max(C/LZ, 1)
 // line totals; `base` is the index of the first one.  Every line total is the
 // same binary tree over lanes (fp add is commutative), for every line.
 template <int C, int W>
@@ -87,66 +90,67 @@ __device__ __forceinline__ TileGeom tile_geom(const Tiling& t, int nvx, int tile
   return g;
 }
 
-// Item j of the segment [g0, g1): each run of consecutive planes of one tile
-// is preceded by its halo (upwind neighbour) plane.
-struct Item {
-  int tile;
-  int plane;  // x cell to load
-  bool halo;
-  bool ghost;  // absorbing ghost: f_pre == 0, nothing to load
-  bool down;
-};
+// Walks the items of a segment [g0, g1) of the (tile, position) sequence:
+// every run of consecutive positions of one tile is preceded by its halo
+// (the upwind neighbour plane of the run's first plane).
+struct ItemIter {
+  int g, g1;    // next plane-item index (global linear) and segment end
+  int tile, p;  // tile and position of g
+  bool halo_next;
 
-__device__ __forceinline__ long long seg_items(long long g0, long long g1, int nx) {
-  if (g1 <= g0) return 0;
-  const long long len0 = min((long long)nx - g0 % nx, g1 - g0);
-  const long long rest = g1 - g0 - len0;
-  const long long runs = 1 + (rest + nx - 1) / nx;
-  return (g1 - g0) + runs;
-}
-
-__device__ __forceinline__ Item seg_item(const SweepArgs& a, long long g0, long long g1,
-                                         long long j) {
-  const int nx = a.nx;
-  const long long len0 = min((long long)nx - g0 % nx, g1 - g0);
-  long long g;
-  bool halo;
-  if (j < 1 + len0) {
-    halo = (j == 0);
-    g = halo ? g0 : g0 + j - 1;
-  } else {
-    const long long jj = j - 1 - len0;
-    const long long r = jj / (1 + nx);
-    const long long q = jj - r * (1 + nx);
-    const long long gs = g0 + len0 + r * nx;
-    halo = (q == 0);
-    g = halo ? gs : gs + q - 1;
+  __device__ __forceinline__ void init(int g0, int end, int nx) {
+    g = g0;
+    g1 = end;
+    tile = g0 / nx;
+    p = g0 - tile * nx;
+    halo_next = g0 < end;
   }
-  Item it;
-  it.tile = (int)(g / nx);
-  const int p = (int)(g - (long long)it.tile * nx);
-  const TileGeom tg = tile_geom(a.t, a.nvx, it.tile);
-  it.down = tg.down;
-  int i = tg.down ? nx - 1 - p : p;
-  it.halo = halo;
-  it.ghost = false;
-  if (halo) {
-    i += tg.down ? 1 : -1;
-    if (i < 0 || i >= nx) {
-      if (a.periodic) {
-        i = (i + nx) % nx;
-      } else {
-        it.ghost = true;
-        i = 0;
-      }
+  __device__ __forceinline__ bool done() const { return g >= g1 && !halo_next; }
+  // current item: (tile, p, halo); then advance
+  __device__ __forceinline__ void next(int nx, int& t_out, int& p_out, bool& halo_out) {
+    t_out = tile;
+    p_out = p;
+    halo_out = halo_next;
+    if (halo_next) {
+      halo_next = false;
+      return;
+    }
+    ++g;
+    if (++p == nx) {
+      p = 0;
+      ++tile;
+      halo_next = g < g1;
     }
   }
-  it.plane = i;
-  return it;
+};
+
+// x cell loaded for an item; -1 = absorbing ghost (f_pre == 0)
+__device__ __forceinline__ int item_plane(int nx, int periodic, const TileGeom& tg, int p, bool halo) {
+  int i = tg.down ? nx - 1 - p : p;
+  if (halo) {
+    i += tg.down ? 1 : -1;
+    if (i < 0 || i >= nx) i = periodic ? (i + nx) % nx : -1;
+  }
+  return i;
+}
+
+template <int V>
+__device__ __forceinline__ void lds_vec(const double* p, double (&x)[V]) {
+  if constexpr (V % 2 == 0) {
+#pragma unroll
+    for (int v = 0; v < V; v += 2) {
+      const double2 t = *reinterpret_cast<const double2*>(p + v);
+      x[v] = t.x;
+      x[v + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int v = 0; v < V; ++v) x[v] = p[v];
+  }
 }
 
 template <int V, int LZ, int K, int NTHR, bool SYNTH, bool FIELD, bool TMA>
-__global__ void __launch_bounds__(NTHR, 1)
+__global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? 2 : 1))
     sweep_kernel(const __grid_constant__ CUtensorMap fmap, const SweepArgs a, int ns) {
   constexpr int NL = NTHR / LZ;  // line groups
   constexpr int NW = NTHR / 32;
@@ -162,174 +166,235 @@ __global__ void __launch_bounds__(NTHR, 1)
   const int lg = tid / LZ;
   const int hoff = (T.rows_load - T.A) >> 1;  // neighbour rows loaded for the field term
   const int lines = T.A * T.By;
+  const int lgBy = __ffs(T.By) - 1;  // By is a power of two
+  const int nx = a.nx;
 
-  const uint32_t box_bytes = SYNTH ? 0u : (uint32_t)(T.rows_load * T.By * BZ * 8);
+  const uint32_t box_elems = (uint32_t)(T.rows_load * T.By * BZ);
+  const uint32_t box_bytes = SYNTH ? 0u : box_elems * 8u;
   const uint32_t tab_bytes = (uint32_t)(a.TL * 8);
-  const uint32_t stage_bytes = TMA ? ((box_bytes + tab_bytes + 127u) & ~127u) : 0u;
+  const uint32_t stage_bytes = (box_bytes + tab_bytes + 127u) & ~127u;
   double* LT = reinterpret_cast<double*>(smem + (size_t)ns * stage_bytes);  // [2][lines]
   double* PZ = LT + 2 * lines;                                              // [2][NW][BZ]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(PZ + 2 * NW * BZ);           // [ns]
+  double* SCX = PZ + 2 * NW * BZ;                                           // [nvx] x-velocity centres
+  uint64_t* bars = reinterpret_cast<uint64_t*>(SCX + ((a.nvx + 1) & ~1));   // [ns]
 
-  const long long g0 = (a.total * blockIdx.x) / gridDim.x;
-  const long long g1 = (a.total * (blockIdx.x + 1)) / gridDim.x;
-  const long long n_items = seg_items(g0, g1, a.nx);
+  const int g0 = (int)((a.total * blockIdx.x) / gridDim.x);
+  const int g1 = (int)((a.total * (blockIdx.x + 1)) / gridDim.x);
 
-  if (TMA) {
-    if (tid == 0) {
-      for (int s = 0; s < ns; ++s) mbar_init(&bars[s], 1);
-      fence_mbar_init();
-    }
-    __syncthreads();
+  for (int j = tid; j < a.nvx; j += NTHR) SCX[j] = a.cx[j];
+  if (TMA && tid == 0) {
+    for (int s = 0; s < ns; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
   }
+  __syncthreads();
 
-  auto issue = [&](long long j) {
-    const Item it = seg_item(a, g0, g1, j);
-    const int s = (int)(j % ns);
+  // producer state (thread 0 only): loads run ns items ahead
+  ItemIter prod;
+  prod.init(g0, g1, nx);
+  int issued = 0;
+  auto issue_next = [&]() {
+    int t, p;
+    bool h;
+    prod.next(nx, t, p, h);
+    const TileGeom tg = tile_geom(T, a.nvx, t);
+    const int i = item_plane(nx, a.periodic, tg, p, h);
+    const int s = (int)(issued % ns);
     uint64_t* bar = &bars[s];
     unsigned char* st = smem + (size_t)s * stage_bytes;
-    if (it.ghost) {
+    ++issued;
+    if (i < 0) {
       mbar_arrive_expect_tx(bar, 0);
       return;
     }
-    const TileGeom tg = tile_geom(T, a.nvx, it.tile);
     mbar_arrive_expect_tx(bar, box_bytes + tab_bytes);
-    if (!SYNTH) tma_load_4d(st, &fmap, tg.z0, tg.y0, tg.r0 - hoff, it.plane, bar);
-    tma_load_1d(st + box_bytes, a.tab + (size_t)it.plane * a.TL, tab_bytes, bar);
+    if (!SYNTH) tma_load_4d(st, &fmap, tg.z0, tg.y0, tg.r0 - hoff, i, bar);
+    tma_load_1d(st + box_bytes, a.tab + (size_t)i * a.TL, tab_bytes, bar);
   };
-
   if (TMA && tid == 0) {
     prefetch_tensormap(&fmap);
-    const long long pre = n_items < ns ? n_items : ns;
-    for (long long j = 0; j < pre; ++j) issue(j);
+    for (int s = 0; s < ns && !prod.done(); ++s) issue_next();
   }
 
-  double prev[K][V];
-  double cur[K][V];
+  // per-thread line constants: smem offset of (line, first v_z of this lane)
+  // in the box, and the line's (row, column) inside the box packed as a<<16|b
+  int soff[K], lab[K];
 #pragma unroll
-  for (int k = 0; k < K; ++k)
-#pragma unroll
-    for (int v = 0; v < V; ++v) prev[k][v] = 0.0;
-  bool bad = false;
+  for (int k = 0; k < K; ++k) {
+    int l = lg + k * NL;
+    if (l >= lines) l = 0;
+    const int aa = l >> lgBy, b = l & (T.By - 1);
+    soff[k] = ((aa + hoff) * T.By + b) * BZ + lz * V;
+    lab[k] = (aa << 16) | b;
+  }
+  unsigned vmask = 0;  // bit k: line k is inside the tile and the grid
+  bool zok = false;
+  int cur_tile = -1;
+  TileGeom tg{};
 
-  for (long long j = 0; j < n_items; ++j) {
-    const Item it = seg_item(a, g0, g1, j);
-    const TileGeom tg = tile_geom(T, a.nvx, it.tile);
+  double prev[K][V];
+  bool zero_prev = true;
+
+  ItemIter it;
+  it.init(g0, g1, nx);
+  int j = 0;
+  while (!it.done()) {
+    int t, p;
+    bool halo;
+    it.next(nx, t, p, halo);
+    if (t != cur_tile) {
+      cur_tile = t;
+      tg = tile_geom(T, a.nvx, t);
+      vmask = 0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int l = lg + k * NL;
+        const int jx = tg.r0 + (lab[k] >> 16), jy = tg.y0 + (lab[k] & 0xffff);
+        if (l < lines && jx < tg.r1 && jy < a.nvy) vmask |= 1u << k;
+      }
+      zok = tg.z0 + lz * V < a.nvz;  // V divides the z extent when TMA is used
+    }
+    const int i = item_plane(nx, a.periodic, tg, p, halo);
     const int s = (int)(j % ns);
     const double* SF = reinterpret_cast<const double*>(smem + (size_t)s * stage_bytes);
     const double* ST = reinterpret_cast<const double*>(smem + (size_t)s * stage_bytes + box_bytes);
-    const double* GT = a.tab + (size_t)it.plane * a.TL;
-    if (TMA) mbar_wait(&bars[s], (uint32_t)((j / ns) & 1));
+    if (TMA) {
+      mbar_wait(&bars[s], (uint32_t)((j / ns) & 1));
+    } else if (i >= 0) {
+      // generic path: cooperative synchronous load of the box and the table row
+      double* sf = reinterpret_cast<double*>(smem);
+      for (uint32_t e = tid; e < box_elems && !SYNTH; e += NTHR) {
+        const int zz = e % BZ, rest = e / BZ;
+        const int b = rest % T.By, br = rest / T.By;
+        const int jx = tg.r0 - hoff + br, jy = tg.y0 + b, jz = tg.z0 + zz;
+        double v = 0.0;
+        if (jx >= 0 && jx < a.nvx && jy < a.nvy && jz < a.nvz)
+          v = a.fin[(size_t)i * a.plane + ((size_t)jx * a.nvy + jy) * a.nvz + jz];
+        sf[e] = v;
+      }
+      for (int e = tid; e < a.TL; e += NTHR) sf[box_bytes / 8 + e] = a.tab[(size_t)i * a.TL + e];
+      __syncthreads();
+    }
 
-    auto tab = [&](int idx) -> double { return TMA ? ST[idx] : __ldg(GT + idx); };
-    // raw f*_{s-1} value at box row `brow` (halo-offset row index), line b, box z `zz`
-    auto raw = [&](int brow, int b, int zz) -> double {
-      if (SYNTH) return 0.0;
-      if (TMA) return SF[(brow * T.By + b) * BZ + zz];
-      const int jx = tg.r0 - hoff + brow, jy = tg.y0 + b, jz = tg.z0 + zz;
-      if (jx < 0 || jx >= a.nvx || jy >= a.nvy || jz >= a.nvz) return 0.0;
-      return __ldg(a.fin + (size_t)it.plane * a.plane + ((size_t)jx * a.nvy + jy) * a.nvz + jz);
-    };
-
-    if (it.ghost) {
+    if (i < 0) {
+      // absorbing ghost plane: f_pre == 0
 #pragma unroll
       for (int k = 0; k < K; ++k)
 #pragma unroll
-        for (int v = 0; v < V; ++v) cur[k][v] = 0.0;
+        for (int v = 0; v < V; ++v) prev[k][v] = 0.0;
+      zero_prev = false;
     } else {
-      const double r = tab(0), ls = tab(1);
+      const double r = ST[0], ls = ST[1];
       double gz[V];
+      lds_vec<V>(ST + a.gzo + (zok ? tg.z0 + lz * V : 0), gz);
+      if (!zok) {
 #pragma unroll
-      for (int v = 0; v < V; ++v) {
-        const int jz = tg.z0 + lz * V + v;
-        gz[v] = (jz < a.nvz) ? tab(a.gzo + jz) : 0.0;
+        for (int v = 0; v < V; ++v) gz[v] = 0.0;
       }
-      double out[K][V];
+      const bool out_plane = !halo;
+      const bool transport = a.dtdx != 0.0;
+      double hE = 0.0;
+      if (FIELD && out_plane) hE = __dmul_rn(0.5, __ldg(a.E + i));
+      double* gdst = (a.fout != nullptr && out_plane) ? a.fout + (size_t)i * a.plane : nullptr;
       double lp[K];
       double pz[V];
 #pragma unroll
       for (int v = 0; v < V; ++v) pz[v] = 0.0;
-      const double hE = (FIELD && !it.halo) ? __dmul_rn(0.5, a.E[it.plane]) : 0.0;
-
+      if (zero_prev) {
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+#pragma unroll
+          for (int v = 0; v < V; ++v) prev[k][v] = 0.0;
+        zero_prev = false;
+      }
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        const int l = lg + k * NL;
-        const int ls_ = (l < lines) ? l : 0;  // keep smem reads inside the box
-        const int aa = ls_ / T.By;
-        const int b = ls_ - aa * T.By;
-        const int jx = tg.r0 + aa;
-        const int jy = tg.y0 + b;
-        const bool okl = (l < lines) && (jx < tg.r1) && (jy < a.nvy);
-        const int jxs = okl ? jx : tg.r0;
-        const int jys = okl ? jy : 0;
-        const double gxy = okl ? tab(a.gxo + jxs) * tab(a.gyo + jys) : 0.0;
-        // f_pre at the neighbour rows (field term only)
-        double gxm = 0.0, gxp = 0.0;
-        if (FIELD && !it.halo && okl) {
-          if (jx > 0) gxm = tab(a.gxo + jx - 1) * tab(a.gyo + jy);
-          if (jx + 1 < a.nvx) gxp = tab(a.gxo + jx + 1) * tab(a.gyo + jy);
-        }
-        const double c = okl ? __ldg(a.cx + jxs) : 0.0;
-        lp[k] = 0.0;
+        const bool ok = ((vmask >> k) & 1u) && zok;
+        const int jx = min(tg.r0 + (lab[k] >> 16), a.nvx - 1);
+        const int jy = min(tg.y0 + (lab[k] & 0xffff), a.nvy - 1);
+        const double gxy = ST[a.gxo + jx] * ST[a.gyo + jy];
+        double x[V];
+        if (SYNTH) {
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-          const int zz = lz * V + v;
-          const bool ok = okl && (tg.z0 + zz < a.nvz);
-          double x;
-          if (SYNTH) {
-            x = (gxy * gz[v]) * ls;
+          for (int v = 0; v < V; ++v) x[v] = (gxy * gz[v]) * ls;
+        } else {
+          double raw[V];
+          lds_vec<V>(SF + soff[k], raw);
+#pragma unroll
+          for (int v = 0; v < V; ++v) x[v] = fma(ls, gxy * gz[v], raw[v]) * r;
+        }
+        if (out_plane) {
+          double o[V];
+          if (transport) {
+            const double c = SCX[jx];
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+              const double y = prev[k][v];
+              const double fhi = tg.down ? __dmul_rn(c, y) : __dmul_rn(c, x[v]);
+              const double flo = tg.down ? __dmul_rn(c, x[v]) : __dmul_rn(c, y);
+              o[v] = __dsub_rn(x[v], __dmul_rn(a.dtdx, __dsub_rn(fhi, flo)));
+            }
           } else {
-            x = fma(ls, gxy * gz[v], raw(aa + hoff, b, zz)) * r;
+#pragma unroll
+            for (int v = 0; v < V; ++v) o[v] = x[v];
           }
-          if (a.check_step > 0 && ok && !isfinite(x)) bad = true;
-          cur[k][v] = x;
-          if (it.halo) continue;
-          double o = x;
-          if (a.dtdx != 0.0) {
-            const double y = prev[k][v];
-            const double fhi = it.down ? __dmul_rn(c, y) : __dmul_rn(c, x);
-            const double flo = it.down ? __dmul_rn(c, x) : __dmul_rn(c, y);
-            o = __dsub_rn(x, __dmul_rn(a.dtdx, __dsub_rn(fhi, flo)));
-          }
-          if (FIELD) {
-            // ref/kinetic.py:114-123, Rusanov flux on interior v_x faces of f_pre
-            double fm = 0.0, fp = 0.0;
-            if (okl && jx > 0) {
-              fm = SYNTH ? (gxm * gz[v]) * ls : fma(ls, gxm * gz[v], raw(aa + hoff - 1, b, zz)) * r;
+          if (FIELD && transport) {
+            // ref/kinetic.py:114-123: Rusanov flux on interior v_x faces of f_pre
+            const bool has_lo = jx > 0, has_hi = jx + 1 < a.nvx;
+            double fm[V], fp[V];
+            const double gym = ST[a.gyo + jy];
+            const double gxm = has_lo ? ST[a.gxo + jx - 1] * gym : 0.0;
+            const double gxp = has_hi ? ST[a.gxo + jx + 1] * gym : 0.0;
+            if (SYNTH) {
+#pragma unroll
+              for (int v = 0; v < V; ++v) {
+                fm[v] = (gxm * gz[v]) * ls;
+                fp[v] = (gxp * gz[v]) * ls;
+              }
+            } else {
+              double rm[V], rp[V];
+              lds_vec<V>(SF + soff[k] - T.By * BZ, rm);
+              lds_vec<V>(SF + soff[k] + T.By * BZ, rp);
+#pragma unroll
+              for (int v = 0; v < V; ++v) {
+                fm[v] = fma(ls, gxm * gz[v], rm[v]) * r;
+                fp[v] = fma(ls, gxp * gz[v], rp[v]) * r;
+              }
             }
-            if (okl && jx + 1 < a.nvx) {
-              fp = SYNTH ? (gxp * gz[v]) * ls : fma(ls, gxp * gz[v], raw(aa + hoff + 1, b, zz)) * r;
-            }
-            const double ghi = (jx + 1 < a.nvx)
-                                   ? __dsub_rn(__dmul_rn(hE, __dadd_rn(x, fp)),
-                                               __dmul_rn(a.half_emax, __dsub_rn(fp, x)))
-                                   : 0.0;
-            const double glo = (jx > 0) ? __dsub_rn(__dmul_rn(hE, __dadd_rn(fm, x)),
-                                                    __dmul_rn(a.half_emax, __dsub_rn(x, fm)))
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+              const double ghi = has_hi ? __dsub_rn(__dmul_rn(hE, __dadd_rn(x[v], fp[v])),
+                                                    __dmul_rn(a.half_emax, __dsub_rn(fp[v], x[v])))
                                         : 0.0;
-            o = __dsub_rn(o, __dmul_rn(a.dtdv, __dsub_rn(ghi, glo)));
-          }
-          const double m = ok ? o : 0.0;
-          out[k][v] = m;
-          pz[v] += m;
-          lp[k] += m;
-        }
-        if (!it.halo && a.fout != nullptr && okl) {
-          double* dst = a.fout + (size_t)it.plane * a.plane + ((size_t)jx * a.nvy + jy) * a.nvz +
-                        tg.z0 + lz * V;
-          if constexpr (V == 2) {
-            if (tg.z0 + lz * V + 1 < a.nvz) {
-              st_global_v2(dst, out[k][0], out[k][1]);
-            } else if (tg.z0 + lz * V < a.nvz) {
-              dst[0] = out[k][0];
+              const double glo = has_lo ? __dsub_rn(__dmul_rn(hE, __dadd_rn(fm[v], x[v])),
+                                                    __dmul_rn(a.half_emax, __dsub_rn(x[v], fm[v])))
+                                        : 0.0;
+              o[v] = __dsub_rn(o[v], __dmul_rn(a.dtdv, __dsub_rn(ghi, glo)));
             }
-          } else {
+          }
+          double sl = 0.0;
 #pragma unroll
-            for (int v = 0; v < V; ++v)
-              if (tg.z0 + lz * V + v < a.nvz) dst[v] = out[k][v];
+          for (int v = 0; v < V; ++v) {
+            const double m = ok ? o[v] : 0.0;
+            pz[v] += m;
+            sl += m;
+          }
+          lp[k] = sl;
+          if (gdst != nullptr && ok) {
+            double* d = gdst + ((jx * a.nvy + jy) * a.nvz + tg.z0 + lz * V);
+            if constexpr (V % 2 == 0) {
+#pragma unroll
+              for (int v = 0; v < V; v += 2) st_global_v2(d + v, o[v], o[v + 1]);
+            } else {
+#pragma unroll
+              for (int v = 0; v < V; ++v)
+                if (tg.z0 + lz * V + v < a.nvz) d[v] = o[v];
+            }
           }
         }
+#pragma unroll
+        for (int v = 0; v < V; ++v) prev[k][v] = x[v];
       }
-      if (!it.halo) {
+      if (out_plane) {
         // line totals -> LT, z partials -> PZ (double-buffered by item parity)
         double* LTb = LT + (j & 1) * lines;
         double* PZb = PZ + (j & 1) * NW * BZ;
@@ -357,14 +422,14 @@ __global__ void __launch_bounds__(NTHR, 1)
     }
 
     __syncthreads();
-    if (TMA && tid == 0 && j + ns < n_items) {
+    if (TMA && tid == 0 && !prod.done()) {
       fence_proxy_async();
-      issue(j + ns);
+      issue_next();
     }
-    if (!it.halo && !it.ghost) {
+    if (!halo && i >= 0) {
       const double* LTb = LT + (j & 1) * lines;
       const double* PZb = PZ + (j & 1) * NW * BZ;
-      double* dst = a.part + ((size_t)it.plane * T.NT + it.tile) * T.PS;
+      double* dst = a.part + ((size_t)i * T.NT + t) * T.PS;
       if (tid < T.A) {
         if (tg.r0 + tid < tg.r1) {
           double s2 = 0.0;
@@ -382,27 +447,20 @@ __global__ void __launch_bounds__(NTHR, 1)
         const int zz = tid - T.A - T.By;
         if (tg.z0 + zz < a.nvz) {
           double s2 = 0.0;
+#pragma unroll
           for (int w = 0; w < NW; ++w) s2 += PZb[w * BZ + zz];
           dst[T.A + T.By + zz] = s2;
         }
       }
     }
-#pragma unroll
-    for (int k = 0; k < K; ++k)
-#pragma unroll
-      for (int v = 0; v < V; ++v) prev[k][v] = cur[k][v];
+    if (!TMA) __syncthreads();  // the single stage is refilled next item
+    ++j;
   }
-  if (bad) atomicMin(a.err, err_key(0, a.check_step, kErrNonFinite));
 }
 
 // ---------------------------------------------------------------------------
 // host-side dispatch
 // ---------------------------------------------------------------------------
-
-struct SweepCfg {
-  int V, LZ, K, NTHR;
-  bool tma;
-};
 
 template <int V, int LZ, int K, int NTHR, bool TMA>
 static cudaError_t launch_cfg(const CUtensorMap& map, const SweepArgs& a, bool synth, bool field,
@@ -424,18 +482,20 @@ static cudaError_t launch_cfg(const CUtensorMap& map, const SweepArgs& a, bool s
 size_t sweep_smem_bytes(const SweepArgs& a, int V, int LZ, int NTHR, bool synth, bool tma, int ns) {
   const int BZ = LZ * V;
   const size_t box = synth ? 0 : (size_t)a.t.rows_load * a.t.By * BZ * 8;
-  const size_t stage = tma ? ((box + (size_t)a.TL * 8 + 127) & ~(size_t)127) : 0;
+  const size_t stage = (box + (size_t)a.TL * 8 + 127) & ~(size_t)127;
   const size_t lines = (size_t)a.t.A * a.t.By;
-  return (size_t)ns * stage + 2 * lines * 8 + 2 * (size_t)(NTHR / 32) * BZ * 8 + (size_t)ns * 8 + 16;
+  if (!tma) ns = 1;
+  return (size_t)ns * stage + 2 * lines * 8 + 2 * (size_t)(NTHR / 32) * BZ * 8 +
+         (size_t)((a.nvx + 1) & ~1) * 8 + (size_t)ns * 8 + 16;
 }
 
 cudaError_t launch_sweep(int cfg_id, const CUtensorMap& map, const SweepArgs& a, bool synth,
                          bool field, int grid, int ns, size_t smem, cudaStream_t st) {
   switch (cfg_id) {
-    case 0: return launch_cfg<2, 32, 8, 512, true>(map, a, synth, field, grid, ns, smem, st);
-    case 1: return launch_cfg<2, 16, 8, 512, true>(map, a, synth, field, grid, ns, smem, st);
-    case 2: return launch_cfg<2, 16, 4, 512, true>(map, a, synth, field, grid, ns, smem, st);
-    case 3: return launch_cfg<3, 16, 4, 512, true>(map, a, synth, field, grid, ns, smem, st);
+    case 0: return launch_cfg<4, 16, 4, 256, true>(map, a, synth, field, grid, ns, smem, st);
+    case 1: return launch_cfg<4, 8, 4, 256, true>(map, a, synth, field, grid, ns, smem, st);
+    case 2: return launch_cfg<2, 16, 4, 256, true>(map, a, synth, field, grid, ns, smem, st);
+    case 3: return launch_cfg<3, 16, 4, 256, true>(map, a, synth, field, grid, ns, smem, st);
     case 4: return launch_cfg<2, 8, 4, 256, true>(map, a, synth, field, grid, ns, smem, st);
     case 5: return launch_cfg<2, 4, 4, 256, true>(map, a, synth, field, grid, ns, smem, st);
     default: return launch_cfg<1, 32, 4, 256, false>(map, a, synth, field, grid, ns, smem, st);
