@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 fine kinetic propagator / parareal slice loop.
+
+Default workload (BASELINE.json configs[4], the config its metric — cell
+updates/s, % HBM roofline and 1/2/4/8-GPU parareal wall time — is quoted on):
+Sod tube 2048 x 64^3 fp64, eps = 1e-2, 64 windows.  One bench step is the
+first parareal iteration (the quantity of the paper's Table 2): the fine
+stage over all 64 windows (32 fine steps each, sharded over the ranks with the
+reference's work_distribution), the jump all-gather and the sequential
+correction.  Total work is fixed, so scaling is "strong".
+``--config 1`` runs BASELINE configs[1] (256 x 32^3 smooth wave, fine
+propagator only, 820 steps per bench step; replicas per rank, "weak").
+
+Contract: W untimed warm-up steps, then K steps timed with CUDA events on the
+launching stream, barrier + synchronize on both sides, max over ranks; rank 0
+prints one JSON line.  ``--impl reference`` times the reference algorithm
+(the bit-identical numpy oracle, oracle/) on the host's cores instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=4, choices=[0, 1, 2, 3, 4])
+    ap.add_argument("--eps", type=float, default=None)
+    ap.add_argument("--bc", default=None, choices=["absorbing", "outflow", "periodic"],
+                    help="override the workload's x boundary")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+def dist_setup(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def build_problem(w):
+    import paper_2502_02704_b200 as P
+    phase = P.PhaseGrid(P.build_spatial_grid(w.x_min, w.x_max, w.nx),
+                        P.build_velocity_grid(w.v_max, w.nv))
+    bc = P.BoundaryKind(w.bc)
+    disc = P.Discretization(phase, P.build_time_grids(w.t_final, w.n_g, max(w.n_f, w.n_g)), bc)
+    E = w.force()
+    kinetic = P.KineticParams(epsilon=w.eps, force=E)
+    fluid = P.FluidParams(force=E)
+    return P, phase, bc, disc, kinetic, fluid
+
+
+def run_ours(args, w, world, rank, local):
+    import torch
+    import torch.distributed as dist
+    import paper_2502_02704_b200 as P
+    from paper_2502_02704_b200 import runtime as rt, _lib
+    from paper_2502_02704_b200.parareal import GpuBackend, ShardedRun
+
+    dev = torch.device("cuda", local)
+    P_, phase, bc, disc, kinetic, fluid = build_problem(w)
+    lib = _lib.load()
+    U_raw = P.MomentField(*w.raw_moments())
+    f_init = P.lift(U_raw, phase, bc=bc)
+    U0 = P.project(f_init, phase, bc=bc)  # ref/runner.py:31
+    stream = torch.cuda.current_stream(dev)
+
+    if w.mode == "parareal":
+        backend = GpuBackend(disc, kinetic, fluid, dev)
+        run = ShardedRun(backend)
+        ctx = backend.ctx
+        snaps0 = run.coarse_sweep(rt.to_device_moments(U0, dev))
+        jumps = backend.empty(w.n_g)
+        steps_per_window = w.window_steps()
+        cell_updates = w.cells * steps_per_window * w.n_g  # iteration 1: all windows
+
+        def step():
+            snaps = snaps0.clone()
+            jumps.zero_()
+            run.jumps(snaps, jumps, 1)
+            run.correct(snaps, jumps, 1)
+    else:
+        ctx = rt.ctx_for(phase, bc, dev)
+        f0 = f_init.device_tensor(dev)
+        nsteps = w.window_steps()
+        cell_updates = w.cells * nsteps
+        from paper_2502_02704_b200.kinetic import _run_schedule, fine_schedule, stable_dt_kinetic
+        dts = fine_schedule(w.t_final, stable_dt_kinetic(phase, kinetic))
+        out = ctx.empty_f()
+
+        def step():
+            code = _run_schedule(ctx, f0, None, dts, kinetic, out)
+            rt.raise_kinetic(code)
+
+    # L2 flush buffer (config 1's buffers are comparable to the 126 MB L2)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    lib.pbgk_profile_enable(ctx.h, 1)
+    launches0 = lib.pbgk_launch_count()
+    total_ms = 0.0
+    for _ in range(args.steps):
+        flush.zero_()
+        barrier()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step()
+        b.record(stream)
+        barrier()
+        total_ms += a.elapsed_time(b)
+    launches = lib.pbgk_launch_count() - launches0
+    prof = _lib.Profile()
+    lib.pbgk_profile_read(ctx.h, prof)
+    lib.pbgk_profile_enable(ctx.h, 0)
+    clk = clocks.stop()
+
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    if w.mode == "parareal":
+        job_updates = cell_updates  # windows are sharded: the job does them once
+    else:
+        job_updates = cell_updates * world  # replicas
+    value = job_updates * args.steps / (total_ms * 1e-3)
+
+    pk, pk_kind = peaks()
+    hbm = float(pk.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
+    achieved = prof.sweep_bytes / (prof.sweep_ms * 1e-3) / 1e9 if prof.sweep_ms > 0 else None
+    traffic = None
+    tfile = ROOT / "profiles" / "sweep_traffic.json"
+    if tfile.exists():
+        traffic = json.loads(tfile.read_text()).get(w.name)
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
+                "peak_kind": pk_kind, "kernel": "sweep_kernel",
+                "algorithmic_bytes_per_cell_update": 16,
+                "sweep_share_of_step": (prof.sweep_ms / total_ms) if total_ms > 0 else None,
+                "finalize_share_of_step": (prof.finalize_ms / total_ms) if total_ms > 0 else None,
+                "sweeps_timed": prof.sweeps}
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_ours(args, w, P, phase, bc, disc, kinetic, fluid, U0, f_init, world, dev,
+                       cell_updates, job_updates)
+    return {"value": value, "ms_per_step": ms_per_step, "roofline": roofline, "clocks": clk,
+            "gpu_launches": int(launches), "e2e": e2e}
+
+
+def e2e_ours(args, w, P, phase, bc, disc, kinetic, fluid, U0, f_init, world, dev, cell_updates,
+             job_updates):
+    """Same metric through the public API with host buffers (copies timed)."""
+    import torch
+    import torch.distributed as dist
+    reps = max(1, min(args.steps, 3))
+    if w.mode == "parareal":
+        U0h = P.MomentField(U0.rho.copy(), U0.u.copy(), U0.theta.copy())
+        cfg = P.PararealConfig(k_max=1, tol=1e-300)
+        nx = w.nx
+        h2d = 5 * nx * 8 + (nx * 8 if w.force() is not None else 0)
+        d2h = (3 * w.n_g + 2) * 5 * nx * 8
+        times = []
+        for _ in range(reps + 1):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize(dev)
+            tic = time.perf_counter()
+            traj, rec = P.run_parareal(U0h, cfg, disc, kinetic, fluid)
+            torch.cuda.synchronize(dev)
+            times.append(time.perf_counter() - tic)
+        sec = float(np.mean(times[1:]))
+    else:
+        host = f_init.values.copy()
+        pinned = torch.from_numpy(host).pin_memory()
+        h2d = d2h = host.nbytes
+        times = []
+        for _ in range(reps + 1):
+            torch.cuda.synchronize(dev)
+            tic = time.perf_counter()
+            f = P.Distribution(pinned)
+            g = P.propagate_kinetic(f, 0.0, w.t_final, phase, kinetic, bc)
+            out = g.values
+            times.append(time.perf_counter() - tic)
+        sec = float(np.mean(times[1:]))
+    t = torch.tensor([sec], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    sec = float(t.item())
+    return {"value": job_updates / sec, "unit": "cell-updates/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "seconds_per_step": sec,
+            "api": "run_parareal(k_max=1)" if w.mode == "parareal" else "propagate_kinetic"}
+
+
+def cpu_baseline(w, steps=6, cells=4.0e6):
+    from oracle.cpu_bench import slab_rate
+    plane = int(np.prod(w.nv))
+    nx_slab = max(4, int(cells // plane))
+    r = slab_rate(w.nx, w.nv, w.v_max, w.eps, nx_slab, steps)
+    return {"value": r["value"], "unit": "cell-updates/s", "cores": r["cores"], "kind": "port",
+            "sample": r["sample"], "seconds": r["per_core_s"]}
+
+
+def main():
+    args = parse()
+    from paper_2502_02704_b200.configs import config
+    w = config(args.config, args.eps)
+    metric = "phase-space cell-updates/s (fp64)"
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    cfg_json = {"workload": w.name + (" parareal iteration 1" if w.mode == "parareal" else
+                                      " fine propagate T=%g" % w.t_final),
+                "nx": w.nx, "nv": list(w.nv), "eps": w.eps, "windows": w.n_g,
+                "fine_steps_per_window": w.window_steps(),
+                "parallelism": ("windows sharded over %d rank(s)" % world) if w.mode == "parareal"
+                else ("replicas x%d" % world),
+                "l2": ("inputs larger than L2 (f = %.2f GB); " % (w.cells * 8 / 1e9)) +
+                      "256 MiB L2 flush write between timed steps"}
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        samples = []
+        for _ in range(args.warmup):
+            pass  # the CPU port has no warm-up effects beyond process start
+        for _ in range(args.steps):
+            samples.append(cpu_baseline(w, steps=3, cells=2.0e6))
+        v = float(np.mean([s["value"] for s in samples]))
+        line = {"metric": metric, "value": v, "unit": "cell-updates/s", "impl": "reference",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": float(np.mean([s["seconds"] for s in samples])) * 1e3,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": cfg_json,
+                "cpu_baseline": {"value": v, "unit": "cell-updates/s", "cores": samples[0]["cores"],
+                                 "kind": "port", "sample": samples[0]["sample"]},
+                "e2e": {"value": v, "unit": "cell-updates/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    world, rank, local = dist_setup(args)
+    res = run_ours(args, w, world, rank, local)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(w)
+    if rank == 0:
+        line = {"metric": metric, "value": res["value"], "unit": "cell-updates/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
+                "higher_is_better": True,
+                "scaling": "strong" if w.mode == "parareal" else "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic (seeded BASELINE.json configs; no dataset)",
+                "config": cfg_json, "roofline": res["roofline"], "cpu_baseline": cpu,
+                "e2e": res["e2e"], "gpu_launches": res["gpu_launches"], "clocks": res["clocks"]}
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -48,7 +48,9 @@ typedef struct pbgk_ctx pbgk_ctx;
 typedef struct pbgk_grid_desc {
   int32_t nx, nvx, nvy, nvz;
   double x_min, x_max, v_max;
-  int32_t periodic; /* 1: BoundaryKind.PERIODIC, 0: BoundaryKind.ABSORBING */
+  int32_t bc;       /* x boundary: 0 ABSORBING (zero inflow ghost, ref/kinetic.py:106-108),
+                       1 PERIODIC, 2 OUTFLOW (zero-gradient ghost; extension asked by
+                       BASELINE.json, not in the reference) */
   int32_t device;   /* CUDA device ordinal the context (and every call on it) uses */
 } pbgk_grid_desc;
 
@@ -117,6 +119,24 @@ int pbgk_fluid_propagate(pbgk_ctx* ctx, int nwin, const double* mom_in, double* 
 int pbgk_parareal_correct(pbgk_ctx* ctx, int n_g, int start, double* snaps, const double* old,
                           const double* jumps, const double* h_times, double dt_max, double cfl,
                           const double* force, void* stream, double* h_err, long long* h_code);
+
+/* ---- measurement (bench.py) ------------------------------------------- */
+/* Total kernel launches issued by this library in the process. */
+long long pbgk_launch_count(void);
+
+typedef struct pbgk_profile {
+  double sweep_ms;        /* summed device time of profiled sweep launches     */
+  double sweep_bytes;     /* their algorithmic HBM bytes (f read + f written)  */
+  long long sweeps;       /* number of profiled sweep launches                 */
+  double finalize_ms;     /* summed device time of finalize launches           */
+  long long finalizes;
+} pbgk_profile;
+
+/* When enabled, every sweep / finalize launch on this context is bracketed
+ * by CUDA events recorded on its own stream. */
+int pbgk_profile_enable(pbgk_ctx* ctx, int on);
+/* Synchronises the recorded events, returns the sums and resets them. */
+int pbgk_profile_read(pbgk_ctx* ctx, pbgk_profile* out);
 
 #ifdef __cplusplus
 }

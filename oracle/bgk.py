@@ -174,17 +174,33 @@ def fine_cap(mesh: Mesh, cfl: float, force=None) -> float:
     return cfl / rate
 
 
-def transport(f: np.ndarray, dt: float, mesh: Mesh, periodic: bool,
-              force=None) -> np.ndarray:
-    """Explicit upwind-x + Rusanov-v_x step (ref/kinetic.py:86-124)."""
+def bc_kind(bc) -> str:
+    """'periodic' | 'absorbing' | 'outflow' from a bool (True = periodic) or a name."""
+    if isinstance(bc, str):
+        return bc
+    return "periodic" if bc else "absorbing"
+
+
+def transport(f: np.ndarray, dt: float, mesh: Mesh, periodic, force=None) -> np.ndarray:
+    """Explicit upwind-x + Rusanov-v_x step (ref/kinetic.py:86-124).
+
+    ``periodic``: True / False (the reference's PERIODIC / ABSORBING) or one of
+    'periodic', 'absorbing', 'outflow'.  'outflow' is an ORACLE EXTENSION
+    (BASELINE.json configs 0/4 ask for zero-gradient boundaries; the reference
+    has only the zero-inflow ghost): ghost planes copy the edge planes, i.e.
+    ref/kinetic.py:106-108 with ``ghosted[0] = vals[0]``, ``ghosted[-1] = vals[-1]``.
+    """
+    kind = bc_kind(periodic)
     nx = f.shape[0]
     c = mesh.vc[0]
     cpos = np.maximum(c, 0.0)[None, :, None, None]
     cneg = np.minimum(c, 0.0)[None, :, None, None]
     g = np.empty((nx + 2,) + f.shape[1:])
     g[1:-1] = f
-    if periodic:
+    if kind == "periodic":
         g[0], g[-1] = f[-1], f[0]
+    elif kind == "outflow":
+        g[0], g[-1] = f[0], f[-1]
     else:
         g[0], g[-1] = 0.0, 0.0
     fl = cpos * g[:-1] + cneg * g[1:]
@@ -330,9 +346,9 @@ def coarse_propagate(rho, u, theta, t0, t1, mesh: Mesh, periodic: bool,
         d = min(d, span - done)
         g = np.empty((v.shape[0] + 2, 5))
         g[1:-1] = v
-        if periodic:
+        if bc_kind(periodic) == "periodic":
             g[0], g[-1] = v[-1], v[0]
-        else:  # transmissive copy (ref/fluid.py:84-87)
+        else:  # transmissive copy (ref/fluid.py:84-87); also for 'outflow'
             g[0], g[-1] = v[0], v[-1]
         H = rusanov(g[:-1], g[1:])
         nv = v - (d / mesh.dx) * (H[1:] - H[:-1])

@@ -18,7 +18,7 @@ class GridDesc(ctypes.Structure):
 
     _fields_ = [("nx", c_int32), ("nvx", c_int32), ("nvy", c_int32), ("nvz", c_int32),
                 ("x_min", c_double), ("x_max", c_double), ("v_max", c_double),
-                ("periodic", c_int32), ("device", c_int32)]
+                ("bc", c_int32), ("device", c_int32)]
 
 
 _P = c_void_p
@@ -45,6 +45,21 @@ PROTOTYPES = {
     "pbgk_parareal_correct": (c_int, [_P, _I, _I, _P, _P, _P, POINTER(c_double), _D, _D, _P,
                                       _P, POINTER(c_double), _CODE]),
 }
+
+
+
+class Profile(ctypes.Structure):
+    """struct pbgk_profile (include/pbgk.h)."""
+
+    _fields_ = [("sweep_ms", c_double), ("sweep_bytes", c_double), ("sweeps", c_longlong),
+                ("finalize_ms", c_double), ("finalizes", c_longlong)]
+
+
+PROTOTYPES.update({
+    "pbgk_launch_count": (c_longlong, []),
+    "pbgk_profile_enable": (c_int, [_P, _I]),
+    "pbgk_profile_read": (c_int, [_P, POINTER(Profile)]),
+})
 
 _lib = None
 

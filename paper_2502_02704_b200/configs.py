@@ -1,0 +1,126 @@
+"""The BASELINE.json workloads as problem definitions (synthetic, seeded).
+
+``BASELINE.json`` configs restated on the reference's semantics (SURVEY.md
+8(d), Appendix B): x in [0, 1], midpoint velocity quadrature, tau = 1,
+cfl_kinetic = 0.5, cfl_fluid = 0.9, alpha = 0.  The Sod tubes (configs 0, 2,
+4) use the zero-gradient ``outflow`` kinetic boundary BASELINE.json asks for
+(an extension: the reference only has the zero-inflow ``absorbing`` ghost, with
+which configs 2 and 4 raise CorrectionOvershootError in iteration 1 -- the
+depleted edge cell accumulates negative jumps; measured).
+Initial moments are ``U0 = project(lift(U_raw))`` as in ref/runner.py:27-32.
+Pure numpy problem data (no solver calls) so the CPU oracle and the GPU path
+build the identical inputs.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field, replace
+from typing import Optional
+
+import numpy as np
+
+__all__ = ["Workload", "config", "reduced"]
+
+
+@dataclass
+class Workload:
+    name: str
+    nx: int
+    nv: tuple
+    v_max: float
+    eps: float
+    periodic: bool  # False: see `bc`
+    t_final: float
+    n_g: int
+    n_f: int
+    k_max: int
+    tol: float
+    mode: str  # "parareal" or "fine"
+    x_min: float = 0.0
+    x_max: float = 1.0
+    force_kind: Optional[str] = None  # "sin" -> E = 0.5 sin(2 pi x)
+    init: str = "sod"  # sod | sod_noise | wave | cos
+    seed: int = 2502
+    outflow: bool = False  # zero-gradient kinetic ghosts (extension) instead of absorbing
+
+    @property
+    def bc(self) -> str:
+        return "periodic" if self.periodic else ("outflow" if self.outflow else "absorbing")
+
+    @property
+    def cells(self) -> int:
+        return self.nx * int(np.prod(self.nv))
+
+    def xc(self) -> np.ndarray:
+        dx = (self.x_max - self.x_min) / self.nx
+        return self.x_min + (np.arange(self.nx) + 0.5) * dx
+
+    def force(self):
+        if self.force_kind is None:
+            return None
+        return 0.5 * np.sin(2 * np.pi * self.xc())
+
+    def raw_moments(self):
+        """(rho, u, theta) before the project(lift(.)) round trip."""
+        x = self.xc()
+        u = np.zeros((self.nx, 3))
+        if self.init in ("sod", "sod_noise"):
+            left = x < 0.5
+            rho = np.where(left, 1.0, 0.125)
+            theta = np.where(left, 1.0, 0.8)
+            if self.init == "sod_noise":
+                r = np.random.default_rng(self.seed).random(self.nx)
+                rho = rho * (1.0 + 0.01 * (2.0 * r - 1.0))
+        elif self.init == "wave":
+            rho = 1.0 + 0.5 * np.sin(2 * np.pi * x)
+            u[:, 0] = 0.2 * np.sin(2 * np.pi * x)
+            theta = np.ones(self.nx)
+        elif self.init == "cos":
+            rho = 1.0 + 0.3 * np.cos(2 * np.pi * x)
+            theta = np.ones(self.nx)
+        else:
+            raise ValueError(self.init)
+        return rho.astype(float), u, theta.astype(float)
+
+    def window_steps(self) -> int:
+        """Fine steps per coarse window (CFL cap vs dt_f, ref/kinetic.py:146-156)."""
+        dx = (self.x_max - self.x_min) / self.nx
+        rate = self.v_max / dx
+        f = self.force()
+        if f is not None and np.max(np.abs(f)) > 0:
+            rate += np.max(np.abs(f)) / (2.0 * self.v_max / self.nv[0])
+        cap = 0.5 / rate
+        span = self.t_final / self.n_g if self.mode == "parareal" else self.t_final
+        if self.mode == "parareal":
+            cap = min(cap, self.t_final / self.n_f)
+        n, done = 0, 0.0
+        while span - done > 1e-12 * span:
+            done += min(cap, span - done)
+            n += 1
+        return n
+
+
+def config(idx: int, eps: Optional[float] = None) -> Workload:
+    """BASELINE.json configs[idx] (config 3 is the pinned alpha=0 variant 3a)."""
+    if idx == 0:
+        return Workload("cfg0-sod-64x16^3", 64, (16,) * 3, 8.0, 1e-2, False, 0.1, 8, 8, 2, 1e-300,
+                        "parareal", outflow=True)
+    if idx == 1:
+        return Workload("cfg1-wave-256x32^3", 256, (32,) * 3, 8.0, 1e-3, True, 0.2, 1, 1, 1, 1e-300,
+                        "fine", init="wave")
+    if idx == 2:
+        return Workload("cfg2-noisy-sod-512x48^3", 512, (48,) * 3, 10.0, 1.0 if eps is None else eps,
+                        False, 0.1, 32, 32, 5, 1e-8, "parareal", init="sod_noise", outflow=True)
+    if idx == 3:
+        return Workload("cfg3a-efield-1024x32^3", 1024, (32,) * 3, 8.0, 1e-2, True, 0.05, 32, 32, 5,
+                        1e-8, "parareal", force_kind="sin", init="cos")
+    if idx == 4:
+        return Workload("cfg4-sod-2048x64^3", 2048, (64,) * 3, 8.0, 1e-2, False, 0.0625, 64, 64, 3,
+                        1e-300, "parareal", outflow=True)
+    raise ValueError("configs are 0..4")
+
+
+def reduced(w: Workload, nx: int, nv, n_g: Optional[int] = None, **kw) -> Workload:
+    """A scaled-down copy (same physics and time grid per window) for CPU parity."""
+    return replace(w, name=w.name + "-reduced", nx=nx, nv=tuple(nv) if not np.isscalar(nv) else (nv,) * 3,
+                   n_g=n_g or w.n_g, n_f=(n_g or w.n_g) * w.n_f // w.n_g, **kw)

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -103,8 +104,16 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 }  // namespace
 
+struct EvPair {
+  cudaEvent_t a, b;
+  int kind;  // 0 sweep, 1 finalize
+  double bytes;
+};
+
 struct pbgk_ctx {
   pbgk_grid_desc g;
+  bool prof = false;
+  std::vector<EvPair> ev_pool, ev_used;
   double dx, dv[3], dvol;
   int dev, nsm;
   size_t smem_optin, smem_per_sm;
@@ -125,6 +134,34 @@ struct pbgk_ctx {
 };
 
 namespace {
+
+std::atomic<long long> g_launches{0};
+
+// CUDA-event bracket around one launch when profiling is on.
+struct ProfScope {
+  pbgk_ctx* c;
+  cudaStream_t st;
+  EvPair* ev = nullptr;
+  ProfScope(pbgk_ctx* c_, cudaStream_t st_, int kind, double bytes) : c(c_), st(st_) {
+    ++g_launches;
+    if (!c->prof) return;
+    if (c->ev_pool.empty()) {
+      EvPair p;
+      cudaEventCreate(&p.a);
+      cudaEventCreate(&p.b);
+      c->ev_pool.push_back(p);
+    }
+    c->ev_used.push_back(c->ev_pool.back());
+    c->ev_pool.pop_back();
+    ev = &c->ev_used.back();
+    ev->kind = kind;
+    ev->bytes = bytes;
+    cudaEventRecord(ev->a, st);
+  }
+  ~ProfScope() {
+    if (ev) cudaEventRecord(ev->b, st);
+  }
+};
 
 // Tile choice for one configuration of the sweep.
 bool make_plan(pbgk_ctx* c, bool field, Plan& out) {
@@ -264,7 +301,7 @@ SweepArgs base_args(pbgk_ctx* c, const Plan& p) {
   a.gyo = c->gyo;
   a.gzo = c->gzo;
   a.cx = c->d_c[0];
-  a.periodic = c->g.periodic;
+  a.bc = c->g.bc;
   a.part = c->d_part;
   a.err = c->d_err;
   return a;
@@ -311,6 +348,8 @@ int run_sweep(pbgk_ctx* c, int pid, bool field, const double* in, const double* 
   const CUtensorMap* map = tensor_map(c, synth ? nullptr : in, p.t, p.cfg);
   if (!map) return fail("tensor map: " + g_last_error);
   const size_t smem = sweep_smem_bytes(a, s.V, s.LZ, s.NTHR, synth, s.tma, p.ns);
+  const double fbytes = 8.0 * (double)a.plane * a.nx;
+  ProfScope ps(c, st, 0, (synth ? 0.0 : fbytes) + (out ? fbytes : 0.0));
   CK(launch_sweep(p.cfg, *map, a, synth, field, p.grid, p.ns, smem, st));
   return 0;
 }
@@ -329,11 +368,13 @@ int run_final(pbgk_ctx* c, int pid, int mode, const double* mom_in, double* mom_
   f.tau = tau;
   f.tau_arr = tau_cells;
   f.step = step;
+  ProfScope ps(c, st, 1, 0.0);
   CK(launch_finalize(f, st));
   return 0;
 }
 
 int reset_err(pbgk_ctx* c, cudaStream_t st) {
+  ++g_launches;
   CK(launch_set_key(c->d_err, kNoError, st));
   return 0;
 }
@@ -408,6 +449,11 @@ int pbgk_ctx_create(const pbgk_grid_desc* g, pbgk_ctx** out) {
 void pbgk_ctx_destroy(pbgk_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->dev);
+  for (auto* v : {&c->ev_pool, &c->ev_used})
+    for (auto& e : *v) {
+      cudaEventDestroy(e.a);
+      cudaEventDestroy(e.b);
+    }
   for (int a = 0; a < 3; ++a) cudaFree(c->d_c[a]);
   cudaFree(c->d_part);
   cudaFree(c->d_tab[0]);
@@ -421,6 +467,36 @@ void pbgk_ctx_destroy(pbgk_ctx* c) {
 }
 
 size_t pbgk_ctx_workspace_bytes(const pbgk_ctx* c) { return c ? c->ws_bytes : 0; }
+
+long long pbgk_launch_count(void) { return g_launches.load(); }
+
+int pbgk_profile_enable(pbgk_ctx* c, int on) {
+  if (!c) return fail("null context");
+  c->prof = on != 0;
+  return 0;
+}
+
+int pbgk_profile_read(pbgk_ctx* c, pbgk_profile* out) {
+  if (!c || !out) return fail("null argument");
+  if (cudaSetDevice(c->dev) != cudaSuccess) return fail("cudaSetDevice");
+  std::memset(out, 0, sizeof *out);
+  for (auto& e : c->ev_used) {
+    CK(cudaEventSynchronize(e.b));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e.a, e.b));
+    if (e.kind == 0) {
+      out->sweep_ms += ms;
+      out->sweep_bytes += e.bytes;
+      out->sweeps += 1;
+    } else {
+      out->finalize_ms += ms;
+      out->finalizes += 1;
+    }
+    c->ev_pool.push_back(e);
+  }
+  c->ev_used.clear();
+  return 0;
+}
 
 int pbgk_lift(pbgk_ctx* c, const double* mom, int normalize, double* f_out, void* stream,
               long long* h_code) {
@@ -557,7 +633,8 @@ int pbgk_fluid_propagate(pbgk_ctx* c, int nwin, const double* mom_in, double* mo
   }
   if (upload_times(c, t.data(), t.size(), st)) return -1;
   if (reset_err(c, st)) return -1;
-  FluidArgs a{c->g.nx, c->dx, c->g.periodic, dt_max, cfl, force, c->d_err};
+  FluidArgs a{c->g.nx, c->dx, c->g.bc == 1 ? 1 : 0, dt_max, cfl, force, c->d_err};
+  ++g_launches;
   CK(launch_fluid_batch(a, nwin, mom_in, mom_out, minuend, c->d_times, c->d_times + nwin, st));
   return fetch_err(c, st, h_code);
 }
@@ -571,9 +648,10 @@ int pbgk_parareal_correct(pbgk_ctx* c, int n_g, int start, double* snaps, const 
   cudaStream_t st = (cudaStream_t)stream;
   if (upload_times(c, h_times, (size_t)n_g + 1, st)) return -1;
   if (reset_err(c, st)) return -1;
-  FluidArgs a{c->g.nx, c->dx, c->g.periodic, dt_max, cfl, force, c->d_err};
+  FluidArgs a{c->g.nx, c->dx, c->g.bc == 1 ? 1 : 0, dt_max, cfl, force, c->d_err};
   double* d_e = c->d_scratch;
   CK(cudaMemsetAsync(d_e, 0, sizeof(double), st));
+  if (start <= n_g) ++g_launches;
   if (start <= n_g) CK(launch_correct(a, n_g, start, snaps, old, jumps, c->d_times, d_e, st));
   CK(cudaMemcpyAsync(c->h_dbl, d_e, sizeof(double), cudaMemcpyDeviceToHost, st));
   long long code = -1;

@@ -53,7 +53,7 @@ struct SweepArgs {
   int TL, gxo, gyo, gzo;
   const double* cx;  // x-velocity centres
   double dtdx;       // 0: no transport (pure relax/copy pass)
-  int periodic;
+  int bc;            // 0 absorbing, 1 periodic, 2 outflow (zero gradient)
   const double* E;   // per-cell field or nullptr
   double half_emax;  // 0.5*max|E|
   double dtdv;       // dt / dv_x

@@ -124,12 +124,13 @@ struct ItemIter {
   }
 };
 
-// x cell loaded for an item; -1 = absorbing ghost (f_pre == 0)
-__device__ __forceinline__ int item_plane(int nx, int periodic, const TileGeom& tg, int p, bool halo) {
+// x cell loaded for an item; -1 = absorbing ghost (f_pre == 0).  Ghost
+// planes: periodic wrap, zero-gradient copy (outflow) or zero (absorbing).
+__device__ __forceinline__ int item_plane(int nx, int bc, const TileGeom& tg, int p, bool halo) {
   int i = tg.down ? nx - 1 - p : p;
   if (halo) {
     i += tg.down ? 1 : -1;
-    if (i < 0 || i >= nx) i = periodic ? (i + nx) % nx : -1;
+    if (i < 0 || i >= nx) i = (bc == 1) ? (i + nx) % nx : (bc == 2 ? (i < 0 ? 0 : nx - 1) : -1);
   }
   return i;
 }
@@ -197,7 +198,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? 2 : 1))
     bool h;
     prod.next(nx, t, p, h);
     const TileGeom tg = tile_geom(T, a.nvx, t);
-    const int i = item_plane(nx, a.periodic, tg, p, h);
+    const int i = item_plane(nx, a.bc, tg, p, h);
     const int s = (int)(issued % ns);
     uint64_t* bar = &bars[s];
     unsigned char* st = smem + (size_t)s * stage_bytes;
@@ -253,7 +254,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? 2 : 1))
       }
       zok = tg.z0 + lz * V < a.nvz;  // V divides the z extent when TMA is used
     }
-    const int i = item_plane(nx, a.periodic, tg, p, halo);
+    const int i = item_plane(nx, a.bc, tg, p, halo);
     const int s = (int)(j % ns);
     const double* SF = reinterpret_cast<const double*>(smem + (size_t)s * stage_bytes);
     const double* ST = reinterpret_cast<const double*>(smem + (size_t)s * stage_bytes + box_bytes);

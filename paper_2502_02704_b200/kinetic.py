@@ -202,7 +202,7 @@ def propagate_window(ctx, mom0: torch.Tensor, t0: float, t1: float, grid, params
     if tau_constant(params.tau) is None:
         from .lifting import lift
         from .moments import MomentField, project_device
-        f = lift(MomentField.from_packed(mom0), grid, bc="periodic" if ctx.periodic else "absorbing")
+        f = lift(MomentField.from_packed(mom0), grid, bc=("absorbing", "periodic", "outflow")[ctx.bc])
         f = _step_by_step(ctx, f.device_tensor(ctx.device), dts, params)
         mom_out.copy_(project_device(f, ctx))
         return -1

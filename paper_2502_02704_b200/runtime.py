@@ -21,7 +21,7 @@ import torch
 
 from . import _lib
 from .errors import BlowUpError, CorrectionOvershootError, DegenerateStateError
-from .grid import is_periodic
+from .grid import bc_code
 
 KIND_PROJECT, KIND_LIFT, KIND_NONFINITE, KIND_UNPHYSICAL, KIND_OVERSHOOT = range(5)
 
@@ -51,16 +51,17 @@ def ptr(t: torch.Tensor | None) -> ctypes.c_void_p:
 class Ctx:
     """A libpbgk context bound to one grid, one x boundary and one device."""
 
-    def __init__(self, shape, x_min, x_max, v_max, periodic: bool, device: torch.device):
+    def __init__(self, shape, x_min, x_max, v_max, bc: int, device: torch.device):
         self.lib = _lib.load()
         self.shape = tuple(int(n) for n in shape)
         self.device = device
-        self.periodic = bool(periodic)
+        self.bc = int(bc)
+        self.periodic = self.bc == 1
         nx, nvx, nvy, nvz = self.shape
         self.dx = (x_max - x_min) / nx
         self.dv = tuple(2.0 * v_max / n for n in (nvx, nvy, nvz))
         desc = _lib.GridDesc(nx, nvx, nvy, nvz, float(x_min), float(x_max), float(v_max),
-                             1 if periodic else 0, device.index)
+                             self.bc, device.index)
         h = ctypes.c_void_p()
         _lib.check(self.lib.pbgk_ctx_create(ctypes.byref(desc), ctypes.byref(h)),
                    "pbgk_ctx_create")
@@ -98,11 +99,11 @@ def ctx_for(grid, bc, device: torch.device | None = None) -> Ctx:
     sp, vel = grid.space, grid.velocity
     nv = tuple(int(n) for n in vel.n_v)
     key = (float(sp.x_min), float(sp.x_max), int(sp.n_x), float(vel.v_max), nv,
-           is_periodic(bc), device.index)
+           bc_code(bc), device.index)
     with _lock:
         c = _ctx_cache.get(key)
         if c is None:
-            c = Ctx((sp.n_x,) + nv, sp.x_min, sp.x_max, vel.v_max, is_periodic(bc), device)
+            c = Ctx((sp.n_x,) + nv, sp.x_min, sp.x_max, vel.v_max, bc_code(bc), device)
             _ctx_cache[key] = c
         return c
 
