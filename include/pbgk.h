@@ -121,6 +121,9 @@ int pbgk_parareal_correct(pbgk_ctx* ctx, int n_g, int start, double* snaps, cons
                           const double* force, void* stream, double* h_err, long long* h_code);
 
 /* ---- measurement (bench.py) ------------------------------------------- */
+/* Human-readable tiling / launch plan of a context (diagnostics). */
+int pbgk_ctx_describe(const pbgk_ctx* ctx, char* buf, size_t n);
+
 /* Total kernel launches issued by this library in the process. */
 long long pbgk_launch_count(void);
 

@@ -39,8 +39,16 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile the CUDA sources to lib/libpbgk.so (skipped when up to date)."""
+def build(force: bool = False, verbose: bool = False, csrc: Path | None = None,
+          out: Path | None = None) -> Path:
+    """Compile the CUDA sources to lib/libpbgk.so (skipped when up to date).
+
+    ``csrc`` / ``out`` let development builds compile another source tree
+    (e.g. the previous revision, for A/B timing) to another file."""
+    global CSRC, LIB
+    if csrc is not None:
+        CSRC, LIB = Path(csrc), Path(out)
+        force = True
     if not force and not _stale():
         return LIB
     LIBDIR.mkdir(exist_ok=True)
@@ -48,12 +56,12 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     objs = []
 
     def one(src):
-        obj = LIBDIR / (Path(src).stem + ".o")
+        obj = LIB.parent / (LIB.stem + "_" + Path(src).stem + ".o")
         cmd = [cc, *ARCH, *FLAGS, "-Xptxas", "-v", "-c", str(CSRC / src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("nvcc failed for %s:\n%s" % (src, r.stderr))
-        (LIBDIR / (Path(src).stem + ".ptxas.txt")).write_text(r.stderr)
+        (LIB.parent / (LIB.stem + "_" + Path(src).stem + ".ptxas.txt")).write_text(r.stderr)
         return obj
 
     with cf.ThreadPoolExecutor(len(SOURCES)) as ex:
@@ -70,4 +78,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
 
 if __name__ == "__main__":
-    build(force=True, verbose=True)
+    import sys
+    if len(sys.argv) == 3:  # python _build.py <csrc dir> <out .so>
+        build(csrc=Path(sys.argv[1]), out=Path(sys.argv[2]), verbose=True)
+    else:
+        build(force=True, verbose=True)

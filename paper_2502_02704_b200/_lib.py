@@ -10,7 +10,9 @@ import ctypes
 from ctypes import POINTER, c_double, c_int, c_int32, c_longlong, c_size_t, c_void_p, c_char_p
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libpbgk.so"
+import os
+
+LIB_PATH = Path(os.environ.get("PBGK_LIB") or Path(__file__).resolve().parent / "lib" / "libpbgk.so")
 
 
 class GridDesc(ctypes.Structure):
@@ -57,6 +59,7 @@ class Profile(ctypes.Structure):
 
 PROTOTYPES.update({
     "pbgk_launch_count": (c_longlong, []),
+    "pbgk_ctx_describe": (c_int, [_P, ctypes.c_char_p, c_size_t]),
     "pbgk_profile_enable": (c_int, [_P, _I]),
     "pbgk_profile_read": (c_int, [_P, POINTER(Profile)]),
 })

@@ -168,13 +168,13 @@ bool make_plan(pbgk_ctx* c, bool field, Plan& out) {
   const int nvx = c->g.nvx, nvy = c->g.nvy, nvz = c->g.nvz;
   const int nneg = nvx / 2;  // centres (j - (n-1)/2) dv are < 0 exactly for j < n/2
   const int npos = nvx - nneg;
+  // tile shapes in measured order of preference (cfg ids of sweep.cu)
   std::vector<int> cands;
   const bool even = (nvz % 2 == 0);
-  if (even && nvz % 64 == 0) cands.push_back(0);
   if (even && nvz % 48 == 0) cands.push_back(3);
-  if (even && nvz % 32 == 0) cands.push_back(2);
-  if (even && nvz % 16 == 0) cands.push_back(4);
-  if (even && nvz % 8 == 0) cands.push_back(5);
+  else if (even && nvz % 32 == 0) cands.push_back(2);
+  else if (even && nvz % 16 == 0) cands.push_back(4);
+  else if (even && nvz % 8 == 0) cands.push_back(5);
   cands.push_back(6);
   if (const char* force = getenv("PBGK_FORCE_CFG")) {  // development knob
     cands.assign(1, atoi(force));
@@ -221,7 +221,7 @@ bool make_plan(pbgk_ctx* c, bool field, Plan& out) {
       const double penalty = (s.tma ? 1.0 : 4.0);
       const double util = (double)(A * By) / lines;  // busy fraction of the thread lines
       const double score = penalty * ((loaded + part) / useful) * (1.0 + halo) * (1.5 - 0.5 * util) +
-                           (id == 6 ? 1.0 : 0.0);
+                           (id == 6 ? 100.0 : 0.0);
       if (score < best) {
         best = score;
         out.cfg = id;
@@ -272,9 +272,19 @@ const CUtensorMap* tensor_map(pbgk_ctx* c, const double* ptr, const Tiling& t, i
                                  (cuuint64_t)c->g.nvx * c->g.nvy * c->g.nvz * 8};
   const cuuint32_t box[4] = {(cuuint32_t)t.Bz, (cuuint32_t)t.By, (cuuint32_t)t.rows_load, 1};
   const cuuint32_t es[4] = {1, 1, 1, 1};
+  // 128B: box rows can be as short as 128 bytes; 256B promotion would fetch the
+  // neighbouring row of another tile (measured +50% DRAM reads)
+  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+  if (const char* p = getenv("PBGK_L2PROMO")) {  // development knob
+    const int v = atoi(p);
+    promo = v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                   : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                             : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                        : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }
   CUresult r = enc(&e.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(ptr), dims,
                    strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     char buf[128];
     snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -469,6 +479,23 @@ void pbgk_ctx_destroy(pbgk_ctx* c) {
 size_t pbgk_ctx_workspace_bytes(const pbgk_ctx* c) { return c ? c->ws_bytes : 0; }
 
 long long pbgk_launch_count(void) { return g_launches.load(); }
+
+int pbgk_ctx_describe(const pbgk_ctx* c, char* buf, size_t n) {
+  if (!c || !buf || n == 0) return fail("null argument");
+  const char* names[2] = {"plain", "field"};
+  int off = 0;
+  for (int f = 0; f < 2; ++f) {
+    const Plan& p = c->plan[f];
+    const CfgShape& s = kCfg[p.cfg];
+    off += snprintf(buf + off, n - off > 0 ? n - off : 0,
+                    "%s: cfg=%d V=%d LZ=%d K=%d T=%d tma=%d box=%dx%dx%d rows_load=%d NT=%d PS=%d "
+                    "grid=%d ns=%d; ",
+                    names[f], p.cfg, s.V, s.LZ, s.K, s.NTHR, (int)s.tma, p.t.A, p.t.By, p.t.Bz,
+                    p.t.rows_load, p.t.NT, p.t.PS, p.grid, p.ns);
+    if (off >= (int)n) break;
+  }
+  return 0;
+}
 
 int pbgk_profile_enable(pbgk_ctx* c, int on) {
   if (!c) return fail("null context");

@@ -71,4 +71,10 @@ __device__ __forceinline__ void st_global_v2(double* p, double a, double b) {
   asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
 }
 
+// 256-bit store: one full 32-byte sector per lane (sm_100 STG.E.ENL2.256).
+__device__ __forceinline__ void st_global_v4(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
+               : "memory");
+}
+
 }  // namespace pbgk

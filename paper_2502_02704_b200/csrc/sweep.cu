@@ -30,6 +30,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -135,6 +137,29 @@ __device__ __forceinline__ int item_plane(int nx, int bc, const TileGeom& tg, in
   return i;
 }
 
+// Lane z layout: V consecutive v_z per lane (16/32-byte vectors) for even V;
+// interleaved (element v of lane lz at v*LZ + lz) for odd V, so that every
+// store instruction of a warp covers whole 32-byte sectors.
+template <int V, int LZ>
+__device__ __forceinline__ constexpr int zpos(int lz, int v) {
+  return (V % 2 == 0 || V == 1) ? lz * V + v : v * LZ + lz;
+}
+
+template <int V, int LZ>
+__device__ __forceinline__ void lds_lane(const double* p, double (&x)[V]) {
+  if constexpr (V % 2 == 0) {
+#pragma unroll
+    for (int v = 0; v < V; v += 2) {
+      const double2 t = *reinterpret_cast<const double2*>(p + v);
+      x[v] = t.x;
+      x[v + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int v = 0; v < V; ++v) x[v] = p[v * LZ];
+  }
+}
+
 template <int V>
 __device__ __forceinline__ void lds_vec(const double* p, double (&x)[V]) {
   if constexpr (V % 2 == 0) {
@@ -192,17 +217,17 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? 2 : 1))
   // producer state (thread 0 only): loads run ns items ahead
   ItemIter prod;
   prod.init(g0, g1, nx);
-  int issued = 0;
+  int pstg = 0;  // ring stage of the next issue
   auto issue_next = [&]() {
     int t, p;
     bool h;
     prod.next(nx, t, p, h);
     const TileGeom tg = tile_geom(T, a.nvx, t);
     const int i = item_plane(nx, a.bc, tg, p, h);
-    const int s = (int)(issued % ns);
+    const int s = pstg;
+    if (++pstg == ns) pstg = 0;
     uint64_t* bar = &bars[s];
     unsigned char* st = smem + (size_t)s * stage_bytes;
-    ++issued;
     if (i < 0) {
       mbar_arrive_expect_tx(bar, 0);
       return;
@@ -216,28 +241,38 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? 2 : 1))
     for (int s = 0; s < ns && !prod.done(); ++s) issue_next();
   }
 
-  // per-thread line constants: smem offset of (line, first v_z of this lane)
-  // in the box, and the line's (row, column) inside the box packed as a<<16|b
+  // per-thread line geometry inside the box (fixed for the kernel): smem
+  // offset of the lane's first element of line k, and the line's (row,
+  // column) inside the box packed as a<<16|b
   int soff[K], lab[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     int l = lg + k * NL;
     if (l >= lines) l = 0;
     const int aa = l >> lgBy, b = l & (T.By - 1);
-    soff[k] = ((aa + hoff) * T.By + b) * BZ + lz * V;
+    soff[k] = ((aa + hoff) * T.By + b) * BZ + zpos<V, LZ>(lz, 0);
     lab[k] = (aa << 16) | b;
   }
+  // per-tile line constants (recomputed when the tile changes)
+  int gxi[K], gyi[K], goff[K];
+  double cvx[K];
   unsigned vmask = 0;  // bit k: line k is inside the tile and the grid
-  bool zok = false;
+  unsigned zmask = 0;  // bit v: element v of this lane is inside the grid
+  bool full = false;   // every line and element of this thread is valid
   int cur_tile = -1;
   TileGeom tg{};
 
   double prev[K][V];
-  bool zero_prev = true;
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int v = 0; v < V; ++v) prev[k][v] = 0.0;
 
   ItemIter it;
   it.init(g0, g1, nx);
-  int j = 0;
+  int j = 0;        // item counter (LT/PZ parity)
+  int stg = 0;      // ring stage of item j
+  uint32_t ph = 0;  // mbarrier phase of that stage
   while (!it.done()) {
     int t, p;
     bool halo;
@@ -249,17 +284,26 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? 2 : 1))
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const int l = lg + k * NL;
-        const int jx = tg.r0 + (lab[k] >> 16), jy = tg.y0 + (lab[k] & 0xffff);
+        int jx = tg.r0 + (lab[k] >> 16), jy = tg.y0 + (lab[k] & 0xffff);
         if (l < lines && jx < tg.r1 && jy < a.nvy) vmask |= 1u << k;
+        jx = min(jx, a.nvx - 1);
+        jy = min(jy, a.nvy - 1);
+        gxi[k] = a.gxo + jx;
+        gyi[k] = a.gyo + jy;
+        goff[k] = (jx * a.nvy + jy) * a.nvz + tg.z0 + zpos<V, LZ>(lz, 0);
+        cvx[k] = SCX[jx];
       }
-      zok = tg.z0 + lz * V < a.nvz;  // V divides the z extent when TMA is used
+      zmask = 0;
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+        if (tg.z0 + zpos<V, LZ>(lz, v) < a.nvz) zmask |= 1u << v;
+      full = (vmask == (1u << K) - 1) && (zmask == (1u << V) - 1);
     }
     const int i = item_plane(nx, a.bc, tg, p, halo);
-    const int s = (int)(j % ns);
-    const double* SF = reinterpret_cast<const double*>(smem + (size_t)s * stage_bytes);
-    const double* ST = reinterpret_cast<const double*>(smem + (size_t)s * stage_bytes + box_bytes);
+    const double* SF = reinterpret_cast<const double*>(smem + (size_t)stg * stage_bytes);
+    const double* ST = reinterpret_cast<const double*>(smem + (size_t)stg * stage_bytes + box_bytes);
     if (TMA) {
-      mbar_wait(&bars[s], (uint32_t)((j / ns) & 1));
+      mbar_wait(&bars[stg], ph);
     } else if (i >= 0) {
       // generic path: cooperative synchronous load of the box and the table row
       double* sf = reinterpret_cast<double*>(smem);
@@ -282,17 +326,19 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? 2 : 1))
       for (int k = 0; k < K; ++k)
 #pragma unroll
         for (int v = 0; v < V; ++v) prev[k][v] = 0.0;
-      zero_prev = false;
     } else {
       const double r = ST[0], ls = ST[1];
       double gz[V];
-      lds_vec<V>(ST + a.gzo + (zok ? tg.z0 + lz * V : 0), gz);
-      if (!zok) {
+      if (zmask == (1u << V) - 1) {
+        lds_lane<V, LZ>(ST + a.gzo + tg.z0 + zpos<V, LZ>(lz, 0), gz);
+      } else {
 #pragma unroll
-        for (int v = 0; v < V; ++v) gz[v] = 0.0;
+        for (int v = 0; v < V; ++v)
+          gz[v] = ((zmask >> v) & 1u) ? ST[a.gzo + tg.z0 + zpos<V, LZ>(lz, v)] : 0.0;
       }
       const bool out_plane = !halo;
       const bool transport = a.dtdx != 0.0;
+      const double dtdx = a.dtdx;
       double hE = 0.0;
       if (FIELD && out_plane) hE = __dmul_rn(0.5, __ldg(a.E + i));
       double* gdst = (a.fout != nullptr && out_plane) ? a.fout + (size_t)i * a.plane : nullptr;
@@ -300,101 +346,115 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? 2 : 1))
       double pz[V];
 #pragma unroll
       for (int v = 0; v < V; ++v) pz[v] = 0.0;
-      if (zero_prev) {
+
+      // One plane: relax R_{s-1} of the loaded f*_{s-1}, transport, store,
+      // marginal partials.  FAST: full tile, transport on, output plane
+      // written (every step but the first/last of a window) -- no masks and no
+      // per-line tests; otherwise the general masked path.  DOWNT: c_x < 0
+      // (the upwind neighbour is plane i+1, already in `prev`).
+      auto body = [&](auto fast_c, auto down_c) {
+        constexpr bool FAST = decltype(fast_c)::value;
+        constexpr bool DOWNT = decltype(down_c)::value;
 #pragma unroll
-        for (int k = 0; k < K; ++k)
+        for (int k = 0; k < K; ++k) {
+          const bool ok = FAST || ((vmask >> k) & 1u);
+          const double gxy = ST[gxi[k]] * ST[gyi[k]];
+          double x[V];
+          if (SYNTH) {
 #pragma unroll
-          for (int v = 0; v < V; ++v) prev[k][v] = 0.0;
-        zero_prev = false;
-      }
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const bool ok = ((vmask >> k) & 1u) && zok;
-        const int jx = min(tg.r0 + (lab[k] >> 16), a.nvx - 1);
-        const int jy = min(tg.y0 + (lab[k] & 0xffff), a.nvy - 1);
-        const double gxy = ST[a.gxo + jx] * ST[a.gyo + jy];
-        double x[V];
-        if (SYNTH) {
-#pragma unroll
-          for (int v = 0; v < V; ++v) x[v] = (gxy * gz[v]) * ls;
-        } else {
-          double raw[V];
-          lds_vec<V>(SF + soff[k], raw);
-#pragma unroll
-          for (int v = 0; v < V; ++v) x[v] = fma(ls, gxy * gz[v], raw[v]) * r;
-        }
-        if (out_plane) {
-          double o[V];
-          if (transport) {
-            const double c = SCX[jx];
-#pragma unroll
-            for (int v = 0; v < V; ++v) {
-              const double y = prev[k][v];
-              const double fhi = tg.down ? __dmul_rn(c, y) : __dmul_rn(c, x[v]);
-              const double flo = tg.down ? __dmul_rn(c, x[v]) : __dmul_rn(c, y);
-              o[v] = __dsub_rn(x[v], __dmul_rn(a.dtdx, __dsub_rn(fhi, flo)));
-            }
+            for (int v = 0; v < V; ++v) x[v] = (gxy * gz[v]) * ls;
           } else {
+            double raw[V];
+            lds_lane<V, LZ>(SF + soff[k], raw);
 #pragma unroll
-            for (int v = 0; v < V; ++v) o[v] = x[v];
+            for (int v = 0; v < V; ++v) x[v] = fma(ls, gxy * gz[v], raw[v]) * r;
           }
-          if (FIELD && transport) {
-            // ref/kinetic.py:114-123: Rusanov flux on interior v_x faces of f_pre
-            const bool has_lo = jx > 0, has_hi = jx + 1 < a.nvx;
-            double fm[V], fp[V];
-            const double gym = ST[a.gyo + jy];
-            const double gxm = has_lo ? ST[a.gxo + jx - 1] * gym : 0.0;
-            const double gxp = has_hi ? ST[a.gxo + jx + 1] * gym : 0.0;
-            if (SYNTH) {
+          if (FAST || out_plane) {
+            double o[V];
+            const double c = cvx[k];
+            if (FAST || transport) {
 #pragma unroll
               for (int v = 0; v < V; ++v) {
-                fm[v] = (gxm * gz[v]) * ls;
-                fp[v] = (gxp * gz[v]) * ls;
+                // ref/kinetic.py:110-112: F = max(c,0) g_m + min(c,0) g_{m+1}
+                const double y = prev[k][v];
+                const double fhi = DOWNT ? __dmul_rn(c, y) : __dmul_rn(c, x[v]);
+                const double flo = DOWNT ? __dmul_rn(c, x[v]) : __dmul_rn(c, y);
+                o[v] = __dsub_rn(x[v], __dmul_rn(dtdx, __dsub_rn(fhi, flo)));
               }
             } else {
-              double rm[V], rp[V];
-              lds_vec<V>(SF + soff[k] - T.By * BZ, rm);
-              lds_vec<V>(SF + soff[k] + T.By * BZ, rp);
+#pragma unroll
+              for (int v = 0; v < V; ++v) o[v] = x[v];
+            }
+            if (FIELD && (FAST || transport)) {
+              // ref/kinetic.py:114-123: Rusanov flux on interior v_x faces of f_pre
+              const int jx = gxi[k] - a.gxo;
+              const bool has_lo = jx > 0, has_hi = jx + 1 < a.nvx;
+              double fm[V], fp[V];
+              const double gym = ST[gyi[k]];
+              const double gxm = has_lo ? ST[gxi[k] - 1] * gym : 0.0;
+              const double gxp = has_hi ? ST[gxi[k] + 1] * gym : 0.0;
+              if (SYNTH) {
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                  fm[v] = (gxm * gz[v]) * ls;
+                  fp[v] = (gxp * gz[v]) * ls;
+                }
+              } else {
+                double rm[V], rp[V];
+                lds_lane<V, LZ>(SF + soff[k] - T.By * BZ, rm);
+                lds_lane<V, LZ>(SF + soff[k] + T.By * BZ, rp);
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                  fm[v] = fma(ls, gxm * gz[v], rm[v]) * r;
+                  fp[v] = fma(ls, gxp * gz[v], rp[v]) * r;
+                }
+              }
 #pragma unroll
               for (int v = 0; v < V; ++v) {
-                fm[v] = fma(ls, gxm * gz[v], rm[v]) * r;
-                fp[v] = fma(ls, gxp * gz[v], rp[v]) * r;
+                const double ghi =
+                    has_hi ? __dsub_rn(__dmul_rn(hE, __dadd_rn(x[v], fp[v])),
+                                       __dmul_rn(a.half_emax, __dsub_rn(fp[v], x[v])))
+                           : 0.0;
+                const double glo =
+                    has_lo ? __dsub_rn(__dmul_rn(hE, __dadd_rn(fm[v], x[v])),
+                                       __dmul_rn(a.half_emax, __dsub_rn(x[v], fm[v])))
+                           : 0.0;
+                o[v] = __dsub_rn(o[v], __dmul_rn(a.dtdv, __dsub_rn(ghi, glo)));
               }
             }
+            double sl = 0.0;
 #pragma unroll
             for (int v = 0; v < V; ++v) {
-              const double ghi = has_hi ? __dsub_rn(__dmul_rn(hE, __dadd_rn(x[v], fp[v])),
-                                                    __dmul_rn(a.half_emax, __dsub_rn(fp[v], x[v])))
-                                        : 0.0;
-              const double glo = has_lo ? __dsub_rn(__dmul_rn(hE, __dadd_rn(fm[v], x[v])),
-                                                    __dmul_rn(a.half_emax, __dsub_rn(x[v], fm[v])))
-                                        : 0.0;
-              o[v] = __dsub_rn(o[v], __dmul_rn(a.dtdv, __dsub_rn(ghi, glo)));
+              const double m = FAST ? o[v] : ((ok && ((zmask >> v) & 1u)) ? o[v] : 0.0);
+              pz[v] += m;
+              sl += m;
+            }
+            lp[k] = sl;
+            if (FAST || (gdst != nullptr && ok)) {
+              double* d = gdst + goff[k];
+              if (V == 4 && (FAST || zmask == 0xfu)) {
+                st_global_v4(d, o[0], o[1 % V], o[2 % V], o[3 % V]);
+              } else if (V == 2 && (FAST || zmask == 0x3u)) {
+                st_global_v2(d, o[0], o[1 % V]);
+              } else {
+#pragma unroll
+                for (int v = 0; v < V; ++v)
+                  if (FAST || ((zmask >> v) & 1u)) d[zpos<V, LZ>(0, v)] = o[v];
+              }
             }
           }
-          double sl = 0.0;
 #pragma unroll
-          for (int v = 0; v < V; ++v) {
-            const double m = ok ? o[v] : 0.0;
-            pz[v] += m;
-            sl += m;
-          }
-          lp[k] = sl;
-          if (gdst != nullptr && ok) {
-            double* d = gdst + ((jx * a.nvy + jy) * a.nvz + tg.z0 + lz * V);
-            if constexpr (V % 2 == 0) {
-#pragma unroll
-              for (int v = 0; v < V; v += 2) st_global_v2(d + v, o[v], o[v + 1]);
-            } else {
-#pragma unroll
-              for (int v = 0; v < V; ++v)
-                if (tg.z0 + lz * V + v < a.nvz) d[v] = o[v];
-            }
-          }
+          for (int v = 0; v < V; ++v) prev[k][v] = x[v];
         }
-#pragma unroll
-        for (int v = 0; v < V; ++v) prev[k][v] = x[v];
+      };
+      using T1 = std::integral_constant<bool, true>;
+      using F1 = std::integral_constant<bool, false>;
+      if (full && out_plane && transport && gdst != nullptr) {
+        if (tg.down) body(T1{}, T1{}); else body(T1{}, F1{});
+      } else {
+        if (tg.down) body(F1{}, T1{}); else body(F1{}, F1{});
       }
+
       if (out_plane) {
         // line totals -> LT, z partials -> PZ (double-buffered by item parity)
         double* LTb = LT + (j & 1) * lines;
@@ -417,7 +477,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? 2 : 1))
         }
         if (lane < LZ) {
 #pragma unroll
-          for (int v = 0; v < V; ++v) PZb[warp * BZ + lane * V + v] = pz[v];
+          for (int v = 0; v < V; ++v) PZb[warp * BZ + zpos<V, LZ>(lane, v)] = pz[v];
         }
       }
     }
@@ -456,6 +516,10 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? 2 : 1))
     }
     if (!TMA) __syncthreads();  // the single stage is refilled next item
     ++j;
+    if (++stg == ns) {
+      stg = 0;
+      ph ^= 1u;
+    }
   }
 }
 

@@ -69,6 +69,11 @@ class Ctx:
         # f-sized scratch buffers reused across calls (allocated lazily)
         self._f_tmp = [None, None]
 
+    def describe(self) -> str:
+        buf = ctypes.create_string_buffer(1024)
+        _lib.check(self.lib.pbgk_ctx_describe(self.h, buf, 1024), "pbgk_ctx_describe")
+        return buf.value.decode()
+
     def __del__(self):
         try:
             if getattr(self, "h", None):

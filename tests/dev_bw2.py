@@ -1,0 +1,10 @@
+import torch
+a = torch.empty(2**29, dtype=torch.float64, device="cuda")
+b = torch.empty_like(a)
+a.fill_(1.0)
+for _ in range(4):
+    torch.add(a, 1.0, out=b)
+torch.cuda.synchronize()
+s = torch.cuda.Event(enable_timing=True); e = torch.cuda.Event(enable_timing=True)
+s.record(); torch.add(a, 1.0, out=b); e.record(); torch.cuda.synchronize()
+print("add %.1f GB/s" % (2 * a.numel() * 8 / s.elapsed_time(e) / 1e6))

@@ -20,4 +20,4 @@ m0 = rt.to_device_moments(U, ctx.device)
 mo = ctx.empty_moments()
 code = propagate_window(ctx, m0, 0.0, nsteps * stable_dt_kinetic(grid, kp), grid, kp, None, mo)
 torch.cuda.synchronize()
-print("done", code)
+print("done", code, ctx.describe())
