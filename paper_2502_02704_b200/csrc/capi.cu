@@ -64,15 +64,19 @@ int fail(const std::string& msg) {
 struct CfgShape {
   int V, LZ, K, NTHR;
   bool tma;
+  int minb;  // CTAs per SM the launch bounds target
 };
 const CfgShape kCfg[] = {
-    {4, 16, 4, 256, true},  // 0: nvz % 64 == 0
-    {4, 8, 4, 256, true},   // 1: nvz % 32 == 0
-    {2, 16, 4, 256, true},  // 2: nvz % 32 == 0 (alternative)
-    {3, 16, 4, 256, true},  // 3: nvz % 48 == 0
-    {2, 8, 4, 256, true},   // 4: nvz % 16 == 0
-    {2, 4, 4, 256, true},   // 5: nvz % 8 == 0
-    {1, 32, 4, 256, false}, // 6: anything (no TMA)
+    {4, 16, 4, 256, true, 2},   // 0: nvz % 64 == 0
+    {4, 8, 4, 256, true, 2},    // 1: nvz % 32 == 0
+    {2, 16, 4, 256, true, 2},   // 2: nvz % 32 == 0
+    {3, 16, 4, 256, true, 2},   // 3: nvz % 48 == 0
+    {2, 8, 4, 256, true, 2},    // 4: nvz % 16 == 0
+    {2, 4, 4, 256, true, 2},    // 5: nvz % 8 == 0
+    {1, 32, 4, 256, false, 2},  // 6: anything (no TMA)
+    {2, 16, 8, 256, true, 2},   // 7: nvz % 32 == 0, 8 lines/thread
+    {2, 16, 16, 256, true, 1},  // 8: nvz % 32 == 0, 16 lines/thread, 1 CTA/SM
+    {2, 16, 8, 256, true, 1},   // 9: nvz % 32 == 0, 8 lines/thread, 1 CTA/SM
 };
 
 struct Plan {
@@ -238,12 +242,14 @@ bool make_plan(pbgk_ctx* c, bool field, Plan& out) {
   dummy.TL = c->TL;
   // two CTAs per SM when the ring fits in half the shared memory, else one
   const size_t half = (c->smem_per_sm / 2) - 2048;
-  int ns = 4;
+  int ns_max = 8;
+  if (const char* e = getenv("PBGK_NS")) ns_max = atoi(e);  // development knob
+  int ns = ns_max;
   while (ns > 2 && sweep_smem_bytes(dummy, s.V, s.LZ, s.NTHR, false, s.tma, ns) > half) --ns;
   int per_sm = 2;
-  if (sweep_smem_bytes(dummy, s.V, s.LZ, s.NTHR, false, s.tma, ns) > half) {
+  if (s.minb == 1 || sweep_smem_bytes(dummy, s.V, s.LZ, s.NTHR, false, s.tma, ns) > half) {
     per_sm = 1;
-    ns = 4;
+    ns = ns_max;
     while (ns > 2 && sweep_smem_bytes(dummy, s.V, s.LZ, s.NTHR, false, s.tma, ns) > c->smem_optin) --ns;
   }
   out.ns = s.tma ? ns : 1;
@@ -314,6 +320,7 @@ SweepArgs base_args(pbgk_ctx* c, const Plan& p) {
   a.bc = c->g.bc;
   a.part = c->d_part;
   a.err = c->d_err;
+  if (const char* d = getenv("PBGK_DEBUG")) a.debug = atoi(d);  // development ablations
   return a;
 }
 

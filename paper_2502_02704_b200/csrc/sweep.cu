@@ -175,8 +175,8 @@ __device__ __forceinline__ void lds_vec(const double* p, double (&x)[V]) {
   }
 }
 
-template <int V, int LZ, int K, int NTHR, bool SYNTH, bool FIELD, bool TMA>
-__global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? 2 : 1))
+template <int V, int LZ, int K, int NTHR, int MINB, bool SYNTH, bool FIELD, bool TMA>
+__global__ void __launch_bounds__(NTHR, MINB)
     sweep_kernel(const __grid_constant__ CUtensorMap fmap, const SweepArgs a, int ns) {
   constexpr int NL = NTHR / LZ;  // line groups
   constexpr int NW = NTHR / 32;
@@ -262,6 +262,8 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? 2 : 1))
   int cur_tile = -1;
   TileGeom tg{};
 
+  // prev[k][v]: the upwind flux c_x f_pre of the previous plane in march
+  // order (the F of ref/kinetic.py:110-112 on the face shared with this plane)
   double prev[K][V];
 #pragma unroll
   for (int k = 0; k < K; ++k)
@@ -359,27 +361,31 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? 2 : 1))
         for (int k = 0; k < K; ++k) {
           const bool ok = FAST || ((vmask >> k) & 1u);
           const double gxy = ST[gxi[k]] * ST[gyi[k]];
+          const double c = cvx[k];
           double x[V];
           if (SYNTH) {
 #pragma unroll
             for (int v = 0; v < V; ++v) x[v] = (gxy * gz[v]) * ls;
           } else {
+            // (f* + ls M) r with M = gxy gz, as (r f*) + (r ls gxy) gz
+            const double w = r * (ls * gxy);
             double raw[V];
             lds_lane<V, LZ>(SF + soff[k], raw);
 #pragma unroll
-            for (int v = 0; v < V; ++v) x[v] = fma(ls, gxy * gz[v], raw[v]) * r;
+            for (int v = 0; v < V; ++v) x[v] = fma(w, gz[v], r * raw[v]);
           }
+          double fl[V];  // this plane's upwind flux c f_pre
+#pragma unroll
+          for (int v = 0; v < V; ++v) fl[v] = __dmul_rn(c, x[v]);
           if (FAST || out_plane) {
             double o[V];
-            const double c = cvx[k];
             if (FAST || transport) {
 #pragma unroll
               for (int v = 0; v < V; ++v) {
-                // ref/kinetic.py:110-112: F = max(c,0) g_m + min(c,0) g_{m+1}
-                const double y = prev[k][v];
-                const double fhi = DOWNT ? __dmul_rn(c, y) : __dmul_rn(c, x[v]);
-                const double flo = DOWNT ? __dmul_rn(c, x[v]) : __dmul_rn(c, y);
-                o[v] = __dsub_rn(x[v], __dmul_rn(dtdx, __dsub_rn(fhi, flo)));
+                // f* = f - (dt/dx)(F_{i+1/2} - F_{i-1/2}); upward: F_{i+1/2} = c f_i,
+                // F_{i-1/2} = c f_{i-1}; downward: F_{i+1/2} = c f_{i+1}, F_{i-1/2} = c f_i
+                const double d = DOWNT ? __dsub_rn(prev[k][v], fl[v]) : __dsub_rn(fl[v], prev[k][v]);
+                o[v] = __dsub_rn(x[v], __dmul_rn(dtdx, d));
               }
             } else {
 #pragma unroll
@@ -400,13 +406,14 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? 2 : 1))
                   fp[v] = (gxp * gz[v]) * ls;
                 }
               } else {
+                const double wm = r * (ls * gxm), wp = r * (ls * gxp);
                 double rm[V], rp[V];
                 lds_lane<V, LZ>(SF + soff[k] - T.By * BZ, rm);
                 lds_lane<V, LZ>(SF + soff[k] + T.By * BZ, rp);
 #pragma unroll
                 for (int v = 0; v < V; ++v) {
-                  fm[v] = fma(ls, gxm * gz[v], rm[v]) * r;
-                  fp[v] = fma(ls, gxp * gz[v], rp[v]) * r;
+                  fm[v] = fma(wm, gz[v], r * rm[v]);
+                  fp[v] = fma(wp, gz[v], r * rp[v]);
                 }
               }
 #pragma unroll
@@ -444,7 +451,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? 2 : 1))
             }
           }
 #pragma unroll
-          for (int v = 0; v < V; ++v) prev[k][v] = x[v];
+          for (int v = 0; v < V; ++v) prev[k][v] = fl[v];
         }
       };
       using T1 = std::integral_constant<bool, true>;
@@ -455,7 +462,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? 2 : 1))
         if (tg.down) body(F1{}, T1{}); else body(F1{}, F1{});
       }
 
-      if (out_plane) {
+      if (out_plane && !(a.debug & 1)) {
         // line totals -> LT, z partials -> PZ (double-buffered by item parity)
         double* LTb = LT + (j & 1) * lines;
         double* PZb = PZ + (j & 1) * NW * BZ;
@@ -482,12 +489,12 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? 2 : 1))
       }
     }
 
-    __syncthreads();
+    if (!(a.debug & 2)) __syncthreads();
     if (TMA && tid == 0 && !prod.done()) {
       fence_proxy_async();
       issue_next();
     }
-    if (!halo && i >= 0) {
+    if (!halo && i >= 0 && !(a.debug & 1)) {
       const double* LTb = LT + (j & 1) * lines;
       const double* PZb = PZ + (j & 1) * NW * BZ;
       double* dst = a.part + ((size_t)i * T.NT + t) * T.PS;
@@ -527,16 +534,16 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? 2 : 1))
 // host-side dispatch
 // ---------------------------------------------------------------------------
 
-template <int V, int LZ, int K, int NTHR, bool TMA>
+template <int V, int LZ, int K, int NTHR, int MINB, bool TMA>
 static cudaError_t launch_cfg(const CUtensorMap& map, const SweepArgs& a, bool synth, bool field,
                               int grid, int ns, size_t smem, cudaStream_t st) {
   void (*fn)(const CUtensorMap, const SweepArgs, int);
   if (synth)
-    fn = field ? sweep_kernel<V, LZ, K, NTHR, true, true, TMA>
-               : sweep_kernel<V, LZ, K, NTHR, true, false, TMA>;
+    fn = field ? sweep_kernel<V, LZ, K, NTHR, MINB, true, true, TMA>
+               : sweep_kernel<V, LZ, K, NTHR, MINB, true, false, TMA>;
   else
-    fn = field ? sweep_kernel<V, LZ, K, NTHR, false, true, TMA>
-               : sweep_kernel<V, LZ, K, NTHR, false, false, TMA>;
+    fn = field ? sweep_kernel<V, LZ, K, NTHR, MINB, false, true, TMA>
+               : sweep_kernel<V, LZ, K, NTHR, MINB, false, false, TMA>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   fn<<<grid, NTHR, smem, st>>>(map, a, ns);
@@ -557,13 +564,16 @@ size_t sweep_smem_bytes(const SweepArgs& a, int V, int LZ, int NTHR, bool synth,
 cudaError_t launch_sweep(int cfg_id, const CUtensorMap& map, const SweepArgs& a, bool synth,
                          bool field, int grid, int ns, size_t smem, cudaStream_t st) {
   switch (cfg_id) {
-    case 0: return launch_cfg<4, 16, 4, 256, true>(map, a, synth, field, grid, ns, smem, st);
-    case 1: return launch_cfg<4, 8, 4, 256, true>(map, a, synth, field, grid, ns, smem, st);
-    case 2: return launch_cfg<2, 16, 4, 256, true>(map, a, synth, field, grid, ns, smem, st);
-    case 3: return launch_cfg<3, 16, 4, 256, true>(map, a, synth, field, grid, ns, smem, st);
-    case 4: return launch_cfg<2, 8, 4, 256, true>(map, a, synth, field, grid, ns, smem, st);
-    case 5: return launch_cfg<2, 4, 4, 256, true>(map, a, synth, field, grid, ns, smem, st);
-    default: return launch_cfg<1, 32, 4, 256, false>(map, a, synth, field, grid, ns, smem, st);
+    case 0: return launch_cfg<4, 16, 4, 256, 2, true>(map, a, synth, field, grid, ns, smem, st);
+    case 1: return launch_cfg<4, 8, 4, 256, 2, true>(map, a, synth, field, grid, ns, smem, st);
+    case 2: return launch_cfg<2, 16, 4, 256, 2, true>(map, a, synth, field, grid, ns, smem, st);
+    case 3: return launch_cfg<3, 16, 4, 256, 2, true>(map, a, synth, field, grid, ns, smem, st);
+    case 4: return launch_cfg<2, 8, 4, 256, 2, true>(map, a, synth, field, grid, ns, smem, st);
+    case 5: return launch_cfg<2, 4, 4, 256, 2, true>(map, a, synth, field, grid, ns, smem, st);
+    case 7: return launch_cfg<2, 16, 8, 256, 2, true>(map, a, synth, field, grid, ns, smem, st);
+    case 8: return launch_cfg<2, 16, 16, 256, 1, true>(map, a, synth, field, grid, ns, smem, st);
+    case 9: return launch_cfg<2, 16, 8, 256, 1, true>(map, a, synth, field, grid, ns, smem, st);
+    default: return launch_cfg<1, 32, 4, 256, 2, false>(map, a, synth, field, grid, ns, smem, st);
   }
 }
 
