@@ -116,7 +116,7 @@ def _relax_dev(ctx, fd, dt, params, out, tau_cells=None):
         from .moments import project_device, MomentField
         U = MomentField.from_packed(project_device(fd, ctx))
         tau = np.broadcast_to(np.asarray(params.tau(U.rho, U.theta), dtype=float), U.rho.shape)
-        tau_cells = torch.from_numpy(np.ascontiguousarray(tau)).to(ctx.device)
+        tau_cells = torch.from_numpy(np.array(tau, dtype=float)).to(ctx.device)
     code = ctypes.c_longlong(-1)
     rt._lib.check(ctx.lib.pbgk_relax(ctx.h, rt.ptr(fd), rt.ptr(out), float(dt),
                                      float(params.epsilon), 1.0 if tc is None else tc,

@@ -246,9 +246,10 @@ class ShardedRun:
             else:
                 words[w] = c
         payload = torch.cat([out.reshape(-1), words.to(out.device).view(torch.float64)])
-        gathered = torch.empty((self.world, payload.numel()), dtype=torch.float64,
-                               device=payload.device)
-        dist.all_gather_into_tensor(gathered, payload, group=self.group)
+        flat = torch.empty(self.world * payload.numel(), dtype=torch.float64,
+                           device=payload.device)
+        dist.all_gather_into_tensor(flat, payload, group=self.group)
+        gathered = flat.view(self.world, payload.numel())
         nj = max(chunk, 1) * 5 * self.b.nx
         all_status = []
         for q in range(self.world):

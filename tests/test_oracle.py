@@ -1,0 +1,265 @@
+"""Pin the CPU oracle (tests only) to the reference.
+
+1. Against the golden vectors written by tests/golden/make_golden.py from the
+   unmodified reference: <= 1e-14 relative (bitwise on the same numpy build;
+   the tolerance only absorbs a different host CPU's SIMD paths).
+2. Against the live reference where it is importable (this container):
+   bit-for-bit on random inputs.
+3. Against the reference test suite's known answers and scalar oracles,
+   restated here independently.
+"""
+
+import math
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import bgk as O
+from helpers import moment_gap, rel_inf
+
+GOLD = Path(__file__).resolve().parent / "golden"
+
+
+def load(name):
+    return np.load(GOLD / ("%s.npz" % name))
+
+
+def mesh_of(d):
+    return O.Mesh(0.0, 1.0, int(d["nx"]), float(d["vmax"]), tuple(int(n) for n in d["nv"]))
+
+
+# ---------------------------------------------------------------------------
+# 1. golden vectors
+# ---------------------------------------------------------------------------
+
+def test_golden_lift_project():
+    d = load("kinetic")
+    m = mesh_of(d)
+    U = (d["rho"], d["u"], d["theta"])
+    assert rel_inf(O.lift(*U, m), d["lift_raw"]) <= 1e-14
+    assert rel_inf(O.lift(*U, m, normalize=True), d["lift_norm"]) <= 1e-14
+    got = O.project(d["f"], m)
+    assert moment_gap(got, (d["proj_rho"], d["proj_u"], d["proj_theta"])) <= 1e-14
+
+
+def test_golden_transport_relax():
+    d = load("kinetic")
+    m = mesh_of(d)
+    f, dt = d["f"], float(d["dt"])
+    assert rel_inf(O.transport(f, dt, m, True), d["tr_per"]) <= 1e-14
+    assert rel_inf(O.transport(f, dt, m, False), d["tr_abs"]) <= 1e-14
+    assert rel_inf(O.transport(f, dt, m, True, d["E"]), d["tr_fieldper"]) <= 1e-14
+    assert rel_inf(O.relax(f, dt, m, 2e-2), d["relax"]) <= 1e-14
+
+
+def test_golden_propagate():
+    d = load("kinetic")
+    m = mesh_of(d)
+    assert O.fine_cap(m, 0.5) == float(d["cap"])
+    assert O.fine_cap(m, 0.5, d["E"]) == float(d["capE"])
+    got = O.fine_propagate(d["f"], 0.0, float(d["t1"]), m, 2e-2, False)
+    assert rel_inf(got, d["prop_abs"]) <= 1e-13
+    got = O.fine_propagate(d["f"], 0.0, 4.5 * float(d["capE"]), m, 2e-2, True, d["E"])
+    assert rel_inf(got, d["prop_fieldper"]) <= 1e-13
+
+
+def test_golden_fluid():
+    d = load("fluid")
+    m = O.Mesh(0.0, 1.0, int(d["nx"]), 8.0, (4, 4, 4))
+    U = (d["rho"], d["u"], d["theta"])
+    got = O.coarse_propagate(*U, 0.0, 0.04, m, False, None, 0.01)
+    assert moment_gap(got, (d["abs_rho"], d["abs_u"], d["abs_theta"])) <= 1e-14
+    got = O.coarse_propagate(*U, 0.0, 0.04, m, True, d["E"], 0.01)
+    assert moment_gap(got, (d["perE_rho"], d["perE_u"], d["perE_theta"])) <= 1e-14
+
+
+def test_golden_parareal():
+    d = load("parareal")
+    nx = int(d["nx"])
+    m = O.Mesh(0.0, 1.0, nx, 8.0, (8, 8, 8))
+    prob = O.Problem(m, 0.05, 4, 16, 1e-2, False)
+    snaps, errs = O.parareal(prob, (d["rho0"], d["u0"], d["theta0"]), 3, 1e-300)
+    assert len(errs) == len(d["errors"])
+    assert np.allclose(errs, d["errors"], rtol=1e-13, atol=0)
+    for n, s in enumerate(snaps):
+        assert moment_gap(s, (d["snap_rho"][n], d["snap_u"][n], d["snap_theta"][n])) <= 1e-13
+    chain = O.fine_chain(prob, (d["rho0"], d["u0"], d["theta0"]))
+    for n, s in enumerate(chain):
+        assert rel_inf(s[0], d["chain_rho"][n]) <= 1e-13
+
+
+def test_golden_scalars():
+    d = load("scalars")
+    assert [O.work_range(10, 3, r)[:2] for r in range(3)] == [tuple(x) for x in d["wd_10_3"]]
+    m = O.Mesh(0.0, 2.0, 200, 8.0, (8, 8, 8))
+    assert O.fine_cap(m, 0.9) == float(d["stable_dt_200"]) == 0.9 * 0.01 / 8.0
+    vl = O.to_conserved(np.array([1.0]), np.zeros((1, 3)), np.array([1.0]))[0]
+    vr = O.to_conserved(np.array([0.125]), np.zeros((1, 3)), np.array([0.8]))[0]
+    assert np.array_equal(O.rusanov(vl, vr), d["rusanov_sod"])
+
+
+# ---------------------------------------------------------------------------
+# 2. live reference, bit for bit
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_bitwise_vs_reference(ref, seed):
+    rng = np.random.default_rng(seed)
+    for nx, nv, vmax, per, field in [(12, (8, 8, 8), 8.0, True, False),
+                                    (9, (7, 6, 5), 5.0, False, True)]:
+        m = O.Mesh(0.0, 1.0, nx, vmax, nv)
+        g = ref.PhaseGrid(ref.build_spatial_grid(0.0, 1.0, nx), ref.build_velocity_grid(vmax, nv))
+        E = 0.5 * np.sin(2 * np.pi * m.xc) if field else None
+        rho, u, th = (rng.uniform(0.6, 1.4, nx), rng.normal(size=(nx, 3)) * 0.3,
+                      rng.uniform(0.5, 1.5, nx))
+        f = O.lift(rho, u, th, m) * rng.uniform(0.9, 1.1, (nx,) + nv)
+        kp = ref.KineticParams(epsilon=1e-2, force=E)
+        bc = ref.BoundaryKind.PERIODIC if per else ref.BoundaryKind.ABSORBING
+        assert np.array_equal(O.lift(rho, u, th, m),
+                              ref.lift(ref.MomentField(rho, u, th), g).values)
+        U = ref.project(ref.Distribution(f), g)
+        for a, b in zip((U.rho, U.u, U.theta), O.project(f, m)):
+            assert np.array_equal(a, b)
+        assert np.array_equal(ref.transport_update(ref.Distribution(f), 1e-3, g, kp, bc).values,
+                              O.transport(f, 1e-3, m, per, E))
+        assert np.array_equal(ref.bgk_relax(ref.Distribution(f), 1e-3, g, kp).values,
+                              O.relax(f, 1e-3, m, 1e-2))
+        a = ref.propagate_kinetic(ref.Distribution(f), 0.0, 0.011, g, kp, bc, dt_max=0.004).values
+        assert np.array_equal(a, O.fine_propagate(f, 0.0, 0.011, m, 1e-2, per, E, 0.004))
+        V = ref.propagate_fluid(ref.MomentField(rho, u, th), 0.0, 0.05, g,
+                                ref.FluidParams(force=E), bc, dt_max=0.01)
+        for a, b in zip((V.rho, V.u, V.theta),
+                        O.coarse_propagate(rho, u, th, 0.0, 0.05, m, per, E, 0.01)):
+            assert np.array_equal(a, b)
+
+
+def test_parareal_bitwise_vs_reference(ref):
+    m = O.Mesh(0.0, 2.0, 12, 8.0, (8, 8, 8))
+    prob = O.Problem(m, 0.1, 4, 16, 1e-2, False)
+    U0 = O.two_state(m, 1.0, (1, 0, 1), (0.125, 0, 0.8))
+    g = ref.PhaseGrid(ref.build_spatial_grid(0.0, 2.0, 12), ref.build_velocity_grid(8.0, 8))
+    disc = ref.Discretization(g, ref.build_time_grids(0.1, 4, 16), ref.BoundaryKind.ABSORBING)
+    for frozen in (True, False):
+        traj, rec = ref.run_parareal(ref.MomentField(*U0),
+                                     ref.PararealConfig(k_max=3, tol=1e-300,
+                                                        use_frozen_prefix=frozen),
+                                     disc, ref.KineticParams(epsilon=1e-2), ref.FluidParams())
+        snaps, errs = O.parareal(prob, U0, 3, 1e-300, frozen)
+        assert [r.error for r in rec] == errs
+        for s, o in zip(traj.snapshots, snaps):
+            for a, b in zip((s.rho, s.u, s.theta), o):
+                assert np.array_equal(a, b)
+
+
+def test_overshoot_slice_matches_reference(ref):
+    m = O.Mesh(0.0, 2.0, 12, 8.0, (8, 8, 8))
+    prob = O.Problem(m, 0.1, 4, 16, 1e-2, False)
+    U0 = O.two_state(m, 1.0, (1, 0, 1), (0.125, 0, 0.8))
+
+    def bad_jump(p, U, n):
+        d = O.window_jump(p, U, n)
+        if n == 3:
+            return (d[0] - 10.0, d[1], d[2])
+        return d
+
+    with pytest.raises(O.OracleOvershoot) as e:
+        O.parareal(prob, U0, 1, 1e-300, jump_fn=bad_jump)
+    assert e.value.slice_index == 3
+
+
+# ---------------------------------------------------------------------------
+# 3. the reference suite's known answers, restated
+# ---------------------------------------------------------------------------
+
+def _bruteforce_moments(rho, u, theta, vc):
+    """Scalar Maxwellian moments over the full 3-D node set with fsum."""
+    dv = 1.0
+    for c in vc:
+        dv *= c[1] - c[0]
+    w, wx, wy, wz = [], [], [], []
+    for a in vc[0]:
+        for b in vc[1]:
+            for c in vc[2]:
+                q = (a - u[0]) ** 2 + (b - u[1]) ** 2 + (c - u[2]) ** 2
+                val = rho / (2 * math.pi * theta) ** 1.5 * math.exp(-q / (2 * theta))
+                w.append(val)
+                wx.append(val * a)
+                wy.append(val * b)
+                wz.append(val * c)
+    mass = math.fsum(w) * dv
+    ub = (math.fsum(wx) * dv / mass, math.fsum(wy) * dv / mass, math.fsum(wz) * dv / mass)
+    e2 = []
+    for a in vc[0]:
+        for b in vc[1]:
+            for c in vc[2]:
+                q = (a - u[0]) ** 2 + (b - u[1]) ** 2 + (c - u[2]) ** 2
+                val = rho / (2 * math.pi * theta) ** 1.5 * math.exp(-q / (2 * theta))
+                e2.append(val * ((a - ub[0]) ** 2 + (b - ub[1]) ** 2 + (c - ub[2]) ** 2))
+    return mass, ub, math.fsum(e2) * dv / (3 * mass)
+
+
+def test_project_vs_bruteforce():
+    m = O.Mesh(0.0, 2.0, 4, 8.0, (16, 16, 16))
+    rho, u, th = 1.3, (0.4, -0.2, 0.9), 0.7
+    R = O.project(O.lift(np.full(4, rho), np.tile(u, (4, 1)), np.full(4, th), m), m)
+    mass, ub, tb = _bruteforce_moments(rho, u, th, m.vc)
+    assert abs(R[0][0] - mass) <= 1e-13 * mass
+    assert np.max(np.abs(R[1][0] - ub)) <= 1e-13
+    assert abs(R[2][0] - tb) <= 1e-13 * tb
+
+
+def test_even_data_zero_velocity_and_point_mass():
+    m = O.Mesh(0.0, 2.0, 2, 8.0, (16, 16, 16))
+    half = np.random.default_rng(7).uniform(0.1, 1.0, size=(2, 8, 16, 16))
+    R = O.project(np.concatenate([half, half[:, ::-1]], axis=1), m)
+    assert np.all(R[1][:, 0] == 0.0)
+    m8 = O.Mesh(0.0, 2.0, 2, 8.0, (8, 8, 8))
+    f = np.zeros((2, 8, 8, 8))
+    f[:, 5, 2, 7] = 1.0 / m8.dvol
+    rho, u, th = O.project(f, m8)
+    assert np.all(rho == 1.0) and np.all(th == 0.0)
+    assert list(u[0]) == [m8.vc[0][5], m8.vc[1][2], m8.vc[2][7]]
+
+
+def test_relax_half_blend_and_homogeneous_closed_form():
+    m = O.Mesh(0.0, 2.0, 2, 8.0, (16, 16, 16))
+    base = O.lift(np.ones(2), np.zeros((2, 3)), np.ones(2), m)
+    f = base * np.random.default_rng(5).uniform(0.5, 1.5, base.shape)
+    out = O.relax(f, 0.25, m, 0.25)  # lambda = 1
+    M = O.lift(*O.project(f, m), m, normalize=True)
+    assert rel_inf(out, 0.5 * (f + M)) <= 1e-14
+    # homogeneous: m steps -> a f0 + (1-a) M with a = prod 1/(1+lam)
+    m32 = O.Mesh(0.0, 2.0, 2, 8.0, (32, 32, 32))
+    u1 = np.zeros((2, 3)); u1[:, 0] = 0.5
+    u2 = np.zeros((2, 3)); u2[:, 0] = -0.75
+    f0 = O.lift(0.6 * np.ones(2), u1, 0.6 * np.ones(2), m32) + \
+        O.lift(0.4 * np.ones(2), u2, 0.5 * np.ones(2), m32)
+    f = f0
+    for _ in range(12):
+        f = O.relax(O.transport(f, 2e-3, m32, True), 2e-3, m32, 0.1)
+    a = (1.0 / (1.0 + 2e-3 / 0.1)) ** 12
+    M0 = O.lift(*O.project(f0, m32), m32, normalize=True)
+    assert np.max(np.abs(f - (a * f0 + (1 - a) * M0))) <= 1e-13 * f0.max()
+
+
+def test_work_range_partitions_exactly():
+    for work in range(0, 65):
+        for n_p in range(1, 17):
+            owned = []
+            for r in range(n_p):
+                s, e, _, size = O.work_range(work, n_p, r)
+                assert size == max(0, e - s + 1)
+                owned.extend(range(s, e + 1))
+            assert owned == list(range(1, work + 1))
+
+
+def test_blow_up_step_and_degenerate_order():
+    m = O.Mesh(0.0, 2.0, 4, 8.0, (8, 8, 8))
+    f = O.lift(np.ones(4), np.zeros((4, 3)), np.ones(4), m)
+    f[0, 0, 0, 0] = np.nan
+    with pytest.raises(O.OracleBlowUp) as e:
+        O.fine_propagate(f, 0.0, 0.1, m, 1e-2, True)
+    assert e.value.step == 1
+    with pytest.raises(O.OracleDegenerate):
+        O.project(np.zeros((2, 8, 8, 8)), m)
