@@ -1,0 +1,126 @@
+"""Parity on the BASELINE.json workloads, GPU vs oracle.
+
+North-star bound: fp64 relative L-inf <= 1e-10 on f and on the moments
+(u scaled by max(|u|, sqrt(theta))) and identical parareal
+iteration counts.  Full-size CPU runs of configs 1-4 take hours (42 core-h
+for config 4), so those are checked at the real velocity grids on reduced x
+ranges / window counts, plus config 0 and config 1 at full shape.
+"""
+
+from dataclasses import replace
+
+import numpy as np
+import pytest
+
+from oracle import bgk as O
+from helpers import moment_gap, rel_inf
+
+pytestmark = pytest.mark.gpu
+P = pytest.importorskip("paper_2502_02704_b200")
+from paper_2502_02704_b200.configs import config  # noqa: E402
+
+TOL = 1e-10
+
+
+def _pkg(w):
+    g = P.PhaseGrid(P.build_spatial_grid(w.x_min, w.x_max, w.nx), P.build_velocity_grid(w.v_max, w.nv))
+    bc = P.BoundaryKind(w.bc)
+    d = P.Discretization(g, P.build_time_grids(w.t_final, w.n_g, w.n_f), bc)
+    E = w.force()
+    return g, bc, d, P.KineticParams(w.eps, force=E), P.FluidParams(force=E)
+
+
+def _oracle(w):
+    m = O.Mesh(w.x_min, w.x_max, w.nx, w.v_max, w.nv)
+    return m, O.Problem(m, w.t_final, w.n_g, w.n_f, w.eps, w.bc, w.force())
+
+
+def _U0_both(w):
+    """U0 = project(lift(U_raw)) on each side (ref/runner.py:31)."""
+    m, _ = _oracle(w)
+    raw = w.raw_moments()
+    U0o = O.project(O.lift(*raw, m), m)
+    g, bc, *_ = _pkg(w)
+    U0p = P.project(P.lift(P.MomentField(*raw), g, bc=bc), g, bc=bc)
+    assert moment_gap((U0p.rho, U0p.u, U0p.theta), U0o) <= 1e-13
+    return U0o, U0p
+
+
+def _parareal_parity(w):
+    _, prob = _oracle(w)
+    U0o, U0p = _U0_both(w)
+    want_s, want_e = O.parareal(prob, U0o, w.k_max, w.tol)
+    g, bc, d, kin, flu = _pkg(w)
+    traj, rec = P.run_parareal(U0p, P.PararealConfig(w.k_max, w.tol), d, kin, flu)
+    assert len(rec) == len(want_e)  # identical iteration counts
+    for a, b in zip(traj.snapshots, want_s):
+        assert moment_gap((a.rho, a.u, a.theta), b) <= TOL
+    for e1, e2 in zip([r.error for r in rec], want_e):
+        assert abs(e1 - e2) <= TOL * max(abs(e2), 1.0)
+    return rec
+
+
+@pytest.mark.parametrize("bc", ["absorbing", "outflow"])
+def test_config0_full_parareal(bc):
+    w = replace(config(0), outflow=(bc == "outflow"))
+    rec = _parareal_parity(w)
+    assert len(rec) == 2
+
+
+def test_config1_full_shape_fine_propagator_prefix():
+    # 256 x 32^3 periodic wave, eps 1e-3: the first 12 of the 820 steps
+    w = config(1)
+    m, _ = _oracle(w)
+    g, bc, d, kin, flu = _pkg(w)
+    f0 = O.lift(*w.raw_moments(), m)
+    cap = O.fine_cap(m, 0.5)
+    t1 = 11.5 * cap
+    want = O.fine_propagate(f0, 0.0, t1, m, w.eps, True)
+    got = P.propagate_kinetic(P.Distribution(f0), 0.0, t1, g, kin, bc)
+    assert rel_inf(got.values, want) <= TOL
+    Up = P.project(got, g)
+    assert moment_gap((Up.rho, Up.u, Up.theta), O.project(want, m)) <= TOL
+
+
+def test_config1_reduced_full_time():
+    # the whole T = 0.2 horizon (104 steps) at 32 x 16^3, same physics
+    w = replace(config(1), nx=32, nv=(16, 16, 16))
+    m, _ = _oracle(w)
+    g, bc, d, kin, flu = _pkg(w)
+    f0 = O.lift(*w.raw_moments(), m)
+    want = O.fine_propagate(f0, 0.0, w.t_final, m, w.eps, True)
+    got = P.propagate_kinetic(P.Distribution(f0), 0.0, w.t_final, g, kin, bc)
+    assert rel_inf(got.values, want) <= TOL
+
+
+@pytest.mark.parametrize("eps", [1.0, 0.1])
+def test_config2_reduced_parareal(eps):
+    w = replace(config(2, eps), nx=64, nv=(16, 16, 16), n_g=8, n_f=8, k_max=3)
+    _parareal_parity(w)
+
+
+def test_config3a_reduced_parareal_with_field():
+    w = replace(config(3), nx=64, nv=(16, 16, 16), n_g=8, n_f=8, k_max=3)
+    _parareal_parity(w)
+
+
+def test_config4_velocity_grid_one_window_on_an_x_slab():
+    # the 64^3 velocity grid and the window schedule of config 4 (32 steps,
+    # dt = 2^-15) on the first 64 of its 2048 cells (x in [0, 1/32])
+    w = config(4)
+    w = replace(w, nx=64, x_max=64.0 / 2048.0, t_final=w.t_final)
+    m, prob = _oracle(w)
+    g, bc, d, kin, flu = _pkg(w)
+    assert d.phase.space.dx == 1.0 / 2048.0
+    raw = w.raw_moments()
+    t0, t1 = float(prob.times[0]), float(prob.times[1])
+    want = O.PFL(prob, raw, 1)
+    from paper_2502_02704_b200 import runtime as rt
+    from paper_2502_02704_b200.kinetic import propagate_window
+    ctx = rt.ctx_for(g, bc)
+    out = ctx.empty_moments()
+    code = propagate_window(ctx, rt.to_device_moments(P.MomentField(*raw), ctx.device), t0, t1, g,
+                            kin, d.time.dt_f, out)
+    assert code == -1
+    got = P.MomentField.from_packed(out)
+    assert moment_gap((got.rho, got.u, got.theta), want) <= TOL
