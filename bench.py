@@ -235,9 +235,11 @@ def run_ours(args, w, world, rank, local):
     traffic = None
     tfile = ROOT / "profiles" / "sweep_traffic.json"
     if tfile.exists():
-        traffic = json.loads(tfile.read_text()).get(w.name)
+        t = json.loads(tfile.read_text()).get(w.name)
+        traffic = t["bytes_per_launch"] if isinstance(t, dict) else t
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
+                "algorithmic_bytes_per_launch": 16.0 * w.cells,
                 "peak_kind": pk_kind, "kernel": "sweep_kernel",
                 "algorithmic_bytes_per_cell_update": 16,
                 "sweep_share_of_step": (prof.sweep_ms / total_ms) if total_ms > 0 else None,
