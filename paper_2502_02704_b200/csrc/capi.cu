@@ -77,6 +77,8 @@ const CfgShape kCfg[] = {
     {2, 16, 8, 256, true, 2},   // 7: nvz % 32 == 0, 8 lines/thread
     {2, 16, 16, 256, true, 1},  // 8: nvz % 32 == 0, 16 lines/thread, 1 CTA/SM
     {2, 16, 8, 256, true, 1},   // 9: nvz % 32 == 0, 8 lines/thread, 1 CTA/SM
+    {2, 32, 4, 256, true, 2},   // 10: nvz % 64 == 0, full 512-byte v_z rows per box line
+    {2, 32, 8, 256, true, 2},   // 11: nvz % 64 == 0, 8 lines/thread
 };
 
 struct Plan {
@@ -175,7 +177,8 @@ bool make_plan(pbgk_ctx* c, bool field, Plan& out) {
   // tile shapes in measured order of preference (cfg ids of sweep.cu)
   std::vector<int> cands;
   const bool even = (nvz % 2 == 0);
-  if (even && nvz % 48 == 0) cands.push_back(3);
+  if (even && nvz % 64 == 0) cands.push_back(10);
+  else if (even && nvz % 48 == 0) cands.push_back(3);
   else if (even && nvz % 32 == 0) cands.push_back(2);
   else if (even && nvz % 16 == 0) cands.push_back(4);
   else if (even && nvz % 8 == 0) cands.push_back(5);
