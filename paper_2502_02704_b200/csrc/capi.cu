@@ -245,7 +245,9 @@ bool make_plan(pbgk_ctx* c, bool field, Plan& out) {
   dummy.TL = c->TL;
   // two CTAs per SM when the ring fits in half the shared memory, else one
   const size_t half = (c->smem_per_sm / 2) - 2048;
-  int ns_max = 8;
+  // ring depth (measured, round 1): fewer boxes in flight is as fast or faster
+  // (48^3: 2 stages +10% over 4); 32-wide boxes prefer 3
+  int ns_max = (s.V == 2 && s.LZ == 16) ? 3 : 2;
   if (const char* e = getenv("PBGK_NS")) ns_max = atoi(e);  // development knob
   int ns = ns_max;
   while (ns > 2 && sweep_smem_bytes(dummy, s.V, s.LZ, s.NTHR, false, s.tma, ns) > half) --ns;

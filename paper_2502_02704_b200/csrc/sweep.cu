@@ -456,7 +456,17 @@ __global__ void __launch_bounds__(NTHR, MINB)
       };
       using T1 = std::integral_constant<bool, true>;
       using F1 = std::integral_constant<bool, false>;
-      if (full && out_plane && transport && gdst != nullptr) {
+      if (!SYNTH && (a.debug & 4)) {
+        // ablation: copy-through skeleton (TMA in, STG out, no arithmetic)
+        if (gdst != nullptr && out_plane) {
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            double raw[V];
+            lds_lane<V, LZ>(SF + soff[k], raw);
+            if constexpr (V == 2) st_global_v2(gdst + goff[k], raw[0], raw[1]);
+          }
+        }
+      } else if (full && out_plane && transport && gdst != nullptr) {
         if (tg.down) body(T1{}, T1{}); else body(T1{}, F1{});
       } else {
         if (tg.down) body(F1{}, T1{}); else body(F1{}, F1{});
