@@ -107,6 +107,23 @@ def main():
             R.primitive_to_conserved(R.MomentField(np.array([0.125]), np.zeros((1, 3)),
                                                    np.array([0.8]))).to_array()[0]))
 
+    # -- run_mode artifacts of the reference's criterion-11 configuration --------
+    import tempfile
+    with tempfile.TemporaryDirectory() as tmp:
+        cfg = R.RunConfig(case="sod", x_min=0.0, x_max=2.0, n_x=20, v_max=5.0, n_vx=8, n_vy=8,
+                          n_vz=8, epsilon=1e-2, bc="absorbing", t_final=0.1, n_g=8, n_f=32,
+                          k_max=8, tol=1e-8, workers=1)
+        outp = R.run_mode(cfg, tmp + "/par")
+        snaps = [R.read_snapshot(p) for p in sorted(Path(outp).glob("snap_*.csv"))]
+        recs = R.read_convergence(Path(outp) / "convergence.csv")
+        from dataclasses import replace as _rep
+        outf = R.run_mode(_rep(cfg, mode="fine"), tmp + "/fine")
+        fine = [R.read_snapshot(p) for p in sorted(Path(outf).glob("snap_*.csv"))]
+    cases["artifacts"] = dict(
+        par=np.stack([np.stack([s[k] for k in ("x", "rho", "ux", "uy", "uz", "theta")]) for s in snaps]),
+        k=np.array([r.k for r in recs]), err=np.array([r.error for r in recs]),
+        fine=np.stack([np.stack([s[k] for k in ("x", "rho", "ux", "uy", "uz", "theta")]) for s in fine]))
+
     for name, d in cases.items():
         np.savez_compressed(OUT / ("%s.npz" % name), **d)
         print("wrote", name, sum(np.asarray(v).nbytes for v in d.values()), "bytes")
