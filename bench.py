@@ -64,9 +64,17 @@ def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # development switch: every rank on cuda:0 with gloo collectives, to run
+    # the multi-rank path on a one-GPU box (never used for reported numbers)
+    shared = os.environ.get("PBGK_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     if world > 1:
         torch.cuda.set_device(local)
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            torch.distributed.init_process_group("gloo")
+        else:
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
     return world, rank, local

@@ -79,6 +79,8 @@ const CfgShape kCfg[] = {
     {2, 16, 8, 256, true, 1},   // 9: nvz % 32 == 0, 8 lines/thread, 1 CTA/SM
     {2, 32, 4, 256, true, 2},   // 10: nvz % 64 == 0, full 512-byte v_z rows per box line
     {2, 32, 8, 256, true, 2},   // 11: nvz % 64 == 0, 8 lines/thread
+    {2, 32, 4, 512, true, 1},   // 12: nvz % 64 == 0, 512 threads, 1 CTA/SM
+    {2, 16, 4, 512, true, 1},   // 13: nvz % 32 == 0, 512 threads, 1 CTA/SM
 };
 
 struct Plan {
@@ -246,8 +248,8 @@ bool make_plan(pbgk_ctx* c, bool field, Plan& out) {
   // two CTAs per SM when the ring fits in half the shared memory, else one
   const size_t half = (c->smem_per_sm / 2) - 2048;
   // ring depth (measured, round 1): fewer boxes in flight is as fast or faster
-  // (48^3: 2 stages +10% over 4); 32-wide boxes prefer 3
-  int ns_max = (s.V == 2 && s.LZ == 16) ? 3 : 2;
+  // (48^3: 2 stages +10% over 4); 32- and 64-wide boxes prefer 3
+  int ns_max = (s.V == 2 && (s.LZ == 16 || s.LZ == 32)) ? 3 : 2;
   if (const char* e = getenv("PBGK_NS")) ns_max = atoi(e);  // development knob
   int ns = ns_max;
   while (ns > 2 && sweep_smem_bytes(dummy, s.V, s.LZ, s.NTHR, false, s.tma, ns) > half) --ns;

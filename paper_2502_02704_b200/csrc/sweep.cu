@@ -585,6 +585,8 @@ cudaError_t launch_sweep(int cfg_id, const CUtensorMap& map, const SweepArgs& a,
     case 9: return launch_cfg<2, 16, 8, 256, 1, true>(map, a, synth, field, grid, ns, smem, st);
     case 10: return launch_cfg<2, 32, 4, 256, 2, true>(map, a, synth, field, grid, ns, smem, st);
     case 11: return launch_cfg<2, 32, 8, 256, 2, true>(map, a, synth, field, grid, ns, smem, st);
+    case 12: return launch_cfg<2, 32, 4, 512, 1, true>(map, a, synth, field, grid, ns, smem, st);
+    case 13: return launch_cfg<2, 16, 4, 512, 1, true>(map, a, synth, field, grid, ns, smem, st);
     default: return launch_cfg<1, 32, 4, 256, 2, false>(map, a, synth, field, grid, ns, smem, st);
   }
 }
