@@ -215,14 +215,23 @@ __global__ void __launch_bounds__(NTHR, MINB)
   __syncthreads();
 
   // producer state (thread 0 only): loads run ns items ahead
+  // producer: lane 0 of the LAST warp (the first warps carry the per-plane
+  // partial sums), with the tile geometry cached across its run
+  const int ptid = NTHR - 32;
   ItemIter prod;
   prod.init(g0, g1, nx);
   int pstg = 0;  // ring stage of the next issue
+  int ptile = -1;
+  TileGeom ptg{};
   auto issue_next = [&]() {
     int t, p;
     bool h;
     prod.next(nx, t, p, h);
-    const TileGeom tg = tile_geom(T, a.nvx, t);
+    if (t != ptile) {
+      ptile = t;
+      ptg = tile_geom(T, a.nvx, t);
+    }
+    const TileGeom& tg = ptg;
     const int i = item_plane(nx, a.bc, tg, p, h);
     const int s = pstg;
     if (++pstg == ns) pstg = 0;
@@ -236,7 +245,7 @@ __global__ void __launch_bounds__(NTHR, MINB)
     if (!SYNTH) tma_load_4d(st, &fmap, tg.z0, tg.y0, tg.r0 - hoff, i, bar);
     tma_load_1d(st + box_bytes, a.tab + (size_t)i * a.TL, tab_bytes, bar);
   };
-  if (TMA && tid == 0) {
+  if (TMA && tid == ptid) {
     prefetch_tensormap(&fmap);
     for (int s = 0; s < ns && !prod.done(); ++s) issue_next();
   }
@@ -500,29 +509,34 @@ __global__ void __launch_bounds__(NTHR, MINB)
     }
 
     if (!(a.debug & 2)) __syncthreads();
-    if (TMA && tid == 0 && !prod.done()) {
+    if (TMA && tid == ptid && !prod.done()) {
       fence_proxy_async();
       issue_next();
     }
     if (!halo && i >= 0 && !(a.debug & 1)) {
+      // one output per thread, in equal contiguous chunks per warp so no warp
+      // carries the serial sums alone (contiguous lanes keep smem reads
+      // conflict-free)
       const double* LTb = LT + (j & 1) * lines;
       const double* PZb = PZ + (j & 1) * NW * BZ;
       double* dst = a.part + ((size_t)i * T.NT + t) * T.PS;
-      if (tid < T.A) {
-        if (tg.r0 + tid < tg.r1) {
+      const int chunk = (T.A + T.By + BZ + NW - 1) / NW;
+      const int o = lane < chunk ? warp * chunk + lane : 1 << 20;
+      if (o < T.A) {
+        if (tg.r0 + o < tg.r1) {
           double s2 = 0.0;
-          for (int b = 0; b < T.By; ++b) s2 += LTb[tid * T.By + b];
-          dst[tid] = s2;
+          for (int b = 0; b < T.By; ++b) s2 += LTb[o * T.By + b];
+          dst[o] = s2;
         }
-      } else if (tid < T.A + T.By) {
-        const int b = tid - T.A;
+      } else if (o < T.A + T.By) {
+        const int b = o - T.A;
         if (tg.y0 + b < a.nvy) {
           double s2 = 0.0;
           for (int aa = 0; aa < T.A; ++aa) s2 += LTb[aa * T.By + b];
           dst[T.A + b] = s2;
         }
-      } else if (tid < T.A + T.By + BZ) {
-        const int zz = tid - T.A - T.By;
+      } else if (o < T.A + T.By + BZ) {
+        const int zz = o - T.A - T.By;
         if (tg.z0 + zz < a.nvz) {
           double s2 = 0.0;
 #pragma unroll
