@@ -57,7 +57,8 @@ def build(force: bool = False, verbose: bool = False, csrc: Path | None = None,
 
     def one(src):
         obj = LIB.parent / (LIB.stem + "_" + Path(src).stem + ".o")
-        cmd = [cc, *ARCH, *FLAGS, "-Xptxas", "-v", "-c", str(CSRC / src), "-o", str(obj)]
+        defs = os.environ.get("PBGK_NVCC_DEFS", "").split()  # dev A/B variants
+        cmd = [cc, *ARCH, *FLAGS, *defs, "-Xptxas", "-v", "-c", str(CSRC / src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("nvcc failed for %s:\n%s" % (src, r.stderr))

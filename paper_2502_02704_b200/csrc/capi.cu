@@ -211,7 +211,7 @@ bool make_plan(pbgk_ctx* c, bool field, Plan& out) {
       t.nty = (nvy + By - 1) / By;
       t.ntz = (nvz + Bz - 1) / Bz;
       t.NT = (t.ntn + t.ntp) * t.nty * t.ntz;
-      t.PS = A + By + Bz;
+      t.PS = (A + By + Bz + 1) & ~1;  // even: 16-B aligned records (bulk copies)
       // loaded elements per useful element, plus marginal-partial traffic
       const double loaded = (double)t.NT * t.rows_load * By * Bz;
       const double useful = (double)nvx * nvy * nvz;

@@ -18,7 +18,15 @@
 
 namespace pbgk {
 
-__global__ void __launch_bounds__(128) finalize_kernel(const FinalArgs a) {
+#ifndef PBGK_FIN_THREADS
+#define PBGK_FIN_THREADS 128
+#endif
+#ifndef PBGK_FIN_MINB
+#define PBGK_FIN_MINB 16
+#endif
+constexpr int kFinThreads = PBGK_FIN_THREADS;
+
+__global__ void __launch_bounds__(kFinThreads, PBGK_FIN_MINB) finalize_kernel(const FinalArgs a) {
   extern __shared__ double sm[];
   __shared__ double sh[16];
   finalize_cell(a, blockIdx.x, sm, sh);
@@ -27,8 +35,15 @@ __global__ void __launch_bounds__(128) finalize_kernel(const FinalArgs a) {
 __global__ void set_key_kernel(ErrKey* p, ErrKey v) { *p = v; }
 
 cudaError_t launch_finalize(const FinalArgs& a, cudaStream_t st) {
-  const size_t smem = (size_t)2 * (a.nvx + a.nvy + a.nvz) * sizeof(double);
-  finalize_kernel<<<a.nx, 128, smem, st>>>(a);
+  size_t smem = (size_t)2 * (a.nvx + a.nvy + a.nvz) * sizeof(double);
+  if (a.mom_in == nullptr && a.mode != kFinIdentity)
+    smem += (size_t)chunk_scratch(a.t, a.nvx, a.nvy, a.nvz) * sizeof(double);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  finalize_kernel<<<a.nx, kFinThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 

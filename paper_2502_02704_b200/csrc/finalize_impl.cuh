@@ -7,29 +7,84 @@
 
 namespace pbgk {
 
-// Sum of one marginal entry over its tiles, outer-major / inner-minor (the
-// fixed order for every entry); loads are batched 8 ahead so the L2
-// latencies overlap while the additions stay in order.
-static __device__ __forceinline__ double tile_sum(const double* P, int PS, int base, int n_out,
-                                                  int s_out, int n_in, int s_in, int off) {
-  const int n = n_out * n_in;
-  double s = 0.0;
-  int q = 0;
-  for (; q + 8 <= n; q += 8) {
-    double v[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const int o = (q + r) / n_in, in = q + r - o * n_in;
-      v[r] = __ldcg(P + (size_t)(base + o * s_out + in * s_in) * PS + off);
+// Gather of the tile partials.  The tiles contributing to one marginal entry
+// are enumerated outer-major / inner-minor (the same order for every entry and
+// its mirror); that list is cut into chunks of kChunk tiles, each chunk summed
+// in order by one thread (all its loads issued before the first add), and the
+// chunk sums of an entry are then added in chunk order.  Adjacent threads take
+// adjacent entries of the same chunk, so each load instruction is coalesced.
+#ifndef PBGK_FIN_CHUNK
+#define PBGK_FIN_CHUNK 16
+#endif
+constexpr int kChunk = PBGK_FIN_CHUNK;
+
+struct EntryList {
+  int base, n_out, s_out, n_in, s_in, off;
+};
+
+// Tile list of entry j of axis ax (0: c_x, 1: c_y, 2: c_z).
+static __device__ __forceinline__ EntryList entry_list(const Tiling& T, int ax, int j) {
+  const int per = T.nty * T.ntz, ntx = T.ntn + T.ntp;
+  EntryList e;
+  if (ax == 0) {
+    int tx, r0;
+    if (j < T.nneg) {
+      tx = j / T.A;
+      r0 = tx * T.A;
+    } else {
+      tx = T.ntn + (j - T.nneg) / T.A;
+      r0 = T.nneg + (tx - T.ntn) * T.A;
     }
+    e = {tx * per, T.nty, T.ntz, T.ntz, 1, j - r0};
+  } else if (ax == 1) {
+    const int ty = j / T.By;
+    e = {ty * T.ntz, ntx, per, T.ntz, 1, T.A + j - ty * T.By};
+  } else {
+    const int tz = j / T.Bz;
+    e = {tz, ntx, per, T.nty, T.ntz, T.A + T.By + j - tz * T.Bz};
+  }
+  return e;
+}
+
+static __device__ __forceinline__ int list_len(const Tiling& T, int ax) {
+  return ax == 0 ? T.nty * T.ntz : (ax == 1 ? (T.ntn + T.ntp) * T.ntz : (T.ntn + T.ntp) * T.nty);
+}
+
+// Sum of tiles [q0, q1) of list e (q1 - q0 <= kChunk), in list order.
+static __device__ __forceinline__ double chunk_sum(const double* P, int PS, const EntryList& e,
+                                                   int q0, int q1) {
+  // branch-free walk: pointer advanced by s_in records, or by the wrap
+  // stride at the end of an inner run; positions past q1 re-load the first
+  // address and add +0.0 (exact: s starts at +0.0 and can never become -0.0)
+  int o = q0 / e.n_in, in = q0 - o * e.n_in;
+  const double* p0 = P + (size_t)(e.base + o * e.s_out + in * e.s_in) * PS + e.off;
+  const long long d_in = (long long)e.s_in * PS;
+  const long long d_wrap = (long long)(e.s_out - (e.n_in - 1) * e.s_in) * PS;
+  const int cnt = q1 - q0;
+  const double* p = p0;
+  double v[kChunk];
 #pragma unroll
-    for (int r = 0; r < 8; ++r) s += v[r];
+  for (int r = 0; r < kChunk; ++r) {
+    const double* q = r < cnt ? p : p0;
+    v[r] = __ldcg(q);
+    ++in;
+    const bool wrap = in == e.n_in;
+    p += wrap ? d_wrap : d_in;
+    in = wrap ? 0 : in;
   }
-  for (; q < n; ++q) {
-    const int o = q / n_in, in = q - o * n_in;
-    s += __ldcg(P + (size_t)(base + o * s_out + in * s_in) * PS + off);
-  }
+  double s = 0.0;
+#pragma unroll
+  for (int r = 0; r < kChunk; ++r) s += r < cnt ? v[r] : 0.0;
   return s;
+}
+
+// Doubles of chunk-sum scratch finalize_cell needs beyond its 2*(nvx+nvy+nvz).
+static __host__ __device__ __forceinline__ int chunk_scratch(const Tiling& T, int nvx, int nvy,
+                                                             int nvz) {
+  const int ntx = T.ntn + T.ntp;
+  const int lx = T.nty * T.ntz, ly = ntx * T.ntz, lz = ntx * T.nty;
+  return nvx * ((lx + kChunk - 1) / kChunk) + nvy * ((ly + kChunk - 1) / kChunk) +
+         nvz * ((lz + kChunk - 1) / kChunk);
 }
 
 static __device__ __forceinline__ double warp_allsum(double x) {
@@ -51,10 +106,12 @@ static __device__ __forceinline__ void finalize_cell(const FinalArgs& a, int i, 
   double* gx = mz + nvz;
   double* gy = gx + nvx;
   double* gz = gy + nvy;
-  const double* cs[3] = {a.cx, a.cy, a.cz};
-  const int nv[3] = {nvx, nvy, nvz};
-  double* ms[3] = {mx, my, mz};
-  double* gs[3] = {gx, gy, gz};
+  // per-axis selectors (ternaries, not arrays: a runtime index would put
+  // an array on the stack)
+  auto nv = [&](int ax) { return ax == 0 ? nvx : (ax == 1 ? nvy : nvz); };
+  auto cs = [&](int ax) { return ax == 0 ? a.cx : (ax == 1 ? a.cy : a.cz); };
+  auto ms = [&](int ax) { return ax == 0 ? mx : (ax == 1 ? my : mz); };
+  auto gs = [&](int ax) { return ax == 0 ? gx : (ax == 1 ? gy : gz); };
 
   if (a.mode == kFinIdentity) {
     double* row = a.tab + (size_t)i * a.TL;
@@ -72,36 +129,32 @@ static __device__ __forceinline__ void finalize_cell(const FinalArgs& a, int i, 
     th = a.mom_in[4 * a.nx + i];
   } else {
     const Tiling& T = a.t;
-    const int per = T.nty * T.ntz;
     const double* P = a.part + (size_t)i * T.NT * T.PS;
+    double* csum = sm + 2 * (nvx + nvy + nvz);
+    const int k0 = (list_len(T, 0) + kChunk - 1) / kChunk;
+    const int k1 = (list_len(T, 1) + kChunk - 1) / kChunk;
+    const int k2 = (list_len(T, 2) + kChunk - 1) / kChunk;
+    const int t1 = k0 * nvx, t2 = t1 + k1 * nvy, t3 = t2 + k2 * nvz;
+    for (int t = tid; t < t3; t += blockDim.x) {
+      const int ax = t < t1 ? 0 : (t < t2 ? 1 : 2);
+      const int q = t - (ax == 0 ? 0 : (ax == 1 ? t1 : t2));
+      const int n = ax == 0 ? nvx : (ax == 1 ? nvy : nvz);
+      const int c = q / n, j = q - c * n;
+      const int len = list_len(T, ax);
+      const EntryList e = entry_list(T, ax, j);
+      const int q1 = min(len, (c + 1) * kChunk);
+      csum[t] = chunk_sum(P, T.PS, e, c * kChunk, q1);
+    }
+    __syncthreads();
     for (int j = tid; j < nvx + nvy + nvz; j += blockDim.x) {
+      const int ax = j < nvx ? 0 : (j < nvx + nvy ? 1 : 2);
+      const int jj = j - (ax == 0 ? 0 : (ax == 1 ? nvx : nvx + nvy));
+      const int n = ax == 0 ? nvx : (ax == 1 ? nvy : nvz);
+      const int kk = ax == 0 ? k0 : (ax == 1 ? k1 : k2);
+      const double* cs0 = csum + (ax == 0 ? 0 : (ax == 1 ? t1 : t2)) + jj;
       double s = 0.0;
-      if (j < nvx) {
-        const int jx = j;
-        int tx, r0;
-        if (jx < T.nneg) {
-          tx = jx / T.A;
-          r0 = tx * T.A;
-        } else {
-          tx = T.ntn + (jx - T.nneg) / T.A;
-          r0 = T.nneg + (tx - T.ntn) * T.A;
-        }
-        const int off = jx - r0;
-        s = tile_sum(P, T.PS, tx * per, T.nty, T.ntz, T.ntz, 1, off);
-        mx[jx] = s;
-      } else if (j < nvx + nvy) {
-        const int jy = j - nvx;
-        const int ty = jy / T.By, off = T.A + jy - ty * T.By;
-        const int ntx = T.ntn + T.ntp;
-        s = tile_sum(P, T.PS, ty * T.ntz, ntx, per, T.ntz, 1, off);
-        my[jy] = s;
-      } else {
-        const int jz = j - nvx - nvy;
-        const int tz = jz / T.Bz, off = T.A + T.By + jz - tz * T.Bz;
-        const int ntx = T.ntn + T.ntp;
-        s = tile_sum(P, T.PS, tz, ntx, per, T.nty, T.ntz, off);
-        mz[jz] = s;
-      }
+      for (int c = 0; c < kk; ++c) s += cs0[c * n];
+      sm[j] = s;  // mx | my | mz are contiguous
     }
     // finiteness of f* (all its values feed these sums; a NaN/Inf anywhere
     // leaves a non-finite marginal) -- the guard of ref/kinetic.py:157-159
@@ -115,9 +168,9 @@ static __device__ __forceinline__ void finalize_cell(const FinalArgs& a, int i, 
       if (lane == 0) sh[0] = s;
     } else if (warp < 4) {
       const int ax = warp - 1;  // warps 1..3 -> axes 0..2
-      const int n = nv[ax], h = n / 2;
-      const double* m = ms[ax];
-      const double* c = cs[ax];
+      const int n = nv(ax), h = n / 2;
+      const double* m = ms(ax);
+      const double* c = cs(ax);
       double s = 0.0;
       for (int j = lane; j < h; j += 32) s += (m[j] - m[n - 1 - j]) * c[j];
       s = warp_allsum(s);
@@ -129,9 +182,9 @@ static __device__ __forceinline__ void finalize_cell(const FinalArgs& a, int i, 
     u1 = (sh[2] * a.dvol) / rho;
     u2 = (sh[3] * a.dvol) / rho;
     if (warp < 3) {
-      const int n = nv[warp];
-      const double* m = ms[warp];
-      const double* c = cs[warp];
+      const int n = nv(warp);
+      const double* m = ms(warp);
+      const double* c = cs(warp);
       const double ua = (warp == 0) ? u0 : (warp == 1 ? u1 : u2);
       double s = 0.0;
       for (int j = lane; j < n; j += 32) {
@@ -161,19 +214,18 @@ static __device__ __forceinline__ void finalize_cell(const FinalArgs& a, int i, 
   if (tid == 0 && (rho <= 0.0 || th <= 0.0)) atomicMin(a.err, err_key(0, a.step, kErrLiftState));
   const double inv2t = 1.0 / (2.0 * th);
   const double amp = rho / pow(6.283185307179586 * th, 1.5);
-  const double us[3] = {u0, u1, u2};
-  for (int ax = 0; ax < 3; ++ax) {
-    for (int j = tid; j < nv[ax]; j += blockDim.x) {
-      const double d = cs[ax][j] - us[ax];
+    for (int ax = 0; ax < 3; ++ax) {
+    for (int j = tid; j < nv(ax); j += blockDim.x) {
+      const double d = cs(ax)[j] - (ax == 0 ? u0 : (ax == 1 ? u1 : u2));
       double g = exp(-(d * d) * inv2t);
       if (ax == 0) g = g * amp;
-      gs[ax][j] = g;
+      gs(ax)[j] = g;
     }
   }
   __syncthreads();
   if (warp < 3) {
     double s = 0.0;
-    for (int j = lane; j < nv[warp]; j += 32) s += gs[warp][j];
+    for (int j = lane; j < nv(warp); j += 32) s += gs(warp)[j];
     s = warp_allsum(s);
     if (lane == 0) sh[8 + warp] = s;
   }

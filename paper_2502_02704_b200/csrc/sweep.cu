@@ -35,6 +35,16 @@
 #include "common.cuh"
 #include "ptx.cuh"
 
+#ifndef PBGK_HINT_LOAD
+#define PBGK_HINT_LOAD 0
+#endif
+#ifndef PBGK_HINT_STORE
+#define PBGK_HINT_STORE 0
+#endif
+#ifndef PBGK_HINT_PART
+#define PBGK_HINT_PART 1
+#endif
+
 namespace pbgk {
 
 constexpr unsigned FULL = 0xffffffffu;
@@ -215,6 +225,11 @@ __global__ void __launch_bounds__(NTHR, MINB)
   __syncthreads();
 
   // producer state (thread 0 only): loads run ns items ahead
+  // L2 policies: f is streamed once per sweep (evict first); the partial
+  // records are re-read by finalize right after the sweep (evict last)
+  const uint64_t pol_stream = make_policy_evict_first();
+  const uint64_t pol_keep = make_policy_evict_last();
+
   // producer: lane 0 of the LAST warp (the first warps carry the per-plane
   // partial sums), with the tile geometry cached across its run
   const int ptid = NTHR - 32;
@@ -242,7 +257,13 @@ __global__ void __launch_bounds__(NTHR, MINB)
       return;
     }
     mbar_arrive_expect_tx(bar, box_bytes + tab_bytes);
-    if (!SYNTH) tma_load_4d(st, &fmap, tg.z0, tg.y0, tg.r0 - hoff, i, bar);
+    if (!SYNTH) {
+#if PBGK_HINT_LOAD
+      tma_load_4d_hint(st, &fmap, tg.z0, tg.y0, tg.r0 - hoff, i, bar, pol_stream);
+#else
+      tma_load_4d(st, &fmap, tg.z0, tg.y0, tg.r0 - hoff, i, bar);
+#endif
+    }
     tma_load_1d(st + box_bytes, a.tab + (size_t)i * a.TL, tab_bytes, bar);
   };
   if (TMA && tid == ptid) {
@@ -451,7 +472,12 @@ __global__ void __launch_bounds__(NTHR, MINB)
               if (V == 4 && (FAST || zmask == 0xfu)) {
                 st_global_v4(d, o[0], o[1 % V], o[2 % V], o[3 % V]);
               } else if (V == 2 && (FAST || zmask == 0x3u)) {
+                
+#if PBGK_HINT_STORE
+                st_global_v2_hint(d, o[0], o[1 % V], pol_stream);
+#else
                 st_global_v2(d, o[0], o[1 % V]);
+#endif
               } else {
 #pragma unroll
                 for (int v = 0; v < V; ++v)
@@ -526,14 +552,26 @@ __global__ void __launch_bounds__(NTHR, MINB)
         if (tg.r0 + o < tg.r1) {
           double s2 = 0.0;
           for (int b = 0; b < T.By; ++b) s2 += LTb[o * T.By + b];
-          dst[o] = s2;
+          
+#if PBGK_HINT_PART
+          st_global_f64_hint(dst + o, s2, pol_keep);
+#else
+          *(dst + o) = s2;
+#endif
+
         }
       } else if (o < T.A + T.By) {
         const int b = o - T.A;
         if (tg.y0 + b < a.nvy) {
           double s2 = 0.0;
           for (int aa = 0; aa < T.A; ++aa) s2 += LTb[aa * T.By + b];
-          dst[T.A + b] = s2;
+          
+#if PBGK_HINT_PART
+          st_global_f64_hint(dst + T.A + b, s2, pol_keep);
+#else
+          *(dst + T.A + b) = s2;
+#endif
+
         }
       } else if (o < T.A + T.By + BZ) {
         const int zz = o - T.A - T.By;
@@ -541,7 +579,13 @@ __global__ void __launch_bounds__(NTHR, MINB)
           double s2 = 0.0;
 #pragma unroll
           for (int w = 0; w < NW; ++w) s2 += PZb[w * BZ + zz];
-          dst[T.A + T.By + zz] = s2;
+          
+#if PBGK_HINT_PART
+          st_global_f64_hint(dst + T.A + T.By + zz, s2, pol_keep);
+#else
+          *(dst + T.A + T.By + zz) = s2;
+#endif
+
         }
       }
     }
