@@ -42,7 +42,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=4, choices=[0, 1, 2, 3, 4])
+    ap.add_argument("--config", type=lambda s: s if s == "3b" else int(s), default=4,
+                    choices=[0, 1, 2, 3, "3b", 4])
     ap.add_argument("--eps", type=float, default=None)
     ap.add_argument("--bc", default=None, choices=["absorbing", "outflow", "periodic"],
                     help="override the workload's x boundary")
@@ -146,8 +147,8 @@ def build_problem(w):
     bc = P.BoundaryKind(w.bc)
     disc = P.Discretization(phase, P.build_time_grids(w.t_final, w.n_g, max(w.n_f, w.n_g)), bc)
     E = w.force()
-    kinetic = P.KineticParams(epsilon=w.eps, force=E)
-    fluid = P.FluidParams(force=E)
+    kinetic = P.KineticParams(epsilon=w.eps, force=E, alpha=w.alpha)
+    fluid = P.FluidParams(force=E, model=w.g_model)
     return P, phase, bc, disc, kinetic, fluid
 
 
@@ -310,7 +311,7 @@ def cpu_baseline(w, steps=6, cells=4.0e6):
     from oracle.cpu_bench import slab_rate
     plane = int(np.prod(w.nv))
     nx_slab = max(4, int(cells // plane))
-    r = slab_rate(w.nx, w.nv, w.v_max, w.eps, nx_slab, steps)
+    r = slab_rate(w.nx, w.nv, w.v_max, w.eps, nx_slab, steps, alpha=w.alpha)
     return {"value": r["value"], "unit": "cell-updates/s", "cores": r["cores"], "kind": "port",
             "sample": r["sample"], "seconds": r["per_core_s"]}
 
@@ -324,7 +325,8 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     cfg_json = {"workload": w.name + (" parareal iteration 1" if w.mode == "parareal" else
                                       " fine propagate T=%g" % w.t_final),
-                "nx": w.nx, "nv": list(w.nv), "eps": w.eps, "windows": w.n_g,
+                "nx": w.nx, "nv": list(w.nv), "eps": w.eps, "alpha": w.alpha, "coarse": w.g_model,
+                "windows": w.n_g,
                 "fine_steps_per_window": w.window_steps(),
                 "parallelism": ("windows sharded over %d rank(s)" % world) if w.mode == "parareal"
                 else ("replicas x%d" % world),

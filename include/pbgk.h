@@ -120,6 +120,14 @@ int pbgk_parareal_correct(pbgk_ctx* ctx, int n_g, int start, double* snaps, cons
                           const double* jumps, const double* h_times, double dt_max, double cfl,
                           const double* force, void* stream, double* h_err, long long* h_code);
 
+/* Selects the coarse propagator used by pbgk_fluid_propagate and
+ * pbgk_parareal_correct on this context: model 0 = the reference's Rusanov
+ * Euler G (default); model 1 = the drift-diffusion G of the diffusive scaling
+ * (EXTENSION, no reference counterpart -- SPEC:8; PAPER eq. (DDbis) with the
+ * central scheme of PAPER:351): d_t rho = D d_x(d_x rho - E rho), output
+ * (rho, u = 0, theta = 1), D = `diffusivity` (> 0). */
+int pbgk_fluid_model(pbgk_ctx* ctx, int model, double diffusivity);
+
 /* ---- measurement (bench.py) ------------------------------------------- */
 /* Human-readable tiling / launch plan of a context (diagnostics). */
 int pbgk_ctx_describe(const pbgk_ctx* ctx, char* buf, size_t n);

@@ -244,19 +244,34 @@ def fine_schedule(t0: float, t1: float, cap: float) -> list:
     return out
 
 
+def scaled_cap(mesh: Mesh, cfl: float, force, eps: float, alpha: int) -> float:
+    """CFL cap in physical time.  ORACLE EXTENSION for alpha = 1 (diffusive
+    scaling, PAPER eq. (1): transport rate 1/eps, relaxation 1/eps^2): the
+    alpha = 0 cap times eps."""
+    cap = fine_cap(mesh, cfl, force)
+    return cap * eps if alpha == 1 else cap
+
+
 def fine_propagate(f0: np.ndarray, t0: float, t1: float, mesh: Mesh,
                    eps: float, periodic: bool, force=None, dt_max=None,
-                   cfl: float = 0.5, tau: Callable = unit_tau) -> np.ndarray:
-    """F over [t0, t1] (ref/kinetic.py:137-161)."""
+                   cfl: float = 0.5, tau: Callable = unit_tau, alpha: int = 0) -> np.ndarray:
+    """F over [t0, t1] (ref/kinetic.py:137-161).
+
+    ``alpha = 1`` is an ORACLE EXTENSION (unpinned; the reference has only
+    alpha = 0): a physical step d runs the reference's transport and relax
+    with the scaled step d / eps, i.e. transport rate d/(eps dx) and
+    lambda = (d/eps) tau / eps = d tau / eps^2."""
     if t1 < t0:
         raise OracleConfigError("t1 < t0")
     if t1 - t0 == 0.0:
         return f0
-    cap = fine_cap(mesh, cfl, force)
+    cap = scaled_cap(mesh, cfl, force, eps, alpha)
     if dt_max is not None:
         cap = min(cap, dt_max)
     f = f0
     for s, d in enumerate(fine_schedule(t0, t1, cap), start=1):
+        if alpha == 1:
+            d = d / eps
         f = transport(f, d, mesh, periodic, force)
         f = relax(f, d, mesh, eps, tau)
         if not np.all(np.isfinite(f)):
@@ -366,6 +381,72 @@ def coarse_propagate(rho, u, theta, t0, t1, mesh: Mesh, periodic: bool,
 
 
 # --------------------------------------------------------------------------
+# drift-diffusion coarse propagator -- ORACLE EXTENSION (unpinned)
+# --------------------------------------------------------------------------
+# PAPER eq. (DDbis): d_t rho - m2 d_x J = 0, J = d_x rho - E rho, with u = 0,
+# theta = 1; discretised by the central finite-difference scheme the paper
+# names, explicit in time.  The reference has no diffusive G
+# (SPEC:8); this is the builder's restatement, the checker of the CUDA G.
+# Conservative face fluxes J_{i+1/2} = (rho_{i+1}-rho_i)/dx
+# - 0.5 (E_i rho_i + E_{i+1} rho_{i+1}); rho_i += (dt D / dx)(J_{i+1/2} - J_{i-1/2}).
+# Ghosts: periodic wrap, else zero-gradient copies of rho and E.
+
+def dd_m2(mesh: Mesh) -> float:
+    """Second moment of the discrete unit Maxwellian along v_x (m2 of DDbis)."""
+    c = mesh.vc[0]
+    w = np.exp(-(c * c) * 0.5)
+    return float(np.sum(c * c * w) / np.sum(w))
+
+
+def dd_cap(dx: float, D: float, e_max: float, cfl: float) -> float:
+    """Explicit stability bound cfl dx^2 / (D (2 + dx e_max))."""
+    return cfl * dx * dx / (D * (2.0 + dx * e_max))
+
+
+def dd_propagate(rho, t0, t1, mesh: Mesh, periodic, force=None, dt_max=None,
+                 cfl: float = 0.9, D: float = 1.0):
+    """G over [t0, t1] for the drift-diffusion model; returns (rho, u=0, theta=1)."""
+    if t1 < t0:
+        raise OracleConfigError("t1 < t0")
+    nx = rho.shape[0]
+    span = t1 - t0
+    if span == 0.0:
+        return rho, np.zeros((nx, 3)), np.ones(nx)
+    E = np.zeros(nx) if force is None else np.asarray(force, dtype=float)
+    cap = dd_cap(mesh.dx, D, field_bound(force), cfl)
+    if dt_max is not None:
+        cap = min(cap, dt_max)
+    r = np.array(rho, dtype=float, copy=True)
+    done = 0.0
+    step = 0
+    g = np.empty(nx + 2)
+    e = np.empty(nx + 2)
+    e[1:-1] = E
+    if bc_kind(periodic) == "periodic":
+        e[0], e[-1] = E[-1], E[0]
+    else:
+        e[0], e[-1] = E[0], E[-1]
+    while span - done > GUARD * span:
+        d = min(cap, span - done)
+        g[1:-1] = r
+        if bc_kind(periodic) == "periodic":
+            g[0], g[-1] = r[-1], r[0]
+        else:
+            g[0], g[-1] = r[0], r[-1]
+        J = (g[1:] - g[:-1]) / mesh.dx - 0.5 * (e[:-1] * g[:-1] + e[1:] * g[1:])
+        coef = d * D / mesh.dx
+        nr = r + coef * (J[1:] - J[:-1])
+        step += 1
+        if not np.all(np.isfinite(nr)):
+            raise OracleBlowUp("drift-diffusion non-finite at step %d" % step, step=step)
+        if np.any(nr <= 0.0):
+            raise OracleBlowUp("drift-diffusion unphysical at step %d" % step, step=step)
+        r = nr
+        done += d
+    return r, np.zeros((nx, 3)), np.ones(nx)
+
+
+# --------------------------------------------------------------------------
 # parareal slice loop (ref/parareal.py:109-314)
 # --------------------------------------------------------------------------
 
@@ -383,6 +464,9 @@ class Problem:
     cfl_kin: float = 0.5
     cfl_fluid: float = 0.9
     tau: Callable = unit_tau
+    alpha: int = 0                 # 1: diffusive scaling (ORACLE EXTENSION)
+    g_model: str = "euler"         # "drift_diffusion": dd_propagate (ORACLE EXTENSION)
+    diffusivity: Optional[float] = None  # D of the drift-diffusion G (default m2 / 1)
 
     @property
     def times(self):
@@ -400,6 +484,10 @@ class Problem:
 def G(prob: Problem, U, n: int):
     """Coarse solve over window n (1-based)."""
     t = prob.times
+    if prob.g_model == "drift_diffusion":
+        D = prob.diffusivity if prob.diffusivity is not None else dd_m2(prob.mesh)
+        return dd_propagate(U[0], float(t[n - 1]), float(t[n]), prob.mesh, prob.periodic,
+                            prob.force, prob.dt_g, prob.cfl_fluid, D)
     return coarse_propagate(*U, float(t[n - 1]), float(t[n]), prob.mesh,
                             prob.periodic, prob.force, prob.dt_g, prob.cfl_fluid)
 
@@ -410,7 +498,7 @@ def PFL(prob: Problem, U, n: int):
     f = lift(*U, prob.mesh, normalize=False)
     f = fine_propagate(f, float(t[n - 1]), float(t[n]), prob.mesh, prob.eps,
                        prob.periodic, prob.force, prob.dt_f, prob.cfl_kin,
-                       prob.tau)
+                       prob.tau, prob.alpha)
     return project(f, prob.mesh)
 
 

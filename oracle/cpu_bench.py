@@ -22,7 +22,7 @@ from . import bgk as O
 
 
 def _slab_worker(args):
-    nx_slab, dx, nv, v_max, eps, steps = args
+    nx_slab, dx, nv, v_max, eps, steps, alpha = args
     try:
         from threadpoolctl import threadpool_limits
         threadpool_limits(1)
@@ -34,14 +34,14 @@ def _slab_worker(args):
     u = np.zeros((nx_slab, 3))
     theta = np.where(x < 0.5, 1.0, 0.8)
     f = O.lift(rho, u, theta, mesh)
-    cap = O.fine_cap(mesh, 0.5)
+    cap = O.scaled_cap(mesh, 0.5, None, eps, alpha)
     tic = time.perf_counter()
-    O.fine_propagate(f, 0.0, steps * cap, mesh, eps, True)
+    O.fine_propagate(f, 0.0, steps * cap, mesh, eps, True, alpha=alpha)
     return time.perf_counter() - tic
 
 
 def slab_rate(nx_full: int, nv, v_max: float, eps: float, nx_slab: int, steps: int,
-              workers: int | None = None) -> dict:
+              workers: int | None = None, alpha: int = 0) -> dict:
     """Aggregate cell-updates/s of `workers` concurrent oracle slab solves."""
     workers = workers or len(os.sched_getaffinity(0))
     dx = 1.0 / nx_full
@@ -50,7 +50,7 @@ def slab_rate(nx_full: int, nv, v_max: float, eps: float, nx_slab: int, steps: i
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     tic = time.perf_counter()
     with ctx.Pool(workers) as pool:
-        secs = pool.map(_slab_worker, [(nx_slab, dx, tuple(nv), v_max, eps, steps)] * workers)
+        secs = pool.map(_slab_worker, [(nx_slab, dx, tuple(nv), v_max, eps, steps, alpha)] * workers)
     wall = time.perf_counter() - tic
     total = workers * cells * steps
     # rate over the slowest worker's compute time (pool start-up excluded)

@@ -44,6 +44,7 @@ PROTOTYPES = {
     "pbgk_fluid_propagate": (c_int, [_P, _I, _P, _P, _P, POINTER(c_double), POINTER(c_double),
                                      _D, _D, _P, _P, _CODE]),
     "pbgk_check_finite": (c_int, [_P, _P, _I, _P, _CODE]),
+    "pbgk_fluid_model": (c_int, [_P, _I, _D]),
     "pbgk_parareal_correct": (c_int, [_P, _I, _I, _P, _P, _P, POINTER(c_double), _D, _D, _P,
                                       _P, POINTER(c_double), _CODE]),
 }

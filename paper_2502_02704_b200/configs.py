@@ -7,6 +7,10 @@ cfl_kinetic = 0.5, cfl_fluid = 0.9, alpha = 0.  The Sod tubes (configs 0, 2,
 (an extension: the reference only has the zero-inflow ``absorbing`` ghost, with
 which configs 2 and 4 raise CorrectionOvershootError in iteration 1 -- the
 depleted edge cell accumulates negative jumps; measured).
+Config 3 comes in two variants: 3a (alpha = 0, Euler G + the same field;
+reference-pinned) and 3b (alpha = 1 diffusive scaling with the drift-diffusion
+G, as BASELINE.json states it; an extension, pinned only to the builder's
+oracle extension).
 Initial moments are ``U0 = project(lift(U_raw))`` as in ref/runner.py:27-32.
 Pure numpy problem data (no solver calls) so the CPU oracle and the GPU path
 build the identical inputs.
@@ -42,6 +46,8 @@ class Workload:
     init: str = "sod"  # sod | sod_noise | wave | cos
     seed: int = 2502
     outflow: bool = False  # zero-gradient kinetic ghosts (extension) instead of absorbing
+    alpha: int = 0  # 1: diffusive scaling (extension)
+    g_model: str = "euler"  # "drift_diffusion": the diffusive G (extension)
 
     @property
     def bc(self) -> str:
@@ -90,6 +96,8 @@ class Workload:
         if f is not None and np.max(np.abs(f)) > 0:
             rate += np.max(np.abs(f)) / (2.0 * self.v_max / self.nv[0])
         cap = 0.5 / rate
+        if self.alpha == 1:
+            cap = cap * self.eps
         span = self.t_final / self.n_g if self.mode == "parareal" else self.t_final
         if self.mode == "parareal":
             cap = min(cap, self.t_final / self.n_f)
@@ -100,8 +108,15 @@ class Workload:
         return n
 
 
-def config(idx: int, eps: Optional[float] = None) -> Workload:
-    """BASELINE.json configs[idx] (config 3 is the pinned alpha=0 variant 3a)."""
+def config(idx, eps: Optional[float] = None) -> Workload:
+    """BASELINE.json configs[idx]; config 3 is the pinned alpha=0 variant 3a,
+    ``"3b"`` the alpha = 1 drift-diffusion variant."""
+    if idx == "3b":
+        return Workload("cfg3b-diffusive-1024x32^3", 1024, (32,) * 3, 8.0, 1e-2, True, 0.05, 32, 32, 5,
+                        1e-8, "parareal", force_kind="sin", init="cos", alpha=1,
+                        g_model="drift_diffusion")
+    if isinstance(idx, str):
+        idx = int(idx)
     if idx == 0:
         return Workload("cfg0-sod-64x16^3", 64, (16,) * 3, 8.0, 1e-2, False, 0.1, 8, 8, 2, 1e-300,
                         "parareal", outflow=True)

@@ -25,15 +25,6 @@ cudaError_t launch_sweep(int cfg_id, const CUtensorMap& map, const SweepArgs& a,
 size_t sweep_smem_bytes(const SweepArgs& a, int V, int LZ, int NTHR, bool synth, bool tma, int ns);
 cudaError_t launch_finalize(const FinalArgs& a, cudaStream_t st);
 cudaError_t launch_set_key(ErrKey* p, ErrKey v, cudaStream_t st);
-struct FluidArgs {
-  int nx;
-  double dx;
-  int periodic;
-  double dt_max;
-  double cfl;
-  const double* force;
-  ErrKey* err;
-};
 cudaError_t launch_fluid_batch(const FluidArgs& a, int nwin, const double* in, double* out,
                                const double* minuend, const double* t0, const double* t1,
                                cudaStream_t st);
@@ -119,6 +110,8 @@ struct EvPair {
 };
 
 struct pbgk_ctx {
+  int g_model = 0;       // coarse G: 0 Euler (reference), 1 drift-diffusion (extension)
+  double g_diff = 1.0;   // drift-diffusion D
   pbgk_grid_desc g;
   bool prof = false;
   std::vector<EvPair> ev_pool, ev_used;
@@ -674,7 +667,8 @@ int pbgk_fluid_propagate(pbgk_ctx* c, int nwin, const double* mom_in, double* mo
   }
   if (upload_times(c, t.data(), t.size(), st)) return -1;
   if (reset_err(c, st)) return -1;
-  FluidArgs a{c->g.nx, c->dx, c->g.bc == 1 ? 1 : 0, dt_max, cfl, force, c->d_err};
+  FluidArgs a{c->g.nx, c->dx, c->g.bc == 1 ? 1 : 0, dt_max, cfl, force, c->d_err, c->g_model,
+              c->g_diff};
   ++g_launches;
   CK(launch_fluid_batch(a, nwin, mom_in, mom_out, minuend, c->d_times, c->d_times + nwin, st));
   return fetch_err(c, st, h_code);
@@ -689,7 +683,8 @@ int pbgk_parareal_correct(pbgk_ctx* c, int n_g, int start, double* snaps, const 
   cudaStream_t st = (cudaStream_t)stream;
   if (upload_times(c, h_times, (size_t)n_g + 1, st)) return -1;
   if (reset_err(c, st)) return -1;
-  FluidArgs a{c->g.nx, c->dx, c->g.bc == 1 ? 1 : 0, dt_max, cfl, force, c->d_err};
+  FluidArgs a{c->g.nx, c->dx, c->g.bc == 1 ? 1 : 0, dt_max, cfl, force, c->d_err, c->g_model,
+              c->g_diff};
   double* d_e = c->d_scratch;
   CK(cudaMemsetAsync(d_e, 0, sizeof(double), st));
   if (start <= n_g) ++g_launches;
@@ -699,6 +694,15 @@ int pbgk_parareal_correct(pbgk_ctx* c, int n_g, int start, double* snaps, const 
   if (fetch_err(c, st, &code)) return -1;
   if (h_code) *h_code = code;
   if (h_err) *h_err = c->h_dbl[0];
+  return 0;
+}
+
+int pbgk_fluid_model(pbgk_ctx* c, int model, double diffusivity) {
+  if (!c) return fail("pbgk_fluid_model: null context");
+  if (model != 0 && model != 1) return fail("pbgk_fluid_model: model must be 0 (Euler) or 1 (drift-diffusion)");
+  if (model == 1 && !(diffusivity > 0.0)) return fail("pbgk_fluid_model: diffusivity must be > 0");
+  c->g_model = model;
+  c->g_diff = diffusivity;
   return 0;
 }
 

@@ -91,4 +91,18 @@ struct FinalArgs {
   int check_finite;      // kFinProject: flag non-finite marginals as BlowUpError(step)
 };
 
+// Coarse propagator arguments (fluid.cu).  model 0: the reference's Rusanov
+// Euler G; model 1: the drift-diffusion G of the diffusive scaling (extension).
+struct FluidArgs {
+  int nx;
+  double dx;
+  int periodic;
+  double dt_max;  // <= 0: none
+  double cfl;
+  const double* force;  // nx or null
+  ErrKey* err;
+  int model;
+  double diff;          // model 1: diffusivity D = m2 / tau
+};
+
 }  // namespace pbgk

@@ -13,16 +13,6 @@
 
 namespace pbgk {
 
-struct FluidArgs {
-  int nx;
-  double dx;
-  int periodic;
-  double dt_max;  // <= 0: none
-  double cfl;
-  const double* force;  // nx or null
-  ErrKey* err;
-};
-
 #define DM __dmul_rn
 #define DA __dadd_rn
 #define DS __dsub_rn
@@ -165,8 +155,93 @@ __device__ ErrKey g_advance(double* V, double* red, int* flag, const FluidArgs& 
   return 0;
 }
 
+// Drift-diffusion G (extension; oracle/bgk.py dd_propagate, same operation
+// order): rho only, held in V[0..nx).  Conservative central fluxes
+//   J_{i+1/2} = (rho_{i+1} - rho_i)/dx - 0.5 (E_i rho_i + E_{i+1} rho_{i+1}),
+//   rho_i += (dt D / dx) (J_{i+1/2} - J_{i-1/2}),
+// dt = min(cfl dx^2 / (D (2 + dx e_max)), dt_max, remaining).  Ghosts: periodic
+// wrap, else zero-gradient copies of rho and E.
+__device__ ErrKey g_advance_dd(double* V, double* red, int* flag, const FluidArgs& a, double span) {
+  const int nx = a.nx;
+  const double guard = 1e-12;
+  double em = 0.0;
+  if (a.force != nullptr) {
+    for (int i = threadIdx.x; i < nx; i += blockDim.x) em = fmax(em, fabs(a.force[i]));
+    em = block_max(em, red);
+  }
+  double cap = DD(DM(DM(a.cfl, a.dx), a.dx), DM(a.diff, DA(2.0, DM(a.dx, em))));
+  if (a.dt_max > 0.0) cap = fmin(cap, a.dt_max);
+  auto E = [&](int i) { return a.force != nullptr ? a.force[i] : 0.0; };
+  double done = 0.0;
+  unsigned long long step = 0;
+  while (DS(span, done) > DM(guard, span)) {
+    const double dt = fmin(cap, DS(span, done));
+    const double coef = DD(DM(dt, a.diff), a.dx);
+    ++step;
+    double nr[kMaxCellsPerThread];
+    int bad = 0;
+#pragma unroll
+    for (int k = 0; k < kMaxCellsPerThread; ++k) {
+      const int i = threadIdx.x + k * blockDim.x;
+      if (i >= nx) break;
+      const int il = i > 0 ? i - 1 : (a.periodic ? nx - 1 : 0);
+      const int ir = i < nx - 1 ? i + 1 : (a.periodic ? 0 : nx - 1);
+      const double gi = V[i], gl = V[il], gr = V[ir];
+      const double ei = E(i), el = E(il), er = E(ir);
+      const double JR = DS(DD(DS(gr, gi), a.dx), DM(0.5, DA(DM(ei, gi), DM(er, gr))));
+      const double JL = DS(DD(DS(gi, gl), a.dx), DM(0.5, DA(DM(el, gl), DM(ei, gi))));
+      const double v = DA(gi, DM(coef, DS(JR, JL)));
+      nr[k] = v;
+      if (!isfinite(v)) bad |= 1;
+      else if (v <= 0.0) bad |= 2;
+    }
+    if (bad) atomicOr(flag, bad);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kMaxCellsPerThread; ++k) {
+      const int i = threadIdx.x + k * blockDim.x;
+      if (i >= nx) break;
+      V[i] = nr[k];
+    }
+    __syncthreads();
+    const int f = *flag;
+    if (f) return (step << 8) | (unsigned long long)((f & 1) ? kErrNonFinite : kErrUnphysical);
+    done = DA(done, dt);
+  }
+  return 0;
+}
+
+// Loads window state into smem V: conserved variables (Euler) or rho (DD).
+__device__ __forceinline__ void load_window(const FluidArgs& a, const double* src, double* V) {
+  const int nx = a.nx;
+  for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+    if (a.model == 1) {
+      V[i] = src[i];
+      continue;
+    }
+    double v[5];
+    to_cons(src[i], src[nx + i], src[2 * nx + i], src[3 * nx + i], src[4 * nx + i], v);
+#pragma unroll
+    for (int q = 0; q < 5; ++q) V[q * nx + i] = v[q];
+  }
+}
+
+__device__ __forceinline__ ErrKey advance(double* V, double* red, int* flag, const FluidArgs& a,
+                                          double span) {
+  return a.model == 1 ? g_advance_dd(V, red, flag, a, span) : g_advance(V, red, flag, a, span);
+}
+
 // conserved -> primitive (ref/moments.py:122-129); returns false if degenerate.
-__device__ bool to_prim(const double* V, int nx, int i, double out[5]) {
+// Drift-diffusion: (rho, 0, 0, 0, 1), never degenerate (rho > 0 is checked per step).
+__device__ bool to_prim(const FluidArgs& a, const double* V, int nx, int i, double out[5]) {
+  if (a.model == 1) {
+    out[0] = V[i];
+    out[1] = 0.0;
+    out[2] = 0.0;
+    out[3] = 0.0;
+    out[4] = 1.0;
+    return true;
+  }
   const double rho = V[i], m0 = V[nx + i], m1 = V[2 * nx + i], m2 = V[3 * nx + i],
                en = V[4 * nx + i];
   const double u0 = DD(m0, rho), u1 = DD(m1, rho), u2 = DD(m2, rho);
@@ -191,22 +266,20 @@ __global__ void __launch_bounds__(1024) fluid_batch_kernel(FluidArgs a, const do
   const int w = blockIdx.x, nx = a.nx;
   const double* src = in + (size_t)w * 5 * nx;
   if (threadIdx.x == 0) flag = 0;
-  for (int i = threadIdx.x; i < nx; i += blockDim.x) {
-    double v[5];
-    to_cons(src[i], src[nx + i], src[2 * nx + i], src[3 * nx + i], src[4 * nx + i], v);
-#pragma unroll
-    for (int q = 0; q < 5; ++q) V[q * nx + i] = v[q];
-  }
+  load_window(a, src, V);
   __syncthreads();
   const double span = DS(t1[w], t0[w]);
   double* dst = out + (size_t)w * 5 * nx;
   const double* mn = minuend ? minuend + (size_t)w * 5 * nx : nullptr;
-  if (span == 0.0) {  // ref/fluid.py:98-99: the input itself
-    for (int i = threadIdx.x; i < 5 * nx; i += blockDim.x)
-      dst[i] = mn ? DS(mn[i], src[i]) : src[i];
+  if (span == 0.0) {  // ref/fluid.py:98-99: the input itself (DD: rho, 0, 1)
+    for (int i = threadIdx.x; i < 5 * nx; i += blockDim.x) {
+      double v = src[i];
+      if (a.model == 1 && i >= nx) v = (i >= 4 * nx) ? 1.0 : 0.0;
+      dst[i] = mn ? DS(mn[i], v) : v;
+    }
     return;
   }
-  const ErrKey code = g_advance(V, red, &flag, a, span);
+  const ErrKey code = advance(V, red, &flag, a, span);
   if (code) {
     if (threadIdx.x == 0) atomicMin(a.err, ((ErrKey)w << 40) | code);
     return;
@@ -214,7 +287,7 @@ __global__ void __launch_bounds__(1024) fluid_batch_kernel(FluidArgs a, const do
   bool ok = true;
   for (int i = threadIdx.x; i < nx; i += blockDim.x) {
     double p[5];
-    ok = to_prim(V, nx, i, p) && ok;
+    ok = to_prim(a, V, nx, i, p) && ok;
 #pragma unroll
     for (int q = 0; q < 5; ++q) dst[q * nx + i] = mn ? DS(mn[q * nx + i], p[q]) : p[q];
   }
@@ -239,19 +312,14 @@ __global__ void __launch_bounds__(1024) correct_kernel(FluidArgs a, int n_g, int
   __syncthreads();
   for (int n = start; n <= n_g; ++n) {
     const double* src = snaps + (size_t)(n - 1) * 5 * nx;
-    for (int i = threadIdx.x; i < nx; i += blockDim.x) {
-      double v[5];
-      to_cons(src[i], src[nx + i], src[2 * nx + i], src[3 * nx + i], src[4 * nx + i], v);
-#pragma unroll
-      for (int q = 0; q < 5; ++q) V[q * nx + i] = v[q];
-    }
+    load_window(a, src, V);
     __syncthreads();
     const double span = DS(times[n], times[n - 1]);
     double* dst = snaps + (size_t)n * 5 * nx;
     const double* jp = jumps + (size_t)(n - 1) * 5 * nx;
     const double* od = old + (size_t)n * 5 * nx;
     ErrKey code = 0;
-    if (span != 0.0) code = g_advance(V, red, &flag, a, span);
+    if (span != 0.0) code = advance(V, red, &flag, a, span);
     if (code) {
       if (threadIdx.x == 0) atomicMin(a.err, ((ErrKey)n << 40) | code);
       return;
@@ -261,10 +329,14 @@ __global__ void __launch_bounds__(1024) correct_kernel(FluidArgs a, int n_g, int
     for (int i = threadIdx.x; i < nx; i += blockDim.x) {
       double p[5];
       if (span != 0.0) {
-        if (!to_prim(V, nx, i, p)) degen = true;
+        if (!to_prim(a, V, nx, i, p)) degen = true;
       } else {
 #pragma unroll
         for (int q = 0; q < 5; ++q) p[q] = src[q * nx + i];
+        if (a.model == 1) {
+          p[1] = p[2] = p[3] = 0.0;
+          p[4] = 1.0;
+        }
       }
       double c[5];
 #pragma unroll

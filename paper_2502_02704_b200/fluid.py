@@ -1,4 +1,5 @@
-"""Coarse propagator G: first-order Rusanov Euler solver with a force source.
+"""Coarse propagator G: first-order Rusanov Euler solver with a force source,
+or (extension) the drift-diffusion solver of the diffusive scaling.
 
 ``propagate_fluid`` runs on the GPU (``pbgk_fluid_propagate``: one CTA holds the
 window's conserved state in shared memory and performs every step, CFL max
@@ -6,6 +7,14 @@ included, in the reference's operation order — bitwise the numpy result of
 ref/fluid.py:91-125 on the same input).  The flux helpers ``euler_flux``,
 ``rusanov_flux`` and ``stable_dt_fluid`` are the reference's small pointwise
 API (ref/fluid.py:45-75), kept as host functions of tiny arrays.
+
+``FluidParams(model="drift_diffusion")`` selects the EXTENSION G for the
+diffusive scaling alpha = 1 (BASELINE.json config 3; the reference has none,
+SPEC:8): PAPER eq. (DDbis) ``d_t rho = D d_x(d_x rho - E rho)`` with u = 0,
+theta = 1, discretised by the explicit central scheme PAPER:351 names
+(``fluid.cu`` ``g_advance_dd``; checker: ``oracle/bgk.py`` ``dd_propagate``).
+``D`` defaults to m2 / tau = the v_x second moment of the discrete unit
+Maxwellian (tau = 1).
 """
 
 from __future__ import annotations
@@ -22,13 +31,56 @@ from .errors import ConfigurationError
 from .moments import ConservedField, MomentField
 
 __all__ = ["FluidParams", "euler_flux", "rusanov_flux", "stable_dt_fluid", "propagate_fluid",
-           "fluid_batch"]
+           "fluid_batch", "drift_diffusion_m2", "stable_dt_drift_diffusion"]
+
+G_MODELS = ("euler", "drift_diffusion")
 
 
 @dataclass
 class FluidParams:
     force: Optional[np.ndarray] = None  # per-cell E_i; None = no field
     cfl: float = 0.9
+    model: str = "euler"                # "drift_diffusion": extension G (alpha = 1)
+    diffusivity: Optional[float] = None  # drift-diffusion D; None = m2 of the grid
+
+    def __post_init__(self):
+        if self.model not in G_MODELS:
+            raise ConfigurationError("unknown coarse model %r (expected one of %s)"
+                                     % (self.model, ", ".join(G_MODELS)))
+        if self.diffusivity is not None and not self.diffusivity > 0.0:
+            raise ConfigurationError("need diffusivity > 0, got %r" % (self.diffusivity,))
+
+
+def drift_diffusion_m2(v_max: float, n_vx: int) -> float:
+    """m2 of PAPER eq. (DDbis): sum c^2 w / sum w, w = exp(-c^2/2) on the v_x centres."""
+    from .grid import _centres
+    c = _centres(v_max, n_vx)
+    w = np.exp(-(c * c) * 0.5)
+    return float(np.sum(c * c * w) / np.sum(w))
+
+
+def _diffusivity(ctx, params: FluidParams) -> float:
+    if params.diffusivity is not None:
+        return float(params.diffusivity)
+    return drift_diffusion_m2(ctx.v_max, ctx.shape[1])
+
+
+def select_model(ctx, params: FluidParams) -> None:
+    """Point the context's G (pbgk_fluid_model) at params.model."""
+    if params.model == "euler":
+        rt._lib.check(ctx.lib.pbgk_fluid_model(ctx.h, 0, 1.0), "pbgk_fluid_model")
+    else:
+        rt._lib.check(ctx.lib.pbgk_fluid_model(ctx.h, 1, _diffusivity(ctx, params)),
+                      "pbgk_fluid_model")
+
+
+def stable_dt_drift_diffusion(grid, params: FluidParams) -> float:
+    """cfl dx^2 / (D (2 + dx e_max)): the explicit central scheme's step bound."""
+    dx = grid.space.dx
+    D = params.diffusivity if params.diffusivity is not None else \
+        drift_diffusion_m2(grid.velocity.v_max, grid.velocity.n_v[0])
+    e = 0.0 if params.force is None else float(np.max(np.abs(params.force)))
+    return params.cfl * dx * dx / (D * (2.0 + dx * e))
 
 
 def _p(v):
@@ -69,6 +121,7 @@ def fluid_batch(ctx, mom_in: torch.Tensor, mom_out: torch.Tensor, t0s, t1s, para
     the output is ``minuend - G(mom_in)`` (the parareal jump).
     """
     nwin = mom_in.shape[0]
+    select_model(ctx, params)
     if force_dev is None and params.force is not None:
         force_dev, _ = rt.to_device_field(params.force, ctx.device, ctx.nx)
     a0 = (ctypes.c_double * nwin)(*map(float, t0s))

@@ -12,6 +12,13 @@ A collision frequency ``tau`` that is ``constant_tau`` / ``ConstantTau`` (the
 reference's defaults, also when imported from the reference package) is
 evaluated on the device.  Any other callable is honoured through a slower
 step-by-step path that evaluates ``tau(rho, theta)`` on the host each step.
+
+``KineticParams(alpha=1)`` is the diffusive scaling of PAPER eq. (1) (an
+EXTENSION; the reference implements alpha = 0 only): transport at rate
+1/eps and relaxation at 1/eps^2.  A physical step d is the reference's
+alpha = 0 step with the scaled step d/eps (transport d/(eps dx),
+lambda = (d/eps) tau/eps), and the CFL cap is eps times the alpha = 0 cap;
+checker: ``oracle/bgk.py`` ``fine_propagate(alpha=1)``.
 """
 
 from __future__ import annotations
@@ -57,6 +64,16 @@ class KineticParams:
     tau: Callable = constant_tau
     force: Optional[np.ndarray] = None
     cfl: float = 0.5
+    alpha: int = 0  # 0 hydrodynamic (reference); 1 diffusive scaling (extension)
+
+    def __post_init__(self):
+        if self.alpha not in (0, 1):
+            raise ConfigurationError("alpha must be 0 or 1, got %r" % (self.alpha,))
+
+
+def _kdt(dt: float, params) -> float:
+    """The step the alpha = 0 kernels take for a physical step dt."""
+    return dt / params.epsilon if getattr(params, "alpha", 0) == 1 else dt
 
 
 def tau_constant(tau) -> Optional[float]:
@@ -84,7 +101,8 @@ def stable_dt_kinetic(grid, params) -> float:
     e = _e_max(params)
     if e > 0.0:
         rate += e / grid.velocity.dv[0]
-    return params.cfl / rate
+    cap = params.cfl / rate
+    return cap * params.epsilon if getattr(params, "alpha", 0) == 1 else cap
 
 
 def fine_schedule(span: float, cap: float) -> list:
@@ -104,8 +122,9 @@ def transport_update(f, dt: float, grid, params, bc) -> Distribution:
     fd = as_device_f(f, ctx)
     E, e_max = rt.to_device_field(params.force, ctx.device, ctx.nx)
     out = ctx.empty_f()
-    rt._lib.check(ctx.lib.pbgk_transport(ctx.h, rt.ptr(fd), rt.ptr(out), float(dt), rt.ptr(E),
-                                         e_max, rt.stream_handle(ctx.device)), "pbgk_transport")
+    rt._lib.check(ctx.lib.pbgk_transport(ctx.h, rt.ptr(fd), rt.ptr(out), float(_kdt(dt, params)),
+                                         rt.ptr(E), e_max, rt.stream_handle(ctx.device)),
+                  "pbgk_transport")
     return Distribution(out)
 
 
@@ -130,14 +149,14 @@ def bgk_relax(f, dt: float, grid, params, bc=None) -> Distribution:
     """Implicit relaxation toward the Maxwellian of f's moments (ref/kinetic.py:127-134)."""
     ctx = rt.ctx_for(grid, bc if bc is not None else "absorbing")
     fd = as_device_f(f, ctx)
-    return Distribution(_relax_dev(ctx, fd, dt, params, ctx.empty_f()))
+    return Distribution(_relax_dev(ctx, fd, _kdt(dt, params), params, ctx.empty_f()))
 
 
 def _run_schedule(ctx, f0, mom0, dts, params, out, want_f=True, mom_out=None):
     """pbgk_propagate over a fixed schedule; returns the status key."""
     tc = tau_constant(params.tau)
     E, e_max = rt.to_device_field(params.force, ctx.device, ctx.nx)
-    arr = (ctypes.c_double * max(len(dts), 1))(*dts)
+    arr = (ctypes.c_double * max(len(dts), 1))(*[_kdt(d, params) for d in dts])
     code = ctypes.c_longlong(-1)
     rt._lib.check(ctx.lib.pbgk_propagate(
         ctx.h, rt.ptr(f0), rt.ptr(mom0), rt.ptr(out), rt.ptr(ctx.f_scratch(0)),
@@ -151,6 +170,7 @@ def _step_by_step(ctx, fd, dts, params):
     E, e_max = rt.to_device_field(params.force, ctx.device, ctx.nx)
     cur = fd
     for s, dt in enumerate(dts, start=1):
+        dt = _kdt(dt, params)
         mid = ctx.empty_f()
         rt._lib.check(ctx.lib.pbgk_transport(ctx.h, rt.ptr(cur), rt.ptr(mid), float(dt), rt.ptr(E),
                                              e_max, rt.stream_handle(ctx.device)), "pbgk_transport")

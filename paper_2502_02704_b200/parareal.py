@@ -34,7 +34,7 @@ import torch
 
 from . import runtime as rt
 from .errors import ConfigurationError
-from .fluid import FluidParams, fluid_batch
+from .fluid import FluidParams, fluid_batch, select_model
 from .kinetic import KineticParams, propagate_window
 from .moments import MomentField
 
@@ -182,6 +182,7 @@ class GpuBackend:
         code = ctypes.c_longlong(-1)
         n_g = len(self.times) - 1
         tarr = (ctypes.c_double * (n_g + 1))(*self.times)
+        select_model(self.ctx, self.fluid)
         rt._lib.check(self.ctx.lib.pbgk_parareal_correct(
             self.ctx.h, n_g, start, rt.ptr(snaps), rt.ptr(old), rt.ptr(jumps), tarr,
             float(self.disc.time.dt_g), float(self.fluid.cfl), rt.ptr(self.force_dev),

@@ -57,6 +57,7 @@ class Ctx:
         self.device = device
         self.bc = int(bc)
         self.periodic = self.bc == 1
+        self.v_max = float(v_max)
         nx, nvx, nvy, nvz = self.shape
         self.dx = (x_max - x_min) / nx
         self.dv = tuple(2.0 * v_max / n for n in (nvx, nvy, nvz))

@@ -263,3 +263,68 @@ def test_blow_up_step_and_degenerate_order():
     assert e.value.step == 1
     with pytest.raises(O.OracleDegenerate):
         O.project(np.zeros((2, 8, 8, 8)), m)
+
+
+# ---------------------------------------------------------------------------
+# 4. oracle EXTENSIONS (self-pinned: no reference counterpart)
+# ---------------------------------------------------------------------------
+
+def test_alpha1_is_the_alpha0_scheme_on_scaled_steps():
+    # diffusive scaling: a physical step d runs transport/relax with d/eps
+    m = O.Mesh(0.0, 1.0, 8, 6.0, (6, 5, 4))
+    rng = np.random.default_rng(3)
+    f = O.lift(rng.uniform(0.5, 1.5, 8), rng.uniform(-0.3, 0.3, (8, 3)), rng.uniform(0.6, 1.4, 8), m)
+    E = 0.4 * np.sin(2 * np.pi * m.xc)
+    eps = 0.05
+    cap1 = O.scaled_cap(m, 0.5, E, eps, 1)
+    assert cap1 == O.fine_cap(m, 0.5, E) * eps
+    t1 = 3.5 * cap1
+    got = O.fine_propagate(f, 0.0, t1, m, eps, True, E, alpha=1)
+    want = f
+    for d in O.fine_schedule(0.0, t1, cap1):
+        want = O.relax(O.transport(want, d / eps, m, True, E), d / eps, m, eps)
+    assert np.array_equal(got, want)
+
+
+def test_drift_diffusion_conserves_mass_and_decays_cosine_mode_exactly():
+    m = O.Mesh(0.0, 1.0, 32, 8.0, (16, 4, 4))
+    D = O.dd_m2(m)
+    assert abs(D - 1.0) < 1e-3  # the unit Maxwellian's v_x variance on a wide grid
+    # periodic, with drift: mass conserved to rounding
+    x = m.xc
+    rho0 = 1.0 + 0.3 * np.cos(2 * np.pi * x)
+    E = 0.5 * np.sin(2 * np.pi * x)
+    r, u, th = O.dd_propagate(rho0, 0.0, 2e-3, m, True, E, None, 0.9, D)
+    assert abs(r.sum() - rho0.sum()) <= 1e-13 * rho0.sum()
+    assert np.all(u == 0.0) and np.all(th == 1.0)
+    # no field: the cosine mode is a discrete eigenvector, amplitude factor
+    # (1 - coef (2 - 2 cos k dx)/dx) per step
+    dx = m.dx
+    k = 2 * np.pi
+    cap = O.dd_cap(dx, D, 0.0, 0.9)
+    t1 = 5.5 * cap
+    r, _, _ = O.dd_propagate(rho0, 0.0, t1, m, True, None, None, 0.9, D)
+    amp = 0.3
+    for d in O.fine_schedule(0.0, t1, cap):
+        amp *= 1.0 - (d * D / dx) * (2.0 - 2.0 * math.cos(k * dx)) / dx
+    assert np.max(np.abs(r - (1.0 + amp * np.cos(k * x)))) <= 1e-13
+    # outflow (zero-gradient ghosts) with no field: also conservative
+    r, _, _ = O.dd_propagate(rho0, 0.0, 1e-3, m, "outflow", None, None, 0.9, D)
+    assert abs(r.sum() - rho0.sum()) <= 1e-13 * rho0.sum()
+
+
+def test_drift_diffusion_guards():
+    m = O.Mesh(0.0, 1.0, 8, 8.0, (8, 4, 4))
+    rho = np.full(8, 1e-3)
+    rho[3] = 1.0
+    # cfl 3 > 1: the explicit step overshoots the spike below zero at step 1
+    with pytest.raises(O.OracleBlowUp) as ei:
+        O.dd_propagate(rho, 0.0, 1.0, m, True, None, None, 3.0, 1.0)
+    assert ei.value.step == 1 and "unphysical" in str(ei.value)
+    bad = rho.copy()
+    bad[5] = np.inf
+    with pytest.raises(O.OracleBlowUp) as ei:
+        O.dd_propagate(bad, 0.0, 1e-3, m, True, None, None, 0.9, 1.0)
+    assert ei.value.step == 1 and "non-finite" in str(ei.value)
+    with pytest.raises(O.OracleConfigError):
+        O.dd_propagate(rho, 1.0, 0.0, m, True)
