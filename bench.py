@@ -49,6 +49,9 @@ def parse():
                     help="override the workload's x boundary")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--schedule", choices=["phased", "pipelined"], default="phased",
+                    help="parareal iteration schedule (pipelined: G jumps + correction on a side "
+                         "stream behind the fine windows; bitwise identical results)")
     return ap.parse_args()
 
 
@@ -157,7 +160,7 @@ def run_ours(args, w, world, rank, local):
     import torch.distributed as dist
     import paper_2502_02704_b200 as P
     from paper_2502_02704_b200 import runtime as rt, _lib
-    from paper_2502_02704_b200.parareal import GpuBackend, ShardedRun
+    from paper_2502_02704_b200.parareal import GpuBackend, PipelinedRun, ShardedRun
 
     dev = torch.device("cuda", local)
     P_, phase, bc, disc, kinetic, fluid = build_problem(w)
@@ -169,7 +172,8 @@ def run_ours(args, w, world, rank, local):
 
     if w.mode == "parareal":
         backend = GpuBackend(disc, kinetic, fluid, dev)
-        run = ShardedRun(backend)
+        pipelined = args.schedule == "pipelined"
+        run = (PipelinedRun if pipelined else ShardedRun)(backend)
         ctx = backend.ctx
         snaps0 = run.coarse_sweep(rt.to_device_moments(U0, dev))
         jumps = backend.empty(w.n_g)
@@ -179,8 +183,11 @@ def run_ours(args, w, world, rank, local):
         def step():
             snaps = snaps0.clone()
             jumps.zero_()
-            run.jumps(snaps, jumps, 1)
-            run.correct(snaps, jumps, 1)
+            if pipelined:
+                run.iterate(snaps, jumps, 1)
+            else:
+                run.jumps(snaps, jumps, 1)
+                run.correct(snaps, jumps, 1)
     else:
         ctx = rt.ctx_for(phase, bc, dev)
         f0 = f_init.device_tensor(dev)
@@ -271,7 +278,7 @@ def e2e_ours(args, w, P, phase, bc, disc, kinetic, fluid, U0, f_init, world, dev
     reps = max(1, min(args.steps, 3))
     if w.mode == "parareal":
         U0h = P.MomentField(U0.rho.copy(), U0.u.copy(), U0.theta.copy())
-        cfg = P.PararealConfig(k_max=1, tol=1e-300)
+        cfg = P.PararealConfig(k_max=1, tol=1e-300, pipelined=args.schedule == "pipelined")
         nx = w.nx
         h2d = 5 * nx * 8 + (nx * 8 if w.force() is not None else 0)
         d2h = (3 * w.n_g + 2) * 5 * nx * 8
@@ -330,6 +337,7 @@ def main():
                 "fine_steps_per_window": w.window_steps(),
                 "parallelism": ("windows sharded over %d rank(s)" % world) if w.mode == "parareal"
                 else ("replicas x%d" % world),
+                "schedule": args.schedule if w.mode == "parareal" else None,
                 "l2": ("inputs larger than L2 (f = %.2f GB); " % (w.cells * 8 / 1e9)) +
                       "256 MiB L2 flush write between timed steps"}
     if args.impl == "reference":

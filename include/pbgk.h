@@ -128,6 +128,31 @@ int pbgk_parareal_correct(pbgk_ctx* ctx, int n_g, int start, double* snaps, cons
  * (rho, u = 0, theta = 1), D = `diffusivity` (> 0). */
 int pbgk_fluid_model(pbgk_ctx* ctx, int model, double diffusivity);
 
+/* ---- pipelined parareal (side stream) ---------------------------------- */
+/* Leave `slots` CTA slots out of the persistent sweep grid (sized for every
+ * slot of every SM), so a side-stream G / correction CTA (launched "lean":
+ * the fewest threads covering nx) is resident beside the sweeps instead of
+ * stalling one of their CTAs.  0 = whole GPU (default). */
+int pbgk_set_grid_reserve(pbgk_ctx* ctx, int slots);
+
+/* pbgk_fluid_propagate without host synchronisation: window times are
+ * device arrays, failure keys are atomicMin-ed into the device word
+ * *d_status (caller initialises it to -1 = clean). */
+int pbgk_fluid_propagate_async(pbgk_ctx* ctx, int nwin, const double* mom_in, double* mom_out,
+                               const double* minuend, const double* d_t0, const double* d_t1,
+                               double dt_max, double cfl, const double* force, void* stream,
+                               long long* d_status);
+
+/* The correction sweep of pbgk_parareal_correct restricted to windows
+ * first..last (1-based, inclusive), asynchronous: d_times are the coarse
+ * times on the device, the sup error is max-accumulated into *d_errmax
+ * (caller zeroes it) and failure keys into *d_status.  Consecutive ranges
+ * give bitwise the result of one full sweep. */
+int pbgk_parareal_correct_range(pbgk_ctx* ctx, int first, int last, double* snaps,
+                                const double* old, const double* jumps, const double* d_times,
+                                double dt_max, double cfl, const double* force, void* stream,
+                                double* d_errmax, long long* d_status);
+
 /* ---- measurement (bench.py) ------------------------------------------- */
 /* Human-readable tiling / launch plan of a context (diagnostics). */
 int pbgk_ctx_describe(const pbgk_ctx* ctx, char* buf, size_t n);

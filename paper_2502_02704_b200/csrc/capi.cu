@@ -27,10 +27,10 @@ cudaError_t launch_finalize(const FinalArgs& a, cudaStream_t st);
 cudaError_t launch_set_key(ErrKey* p, ErrKey v, cudaStream_t st);
 cudaError_t launch_fluid_batch(const FluidArgs& a, int nwin, const double* in, double* out,
                                const double* minuend, const double* t0, const double* t1,
-                               cudaStream_t st);
-cudaError_t launch_correct(const FluidArgs& a, int n_g, int start, double* snaps, const double* old,
+                               cudaStream_t st, bool lean = false);
+cudaError_t launch_correct(const FluidArgs& a, int last, int start, double* snaps, const double* old,
                            const double* jumps, const double* times, double* err_out,
-                           cudaStream_t st);
+                           cudaStream_t st, bool lean = false);
 }  // namespace pbgk
 
 using namespace pbgk;
@@ -79,6 +79,7 @@ struct Plan {
   Tiling t;
   int grid;
   int ns;
+  int per_sm;  // resident CTAs per SM the grid was sized for
 };
 
 struct MapEntry {
@@ -111,6 +112,7 @@ struct EvPair {
 
 struct pbgk_ctx {
   int g_model = 0;       // coarse G: 0 Euler (reference), 1 drift-diffusion (extension)
+  int slot_reserve = 0;  // CTA slots the sweep grid leaves free (pipelined parareal side stream)
   double g_diff = 1.0;   // drift-diffusion D
   pbgk_grid_desc g;
   bool prof = false;
@@ -259,6 +261,7 @@ bool make_plan(pbgk_ctx* c, bool field, Plan& out) {
   long long grid = (long long)c->nsm * per_sm;
   if (grid > items) grid = items;
   out.grid = (int)std::max<long long>(grid, 1);
+  out.per_sm = per_sm;
   return true;
 }
 
@@ -369,7 +372,10 @@ int run_sweep(pbgk_ctx* c, int pid, bool field, const double* in, const double* 
   const size_t smem = sweep_smem_bytes(a, s.V, s.LZ, s.NTHR, synth, s.tma, p.ns);
   const double fbytes = 8.0 * (double)a.plane * a.nx;
   ProfScope ps(c, st, 0, (synth ? 0.0 : fbytes) + (out ? fbytes : 0.0));
-  CK(launch_sweep(p.cfg, *map, a, synth, field, p.grid, p.ns, smem, st));
+  // persistent grid, minus the CTA slots left to side-stream work
+  int grid = p.grid;
+  if (c->slot_reserve > 0) grid = std::max(1, std::min(grid, c->nsm * p.per_sm - c->slot_reserve));
+  CK(launch_sweep(p.cfg, *map, a, synth, field, grid, p.ns, smem, st));
   return 0;
 }
 
@@ -696,6 +702,44 @@ int pbgk_parareal_correct(pbgk_ctx* c, int n_g, int start, double* snaps, const 
   if (fetch_err(c, st, &code)) return -1;
   if (h_code) *h_code = code;
   if (h_err) *h_err = c->h_dbl[0];
+  return 0;
+}
+
+int pbgk_set_grid_reserve(pbgk_ctx* c, int slots) {
+  if (!c) return fail("pbgk_set_grid_reserve: null context");
+  if (slots < 0 || slots >= c->nsm) return fail("pbgk_set_grid_reserve: need 0 <= slots < SM count");
+  c->slot_reserve = slots;
+  return 0;
+}
+
+int pbgk_fluid_propagate_async(pbgk_ctx* c, int nwin, const double* mom_in, double* mom_out,
+                               const double* minuend, const double* d_t0, const double* d_t1,
+                               double dt_max, double cfl, const double* force, void* stream,
+                               long long* d_status) {
+  if (!c || !mom_in || !mom_out || !d_t0 || !d_t1 || !d_status)
+    return fail("pbgk_fluid_propagate_async: null argument");
+  if (cudaSetDevice(c->dev) != cudaSuccess) return fail("cudaSetDevice");
+  if (nwin <= 0) return 0;
+  FluidArgs a{c->g.nx, c->dx, c->g.bc == 1 ? 1 : 0, dt_max, cfl, force,
+              reinterpret_cast<ErrKey*>(d_status), c->g_model, c->g_diff};
+  ++g_launches;
+  CK(launch_fluid_batch(a, nwin, mom_in, mom_out, minuend, d_t0, d_t1, (cudaStream_t)stream, true));
+  return 0;
+}
+
+int pbgk_parareal_correct_range(pbgk_ctx* c, int first, int last, double* snaps, const double* old,
+                                const double* jumps, const double* d_times, double dt_max,
+                                double cfl, const double* force, void* stream, double* d_errmax,
+                                long long* d_status) {
+  if (!c || !snaps || !old || !jumps || !d_times || !d_errmax || !d_status)
+    return fail("pbgk_parareal_correct_range: null argument");
+  if (cudaSetDevice(c->dev) != cudaSuccess) return fail("cudaSetDevice");
+  if (first < 1) return fail("pbgk_parareal_correct_range: first < 1");
+  if (last < first) return 0;
+  FluidArgs a{c->g.nx, c->dx, c->g.bc == 1 ? 1 : 0, dt_max, cfl, force,
+              reinterpret_cast<ErrKey*>(d_status), c->g_model, c->g_diff};
+  ++g_launches;
+  CK(launch_correct(a, last, first, snaps, old, jumps, d_times, d_errmax, (cudaStream_t)stream, true));
   return 0;
 }
 

@@ -295,8 +295,11 @@ __global__ void __launch_bounds__(1024) fluid_batch_kernel(FluidArgs a, const do
 }
 
 // Sequential correction sweep (one CTA): U_n = G(U_{n-1}) + jump_n for
-// n = start..n_g, overshoot guard, sup error (ref/parareal.py:226-248).
-__global__ void __launch_bounds__(1024) correct_kernel(FluidArgs a, int n_g, int start, double* snaps,
+// n = start..last, overshoot guard, sup error (ref/parareal.py:226-248).
+// The error is max-accumulated into *err_out (non-negative doubles order as
+// their bit patterns), so a sweep split into consecutive ranges gives the
+// same value as one launch.
+__global__ void __launch_bounds__(1024) correct_kernel(FluidArgs a, int last, int start, double* snaps,
                                                        const double* old, const double* jumps,
                                                        const double* times, double* err_out) {
   extern __shared__ double V[];
@@ -310,7 +313,7 @@ __global__ void __launch_bounds__(1024) correct_kernel(FluidArgs a, int n_g, int
     over = 0;
   }
   __syncthreads();
-  for (int n = start; n <= n_g; ++n) {
+  for (int n = start; n <= last; ++n) {
     const double* src = snaps + (size_t)(n - 1) * 5 * nx;
     load_window(a, src, V);
     __syncthreads();
@@ -362,19 +365,25 @@ __global__ void __launch_bounds__(1024) correct_kernel(FluidArgs a, int n_g, int
     }
   }
   emax = block_max(emax, red);
-  if (threadIdx.x == 0) *err_out = emax;
+  if (threadIdx.x == 0)
+    atomicMax(reinterpret_cast<unsigned long long*>(err_out),
+              (unsigned long long)__double_as_longlong(emax));
 }
 
-static int fluid_threads(int nx) {
+// Threads of a G CTA: one per cell up to 1024; `lean` (side-stream launches
+// that must fit next to a sweep CTA): the fewest covering nx at
+// kMaxCellsPerThread cells each.
+static int fluid_threads(int nx, bool lean = false) {
   int t = 32;
-  while (t < nx && t < 1024) t <<= 1;
+  const int need = lean ? (nx + kMaxCellsPerThread - 1) / kMaxCellsPerThread : nx;
+  while (t < need && t < 1024) t <<= 1;
   return t;
 }
 
 cudaError_t launch_fluid_batch(const FluidArgs& a, int nwin, const double* in, double* out,
                                const double* minuend, const double* t0, const double* t1,
-                               cudaStream_t st) {
-  const int thr = fluid_threads(a.nx);
+                               cudaStream_t st, bool lean) {
+  const int thr = fluid_threads(a.nx, lean);
   if ((size_t)thr * kMaxCellsPerThread < (size_t)a.nx) return cudaErrorInvalidValue;
   const size_t smem = (size_t)5 * a.nx * sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(fluid_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -384,16 +393,16 @@ cudaError_t launch_fluid_batch(const FluidArgs& a, int nwin, const double* in, d
   return cudaGetLastError();
 }
 
-cudaError_t launch_correct(const FluidArgs& a, int n_g, int start, double* snaps, const double* old,
+cudaError_t launch_correct(const FluidArgs& a, int last, int start, double* snaps, const double* old,
                            const double* jumps, const double* times, double* err_out,
-                           cudaStream_t st) {
-  const int thr = fluid_threads(a.nx);
+                           cudaStream_t st, bool lean) {
+  const int thr = fluid_threads(a.nx, lean);
   if ((size_t)thr * kMaxCellsPerThread < (size_t)a.nx) return cudaErrorInvalidValue;
   const size_t smem = (size_t)5 * a.nx * sizeof(double);
   cudaError_t e =
       cudaFuncSetAttribute(correct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  correct_kernel<<<1, thr, smem, st>>>(a, n_g, start, snaps, old, jumps, times, err_out);
+  correct_kernel<<<1, thr, smem, st>>>(a, last, start, snaps, old, jumps, times, err_out);
   return cudaGetLastError();
 }
 

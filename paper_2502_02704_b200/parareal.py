@@ -41,7 +41,7 @@ from .moments import MomentField
 __all__ = ["PararealConfig", "ConvergenceRecord", "ParTrajectory", "WorkRange",
            "initial_coarse_sweep", "compute_jumps", "sequential_correction", "run_parareal",
            "fine_moment_chain", "work_distribution", "parareal_cost", "estimate_k_opt",
-           "make_executor", "GpuBackend", "ShardedRun"]
+           "make_executor", "GpuBackend", "ShardedRun", "PipelinedRun"]
 
 
 @dataclass
@@ -56,6 +56,7 @@ class PararealConfig:
     tol: float
     use_frozen_prefix: bool = True
     workers: int = 1
+    pipelined: bool = False  # extension: overlap G / correction with the fine windows
 
     def __post_init__(self):
         if self.k_max < 1:
@@ -190,6 +191,85 @@ class GpuBackend:
             "pbgk_parareal_correct")
         return e.value, code.value
 
+    # -- pipelined mode (PipelinedRun): F on the current stream, the G jumps
+    # and the correction on a side stream that trails the fine windows --------
+    def fine_into(self, src: torch.Tensor, n: int, out: torch.Tensor) -> int:
+        """out = P F L(src) of window n on the current stream; returns the status key."""
+        t = self.times
+        tic = time.perf_counter()
+        c = propagate_window(self.ctx, src, t[n - 1], t[n], self.disc.phase, self.kinetic,
+                             self.disc.time.dt_f, out)
+        self.t_kin = max(self.t_kin, time.perf_counter() - tic)
+        return c
+
+    def side_begin(self, snaps: torch.Tensor) -> torch.Tensor:
+        """Start an iteration: old = snaps (main stream); side stream state reset."""
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(self.device, priority=-1)
+            self._dtimes = torch.tensor(self.times, dtype=torch.float64, device=self.device)
+            n_g = len(self.times) - 1
+            self._gstat = torch.empty(n_g, dtype=torch.int64, device=self.device)
+            self._cstat = torch.empty(1, dtype=torch.int64, device=self.device)
+            self._emax = torch.empty(1, dtype=torch.float64, device=self.device)
+            self._ring = [None, None]
+            self._free = [None, None]
+        main = torch.cuda.current_stream(self.device)
+        old = snaps.clone()
+        self._side.wait_stream(main)
+        with torch.cuda.stream(self._side):
+            self._gstat.fill_(-1)
+            self._cstat.fill_(-1)
+            self._emax.zero_()
+        rt._lib.check(self.ctx.lib.pbgk_set_grid_reserve(self.ctx.h, 1), "pbgk_set_grid_reserve")
+        select_model(self.ctx, self.fluid)
+        return old
+
+    def round_slot(self, r: int, nslots: int) -> torch.Tensor:
+        """Buffer for the fine outputs of round r (ring of two; waits until the
+        side stream has consumed the round that used it before)."""
+        i = r & 1
+        buf = self._ring[i]
+        if buf is None or buf.shape[0] < nslots:
+            buf = self._ring[i] = torch.empty((nslots, 5, self.nx), dtype=torch.float64,
+                                              device=self.device)
+        if self._free[i] is not None:
+            torch.cuda.current_stream(self.device).wait_event(self._free[i])
+        return buf
+
+    def side_round(self, r: int, fine: torch.Tensor, windows: List[int], snaps, old, jumps):
+        """Side stream, after everything queued so far on the main stream:
+        jumps[n-1] = fine[q] - G(old[n-1]) for each window n = windows[q], then
+        the correction U_n = G(U_{n-1}) + jumps[n-1] over the round's windows."""
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.device))
+        side = self._side
+        side.wait_event(ev)
+        lib, h = self.ctx.lib, self.ctx.h
+        sh = side.cuda_stream
+        dt_g, cfl = float(self.disc.time.dt_g), float(self.fluid.cfl)
+        force = rt.ptr(self.force_dev)
+        dt = self._dtimes
+        for q, n in enumerate(windows):
+            rt._lib.check(lib.pbgk_fluid_propagate_async(
+                h, 1, rt.ptr(old[n - 1]), rt.ptr(jumps[n - 1]), rt.ptr(fine[q]),
+                rt.ptr(dt[n - 1:]), rt.ptr(dt[n:]), dt_g, cfl, force, ctypes.c_void_p(sh),
+                rt.ptr(self._gstat[n - 1:])), "pbgk_fluid_propagate_async")
+        if windows:
+            rt._lib.check(lib.pbgk_parareal_correct_range(
+                h, windows[0], windows[-1], rt.ptr(snaps), rt.ptr(old), rt.ptr(jumps), rt.ptr(dt),
+                dt_g, cfl, force, ctypes.c_void_p(sh), rt.ptr(self._emax), rt.ptr(self._cstat)),
+                "pbgk_parareal_correct_range")
+        free = torch.cuda.Event()
+        free.record(side)
+        self._free[r & 1] = free
+
+    def side_finish(self):
+        """Wait for the side stream; (sup error, G-jump keys per window, correction key)."""
+        self._side.synchronize()
+        torch.cuda.current_stream(self.device).wait_stream(self._side)
+        rt._lib.check(self.ctx.lib.pbgk_set_grid_reserve(self.ctx.h, 0), "pbgk_set_grid_reserve")
+        return (float(self._emax.item()), self._gstat.cpu().tolist(), int(self._cstat.item()))
+
 
 def _raise_window_status(status):
     """Raise the reference's exception for the first failing window."""
@@ -271,6 +351,66 @@ class ShardedRun:
         old = snaps.clone()
         err, code = self.b.correct(snaps, old, jumps, start)
         rt.raise_fluid(code)
+        return old, err
+
+
+class PipelinedRun(ShardedRun):
+    """Iteration k with the coarse work trailing the fine windows (SURVEY.md
+    8(f) rank 1).  Windows k..n_g are dealt CYCLICALLY to the ranks, one per
+    rank per round; after each round the fine outputs are all-gathered and
+    every rank queues, on a side stream, the round's G jumps and the
+    correction of those windows -- which needs only the previous windows'
+    corrections and the round's jumps -- while its next fine window runs.
+    Only the last round's coarse work is exposed.  Every value is computed
+    from the same inputs by the same kernels as in the phased ShardedRun, so
+    trajectories are bitwise identical; no work is speculative (iteration
+    k+1 starts after the correction of iteration k, as the reference's stop
+    test requires).  Failure precedence is the phased one: the first failing
+    window of the fine stage (F, then its G jump), then the correction.
+    """
+
+    def iterate(self, snaps: torch.Tensor, jumps: torch.Tensor, start: int):
+        b = self.b
+        N = self.world
+        old = b.side_begin(snaps)
+        windows = list(range(start, self.n_g + 1))
+        rounds = [windows[i:i + N] for i in range(0, len(windows), N)]
+        fstat = {}
+        dist = torch.distributed
+        for r, wr in enumerate(rounds):
+            mine = wr[self.rank] if self.rank < len(wr) else None
+            if N == 1:
+                buf = b.round_slot(r, 1)
+                fstat[mine] = b.fine_into(old[mine - 1], mine, buf[0])
+                b.side_round(r, buf, wr, snaps, old, jumps)
+                continue
+            local = b.empty(1)
+            code = -1
+            if mine is not None:
+                code = b.fine_into(old[mine - 1], mine, local[0])
+            else:
+                local.zero_()
+            word = torch.tensor([code], dtype=torch.int64).to(local.device).view(torch.float64)
+            payload = torch.cat([local.reshape(-1), word])
+            flat = torch.empty(N * payload.numel(), dtype=torch.float64, device=payload.device)
+            dist.all_gather_into_tensor(flat, payload, group=self.group)
+            g = flat.view(N, payload.numel())
+            nj = 5 * b.nx
+            buf = b.round_slot(r, N)
+            buf[:N].copy_(g[:, :nj].view(N, 5, b.nx))
+            words = g[:, nj:].contiguous().view(torch.int64).cpu().tolist()
+            for q, n in enumerate(wr):
+                fstat[n] = words[q][0]
+            b.side_round(r, buf, wr, snaps, old, jumps)
+        err, gstat, cstat = b.side_finish()
+        status = []
+        for n in windows:
+            c = fstat[n]
+            if c < 0 and gstat[n - 1] >= 0:
+                c = ("G", gstat[n - 1] & ~(0xFFFFFF << 40))  # unit: the batch index 0
+            status.append(c)
+        _raise_window_status(status)
+        rt.raise_fluid(cstat)
         return old, err
 
 
@@ -356,7 +496,7 @@ def run_parareal(U0: MomentField, config: PararealConfig, disc, kinetic: Kinetic
     (bitwise) trajectory.
     """
     b = backend or GpuBackend(disc, kinetic, fluid)
-    run = ShardedRun(b, group)
+    run = (PipelinedRun if config.pipelined else ShardedRun)(b, group)
     n_g = disc.time.n_g
     U0d = rt.to_device_moments(U0, b.device) if b.device.type == "cuda" else \
         torch.from_numpy(rt.pack_moments_np(U0.rho, U0.u, U0.theta))
@@ -369,7 +509,9 @@ def run_parareal(U0: MomentField, config: PararealConfig, disc, kinetic: Kinetic
     for k in range(1, config.k_max + 1):
         tic = time.perf_counter()
         start = k if config.use_frozen_prefix else 1
-        if start <= n_g:
+        if start <= n_g and config.pipelined:
+            prev, err = run.iterate(snaps, jumps, start)
+        elif start <= n_g:
             run.jumps(snaps, jumps, start)
             prev, err = run.correct(snaps, jumps, start)
         else:

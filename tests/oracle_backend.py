@@ -63,3 +63,48 @@ class OracleBackend:
             err = max(err, O.sup_gap(cor, unpack(old[n])))
             snaps[n] = pack(cor)
         return err, -1
+
+    # -- pipelined interface (PipelinedRun), synchronous on the CPU ----------
+    def fine_into(self, src, n, out):
+        self.windows_done.append(n)
+        if n == self.fail_window:
+            out.fill_(float("nan"))
+            return key(0, 2, 2)  # BlowUpError(step=2)
+        out.copy_(pack(O.PFL(self.prob, unpack(src), n)))
+        return -1
+
+    def side_begin(self, snaps):
+        self._gst = [-1] * (len(self.times) - 1)
+        self._cst = -1
+        self._emax = 0.0
+        return snaps.clone()
+
+    def round_slot(self, r, nslots):
+        return torch.empty((nslots, 5, self.nx), dtype=torch.float64)
+
+    def side_round(self, r, fine, windows, snaps, old, jumps):
+        for q, n in enumerate(windows):
+            try:
+                G = O.G(self.prob, unpack(old[n - 1]), n)
+            except O.OracleError:
+                self._gst[n - 1] = key(0, 1, 2)
+                continue
+            jumps[n - 1] = pack(O._sub(unpack(fine[q]), G))
+        for n in windows:
+            if self._cst >= 0:
+                return
+            try:
+                Gn = O.G(self.prob, unpack(snaps[n - 1]), n)
+            except O.OracleError:
+                self._cst = key(n, 1, 3)
+                return
+            cor = O._add(Gn, unpack(jumps[n - 1]))
+            ok = all(np.all(np.isfinite(x)) for x in cor)
+            if not ok or np.any(cor[0] <= 0.0) or np.any(cor[2] <= 0.0):
+                self._cst = key(n, 0, 4)
+                return
+            self._emax = max(self._emax, O.sup_gap(cor, unpack(old[n])))
+            snaps[n] = pack(cor)
+
+    def side_finish(self):
+        return self._emax, list(self._gst), self._cst

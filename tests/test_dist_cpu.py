@@ -36,7 +36,7 @@ def _disc(P):
     return P.Discretization(g, P.build_time_grids(0.04, 5, 10), P.BoundaryKind.ABSORBING)
 
 
-def _worker(rank, world, port, frozen, fail_window, q):
+def _worker(rank, world, port, frozen, fail_window, q, pipelined=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -47,7 +47,8 @@ def _worker(rank, world, port, frozen, fail_window, q):
         U0 = O.two_state(prob.mesh, 0.5, (1.0, 0.0, 1.0), (0.125, 0.0, 0.8))
         be = OracleBackend(prob, fail_window)
         try:
-            traj, rec = P.run_parareal(P.MomentField(*U0), P.PararealConfig(3, 1e-300, frozen),
+            traj, rec = P.run_parareal(P.MomentField(*U0),
+                                       P.PararealConfig(3, 1e-300, frozen, pipelined=pipelined),
                                        _disc(P), P.KineticParams(1e-2), P.FluidParams(),
                                        backend=be)
             out = ("ok", [np.stack([s.rho, s.theta]) for s in traj.snapshots],
@@ -61,11 +62,11 @@ def _worker(rank, world, port, frozen, fail_window, q):
         dist.destroy_process_group()
 
 
-def _run(world, frozen=True, fail_window=None):
+def _run(world, frozen=True, fail_window=None, pipelined=False):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, frozen, fail_window, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, frozen, fail_window, q, pipelined))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -84,9 +85,10 @@ def _serial(frozen=True):
 
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("frozen", [True, False])
-def test_sharded_parareal_bitwise_equals_serial(world, frozen):
+@pytest.mark.parametrize("pipelined", [False, True])
+def test_sharded_parareal_bitwise_equals_serial(world, frozen, pipelined):
     snaps, errs = _serial(frozen)
-    res = _run(world, frozen)
+    res = _run(world, frozen, pipelined=pipelined)
     first = None
     all_windows = []
     for rank in range(world):
@@ -105,8 +107,24 @@ def test_sharded_parareal_bitwise_equals_serial(world, frozen):
     assert sorted(all_windows) == expect
 
 
-def test_sharded_failure_raises_same_error_on_every_rank():
-    res = _run(2, fail_window=4)
+@pytest.mark.parametrize("pipelined", [False, True])
+def test_sharded_failure_raises_same_error_on_every_rank(pipelined):
+    res = _run(2, fail_window=4, pipelined=pipelined)
     for rank in range(2):
         status, name, step, sl, _ = res[rank]
         assert status == "err" and name == "BlowUpError" and step == 2
+
+
+@pytest.mark.parametrize("frozen", [True, False])
+def test_pipelined_single_process_bitwise_equals_serial(frozen):
+    import paper_2502_02704_b200 as P
+    from oracle_backend import OracleBackend
+    snaps, errs = _serial(frozen)
+    prob = _problem()
+    U0 = O.two_state(prob.mesh, 0.5, (1.0, 0.0, 1.0), (0.125, 0.0, 0.8))
+    be = OracleBackend(prob)
+    traj, rec = P.run_parareal(P.MomentField(*U0), P.PararealConfig(3, 1e-300, frozen, pipelined=True),
+                               _disc(P), P.KineticParams(1e-2), P.FluidParams(), backend=be)
+    assert [r.error for r in rec] == errs
+    for a, s in zip(traj.snapshots, snaps):
+        assert np.array_equal(a.rho, s[0]) and np.array_equal(a.u, s[1]) and np.array_equal(a.theta, s[2])
