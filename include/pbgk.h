@@ -128,6 +128,13 @@ int pbgk_parareal_correct(pbgk_ctx* ctx, int n_g, int start, double* snaps, cons
  * (rho, u = 0, theta = 1), D = `diffusivity` (> 0). */
 int pbgk_fluid_model(pbgk_ctx* ctx, int model, double diffusivity);
 
+/* x transport of every sweep on this context: 0 = the reference's first-order
+ * upwind flux (default); 1 = MUSCL reconstruction with the minmod limiter
+ * (EXTENSION: BASELINE north_star "upwind/MUSCL", PAPER flux limiters;
+ * no reference counterpart; two ghost planes per side by the x boundary).
+ * MUSCL has no v_x field term: sweeps with E != 0 fail on a MUSCL context. */
+int pbgk_set_x_scheme(pbgk_ctx* ctx, int scheme);
+
 /* ---- pipelined parareal (side stream) ---------------------------------- */
 /* Leave `slots` CTA slots out of the persistent sweep grid (sized for every
  * slot of every SM), so a side-stream G / correction CTA (launched "lean":

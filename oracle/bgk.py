@@ -217,6 +217,41 @@ def transport(f: np.ndarray, dt: float, mesh: Mesh, periodic, force=None) -> np.
     return out
 
 
+def minmod(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """0 where a, b differ in sign (or one is 0), else the smaller magnitude with their sign."""
+    return np.where(a * b > 0.0, np.sign(a) * np.minimum(np.abs(a), np.abs(b)), 0.0)
+
+
+def transport_muscl(f: np.ndarray, dt: float, mesh: Mesh, periodic) -> np.ndarray:
+    """Second-order x transport (ORACLE EXTENSION; BASELINE north_star's
+    "upwind/MUSCL", PAPER's flux limiters): MUSCL reconstruction with the
+    minmod limiter, upwind face states, forward Euler, on the reference's
+    flux form (ref/kinetic.py:110-112 with g -> reconstructed face states):
+        s_j = minmod(g_j - g_{j-1}, g_{j+1} - g_j),
+        F_{j+1/2} = max(c,0) (g_j + s_j/2) + min(c,0) (g_{j+1} - s_{j+1}/2),
+        f* = f - (dt/dx)(F_{i+1/2} - F_{i-1/2}).
+    Two ghost planes per side: periodic wrap, zero (absorbing) or copies of
+    the edge plane (outflow).  No v_x field term (upwind only)."""
+    kind = bc_kind(periodic)
+    nx = f.shape[0]
+    c = mesh.vc[0]
+    cpos = np.maximum(c, 0.0)[None, :, None, None]
+    cneg = np.minimum(c, 0.0)[None, :, None, None]
+    g = np.empty((nx + 4,) + f.shape[1:])
+    g[2:-2] = f
+    if kind == "periodic":
+        g[0], g[1], g[-2], g[-1] = f[-2], f[-1], f[0], f[1]
+    elif kind == "outflow":
+        g[0], g[1], g[-2], g[-1] = f[0], f[0], f[-1], f[-1]
+    else:
+        g[0] = g[1] = g[-2] = g[-1] = 0.0
+    sl = minmod(g[1:-1] - g[:-2], g[2:] - g[1:-1])  # slopes of g[1..nx+2]
+    gL = g[1:-2] + 0.5 * sl[:-1]  # left state of faces g[1]|g[2] .. g[nx+1]|g[nx+2]
+    gR = g[2:-1] - 0.5 * sl[1:]   # right state of the same faces
+    fl = cpos * gL + cneg * gR
+    return f - (dt / mesh.dx) * (fl[1:] - fl[:-1])
+
+
 def unit_tau(rho, theta):
     """Default collision frequency (ref/kinetic.py:42-44)."""
     return 1.0
@@ -254,7 +289,8 @@ def scaled_cap(mesh: Mesh, cfl: float, force, eps: float, alpha: int) -> float:
 
 def fine_propagate(f0: np.ndarray, t0: float, t1: float, mesh: Mesh,
                    eps: float, periodic: bool, force=None, dt_max=None,
-                   cfl: float = 0.5, tau: Callable = unit_tau, alpha: int = 0) -> np.ndarray:
+                   cfl: float = 0.5, tau: Callable = unit_tau, alpha: int = 0,
+                   scheme: str = "upwind") -> np.ndarray:
     """F over [t0, t1] (ref/kinetic.py:137-161).
 
     ``alpha = 1`` is an ORACLE EXTENSION (unpinned; the reference has only
@@ -272,7 +308,12 @@ def fine_propagate(f0: np.ndarray, t0: float, t1: float, mesh: Mesh,
     for s, d in enumerate(fine_schedule(t0, t1, cap), start=1):
         if alpha == 1:
             d = d / eps
-        f = transport(f, d, mesh, periodic, force)
+        if scheme == "muscl":
+            if field_bound(force) > 0.0:
+                raise OracleConfigError("MUSCL x transport has no field term")
+            f = transport_muscl(f, d, mesh, periodic)
+        else:
+            f = transport(f, d, mesh, periodic, force)
         f = relax(f, d, mesh, eps, tau)
         if not np.all(np.isfinite(f)):
             raise OracleBlowUp("non-finite at step %d" % s, step=s)
@@ -466,6 +507,7 @@ class Problem:
     tau: Callable = unit_tau
     alpha: int = 0                 # 1: diffusive scaling (ORACLE EXTENSION)
     g_model: str = "euler"         # "drift_diffusion": dd_propagate (ORACLE EXTENSION)
+    scheme: str = "upwind"         # "muscl": transport_muscl (ORACLE EXTENSION)
     diffusivity: Optional[float] = None  # D of the drift-diffusion G (default m2 / 1)
 
     @property
@@ -498,7 +540,7 @@ def PFL(prob: Problem, U, n: int):
     f = lift(*U, prob.mesh, normalize=False)
     f = fine_propagate(f, float(t[n - 1]), float(t[n]), prob.mesh, prob.eps,
                        prob.periodic, prob.force, prob.dt_f, prob.cfl_kin,
-                       prob.tau, prob.alpha)
+                       prob.tau, prob.alpha, prob.scheme)
     return project(f, prob.mesh)
 
 

@@ -46,6 +46,7 @@ PROTOTYPES = {
     "pbgk_check_finite": (c_int, [_P, _P, _I, _P, _CODE]),
     "pbgk_fluid_model": (c_int, [_P, _I, _D]),
     "pbgk_set_grid_reserve": (c_int, [_P, _I]),
+    "pbgk_set_x_scheme": (c_int, [_P, _I]),
     "pbgk_fluid_propagate_async": (c_int, [_P, _I, _P, _P, _P, _P, _P, _D, _D, _P, _P, _P]),
     "pbgk_parareal_correct_range": (c_int, [_P, _I, _I, _P, _P, _P, _P, _D, _D, _P, _P, _P, _P]),
     "pbgk_parareal_correct": (c_int, [_P, _I, _I, _P, _P, _P, POINTER(c_double), _D, _D, _P,

@@ -112,6 +112,7 @@ struct EvPair {
 
 struct pbgk_ctx {
   int g_model = 0;       // coarse G: 0 Euler (reference), 1 drift-diffusion (extension)
+  int x_scheme = 0;      // 0 first-order upwind (reference), 1 MUSCL-minmod (extension)
   int slot_reserve = 0;  // CTA slots the sweep grid leaves free (pipelined parareal side stream)
   double g_diff = 1.0;   // drift-diffusion D
   pbgk_grid_desc g;
@@ -366,6 +367,8 @@ int run_sweep(pbgk_ctx* c, int pid, bool field, const double* in, const double* 
   a.half_emax = half_emax;
   a.dtdv = dtdv;
   a.check_step = check_step;
+  a.muscl = (c->x_scheme == 1 && dtdx != 0.0) ? 1 : 0;
+  if (a.muscl && field) return fail("MUSCL x transport has no v_x field term (use the upwind scheme)");
   const bool synth = (in == nullptr);
   const CUtensorMap* map = tensor_map(c, synth ? nullptr : in, p.t, p.cfg);
   if (!map) return fail("tensor map: " + g_last_error);
@@ -702,6 +705,13 @@ int pbgk_parareal_correct(pbgk_ctx* c, int n_g, int start, double* snaps, const 
   if (fetch_err(c, st, &code)) return -1;
   if (h_code) *h_code = code;
   if (h_err) *h_err = c->h_dbl[0];
+  return 0;
+}
+
+int pbgk_set_x_scheme(pbgk_ctx* c, int scheme) {
+  if (!c) return fail("pbgk_set_x_scheme: null context");
+  if (scheme != 0 && scheme != 1) return fail("pbgk_set_x_scheme: scheme must be 0 (upwind) or 1 (MUSCL)");
+  c->x_scheme = scheme;
   return 0;
 }
 

@@ -60,6 +60,7 @@ struct SweepArgs {
   double* part;
   ErrKey* err;
   int check_step;    // >0: flag non-finite f_pre as step `check_step`
+  int muscl;         // 1: MUSCL (minmod) x transport instead of first-order upwind
   int debug;         // development ablations (PBGK_DEBUG): 1 no reductions, 2 no CTA barrier
 };
 

@@ -103,47 +103,76 @@ __device__ __forceinline__ TileGeom tile_geom(const Tiling& t, int nvx, int tile
 }
 
 // Walks the items of a segment [g0, g1) of the (tile, position) sequence:
-// every run of consecutive positions of one tile is preceded by its halo
-// (the upwind neighbour plane of the run's first plane).
+// every run of consecutive positions of one tile is preceded by LEAD halo
+// items (its upwind neighbour planes: 1 for upwind, 2 for MUSCL) and, with
+// TRAIL, followed by one look-ahead item (MUSCL's downwind neighbour of the
+// run's last plane).  Item kinds: lead halo, first / later plane of the run,
+// trail.  Positions of halo / trail items may fall outside [0, nx).
+enum ItemKind : int { kLead = 0, kFirst = 1, kNormal = 2, kTrail = 3 };
+
+template <int LEAD, int TRAIL>
 struct ItemIter {
   int g, g1;    // next plane-item index (global linear) and segment end
   int tile, p;  // tile and position of g
-  bool halo_next;
+  int lead_left;
+  bool first;
+  bool trail_next;
+  int trail_tile, trail_p;
 
   __device__ __forceinline__ void init(int g0, int end, int nx) {
     g = g0;
     g1 = end;
     tile = g0 / nx;
     p = g0 - tile * nx;
-    halo_next = g0 < end;
+    lead_left = g0 < end ? LEAD : 0;
+    first = true;
+    trail_next = false;
   }
-  __device__ __forceinline__ bool done() const { return g >= g1 && !halo_next; }
-  // current item: (tile, p, halo); then advance
-  __device__ __forceinline__ void next(int nx, int& t_out, int& p_out, bool& halo_out) {
-    t_out = tile;
-    p_out = p;
-    halo_out = halo_next;
-    if (halo_next) {
-      halo_next = false;
+  __device__ __forceinline__ bool done() const { return g >= g1 && lead_left == 0 && !trail_next; }
+  // current item: (tile, position, kind); then advance
+  __device__ __forceinline__ void next(int nx, int& t_out, int& p_out, int& kind) {
+    if (TRAIL && trail_next) {
+      t_out = trail_tile;
+      p_out = trail_p;
+      kind = kTrail;
+      trail_next = false;
       return;
     }
+    t_out = tile;
+    if (lead_left > 0) {
+      p_out = p - lead_left;
+      kind = kLead;
+      --lead_left;
+      return;
+    }
+    p_out = p;
+    kind = first ? kFirst : kNormal;
+    first = false;
     ++g;
-    if (++p == nx) {
-      p = 0;
-      ++tile;
-      halo_next = g < g1;
+    if (++p == nx || g >= g1) {  // end of this run
+      if (TRAIL) {
+        trail_next = true;
+        trail_tile = tile;
+        trail_p = p;
+      }
+      if (p == nx) {
+        p = 0;
+        ++tile;
+      }
+      if (g < g1) {
+        lead_left = LEAD;
+        first = true;
+      }
     }
   }
 };
 
-// x cell loaded for an item; -1 = absorbing ghost (f_pre == 0).  Ghost
-// planes: periodic wrap, zero-gradient copy (outflow) or zero (absorbing).
-__device__ __forceinline__ int item_plane(int nx, int bc, const TileGeom& tg, int p, bool halo) {
+// x cell of march position p of a tile (p may be outside [0, nx) for halo /
+// trail items); -1 = absorbing ghost (f == 0).  Ghost planes: periodic wrap,
+// zero-gradient copy of the edge plane (outflow) or zero (absorbing).
+__device__ __forceinline__ int item_plane(int nx, int bc, const TileGeom& tg, int p) {
   int i = tg.down ? nx - 1 - p : p;
-  if (halo) {
-    i += tg.down ? 1 : -1;
-    if (i < 0 || i >= nx) i = (bc == 1) ? (i + nx) % nx : (bc == 2 ? (i < 0 ? 0 : nx - 1) : -1);
-  }
+  if (i < 0 || i >= nx) i = (bc == 1) ? ((i % nx) + nx) % nx : (bc == 2 ? (i < 0 ? 0 : nx - 1) : -1);
   return i;
 }
 
@@ -185,9 +214,11 @@ __device__ __forceinline__ void lds_vec(const double* p, double (&x)[V]) {
   }
 }
 
-template <int V, int LZ, int K, int NTHR, int MINB, bool SYNTH, bool FIELD, bool TMA>
+template <int V, int LZ, int K, int NTHR, int MINB, bool SYNTH, bool FIELD, bool TMA, bool MUSCL>
 __global__ void __launch_bounds__(NTHR, MINB)
     sweep_kernel(const __grid_constant__ CUtensorMap fmap, const SweepArgs a, int ns) {
+  static_assert(!(MUSCL && FIELD), "MUSCL x transport has no v_x field term");
+  constexpr int LEAD = MUSCL ? 2 : 1, TRAIL = MUSCL ? 1 : 0;
   constexpr int NL = NTHR / LZ;  // line groups
   constexpr int NW = NTHR / 32;
   constexpr int BZ = LZ * V;
@@ -233,21 +264,20 @@ __global__ void __launch_bounds__(NTHR, MINB)
   // producer: lane 0 of the LAST warp (the first warps carry the per-plane
   // partial sums), with the tile geometry cached across its run
   const int ptid = NTHR - 32;
-  ItemIter prod;
+  ItemIter<LEAD, TRAIL> prod;
   prod.init(g0, g1, nx);
   int pstg = 0;  // ring stage of the next issue
   int ptile = -1;
   TileGeom ptg{};
   auto issue_next = [&]() {
-    int t, p;
-    bool h;
+    int t, p, h;
     prod.next(nx, t, p, h);
     if (t != ptile) {
       ptile = t;
       ptg = tile_geom(T, a.nvx, t);
     }
     const TileGeom& tg = ptg;
-    const int i = item_plane(nx, a.bc, tg, p, h);
+    const int i = item_plane(nx, a.bc, tg, p);
     const int s = pstg;
     if (++pstg == ns) pstg = 0;
     uint64_t* bar = &bars[s];
@@ -312,16 +342,18 @@ __global__ void __launch_bounds__(NTHR, MINB)
   for (int k = 0; k < K; ++k)
 #pragma unroll
     for (int v = 0; v < V; ++v) prev[k][v] = 0.0;
+  // MUSCL: the relaxed values of the two previous planes in march order
+  double xm1[MUSCL ? K : 1][V], xm2[MUSCL ? K : 1][V];
 
-  ItemIter it;
+  ItemIter<LEAD, TRAIL> it;
   it.init(g0, g1, nx);
   int j = 0;        // item counter (LT/PZ parity)
   int stg = 0;      // ring stage of item j
   uint32_t ph = 0;  // mbarrier phase of that stage
   while (!it.done()) {
-    int t, p;
-    bool halo;
-    it.next(nx, t, p, halo);
+    int t, p, kind;
+    it.next(nx, t, p, kind);
+    const bool halo = kind == kLead;
     if (t != cur_tile) {
       cur_tile = t;
       tg = tile_geom(T, a.nvx, t);
@@ -344,7 +376,11 @@ __global__ void __launch_bounds__(NTHR, MINB)
         if (tg.z0 + zpos<V, LZ>(lz, v) < a.nvz) zmask |= 1u << v;
       full = (vmask == (1u << K) - 1) && (zmask == (1u << V) - 1);
     }
-    const int i = item_plane(nx, a.bc, tg, p, halo);
+    const int i = item_plane(nx, a.bc, tg, p);
+    // output: upwind -> this plane (not for halos); MUSCL -> the previous
+    // plane of the run (lags one item), emitted by every item after the first
+    const bool out_plane = MUSCL ? (kind == kNormal || kind == kTrail) : !halo;
+    const int i_out = MUSCL ? item_plane(nx, a.bc, tg, p - 1) : i;
     const double* SF = reinterpret_cast<const double*>(smem + (size_t)stg * stage_bytes);
     const double* ST = reinterpret_cast<const double*>(smem + (size_t)stg * stage_bytes + box_bytes);
     if (TMA) {
@@ -365,7 +401,7 @@ __global__ void __launch_bounds__(NTHR, MINB)
       __syncthreads();
     }
 
-    if (i < 0) {
+    if (!MUSCL && i < 0) {
       // absorbing ghost plane: f_pre == 0
 #pragma unroll
       for (int k = 0; k < K; ++k)
@@ -381,12 +417,11 @@ __global__ void __launch_bounds__(NTHR, MINB)
         for (int v = 0; v < V; ++v)
           gz[v] = ((zmask >> v) & 1u) ? ST[a.gzo + tg.z0 + zpos<V, LZ>(lz, v)] : 0.0;
       }
-      const bool out_plane = !halo;
       const bool transport = a.dtdx != 0.0;
       const double dtdx = a.dtdx;
       double hE = 0.0;
       if (FIELD && out_plane) hE = __dmul_rn(0.5, __ldg(a.E + i));
-      double* gdst = (a.fout != nullptr && out_plane) ? a.fout + (size_t)i * a.plane : nullptr;
+      double* gdst = (a.fout != nullptr && out_plane) ? a.fout + (size_t)i_out * a.plane : nullptr;
       double lp[K];
       double pz[V];
 #pragma unroll
@@ -610,9 +645,92 @@ __global__ void __launch_bounds__(NTHR, MINB)
           for (int v = 0; v < V; ++v) prev[k][v] = fl[v];
         }
       };
+      // MUSCL (minmod) x transport, one plane behind the loads: item q
+      // relaxes plane q, forms the slope of plane q-1 from planes q-2..q and
+      // the face flux between q-1 and q (march order), and outputs plane q-1
+      // (oracle/bgk.py transport_muscl, same operation order).
+      auto body_m = [&](auto fast_c, auto down_c) {
+        constexpr bool FAST = decltype(fast_c)::value;
+        constexpr bool DOWNT = decltype(down_c)::value;
+        if constexpr (MUSCL) {
+          const bool ghost = i < 0;
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const bool ok = FAST || ((vmask >> k) & 1u);
+            double x[V];
+            if (ghost) {
+#pragma unroll
+              for (int v = 0; v < V; ++v) x[v] = 0.0;
+            } else {
+              const double gxy = ST[gxi[k]] * ST[gyi[k]];
+              if (SYNTH) {
+#pragma unroll
+                for (int v = 0; v < V; ++v) x[v] = (gxy * gz[v]) * ls;
+              } else {
+                const double w = r * (ls * gxy);
+                double raw[V];
+                lds_lane<V, LZ>(SF + soff[k], raw);
+#pragma unroll
+                for (int v = 0; v < V; ++v) x[v] = fma(w, gz[v], r * raw[v]);
+              }
+            }
+            const double c = cvx[k];
+            double F[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+              // physical order: a = f_i - f_{i-1}, b = f_{i+1} - f_i for plane i = q-1
+              const double am = DOWNT ? __dsub_rn(xm1[k][v], x[v]) : __dsub_rn(xm1[k][v], xm2[k][v]);
+              const double bm = DOWNT ? __dsub_rn(xm2[k][v], xm1[k][v]) : __dsub_rn(x[v], xm1[k][v]);
+              const double sg = (__dmul_rn(am, bm) > 0.0) ? copysign(fmin(fabs(am), fabs(bm)), am) : 0.0;
+              const double hs = __dmul_rn(0.5, sg);
+              F[v] = __dmul_rn(c, DOWNT ? __dsub_rn(xm1[k][v], hs) : __dadd_rn(xm1[k][v], hs));
+            }
+            if (FAST || out_plane) {
+              double o[V];
+#pragma unroll
+              for (int v = 0; v < V; ++v) {
+                const double d = DOWNT ? __dsub_rn(prev[k][v], F[v]) : __dsub_rn(F[v], prev[k][v]);
+                o[v] = __dsub_rn(xm1[k][v], __dmul_rn(dtdx, d));
+              }
+              double sl = 0.0;
+#pragma unroll
+              for (int v = 0; v < V; ++v) {
+                const double m = FAST ? o[v] : ((ok && ((zmask >> v) & 1u)) ? o[v] : 0.0);
+                pz[v] += m;
+                sl += m;
+              }
+              lp[k] = sl;
+              if (FAST || (gdst != nullptr && ok)) {
+                double* d = gdst + goff[k];
+                if (V == 4 && (FAST || zmask == 0xfu)) {
+                  st_global_v4(d, o[0], o[1 % V], o[2 % V], o[3 % V]);
+                } else if (V == 2 && (FAST || zmask == 0x3u)) {
+                  st_global_v2(d, o[0], o[1 % V]);
+                } else {
+#pragma unroll
+                  for (int v = 0; v < V; ++v)
+                    if (FAST || ((zmask >> v) & 1u)) d[zpos<V, LZ>(0, v)] = o[v];
+                }
+              }
+            }
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+              xm2[k][v] = xm1[k][v];
+              xm1[k][v] = x[v];
+              prev[k][v] = F[v];
+            }
+          }
+        }
+      };
       using T1 = std::integral_constant<bool, true>;
       using F1 = std::integral_constant<bool, false>;
-      if (!SYNTH && (a.debug & 4)) {
+      if constexpr (MUSCL) {
+        if (full && out_plane && gdst != nullptr) {
+          if (tg.down) body_m(T1{}, T1{}); else body_m(T1{}, F1{});
+        } else {
+          if (tg.down) body_m(F1{}, T1{}); else body_m(F1{}, F1{});
+        }
+      } else if (!SYNTH && (a.debug & 4)) {
         // ablation: copy-through skeleton (TMA in, STG out, no arithmetic)
         if (gdst != nullptr && out_plane) {
 #pragma unroll
@@ -666,13 +784,13 @@ __global__ void __launch_bounds__(NTHR, MINB)
       fence_proxy_async();
       issue_next();
     }
-    if (!halo && i >= 0 && !(a.debug & 1)) {
+    if (out_plane && i_out >= 0 && !(a.debug & 1)) {
       // one output per thread, in equal contiguous chunks per warp so no warp
       // carries the serial sums alone (contiguous lanes keep smem reads
       // conflict-free)
       const double* LTb = LT + (j & 1) * lines;
       const double* PZb = PZ + (j & 1) * NW * BZ;
-      double* dst = a.part + ((size_t)i * T.NT + t) * T.PS;
+      double* dst = a.part + ((size_t)i_out * T.NT + t) * T.PS;
       const int chunk = (T.A + T.By + BZ + NW - 1) / NW;
       const int o = lane < chunk ? warp * chunk + lane : 1 << 20;
       if (o < T.A) {
@@ -733,12 +851,15 @@ template <int V, int LZ, int K, int NTHR, int MINB, bool TMA>
 static cudaError_t launch_cfg(const CUtensorMap& map, const SweepArgs& a, bool synth, bool field,
                               int grid, int ns, size_t smem, cudaStream_t st) {
   void (*fn)(const CUtensorMap, const SweepArgs, int);
-  if (synth)
-    fn = field ? sweep_kernel<V, LZ, K, NTHR, MINB, true, true, TMA>
-               : sweep_kernel<V, LZ, K, NTHR, MINB, true, false, TMA>;
+  if (a.muscl)
+    fn = synth ? sweep_kernel<V, LZ, K, NTHR, MINB, true, false, TMA, true>
+               : sweep_kernel<V, LZ, K, NTHR, MINB, false, false, TMA, true>;
+  else if (synth)
+    fn = field ? sweep_kernel<V, LZ, K, NTHR, MINB, true, true, TMA, false>
+               : sweep_kernel<V, LZ, K, NTHR, MINB, true, false, TMA, false>;
   else
-    fn = field ? sweep_kernel<V, LZ, K, NTHR, MINB, false, true, TMA>
-               : sweep_kernel<V, LZ, K, NTHR, MINB, false, false, TMA>;
+    fn = field ? sweep_kernel<V, LZ, K, NTHR, MINB, false, true, TMA, false>
+               : sweep_kernel<V, LZ, K, NTHR, MINB, false, false, TMA, false>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   fn<<<grid, NTHR, smem, st>>>(map, a, ns);

@@ -19,6 +19,11 @@ EXTENSION; the reference implements alpha = 0 only): transport at rate
 alpha = 0 step with the scaled step d/eps (transport d/(eps dx),
 lambda = (d/eps) tau/eps), and the CFL cap is eps times the alpha = 0 cap;
 checker: ``oracle/bgk.py`` ``fine_propagate(alpha=1)``.
+
+``KineticParams(scheme="muscl")`` replaces the first-order upwind x flux by a
+MUSCL reconstruction with the minmod limiter (EXTENSION: BASELINE north_star
+"upwind/MUSCL", the paper's flux limiters; checker ``oracle/bgk.py``
+``transport_muscl``).  It has no v_x field term (E must be None).
 """
 
 from __future__ import annotations
@@ -65,10 +70,21 @@ class KineticParams:
     force: Optional[np.ndarray] = None
     cfl: float = 0.5
     alpha: int = 0  # 0 hydrodynamic (reference); 1 diffusive scaling (extension)
+    scheme: str = "upwind"  # x flux: "upwind" (reference) or "muscl" (extension)
 
     def __post_init__(self):
         if self.alpha not in (0, 1):
             raise ConfigurationError("alpha must be 0 or 1, got %r" % (self.alpha,))
+        if self.scheme not in ("upwind", "muscl"):
+            raise ConfigurationError("unknown x scheme %r (upwind | muscl)" % (self.scheme,))
+        if self.scheme == "muscl" and self.force is not None and np.max(np.abs(self.force)) > 0:
+            raise ConfigurationError("the MUSCL x scheme has no v_x field term; use scheme='upwind'")
+
+
+def _scheme(ctx, params) -> None:
+    """Point the context's sweeps at params.scheme (pbgk_set_x_scheme)."""
+    code = 1 if getattr(params, "scheme", "upwind") == "muscl" else 0
+    rt._lib.check(ctx.lib.pbgk_set_x_scheme(ctx.h, code), "pbgk_set_x_scheme")
 
 
 def _kdt(dt: float, params) -> float:
@@ -119,6 +135,7 @@ def fine_schedule(span: float, cap: float) -> list:
 def transport_update(f, dt: float, grid, params, bc) -> Distribution:
     """One explicit transport step on the GPU (ref/kinetic.py:86-124)."""
     ctx = rt.ctx_for(grid, bc)
+    _scheme(ctx, params)
     fd = as_device_f(f, ctx)
     E, e_max = rt.to_device_field(params.force, ctx.device, ctx.nx)
     out = ctx.empty_f()
@@ -155,6 +172,7 @@ def bgk_relax(f, dt: float, grid, params, bc=None) -> Distribution:
 def _run_schedule(ctx, f0, mom0, dts, params, out, want_f=True, mom_out=None):
     """pbgk_propagate over a fixed schedule; returns the status key."""
     tc = tau_constant(params.tau)
+    _scheme(ctx, params)
     E, e_max = rt.to_device_field(params.force, ctx.device, ctx.nx)
     arr = (ctypes.c_double * max(len(dts), 1))(*[_kdt(d, params) for d in dts])
     code = ctypes.c_longlong(-1)
@@ -167,6 +185,7 @@ def _run_schedule(ctx, f0, mom0, dts, params, out, want_f=True, mom_out=None):
 
 def _step_by_step(ctx, fd, dts, params):
     """Slow path for a non-constant tau callable: transport, host tau, relax."""
+    _scheme(ctx, params)
     E, e_max = rt.to_device_field(params.force, ctx.device, ctx.nx)
     cur = fd
     for s, dt in enumerate(dts, start=1):

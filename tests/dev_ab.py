@@ -10,12 +10,12 @@ from paper_2502_02704_b200 import runtime as rt, _lib
 from paper_2502_02704_b200.kinetic import propagate_window, stable_dt_kinetic
 
 
-def run(nx, nv, vm, nsteps, periodic, reps=3, field=False):
+def run(nx, nv, vm, nsteps, periodic, reps=3, field=False, scheme="upwind"):
     grid = P.PhaseGrid(P.build_spatial_grid(0.0, 1.0, nx), P.build_velocity_grid(vm, nv))
     bc = P.BoundaryKind.PERIODIC if periodic else P.BoundaryKind.OUTFLOW
     ctx = rt.ctx_for(grid, bc)
     E = 0.5 * np.sin(2 * np.pi * grid.space.centers) if field else None
-    kp = P.KineticParams(1e-2, force=E)
+    kp = P.KineticParams(1e-2, force=E, scheme=scheme)
     x = grid.space.centers
     U = P.MomentField(np.where(x < 0.5, 1.0, 0.125), np.zeros((nx, 3)), np.where(x < 0.5, 1.0, 0.8))
     m0 = rt.to_device_moments(U, ctx.device)
@@ -37,12 +37,17 @@ def run(nx, nv, vm, nsteps, periodic, reps=3, field=False):
     lib.pbgk_profile_read(ctx.h, prof)
     lib.pbgk_profile_enable(ctx.h, 0)
     cells = nx * np.prod(nv) * nsteps
-    print(f"{nx}x{nv[0]}^3{' E' if field else ''} x{nsteps}: {best:7.2f} ms {16*cells/best/1e6:6.0f} GB/s | sweep "
+    print(f"{nx}x{nv[0]}^3{' E' if field else ''}{' M' if scheme == 'muscl' else ''} x{nsteps}: {best:7.2f} ms {16*cells/best/1e6:6.0f} GB/s | sweep "
           f"{prof.sweep_bytes/prof.sweep_ms/1e6:6.0f} GB/s fin {prof.finalize_ms/max(prof.finalizes,1)*1e3:6.1f} us"
           f" ({prof.finalize_ms/(prof.sweep_ms+prof.finalize_ms):.3f})")
 
 
-if len(sys.argv) > 1 and sys.argv[1] == "field":
+if len(sys.argv) > 1 and sys.argv[1] == "muscl":
+    for sch in ("upwind", "muscl"):
+        run(2048, (64, 64, 64), 8.0, 16, False, scheme=sch)
+        run(512, (48, 48, 48), 10.0, 16, False, scheme=sch)
+        run(1024, (32, 32, 32), 8.0, 26, True, scheme=sch)
+elif len(sys.argv) > 1 and sys.argv[1] == "field":
     run(1024, (32, 32, 32), 8.0, 26, True)
     run(1024, (32, 32, 32), 8.0, 26, True, field=True)
     run(2048, (64, 64, 64), 8.0, 8, True, field=True)

@@ -328,3 +328,66 @@ def test_drift_diffusion_guards():
     assert ei.value.step == 1 and "non-finite" in str(ei.value)
     with pytest.raises(O.OracleConfigError):
         O.dd_propagate(rho, 1.0, 0.0, m, True)
+
+
+def _muscl_loop(f1, c, dtdx, bc):
+    """Scalar restatement of the MUSCL-minmod flux on one velocity line."""
+    n = len(f1)
+
+    def g(i):
+        if 0 <= i < n:
+            return f1[i]
+        if bc == "periodic":
+            return f1[i % n]
+        if bc == "outflow":
+            return f1[0] if i < 0 else f1[n - 1]
+        return 0.0
+
+    def mm(a, b):
+        return 0.0 if a * b <= 0.0 else math.copysign(min(abs(a), abs(b)), a)
+
+    def face(i):  # flux between cells i and i+1
+        if c >= 0:
+            return c * (g(i) + 0.5 * mm(g(i) - g(i - 1), g(i + 1) - g(i)))
+        return c * (g(i + 1) - 0.5 * mm(g(i + 1) - g(i), g(i + 2) - g(i + 1)))
+
+    return np.array([f1[i] - dtdx * (face(i) - face(i - 1)) for i in range(n)])
+
+
+@pytest.mark.parametrize("bc", ["periodic", "absorbing", "outflow"])
+def test_muscl_matches_scalar_loop_and_conserves(bc):
+    m = O.Mesh(0.0, 1.0, 11, 6.0, (6, 3, 2))
+    rng = np.random.default_rng(5)
+    f = rng.uniform(0.1, 2.0, (11, 6, 3, 2))
+    f[4] = 3.0  # a local extremum: the limiter must clip it
+    dt = 0.4 * O.fine_cap(m, 1.0)
+    got = O.transport_muscl(f, dt, m, bc)
+    for jx in range(6):
+        c = m.vc[0][jx]
+        want = _muscl_loop(f[:, jx, 1, 0], c, dt / m.dx, bc)
+        assert np.allclose(got[:, jx, 1, 0], want, rtol=1e-14, atol=1e-15)
+    if bc == "periodic":
+        assert abs(got.sum() - f.sum()) <= 1e-12 * f.sum()
+
+
+def test_muscl_more_accurate_than_upwind_and_tvd():
+    # smooth periodic advection at fixed CFL: with forward Euler (the
+    # reference's explicit step) both converge at first order in time, but
+    # the limited reconstruction cuts the error ~3x; and no new extrema (TVD)
+    def err(nx, scheme):
+        m = O.Mesh(0.0, 1.0, nx, 1.0, (2, 1, 1))  # c = +-0.5
+        x = m.xc
+        f = np.broadcast_to((1.0 + 0.5 * np.sin(2 * np.pi * x))[:, None, None, None], (nx, 2, 1, 1)).copy()
+        dt = 0.25 * m.dx
+        steps = int(round(0.25 / dt))
+        g = f
+        for _ in range(steps):
+            g = O.transport_muscl(g, dt, m, True) if scheme == "muscl" else O.transport(g, dt, m, True)
+        t = steps * dt
+        exact = 1.0 + 0.5 * np.sin(2 * np.pi * (x - 0.5 * t))
+        return float(np.max(np.abs(g[:, 1, 0, 0] - exact))), g
+    for nx in (64, 128):
+        e, g = err(nx, "muscl")
+        u, _ = err(nx, "upwind")
+        assert e < u / 3.0
+        assert g.max() <= 1.5 + 1e-14 and g.min() >= 0.5 - 1e-14
