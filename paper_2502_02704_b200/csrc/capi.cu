@@ -58,21 +58,21 @@ struct CfgShape {
   int minb;  // CTAs per SM the launch bounds target
 };
 const CfgShape kCfg[] = {
-    {4, 16, 4, 256, true, 2},   // 0: nvz % 64 == 0
-    {4, 8, 4, 256, true, 2},    // 1: nvz % 32 == 0
+    // first-order upwind (and the v_x field term), 4 lines per thread
+    {2, 32, 4, 256, true, 2},   // 0: nvz % 64 == 0, full 512-byte v_z rows per box line
+    {3, 16, 4, 256, true, 2},   // 1: nvz % 48 == 0
     {2, 16, 4, 256, true, 2},   // 2: nvz % 32 == 0
-    {3, 16, 4, 256, true, 2},   // 3: nvz % 48 == 0
-    {2, 8, 4, 256, true, 2},    // 4: nvz % 16 == 0
-    {2, 4, 4, 256, true, 2},    // 5: nvz % 8 == 0
-    {1, 32, 4, 256, false, 2},  // 6: anything (no TMA)
-    {2, 16, 8, 256, true, 2},   // 7: nvz % 32 == 0, 8 lines/thread
-    {2, 16, 16, 256, true, 1},  // 8: nvz % 32 == 0, 16 lines/thread, 1 CTA/SM
-    {2, 16, 8, 256, true, 1},   // 9: nvz % 32 == 0, 8 lines/thread, 1 CTA/SM
-    {2, 32, 4, 256, true, 2},   // 10: nvz % 64 == 0, full 512-byte v_z rows per box line
-    {2, 32, 8, 256, true, 2},   // 11: nvz % 64 == 0, 8 lines/thread
-    {2, 32, 4, 512, true, 1},   // 12: nvz % 64 == 0, 512 threads, 1 CTA/SM
-    {2, 16, 4, 512, true, 1},   // 13: nvz % 32 == 0, 512 threads, 1 CTA/SM
+    {2, 8, 4, 256, true, 2},    // 3: nvz % 16 == 0
+    {2, 4, 4, 256, true, 2},    // 4: nvz % 8 == 0
+    {1, 32, 4, 256, false, 2},  // 5: anything (no TMA; also MUSCL)
+    // MUSCL: three planes of per-line state; one CTA per SM, 255 registers
+    {2, 32, 4, 256, true, 1},   // 6: nvz % 64 == 0 (measured slower than cfg 0; unused)
+    {3, 16, 4, 256, true, 1},   // 7: nvz % 48 == 0
+    {2, 16, 4, 256, true, 1},   // 8: nvz % 32 == 0
+    {2, 8, 4, 256, true, 1},    // 9: nvz % 16 == 0
+    {2, 4, 4, 256, true, 1},    // 10: nvz % 8 == 0
 };
+
 
 struct Plan {
   int cfg;
@@ -122,7 +122,7 @@ struct pbgk_ctx {
   int dev, nsm;
   size_t smem_optin, smem_per_sm;
   double* d_c[3] = {nullptr, nullptr, nullptr};
-  Plan plan[2];  // [0] no field, [1] v_x field term
+  Plan plan[3];  // [0] upwind, [1] upwind + v_x field term, [2] MUSCL
   int TL, gxo, gyo, gzo;
   double* d_part = nullptr;
   size_t part_elems = 0;
@@ -168,19 +168,24 @@ struct ProfScope {
 };
 
 // Tile choice for one configuration of the sweep.
-bool make_plan(pbgk_ctx* c, bool field, Plan& out) {
+bool make_plan(pbgk_ctx* c, bool field, bool muscl, Plan& out) {
   const int nvx = c->g.nvx, nvy = c->g.nvy, nvz = c->g.nvz;
   const int nneg = nvx / 2;  // centres (j - (n-1)/2) dv are < 0 exactly for j < n/2
   const int npos = nvx - nneg;
   // tile shapes in measured order of preference (cfg ids of sweep.cu)
   std::vector<int> cands;
   const bool even = (nvz % 2 == 0);
-  if (even && nvz % 64 == 0) cands.push_back(10);
-  else if (even && nvz % 48 == 0) cands.push_back(3);
-  else if (even && nvz % 32 == 0) cands.push_back(2);
-  else if (even && nvz % 16 == 0) cands.push_back(4);
-  else if (even && nvz % 8 == 0) cands.push_back(5);
-  cands.push_back(6);
+  // MUSCL (measured, round 1): 64-wide rows keep 2 CTAs/SM (cfg 0, K=4 with a
+  // few spilled registers); the other shapes prefer 1 CTA/SM with 255 registers
+  const int* ids = nullptr;
+  static const int upw[5] = {0, 1, 2, 3, 4}, mus[5] = {0, 7, 8, 9, 10};
+  ids = muscl ? mus : upw;
+  if (even && nvz % 64 == 0) cands.push_back(ids[0]);
+  else if (even && nvz % 48 == 0) cands.push_back(ids[1]);
+  else if (even && nvz % 32 == 0) cands.push_back(ids[2]);
+  else if (even && nvz % 16 == 0) cands.push_back(ids[3]);
+  else if (even && nvz % 8 == 0) cands.push_back(ids[4]);
+  cands.push_back(5);
   if (const char* force = getenv("PBGK_FORCE_CFG")) {  // development knob
     cands.assign(1, atoi(force));
   }
@@ -228,7 +233,7 @@ bool make_plan(pbgk_ctx* c, bool field, Plan& out) {
       const double penalty = (s.tma ? 1.0 : 4.0);
       const double util = (double)(A * By) / lines;  // busy fraction of the thread lines
       const double score = penalty * ((loaded + part) / useful) * (1.0 + halo) * (1.5 - 0.5 * util) +
-                           (id == 6 ? 100.0 : 0.0);
+                           (id == 5 ? 100.0 : 0.0);
       if (score < best) {
         best = score;
         out.cfg = id;
@@ -449,7 +454,8 @@ int pbgk_ctx_create(const pbgk_grid_desc* g, pbgk_ctx** out) {
   c->gyo = c->gxo + g->nvx;
   c->gzo = (c->gyo + g->nvy + 1) & ~1;  // 16-byte aligned for vector reads
   c->TL = (c->gzo + g->nvz + 1) & ~1;
-  if (!make_plan(c, false, c->plan[0]) || !make_plan(c, true, c->plan[1]))
+  if (!make_plan(c, false, false, c->plan[0]) || !make_plan(c, true, false, c->plan[1]) ||
+      !make_plan(c, false, true, c->plan[2]))
     return bail(fail("no tiling fits this velocity grid"));
   for (int a = 0; a < 3; ++a) {
     std::vector<double> h(nv[a]);
@@ -458,7 +464,7 @@ int pbgk_ctx_create(const pbgk_grid_desc* g, pbgk_ctx** out) {
     cudaMemcpy(c->d_c[a], h.data(), nv[a] * sizeof(double), cudaMemcpyHostToDevice);
   }
   c->part_elems = 0;
-  for (int f = 0; f < 2; ++f)
+  for (int f = 0; f < 3; ++f)
     c->part_elems = std::max(c->part_elems, (size_t)g->nx * c->plan[f].t.NT * c->plan[f].t.PS);
   size_t bytes = c->part_elems * 8 + 2 * (size_t)g->nx * c->TL * 8 + (size_t)5 * g->nx * 8 + 64;
   if (cudaMalloc(&c->d_part, c->part_elems * 8) != cudaSuccess ||
@@ -500,9 +506,9 @@ long long pbgk_launch_count(void) { return g_launches.load(); }
 
 int pbgk_ctx_describe(const pbgk_ctx* c, char* buf, size_t n) {
   if (!c || !buf || n == 0) return fail("null argument");
-  const char* names[2] = {"plain", "field"};
+  const char* names[3] = {"plain", "field", "muscl"};
   int off = 0;
-  for (int f = 0; f < 2; ++f) {
+  for (int f = 0; f < 3; ++f) {
     const Plan& p = c->plan[f];
     const CfgShape& s = kCfg[p.cfg];
     off += snprintf(buf + off, n - off > 0 ? n - off : 0,
@@ -573,7 +579,7 @@ int pbgk_transport(pbgk_ctx* c, const double* f, double* f_out, double dt, const
   if (cudaSetDevice(c->dev) != cudaSuccess) return fail("cudaSetDevice");
   cudaStream_t st = (cudaStream_t)stream;
   const bool field = (E != nullptr && e_max > 0.0);
-  const int pid = field ? 1 : 0;
+  const int pid = field ? 1 : (c->x_scheme == 1 ? 2 : 0);
   if (run_final(c, pid, kFinIdentity, nullptr, nullptr, c->d_tab[0], 0, 1, 1, nullptr, 0, st)) return -1;
   return run_sweep(c, pid, field, f, c->d_tab[0], f_out, dt / c->dx, E, 0.5 * e_max, dt / c->dv[0], 0,
                    st);
@@ -615,7 +621,7 @@ int pbgk_propagate(pbgk_ctx* c, const double* f0, const double* mom0, double* f_
   cudaStream_t st = (cudaStream_t)stream;
   if (reset_err(c, st)) return -1;
   const bool field = (E != nullptr && e_max > 0.0);
-  const int pid = field ? 1 : 0;
+  const int pid = field ? 1 : (c->x_scheme == 1 ? 2 : 0);
   const int S = nsteps;
   const int W = S + (write_final ? 1 : 0);
   auto buf = [&](int w) { return ((W - w) % 2 == 0) ? f_out : f_tmp; };

@@ -847,19 +847,28 @@ __global__ void __launch_bounds__(NTHR, MINB)
 // host-side dispatch
 // ---------------------------------------------------------------------------
 
-template <int V, int LZ, int K, int NTHR, int MINB, bool TMA>
+// MODES: bit 0 = first-order upwind kernels, bit 1 = MUSCL kernels, bit 2 =
+// upwind with the v_x field term; a shape only instantiates what it serves.
+template <int V, int LZ, int K, int NTHR, int MINB, bool TMA, int MODES>
 static cudaError_t launch_cfg(const CUtensorMap& map, const SweepArgs& a, bool synth, bool field,
                               int grid, int ns, size_t smem, cudaStream_t st) {
-  void (*fn)(const CUtensorMap, const SweepArgs, int);
-  if (a.muscl)
-    fn = synth ? sweep_kernel<V, LZ, K, NTHR, MINB, true, false, TMA, true>
-               : sweep_kernel<V, LZ, K, NTHR, MINB, false, false, TMA, true>;
-  else if (synth)
-    fn = field ? sweep_kernel<V, LZ, K, NTHR, MINB, true, true, TMA, false>
-               : sweep_kernel<V, LZ, K, NTHR, MINB, true, false, TMA, false>;
-  else
-    fn = field ? sweep_kernel<V, LZ, K, NTHR, MINB, false, true, TMA, false>
-               : sweep_kernel<V, LZ, K, NTHR, MINB, false, false, TMA, false>;
+  void (*fn)(const CUtensorMap, const SweepArgs, int) = nullptr;
+  if (a.muscl) {
+    if constexpr ((MODES & 2) != 0)
+      fn = synth ? sweep_kernel<V, LZ, K, NTHR, MINB, true, false, TMA, true>
+                 : sweep_kernel<V, LZ, K, NTHR, MINB, false, false, TMA, true>;
+  } else {
+    if (field) {
+      if constexpr ((MODES & 4) != 0)
+        fn = synth ? sweep_kernel<V, LZ, K, NTHR, MINB, true, true, TMA, false>
+                   : sweep_kernel<V, LZ, K, NTHR, MINB, false, true, TMA, false>;
+    } else {
+      if constexpr ((MODES & 1) != 0)
+        fn = synth ? sweep_kernel<V, LZ, K, NTHR, MINB, true, false, TMA, false>
+                   : sweep_kernel<V, LZ, K, NTHR, MINB, false, false, TMA, false>;
+    }
+  }
+  if (fn == nullptr) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   fn<<<grid, NTHR, smem, st>>>(map, a, ns);
@@ -880,20 +889,17 @@ size_t sweep_smem_bytes(const SweepArgs& a, int V, int LZ, int NTHR, bool synth,
 cudaError_t launch_sweep(int cfg_id, const CUtensorMap& map, const SweepArgs& a, bool synth,
                          bool field, int grid, int ns, size_t smem, cudaStream_t st) {
   switch (cfg_id) {
-    case 0: return launch_cfg<4, 16, 4, 256, 2, true>(map, a, synth, field, grid, ns, smem, st);
-    case 1: return launch_cfg<4, 8, 4, 256, 2, true>(map, a, synth, field, grid, ns, smem, st);
-    case 2: return launch_cfg<2, 16, 4, 256, 2, true>(map, a, synth, field, grid, ns, smem, st);
-    case 3: return launch_cfg<3, 16, 4, 256, 2, true>(map, a, synth, field, grid, ns, smem, st);
-    case 4: return launch_cfg<2, 8, 4, 256, 2, true>(map, a, synth, field, grid, ns, smem, st);
-    case 5: return launch_cfg<2, 4, 4, 256, 2, true>(map, a, synth, field, grid, ns, smem, st);
-    case 7: return launch_cfg<2, 16, 8, 256, 2, true>(map, a, synth, field, grid, ns, smem, st);
-    case 8: return launch_cfg<2, 16, 16, 256, 1, true>(map, a, synth, field, grid, ns, smem, st);
-    case 9: return launch_cfg<2, 16, 8, 256, 1, true>(map, a, synth, field, grid, ns, smem, st);
-    case 10: return launch_cfg<2, 32, 4, 256, 2, true>(map, a, synth, field, grid, ns, smem, st);
-    case 11: return launch_cfg<2, 32, 8, 256, 2, true>(map, a, synth, field, grid, ns, smem, st);
-    case 12: return launch_cfg<2, 32, 4, 512, 1, true>(map, a, synth, field, grid, ns, smem, st);
-    case 13: return launch_cfg<2, 16, 4, 512, 1, true>(map, a, synth, field, grid, ns, smem, st);
-    default: return launch_cfg<1, 32, 4, 256, 2, false>(map, a, synth, field, grid, ns, smem, st);
+    case 0: return launch_cfg<2, 32, 4, 256, 2, true, 7>(map, a, synth, field, grid, ns, smem, st);
+    case 1: return launch_cfg<3, 16, 4, 256, 2, true, 7>(map, a, synth, field, grid, ns, smem, st);
+    case 2: return launch_cfg<2, 16, 4, 256, 2, true, 7>(map, a, synth, field, grid, ns, smem, st);
+    case 3: return launch_cfg<2, 8, 4, 256, 2, true, 7>(map, a, synth, field, grid, ns, smem, st);
+    case 4: return launch_cfg<2, 4, 4, 256, 2, true, 7>(map, a, synth, field, grid, ns, smem, st);
+    case 5: return launch_cfg<1, 32, 4, 256, 2, false, 7>(map, a, synth, field, grid, ns, smem, st);
+    case 7: return launch_cfg<3, 16, 4, 256, 1, true, 3>(map, a, synth, field, grid, ns, smem, st);
+    case 8: return launch_cfg<2, 16, 4, 256, 1, true, 3>(map, a, synth, field, grid, ns, smem, st);
+    case 9: return launch_cfg<2, 8, 4, 256, 1, true, 3>(map, a, synth, field, grid, ns, smem, st);
+    case 10: return launch_cfg<2, 4, 4, 256, 1, true, 3>(map, a, synth, field, grid, ns, smem, st);
+    default: return cudaErrorInvalidValue;
   }
 }
 
