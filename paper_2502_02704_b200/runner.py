@@ -163,6 +163,11 @@ class RunConfig:
     out_dir: str = "out"
     use_frozen_prefix: bool = True
     preset: Optional[str] = None
+    # extensions beyond the reference
+    alpha: int = 0                 # 1: diffusive scaling
+    coarse: str = "euler"          # "drift_diffusion": the diffusive G
+    x_scheme: str = "upwind"       # "muscl": minmod-limited x transport
+    schedule: str = "phased"       # "pipelined": coarse work trails the fine windows
 
 
 def _boolean(text: str) -> bool:
@@ -177,7 +182,8 @@ def _boolean(text: str) -> bool:
 _TYPES = dict(preset=str, case=str, bc=str, mode=str, out_dir=str, x_min=float, x_max=float,
               v_max=float, epsilon=float, t_final=float, tol=float, tau=float, cfl_kinetic=float,
               cfl_fluid=float, n_x=int, n_vx=int, n_vy=int, n_vz=int, n_g=int, n_f=int, k_max=int,
-              workers=int, use_frozen_prefix=_boolean)
+              workers=int, use_frozen_prefix=_boolean, alpha=int, coarse=str, x_scheme=str,
+              schedule=str)
 _NEEDED = ("case", "x_min", "x_max", "n_x", "v_max", "n_vx", "n_vy", "n_vz", "epsilon", "bc",
            "t_final", "n_g", "n_f", "k_max", "tol")
 
@@ -232,6 +238,14 @@ def parse_config(path) -> RunConfig:
             raise ConfigurationError("need 0 < %s <= 1, got %r" % (label, getattr(cfg, label)))
     if cfg.k_max < 1 or cfg.workers < 1:
         raise ConfigurationError("need k_max >= 1 and workers >= 1")
+    if cfg.alpha not in (0, 1):
+        raise ConfigurationError("need alpha in {0, 1}, got %r" % (cfg.alpha,))
+    if cfg.coarse not in ("euler", "drift_diffusion"):
+        raise ConfigurationError("unknown coarse model '%s'" % cfg.coarse)
+    if cfg.x_scheme not in ("upwind", "muscl"):
+        raise ConfigurationError("unknown x_scheme '%s'" % cfg.x_scheme)
+    if cfg.schedule not in ("phased", "pipelined"):
+        raise ConfigurationError("unknown schedule '%s'" % cfg.schedule)
     return cfg
 
 
@@ -244,8 +258,9 @@ def build_discretization(cfg: RunConfig) -> Discretization:
 def build_params(cfg: RunConfig, disc: Discretization):
     E = force_field(cfg.case, disc.phase.space)
     tau = constant_tau if cfg.tau == 1.0 else ConstantTau(cfg.tau)
-    return (KineticParams(cfg.epsilon, tau=tau, force=E, cfl=cfg.cfl_kinetic),
-            FluidParams(force=E, cfl=cfg.cfl_fluid))
+    return (KineticParams(cfg.epsilon, tau=tau, force=E, cfl=cfg.cfl_kinetic, alpha=cfg.alpha,
+                          scheme=cfg.x_scheme),
+            FluidParams(force=E, cfl=cfg.cfl_fluid, model=cfg.coarse))
 
 
 # ---------------------------------------------------------------------------
@@ -344,7 +359,7 @@ def run_fine_mode(cfg, disc, kinetic):
 
 def run_parareal_mode(cfg, disc, kinetic, fluid, U0, timing=None):
     pc = PararealConfig(cfg.k_max, cfg.tol, use_frozen_prefix=cfg.use_frozen_prefix,
-                        workers=cfg.workers)
+                        workers=cfg.workers, pipelined=cfg.schedule == "pipelined")
     return run_parareal(U0, pc, disc, kinetic, fluid, timing=timing)
 
 

@@ -47,10 +47,25 @@ def test_config_presets_overrides_and_errors(tmp_path):
                      ("preset = sod\nn_x = many\n", ":2: bad value"),
                      ("case = sod\n", "required keys missing"), ("preset = jet\n", "unknown preset"),
                      ("preset = sod\nmode = magic\n", "unknown mode"),
-                     ("preset = sod\ncfl_fluid = 1.5\n", "cfl_fluid")):
+                     ("preset = sod\ncfl_fluid = 1.5\n", "cfl_fluid"),
+                     ("preset = sod\nalpha = 2\n", "alpha"),
+                     ("preset = sod\ncoarse = navier\n", "coarse model"),
+                     ("preset = sod\nx_scheme = weno\n", "x_scheme"),
+                     ("preset = sod\nschedule = eager\n", "schedule")):
         p.write_text(bad)
         with pytest.raises(P.ConfigurationError, match=msg):
             P.parse_config(p)
+
+
+def test_config_extension_keys(tmp_path):
+    p = tmp_path / "x.cfg"
+    p.write_text("preset = sod\nalpha = 1\ncoarse = drift_diffusion\nschedule = pipelined\n")
+    cfg = P.parse_config(p)
+    kin, flu = P.build_params(cfg, P.build_discretization(cfg))
+    assert (kin.alpha, flu.model, cfg.schedule) == (1, "drift_diffusion", "pipelined")
+    p.write_text("preset = sod\nx_scheme = muscl\n")
+    kin, _ = P.build_params(P.parse_config(p), P.build_discretization(P.parse_config(p)))
+    assert kin.scheme == "muscl"
 
 
 def test_artifacts_round_trip_exactly(tmp_path):
