@@ -49,6 +49,9 @@ def parse():
                     help="override the workload's x boundary")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--xshard", action="store_true",
+                    help="fine-only configs: shard the x cells over the ranks (halo exchange per "
+                         "step, strong scaling) instead of replicas")
     ap.add_argument("--schedule", choices=["phased", "pipelined"], default="phased",
                     help="parareal iteration schedule (pipelined: G jumps + correction on a side "
                          "stream behind the fine windows; bitwise identical results)")
@@ -188,6 +191,17 @@ def run_ours(args, w, world, rank, local):
             else:
                 run.jumps(snaps, jumps, 1)
                 run.correct(snaps, jumps, 1)
+    elif args.xshard:
+        # x cells sharded over the ranks, halo exchange per step (sharded.py)
+        from paper_2502_02704_b200.sharded import SlabFine
+        sl = SlabFine(phase, bc, kinetic, dev)
+        ctx = sl.ctx
+        f0 = f_init.device_tensor(dev)[sl.x0:sl.x0 + sl.n].contiguous()
+        nsteps = w.window_steps()
+        cell_updates = w.cells * nsteps
+
+        def step():
+            sl.propagate(0.0, w.t_final, f0=f0)
     else:
         ctx = rt.ctx_for(phase, bc, dev)
         f0 = f_init.device_tensor(dev)
@@ -239,8 +253,8 @@ def run_ours(args, w, world, rank, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    if w.mode == "parareal":
-        job_updates = cell_updates  # windows are sharded: the job does them once
+    if w.mode == "parareal" or args.xshard:
+        job_updates = cell_updates  # windows / x cells are sharded: the job does them once
     else:
         job_updates = cell_updates * world  # replicas
     value = job_updates * args.steps / (total_ms * 1e-3)
@@ -336,7 +350,8 @@ def main():
                 "windows": w.n_g,
                 "fine_steps_per_window": w.window_steps(),
                 "parallelism": ("windows sharded over %d rank(s)" % world) if w.mode == "parareal"
-                else ("replicas x%d" % world),
+                else (("x cells sharded over %d rank(s)" % world) if args.xshard
+                      else ("replicas x%d" % world)),
                 "schedule": args.schedule if w.mode == "parareal" else None,
                 "l2": ("inputs larger than L2 (f = %.2f GB); " % (w.cells * 8 / 1e9)) +
                       "256 MiB L2 flush write between timed steps"}
@@ -370,7 +385,7 @@ def main():
         line = {"metric": metric, "value": res["value"], "unit": "cell-updates/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
                 "higher_is_better": True,
-                "scaling": "strong" if w.mode == "parareal" else "weak", "vs_baseline": None,
+                "scaling": "strong" if (w.mode == "parareal" or args.xshard) else "weak", "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic (seeded BASELINE.json configs; no dataset)",
                 "config": cfg_json, "roofline": res["roofline"], "cpu_baseline": cpu,
                 "e2e": res["e2e"], "gpu_launches": res["gpu_launches"], "clocks": res["clocks"]}

@@ -50,7 +50,8 @@ typedef struct pbgk_grid_desc {
   double x_min, x_max, v_max;
   int32_t bc;       /* x boundary: 0 ABSORBING (zero inflow ghost, ref/kinetic.py:106-108),
                        1 PERIODIC, 2 OUTFLOW (zero-gradient ghost; extension asked by
-                       BASELINE.json, not in the reference) */
+                       BASELINE.json, not in the reference), 3 SLAB (one x-slab of a
+                       sharded domain, halos supplied by the caller; see pbgk_slab_*) */
   int32_t device;   /* CUDA device ordinal the context (and every call on it) uses */
 } pbgk_grid_desc;
 
@@ -134,6 +135,38 @@ int pbgk_fluid_model(pbgk_ctx* ctx, int model, double diffusivity);
  * no reference counterpart; two ghost planes per side by the x boundary).
  * MUSCL has no v_x field term: sweeps with E != 0 fail on a MUSCL context. */
 int pbgk_set_x_scheme(pbgk_ctx* ctx, int scheme);
+
+/* ---- x-sharded fine propagation (slabs) --------------------------------- */
+/* A context created with bc = 3 is one x-slab of a larger domain (one rank
+ * of an x-sharded F, EXTENSION: SURVEY 8(f) rank 2).  Its f buffers are
+ * PADDED, double[nx+2][nvx][nvy][nvz], and so are its table buffers,
+ * double[nx+2][TL]: index 0 and nx+1 are halo planes / rows that the caller
+ * fills between steps (neighbours' boundary planes f*_s and table rows R_s;
+ * zeros for an absorbing global edge, the edge itself for outflow).  Every
+ * sweep / finalize is the unsharded one restricted to the slab, so the
+ * sharded F is bitwise the single-GPU F. */
+int pbgk_table_len(const pbgk_ctx* ctx);
+/* Exact cell width (a slab inherits the global dx; (x_max-x_min)/nx of the
+ * slab's bounds may round differently). */
+int pbgk_ctx_set_dx(pbgk_ctx* ctx, double dx);
+/* Table rows 1..nx: kind 0 identity (relax = id, for an f given directly),
+ * kind 1 lift tables of the moments mom (double[5][nx]).  Starts a
+ * propagation: resets the context's failure key. */
+int pbgk_slab_tables(pbgk_ctx* ctx, int kind, const double* mom, double* tab_pad, void* stream,
+                     long long* h_code);
+/* One sweep: relax the padded input by tab_pad, transport by dt (0: relax
+ * only), write the interior planes of fout_pad (NULL: partials only);
+ * fin_pad NULL synthesises the input from the lift tables. */
+int pbgk_slab_sweep(pbgk_ctx* ctx, const double* fin_pad, const double* tab_pad, double* fout_pad,
+                    double dt, const double* E, double e_max, void* stream);
+/* After a sweep: mode 0 = relax tables R(dt, eps, tau) into rows 1..nx of
+ * tab_pad (BlowUpError(step) on non-finite marginals); mode 1 = the moments
+ * of the swept planes into mom_out (double[5][nx]).  `field`: the sweep had
+ * the v_x field term (its partial layout).  Asynchronous unless h_code is
+ * non-NULL, which synchronises and returns the earliest failure key since
+ * pbgk_slab_tables (-1 clean). */
+int pbgk_slab_finalize(pbgk_ctx* ctx, int mode, int field, double* tab_pad, double* mom_out,
+                       double dt, double eps, double tau, int step, void* stream, long long* h_code);
 
 /* ---- pipelined parareal (side stream) ---------------------------------- */
 /* Leave `slots` CTA slots out of the persistent sweep grid (sized for every

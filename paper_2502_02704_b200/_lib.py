@@ -47,6 +47,11 @@ PROTOTYPES = {
     "pbgk_fluid_model": (c_int, [_P, _I, _D]),
     "pbgk_set_grid_reserve": (c_int, [_P, _I]),
     "pbgk_set_x_scheme": (c_int, [_P, _I]),
+    "pbgk_table_len": (c_int, [_P]),
+    "pbgk_ctx_set_dx": (c_int, [_P, _D]),
+    "pbgk_slab_tables": (c_int, [_P, _I, _P, _P, _P, _P]),
+    "pbgk_slab_sweep": (c_int, [_P, _P, _P, _P, _D, _P, _D, _P]),
+    "pbgk_slab_finalize": (c_int, [_P, _I, _I, _P, _P, _D, _D, _D, _I, _P, _P]),
     "pbgk_fluid_propagate_async": (c_int, [_P, _I, _P, _P, _P, _P, _P, _D, _D, _P, _P, _P]),
     "pbgk_parareal_correct_range": (c_int, [_P, _I, _I, _P, _P, _P, _P, _D, _D, _P, _P, _P, _P]),
     "pbgk_parareal_correct": (c_int, [_P, _I, _I, _P, _P, _P, POINTER(c_double), _D, _D, _P,

@@ -283,8 +283,9 @@ const CUtensorMap* tensor_map(pbgk_ctx* c, const double* ptr, const Tiling& t, i
   e.rows_load = t.rows_load;
   e.By = t.By;
   e.Bz = t.Bz;
+  // slab contexts (bc 3) address padded buffers: one halo plane per side
   const cuuint64_t dims[4] = {(cuuint64_t)c->g.nvz, (cuuint64_t)c->g.nvy, (cuuint64_t)c->g.nvx,
-                              (cuuint64_t)c->g.nx};
+                              (cuuint64_t)c->g.nx + (c->g.bc == 3 ? 2 : 0)};
   const cuuint64_t strides[3] = {(cuuint64_t)c->g.nvz * 8, (cuuint64_t)c->g.nvy * c->g.nvz * 8,
                                  (cuuint64_t)c->g.nvx * c->g.nvy * c->g.nvz * 8};
   const cuuint32_t box[4] = {(cuuint32_t)t.Bz, (cuuint32_t)t.By, (cuuint32_t)t.rows_load, 1};
@@ -432,6 +433,7 @@ int pbgk_ctx_create(const pbgk_grid_desc* g, pbgk_ctx** out) {
   if (!g || !out) return fail("null argument");
   if (g->nx < 1 || g->nvx < 1 || g->nvy < 1 || g->nvz < 1) return fail("bad grid sizes");
   if (g->nvx > 4096 || g->nvy > 4096 || g->nvz > 4096) return fail("velocity axis too long");
+  if (g->bc < 0 || g->bc > 3) return fail("bc must be 0 (absorbing), 1 (periodic), 2 (outflow) or 3 (slab)");
   pbgk_ctx* c = new pbgk_ctx();
   c->g = *g;
   c->dx = (g->x_max - g->x_min) / g->nx;  // ref/grid.py:95
@@ -712,6 +714,66 @@ int pbgk_parareal_correct(pbgk_ctx* c, int n_g, int start, double* snaps, const 
   if (h_code) *h_code = code;
   if (h_err) *h_err = c->h_dbl[0];
   return 0;
+}
+
+int pbgk_table_len(const pbgk_ctx* c) { return c ? c->TL : -1; }
+
+int pbgk_ctx_set_dx(pbgk_ctx* c, double dx) {
+  if (!c) return fail("pbgk_ctx_set_dx: null context");
+  if (!(dx > 0.0)) return fail("pbgk_ctx_set_dx: dx must be > 0");
+  c->dx = dx;
+  return 0;
+}
+
+namespace {
+int slab_check(pbgk_ctx* c, const char* who) {
+  if (!c) return fail(std::string(who) + ": null context");
+  if (c->g.bc != 3) return fail(std::string(who) + ": needs a slab context (bc 3)");
+  if (cudaSetDevice(c->dev) != cudaSuccess) return fail("cudaSetDevice");
+  return 0;
+}
+}  // namespace
+
+int pbgk_slab_tables(pbgk_ctx* c, int kind, const double* mom, double* tab_pad, void* stream,
+                     long long* h_code) {
+  if (slab_check(c, "pbgk_slab_tables")) return -1;
+  if (!tab_pad || (kind == 1 && !mom)) return fail("pbgk_slab_tables: null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (reset_err(c, st)) return -1;
+  // rows 1..nx (row 0 / nx+1 are the halos, filled by the caller)
+  if (run_final(c, 0, kind == 1 ? kFinSynthRaw : kFinIdentity, mom, nullptr, tab_pad + c->TL, 0, 1, 1,
+                nullptr, 0, st))
+    return -1;
+  return fetch_err(c, st, h_code);
+}
+
+int pbgk_slab_sweep(pbgk_ctx* c, const double* fin_pad, const double* tab_pad, double* fout_pad,
+                    double dt, const double* E, double e_max, void* stream) {
+  if (slab_check(c, "pbgk_slab_sweep")) return -1;
+  if (!tab_pad) return fail("pbgk_slab_sweep: null table");
+  if (c->x_scheme == 1 && dt != 0.0) return fail("pbgk_slab_sweep: MUSCL needs two halo planes (upwind only)");
+  const bool field = E != nullptr && e_max > 0.0 && dt != 0.0;
+  const int pid = field ? 1 : 0;
+  return run_sweep(c, pid, field, fin_pad, tab_pad, fout_pad, dt / c->dx, E, 0.5 * e_max,
+                   dt / c->dv[0], 0, (cudaStream_t)stream);
+}
+
+int pbgk_slab_finalize(pbgk_ctx* c, int mode, int field, double* tab_pad, double* mom_out,
+                       double dt, double eps, double tau, int step, void* stream, long long* h_code) {
+  if (slab_check(c, "pbgk_slab_finalize")) return -1;
+  if ((mode == 0 && !tab_pad) || (mode == 1 && !mom_out)) return fail("pbgk_slab_finalize: null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  // no reset: failure keys accumulate (atomicMin) from pbgk_slab_tables on,
+  // and are only read back (synchronising) when h_code is given
+  const int pid = field ? 1 : 0;
+  if (mode == 0) {
+    if (run_final(c, pid, kFinRelax, nullptr, nullptr, tab_pad + c->TL, dt, eps, tau, nullptr, step, st))
+      return -1;
+  } else {
+    if (run_final(c, pid, kFinProject, nullptr, mom_out, nullptr, 0, 1, 1, nullptr, step, st))
+      return -1;
+  }
+  return fetch_err(c, st, h_code);
 }
 
 int pbgk_set_x_scheme(pbgk_ctx* c, int scheme) {

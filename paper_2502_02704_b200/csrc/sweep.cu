@@ -169,10 +169,13 @@ struct ItemIter {
 
 // x cell of march position p of a tile (p may be outside [0, nx) for halo /
 // trail items); -1 = absorbing ghost (f == 0).  Ghost planes: periodic wrap,
-// zero-gradient copy of the edge plane (outflow) or zero (absorbing).
+// zero-gradient copy of the edge plane (outflow) or zero (absorbing).  bc 3
+// (a slab of an x-sharded domain): -1 and nx are the halo planes, kept as
+// such; the slab's buffers are padded by one plane / table row per side.
 __device__ __forceinline__ int item_plane(int nx, int bc, const TileGeom& tg, int p) {
   int i = tg.down ? nx - 1 - p : p;
-  if (i < 0 || i >= nx) i = (bc == 1) ? ((i % nx) + nx) % nx : (bc == 2 ? (i < 0 ? 0 : nx - 1) : -1);
+  if ((i < 0 || i >= nx) && bc != 3)
+    i = (bc == 1) ? ((i % nx) + nx) % nx : (bc == 2 ? (i < 0 ? 0 : nx - 1) : -1);
   return i;
 }
 
@@ -282,19 +285,20 @@ __global__ void __launch_bounds__(NTHR, MINB)
     if (++pstg == ns) pstg = 0;
     uint64_t* bar = &bars[s];
     unsigned char* st = smem + (size_t)s * stage_bytes;
-    if (i < 0) {
+    if (i < 0 && a.bc != 3) {
       mbar_arrive_expect_tx(bar, 0);
       return;
     }
+    const int im = i + (a.bc == 3 ? 1 : 0);  // plane / row in memory (slab buffers are padded)
     mbar_arrive_expect_tx(bar, box_bytes + tab_bytes);
     if (!SYNTH) {
 #if PBGK_HINT_LOAD
-      tma_load_4d_hint(st, &fmap, tg.z0, tg.y0, tg.r0 - hoff, i, bar, pol_stream);
+      tma_load_4d_hint(st, &fmap, tg.z0, tg.y0, tg.r0 - hoff, im, bar, pol_stream);
 #else
-      tma_load_4d(st, &fmap, tg.z0, tg.y0, tg.r0 - hoff, i, bar);
+      tma_load_4d(st, &fmap, tg.z0, tg.y0, tg.r0 - hoff, im, bar);
 #endif
     }
-    tma_load_1d(st + box_bytes, a.tab + (size_t)i * a.TL, tab_bytes, bar);
+    tma_load_1d(st + box_bytes, a.tab + (size_t)im * a.TL, tab_bytes, bar);
   };
   if (TMA && tid == ptid) {
     prefetch_tensormap(&fmap);
@@ -381,11 +385,12 @@ __global__ void __launch_bounds__(NTHR, MINB)
     // plane of the run (lags one item), emitted by every item after the first
     const bool out_plane = MUSCL ? (kind == kNormal || kind == kTrail) : !halo;
     const int i_out = MUSCL ? item_plane(nx, a.bc, tg, p - 1) : i;
+    const int sh = a.bc == 3 ? 1 : 0;  // slab buffers: one padding plane / row
     const double* SF = reinterpret_cast<const double*>(smem + (size_t)stg * stage_bytes);
     const double* ST = reinterpret_cast<const double*>(smem + (size_t)stg * stage_bytes + box_bytes);
     if (TMA) {
       mbar_wait(&bars[stg], ph);
-    } else if (i >= 0) {
+    } else if (i >= 0 || a.bc == 3) {
       // generic path: cooperative synchronous load of the box and the table row
       double* sf = reinterpret_cast<double*>(smem);
       for (uint32_t e = tid; e < box_elems && !SYNTH; e += NTHR) {
@@ -394,14 +399,14 @@ __global__ void __launch_bounds__(NTHR, MINB)
         const int jx = tg.r0 - hoff + br, jy = tg.y0 + b, jz = tg.z0 + zz;
         double v = 0.0;
         if (jx >= 0 && jx < a.nvx && jy < a.nvy && jz < a.nvz)
-          v = a.fin[(size_t)i * a.plane + ((size_t)jx * a.nvy + jy) * a.nvz + jz];
+          v = a.fin[(size_t)(i + sh) * a.plane + ((size_t)jx * a.nvy + jy) * a.nvz + jz];
         sf[e] = v;
       }
-      for (int e = tid; e < a.TL; e += NTHR) sf[box_bytes / 8 + e] = a.tab[(size_t)i * a.TL + e];
+      for (int e = tid; e < a.TL; e += NTHR) sf[box_bytes / 8 + e] = a.tab[(size_t)(i + sh) * a.TL + e];
       __syncthreads();
     }
 
-    if (!MUSCL && i < 0) {
+    if (!MUSCL && i < 0 && a.bc != 3) {
       // absorbing ghost plane: f_pre == 0
 #pragma unroll
       for (int k = 0; k < K; ++k)
@@ -421,7 +426,7 @@ __global__ void __launch_bounds__(NTHR, MINB)
       const double dtdx = a.dtdx;
       double hE = 0.0;
       if (FIELD && out_plane) hE = __dmul_rn(0.5, __ldg(a.E + i));
-      double* gdst = (a.fout != nullptr && out_plane) ? a.fout + (size_t)i_out * a.plane : nullptr;
+      double* gdst = (a.fout != nullptr && out_plane) ? a.fout + (size_t)(i_out + sh) * a.plane : nullptr;
       double lp[K];
       double pz[V];
 #pragma unroll

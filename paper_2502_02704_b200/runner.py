@@ -345,8 +345,15 @@ def run_fluid_mode(cfg, disc, fluid, U0):
     return initial_coarse_sweep(U0, disc, fluid).snapshots
 
 
-def run_fine_mode(cfg, disc, kinetic):
-    """One distribution marched across all windows, f resident on the device."""
+def run_fine_mode(cfg, disc, kinetic, group=None):
+    """One distribution marched across all windows, f resident on the device.
+
+    Under torch.distributed (world > 1) the x cells are sharded over the
+    ranks (``sharded.SlabFine``, halo exchange per step) -- bitwise the
+    single-GPU run, the snapshots gathered on every rank."""
+    dist = torch.distributed
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        return _run_fine_sharded(cfg, disc, kinetic, group)
     f = initial_distribution(cfg.case, disc.phase, disc.bc)
     t = disc.time.coarse_times
     snaps = [project(f, disc.phase, disc.bc)]
@@ -354,6 +361,21 @@ def run_fine_mode(cfg, disc, kinetic):
         f = propagate_kinetic(f, float(t[n - 1]), float(t[n]), disc.phase, kinetic, disc.bc,
                               dt_max=disc.time.dt_f)
         snaps.append(project(f, disc.phase, disc.bc))
+    return snaps
+
+
+def _run_fine_sharded(cfg, disc, kinetic, group):
+    from .sharded import SlabFine
+    sl = SlabFine(disc.phase, disc.bc, kinetic, group=group)
+    f = initial_distribution(cfg.case, disc.phase, disc.bc).device_tensor(sl.device)
+    f = f[sl.x0:sl.x0 + sl.n].contiguous()
+    t = disc.time.coarse_times
+    f, m = sl.propagate(0.0, 0.0, f0=f, want_moments=True)  # the projection of f0
+    snaps = [MomentField.from_packed(sl.gather(m, 1))]
+    for n in range(1, disc.time.n_g + 1):
+        f, m = sl.propagate(float(t[n - 1]), float(t[n]), f0=f, dt_max=disc.time.dt_f,
+                            want_moments=True)
+        snaps.append(MomentField.from_packed(sl.gather(m, 1)))
     return snaps
 
 
