@@ -217,6 +217,27 @@ __device__ __forceinline__ void lds_vec(const double* p, double (&x)[V]) {
   }
 }
 
+// Store of one lane's V outputs of a line: one 32-byte vector (V = 4), 16-byte
+// pairs (other even V) or masked scalars (odd V / partial rows).
+template <int V, int LZ, bool FAST>
+__device__ __forceinline__ void store_line(double* d, const double (&o)[V], unsigned zmask) {
+  if constexpr (V == 4) {
+    if (FAST || zmask == 0xfu) {
+      st_global_v4(d, o[0], o[1], o[2], o[3]);
+      return;
+    }
+  } else if constexpr (V % 2 == 0) {
+    if (FAST || zmask == (1u << V) - 1) {
+#pragma unroll
+      for (int v = 0; v < V; v += 2) st_global_v2(d + v, o[v], o[v + 1]);
+      return;
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < V; ++v)
+    if (FAST || ((zmask >> v) & 1u)) d[zpos<V, LZ>(0, v)] = o[v];
+}
+
 template <int V, int LZ, int K, int NTHR, int MINB, bool SYNTH, bool FIELD, bool TMA, bool MUSCL>
 __global__ void __launch_bounds__(NTHR, MINB)
     sweep_kernel(const __grid_constant__ CUtensorMap fmap, const SweepArgs a, int ns) {
@@ -521,21 +542,7 @@ __global__ void __launch_bounds__(NTHR, MINB)
             }
             lp[k] = sl;
             if (FAST || (gdst != nullptr && ok)) {
-              double* d = gdst + goff[k];
-              if (V == 4 && (FAST || zmask == 0xfu)) {
-                st_global_v4(d, o[0], o[1 % V], o[2 % V], o[3 % V]);
-              } else if (V == 2 && (FAST || zmask == 0x3u)) {
-                
-#if PBGK_HINT_STORE
-                st_global_v2_hint(d, o[0], o[1 % V], pol_stream);
-#else
-                st_global_v2(d, o[0], o[1 % V]);
-#endif
-              } else {
-#pragma unroll
-                for (int v = 0; v < V; ++v)
-                  if (FAST || ((zmask >> v) & 1u)) d[zpos<V, LZ>(0, v)] = o[v];
-              }
+              store_line<V, LZ, FAST>(gdst + goff[k], o, zmask);
             }
           }
 #pragma unroll
@@ -634,16 +641,7 @@ __global__ void __launch_bounds__(NTHR, MINB)
             }
             lp[k] = sl;
             if (FAST || (gdst != nullptr && ok)) {
-              double* d = gdst + goff[k];
-              if (V == 4 && (FAST || zmask == 0xfu)) {
-                st_global_v4(d, o[0], o[1 % V], o[2 % V], o[3 % V]);
-              } else if (V == 2 && (FAST || zmask == 0x3u)) {
-                st_global_v2(d, o[0], o[1 % V]);
-              } else {
-#pragma unroll
-                for (int v = 0; v < V; ++v)
-                  if (FAST || ((zmask >> v) & 1u)) d[zpos<V, LZ>(0, v)] = o[v];
-              }
+              store_line<V, LZ, FAST>(gdst + goff[k], o, zmask);
             }
           }
 #pragma unroll
@@ -706,16 +704,7 @@ __global__ void __launch_bounds__(NTHR, MINB)
               }
               lp[k] = sl;
               if (FAST || (gdst != nullptr && ok)) {
-                double* d = gdst + goff[k];
-                if (V == 4 && (FAST || zmask == 0xfu)) {
-                  st_global_v4(d, o[0], o[1 % V], o[2 % V], o[3 % V]);
-                } else if (V == 2 && (FAST || zmask == 0x3u)) {
-                  st_global_v2(d, o[0], o[1 % V]);
-                } else {
-#pragma unroll
-                  for (int v = 0; v < V; ++v)
-                    if (FAST || ((zmask >> v) & 1u)) d[zpos<V, LZ>(0, v)] = o[v];
-                }
+                store_line<V, LZ, FAST>(gdst + goff[k], o, zmask);
               }
             }
 #pragma unroll
@@ -904,6 +893,7 @@ cudaError_t launch_sweep(int cfg_id, const CUtensorMap& map, const SweepArgs& a,
     case 8: return launch_cfg<2, 16, 4, 256, 1, true, 3>(map, a, synth, field, grid, ns, smem, st);
     case 9: return launch_cfg<2, 8, 4, 256, 1, true, 3>(map, a, synth, field, grid, ns, smem, st);
     case 10: return launch_cfg<2, 4, 4, 256, 1, true, 3>(map, a, synth, field, grid, ns, smem, st);
+    case 11: return launch_cfg<6, 8, 2, 256, 2, true, 7>(map, a, synth, field, grid, ns, smem, st);
     default: return cudaErrorInvalidValue;
   }
 }
