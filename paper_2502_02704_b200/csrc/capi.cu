@@ -192,6 +192,8 @@ bool make_plan(pbgk_ctx* c, bool field, bool muscl, Plan& out) {
   if (const char* force = getenv("PBGK_FORCE_CFG")) {  // development knob
     cands.assign(1, atoi(force));
   }
+  if (const char* force = getenv("PBGK_FORCE_FIELD_CFG"))  // development knob
+    if (field) cands.assign(1, atoi(force));
   double best = 1e300;
   bool found = false;
   for (int id : cands) {

@@ -42,7 +42,10 @@ def run(nx, nv, vm, nsteps, periodic, reps=3, field=False, scheme="upwind"):
           f" ({prof.finalize_ms/(prof.sweep_ms+prof.finalize_ms):.3f})")
 
 
-if len(sys.argv) > 1 and sys.argv[1] == "muscl":
+if len(sys.argv) > 1 and sys.argv[1] == "one":  # one case: nx nv steps [field]
+    nx, nv, st = int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
+    run(nx, (nv,) * 3, 10.0 if nv == 48 else 8.0, st, True, field=len(sys.argv) > 5)
+elif len(sys.argv) > 1 and sys.argv[1] == "muscl":
     for sch in ("upwind", "muscl"):
         run(2048, (64, 64, 64), 8.0, 16, False, scheme=sch)
         run(512, (48, 48, 48), 10.0, 16, False, scheme=sch)
