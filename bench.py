@@ -227,26 +227,37 @@ def run_ours(args, w, world, rank, local):
         step()
     barrier()
 
+    def timed(nsteps):
+        ms = 0.0
+        for _ in range(nsteps):
+            flush.zero_()
+            barrier()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            step()
+            b.record(stream)
+            barrier()
+            ms += a.elapsed_time(b)
+        return ms
+
+    # headline: K steps with events around each step only (per-kernel events
+    # would sit between the sweep and finalize launches and defeat their
+    # programmatic dependent launch)
     clocks = ClockSampler(local)
     clocks.start()
-    lib.pbgk_profile_enable(ctx.h, 1)
     launches0 = lib.pbgk_launch_count()
-    total_ms = 0.0
-    for _ in range(args.steps):
-        flush.zero_()
-        barrier()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        step()
-        b.record(stream)
-        barrier()
-        total_ms += a.elapsed_time(b)
+    total_ms = timed(args.steps)
     launches = lib.pbgk_launch_count() - launches0
+    clk = clocks.stop()
+    # roofline: a second timed pass with per-launch CUDA events on the
+    # launching stream (sweep / finalize durations and algorithmic bytes)
+    prof_steps = max(1, min(args.steps, 2))
+    lib.pbgk_profile_enable(ctx.h, 1)
+    prof_ms = timed(prof_steps)
     prof = _lib.Profile()
     lib.pbgk_profile_read(ctx.h, prof)
     lib.pbgk_profile_enable(ctx.h, 0)
-    clk = clocks.stop()
 
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -272,9 +283,11 @@ def run_ours(args, w, world, rank, local):
                 "algorithmic_bytes_per_launch": 16.0 * w.cells,
                 "peak_kind": pk_kind, "kernel": "sweep_kernel",
                 "algorithmic_bytes_per_cell_update": 16,
-                "sweep_share_of_step": (prof.sweep_ms / total_ms) if total_ms > 0 else None,
-                "finalize_share_of_step": (prof.finalize_ms / total_ms) if total_ms > 0 else None,
-                "sweeps_timed": prof.sweeps}
+                "sweep_share_of_step": (prof.sweep_ms / prof_ms) if prof_ms > 0 else None,
+                "finalize_share_of_step": (prof.finalize_ms / prof_ms) if prof_ms > 0 else None,
+                "sweeps_timed": prof.sweeps,
+                "timed_in": "a second pass of %d step(s) with per-launch CUDA events on the "
+                            "launching stream (kept out of the headline pass)" % prof_steps}
 
     e2e = None
     if not args.no_e2e:

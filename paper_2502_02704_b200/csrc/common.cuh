@@ -11,6 +11,9 @@
 // Moments (SoA, 5*nx): rho, u_x, u_y, u_z, theta.
 // Partial marginals: part[(i*NT + tile)*PS + {0..A) m_x rows, A..A+By) m_y, A+By..) m_z].
 #pragma once
+#include <cuda_runtime.h>
+#include <utility>
+#include <cstdlib>
 #include <cstdint>
 
 namespace pbgk {
@@ -105,5 +108,25 @@ struct FluidArgs {
   int model;
   double diff;          // model 1: diffusivity D = m2 / tau
 };
+
+// Launch with programmatic dependent launch enabled: the kernel may begin
+// launching while the preceding kernel of the stream finishes; it must call
+// pdl_wait() (ptx.cuh) before consuming that kernel's results.
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, size_t smem,
+                                     cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  static const bool off = getenv("PBGK_NO_PDL") != nullptr;  // development A/B knob
+  attr[0].val.programmaticStreamSerializationAllowed = off ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 }  // namespace pbgk

@@ -15,6 +15,7 @@
 
 #include "common.cuh"
 #include "finalize_impl.cuh"
+#include "ptx.cuh"
 
 namespace pbgk {
 
@@ -27,6 +28,8 @@ namespace pbgk {
 constexpr int kFinThreads = PBGK_FIN_THREADS;
 
 __global__ void __launch_bounds__(kFinThreads, PBGK_FIN_MINB) finalize_kernel(const FinalArgs a) {
+  pdl_wait();  // the partials / moments come from the preceding kernel
+  pdl_trigger();
   extern __shared__ double sm[];
   __shared__ double sh[16];
   finalize_cell(a, blockIdx.x, sm, sh);
@@ -43,8 +46,7 @@ cudaError_t launch_finalize(const FinalArgs& a, cudaStream_t st) {
                                          (int)smem);
     if (e != cudaSuccess) return e;
   }
-  finalize_kernel<<<a.nx, kFinThreads, smem, st>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(finalize_kernel, a.nx, kFinThreads, smem, st, a);
 }
 
 cudaError_t launch_set_key(ErrKey* p, ErrKey v, cudaStream_t st) {

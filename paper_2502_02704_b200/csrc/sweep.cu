@@ -277,6 +277,10 @@ __global__ void __launch_bounds__(NTHR, MINB)
     for (int s = 0; s < ns; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
   }
+  // the prologue above reads only constant inputs; f, the tables and the
+  // partial buffer belong to the preceding kernels of the step chain
+  pdl_wait();
+  pdl_trigger();
   __syncthreads();
 
   // producer state (thread 0 only): loads run ns items ahead
@@ -865,8 +869,7 @@ static cudaError_t launch_cfg(const CUtensorMap& map, const SweepArgs& a, bool s
   if (fn == nullptr) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  fn<<<grid, NTHR, smem, st>>>(map, a, ns);
-  return cudaGetLastError();
+  return launch_pdl(fn, grid, NTHR, smem, st, map, a, ns);
 }
 
 // Shared memory the kernel needs for `ns` stages.
