@@ -27,7 +27,10 @@ namespace pbgk {
 #endif
 constexpr int kFinThreads = PBGK_FIN_THREADS;
 
-__global__ void __launch_bounds__(kFinThreads, PBGK_FIN_MINB) finalize_kernel(const FinalArgs a) {
+// MINB: resident CTAs per SM the register budget targets -- 16 (32 registers)
+// when there are enough cells to fill the GPU, 4 (no spills) for few cells.
+template <int MINB>
+__global__ void __launch_bounds__(kFinThreads, MINB) finalize_kernel(const FinalArgs a) {
   pdl_wait();  // the partials / moments come from the preceding kernel
   pdl_trigger();
   extern __shared__ double sm[];
@@ -41,12 +44,23 @@ cudaError_t launch_finalize(const FinalArgs& a, cudaStream_t st) {
   size_t smem = (size_t)2 * (a.nvx + a.nvy + a.nvz) * sizeof(double);
   if (a.mom_in == nullptr && a.mode != kFinIdentity)
     smem += (size_t)chunk_scratch(a.t, a.nvx, a.nvy, a.nvz) * sizeof(double);
+  int nsm = 148;
+  {
+    static int cached = 0;
+    if (!cached) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
+    }
+    if (cached > 0) nsm = cached;
+  }
+  // one wave at 4 CTAs/SM: registers; otherwise occupancy
+  auto k = (a.nx > nsm * 4) ? finalize_kernel<PBGK_FIN_MINB> : finalize_kernel<4>;
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  return launch_pdl(finalize_kernel, a.nx, kFinThreads, smem, st, a);
+  return launch_pdl(k, a.nx, kFinThreads, smem, st, a);
 }
 
 cudaError_t launch_set_key(ErrKey* p, ErrKey v, cudaStream_t st) {

@@ -213,7 +213,8 @@ static __device__ __forceinline__ void finalize_cell(const FinalArgs& a, int i, 
 
   if (tid == 0 && (rho <= 0.0 || th <= 0.0)) atomicMin(a.err, err_key(0, a.step, kErrLiftState));
   const double inv2t = 1.0 / (2.0 * th);
-  const double amp = rho / pow(6.283185307179586 * th, 1.5);
+  const double tt = 6.283185307179586 * th;
+  const double amp = rho / (tt * sqrt(tt));  // (2 pi theta)^1.5, ref/lifting.py:50
     for (int ax = 0; ax < 3; ++ax) {
     for (int j = tid; j < nv(ax); j += blockDim.x) {
       const double d = cs(ax)[j] - (ax == 0 ? u0 : (ax == 1 ? u1 : u2));
