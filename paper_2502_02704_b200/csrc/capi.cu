@@ -114,6 +114,7 @@ struct EvPair {
 struct pbgk_ctx {
   int g_model = 0;       // coarse G: 0 Euler (reference), 1 drift-diffusion (extension)
   int x_scheme = 0;      // 0 first-order upwind (reference), 1 MUSCL-minmod (extension)
+  int l2_keep = 0;       // f ping-pong small enough to live in L2 (sweep cache policies)
   int slot_reserve = 0;  // CTA slots the sweep grid leaves free (pipelined parareal side stream)
   double g_diff = 1.0;   // drift-diffusion D
   pbgk_grid_desc g;
@@ -379,6 +380,7 @@ int run_sweep(pbgk_ctx* c, int pid, bool field, const double* in, const double* 
   a.dtdv = dtdv;
   a.check_step = check_step;
   a.muscl = (c->x_scheme == 1 && dtdx != 0.0) ? 1 : 0;
+  a.l2_keep = c->l2_keep;
   if (a.muscl && field) return fail("MUSCL x transport has no v_x field term (use the upwind scheme)");
   const bool synth = (in == nullptr);
   const CUtensorMap* map = tensor_map(c, synth ? nullptr : in, p.t, p.cfg);
@@ -454,6 +456,7 @@ int pbgk_ctx_create(const pbgk_grid_desc* g, pbgk_ctx** out) {
   cudaDeviceProp prop;
   if (cudaGetDeviceProperties(&prop, c->dev) != cudaSuccess) return bail(fail("device query failed"));
   c->nsm = prop.multiProcessorCount;
+  if (const char* k = getenv("PBGK_L2KEEP")) c->l2_keep = atoi(k);  // development knob
   c->smem_optin = prop.sharedMemPerBlockOptin;
   c->smem_per_sm = prop.sharedMemPerMultiprocessor;
   // table row: [r, ls, gx(nvx), gy(nvy), gz(nvz)] padded to 16 bytes

@@ -220,7 +220,8 @@ __device__ __forceinline__ void lds_vec(const double* p, double (&x)[V]) {
 // Store of one lane's V outputs of a line: one 32-byte vector (V = 4), 16-byte
 // pairs (other even V) or masked scalars (odd V / partial rows).
 template <int V, int LZ, bool FAST>
-__device__ __forceinline__ void store_line(double* d, const double (&o)[V], unsigned zmask) {
+__device__ __forceinline__ void store_line(double* d, const double (&o)[V], unsigned zmask,
+                                           bool keep = false, uint64_t pol = 0) {
   if constexpr (V == 4) {
     if (FAST || zmask == 0xfu) {
       st_global_v4(d, o[0], o[1], o[2], o[3]);
@@ -229,7 +230,10 @@ __device__ __forceinline__ void store_line(double* d, const double (&o)[V], unsi
   } else if constexpr (V % 2 == 0) {
     if (FAST || zmask == (1u << V) - 1) {
 #pragma unroll
-      for (int v = 0; v < V; v += 2) st_global_v2(d + v, o[v], o[v + 1]);
+      for (int v = 0; v < V; v += 2) {
+        if (keep) st_global_v2_hint(d + v, o[v], o[v + 1], pol);
+        else st_global_v2(d + v, o[v], o[v + 1]);
+      }
       return;
     }
   }
@@ -317,11 +321,12 @@ __global__ void __launch_bounds__(NTHR, MINB)
     const int im = i + (a.bc == 3 ? 1 : 0);  // plane / row in memory (slab buffers are padded)
     mbar_arrive_expect_tx(bar, box_bytes + tab_bytes);
     if (!SYNTH) {
-#if PBGK_HINT_LOAD
-      tma_load_4d_hint(st, &fmap, tg.z0, tg.y0, tg.r0 - hoff, im, bar, pol_stream);
-#else
-      tma_load_4d(st, &fmap, tg.z0, tg.y0, tg.r0 - hoff, im, bar);
-#endif
+      // L2-resident ping-pong (f fits in L2): the loaded f*_{s-1} is dead
+      // after this read, the stored f*_s is re-read by the next step
+      if (PBGK_HINT_LOAD || a.l2_keep)
+        tma_load_4d_hint(st, &fmap, tg.z0, tg.y0, tg.r0 - hoff, im, bar, pol_stream);
+      else
+        tma_load_4d(st, &fmap, tg.z0, tg.y0, tg.r0 - hoff, im, bar);
     }
     tma_load_1d(st + box_bytes, a.tab + (size_t)im * a.TL, tab_bytes, bar);
   };
@@ -546,7 +551,7 @@ __global__ void __launch_bounds__(NTHR, MINB)
             }
             lp[k] = sl;
             if (FAST || (gdst != nullptr && ok)) {
-              store_line<V, LZ, FAST>(gdst + goff[k], o, zmask);
+              store_line<V, LZ, FAST>(gdst + goff[k], o, zmask, a.l2_keep != 0, pol_keep);
             }
           }
 #pragma unroll
@@ -645,7 +650,7 @@ __global__ void __launch_bounds__(NTHR, MINB)
             }
             lp[k] = sl;
             if (FAST || (gdst != nullptr && ok)) {
-              store_line<V, LZ, FAST>(gdst + goff[k], o, zmask);
+              store_line<V, LZ, FAST>(gdst + goff[k], o, zmask, a.l2_keep != 0, pol_keep);
             }
           }
 #pragma unroll
@@ -708,7 +713,7 @@ __global__ void __launch_bounds__(NTHR, MINB)
               }
               lp[k] = sl;
               if (FAST || (gdst != nullptr && ok)) {
-                store_line<V, LZ, FAST>(gdst + goff[k], o, zmask);
+                store_line<V, LZ, FAST>(gdst + goff[k], o, zmask, a.l2_keep != 0, pol_keep);
               }
             }
 #pragma unroll
