@@ -87,7 +87,10 @@ def load():
             "libpbgk.so is not built (%s); run `python -c 'import __graft_entry__ as g; "
             "g.build()'` — there is no CPU fallback" % LIB_PATH)
     lib = ctypes.CDLL(str(LIB_PATH))
+    dev_override = bool(os.environ.get("PBGK_LIB"))  # A/B of older builds: tolerate gaps
     for name, (res, args) in PROTOTYPES.items():
+        if dev_override and not hasattr(lib, name):
+            continue
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
