@@ -158,3 +158,39 @@ def test_no_cpu_fallback_without_device(monkeypatch):
     g = P.PhaseGrid(P.build_spatial_grid(0.0, 1.0, 4), P.build_velocity_grid(8.0, 8))
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         P.project(P.Distribution(np.ones((4, 8, 8, 8))), g)
+
+
+from hypothesis import given, settings, strategies as st  # noqa: E402
+
+
+@settings(max_examples=200, deadline=None)
+@given(st.integers(0, 5000), st.integers(1, 64))
+def test_partition_property(work, n_p):
+    # ref tests/test_parareal.py:199-230: exhaustive, contiguous, balanced
+    sizes, prev_end = [], 0
+    for r in range(n_p):
+        w = P.work_distribution(work, n_p, r)
+        assert w.start == prev_end + 1
+        prev_end = w.end if w.size else prev_end
+        sizes.append(w.size)
+        assert w == P.WorkRange(*O.work_range(work, n_p, r))
+    assert sum(sizes) == work and max(sizes) - min(sizes) <= 1
+
+
+@settings(max_examples=100, deadline=None)
+@given(st.integers(1, 80), st.integers(1, 80), st.integers(1, 9))
+def test_pipelined_rounds_cover_each_window_once(n_g, k, world):
+    # PipelinedRun deals windows k..n_g cyclically, one per rank per round
+    start = min(k, n_g)
+    windows = list(range(start, n_g + 1))
+    rounds = [windows[i:i + world] for i in range(0, len(windows), world)]
+    mine = [[wr[r] for wr in rounds if r < len(wr)] for r in range(world)]
+    assert sorted(sum(mine, [])) == windows
+    assert all(r == sorted(r) for r in mine)
+
+
+def test_velocity_centres_odd_symmetric_bitwise():
+    # ref tests/test_grid.py:47-52
+    for n in (1, 2, 7, 8, 16, 33, 48, 64):
+        c = P.build_velocity_grid(8.0, n).centers[0]
+        assert np.array_equal(c, -c[::-1])
