@@ -103,15 +103,11 @@ static __device__ __forceinline__ void finalize_cell(const FinalArgs& a, int i, 
   double* mx = sm;
   double* my = mx + nvx;
   double* mz = my + nvy;
-  double* gx = mz + nvz;
-  double* gy = gx + nvx;
-  double* gz = gy + nvy;
   // per-axis selectors (ternaries, not arrays: a runtime index would put
   // an array on the stack)
   auto nv = [&](int ax) { return ax == 0 ? nvx : (ax == 1 ? nvy : nvz); };
   auto cs = [&](int ax) { return ax == 0 ? a.cx : (ax == 1 ? a.cy : a.cz); };
   auto ms = [&](int ax) { return ax == 0 ? mx : (ax == 1 ? my : mz); };
-  auto gs = [&](int ax) { return ax == 0 ? gx : (ax == 1 ? gy : gz); };
 
   if (a.mode == kFinIdentity) {
     double* row = a.tab + (size_t)i * a.TL;
@@ -135,6 +131,9 @@ static __device__ __forceinline__ void finalize_cell(const FinalArgs& a, int i, 
     const int k1 = (list_len(T, 1) + kChunk - 1) / kChunk;
     const int k2 = (list_len(T, 2) + kChunk - 1) / kChunk;
     const int t1 = k0 * nvx, t2 = t1 + k1 * nvy, t3 = t2 + k2 * nvz;
+    // one chunk per entry (small tilings): the chunk sum IS the marginal
+    const bool single = (t3 == nvx + nvy + nvz);
+    double* dst = single ? sm : csum;
     for (int t = tid; t < t3; t += blockDim.x) {
       const int ax = t < t1 ? 0 : (t < t2 ? 1 : 2);
       const int q = t - (ax == 0 ? 0 : (ax == 1 ? t1 : t2));
@@ -143,24 +142,25 @@ static __device__ __forceinline__ void finalize_cell(const FinalArgs& a, int i, 
       const int len = list_len(T, ax);
       const EntryList e = entry_list(T, ax, j);
       const int q1 = min(len, (c + 1) * kChunk);
-      csum[t] = chunk_sum(P, T.PS, e, c * kChunk, q1);
+      dst[t] = chunk_sum(P, T.PS, e, c * kChunk, q1);
     }
     __syncthreads();
-    for (int j = tid; j < nvx + nvy + nvz; j += blockDim.x) {
-      const int ax = j < nvx ? 0 : (j < nvx + nvy ? 1 : 2);
-      const int jj = j - (ax == 0 ? 0 : (ax == 1 ? nvx : nvx + nvy));
-      const int n = ax == 0 ? nvx : (ax == 1 ? nvy : nvz);
-      const int kk = ax == 0 ? k0 : (ax == 1 ? k1 : k2);
-      const double* cs0 = csum + (ax == 0 ? 0 : (ax == 1 ? t1 : t2)) + jj;
-      double s = 0.0;
-      for (int c = 0; c < kk; ++c) s += cs0[c * n];
-      sm[j] = s;  // mx | my | mz are contiguous
+    if (!single) {
+      for (int j = tid; j < nvx + nvy + nvz; j += blockDim.x) {
+        const int ax = j < nvx ? 0 : (j < nvx + nvy ? 1 : 2);
+        const int jj = j - (ax == 0 ? 0 : (ax == 1 ? nvx : nvx + nvy));
+        const int n = ax == 0 ? nvx : (ax == 1 ? nvy : nvz);
+        const int kk = ax == 0 ? k0 : (ax == 1 ? k1 : k2);
+        const double* cs0 = csum + (ax == 0 ? 0 : (ax == 1 ? t1 : t2)) + jj;
+        double s = 0.0;
+        for (int c = 0; c < kk; ++c) s += cs0[c * n];
+        sm[j] = s;  // mx | my | mz are contiguous
+      }
+      __syncthreads();
     }
     // finiteness of f* (all its values feed these sums; a NaN/Inf anywhere
-    // leaves a non-finite marginal) -- the guard of ref/kinetic.py:157-159
-    int bad = 0;
-    for (int j = tid; j < nvx + nvy + nvz; j += blockDim.x) bad |= !isfinite(sm[j]);
-    nonfinite = __syncthreads_or(bad);
+    // leaves a non-finite marginal) -- the guard of ref/kinetic.py:157-159;
+    // warps 1..3 test their axis while reducing the folded first moment
     if (warp == 0) {
       double s = 0.0;
       for (int j = lane; j < nvx; j += 32) s += mx[j];
@@ -174,9 +174,16 @@ static __device__ __forceinline__ void finalize_cell(const FinalArgs& a, int i, 
       double s = 0.0;
       for (int j = lane; j < h; j += 32) s += (m[j] - m[n - 1 - j]) * c[j];
       s = warp_allsum(s);
-      if (lane == 0) sh[1 + ax] = s;
+      int bad = 0;
+      for (int j = lane; j < n; j += 32) bad |= !isfinite(m[j]);
+      bad = __any_sync(0xffffffffu, bad);
+      if (lane == 0) {
+        sh[1 + ax] = s;
+        sh[12 + ax] = bad ? 1.0 : 0.0;
+      }
     }
     __syncthreads();
+    nonfinite = (sh[12] != 0.0) || (sh[13] != 0.0) || (sh[14] != 0.0);
     rho = sh[0] * a.dvol;
     u0 = (sh[1] * a.dvol) / rho;
     u1 = (sh[2] * a.dvol) / rho;
@@ -215,20 +222,29 @@ static __device__ __forceinline__ void finalize_cell(const FinalArgs& a, int i, 
   const double inv2t = 1.0 / (2.0 * th);
   const double tt = 6.283185307179586 * th;
   const double amp = rho / (tt * sqrt(tt));  // (2 pi theta)^1.5, ref/lifting.py:50
-    for (int ax = 0; ax < 3; ++ax) {
-    for (int j = tid; j < nv(ax); j += blockDim.x) {
-      const double d = cs(ax)[j] - (ax == 0 ? u0 : (ax == 1 ? u1 : u2));
+  double* row = a.tab + (size_t)i * a.TL;
+  // warp a < 3: the Maxwellian factors of axis a, their sum (lane-strided
+  // sequential + xor butterfly, the fixed tree of every reduction here) and
+  // the row segment; warp 3: the row's zero padding
+  if (warp < 3) {
+    const int ax = warp;
+    const int n = nv(ax);
+    const double* c = cs(ax);
+    const double ua = ax == 0 ? u0 : (ax == 1 ? u1 : u2);
+    const int off = ax == 0 ? a.gxo : (ax == 1 ? a.gyo : a.gzo);
+    double s = 0.0;
+    for (int j = lane; j < n; j += 32) {
+      const double d = c[j] - ua;
       double g = exp(-(d * d) * inv2t);
       if (ax == 0) g = g * amp;
-      gs(ax)[j] = g;
+      s += g;
+      row[off + j] = g;
     }
-  }
-  __syncthreads();
-  if (warp < 3) {
-    double s = 0.0;
-    for (int j = lane; j < nv(warp); j += 32) s += gs(warp)[j];
     s = warp_allsum(s);
-    if (lane == 0) sh[8 + warp] = s;
+    if (lane == 0) sh[8 + ax] = s;
+  } else if (warp == 3) {
+    for (int j = a.gyo + nvy + lane; j < a.gzo; j += 32) row[j] = 0.0;
+    for (int j = a.gzo + nvz + lane; j < a.TL; j += 32) row[j] = 0.0;
   }
   __syncthreads();
   double r = 0.0, ls = 1.0;
@@ -244,20 +260,14 @@ static __device__ __forceinline__ void finalize_cell(const FinalArgs& a, int i, 
       ls = scale;
     }
   }
-  // f_s = R_s(f*_s) is finite iff f*_s and the table row are (BlowUpError(step))
-  if (a.mode == kFinRelax && tid == 0 &&
-      (nonfinite || !isfinite(r) || !isfinite(ls) || !isfinite(amp) || !isfinite(u0) ||
-       !isfinite(u1) || !isfinite(u2) || !isfinite(th)))
-    atomicMin(a.err, err_key(0, a.step, kErrNonFinite));
-  double* row = a.tab + (size_t)i * a.TL;
-  for (int j = tid; j < a.TL; j += blockDim.x) {
-    double v = 0.0;
-    if (j == 0) v = r;
-    else if (j == 1) v = ls;
-    else if (j >= a.gxo && j < a.gxo + nvx) v = gx[j - a.gxo];
-    else if (j >= a.gyo && j < a.gyo + nvy) v = gy[j - a.gyo];
-    else if (j >= a.gzo && j < a.gzo + nvz) v = gz[j - a.gzo];
-    row[j] = v;
+  if (tid == 0) {
+    row[0] = r;
+    row[1] = ls;
+    // f_s = R_s(f*_s) is finite iff f*_s and the table row are (BlowUpError(step))
+    if (a.mode == kFinRelax &&
+        (nonfinite || !isfinite(r) || !isfinite(ls) || !isfinite(amp) || !isfinite(u0) ||
+         !isfinite(u1) || !isfinite(u2) || !isfinite(th)))
+      atomicMin(a.err, err_key(0, a.step, kErrNonFinite));
   }
 }
 
