@@ -338,7 +338,8 @@ SweepArgs base_args(pbgk_ctx* c, const Plan& p) {
   a.bc = c->g.bc;
   a.part = c->d_part;
   a.err = c->d_err;
-  if (const char* d = getenv("PBGK_DEBUG")) a.debug = atoi(d);  // development ablations
+  static const int debug = getenv("PBGK_DEBUG") ? atoi(getenv("PBGK_DEBUG")) : 0;  // dev ablations
+  a.debug = debug & ~2;  // bit 2 (no CTA barrier) was removed: it races the TMA ring
   return a;
 }
 

@@ -65,7 +65,7 @@ struct SweepArgs {
   int check_step;    // >0: flag non-finite f_pre as step `check_step`
   int muscl;         // 1: MUSCL (minmod) x transport instead of first-order upwind
   int l2_keep;       // 1: f stores evict_last / loads evict_first (f ping-pong fits in L2)
-  int debug;         // development ablations (PBGK_DEBUG): 1 no reductions, 2 no CTA barrier
+  int debug;         // development ablations (PBGK_DEBUG): 1 no reductions, 4 copy-through
 };
 
 enum FinalMode : int {

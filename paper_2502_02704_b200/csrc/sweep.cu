@@ -782,7 +782,7 @@ __global__ void __launch_bounds__(NTHR, MINB)
       }
     }
 
-    if (!(a.debug & 2)) __syncthreads();
+    __syncthreads();
     if (TMA && tid == ptid && !prod.done()) {
       fence_proxy_async();
       issue_next();
