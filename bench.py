@@ -42,8 +42,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=lambda s: s if s == "3b" else int(s), default=4,
-                    choices=[0, 1, 2, 3, "3b", 4])
+    ap.add_argument("--config", type=lambda s: s if s in ("3b", "0t") else int(s), default=4,
+                    choices=[0, "0t", 1, 2, 3, "3b", 4])
     ap.add_argument("--eps", type=float, default=None)
     ap.add_argument("--bc", default=None, choices=["absorbing", "outflow", "periodic"],
                     help="override the workload's x boundary")
@@ -149,7 +149,7 @@ class ClockSampler:
 def build_problem(w):
     import paper_2502_02704_b200 as P
     phase = P.PhaseGrid(P.build_spatial_grid(w.x_min, w.x_max, w.nx),
-                        P.build_velocity_grid(w.v_max, w.nv))
+                        P.build_velocity_grid(w.v_max, w.nv, quadrature=w.quadrature))
     bc = P.BoundaryKind(w.bc)
     disc = P.Discretization(phase, P.build_time_grids(w.t_final, w.n_g, max(w.n_f, w.n_g)), bc)
     E = w.force()

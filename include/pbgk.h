@@ -129,6 +129,12 @@ int pbgk_parareal_correct(pbgk_ctx* ctx, int n_g, int start, double* snaps, cons
  * (rho, u = 0, theta = 1), D = `diffusivity` (> 0). */
 int pbgk_fluid_model(pbgk_ctx* ctx, int model, double diffusivity);
 
+/* Velocity quadrature of the context: 0 = the reference's midpoint cells
+ * (default), 1 = trapezoidal (EXTENSION: BASELINE config 0's wording; n
+ * nodes on [-v_max, v_max] including the ends, dv = 2 v_max/(n-1), end
+ * nodes weigh 1/2 in every velocity sum).  Call before any use. */
+int pbgk_ctx_set_quadrature(pbgk_ctx* ctx, int quadrature);
+
 /* x transport of every sweep on this context: 0 = the reference's first-order
  * upwind flux (default); 1 = MUSCL reconstruction with the minmod limiter
  * (EXTENSION: BASELINE north_star "upwind/MUSCL", PAPER flux limiters;

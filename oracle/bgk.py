@@ -62,16 +62,31 @@ class Mesh:
     nx: int
     v_max: float
     nv: tuple
+    quadrature: str = "midpoint"
 
     def __post_init__(self):
         self.nv = tuple(int(n) for n in self.nv)
         # ref/grid.py:95-96
         self.dx = (self.x_max - self.x_min) / self.nx
         self.xc = self.x_min + (np.arange(self.nx) + 0.5) * self.dx
-        # ref/grid.py:100-103, 114-115
-        self.dv = tuple(2.0 * self.v_max / n for n in self.nv)
-        self.vc = tuple((np.arange(n) - (n - 1) / 2.0) * (2.0 * self.v_max / n)
-                        for n in self.nv)
+        if self.quadrature == "trapezoid":
+            # ORACLE EXTENSION (BASELINE config 0's "trapezoidal quadrature"; the
+            # reference has midpoint only): n nodes on
+            # [-v_max, v_max] including the ends, dv = 2 v_max/(n-1), weights
+            # dv * (1/2 at the two end nodes, 1 elsewhere) on every velocity sum
+            if min(self.nv) < 2:
+                raise OracleConfigError("trapezoidal quadrature needs >= 2 nodes per axis")
+            self.dv = tuple(2.0 * self.v_max / (n - 1) for n in self.nv)
+            self.vc = tuple((np.arange(n) - (n - 1) / 2.0) * (2.0 * self.v_max / (n - 1))
+                            for n in self.nv)
+            self.wq = tuple(np.where((np.arange(n) == 0) | (np.arange(n) == n - 1), 0.5, 1.0)
+                            for n in self.nv)
+        else:
+            # ref/grid.py:100-103, 114-115
+            self.dv = tuple(2.0 * self.v_max / n for n in self.nv)
+            self.vc = tuple((np.arange(n) - (n - 1) / 2.0) * (2.0 * self.v_max / n)
+                            for n in self.nv)
+            self.wq = None
         # ref/grid.py:57-59
         self.dvol = self.dv[0] * self.dv[1] * self.dv[2]
 
@@ -85,10 +100,16 @@ def coarse_grid(t_final: float, n_g: int, n_f: int):
 # moments: P (ref/moments.py:80-129)
 # --------------------------------------------------------------------------
 
-def marginals(f: np.ndarray):
-    """Three per-cell velocity marginals (ref/moments.py:100)."""
-    return (np.add.reduce(f, axis=(2, 3)), np.add.reduce(f, axis=(1, 3)),
-            np.add.reduce(f, axis=(1, 2)))
+def marginals(f: np.ndarray, mesh: Optional[Mesh] = None):
+    """Three per-cell velocity marginals (ref/moments.py:100).  Trapezoidal
+    meshes weight the two summed axes (exact: the weights are 1/2 or 1)."""
+    if mesh is None or mesh.wq is None:
+        return (np.add.reduce(f, axis=(2, 3)), np.add.reduce(f, axis=(1, 3)),
+                np.add.reduce(f, axis=(1, 2)))
+    wx, wy, wz = mesh.wq
+    return (np.add.reduce(f * (wy[:, None] * wz[None, :])[None, None], axis=(2, 3)),
+            np.add.reduce(f * (wx[:, None] * wz[None, :])[None, :, None, :], axis=(1, 3)),
+            np.add.reduce(f * (wx[:, None] * wy[None, :])[None, :, :, None], axis=(1, 2)))
 
 
 def _mirror_weighted(m: np.ndarray, c: np.ndarray) -> np.ndarray:
@@ -101,24 +122,26 @@ def _mirror_weighted(m: np.ndarray, c: np.ndarray) -> np.ndarray:
 def moments_of(margs, mesh: Mesh):
     """(rho, u, theta) from marginals (ref/moments.py:101-113)."""
     w = mesh.dvol
-    rho = np.add.reduce(margs[0], axis=1) * w
+    q = mesh.wq  # trapezoid: the remaining axis is weighted here
+    m0 = margs[0] if q is None else margs[0] * q[0]
+    rho = np.add.reduce(m0, axis=1) * w
     if np.any(rho <= 0.0):
         raise OracleDegenerate("rho <= 0 in projection at cell %d"
                                % int(np.argmax(rho <= 0.0)))
-    ru = np.stack([_mirror_weighted(margs[a], mesh.vc[a]) for a in range(3)],
-                  axis=1) * w
+    ru = np.stack([_mirror_weighted(margs[a], mesh.vc[a] if q is None else mesh.vc[a] * q[a])
+                   for a in range(3)], axis=1) * w
     u = ru / rho[:, None]
     acc = np.zeros_like(rho)
     for a in range(3):
         d = mesh.vc[a][None, :] - u[:, a, None]
-        acc += np.einsum("ij,ij->i", d * d, margs[a])
+        acc += np.einsum("ij,ij->i", d * d, margs[a] if q is None else margs[a] * q[a])
     theta = acc * w / (3.0 * rho)
     return rho, u, theta
 
 
 def project(f: np.ndarray, mesh: Mesh):
     """P: ref/moments.py:91-113."""
-    return moments_of(marginals(f), mesh)
+    return moments_of(marginals(f, mesh), mesh)
 
 
 # --------------------------------------------------------------------------
@@ -143,7 +166,9 @@ def lift(rho, u, theta, mesh: Mesh, normalize: bool = False) -> np.ndarray:
     gxa, gy, gz = maxwell_factors(rho, u, theta, mesh)
     f = gxa[:, :, None, None] * gy[:, None, :, None] * gz[:, None, None, :]
     if normalize:
-        mass = np.add.reduce(f, axis=(1, 2, 3)) * mesh.dvol
+        fw = f if mesh.wq is None else f * (mesh.wq[0][:, None, None] * mesh.wq[1][None, :, None]
+                                             * mesh.wq[2][None, None, :])[None]
+        mass = np.add.reduce(fw, axis=(1, 2, 3)) * mesh.dvol
         f *= (rho / mass)[:, None, None, None]
     return f
 

@@ -48,6 +48,7 @@ PROTOTYPES = {
     "pbgk_set_grid_reserve": (c_int, [_P, _I]),
     "pbgk_set_x_scheme": (c_int, [_P, _I]),
     "pbgk_table_len": (c_int, [_P]),
+    "pbgk_ctx_set_quadrature": (c_int, [_P, _I]),
     "pbgk_ctx_set_dx": (c_int, [_P, _D]),
     "pbgk_slab_tables": (c_int, [_P, _I, _P, _P, _P, _P]),
     "pbgk_slab_sweep": (c_int, [_P, _P, _P, _P, _D, _P, _D, _P]),

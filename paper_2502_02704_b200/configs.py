@@ -48,6 +48,7 @@ class Workload:
     outflow: bool = False  # zero-gradient kinetic ghosts (extension) instead of absorbing
     alpha: int = 0  # 1: diffusive scaling (extension)
     g_model: str = "euler"  # "drift_diffusion": the diffusive G (extension)
+    quadrature: str = "midpoint"  # "trapezoid": BASELINE config 0's wording (extension)
 
     @property
     def bc(self) -> str:
@@ -110,7 +111,11 @@ class Workload:
 
 def config(idx, eps: Optional[float] = None) -> Workload:
     """BASELINE.json configs[idx]; config 3 is the pinned alpha=0 variant 3a,
-    ``"3b"`` the alpha = 1 drift-diffusion variant."""
+    ``"3b"`` the alpha = 1 drift-diffusion variant, ``"0t"`` config 0 with the
+    trapezoidal velocity quadrature BASELINE.json names."""
+    if idx == "0t":
+        return Workload("cfg0t-sod-64x16^3-trapezoid", 64, (16,) * 3, 8.0, 1e-2, False, 0.1, 8, 8, 2,
+                        1e-300, "parareal", outflow=True, quadrature="trapezoid")
     if idx == "3b":
         return Workload("cfg3b-diffusive-1024x32^3", 1024, (32,) * 3, 8.0, 1e-2, True, 0.05, 32, 32, 5,
                         1e-8, "parareal", force_kind="sin", init="cos", alpha=1,

@@ -115,6 +115,7 @@ struct pbgk_ctx {
   int g_model = 0;       // coarse G: 0 Euler (reference), 1 drift-diffusion (extension)
   int x_scheme = 0;      // 0 first-order upwind (reference), 1 MUSCL-minmod (extension)
   int l2_keep = 0;       // f ping-pong small enough to live in L2 (sweep cache policies)
+  int quad = 0;          // velocity quadrature: 0 midpoint (reference), 1 trapezoidal (extension)
   int slot_reserve = 0;  // CTA slots the sweep grid leaves free (pipelined parareal side stream)
   double g_diff = 1.0;   // drift-diffusion D
   pbgk_grid_desc g;
@@ -360,6 +361,7 @@ FinalArgs fin_args(pbgk_ctx* c, const Plan& p) {
   f.gyo = c->gyo;
   f.gzo = c->gzo;
   f.err = c->d_err;
+  f.trap = c->quad;
   f.tau = 1.0;
   f.eps = 1.0;
   return f;
@@ -382,6 +384,7 @@ int run_sweep(pbgk_ctx* c, int pid, bool field, const double* in, const double* 
   a.check_step = check_step;
   a.muscl = (c->x_scheme == 1 && dtdx != 0.0) ? 1 : 0;
   a.l2_keep = c->l2_keep;
+  a.trap = c->quad;
   if (a.muscl && field) return fail("MUSCL x transport has no v_x field term (use the upwind scheme)");
   const bool synth = (in == nullptr);
   const CUtensorMap* map = tensor_map(c, synth ? nullptr : in, p.t, p.cfg);
@@ -726,6 +729,25 @@ int pbgk_parareal_correct(pbgk_ctx* c, int n_g, int start, double* snaps, const 
 }
 
 int pbgk_table_len(const pbgk_ctx* c) { return c ? c->TL : -1; }
+
+int pbgk_ctx_set_quadrature(pbgk_ctx* c, int quadrature) {
+  if (!c) return fail("pbgk_ctx_set_quadrature: null context");
+  if (quadrature != 0 && quadrature != 1) return fail("pbgk_ctx_set_quadrature: 0 (midpoint) or 1 (trapezoid)");
+  const int nv[3] = {c->g.nvx, c->g.nvy, c->g.nvz};
+  if (quadrature == 1 && (nv[0] < 2 || nv[1] < 2 || nv[2] < 2))
+    return fail("pbgk_ctx_set_quadrature: trapezoidal quadrature needs >= 2 nodes per axis");
+  if (cudaSetDevice(c->dev) != cudaSuccess) return fail("cudaSetDevice");
+  for (int a = 0; a < 3; ++a) {
+    c->dv[a] = quadrature == 1 ? 2.0 * c->g.v_max / (nv[a] - 1) : 2.0 * c->g.v_max / nv[a];
+    std::vector<double> h(nv[a]);
+    for (int j = 0; j < nv[a]; ++j) h[j] = ((double)j - (nv[a] - 1) / 2.0) * c->dv[a];
+    if (cudaMemcpy(c->d_c[a], h.data(), nv[a] * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
+      return fail("cudaMemcpy");
+  }
+  c->dvol = c->dv[0] * c->dv[1] * c->dv[2];
+  c->quad = quadrature;
+  return 0;
+}
 
 int pbgk_ctx_set_dx(pbgk_ctx* c, double dx) {
   if (!c) return fail("pbgk_ctx_set_dx: null context");

@@ -65,6 +65,7 @@ struct SweepArgs {
   int check_step;    // >0: flag non-finite f_pre as step `check_step`
   int muscl;         // 1: MUSCL (minmod) x transport instead of first-order upwind
   int l2_keep;       // 1: f stores evict_last / loads evict_first (f ping-pong fits in L2)
+  int trap;          // 1: trapezoidal velocity quadrature (end nodes weigh 1/2)
   int debug;         // development ablations (PBGK_DEBUG): 1 no reductions, 4 copy-through
 };
 
@@ -94,6 +95,7 @@ struct FinalArgs {
   ErrKey* err;
   int step;
   int check_finite;      // kFinProject: flag non-finite marginals as BlowUpError(step)
+  int trap;              // trapezoidal velocity quadrature (end nodes weigh 1/2)
 };
 
 // Coarse propagator arguments (fluid.cu).  model 0: the reference's Rusanov

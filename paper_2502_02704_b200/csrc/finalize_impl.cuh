@@ -161,9 +161,12 @@ static __device__ __forceinline__ void finalize_cell(const FinalArgs& a, int i, 
     // finiteness of f* (all its values feed these sums; a NaN/Inf anywhere
     // leaves a non-finite marginal) -- the guard of ref/kinetic.py:157-159;
     // warps 1..3 test their axis while reducing the folded first moment
+    // trapezoid: the marginals carry the weights of the two summed axes; the
+    // remaining axis is weighted here (end nodes 1/2, exact)
+    auto wq = [&](int j, int n) { return (a.trap && (j == 0 || j == n - 1)) ? 0.5 : 1.0; };
     if (warp == 0) {
       double s = 0.0;
-      for (int j = lane; j < nvx; j += 32) s += mx[j];
+      for (int j = lane; j < nvx; j += 32) s += a.trap ? mx[j] * wq(j, nvx) : mx[j];
       s = warp_allsum(s);
       if (lane == 0) sh[0] = s;
     } else if (warp < 4) {
@@ -172,7 +175,7 @@ static __device__ __forceinline__ void finalize_cell(const FinalArgs& a, int i, 
       const double* m = ms(ax);
       const double* c = cs(ax);
       double s = 0.0;
-      for (int j = lane; j < h; j += 32) s += (m[j] - m[n - 1 - j]) * c[j];
+      for (int j = lane; j < h; j += 32) s += (m[j] - m[n - 1 - j]) * (a.trap ? c[j] * wq(j, n) : c[j]);
       s = warp_allsum(s);
       int bad = 0;
       for (int j = lane; j < n; j += 32) bad |= !isfinite(m[j]);
@@ -196,7 +199,7 @@ static __device__ __forceinline__ void finalize_cell(const FinalArgs& a, int i, 
       double s = 0.0;
       for (int j = lane; j < n; j += 32) {
         const double d = c[j] - ua;
-        s += (d * d) * m[j];
+        s += (d * d) * (a.trap ? m[j] * wq(j, n) : m[j]);
       }
       s = warp_allsum(s);
       if (lane == 0) sh[4 + warp] = s;
@@ -237,7 +240,7 @@ static __device__ __forceinline__ void finalize_cell(const FinalArgs& a, int i, 
       const double d = c[j] - ua;
       double g = exp(-(d * d) * inv2t);
       if (ax == 0) g = g * amp;
-      s += g;
+      s += (a.trap && (j == 0 || j == n - 1)) ? 0.5 * g : g;
       row[off + j] = g;
     }
     s = warp_allsum(s);

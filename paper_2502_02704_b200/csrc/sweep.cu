@@ -242,9 +242,11 @@ __device__ __forceinline__ void store_line(double* d, const double (&o)[V], unsi
     if (FAST || ((zmask >> v) & 1u)) d[zpos<V, LZ>(0, v)] = o[v];
 }
 
-template <int V, int LZ, int K, int NTHR, int MINB, bool SYNTH, bool FIELD, bool TMA, bool MUSCL>
+template <int V, int LZ, int K, int NTHR, int MINB, bool SYNTH, bool FIELD, bool TMA, bool MUSCL,
+          bool TRAP>
 __global__ void __launch_bounds__(NTHR, MINB)
     sweep_kernel(const __grid_constant__ CUtensorMap fmap, const SweepArgs a, int ns) {
+  static_assert(!(TRAP && FIELD), "the field term is defined on midpoint velocity cells only");
   static_assert(!(MUSCL && FIELD), "MUSCL x transport has no v_x field term");
   constexpr int LEAD = MUSCL ? 2 : 1, TRAIL = MUSCL ? 1 : 0;
   constexpr int NL = NTHR / LZ;  // line groups
@@ -364,6 +366,9 @@ __global__ void __launch_bounds__(NTHR, MINB)
   int gxi[K], gyi[K], goff[K];
   double cvx[K];
   unsigned vmask = 0;  // bit k: line k is inside the tile and the grid
+  // trapezoidal quadrature (a.trap): lines / lanes on the end nodes of an axis
+  // take weight 1/2 (exact) in the marginal partials
+  unsigned xedge = 0, yedge = 0, zedge = 0;
   unsigned zmask = 0;  // bit v: element v of this lane is inside the grid
   bool full = false;   // every line and element of this thread is valid
   int cur_tile = -1;
@@ -392,6 +397,7 @@ __global__ void __launch_bounds__(NTHR, MINB)
       cur_tile = t;
       tg = tile_geom(T, a.nvx, t);
       vmask = 0;
+      xedge = yedge = zedge = 0;
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const int l = line_of(k);
@@ -403,11 +409,16 @@ __global__ void __launch_bounds__(NTHR, MINB)
         gyi[k] = a.gyo + jy;
         goff[k] = (jx * a.nvy + jy) * a.nvz + tg.z0 + zpos<V, LZ>(lz, 0);
         cvx[k] = SCX[jx];
+        if (jx == 0 || jx == a.nvx - 1) xedge |= 1u << k;
+        if (jy == 0 || jy == a.nvy - 1) yedge |= 1u << k;
       }
       zmask = 0;
 #pragma unroll
-      for (int v = 0; v < V; ++v)
-        if (tg.z0 + zpos<V, LZ>(lz, v) < a.nvz) zmask |= 1u << v;
+      for (int v = 0; v < V; ++v) {
+        const int jz = tg.z0 + zpos<V, LZ>(lz, v);
+        if (jz < a.nvz) zmask |= 1u << v;
+        if (jz == 0 || jz == a.nvz - 1) zedge |= 1u << v;
+      }
       full = (vmask == (1u << K) - 1) && (zmask == (1u << V) - 1);
     }
     const int i = item_plane(nx, a.bc, tg, p);
@@ -461,6 +472,19 @@ __global__ void __launch_bounds__(NTHR, MINB)
       double pz[V];
 #pragma unroll
       for (int v = 0; v < V; ++v) pz[v] = 0.0;
+      // z partial += m (weight of the line's x, y nodes), line total += m
+      // (weight of the z node); the weights are 1 except for trapezoidal
+      // quadrature, where end nodes count 1/2 (exact scalings)
+      auto accum = [&](double m, int k, int v, double& sl) {
+        if constexpr (TRAP) {
+          const double wl = (((xedge >> k) & 1u) ? 0.5 : 1.0) * (((yedge >> k) & 1u) ? 0.5 : 1.0);
+          pz[v] += m * wl;
+          sl += m * (((zedge >> v) & 1u) ? 0.5 : 1.0);
+        } else {
+          pz[v] += m;
+          sl += m;
+        }
+      };
 
       // One plane: relax R_{s-1} of the loaded f*_{s-1}, transport, store,
       // marginal partials.  FAST: full tile, transport on, output plane
@@ -546,8 +570,7 @@ __global__ void __launch_bounds__(NTHR, MINB)
 #pragma unroll
             for (int v = 0; v < V; ++v) {
               const double m = FAST ? o[v] : ((ok && ((zmask >> v) & 1u)) ? o[v] : 0.0);
-              pz[v] += m;
-              sl += m;
+              accum(m, k, v, sl);
             }
             lp[k] = sl;
             if (FAST || (gdst != nullptr && ok)) {
@@ -645,8 +668,7 @@ __global__ void __launch_bounds__(NTHR, MINB)
 #pragma unroll
             for (int v = 0; v < V; ++v) {
               const double m = FAST ? o[v] : ((ok && ((zmask >> v) & 1u)) ? o[v] : 0.0);
-              pz[v] += m;
-              sl += m;
+              accum(m, k, v, sl);
             }
             lp[k] = sl;
             if (FAST || (gdst != nullptr && ok)) {
@@ -708,8 +730,7 @@ __global__ void __launch_bounds__(NTHR, MINB)
 #pragma unroll
               for (int v = 0; v < V; ++v) {
                 const double m = FAST ? o[v] : ((ok && ((zmask >> v) & 1u)) ? o[v] : 0.0);
-                pz[v] += m;
-                sl += m;
+                accum(m, k, v, sl);
               }
               lp[k] = sl;
               if (FAST || (gdst != nullptr && ok)) {
@@ -799,7 +820,10 @@ __global__ void __launch_bounds__(NTHR, MINB)
       if (o < T.A) {
         if (tg.r0 + o < tg.r1) {
           double s2 = 0.0;
-          for (int b = 0; b < T.By; ++b) s2 += LTb[o * T.By + b];
+          for (int b = 0; b < T.By; ++b) {
+            const int y = tg.y0 + b;
+            s2 += (TRAP && (y == 0 || y == a.nvy - 1)) ? 0.5 * LTb[o * T.By + b] : LTb[o * T.By + b];
+          }
           
 #if PBGK_HINT_PART
           st_global_f64_hint(dst + o, s2, pol_keep);
@@ -812,7 +836,10 @@ __global__ void __launch_bounds__(NTHR, MINB)
         const int b = o - T.A;
         if (tg.y0 + b < a.nvy) {
           double s2 = 0.0;
-          for (int aa = 0; aa < T.A; ++aa) s2 += LTb[aa * T.By + b];
+          for (int aa = 0; aa < T.A; ++aa) {
+            const int x = tg.r0 + aa;
+            s2 += (TRAP && (x == 0 || x == a.nvx - 1)) ? 0.5 * LTb[aa * T.By + b] : LTb[aa * T.By + b];
+          }
           
 #if PBGK_HINT_PART
           st_global_f64_hint(dst + T.A + b, s2, pol_keep);
@@ -851,24 +878,38 @@ __global__ void __launch_bounds__(NTHR, MINB)
 // ---------------------------------------------------------------------------
 
 // MODES: bit 0 = first-order upwind kernels, bit 1 = MUSCL kernels, bit 2 =
-// upwind with the v_x field term; a shape only instantiates what it serves.
+// upwind with the v_x field term, bit 3 = trapezoidal-quadrature variants of
+// the bit 0 / bit 1 kernels; a shape only instantiates what it serves.
 template <int V, int LZ, int K, int NTHR, int MINB, bool TMA, int MODES>
 static cudaError_t launch_cfg(const CUtensorMap& map, const SweepArgs& a, bool synth, bool field,
                               int grid, int ns, size_t smem, cudaStream_t st) {
   void (*fn)(const CUtensorMap, const SweepArgs, int) = nullptr;
-  if (a.muscl) {
+  constexpr bool TR = (MODES & 8) != 0;
+  if (a.trap) {
+    if constexpr (TR) {
+      if (a.muscl) {
+        if constexpr ((MODES & 2) != 0)
+          fn = synth ? sweep_kernel<V, LZ, K, NTHR, MINB, true, false, TMA, true, true>
+                     : sweep_kernel<V, LZ, K, NTHR, MINB, false, false, TMA, true, true>;
+      } else if (!field) {
+        if constexpr ((MODES & 1) != 0)
+          fn = synth ? sweep_kernel<V, LZ, K, NTHR, MINB, true, false, TMA, false, true>
+                     : sweep_kernel<V, LZ, K, NTHR, MINB, false, false, TMA, false, true>;
+      }
+    }
+  } else if (a.muscl) {
     if constexpr ((MODES & 2) != 0)
-      fn = synth ? sweep_kernel<V, LZ, K, NTHR, MINB, true, false, TMA, true>
-                 : sweep_kernel<V, LZ, K, NTHR, MINB, false, false, TMA, true>;
+      fn = synth ? sweep_kernel<V, LZ, K, NTHR, MINB, true, false, TMA, true, false>
+                 : sweep_kernel<V, LZ, K, NTHR, MINB, false, false, TMA, true, false>;
   } else {
     if (field) {
       if constexpr ((MODES & 4) != 0)
-        fn = synth ? sweep_kernel<V, LZ, K, NTHR, MINB, true, true, TMA, false>
-                   : sweep_kernel<V, LZ, K, NTHR, MINB, false, true, TMA, false>;
+        fn = synth ? sweep_kernel<V, LZ, K, NTHR, MINB, true, true, TMA, false, false>
+                   : sweep_kernel<V, LZ, K, NTHR, MINB, false, true, TMA, false, false>;
     } else {
       if constexpr ((MODES & 1) != 0)
-        fn = synth ? sweep_kernel<V, LZ, K, NTHR, MINB, true, false, TMA, false>
-                   : sweep_kernel<V, LZ, K, NTHR, MINB, false, false, TMA, false>;
+        fn = synth ? sweep_kernel<V, LZ, K, NTHR, MINB, true, false, TMA, false, false>
+                   : sweep_kernel<V, LZ, K, NTHR, MINB, false, false, TMA, false, false>;
     }
   }
   if (fn == nullptr) return cudaErrorInvalidValue;
@@ -890,18 +931,22 @@ size_t sweep_smem_bytes(const SweepArgs& a, int V, int LZ, int NTHR, bool synth,
 
 cudaError_t launch_sweep(int cfg_id, const CUtensorMap& map, const SweepArgs& a, bool synth,
                          bool field, int grid, int ns, size_t smem, cudaStream_t st) {
+  // modes per shape = what make_plan (capi.cu) uses it for: 0 every plan at
+  // 64-wide rows; 1 the 48-wide field plan; 2-4 upwind + field (+ trapezoid);
+  // 5 the generic fallback; 7-10 MUSCL (and their relax-only final pass);
+  // 11 the 48-wide upwind plan
   switch (cfg_id) {
-    case 0: return launch_cfg<2, 32, 4, 256, 2, true, 7>(map, a, synth, field, grid, ns, smem, st);
-    case 1: return launch_cfg<3, 16, 4, 256, 2, true, 7>(map, a, synth, field, grid, ns, smem, st);
-    case 2: return launch_cfg<2, 16, 4, 256, 2, true, 7>(map, a, synth, field, grid, ns, smem, st);
-    case 3: return launch_cfg<2, 8, 4, 256, 2, true, 7>(map, a, synth, field, grid, ns, smem, st);
-    case 4: return launch_cfg<2, 4, 4, 256, 2, true, 7>(map, a, synth, field, grid, ns, smem, st);
-    case 5: return launch_cfg<1, 32, 4, 256, 2, false, 7>(map, a, synth, field, grid, ns, smem, st);
-    case 7: return launch_cfg<3, 16, 4, 256, 1, true, 3>(map, a, synth, field, grid, ns, smem, st);
-    case 8: return launch_cfg<2, 16, 4, 256, 1, true, 3>(map, a, synth, field, grid, ns, smem, st);
-    case 9: return launch_cfg<2, 8, 4, 256, 1, true, 3>(map, a, synth, field, grid, ns, smem, st);
-    case 10: return launch_cfg<2, 4, 4, 256, 1, true, 3>(map, a, synth, field, grid, ns, smem, st);
-    case 11: return launch_cfg<6, 8, 2, 256, 2, true, 7>(map, a, synth, field, grid, ns, smem, st);
+    case 0: return launch_cfg<2, 32, 4, 256, 2, true, 15>(map, a, synth, field, grid, ns, smem, st);
+    case 1: return launch_cfg<3, 16, 4, 256, 2, true, 5>(map, a, synth, field, grid, ns, smem, st);
+    case 2: return launch_cfg<2, 16, 4, 256, 2, true, 13>(map, a, synth, field, grid, ns, smem, st);
+    case 3: return launch_cfg<2, 8, 4, 256, 2, true, 13>(map, a, synth, field, grid, ns, smem, st);
+    case 4: return launch_cfg<2, 4, 4, 256, 2, true, 13>(map, a, synth, field, grid, ns, smem, st);
+    case 5: return launch_cfg<1, 32, 4, 256, 2, false, 15>(map, a, synth, field, grid, ns, smem, st);
+    case 7: return launch_cfg<3, 16, 4, 256, 1, true, 11>(map, a, synth, field, grid, ns, smem, st);
+    case 8: return launch_cfg<2, 16, 4, 256, 1, true, 11>(map, a, synth, field, grid, ns, smem, st);
+    case 9: return launch_cfg<2, 8, 4, 256, 1, true, 11>(map, a, synth, field, grid, ns, smem, st);
+    case 10: return launch_cfg<2, 4, 4, 256, 1, true, 11>(map, a, synth, field, grid, ns, smem, st);
+    case 11: return launch_cfg<6, 8, 2, 256, 2, true, 9>(map, a, synth, field, grid, ns, smem, st);
     default: return cudaErrorInvalidValue;
   }
 }

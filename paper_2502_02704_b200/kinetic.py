@@ -81,6 +81,14 @@ class KineticParams:
             raise ConfigurationError("the MUSCL x scheme has no v_x field term; use scheme='upwind'")
 
 
+def _check_grid(grid, params) -> None:
+    """Combinations the extensions do not define."""
+    if getattr(grid.velocity, "quadrature", "midpoint") == "trapezoid" and \
+            params.force is not None and np.max(np.abs(params.force)) > 0:
+        raise ConfigurationError("the v_x field term is defined on midpoint velocity cells only "
+                                 "(trapezoidal quadrature needs force=None)")
+
+
 def _scheme(ctx, params) -> None:
     """Point the context's sweeps at params.scheme (pbgk_set_x_scheme)."""
     code = 1 if getattr(params, "scheme", "upwind") == "muscl" else 0
@@ -134,6 +142,7 @@ def fine_schedule(span: float, cap: float) -> list:
 
 def transport_update(f, dt: float, grid, params, bc) -> Distribution:
     """One explicit transport step on the GPU (ref/kinetic.py:86-124)."""
+    _check_grid(grid, params)
     ctx = rt.ctx_for(grid, bc)
     _scheme(ctx, params)
     fd = as_device_f(f, ctx)
@@ -205,6 +214,7 @@ def propagate_kinetic(f0, t0: float, t1: float, grid, params, bc, dt_max=None) -
     """Advance f0 from t0 to t1 (ref/kinetic.py:137-161), on the GPU."""
     if t1 < t0:
         raise ConfigurationError("need t1 >= t0, got [%r, %r]" % (t0, t1))
+    _check_grid(grid, params)
     span = t1 - t0
     if span == 0.0:
         return f0
@@ -230,6 +240,7 @@ def propagate_window(ctx, mom0: torch.Tensor, t0: float, t1: float, grid, params
     from the moment tables and the last one only projects.  Returns the
     status key (-1 clean) without raising, so callers can order failures.
     """
+    _check_grid(grid, params)
     span = t1 - t0
     cap = stable_dt_kinetic(grid, params)
     if dt_max is not None:

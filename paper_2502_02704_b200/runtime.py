@@ -70,6 +70,12 @@ class Ctx:
         # f-sized scratch buffers reused across calls (allocated lazily)
         self._f_tmp = [None, None]
 
+    def set_quadrature(self, q: int) -> None:
+        _lib.check(self.lib.pbgk_ctx_set_quadrature(self.h, int(q)), "pbgk_ctx_set_quadrature")
+        nv = self.shape[1:]
+        self.dv = tuple(2.0 * self.v_max / ((n - 1) if q else n) for n in nv)
+        self.quadrature = "trapezoid" if q else "midpoint"
+
     def describe(self) -> str:
         buf = ctypes.create_string_buffer(1024)
         _lib.check(self.lib.pbgk_ctx_describe(self.h, buf, 1024), "pbgk_ctx_describe")
@@ -104,12 +110,15 @@ def ctx_for(grid, bc, device: torch.device | None = None) -> Ctx:
     device = device or current_device()
     sp, vel = grid.space, grid.velocity
     nv = tuple(int(n) for n in vel.n_v)
+    quad = getattr(vel, "quadrature", "midpoint")
     key = (float(sp.x_min), float(sp.x_max), int(sp.n_x), float(vel.v_max), nv,
-           bc_code(bc), device.index)
+           bc_code(bc), device.index, quad)
     with _lock:
         c = _ctx_cache.get(key)
         if c is None:
             c = Ctx((sp.n_x,) + nv, sp.x_min, sp.x_max, vel.v_max, bc_code(bc), device)
+            if quad == "trapezoid":
+                c.set_quadrature(1)
             _ctx_cache[key] = c
         return c
 

@@ -67,6 +67,8 @@ class SlabFine:
                           self.device)
         lib, h = self.ctx.lib, self.ctx.h
         rt._lib.check(lib.pbgk_ctx_set_dx(h, float(dx)), "pbgk_ctx_set_dx")
+        if getattr(grid.velocity, "quadrature", "midpoint") == "trapezoid":
+            self.ctx.set_quadrature(1)
         _scheme(self.ctx, params)
         self.TL = lib.pbgk_table_len(h)
         shp = (self.n + 2,) + nv

@@ -391,3 +391,22 @@ def test_muscl_more_accurate_than_upwind_and_tvd():
         u, _ = err(nx, "upwind")
         assert e < u / 3.0
         assert g.max() <= 1.5 + 1e-14 and g.min() >= 0.5 - 1e-14
+
+
+def test_trapezoid_mesh_known_answers():
+    m = O.Mesh(0.0, 1.0, 3, 8.0, (17, 17, 17), "trapezoid")
+    assert m.vc[0][0] == -8.0 and m.vc[0][-1] == 8.0 and m.vc[0][8] == 0.0
+    assert np.array_equal(m.vc[0], -m.vc[0][::-1])
+    # constant f = 1: the trapezoid rule integrates it exactly -> rho = (2 v_max)^3
+    rho, u, th = O.project(np.ones((3, 17, 17, 17)), m)
+    assert np.allclose(rho, 16.0 ** 3, rtol=1e-14) and np.all(u == 0.0)
+    # theta of f = 1 is the rule's mean of c^2: (sum w c^2) / (sum w) = 21.5 here
+    # (the continuous value is 64/3)
+    assert np.allclose(th, 21.5, rtol=1e-14)
+    # a Maxwellian: the trapezoid rule on 17 nodes is as accurate as the
+    # reference's midpoint rule on 16 cells (same dv = 1)
+    U = (np.array([1.0, 0.4, 2.0]), np.array([[0.3, -0.1, 0.2]] * 3), np.array([1.0, 0.6, 1.4]))
+    gap = moment_gap(O.project(O.lift(*U, m), m), U)
+    m16 = O.Mesh(0.0, 1.0, 3, 8.0, (16, 16, 16))
+    assert gap <= 1e-4 and abs(gap - moment_gap(O.project(O.lift(*U, m16), m16), U)) <= 1e-9
+    assert np.allclose(O.project(O.lift(*U, m, normalize=True), m)[0], U[0], rtol=1e-14)
