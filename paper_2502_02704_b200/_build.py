@@ -18,7 +18,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIBDIR = PKG / "lib"
 LIB = LIBDIR / "libpbgk.so"
-SOURCES = ["sweep.cu", "finalize.cu", "fluid.cu", "capi.cu"]
+SOURCES = ["sweep.cu", "sweep_a.cu", "sweep_b.cu", "sweep_c.cu", "finalize.cu", "fluid.cu", "capi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "-I", str(ROOT / "include")]
@@ -73,6 +73,8 @@ def build(force: bool = False, verbose: bool = False, csrc: Path | None = None,
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + r.stderr)
     os.replace(tmp, LIB)
+    for o in objs:  # every build recompiles all sources; keep the snapshot lean
+        Path(o).unlink(missing_ok=True)
     if verbose:
         print("built", LIB)
     return LIB
