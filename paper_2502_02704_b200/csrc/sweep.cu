@@ -1,32 +1,6 @@
-// Fused fine-step sweep: one HBM read and one HBM write of f per fine step.
-//
-// Step s of the fine propagator (ref/kinetic.py:152-160) is
-//     f*_s = T_dt(f_{s-1}),   f_s = R_s(f*_s) = (f*_s + lam M[f*_s]) / (1 + lam).
-// R_s needs per-x-cell velocity reductions of f*_s, a grid-wide dependency.
-// The sweep therefore runs skewed: pass s reads f*_{s-1} (already in HBM),
-// applies R_{s-1} pointwise from a small per-cell table row (lambda and the
-// separable Maxwellian factors, written by finalize.cu), applies T_dt for step
-// s, writes f*_s and accumulates fixed-order marginal partials of f*_s.  The
-// first pass of a window synthesises f_0 = L(U) from the lift tables instead
-// of reading it (SYNTH); the last pass applies R_S only (dtdx == 0) and may
-// skip the write (the window only needs P(f_S)).
-//
-// Work decomposition (persistent CTAs, 2 per SM):
-//   velocity box "tile" (A rows of v_x, By of v_y, Bz of v_z) x all x cells.
-//   Every tile has one sign of c_x, so its upwind neighbour plane is on one
-//   side: c_x >= 0 tiles march upward in x, c_x < 0 tiles march downward, and
-//   each thread keeps f_pre of the previous plane for its elements in
-//   registers.  The (tile, plane) sequence is cut into gridDim.x contiguous
-//   segments; a segment pays one halo plane per tile run it touches.
-//   Each plane's box arrives by one 4-D TMA copy (plus a 1-D bulk copy of the
-//   cell's table row) into a ring of `ns` shared-memory stages.
-//   Thread layout: LZ lanes x V consecutive v_z per box line (a line is one
-//   (v_x, v_y) pair of the box), K lines per thread.
-//
-// Reductions are deterministic and mirror-symmetric (the same tree for every
-// marginal index), so even data keeps an exactly-zero folded first moment
-// (ref/moments.py:80-88).  Non-finite values are not tested per element here:
-// they propagate into the marginals and the finalize kernel flags the step.
+// Sweep dispatch: shared-memory sizing and the switch from a configuration id
+// (capi.cu make_plan) to the translation unit that instantiates that shape
+// (sweep_a/b/c.cu).  The kernel itself and its design are in sweep_impl.cuh.
 #include <cuda.h>
 #include <cuda_runtime.h>
 

@@ -27,6 +27,14 @@
 // marginal index), so even data keeps an exactly-zero folded first moment
 // (ref/moments.py:80-88).  Non-finite values are not tested per element here:
 // they propagate into the marginals and the finalize kernel flags the step.
+//
+// Template variants: SYNTH (first pass from lift tables), FIELD (the v_x
+// Rusanov term of ref/kinetic.py:114-123), TMA (vs a cooperative-load
+// fallback for odd shapes), and three extensions: MUSCL (minmod x transport,
+// output one plane behind the loads, 2 lead / 1 trail halo items per run),
+// TRAP (trapezoidal velocity quadrature: end nodes weigh 1/2 in the
+// reductions).  bc 3 (runtime) is a slab of an x-sharded domain whose halo
+// planes sit in the padded buffers.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
