@@ -26,7 +26,7 @@ from __future__ import annotations
 import ctypes
 import math
 import time
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from typing import Callable, List, NamedTuple, Optional
 
 import numpy as np
