@@ -109,7 +109,8 @@ __device__ ErrKey g_advance(double* V, double* red, int* flag, const FluidArgs& 
     double dt = DD(DM(a.cfl, a.dx), rate);
     if (a.dt_max > 0.0) dt = fmin(dt, a.dt_max);
     dt = fmin(dt, DS(span, done));
-    const double dtdx = DD(dt, a.dx);
+    int dx_exp;
+    const double dtdx = frexp(a.dx, &dx_exp) == 0.5 ? DM(dt, DD(1.0, a.dx)) : DD(dt, a.dx);  // exact either way
     ++step;
     double nv[kMaxCellsPerThread][5];
     int bad = 0;
@@ -172,13 +173,33 @@ __device__ ErrKey g_advance_dd(double* V, double* red, int* flag, const FluidArg
   double cap = DD(DM(DM(a.cfl, a.dx), a.dx), DM(a.diff, DA(2.0, DM(a.dx, em))));
   if (a.dt_max > 0.0) cap = fmin(cap, a.dt_max);
   auto E = [&](int i) { return a.force != nullptr ? a.force[i] : 0.0; };
+  // x / dx is exactly x * (1 / dx) when dx is a power of two (every config
+  // here: x in [0, 1] on 2^k cells): the fp64 divisions leave the critical path
+  int dx_exp;
+  const bool pow2 = frexp(a.dx, &dx_exp) == 0.5;
+  const double rdx = pow2 ? DD(1.0, a.dx) : 0.0;
+  auto over_dx = [&](double x) { return pow2 ? DM(x, rdx) : DD(x, a.dx); };
+  // the field at each cell and its neighbours is constant over the window
+  double eC[kMaxCellsPerThread], eL[kMaxCellsPerThread], eR[kMaxCellsPerThread];
+#pragma unroll
+  for (int k = 0; k < kMaxCellsPerThread; ++k) {
+    const int i = threadIdx.x + k * blockDim.x;
+    const int ii = i < nx ? i : nx - 1;
+    const int il = ii > 0 ? ii - 1 : (a.periodic ? nx - 1 : 0);
+    const int ir = ii < nx - 1 ? ii + 1 : (a.periodic ? 0 : nx - 1);
+    eC[k] = E(ii);
+    eL[k] = E(il);
+    eR[k] = E(ir);
+  }
   double done = 0.0;
   unsigned long long step = 0;
   while (DS(span, done) > DM(guard, span)) {
     const double dt = fmin(cap, DS(span, done));
-    const double coef = DD(DM(dt, a.diff), a.dx);
+    const double coef = over_dx(DM(dt, a.diff));
     ++step;
-    double nr[kMaxCellsPerThread];
+    // ping-pong between V[0..nx) and V[nx..2nx): one barrier per step
+    const double* Vin = V + ((step - 1) & 1) * nx;
+    double* Vout = V + (step & 1) * nx;
     int bad = 0;
 #pragma unroll
     for (int k = 0; k < kMaxCellsPerThread; ++k) {
@@ -186,27 +207,24 @@ __device__ ErrKey g_advance_dd(double* V, double* red, int* flag, const FluidArg
       if (i >= nx) break;
       const int il = i > 0 ? i - 1 : (a.periodic ? nx - 1 : 0);
       const int ir = i < nx - 1 ? i + 1 : (a.periodic ? 0 : nx - 1);
-      const double gi = V[i], gl = V[il], gr = V[ir];
-      const double ei = E(i), el = E(il), er = E(ir);
-      const double JR = DS(DD(DS(gr, gi), a.dx), DM(0.5, DA(DM(ei, gi), DM(er, gr))));
-      const double JL = DS(DD(DS(gi, gl), a.dx), DM(0.5, DA(DM(el, gl), DM(ei, gi))));
+      const double gi = Vin[i], gl = Vin[il], gr = Vin[ir];
+      const double ei = eC[k], el = eL[k], er = eR[k];
+      const double JR = DS(over_dx(DS(gr, gi)), DM(0.5, DA(DM(ei, gi), DM(er, gr))));
+      const double JL = DS(over_dx(DS(gi, gl)), DM(0.5, DA(DM(el, gl), DM(ei, gi))));
       const double v = DA(gi, DM(coef, DS(JR, JL)));
-      nr[k] = v;
+      Vout[i] = v;
       if (!isfinite(v)) bad |= 1;
       else if (v <= 0.0) bad |= 2;
     }
     if (bad) atomicOr(flag, bad);
     __syncthreads();
-#pragma unroll
-    for (int k = 0; k < kMaxCellsPerThread; ++k) {
-      const int i = threadIdx.x + k * blockDim.x;
-      if (i >= nx) break;
-      V[i] = nr[k];
-    }
-    __syncthreads();
     const int f = *flag;
     if (f) return (step << 8) | (unsigned long long)((f & 1) ? kErrNonFinite : kErrUnphysical);
     done = DA(done, dt);
+  }
+  if (step & 1) {  // the state ended in V[nx..2nx)
+    for (int i = threadIdx.x; i < nx; i += blockDim.x) V[i] = V[nx + i];
+    __syncthreads();
   }
   return 0;
 }
@@ -257,9 +275,13 @@ __device__ bool to_prim(const FluidArgs& a, const double* V, int nx, int i, doub
 
 // Batched independent G solves: blockIdx.x = window.  out = minuend - G(in)
 // when minuend != null (the parareal jump, ref/parareal.py:142).
-__global__ void __launch_bounds__(1024) fluid_batch_kernel(FluidArgs a, const double* in, double* out,
+template <int M>
+__global__ void __launch_bounds__(1024) fluid_batch_kernel(FluidArgs a0, const double* in, double* out,
                                                            const double* minuend, const double* t0,
                                                            const double* t1) {
+  FluidArgs a = a0;
+  a.model = M;  // compile-time model: each variant carries only its own G
+
   extern __shared__ double V[];
   __shared__ double red[32];
   __shared__ int flag;
@@ -299,9 +321,13 @@ __global__ void __launch_bounds__(1024) fluid_batch_kernel(FluidArgs a, const do
 // The error is max-accumulated into *err_out (non-negative doubles order as
 // their bit patterns), so a sweep split into consecutive ranges gives the
 // same value as one launch.
-__global__ void __launch_bounds__(1024) correct_kernel(FluidArgs a, int last, int start, double* snaps,
+template <int M>
+__global__ void __launch_bounds__(1024) correct_kernel(FluidArgs a0, int last, int start, double* snaps,
                                                        const double* old, const double* jumps,
                                                        const double* times, double* err_out) {
+  FluidArgs a = a0;
+  a.model = M;
+
   extern __shared__ double V[];
   __shared__ double red[32];
   __shared__ int flag;
@@ -386,10 +412,10 @@ cudaError_t launch_fluid_batch(const FluidArgs& a, int nwin, const double* in, d
   const int thr = fluid_threads(a.nx, lean);
   if ((size_t)thr * kMaxCellsPerThread < (size_t)a.nx) return cudaErrorInvalidValue;
   const size_t smem = (size_t)5 * a.nx * sizeof(double);
-  cudaError_t e = cudaFuncSetAttribute(fluid_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  auto k = a.model == 1 ? fluid_batch_kernel<1> : fluid_batch_kernel<0>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  fluid_batch_kernel<<<nwin, thr, smem, st>>>(a, in, out, minuend, t0, t1);
+  k<<<nwin, thr, smem, st>>>(a, in, out, minuend, t0, t1);
   return cudaGetLastError();
 }
 
@@ -400,9 +426,13 @@ cudaError_t launch_correct(const FluidArgs& a, int last, int start, double* snap
   if ((size_t)thr * kMaxCellsPerThread < (size_t)a.nx) return cudaErrorInvalidValue;
   const size_t smem = (size_t)5 * a.nx * sizeof(double);
   cudaError_t e =
-      cudaFuncSetAttribute(correct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(a.model == 1 ? correct_kernel<1> : correct_kernel<0>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  correct_kernel<<<1, thr, smem, st>>>(a, last, start, snaps, old, jumps, times, err_out);
+  if (a.model == 1)
+    correct_kernel<1><<<1, thr, smem, st>>>(a, last, start, snaps, old, jumps, times, err_out);
+  else
+    correct_kernel<0><<<1, thr, smem, st>>>(a, last, start, snaps, old, jumps, times, err_out);
   return cudaGetLastError();
 }
 
