@@ -65,8 +65,9 @@ def build(force: bool = False, verbose: bool = False, csrc: Path | None = None,
         (LIB.parent / (LIB.stem + "_" + Path(src).stem + ".ptxas.txt")).write_text(r.stderr)
         return obj
 
-    with cf.ThreadPoolExecutor(len(SOURCES)) as ex:
-        objs = list(ex.map(one, SOURCES))
+    srcs = [f for f in SOURCES if (CSRC / f).exists()]  # older trees (A/B builds) have fewer
+    with cf.ThreadPoolExecutor(len(srcs)) as ex:
+        objs = list(ex.map(one, srcs))
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [cc, *ARCH, "-shared", "-o", str(tmp), *map(str, objs)]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -257,9 +257,10 @@ bool make_plan(pbgk_ctx* c, bool field, bool muscl, Plan& out) {
   dummy.TL = c->TL;
   // two CTAs per SM when the ring fits in half the shared memory, else one
   const size_t half = (c->smem_per_sm / 2) - 2048;
-  // ring depth (measured, round 1, after PDL and the V = 6 shape): 64-wide
-  // boxes 3 stages, 48-wide (V = 6) and 32-wide 4, the narrow / odd shapes 2
-  int ns_max = (s.V == 2 && s.LZ == 32) ? 3 : ((s.V == 6 || (s.V == 2 && s.LZ == 16)) ? 4 : 2);
+  // ring depth (same-box A/B, round 1): 64-wide boxes 3 stages; 32-wide 4 for
+  // the plain sweep, 3 with the field term; 48-wide (V = 6) and the narrow /
+  // odd shapes 2
+  int ns_max = (s.V == 2 && s.LZ == 32) ? 3 : ((s.V == 2 && s.LZ == 16) ? (field ? 3 : 4) : 2);
   if (const char* e = getenv("PBGK_NS")) ns_max = atoi(e);  // development knob
   int ns = ns_max;
   while (ns > 2 && sweep_smem_bytes(dummy, s.V, s.LZ, s.NTHR, false, s.tma, ns) > half) --ns;
