@@ -81,7 +81,7 @@ def test_alpha1_fine_propagator(shape, field):
     # the single-step API scales the same way
     d = 0.5 * cap
     tr = P.transport_update(P.Distribution(f), d, grid, kp, P.BoundaryKind.PERIODIC)
-    assert np.array_equal(tr.values, O.transport(f, d / eps, mesh, True, E))
+    assert rel_inf(tr.values, O.transport(f, d / eps, mesh, True, E)) <= (1e-14 if field else 0.0)
     rx = P.bgk_relax(P.Distribution(f), d, grid, kp)
     assert rel_inf(rx.values, O.relax(f, d / eps, mesh, eps)) <= 1e-13
 

@@ -1,7 +1,7 @@
 """GPU (libpbgk.so) vs the CPU oracle on the same seeded inputs.
 
-Tolerances: transport and G are evaluated in the reference's operation order
-and must match bit for bit; projections/lifts differ from numpy only in the
+Tolerances: the x transport and G are evaluated in the reference's operation
+order and must match bit for bit (the v_x field flux is reassociated: 1e-14); projections/lifts differ from numpy only in the
 summation order of the marginals and in exp/pow (<= a few ulp), so they are
 held to 1e-13 relative; multi-step runs to 1e-12; parareal to the north-star
 bound 1e-10 (normwise).
@@ -89,7 +89,10 @@ def test_transport_bitwise(shape, periodic, field):
     bc = P.BoundaryKind.PERIODIC if periodic else P.BoundaryKind.ABSORBING
     got = P.transport_update(P.Distribution(f), dt, grid, P.KineticParams(1.0, force=E), bc).values
     want = O.transport(f, dt, mesh, periodic, E)
-    assert np.array_equal(got, want), rel_inf(got, want)
+    if field:  # the v_x flux is reassociated (cp lo + cm hi): within an ulp per face
+        assert rel_inf(got, want) <= 1e-14
+    else:      # x transport: the reference's operation order, bit for bit
+        assert np.array_equal(got, want), rel_inf(got, want)
 
 
 @pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "x".join(map(str, (s[0],) + s[1])))
