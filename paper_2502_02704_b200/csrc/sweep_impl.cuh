@@ -346,16 +346,8 @@ __global__ void __launch_bounds__(NTHR, MINB)
     for (int s = 0; s < ns && !prod.done(); ++s) issue_next();
   }
 
-  // Line k of this thread: strided (l = lg + k NL) in general; for the field
-  // term with A % K == 0, K CONSECUTIVE rows of one v_y column (row
-  // (lg / By) K + k, column lg % By), so the v_x neighbours of the inner
-  // lines are in registers and each v_x face flux is formed once.
-  const bool consec = FIELD && V <= 2 && (T.A % K == 0);  // V = 3: register pressure (measured)
+  // Line k of this thread: l = lg + k NL (strided over the box's lines)
   auto line_of = [&](int k) {  // natural line index aa*By + b, or -1 outside the box
-    if (consec) {
-      const int aa = (lg >> lgBy) * K + k;
-      return aa < T.A ? (aa << lgBy) | (lg & (T.By - 1)) : -1;
-    }
     const int l = lg + k * NL;
     return l < lines ? l : -1;
   };
@@ -589,103 +581,6 @@ __global__ void __launch_bounds__(NTHR, MINB)
           for (int v = 0; v < V; ++v) prev[k][v] = fl[v];
         }
       };
-      // Field term with consecutive rows per thread: relax all K lines first,
-      // then the two boundary rows from smem, then the K+1 v_x faces
-      // (ref/kinetic.py:114-123, each face in the reference's operation
-      // order), then per line the same output/partials/store as `body`.
-      auto body_fc = [&](auto fast_c, auto down_c) {
-        constexpr bool FAST = decltype(fast_c)::value;
-        constexpr bool DOWNT = decltype(down_c)::value;
-        const double gym = ST[gyi[0]];
-        double xs[K][V];
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          const double gxy = ST[gxi[k]] * gym;
-          if (SYNTH) {
-#pragma unroll
-            for (int v = 0; v < V; ++v) xs[k][v] = (gxy * gz[v]) * ls;
-          } else {
-            const double w = r * (ls * gxy);
-            double raw[V];
-            lds_lane<V, LZ>(SF + soff[k], raw);
-#pragma unroll
-            for (int v = 0; v < V; ++v) xs[k][v] = fma(w, gz[v], r * raw[v]);
-          }
-        }
-        const int jx0 = gxi[0] - a.gxo;  // row of line 0 (consecutive rows)
-        const bool lo0 = jx0 > 0, hiK = jx0 + K < a.nvx;
-        double fm[V], fp[V];
-        {
-          const double gxm = lo0 ? ST[gxi[0] - 1] * gym : 0.0;
-          const double gxp = hiK ? ST[gxi[0] + K] * gym : 0.0;
-          if (SYNTH) {
-#pragma unroll
-            for (int v = 0; v < V; ++v) {
-              fm[v] = (gxm * gz[v]) * ls;
-              fp[v] = (gxp * gz[v]) * ls;
-            }
-          } else {
-            const double wm = r * (ls * gxm), wp = r * (ls * gxp);
-            double rm[V], rp[V];
-            lds_lane<V, LZ>(SF + soff[0] - T.By * BZ, rm);
-            lds_lane<V, LZ>(SF + soff[0] + K * T.By * BZ, rp);
-#pragma unroll
-            for (int v = 0; v < V; ++v) {
-              fm[v] = fma(wm, gz[v], r * rm[v]);
-              fp[v] = fma(wp, gz[v], r * rp[v]);
-            }
-          }
-        }
-        // gf[q]: face between rows jx0+q-1 and jx0+q (lower value a, upper b)
-        double gf[K + 1][V];
-#pragma unroll
-        for (int q = 0; q <= K; ++q) {
-#pragma unroll
-          for (int v = 0; v < V; ++v) {
-            const double lo = q == 0 ? fm[v] : xs[q - 1][v];
-            const double hi = q == K ? fp[v] : xs[q][v];
-            gf[q][v] = fma(cp, lo, cm * hi);
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          const bool ok = FAST || ((vmask >> k) & 1u);
-          const double c = cvx[k];
-          const int jx = jx0 + k;
-          const bool has_lo = jx > 0, has_hi = jx + 1 < a.nvx;
-          double fl[V];
-#pragma unroll
-          for (int v = 0; v < V; ++v) fl[v] = __dmul_rn(c, xs[k][v]);
-          if (FAST || out_plane) {
-            double o[V];
-            if (FAST || transport) {
-#pragma unroll
-              for (int v = 0; v < V; ++v) {
-                const double d = DOWNT ? __dsub_rn(prev[k][v], fl[v]) : __dsub_rn(fl[v], prev[k][v]);
-                o[v] = __dsub_rn(xs[k][v], __dmul_rn(dtdx, d));
-                const double ghi = has_hi ? gf[k + 1][v] : 0.0;
-                const double glo = has_lo ? gf[k][v] : 0.0;
-                o[v] = fma(-a.dtdv, ghi - glo, o[v]);
-              }
-            } else {
-#pragma unroll
-              for (int v = 0; v < V; ++v) o[v] = xs[k][v];
-            }
-            double sl = 0.0;
-#pragma unroll
-            for (int v = 0; v < V; ++v) {
-              const double m = FAST ? o[v] : ((ok && ((zmask >> v) & 1u)) ? o[v] : 0.0);
-              accum(m, k, v, sl);
-            }
-            lp[k] = sl;
-            if (FAST || (gdst != nullptr && ok)) {
-              store_line<V, LZ, FAST>(gdst + goff[k], o, zmask, a.l2_keep != 0, pol_keep);
-            }
-          }
-#pragma unroll
-          for (int v = 0; v < V; ++v) prev[k][v] = fl[v];
-        }
-      };
       // MUSCL (minmod) x transport, one plane behind the loads: item q
       // relaxes plane q, forms the slope of plane q-1 from planes q-2..q and
       // the face flux between q-1 and q (march order), and outputs plane q-1
@@ -770,12 +665,6 @@ __global__ void __launch_bounds__(NTHR, MINB)
             lds_lane<V, LZ>(SF + soff[k], raw);
             if constexpr (V == 2) st_global_v2(gdst + goff[k], raw[0], raw[1]);
           }
-        }
-      } else if (FIELD && consec) {
-        if (full && out_plane && transport && gdst != nullptr) {
-          if (tg.down) body_fc(T1{}, T1{}); else body_fc(T1{}, F1{});
-        } else {
-          if (tg.down) body_fc(F1{}, T1{}); else body_fc(F1{}, F1{});
         }
       } else if (full && out_plane && transport && gdst != nullptr) {
         if (tg.down) body(T1{}, T1{}); else body(T1{}, F1{});
