@@ -208,8 +208,11 @@ bool make_plan(pbgk_ctx* c, bool field, bool muscl, Plan& out) {
       while (By > nvy && By > 1) By >>= 1;  // power of two (the kernel shifts by log2 By)
       if (By < 1 || By > 256 || A + (field ? 2 : 0) > 256) continue;
       if (A + By + Bz > s.NTHR) continue;
-      if (const char* fa = getenv("PBGK_FORCE_A"))  // development knob
+      if (const char* fa = getenv("PBGK_FORCE_A")) {  // development knob
         if (A != atoi(fa)) continue;
+      } else if (field && A > 8) {
+        continue;  // field term: <= 8 rows per box (measured: 64^3 A=8 +7 % over A=32)
+      }
       Tiling t;
       t.A = A;
       t.By = By;
