@@ -212,6 +212,8 @@ bool make_plan(pbgk_ctx* c, bool field, bool muscl, Plan& out) {
         if (A != atoi(fa)) continue;
       } else if (field && A > 8) {
         continue;  // field term: <= 8 rows per box (measured: 64^3 A=8 +7 % over A=32)
+      } else if (!field && s.V == 6 && A > 4) {
+        continue;  // 48-wide V = 6 boxes: 4 x 16 lines (measured +3.5 % over 8 x 8)
       }
       Tiling t;
       t.A = A;
