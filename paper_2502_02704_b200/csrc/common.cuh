@@ -110,6 +110,7 @@ struct FluidArgs {
   ErrKey* err;
   int model;
   double diff;          // model 1: diffusivity D = m2 / tau
+  int fastg;            // set by the launcher: per-cell wave / flux arrays fit in smem
 };
 
 // Launch with programmatic dependent launch enabled: the kernel may begin

@@ -156,6 +156,87 @@ __device__ ErrKey g_advance(double* V, double* red, int* flag, const FluidArgs& 
   return 0;
 }
 
+// g_advance with each cell's wave speed and Euler flux evaluated once per step
+// into shared memory (S[nx], Hf[5][nx] after V): the faces then need no
+// division.  Every value is the same function of the same cell state as in
+// g_advance (rusanov() recomputes them per face), so the result is bitwise
+// identical; needs 11 nx doubles of shared memory (a.fastg).
+__device__ ErrKey g_advance_fast(double* V, double* red, int* flag, const FluidArgs& a,
+                                 double span) {
+  const int nx = a.nx;
+  double* S = V + 5 * nx;
+  double* Hf = S + nx;
+  const double guard = 1e-12;  // ref/fluid.py:30
+  int dx_exp;
+  const bool pow2 = frexp(a.dx, &dx_exp) == 0.5;
+  double done = 0.0;
+  unsigned long long step = 0;
+  while (DS(span, done) > DM(guard, span)) {
+    double rate = 0.0;
+    for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+      const St c = load_state(V, nx, i);
+      const double w = wave(c);
+      double h[5];
+      eflux(c, h);
+      S[i] = w;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) Hf[q * nx + i] = h[q];
+      rate = fmax(rate, w);
+    }
+    rate = block_max(rate, red);  // its barriers also publish S and Hf
+    double dt = DD(DM(a.cfl, a.dx), rate);
+    if (a.dt_max > 0.0) dt = fmin(dt, a.dt_max);
+    dt = fmin(dt, DS(span, done));
+    const double dtdx = pow2 ? DM(dt, DD(1.0, a.dx)) : DD(dt, a.dx);  // exact either way
+    ++step;
+    double nv[kMaxCellsPerThread][5];
+    int bad = 0;
+#pragma unroll
+    for (int k = 0; k < kMaxCellsPerThread; ++k) {
+      const int i = threadIdx.x + k * blockDim.x;
+      if (i >= nx) break;
+      const int il = i > 0 ? i - 1 : (a.periodic ? nx - 1 : 0);
+      const int ir = i < nx - 1 ? i + 1 : (a.periodic ? 0 : nx - 1);
+      const St c = load_state(V, nx, i);
+      const St l = load_state(V, nx, il);
+      const St r = load_state(V, nx, ir);
+      const double hsl = DM(0.5, fmax(S[il], S[i])), hsr = DM(0.5, fmax(S[i], S[ir]));
+      double* w = nv[k];
+#pragma unroll
+      for (int q = 0; q < 5; ++q) {
+        const double hc = Hf[q * nx + i];
+        const double HL = DS(DM(0.5, DA(Hf[q * nx + il], hc)), DM(hsl, DS(c.v[q], l.v[q])));
+        const double HR = DS(DM(0.5, DA(hc, Hf[q * nx + ir])), DM(hsr, DS(r.v[q], c.v[q])));
+        w[q] = DS(c.v[q], DM(dtdx, DS(HR, HL)));
+      }
+      if (a.force != nullptr) {  // ref/fluid.py:113-115 (old state)
+        const double E = a.force[i];
+        w[1] = DA(w[1], DM(DM(dt, c.v[0]), E));
+        w[4] = DA(w[4], DM(DM(dt, c.v[1]), E));
+      }
+      bool fin = true;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) fin = fin && isfinite(w[q]);
+      if (!fin) bad |= 1;
+      else if (w[0] <= 0.0 || press(w[0], w[1], w[2], w[3], w[4]) <= 0.0) bad |= 2;
+    }
+    if (bad) atomicOr(flag, bad);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kMaxCellsPerThread; ++k) {
+      const int i = threadIdx.x + k * blockDim.x;
+      if (i >= nx) break;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) V[q * nx + i] = nv[k][q];
+    }
+    __syncthreads();
+    const int f = *flag;
+    if (f) return (step << 8) | (unsigned long long)((f & 1) ? kErrNonFinite : kErrUnphysical);
+    done = DA(done, dt);
+  }
+  return 0;
+}
+
 // Drift-diffusion G (extension; oracle/bgk.py dd_propagate, same operation
 // order): rho only, held in V[0..nx).  Conservative central fluxes
 //   J_{i+1/2} = (rho_{i+1} - rho_i)/dx - 0.5 (E_i rho_i + E_{i+1} rho_{i+1}),
@@ -246,7 +327,8 @@ __device__ __forceinline__ void load_window(const FluidArgs& a, const double* sr
 
 __device__ __forceinline__ ErrKey advance(double* V, double* red, int* flag, const FluidArgs& a,
                                           double span) {
-  return a.model == 1 ? g_advance_dd(V, red, flag, a, span) : g_advance(V, red, flag, a, span);
+  if (a.model == 1) return g_advance_dd(V, red, flag, a, span);
+  return a.fastg ? g_advance_fast(V, red, flag, a, span) : g_advance(V, red, flag, a, span);
 }
 
 // conserved -> primitive (ref/moments.py:122-129); returns false if degenerate.
@@ -411,11 +493,14 @@ cudaError_t launch_fluid_batch(const FluidArgs& a, int nwin, const double* in, d
                                cudaStream_t st, bool lean) {
   const int thr = fluid_threads(a.nx, lean);
   if ((size_t)thr * kMaxCellsPerThread < (size_t)a.nx) return cudaErrorInvalidValue;
-  const size_t smem = (size_t)5 * a.nx * sizeof(double);
+  FluidArgs b = a;
+  // Euler G: per-cell wave speeds / fluxes in shared memory when they fit
+  b.fastg = (a.model == 0 && (size_t)11 * a.nx * sizeof(double) <= 220 * 1024) ? 1 : 0;
+  const size_t smem = (size_t)(b.fastg ? 11 : 5) * a.nx * sizeof(double);
   auto k = a.model == 1 ? fluid_batch_kernel<1> : fluid_batch_kernel<0>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k<<<nwin, thr, smem, st>>>(a, in, out, minuend, t0, t1);
+  k<<<nwin, thr, smem, st>>>(b, in, out, minuend, t0, t1);
   return cudaGetLastError();
 }
 
@@ -424,15 +509,18 @@ cudaError_t launch_correct(const FluidArgs& a, int last, int start, double* snap
                            cudaStream_t st, bool lean) {
   const int thr = fluid_threads(a.nx, lean);
   if ((size_t)thr * kMaxCellsPerThread < (size_t)a.nx) return cudaErrorInvalidValue;
-  const size_t smem = (size_t)5 * a.nx * sizeof(double);
+  FluidArgs b = a;
+  // Euler G: per-cell wave speeds / fluxes in shared memory when they fit
+  b.fastg = (a.model == 0 && (size_t)11 * a.nx * sizeof(double) <= 220 * 1024) ? 1 : 0;
+  const size_t smem = (size_t)(b.fastg ? 11 : 5) * a.nx * sizeof(double);
   cudaError_t e =
       cudaFuncSetAttribute(a.model == 1 ? correct_kernel<1> : correct_kernel<0>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (a.model == 1)
-    correct_kernel<1><<<1, thr, smem, st>>>(a, last, start, snaps, old, jumps, times, err_out);
+    correct_kernel<1><<<1, thr, smem, st>>>(b, last, start, snaps, old, jumps, times, err_out);
   else
-    correct_kernel<0><<<1, thr, smem, st>>>(a, last, start, snaps, old, jumps, times, err_out);
+    correct_kernel<0><<<1, thr, smem, st>>>(b, last, start, snaps, old, jumps, times, err_out);
   return cudaGetLastError();
 }
 
