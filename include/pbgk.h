@@ -99,6 +99,18 @@ int pbgk_propagate(pbgk_ctx* ctx, const double* f0, const double* mom0, double* 
                    const double* h_dts, double eps, double tau, const double* E, double e_max,
                    void* stream, long long* h_code);
 
+/* The fine stage of one parareal iteration on this GPU: P(F(L(U_w))) for
+ * nwin windows back to back (ref/parareal.py:123-142 without the G part),
+ * mom_in / mom_out double[nwin][5][nx] on the device, window w taking
+ * h_nsteps[w] steps of h_dts (concatenated), f_a / f_b two f-sized device
+ * scratch buffers.  One host synchronisation for the whole batch; h_codes[w]
+ * receives window w's failure key (-1 clean).  Same kernels and order as
+ * pbgk_propagate per window, so results are bitwise those of nwin calls. */
+int pbgk_propagate_windows(pbgk_ctx* ctx, int nwin, const double* mom_in, double* mom_out,
+                           double* f_a, double* f_b, const int* h_nsteps, const double* h_dts,
+                           double eps, double tau, const double* E, double e_max, void* stream,
+                           long long* h_codes);
+
 /* Coarse Euler propagator G (ref/fluid.py:91-125) on one GPU: advance
  * `nwin` independent primitive states mom_in[w] (double[nwin][5][nx]) over
  * [h_t0[w], h_t1[w]] into mom_out[w]; when `minuend` is non-NULL the output

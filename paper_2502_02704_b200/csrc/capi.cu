@@ -132,6 +132,10 @@ struct pbgk_ctx {
   double* d_tab[2] = {nullptr, nullptr};
   double* d_scratch = nullptr;  // 5*nx moments / small host-visible staging
   ErrKey* d_err = nullptr;
+  ErrKey* err_slot = nullptr;   // where sweeps / finalizes record failures (d_err, or a window's slot)
+  ErrKey* d_keys = nullptr;     // pbgk_propagate_windows: one failure key per window
+  ErrKey* h_keys = nullptr;
+  int keys_cap = 0;
   ErrKey* h_err = nullptr;  // pinned
   double* h_dbl = nullptr;  // pinned small
   double* d_times = nullptr;
@@ -344,7 +348,7 @@ SweepArgs base_args(pbgk_ctx* c, const Plan& p) {
   a.cx = c->d_c[0];
   a.bc = c->g.bc;
   a.part = c->d_part;
-  a.err = c->d_err;
+  a.err = c->err_slot ? c->err_slot : c->d_err;
   static const int debug = getenv("PBGK_DEBUG") ? atoi(getenv("PBGK_DEBUG")) : 0;  // dev ablations
   a.debug = debug & ~2;  // bit 2 (no CTA barrier) was removed: it races the TMA ring
   return a;
@@ -366,7 +370,7 @@ FinalArgs fin_args(pbgk_ctx* c, const Plan& p) {
   f.gxo = c->gxo;
   f.gyo = c->gyo;
   f.gzo = c->gzo;
-  f.err = c->d_err;
+  f.err = c->err_slot ? c->err_slot : c->d_err;
   f.trap = c->quad;
   f.tau = 1.0;
   f.eps = 1.0;
@@ -514,6 +518,8 @@ void pbgk_ctx_destroy(pbgk_ctx* c) {
   cudaFree(c->d_tab[1]);
   cudaFree(c->d_scratch);
   cudaFree(c->d_err);
+  cudaFree(c->d_keys);
+  cudaFreeHost(c->h_keys);
   cudaFree(c->d_times);
   if (c->h_err) cudaFreeHost(c->h_err);
   if (c->h_dbl) cudaFreeHost(c->h_dbl);
@@ -630,19 +636,14 @@ int pbgk_check_finite(pbgk_ctx* c, const double* f, int step, void* stream, long
   return fetch_err(c, st, h_code);
 }
 
-int pbgk_propagate(pbgk_ctx* c, const double* f0, const double* mom0, double* f_out, double* f_tmp,
-                   int write_final, double* mom_out, int nsteps, const double* h_dts, double eps,
-                   double tau, const double* E, double e_max, void* stream, long long* h_code) {
-  if (!c || (!f0 && !mom0) || !f_out || !f_tmp || (nsteps > 0 && !h_dts))
-    return fail("pbgk_propagate: null argument");
-  if (cudaSetDevice(c->dev) != cudaSuccess) return fail("cudaSetDevice");
-  if (f_out == f_tmp || (f0 && (f0 == f_out || f0 == f_tmp)))
-    return fail("pbgk_propagate: buffers alias");
-  cudaStream_t st = (cudaStream_t)stream;
-  if (reset_err(c, st)) return -1;
+namespace {
+// One propagation on the stream, failures atomicMin-ed into the current
+// error slot; no reset, no host synchronisation.
+int propagate_body(pbgk_ctx* c, const double* f0, const double* mom0, double* f_out, double* f_tmp,
+                   int write_final, double* mom_out, int S, const double* h_dts, double eps,
+                   double tau, const double* E, double e_max, cudaStream_t st) {
   const bool field = (E != nullptr && e_max > 0.0);
   const int pid = field ? 1 : (c->x_scheme == 1 ? 2 : 0);
-  const int S = nsteps;
   const int W = S + (write_final ? 1 : 0);
   auto buf = [&](int w) { return ((W - w) % 2 == 0) ? f_out : f_tmp; };
   // f_0: the given distribution (identity tables) or the raw lift of mom0
@@ -668,7 +669,69 @@ int pbgk_propagate(pbgk_ctx* c, const double* f0, const double* mom0, double* f_
         run_final(c, pid, kFinProject, nullptr, mom_out, nullptr, 0, 1, 1, nullptr, S + 1, st))
       return -1;
   }
+  return 0;
+}
+}  // namespace
+
+int pbgk_propagate(pbgk_ctx* c, const double* f0, const double* mom0, double* f_out, double* f_tmp,
+                   int write_final, double* mom_out, int nsteps, const double* h_dts, double eps,
+                   double tau, const double* E, double e_max, void* stream, long long* h_code) {
+  if (!c || (!f0 && !mom0) || !f_out || !f_tmp || (nsteps > 0 && !h_dts))
+    return fail("pbgk_propagate: null argument");
+  if (cudaSetDevice(c->dev) != cudaSuccess) return fail("cudaSetDevice");
+  if (f_out == f_tmp || (f0 && (f0 == f_out || f0 == f_tmp)))
+    return fail("pbgk_propagate: buffers alias");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (reset_err(c, st)) return -1;
+  c->err_slot = nullptr;
+  if (propagate_body(c, f0, mom0, f_out, f_tmp, write_final, mom_out, nsteps, h_dts, eps, tau, E,
+                     e_max, st))
+    return -1;
   return fetch_err(c, st, h_code);
+}
+
+int pbgk_propagate_windows(pbgk_ctx* c, int nwin, const double* mom_in, double* mom_out,
+                           double* f_a, double* f_b, const int* h_nsteps, const double* h_dts,
+                           double eps, double tau, const double* E, double e_max, void* stream,
+                           long long* h_codes) {
+  if (!c || !mom_in || !mom_out || !f_a || !f_b || !h_nsteps || !h_codes)
+    return fail("pbgk_propagate_windows: null argument");
+  if (f_a == f_b) return fail("pbgk_propagate_windows: buffers alias");
+  if (nwin <= 0) return 0;
+  if (cudaSetDevice(c->dev) != cudaSuccess) return fail("cudaSetDevice");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (nwin > c->keys_cap) {
+    CK(cudaStreamSynchronize(st));
+    cudaFree(c->d_keys);
+    cudaFreeHost(c->h_keys);
+    c->d_keys = nullptr;
+    c->h_keys = nullptr;
+    c->keys_cap = 0;
+    CK(cudaMalloc(&c->d_keys, (size_t)nwin * sizeof(ErrKey)));
+    CK(cudaMallocHost(&c->h_keys, (size_t)nwin * sizeof(ErrKey)));
+    c->keys_cap = nwin;
+  }
+  CK(cudaMemsetAsync(c->d_keys, 0xFF, (size_t)nwin * sizeof(ErrKey), st));  // kNoError = ~0
+  const size_t m = (size_t)5 * c->g.nx;
+  size_t off = 0;
+  for (int w = 0; w < nwin; ++w) {
+    const int S = h_nsteps[w];
+    if (S == 0) {  // empty window: the moments themselves
+      CK(cudaMemcpyAsync(mom_out + w * m, mom_in + w * m, m * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      continue;
+    }
+    c->err_slot = c->d_keys + w;
+    const int rc = propagate_body(c, nullptr, mom_in + w * m, f_a, f_b, 0, mom_out + w * m, S,
+                                  h_dts + off, eps, tau, E, e_max, st);
+    c->err_slot = nullptr;
+    if (rc) return -1;
+    off += S;
+  }
+  CK(cudaMemcpyAsync(c->h_keys, c->d_keys, (size_t)nwin * sizeof(ErrKey), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int w = 0; w < nwin; ++w)
+    h_codes[w] = (c->h_keys[w] == kNoError) ? -1 : (long long)c->h_keys[w];
+  return 0;
 }
 
 namespace {

@@ -41,7 +41,7 @@ from .lifting import Distribution, as_device_f
 
 __all__ = ["constant_tau", "ConstantTau", "KineticParams", "stable_dt_kinetic",
            "transport_update", "bgk_relax", "propagate_kinetic", "fine_schedule",
-           "propagate_window"]
+           "propagate_window", "propagate_windows"]
 
 SPAN_GUARD = 1e-12  # ref/kinetic.py:39
 
@@ -258,3 +258,37 @@ def propagate_window(ctx, mom0: torch.Tensor, t0: float, t1: float, grid, params
         return -1
     return _run_schedule(ctx, None, mom0, dts, params, ctx.f_scratch(1), want_f=False,
                          mom_out=mom_out)
+
+
+def propagate_windows(ctx, mom_in: torch.Tensor, spans, grid, params, dt_max,
+                      mom_out: torch.Tensor) -> list:
+    """P(F(L(U_w))) for every window w of a batch in one library call
+    (``pbgk_propagate_windows``: one host synchronisation for the batch).
+
+    mom_in / mom_out: (nwin, 5, nx) device tensors; spans[w] = t1 - t0 of
+    window w.  Returns the status keys (-1 clean).  Constant tau only; the
+    schedule of each window is that of ``propagate_window``."""
+    _check_grid(grid, params)
+    tc = tau_constant(params.tau)
+    if tc is None:
+        raise ConfigurationError("propagate_windows needs a constant tau")
+    cap = stable_dt_kinetic(grid, params)
+    if dt_max is not None:
+        cap = min(cap, dt_max)
+    counts, dts = [], []
+    for span in spans:
+        d = fine_schedule(span, cap) if span > 0.0 else []
+        counts.append(len(d))
+        dts += [_kdt(x, params) for x in d]
+    nwin = len(spans)
+    _scheme(ctx, params)
+    E, e_max = rt.to_device_field(params.force, ctx.device, ctx.nx)
+    c_counts = (ctypes.c_int * max(nwin, 1))(*counts)
+    c_dts = (ctypes.c_double * max(len(dts), 1))(*dts)
+    codes = (ctypes.c_longlong * max(nwin, 1))()
+    rt._lib.check(ctx.lib.pbgk_propagate_windows(
+        ctx.h, nwin, rt.ptr(mom_in), rt.ptr(mom_out), rt.ptr(ctx.f_scratch(0)),
+        rt.ptr(ctx.f_scratch(1)), c_counts, c_dts, float(params.epsilon), tc, rt.ptr(E), e_max,
+        rt.stream_handle(ctx.device), codes), "pbgk_propagate_windows")
+    return [codes[w] for w in range(nwin)]
+
