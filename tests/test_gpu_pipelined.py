@@ -81,3 +81,19 @@ def test_pipelined_overshoot_raises_like_phased():
         except P.CorrectionOvershootError as e:
             out.append(e.slice_index)
     assert out[0] == out[1]
+
+
+def test_fine_stage_failure_same_error_both_schedules():
+    # an unstable kinetic CFL: the batched fine stage (phased) and the
+    # per-window calls (pipelined) must raise the same error -- the
+    # reference's precedence makes it DegenerateStateError (rho or theta <= 0)
+    # or BlowUpError (non-finite), with the same step
+    # long windows (~85 steps at CFL 6): the upwind amplification runs away
+    d, U0 = _sod(32, 8, 4.0, 2, 2, P.BoundaryKind.PERIODIC)
+    kp, fp = P.KineticParams(1e-2, cfl=6.0), P.FluidParams()
+    seen = []
+    for pipe in (False, True):
+        with pytest.raises(P.SolverError) as ei:
+            P.run_parareal(U0, P.PararealConfig(2, 1e-300, pipelined=pipe), d, kp, fp)
+        seen.append((type(ei.value).__name__, getattr(ei.value, "step", None), str(ei.value)))
+    assert seen[0] == seen[1]
