@@ -31,6 +31,11 @@
  *    Keys are min-reduced: lowest unit, then earliest step, then the
  *    reference's raise order within a step (ref/moments.py:102-104,
  *    ref/lifting.py:44-45, ref/kinetic.py:157-159, ref/fluid.py:117-122).
+ *  - Threads: pbgk_last_error() is per thread; a context holds mutable
+ *    workspaces (tables, partial records, failure word, tensor-map cache), so
+ *    calls on one context must not run concurrently from several threads, and
+ *    its own workspaces are used on one stream at a time (the *_async / *_range
+ *    entry points take caller-owned buffers and may run on a second stream).
  */
 #ifndef PBGK_H
 #define PBGK_H
