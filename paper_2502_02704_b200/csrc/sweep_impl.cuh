@@ -258,6 +258,9 @@ __global__ void __launch_bounds__(NTHR, MINB)
   static_assert(!(TRAP && FIELD), "the field term is defined on midpoint velocity cells only");
   static_assert(!(MUSCL && FIELD), "MUSCL x transport has no v_x field term");
   constexpr int LEAD = MUSCL ? 2 : 1, TRAIL = MUSCL ? 1 : 0;
+  // field term formulation: expanded per-cell coefficients (even V) or
+  // relaxed neighbour rows (odd V); see the body
+  constexpr bool FEXP = (V % 2 == 0);
   constexpr int NL = NTHR / LZ;  // line groups
   constexpr int NW = NTHR / 32;
   constexpr int BZ = LZ * V;
@@ -370,6 +373,7 @@ __global__ void __launch_bounds__(NTHR, MINB)
   // trapezoidal quadrature (a.trap): lines / lanes on the end nodes of an axis
   // take weight 1/2 (exact) in the marginal partials
   unsigned xedge = 0, yedge = 0, zedge = 0;
+  unsigned xlo = 0, xhi = 0;  // field term: lines on the first / last v_x row
   unsigned zmask = 0;  // bit v: element v of this lane is inside the grid
   bool full = false;   // every line and element of this thread is valid
   int cur_tile = -1;
@@ -399,6 +403,7 @@ __global__ void __launch_bounds__(NTHR, MINB)
       tg = tile_geom(T, a.nvx, t);
       vmask = 0;
       xedge = yedge = zedge = 0;
+      xlo = xhi = 0;
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const int l = line_of(k);
@@ -411,6 +416,8 @@ __global__ void __launch_bounds__(NTHR, MINB)
         goff[k] = (jx * a.nvy + jy) * a.nvz + tg.z0 + zpos<V, LZ>(lz, 0);
         cvx[k] = SCX[jx];
         if (jx == 0 || jx == a.nvx - 1) xedge |= 1u << k;
+        if (jx == 0) xlo |= 1u << k;
+        if (jx == a.nvx - 1) xhi |= 1u << k;
         if (jy == 0 || jy == a.nvy - 1) yedge |= 1u << k;
       }
       zmask = 0;
@@ -430,6 +437,11 @@ __global__ void __launch_bounds__(NTHR, MINB)
     const int sh = a.bc == 3 ? 1 : 0;  // slab buffers: one padding plane / row
     const double* SF = reinterpret_cast<const double*>(smem + (size_t)stg * stage_bytes);
     const double* ST = reinterpret_cast<const double*>(smem + (size_t)stg * stage_bytes + box_bytes);
+    // the cell's field value is read before the stage wait so its global-load
+    // latency overlaps the wait (the wait's memory clobber keeps the order)
+    // (not for odd V: those kernels run at the register limit)
+    double e_cell = 0.0;
+    if (FIELD && FEXP && out_plane) e_cell = __ldg(a.E + i);
     if (TMA) {
       mbar_wait(&bars[stg], ph);
     } else if (i >= 0 || a.bc == 3) {
@@ -467,12 +479,32 @@ __global__ void __launch_bounds__(NTHR, MINB)
       const bool transport = a.dtdx != 0.0;
       const double dtdx = a.dtdx;
       double hE = 0.0;
-      if (FIELD && out_plane) hE = __dmul_rn(0.5, __ldg(a.E + i));
+      if (FIELD && out_plane) hE = __dmul_rn(0.5, FEXP ? e_cell : __ldg(a.E + i));
       // v_x Rusanov flux of ref/kinetic.py:114-123 reassociated per cell:
-      // G(lo, hi) = E/2 (lo + hi) - e_max/2 (hi - lo) = cp lo + cm hi
-      // (2 fp64 ops per face instead of 5; within an ulp of the reference's
-      // order, well inside the 1e-10 parity bound)
+      // G(lo, hi) = E/2 (lo + hi) - e_max/2 (hi - lo) = cp lo + cm hi.  The
+      // update -dt/dv (G_{j+1/2} - G_{j-1/2}) of row j is linear in the
+      // relaxed rows x (j), fp (j+1), fm (j-1):
+      //   interior  -dt/dv ((cp - cm) x + cm fp - cp fm)
+      //   j = 0     -dt/dv (cp x + cm fp)          (no lower face)
+      //   j = n-1   -dt/dv (-cm x - cp fm)         (no upper face)
+      // and fp = r raw_p + s g_x[j+1] g_y g_z with s = r ls (s = ls, no raw,
+      // for the synthesised first pass), likewise fm.  So per cell: kx_* on x,
+      // kp / km on the raw neighbours, and per line kg on g_z -- 4 FMAs per
+      // element instead of relaxing both neighbours (within a few ulps of the
+      // reference's order, far inside the 1e-10 parity bound)
       const double cp = hE + a.half_emax, cm = hE - a.half_emax;
+      double kx_in = 0.0, kx_lo = 0.0, kx_hi = 0.0, kp = 0.0, km = 0.0, fCm = 0.0, fCp = 0.0;
+      if (FIELD && FEXP) {
+        const double D = -a.dtdv;
+        kx_in = D * (cp - cm);
+        kx_lo = D * cp;
+        kx_hi = -(D * cm);
+        const double s = SYNTH ? ls : r * ls;
+        fCm = (D * s) * cm;
+        fCp = -((D * s) * cp);
+        kp = (D * r) * cm;
+        km = -((D * r) * cp);
+      }
       double* gdst = (a.fout != nullptr && out_plane) ? a.fout + (size_t)(i_out + sh) * a.plane : nullptr;
       double lp[K];
       double pz[V];
@@ -534,8 +566,31 @@ __global__ void __launch_bounds__(NTHR, MINB)
 #pragma unroll
               for (int v = 0; v < V; ++v) o[v] = x[v];
             }
-            if (FIELD && (FAST || transport)) {
-              // ref/kinetic.py:114-123: Rusanov flux on interior v_x faces of f_pre
+            if (FIELD && FEXP && (FAST || transport)) {
+              // ref/kinetic.py:114-123: Rusanov flux on interior v_x faces of
+              // f_pre, expanded over the relaxed neighbours (see kx_* above):
+              // -dt/dv (G_hi - G_lo) = kx x + kp rp + km rm + kg gz
+              const bool has_lo = !((xlo >> k) & 1u), has_hi = !((xhi >> k) & 1u);
+              const double gpl = has_hi ? ST[gxi[k] + 1] : 0.0;
+              const double gmi = has_lo ? ST[gxi[k] - 1] : 0.0;
+              const double kg = ST[gyi[k]] * fma(fCm, gpl, fCp * gmi);
+              const double kx = has_lo ? (has_hi ? kx_in : kx_hi) : (has_hi ? kx_lo : 0.0);
+              if (SYNTH) {
+#pragma unroll
+                for (int v = 0; v < V; ++v) o[v] = fma(kg, gz[v], fma(kx, x[v], o[v]));
+              } else {
+                // neighbour rows outside the cube are zero-filled by the load
+                double rm[V], rp[V];
+                lds_lane<V, LZ>(SF + soff[k] - T.By * BZ, rm);
+                lds_lane<V, LZ>(SF + soff[k] + T.By * BZ, rp);
+#pragma unroll
+                for (int v = 0; v < V; ++v)
+                  o[v] = fma(kg, gz[v], fma(km, rm[v], fma(kp, rp[v], fma(kx, x[v], o[v]))));
+              }
+            } else if (FIELD && (FAST || transport)) {
+              // the same flux with both neighbour rows relaxed first (fewer
+              // live per-cell coefficients: measured faster for odd V, whose
+              // kernels run at the register limit)
               const int jx = gxi[k] - a.gxo;
               const bool has_lo = jx > 0, has_hi = jx + 1 < a.nvx;
               double fm[V], fp[V];
