@@ -53,6 +53,9 @@
 #ifndef PBGK_HINT_PART
 #define PBGK_HINT_PART 1
 #endif
+#ifndef PBGK_OUT_ROT
+#define PBGK_OUT_ROT 1
+#endif
 
 namespace pbgk {
 
@@ -766,8 +769,16 @@ __global__ void __launch_bounds__(NTHR, MINB)
       const double* LTb = LT + (j & 1) * lines;
       const double* PZb = PZ + (j & 1) * NW * BZ;
       double* dst = a.part + ((size_t)i_out * T.NT + t) * T.PS;
+#if PBGK_OUT_ROT
+      // z outputs first, then x, then y, on consecutive threads starting at a
+      // warp that rotates with the item (the serial sums move round the CTA)
+      int q = tid - (j & (NW - 1)) * 32;
+      if (q < 0) q += NTHR;
+      const int o = q < BZ ? T.A + T.By + q : (q < BZ + T.A + T.By ? q - BZ : 1 << 20);
+#else
       const int chunk = (T.A + T.By + BZ + NW - 1) / NW;
       const int o = lane < chunk ? warp * chunk + lane : 1 << 20;
+#endif
       if (o < T.A) {
         if (tg.r0 + o < tg.r1) {
           double s2 = 0.0;
