@@ -159,6 +159,16 @@ int pbgk_ctx_set_quadrature(pbgk_ctx* ctx, int quadrature);
  * MUSCL has no v_x field term: sweeps with E != 0 fail on a MUSCL context. */
 int pbgk_set_x_scheme(pbgk_ctx* ctx, int scheme);
 
+/* Multi-step path of pbgk_propagate / pbgk_propagate_windows for windows
+ * that start from moments (mom0, f0 == NULL) with the upwind scheme, no v_x
+ * field term and bc 0..2: `levels` (1..3; default 2) fine steps per pass
+ * over f, their relax tables from the 2-D marginal recursion (the marginals
+ * of f over v_z and over v_y evolve in closed form under the upwind x
+ * transport and the separable BGK relaxation), so f is read and written once
+ * per `levels` steps.  Same results as the one-step path to rounding (the
+ * marginal sums are taken in another order); 0 = always the one-step path. */
+int pbgk_set_fusion(pbgk_ctx* ctx, int levels);
+
 /* ---- x-sharded fine propagation (slabs) --------------------------------- */
 /* A context created with bc = 3 is one x-slab of a larger domain (one rank
  * of an x-sharded F, EXTENSION: SURVEY 8(f) rank 2).  Its f buffers are

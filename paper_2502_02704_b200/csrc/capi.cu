@@ -24,6 +24,12 @@ cudaError_t launch_sweep(int cfg_id, const CUtensorMap& map, const SweepArgs& a,
                          bool field, int grid, int ns, size_t smem, cudaStream_t st);
 size_t sweep_smem_bytes(const SweepArgs& a, int V, int LZ, int NTHR, bool synth, bool tma, int ns);
 cudaError_t launch_finalize(const FinalArgs& a, cudaStream_t st);
+cudaError_t launch_fsweep(int cfg_id, const CUtensorMap& map, const FSweepArgs& a, bool synth, int L,
+                          int grid, int ns, size_t smem, cudaStream_t st);
+size_t fsweep_smem_bytes(const FSweepArgs& a, int V, int LZ, bool synth, int L, int ns);
+bool fsweep_has_cfg(int cfg_id);
+cudaError_t launch_marg(const MargArgs& m, const FinalArgs& f, cudaStream_t st);
+size_t marg_smem_bytes(int nvx, int nvy, int nvz, int TL);
 cudaError_t launch_set_key(ErrKey* p, ErrKey v, cudaStream_t st);
 cudaError_t launch_fluid_batch(const FluidArgs& a, int nwin, const double* in, double* out,
                                const double* minuend, const double* t0, const double* t1,
@@ -142,6 +148,11 @@ struct pbgk_ctx {
   size_t times_cap = 0;
   std::vector<MapEntry> maps;
   size_t ws_bytes = 0;
+  // multi-step path (fsweep.cu + marginal.cu): levels per pass (0 = off),
+  // the 2-D marginal ping-pong and a ring of four relax-table buffers
+  int fuse = 2;
+  double* d_marg[2] = {nullptr, nullptr};
+  double* d_tabs[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 
 namespace {
@@ -516,6 +527,8 @@ void pbgk_ctx_destroy(pbgk_ctx* c) {
   cudaFree(c->d_part);
   cudaFree(c->d_tab[0]);
   cudaFree(c->d_tab[1]);
+  for (auto* p : c->d_marg) cudaFree(p);
+  for (auto* p : c->d_tabs) cudaFree(p);
   cudaFree(c->d_scratch);
   cudaFree(c->d_err);
   cudaFree(c->d_keys);
@@ -637,12 +650,19 @@ int pbgk_check_finite(pbgk_ctx* c, const double* f, int step, void* stream, long
 }
 
 namespace {
+bool fused_ok(pbgk_ctx* c, bool field);
+int propagate_body_fused(pbgk_ctx* c, const double* mom0, double* f_out, double* f_tmp,
+                         int write_final, double* mom_out, int S, const double* h_dts, double eps,
+                         double tau, cudaStream_t st);
+
 // One propagation on the stream, failures atomicMin-ed into the current
 // error slot; no reset, no host synchronisation.
 int propagate_body(pbgk_ctx* c, const double* f0, const double* mom0, double* f_out, double* f_tmp,
                    int write_final, double* mom_out, int S, const double* h_dts, double eps,
                    double tau, const double* E, double e_max, cudaStream_t st) {
   const bool field = (E != nullptr && e_max > 0.0);
+  if (!f0 && S > 0 && fused_ok(c, field))
+    return propagate_body_fused(c, mom0, f_out, f_tmp, write_final, mom_out, S, h_dts, eps, tau, st);
   const int pid = field ? 1 : (c->x_scheme == 1 ? 2 : 0);
   const int W = S + (write_final ? 1 : 0);
   auto buf = [&](int w) { return ((W - w) % 2 == 0) ? f_out : f_tmp; };
@@ -669,6 +689,145 @@ int propagate_body(pbgk_ctx* c, const double* f0, const double* mom0, double* f_
         run_final(c, pid, kFinProject, nullptr, mom_out, nullptr, 0, 1, 1, nullptr, S + 1, st))
       return -1;
   }
+  return 0;
+}
+}  // namespace
+
+namespace {
+// Multi-step path usable on this context for an upwind propagation without
+// the v_x field term (the marginal recursion is closed for it; MUSCL's
+// limiter is not linear, slabs exchange halos per step).
+bool fused_ok(pbgk_ctx* c, bool field) {
+  static const int env = getenv("PBGK_FUSE") ? atoi(getenv("PBGK_FUSE")) : -1;  // dev A/B knob
+  const int L = env >= 0 ? env : c->fuse;
+  if (L < 1 || field || c->x_scheme != 0 || c->g.bc == 3) return false;
+  if (!fsweep_has_cfg(c->plan[0].cfg)) return false;
+  if (marg_smem_bytes(c->g.nvx, c->g.nvy, c->g.nvz, c->TL) > c->smem_optin) return false;
+  if (!c->d_marg[0]) {
+    const size_t ms = (size_t)c->g.nx * c->g.nvx * (c->g.nvy + c->g.nvz) * sizeof(double);
+    const size_t tb = (size_t)c->g.nx * c->TL * sizeof(double);
+    for (auto*& p : c->d_marg)
+      if (cudaMalloc(&p, ms) != cudaSuccess) return false;
+    for (auto*& p : c->d_tabs)
+      if (cudaMalloc(&p, tb) != cudaSuccess) return false;
+    c->ws_bytes += 2 * ms + 4 * tb;
+  }
+  return true;
+}
+
+int fuse_levels(pbgk_ctx* c) {
+  static const int env = getenv("PBGK_FUSE") ? atoi(getenv("PBGK_FUSE")) : -1;
+  return std::min(env >= 0 ? env : c->fuse, 3);
+}
+
+int run_marg(pbgk_ctx* c, const double* min, double* mout, const double* tab_in, double* tab_out,
+             double dt, double eps, double tau, int step, cudaStream_t st) {
+  MargArgs m{};
+  m.nx = c->g.nx;
+  m.nvx = c->g.nvx;
+  m.nvy = c->g.nvy;
+  m.nvz = c->g.nvz;
+  m.bc = c->g.bc;
+  m.min = min;
+  m.mout = mout;
+  m.tab_in = tab_in;
+  m.cx = c->d_c[0];
+  m.dtdx = dt / c->dx;
+  FinalArgs f = fin_args(c, c->plan[0]);
+  f.mode = kFinRelax;
+  f.tab = tab_out;
+  f.dt = dt;
+  f.eps = eps;
+  f.tau = tau;
+  f.step = step;
+  ProfScope ps(c, st, 1, 0.0);
+  CK(launch_marg(m, f, st));
+  return 0;
+}
+
+// One pass of n <= 3 fine steps (steps s0+1 .. s0+n) over f.
+int run_fsweep(pbgk_ctx* c, int n, const double* in, double* out, const double* const* tabs,
+               const double* dtdx, int step0, cudaStream_t st) {
+  const Plan& p = c->plan[0];
+  const CfgShape& s = kCfg[p.cfg];
+  FSweepArgs a{};
+  a.nx = c->g.nx;
+  a.nvx = c->g.nvx;
+  a.nvy = c->g.nvy;
+  a.nvz = c->g.nvz;
+  a.plane = (long long)c->g.nvx * c->g.nvy * c->g.nvz;
+  a.t = p.t;
+  a.total = (long long)p.t.NT * c->g.nx;
+  a.fin = in;
+  a.fout = out;
+  for (int l = 0; l < n; ++l) {
+    a.tab[l] = tabs[l];
+    a.dtdx[l] = dtdx[l];
+  }
+  a.TL = c->TL;
+  a.gxo = c->gxo;
+  a.gyo = c->gyo;
+  a.gzo = c->gzo;
+  a.cx = c->d_c[0];
+  a.bc = c->g.bc;
+  a.err = c->err_slot ? c->err_slot : c->d_err;
+  a.step0 = step0;
+  const bool synth = (in == nullptr);
+  const CUtensorMap* map = tensor_map(c, synth ? nullptr : in, p.t, p.cfg);
+  if (!map) return fail("tensor map: " + g_last_error);
+  // ring depth: the plan's, fewer stages if the L table rows per stage do not
+  // fit the plan's CTAs per SM
+  const size_t budget = (p.per_sm == 2) ? (c->smem_per_sm / 2) - 2048 : c->smem_optin;
+  int ns = p.ns;
+  while (ns > 2 && fsweep_smem_bytes(a, s.V, s.LZ, synth, n, ns) > budget) --ns;
+  const size_t smem = fsweep_smem_bytes(a, s.V, s.LZ, synth, n, ns);
+  const double fbytes = 8.0 * (double)a.plane * a.nx;
+  ProfScope ps(c, st, 0, (synth ? 0.0 : fbytes) + fbytes);
+  int grid = p.grid;
+  if (c->slot_reserve > 0) grid = std::max(1, std::min(grid, c->nsm * p.per_sm - c->slot_reserve));
+  CK(launch_fsweep(p.cfg, *map, a, synth, n, grid, ns, smem, st));
+  return 0;
+}
+
+// propagate_body for a window from moments on the multi-step path: the
+// marginal recursion produces R_1..R_S one step ahead of the passes; the
+// passes take up to L steps each; the last relax + projection is the
+// reference-order marginal sweep of f_S (P(f_S) comes from f itself).
+int propagate_body_fused(pbgk_ctx* c, const double* mom0, double* f_out, double* f_tmp,
+                         int write_final, double* mom_out, int S, const double* h_dts, double eps,
+                         double tau, cudaStream_t st) {
+  const int L = fuse_levels(c);
+  const int P = (S + L - 1) / L;  // passes
+  const int W = P + (write_final ? 1 : 0);
+  auto buf = [&](int w) { return ((W - w) % 2 == 0) ? f_out : f_tmp; };
+  double** T4 = c->d_tabs;
+  if (run_final(c, 0, kFinSynthRaw, mom0, nullptr, T4[0], 0, 1, 1, nullptr, 0, st)) return -1;
+  int s0 = 0, w = 0;
+  const double* in = nullptr;
+  for (int s = 1; s <= S; ++s) {
+    const double dt = h_dts[s - 1];
+    if (run_marg(c, s == 1 ? nullptr : c->d_marg[(s - 1) & 1], c->d_marg[s & 1], T4[(s - 1) & 3],
+                 T4[s & 3], dt, eps, tau, s, st))
+      return -1;
+    if (s - s0 == L || s == S) {
+      const int n = s - s0;
+      const double* tabs[kMaxLevels];
+      double dtdx[kMaxLevels];
+      for (int l = 0; l < n; ++l) {
+        tabs[l] = T4[(s0 + l) & 3];
+        dtdx[l] = h_dts[s0 + l] / c->dx;
+      }
+      double* out = buf(++w);
+      if (run_fsweep(c, n, in, out, tabs, dtdx, s0 + 1, st)) return -1;
+      in = out;
+      s0 = s;
+    }
+  }
+  if (run_sweep(c, 0, false, in, T4[S & 3], write_final ? f_out : nullptr, 0.0, nullptr, 0.0, 0.0, S,
+                st))
+    return -1;
+  if (mom_out && run_final(c, 0, kFinProject, nullptr, mom_out, nullptr, 0, 1, 1, nullptr, S + 1, st))
+    return -1;
   return 0;
 }
 }  // namespace
@@ -880,6 +1039,13 @@ int pbgk_set_x_scheme(pbgk_ctx* c, int scheme) {
   if (!c) return fail("pbgk_set_x_scheme: null context");
   if (scheme != 0 && scheme != 1) return fail("pbgk_set_x_scheme: scheme must be 0 (upwind) or 1 (MUSCL)");
   c->x_scheme = scheme;
+  return 0;
+}
+
+int pbgk_set_fusion(pbgk_ctx* c, int levels) {
+  if (!c) return fail("pbgk_set_fusion: null context");
+  if (levels < 0 || levels > 3) return fail("pbgk_set_fusion: levels must be 0 (off) .. 3");
+  c->fuse = levels;
   return 0;
 }
 

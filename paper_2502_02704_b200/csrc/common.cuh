@@ -69,6 +69,41 @@ struct SweepArgs {
   int debug;         // development ablations (PBGK_DEBUG): 1 no reductions, 4 copy-through
 };
 
+// Multi-step sweep (fsweep.cu): L consecutive fine steps per pass over f,
+// the relax tables of every step known beforehand (marginal recursion,
+// marginal.cu), no reductions.  Level l reads the tables tab[l] and moves by
+// dtdx[l]; the pass reads f*_s (or synthesises f_0) and writes f*_{s+L}.
+constexpr int kMaxLevels = 4;
+struct FSweepArgs {
+  int nx, nvx, nvy, nvz;
+  long long plane;
+  Tiling t;
+  long long total;
+  const double* fin;   // null: level 0 synthesises f_0 from tab[0]
+  double* fout;
+  const double* tab[kMaxLevels];
+  int TL, gxo, gyo, gzo;
+  const double* cx;
+  double dtdx[kMaxLevels];
+  int bc;
+  ErrKey* err;
+  int step0;           // step number of level 0's output (BlowUpError keys)
+};
+
+// Marginal recursion (marginal.cu): the 2-D marginals M_xy = sum_z f and
+// M_xz = sum_y f of f*_s obey a closed recursion under the upwind x transport
+// and the separable BGK relaxation (both act on a v_x row with coefficients
+// independent of v_y, v_z).  One step maps M(f*_{s-1}) and the tables of
+// R_{s-1} to M(f*_s), its 1-D marginals and the tables of R_s.
+struct MargArgs {
+  int nx, nvx, nvy, nvz, bc;
+  const double* min;   // M(f*_{s-1}): nx * MS doubles; null: f_{s-1} = lift (tab_in r = 0)
+  double* mout;        // M(f*_s)
+  const double* tab_in;
+  const double* cx;
+  double dtdx;
+};
+
 enum FinalMode : int {
   kFinRelax = 0,      // tables of the normalised Maxwellian + lambda (bgk_relax)
   kFinSynthRaw = 1,   // tables of the un-normalised lift (window start)

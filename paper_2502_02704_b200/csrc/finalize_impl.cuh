@@ -93,8 +93,51 @@ static __device__ __forceinline__ double warp_allsum(double x) {
   return x;
 }
 
+// Tile partials of cell i -> marginals m_x | m_y | m_z in sm (contiguous),
+// by the whole calling CTA; ends with a CTA barrier.
+static __device__ __forceinline__ void gather_marginals(const FinalArgs& a, int i, double* sm) {
+  const int tid = threadIdx.x;
+  const int nvx = a.nvx, nvy = a.nvy, nvz = a.nvz;
+  const Tiling& T = a.t;
+  const double* P = a.part + (size_t)i * T.NT * T.PS;
+  double* csum = sm + 2 * (nvx + nvy + nvz);
+  const int k0 = (list_len(T, 0) + kChunk - 1) / kChunk;
+  const int k1 = (list_len(T, 1) + kChunk - 1) / kChunk;
+  const int k2 = (list_len(T, 2) + kChunk - 1) / kChunk;
+  const int t1 = k0 * nvx, t2 = t1 + k1 * nvy, t3 = t2 + k2 * nvz;
+  // one chunk per entry (small tilings): the chunk sum IS the marginal
+  const bool single = (t3 == nvx + nvy + nvz);
+  double* dst = single ? sm : csum;
+  for (int t = tid; t < t3; t += blockDim.x) {
+    const int ax = t < t1 ? 0 : (t < t2 ? 1 : 2);
+    const int q = t - (ax == 0 ? 0 : (ax == 1 ? t1 : t2));
+    const int n = ax == 0 ? nvx : (ax == 1 ? nvy : nvz);
+    const int c = q / n, j = q - c * n;
+    const int len = list_len(T, ax);
+    const EntryList e = entry_list(T, ax, j);
+    const int q1 = min(len, (c + 1) * kChunk);
+    dst[t] = chunk_sum(P, T.PS, e, c * kChunk, q1);
+  }
+  __syncthreads();
+  if (!single) {
+    for (int j = tid; j < nvx + nvy + nvz; j += blockDim.x) {
+      const int ax = j < nvx ? 0 : (j < nvx + nvy ? 1 : 2);
+      const int jj = j - (ax == 0 ? 0 : (ax == 1 ? nvx : nvx + nvy));
+      const int n = ax == 0 ? nvx : (ax == 1 ? nvy : nvz);
+      const int kk = ax == 0 ? k0 : (ax == 1 ? k1 : k2);
+      const double* cs0 = csum + (ax == 0 ? 0 : (ax == 1 ? t1 : t2)) + jj;
+      double s = 0.0;
+      for (int c = 0; c < kk; ++c) s += cs0[c * n];
+      sm[j] = s;  // mx | my | mz are contiguous
+    }
+    __syncthreads();
+  }
+}
+
 // One x cell, by the whole calling CTA (blockDim >= 128; warps 0-3 reduce).
 // sm: 2*(nvx+nvy+nvz) doubles of scratch, sh: 16 doubles.  Block-uniform call.
+// HAVE_MARG: the marginals are already in sm (marginal recursion, marginal.cu).
+template <bool HAVE_MARG = false>
 static __device__ __forceinline__ void finalize_cell(const FinalArgs& a, int i, double* sm, double* sh) {
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -124,40 +167,7 @@ static __device__ __forceinline__ void finalize_cell(const FinalArgs& a, int i, 
     u2 = a.mom_in[3 * a.nx + i];
     th = a.mom_in[4 * a.nx + i];
   } else {
-    const Tiling& T = a.t;
-    const double* P = a.part + (size_t)i * T.NT * T.PS;
-    double* csum = sm + 2 * (nvx + nvy + nvz);
-    const int k0 = (list_len(T, 0) + kChunk - 1) / kChunk;
-    const int k1 = (list_len(T, 1) + kChunk - 1) / kChunk;
-    const int k2 = (list_len(T, 2) + kChunk - 1) / kChunk;
-    const int t1 = k0 * nvx, t2 = t1 + k1 * nvy, t3 = t2 + k2 * nvz;
-    // one chunk per entry (small tilings): the chunk sum IS the marginal
-    const bool single = (t3 == nvx + nvy + nvz);
-    double* dst = single ? sm : csum;
-    for (int t = tid; t < t3; t += blockDim.x) {
-      const int ax = t < t1 ? 0 : (t < t2 ? 1 : 2);
-      const int q = t - (ax == 0 ? 0 : (ax == 1 ? t1 : t2));
-      const int n = ax == 0 ? nvx : (ax == 1 ? nvy : nvz);
-      const int c = q / n, j = q - c * n;
-      const int len = list_len(T, ax);
-      const EntryList e = entry_list(T, ax, j);
-      const int q1 = min(len, (c + 1) * kChunk);
-      dst[t] = chunk_sum(P, T.PS, e, c * kChunk, q1);
-    }
-    __syncthreads();
-    if (!single) {
-      for (int j = tid; j < nvx + nvy + nvz; j += blockDim.x) {
-        const int ax = j < nvx ? 0 : (j < nvx + nvy ? 1 : 2);
-        const int jj = j - (ax == 0 ? 0 : (ax == 1 ? nvx : nvx + nvy));
-        const int n = ax == 0 ? nvx : (ax == 1 ? nvy : nvz);
-        const int kk = ax == 0 ? k0 : (ax == 1 ? k1 : k2);
-        const double* cs0 = csum + (ax == 0 ? 0 : (ax == 1 ? t1 : t2)) + jj;
-        double s = 0.0;
-        for (int c = 0; c < kk; ++c) s += cs0[c * n];
-        sm[j] = s;  // mx | my | mz are contiguous
-      }
-      __syncthreads();
-    }
+    if (!HAVE_MARG) gather_marginals(a, i, sm);
     // finiteness of f* (all its values feed these sums; a NaN/Inf anywhere
     // leaves a non-finite marginal) -- the guard of ref/kinetic.py:157-159;
     // warps 1..3 test their axis while reducing the folded first moment

@@ -1,0 +1,304 @@
+// Multi-step sweep: L fine steps of f per pass, no reductions.
+//
+// With the relax tables of every step computed beforehand by the marginal
+// recursion (marginal.cu), step s+1 of ref/kinetic.py:152-160 needs nothing
+// grid-wide: f*_{s+1}(i) = T(R_s(f*_s))(i) depends on the cell itself and its
+// upwind neighbour plane only.  A tile marching in x (sweep_impl.cuh) can then
+// run L steps at once: every level keeps the upwind flux of the previous plane
+// in registers, level l+1 relaxes level l's output with its own table row and
+// transports it, and only the last level is stored.  HBM traffic per
+// cell-update drops from 16 B to 16/L B.
+//
+// Halo: a tile run that starts at plane p0 is preceded by L lead items at
+// p0-L .. p0-1; lead item k (depth k) completes levels < k and relaxes level k
+// (its flux becomes `prev` for the next plane).  Ghost planes: absorbing =
+// zero flux at every level; periodic = wrap; outflow = the edge plane again,
+// which reproduces the zero-gradient ghost at every level (the edge cell's
+// inflow flux difference is exactly zero).
+//
+// Finiteness (ref/kinetic.py:157-159): each thread sums its stored values of
+// every level; a non-finite sum flags BlowUpError at that level's step (same
+// documented corner as the marginal check: finite values whose sum overflows).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <type_traits>
+
+#include "common.cuh"
+#include "ptx.cuh"
+#include "sweep_impl.cuh"
+
+namespace pbgk {
+
+template <int V, int LZ, int K, int NTHR, int MINB, bool SYNTH, int L>
+__global__ void __launch_bounds__(NTHR, MINB)
+    fsweep_kernel(const __grid_constant__ CUtensorMap fmap, const FSweepArgs a, int ns) {
+  constexpr int NL = NTHR / LZ;
+  constexpr int BZ = LZ * V;
+  extern __shared__ __align__(128) unsigned char smem[];
+
+  const Tiling& T = a.t;
+  const int tid = threadIdx.x;
+  const int lz = tid % LZ;
+  const int lg = tid / LZ;
+  const int lines = T.A * T.By;
+  const int lgBy = __ffs(T.By) - 1;
+  const int nx = a.nx;
+
+  const uint32_t box_bytes = SYNTH ? 0u : (uint32_t)(T.A * T.By * BZ) * 8u;
+  const uint32_t tab_bytes = (uint32_t)(a.TL * 8);
+  const uint32_t stage_bytes = (box_bytes + L * tab_bytes + 127u) & ~127u;
+  double* SCX = reinterpret_cast<double*>(smem + (size_t)ns * stage_bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(SCX + ((a.nvx + 1) & ~1));
+
+  const int g0 = (int)((a.total * blockIdx.x) / gridDim.x);
+  const int g1 = (int)((a.total * (blockIdx.x + 1)) / gridDim.x);
+
+  for (int j = tid; j < a.nvx; j += NTHR) SCX[j] = a.cx[j];
+  if (tid == 0) {
+    for (int s = 0; s < ns; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  pdl_wait();
+  pdl_trigger();
+  __syncthreads();
+
+  const int ptid = NTHR - 32;
+  ItemIter<L, 0> prod;
+  prod.init(g0, g1, nx);
+  int pstg = 0, ptile = -1;
+  TileGeom ptg{};
+  auto issue_next = [&]() {
+    int t, p, h;
+    prod.next(nx, t, p, h);
+    if (t != ptile) {
+      ptile = t;
+      ptg = tile_geom(T, a.nvx, t);
+    }
+    const int i = item_plane(nx, a.bc, ptg, p);
+    const int s = pstg;
+    if (++pstg == ns) pstg = 0;
+    uint64_t* bar = &bars[s];
+    unsigned char* st = smem + (size_t)s * stage_bytes;
+    if (i < 0) {
+      mbar_arrive_expect_tx(bar, 0);
+      return;
+    }
+    mbar_arrive_expect_tx(bar, box_bytes + L * tab_bytes);
+    if (!SYNTH) tma_load_4d(st, &fmap, ptg.z0, ptg.y0, ptg.r0, i, bar);
+#pragma unroll
+    for (int l = 0; l < L; ++l)
+      tma_load_1d(st + box_bytes + l * tab_bytes, a.tab[l] + (size_t)i * a.TL, tab_bytes, bar);
+  };
+  if (tid == ptid) {
+    prefetch_tensormap(&fmap);
+    for (int s = 0; s < ns && !prod.done(); ++s) issue_next();
+  }
+
+  int soff[K], lab[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    int l = lg + k * NL;
+    if (l >= lines) l = 0;
+    const int aa = l >> lgBy, b = l & (T.By - 1);
+    soff[k] = (aa * T.By + b) * BZ + zpos<V, LZ>(lz, 0);
+    lab[k] = (aa << 16) | b;
+  }
+  int gxi[K], gyi[K], goff[K];
+  double cvx[K];
+  unsigned vmask = 0, zmask = 0;
+  bool full = false;
+  int cur_tile = -1;
+  TileGeom tg{};
+
+  double prev[L][K][V];
+#pragma unroll
+  for (int l = 0; l < L; ++l)
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int v = 0; v < V; ++v) prev[l][k][v] = 0.0;
+  double acc[L];
+#pragma unroll
+  for (int l = 0; l < L; ++l) acc[l] = 0.0;
+
+  ItemIter<L, 0> it;
+  it.init(g0, g1, nx);
+  int stg = 0;
+  uint32_t ph = 0;
+  while (!it.done()) {
+    int t, p, kind;
+    it.next(nx, t, p, kind);
+    // depth: levels this item completes (lead item k of a run: k; a plane of
+    // the run: L, stored)
+    const int depth = (kind == kLead) ? L - (it.p - p) : L;
+    if (t != cur_tile) {
+      cur_tile = t;
+      tg = tile_geom(T, a.nvx, t);
+      vmask = 0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int l = lg + k * NL;
+        int jx = tg.r0 + (lab[k] >> 16), jy = tg.y0 + (lab[k] & 0xffff);
+        if (l < lines && jx < tg.r1 && jy < a.nvy) vmask |= 1u << k;
+        jx = min(jx, a.nvx - 1);
+        jy = min(jy, a.nvy - 1);
+        gxi[k] = a.gxo + jx;
+        gyi[k] = a.gyo + jy;
+        goff[k] = (jx * a.nvy + jy) * a.nvz + tg.z0 + zpos<V, LZ>(lz, 0);
+        cvx[k] = SCX[jx];
+      }
+      zmask = 0;
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+        if (tg.z0 + zpos<V, LZ>(lz, v) < a.nvz) zmask |= 1u << v;
+      full = (vmask == (1u << K) - 1) && (zmask == (1u << V) - 1);
+    }
+    const int i = item_plane(nx, a.bc, tg, p);
+    const double* SF = reinterpret_cast<const double*>(smem + (size_t)stg * stage_bytes);
+    mbar_wait(&bars[stg], ph);
+
+    if (i < 0) {
+      // absorbing ghost plane: zero flux at every level
+#pragma unroll
+      for (int l = 0; l < L; ++l)
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+#pragma unroll
+          for (int v = 0; v < V; ++v) prev[l][k][v] = 0.0;
+    } else {
+      double* gdst = (depth == L) ? a.fout + (size_t)i * a.plane : nullptr;
+      // per level: relax factors and this lane's g_z values of the plane's row
+      double rr[L], lss[L], gz[L][V];
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        const double* ST = reinterpret_cast<const double*>(
+            reinterpret_cast<const unsigned char*>(SF) + box_bytes + l * tab_bytes);
+        rr[l] = ST[0];
+        lss[l] = ST[1];
+        if (zmask == (1u << V) - 1) {
+          lds_lane<V, LZ>(ST + a.gzo + tg.z0 + zpos<V, LZ>(lz, 0), gz[l]);
+        } else {
+#pragma unroll
+          for (int v = 0; v < V; ++v)
+            gz[l][v] = ((zmask >> v) & 1u) ? ST[a.gzo + tg.z0 + zpos<V, LZ>(lz, v)] : 0.0;
+        }
+      }
+      auto body = [&](auto fast_c, auto down_c) {
+        constexpr bool FAST = decltype(fast_c)::value;
+        constexpr bool DOWNT = decltype(down_c)::value;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const double c = cvx[k];
+          double x[V];
+#pragma unroll
+          for (int l = 0; l < L; ++l) {
+            if (!FAST && l > depth) break;
+            const double* ST = reinterpret_cast<const double*>(
+                reinterpret_cast<const unsigned char*>(SF) + box_bytes + l * tab_bytes);
+            const double gxy = ST[gxi[k]] * ST[gyi[k]];
+            // relax R of this level (level 0 of a synthesising pass: f_0 = L(U))
+            if (l == 0 && SYNTH) {
+#pragma unroll
+              for (int v = 0; v < V; ++v) x[v] = (gxy * gz[0][v]) * lss[0];
+            } else {
+              double raw[V];
+              if (l == 0) {
+                lds_lane<V, LZ>(SF + soff[k], raw);
+              } else {
+#pragma unroll
+                for (int v = 0; v < V; ++v) raw[v] = x[v];
+              }
+              const double w = rr[l] * (lss[l] * gxy);
+#pragma unroll
+              for (int v = 0; v < V; ++v) x[v] = fma(w, gz[l][v], rr[l] * raw[v]);
+            }
+            double fl[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) fl[v] = __dmul_rn(c, x[v]);
+            if (FAST || l < depth) {
+              // upwind transport of ref/kinetic.py:110-112, the sweep's order
+              const double dtdx = a.dtdx[l];
+#pragma unroll
+              for (int v = 0; v < V; ++v) {
+                const double d = DOWNT ? __dsub_rn(prev[l][k][v], fl[v]) : __dsub_rn(fl[v], prev[l][k][v]);
+                x[v] = __dsub_rn(x[v], __dmul_rn(dtdx, d));
+              }
+            }
+#pragma unroll
+            for (int v = 0; v < V; ++v) prev[l][k][v] = fl[v];
+            if (FAST || depth == L) {
+              const bool ok = FAST || ((vmask >> k) & 1u);
+              double sl = 0.0;
+#pragma unroll
+              for (int v = 0; v < V; ++v) sl += (FAST || (ok && ((zmask >> v) & 1u))) ? x[v] : 0.0;
+              acc[l] += sl;
+              if (l == L - 1 && (FAST || ok)) store_line<V, LZ, FAST>(gdst + goff[k], x, zmask);
+            }
+          }
+        }
+      };
+      using T1 = std::integral_constant<bool, true>;
+      using F1 = std::integral_constant<bool, false>;
+      if (full && depth == L) {
+        if (tg.down) body(T1{}, T1{}); else body(T1{}, F1{});
+      } else {
+        if (tg.down) body(F1{}, T1{}); else body(F1{}, F1{});
+      }
+    }
+
+    __syncthreads();  // the stage is consumed: the producer may refill it
+    if (tid == ptid && !prod.done()) {
+      fence_proxy_async();
+      issue_next();
+    }
+    if (++stg == ns) {
+      stg = 0;
+      ph ^= 1u;
+    }
+  }
+#pragma unroll
+  for (int l = 0; l < L; ++l)
+    if (!isfinite(acc[l])) atomicMin(a.err, err_key(0, a.step0 + l, kErrNonFinite));
+}
+
+size_t fsweep_smem_bytes(const FSweepArgs& a, int V, int LZ, bool synth, int L, int ns) {
+  const int BZ = LZ * V;
+  const size_t box = synth ? 0 : (size_t)a.t.A * a.t.By * BZ * 8;
+  const size_t stage = (box + (size_t)L * a.TL * 8 + 127) & ~(size_t)127;
+  return (size_t)ns * stage + (size_t)((a.nvx + 1) & ~1) * 8 + (size_t)ns * 8 + 16;
+}
+
+template <int V, int LZ, int K, int NTHR, int MINB>
+static cudaError_t launch_f(const CUtensorMap& map, const FSweepArgs& a, bool synth, int L, int grid,
+                            int ns, size_t smem, cudaStream_t st) {
+  void (*fn)(const CUtensorMap, const FSweepArgs, int) = nullptr;
+  switch (L) {
+    case 1: fn = synth ? fsweep_kernel<V, LZ, K, NTHR, MINB, true, 1> : fsweep_kernel<V, LZ, K, NTHR, MINB, false, 1>; break;
+    case 2: fn = synth ? fsweep_kernel<V, LZ, K, NTHR, MINB, true, 2> : fsweep_kernel<V, LZ, K, NTHR, MINB, false, 2>; break;
+    case 3: fn = synth ? fsweep_kernel<V, LZ, K, NTHR, MINB, true, 3> : fsweep_kernel<V, LZ, K, NTHR, MINB, false, 3>; break;
+    default: return cudaErrorInvalidValue;
+  }
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(fn, grid, NTHR, smem, st, map, a, ns);
+}
+
+// Shapes: the TMA tile shapes of the upwind sweep (capi.cu kCfg ids).
+cudaError_t launch_fsweep(int cfg_id, const CUtensorMap& map, const FSweepArgs& a, bool synth, int L,
+                          int grid, int ns, size_t smem, cudaStream_t st) {
+  switch (cfg_id) {
+    case 0: return launch_f<2, 32, 4, 256, 2>(map, a, synth, L, grid, ns, smem, st);
+    case 2: return launch_f<2, 16, 4, 256, 2>(map, a, synth, L, grid, ns, smem, st);
+    case 3: return launch_f<2, 8, 4, 256, 2>(map, a, synth, L, grid, ns, smem, st);
+    case 4: return launch_f<2, 4, 4, 256, 2>(map, a, synth, L, grid, ns, smem, st);
+    case 11: return launch_f<6, 8, 2, 256, 2>(map, a, synth, L, grid, ns, smem, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+bool fsweep_has_cfg(int cfg_id) {
+  return cfg_id == 0 || cfg_id == 2 || cfg_id == 3 || cfg_id == 4 || cfg_id == 11;
+}
+
+}  // namespace pbgk

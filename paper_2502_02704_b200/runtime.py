@@ -13,6 +13,7 @@ the path runs in the kernels of libpbgk.so.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import threading
 
@@ -22,6 +23,9 @@ import torch
 from . import _lib
 from .errors import BlowUpError, CorrectionOvershootError, DegenerateStateError
 from .grid import bc_code
+
+# fine steps per pass of the multi-step path (the C default, pbgk_set_fusion)
+DEFAULT_FUSION = 2
 
 KIND_PROJECT, KIND_LIFT, KIND_NONFINITE, KIND_UNPHYSICAL, KIND_OVERSHOOT = range(5)
 
@@ -75,6 +79,26 @@ class Ctx:
         nv = self.shape[1:]
         self.dv = tuple(2.0 * self.v_max / ((n - 1) if q else n) for n in nv)
         self.quadrature = "trapezoid" if q else "midpoint"
+
+    def set_fusion(self, levels: int) -> None:
+        """Fine steps per pass over f on the multi-step path (include/pbgk.h
+        pbgk_set_fusion; 0 = always the one-step path)."""
+        _lib.check(self.lib.pbgk_set_fusion(self.h, int(levels)), "pbgk_set_fusion")
+        self.fusion = int(levels)
+
+    @contextlib.contextmanager
+    def fusion_levels(self, levels: int):
+        """Temporarily run this context with `levels` steps per pass."""
+        old = getattr(self, "fusion", None)
+        self.set_fusion(levels)
+        try:
+            yield self
+        finally:
+            if old is None:
+                self.lib.pbgk_set_fusion(self.h, DEFAULT_FUSION)
+                self.fusion = DEFAULT_FUSION
+            else:
+                self.set_fusion(old)
 
     def describe(self) -> str:
         buf = ctypes.create_string_buffer(1024)

@@ -1,0 +1,150 @@
+"""Multi-step path (fsweep.cu + marginal.cu, include/pbgk.h pbgk_set_fusion):
+windows from moments advanced L fine steps per pass over f, with the relax
+tables of every step from the 2-D marginal recursion.
+
+Parity: the oracle's F (ref/kinetic.py:137-161) from L(U) to 1e-12 on f_S and
+on the moments, the one-step path to 1e-13 (only the marginal summation order
+differs), every boundary, both quadratures, 1-3 levels and ragged pass counts;
+the status keys (step and kind of a failure) equal to the one-step path's."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import bgk as O
+from helpers import moment_gap, random_moments, rel_inf
+
+pytestmark = pytest.mark.gpu
+P = pytest.importorskip("paper_2502_02704_b200")
+from paper_2502_02704_b200 import runtime as rt  # noqa: E402
+from paper_2502_02704_b200.kinetic import _run_schedule, fine_schedule, stable_dt_kinetic  # noqa: E402
+
+# one per multi-step tile shape (nvz % 64, 48, 32, 16, 8) plus a generic shape
+# that falls back to the one-step path
+SHAPES = [
+    (12, (8, 8, 8), 8.0),
+    (10, (16, 16, 16), 8.0),
+    (9, (32, 32, 32), 8.0),
+    (7, (48, 48, 48), 10.0),
+    (5, (64, 64, 64), 8.0),
+    (10, (64, 8, 8), 6.0),
+    (8, (16, 8, 6), 5.0),
+]
+BCS = ["periodic", "absorbing", "outflow"]
+
+
+def _grids(nx, nv, vm, quad="midpoint"):
+    g = P.PhaseGrid(P.build_spatial_grid(0.0, 1.0, nx), P.build_velocity_grid(vm, nv, quadrature=quad))
+    return g, O.Mesh(0.0, 1.0, nx, vm, nv, quadrature=quad)
+
+
+def _window(g, bc, U, t1, levels, kp=None):
+    """f_S and P(f_S) of one window from moments U on `levels` steps per pass."""
+    kp = kp or P.KineticParams(1e-2)
+    ctx = rt.ctx_for(g, P.BoundaryKind(bc))
+    m0 = rt.to_device_moments(P.MomentField(*U), ctx.device)
+    dts = fine_schedule(t1, stable_dt_kinetic(g, kp))
+    out, mo = ctx.empty_f(), ctx.empty_moments()
+    with ctx.fusion_levels(levels):
+        code = _run_schedule(ctx, None, m0, dts, kp, out, want_f=True, mom_out=mo)
+    torch.cuda.synchronize()
+    return out.cpu().numpy(), mo.cpu().numpy(), code, len(dts)
+
+
+def _unpack(m):
+    return m[0], m[1:4].T, m[4]
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "x".join(map(str, (s[0],) + s[1])))
+@pytest.mark.parametrize("bc", BCS)
+@pytest.mark.parametrize("levels", [2, 3])
+def test_window_matches_oracle(shape, bc, levels):
+    nx, nv, vm = shape
+    g, mesh = _grids(nx, nv, vm)
+    U = random_moments(nx, np.random.default_rng(nx + len(bc)))
+    t1 = 6.5 * O.fine_cap(mesh, 0.5, None)  # 7 steps, the last one partial
+    f, m, code, S = _window(g, bc, U, t1, levels)
+    assert code == -1 and S == 7
+    want_f = O.fine_propagate(O.lift(*U, mesh), 0.0, t1, mesh, 1e-2, bc)
+    assert rel_inf(f, want_f) <= 1e-12
+    assert moment_gap(_unpack(m), O.project(want_f, mesh)) <= 1e-12
+
+
+@pytest.mark.parametrize("shape", SHAPES[:6], ids=lambda s: "x".join(map(str, (s[0],) + s[1])))
+@pytest.mark.parametrize("bc", BCS)
+def test_levels_agree_with_one_step_path(shape, bc):
+    nx, nv, vm = shape
+    g, mesh = _grids(nx, nv, vm)
+    U = random_moments(nx, np.random.default_rng(7 * nx))
+    t1 = 9.3 * O.fine_cap(mesh, 0.5, None)  # 10 steps: ragged passes for L = 3
+    f0, m0, c0, _ = _window(g, bc, U, t1, 0)
+    for L in (1, 2, 3):
+        f, m, c, _ = _window(g, bc, U, t1, L)
+        assert c == c0 == -1
+        assert rel_inf(f, f0) <= 1e-13
+        assert moment_gap(_unpack(m), _unpack(m0)) <= 1e-13
+
+
+@pytest.mark.parametrize("bc", BCS)
+@pytest.mark.parametrize("levels", [1, 2, 3])
+def test_trapezoid_matches_oracle(bc, levels):
+    g, mesh = _grids(9, (16, 16, 16), 8.0, quad="trapezoid")
+    U = random_moments(9, np.random.default_rng(3))
+    t1 = 4.5 * O.fine_cap(mesh, 0.5, None)
+    f, m, code, _ = _window(g, bc, U, t1, levels)
+    assert code == -1
+    want_f = O.fine_propagate(O.lift(*U, mesh), 0.0, t1, mesh, 1e-2, bc)
+    assert rel_inf(f, want_f) <= 1e-12
+    assert moment_gap(_unpack(m), O.project(want_f, mesh)) <= 1e-12
+
+
+@pytest.mark.parametrize("levels", [2, 3])
+def test_even_data_keeps_exact_zero_velocity(levels):
+    # x-homogeneous, velocity-even data: transport cancels exactly and every
+    # marginal stays mirror-symmetric, so u is exactly 0 (ref/moments.py:80-88)
+    nx = 6
+    g, _ = _grids(nx, (32, 32, 32), 8.0)
+    U = (np.full(nx, 1.3), np.zeros((nx, 3)), np.full(nx, 0.9))
+    t1 = 5.0 * stable_dt_kinetic(g, P.KineticParams(1e-2))
+    _, m, code, _ = _window(g, "periodic", U, t1, levels)
+    assert code == -1
+    assert np.all(m[1:4] == 0.0)
+
+
+@pytest.mark.parametrize("levels", [1, 2, 3])
+def test_failure_keys_equal_one_step_path(levels):
+    # a NaN density passes the reference's rho <= 0 test and surfaces as
+    # BlowUpError; a negative one as DegenerateStateError -- same step and
+    # kind on both paths
+    g, _ = _grids(8, (16, 16, 16), 8.0)
+    t1 = 4.5 * stable_dt_kinetic(g, P.KineticParams(1e-2))
+    for bad in (np.nan, -0.5):
+        rho, u, th = random_moments(8, np.random.default_rng(5))
+        rho[3] = bad
+        _, _, c0, _ = _window(g, "outflow", (rho, u, th), t1, 0)
+        _, _, c, _ = _window(g, "outflow", (rho, u, th), t1, levels)
+        assert c0 != -1
+        assert c == c0
+
+
+def test_parareal_equals_one_step_path():
+    # BASELINE config 0 parareal (outflow) on both paths: same iteration
+    # count, snapshots within 1e-12 (the oracle parity of this run is in
+    # test_gpu_configs.py, on the default multi-step path)
+    from dataclasses import replace
+    from paper_2502_02704_b200.configs import config
+    w = replace(config(0), outflow=True)
+    g = P.PhaseGrid(P.build_spatial_grid(w.x_min, w.x_max, w.nx), P.build_velocity_grid(w.v_max, w.nv))
+    bc = P.BoundaryKind(w.bc)
+    d = P.Discretization(g, P.build_time_grids(w.t_final, w.n_g, w.n_f), bc)
+    U0 = P.project(P.lift(P.MomentField(*w.raw_moments()), g, bc=bc), g, bc=bc)
+    cfg = P.PararealConfig(w.k_max, w.tol)
+    runs = []
+    for L in (0, 2, 3):
+        with rt.ctx_for(g, bc).fusion_levels(L):
+            runs.append(P.run_parareal(U0, cfg, d, P.KineticParams(w.eps), P.FluidParams()))
+    (t0, r0), *rest = runs
+    for t, r in rest:
+        assert len(r) == len(r0)
+        for a, b in zip(t.snapshots, t0.snapshots):
+            assert moment_gap((a.rho, a.u, a.theta), (b.rho, b.u, b.theta)) <= 1e-12
