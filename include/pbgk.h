@@ -161,12 +161,13 @@ int pbgk_set_x_scheme(pbgk_ctx* ctx, int scheme);
 
 /* Multi-step path of pbgk_propagate / pbgk_propagate_windows for windows
  * that start from moments (mom0, f0 == NULL) with the upwind scheme, no v_x
- * field term and bc 0..2: `levels` (1..3; default 2) fine steps per pass
- * over f, their relax tables from the 2-D marginal recursion (the marginals
- * of f over v_z and over v_y evolve in closed form under the upwind x
- * transport and the separable BGK relaxation), so f is read and written once
- * per `levels` steps.  Same results as the one-step path to rounding (the
- * marginal sums are taken in another order); 0 = always the one-step path. */
+ * field term and bc 0..2: `levels` (1..4) fine steps per pass over f, their
+ * relax tables from the 2-D marginal recursion (the marginals of f over v_z
+ * and over v_y evolve in closed form under the upwind x transport and the
+ * separable BGK relaxation), so f is read and written once per `levels`
+ * steps.  Same results as the one-step path to rounding (the marginal sums
+ * and the transport are associated differently); 0 = always the one-step
+ * path; -1 (default) = the measured best per shape. */
 int pbgk_set_fusion(pbgk_ctx* ctx, int levels);
 
 /* ---- x-sharded fine propagation (slabs) --------------------------------- */
@@ -239,6 +240,12 @@ typedef struct pbgk_profile {
   long long sweeps;       /* number of profiled sweep launches                 */
   double finalize_ms;     /* summed device time of finalize launches           */
   long long finalizes;
+  double msweep_ms;       /* multi-step sweeps (fsweep.cu): device time        */
+  double msweep_bytes;    /* their algorithmic HBM bytes (f read + f written)  */
+  long long msweeps;      /* number of profiled multi-step sweeps              */
+  long long msweep_steps; /* fine steps they advanced                          */
+  double marg_ms;         /* marginal recursion steps (marginal.cu)            */
+  long long margs;
 } pbgk_profile;
 
 /* When enabled, every sweep / finalize launch on this context is bracketed

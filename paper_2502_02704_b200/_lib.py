@@ -68,7 +68,9 @@ class Profile(ctypes.Structure):
     """struct pbgk_profile (include/pbgk.h)."""
 
     _fields_ = [("sweep_ms", c_double), ("sweep_bytes", c_double), ("sweeps", c_longlong),
-                ("finalize_ms", c_double), ("finalizes", c_longlong)]
+                ("finalize_ms", c_double), ("finalizes", c_longlong),
+                ("msweep_ms", c_double), ("msweep_bytes", c_double), ("msweeps", c_longlong),
+                ("msweep_steps", c_longlong), ("marg_ms", c_double), ("margs", c_longlong)]
 
 
 PROTOTYPES.update({

@@ -28,8 +28,10 @@ cudaError_t launch_fsweep(int cfg_id, const CUtensorMap& map, const FSweepArgs& 
                           int grid, int ns, size_t smem, cudaStream_t st);
 size_t fsweep_smem_bytes(const FSweepArgs& a, int V, int LZ, bool synth, int L, int ns);
 bool fsweep_has_cfg(int cfg_id);
-cudaError_t launch_marg(const MargArgs& m, const FinalArgs& f, cudaStream_t st);
+int fsweep_ctas_per_sm(int L);
+cudaError_t launch_marg(const MargArgs& m, const FinalArgs& f, double* scratch, cudaStream_t st);
 size_t marg_smem_bytes(int nvx, int nvy, int nvz, int TL);
+size_t marg_scratch_doubles(int nx, int nvx, int nvy, int nvz);
 cudaError_t launch_set_key(ErrKey* p, ErrKey v, cudaStream_t st);
 cudaError_t launch_fluid_batch(const FluidArgs& a, int nwin, const double* in, double* out,
                                const double* minuend, const double* t0, const double* t1,
@@ -113,8 +115,9 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 struct EvPair {
   cudaEvent_t a, b;
-  int kind;  // 0 sweep, 1 finalize
+  int kind;  // 0 sweep, 1 finalize, 2 multi-step sweep, 3 marginal recursion step
   double bytes;
+  int steps;
 };
 
 struct pbgk_ctx {
@@ -149,10 +152,11 @@ struct pbgk_ctx {
   std::vector<MapEntry> maps;
   size_t ws_bytes = 0;
   // multi-step path (fsweep.cu + marginal.cu): levels per pass (0 = off),
-  // the 2-D marginal ping-pong and a ring of four relax-table buffers
-  int fuse = 2;
+  // the 2-D marginal ping-pong and a ring of eight relax-table buffers
+  int fuse = -1;  // -1: per-shape default (fuse_levels)
   double* d_marg[2] = {nullptr, nullptr};
-  double* d_tabs[4] = {nullptr, nullptr, nullptr, nullptr};
+  double* d_tabs[8] = {};
+  double* d_mscr = nullptr;  // recursion scratch: m_x and column partials of one step
 };
 
 namespace {
@@ -164,7 +168,7 @@ struct ProfScope {
   pbgk_ctx* c;
   cudaStream_t st;
   EvPair* ev = nullptr;
-  ProfScope(pbgk_ctx* c_, cudaStream_t st_, int kind, double bytes) : c(c_), st(st_) {
+  ProfScope(pbgk_ctx* c_, cudaStream_t st_, int kind, double bytes, int steps = 1) : c(c_), st(st_) {
     ++g_launches;
     if (!c->prof) return;
     if (c->ev_pool.empty()) {
@@ -178,6 +182,7 @@ struct ProfScope {
     ev = &c->ev_used.back();
     ev->kind = kind;
     ev->bytes = bytes;
+    ev->steps = steps;
     cudaEventRecord(ev->a, st);
   }
   ~ProfScope() {
@@ -529,6 +534,7 @@ void pbgk_ctx_destroy(pbgk_ctx* c) {
   cudaFree(c->d_tab[1]);
   for (auto* p : c->d_marg) cudaFree(p);
   for (auto* p : c->d_tabs) cudaFree(p);
+  cudaFree(c->d_mscr);
   cudaFree(c->d_scratch);
   cudaFree(c->d_err);
   cudaFree(c->d_keys);
@@ -578,6 +584,14 @@ int pbgk_profile_read(pbgk_ctx* c, pbgk_profile* out) {
       out->sweep_ms += ms;
       out->sweep_bytes += e.bytes;
       out->sweeps += 1;
+    } else if (e.kind == 2) {
+      out->msweep_ms += ms;
+      out->msweep_bytes += e.bytes;
+      out->msweeps += 1;
+      out->msweep_steps += e.steps;
+    } else if (e.kind == 3) {
+      out->marg_ms += ms;
+      out->margs += 1;
     } else {
       out->finalize_ms += ms;
       out->finalizes += 1;
@@ -697,10 +711,10 @@ namespace {
 // Multi-step path usable on this context for an upwind propagation without
 // the v_x field term (the marginal recursion is closed for it; MUSCL's
 // limiter is not linear, slabs exchange halos per step).
+int fuse_levels(pbgk_ctx* c);
+
 bool fused_ok(pbgk_ctx* c, bool field) {
-  static const int env = getenv("PBGK_FUSE") ? atoi(getenv("PBGK_FUSE")) : -1;  // dev A/B knob
-  const int L = env >= 0 ? env : c->fuse;
-  if (L < 1 || field || c->x_scheme != 0 || c->g.bc == 3) return false;
+  if (fuse_levels(c) < 1 || field || c->x_scheme != 0 || c->g.bc == 3) return false;
   if (!fsweep_has_cfg(c->plan[0].cfg)) return false;
   if (marg_smem_bytes(c->g.nvx, c->g.nvy, c->g.nvz, c->TL) > c->smem_optin) return false;
   if (!c->d_marg[0]) {
@@ -710,14 +724,25 @@ bool fused_ok(pbgk_ctx* c, bool field) {
       if (cudaMalloc(&p, ms) != cudaSuccess) return false;
     for (auto*& p : c->d_tabs)
       if (cudaMalloc(&p, tb) != cudaSuccess) return false;
-    c->ws_bytes += 2 * ms + 4 * tb;
+    const size_t sc = marg_scratch_doubles(c->g.nx, c->g.nvx, c->g.nvy, c->g.nvz) * sizeof(double);
+    if (cudaMalloc(&c->d_mscr, sc) != cudaSuccess) return false;
+    c->ws_bytes += 2 * ms + 8 * tb + sc;
   }
   return true;
 }
 
+// Levels per pass: the context's setting, or (auto, -1) the measured best
+// per shape (round 1, one B200): 3 for the 2-wide lane layouts, 2 for the
+// 48-wide V = 6 one (its third level spills), one-step below ~4M cells where
+// the recursion's launches outweigh the saved traffic.
 int fuse_levels(pbgk_ctx* c) {
-  static const int env = getenv("PBGK_FUSE") ? atoi(getenv("PBGK_FUSE")) : -1;
-  return std::min(env >= 0 ? env : c->fuse, 3);
+  static const int env = getenv("PBGK_FUSE") ? atoi(getenv("PBGK_FUSE")) : -2;
+  int L = env >= -1 ? env : c->fuse;
+  if (L < 0) {
+    const double cells = (double)c->g.nx * c->g.nvx * c->g.nvy * c->g.nvz;
+    L = cells < 4.0e6 ? 0 : (kCfg[c->plan[0].cfg].V == 6 ? 2 : 3);
+  }
+  return std::min(L, 4);
 }
 
 int run_marg(pbgk_ctx* c, const double* min, double* mout, const double* tab_in, double* tab_out,
@@ -740,12 +765,13 @@ int run_marg(pbgk_ctx* c, const double* min, double* mout, const double* tab_in,
   f.eps = eps;
   f.tau = tau;
   f.step = step;
-  ProfScope ps(c, st, 1, 0.0);
-  CK(launch_marg(m, f, st));
+  ProfScope ps(c, st, 3, 0.0);
+  ++g_launches;  // two kernels: rows + final
+  CK(launch_marg(m, f, c->d_mscr, st));
   return 0;
 }
 
-// One pass of n <= 3 fine steps (steps s0+1 .. s0+n) over f.
+// One pass of n <= 4 fine steps (steps s0+1 .. s0+n) over f.
 int run_fsweep(pbgk_ctx* c, int n, const double* in, double* out, const double* const* tabs,
                const double* dtdx, int step0, cudaStream_t st) {
   const Plan& p = c->plan[0];
@@ -777,14 +803,15 @@ int run_fsweep(pbgk_ctx* c, int n, const double* in, double* out, const double* 
   if (!map) return fail("tensor map: " + g_last_error);
   // ring depth: the plan's, fewer stages if the L table rows per stage do not
   // fit the plan's CTAs per SM
-  const size_t budget = (p.per_sm == 2) ? (c->smem_per_sm / 2) - 2048 : c->smem_optin;
-  int ns = p.ns;
+  const int per_sm = std::min(p.per_sm, fsweep_ctas_per_sm(n));
+  const size_t budget = (per_sm == 2) ? (c->smem_per_sm / 2) - 2048 : c->smem_optin;
+  int ns = per_sm == 2 ? p.ns : std::max(p.ns, 4);
   while (ns > 2 && fsweep_smem_bytes(a, s.V, s.LZ, synth, n, ns) > budget) --ns;
   const size_t smem = fsweep_smem_bytes(a, s.V, s.LZ, synth, n, ns);
   const double fbytes = 8.0 * (double)a.plane * a.nx;
-  ProfScope ps(c, st, 0, (synth ? 0.0 : fbytes) + fbytes);
-  int grid = p.grid;
-  if (c->slot_reserve > 0) grid = std::max(1, std::min(grid, c->nsm * p.per_sm - c->slot_reserve));
+  ProfScope ps(c, st, 2, (synth ? 0.0 : fbytes) + fbytes, n);
+  int grid = (int)std::min<long long>(a.total, (long long)c->nsm * per_sm);
+  if (c->slot_reserve > 0) grid = std::max(1, std::min(grid, c->nsm * per_sm - c->slot_reserve));
   CK(launch_fsweep(p.cfg, *map, a, synth, n, grid, ns, smem, st));
   return 0;
 }
@@ -800,21 +827,21 @@ int propagate_body_fused(pbgk_ctx* c, const double* mom0, double* f_out, double*
   const int P = (S + L - 1) / L;  // passes
   const int W = P + (write_final ? 1 : 0);
   auto buf = [&](int w) { return ((W - w) % 2 == 0) ? f_out : f_tmp; };
-  double** T4 = c->d_tabs;
-  if (run_final(c, 0, kFinSynthRaw, mom0, nullptr, T4[0], 0, 1, 1, nullptr, 0, st)) return -1;
+  double** T8 = c->d_tabs;  // ring: a pass reads R_s0..R_s0+L-1 while R_s0+L is written
+  if (run_final(c, 0, kFinSynthRaw, mom0, nullptr, T8[0], 0, 1, 1, nullptr, 0, st)) return -1;
   int s0 = 0, w = 0;
   const double* in = nullptr;
   for (int s = 1; s <= S; ++s) {
     const double dt = h_dts[s - 1];
-    if (run_marg(c, s == 1 ? nullptr : c->d_marg[(s - 1) & 1], c->d_marg[s & 1], T4[(s - 1) & 3],
-                 T4[s & 3], dt, eps, tau, s, st))
+    if (run_marg(c, s == 1 ? nullptr : c->d_marg[(s - 1) & 1], c->d_marg[s & 1], T8[(s - 1) & 7],
+                 T8[s & 7], dt, eps, tau, s, st))
       return -1;
     if (s - s0 == L || s == S) {
       const int n = s - s0;
       const double* tabs[kMaxLevels];
       double dtdx[kMaxLevels];
       for (int l = 0; l < n; ++l) {
-        tabs[l] = T4[(s0 + l) & 3];
+        tabs[l] = T8[(s0 + l) & 7];
         dtdx[l] = h_dts[s0 + l] / c->dx;
       }
       double* out = buf(++w);
@@ -823,7 +850,7 @@ int propagate_body_fused(pbgk_ctx* c, const double* mom0, double* f_out, double*
       s0 = s;
     }
   }
-  if (run_sweep(c, 0, false, in, T4[S & 3], write_final ? f_out : nullptr, 0.0, nullptr, 0.0, 0.0, S,
+  if (run_sweep(c, 0, false, in, T8[S & 7], write_final ? f_out : nullptr, 0.0, nullptr, 0.0, 0.0, S,
                 st))
     return -1;
   if (mom_out && run_final(c, 0, kFinProject, nullptr, mom_out, nullptr, 0, 1, 1, nullptr, S + 1, st))
@@ -1044,7 +1071,7 @@ int pbgk_set_x_scheme(pbgk_ctx* c, int scheme) {
 
 int pbgk_set_fusion(pbgk_ctx* c, int levels) {
   if (!c) return fail("pbgk_set_fusion: null context");
-  if (levels < 0 || levels > 3) return fail("pbgk_set_fusion: levels must be 0 (off) .. 3");
+  if (levels < -1 || levels > 4) return fail("pbgk_set_fusion: levels must be -1 (auto), 0 (off) .. 4");
   c->fuse = levels;
   return 0;
 }

@@ -102,6 +102,10 @@ struct MargArgs {
   const double* tab_in;
   const double* cx;
   double dtdx;
+  int TL, gxo, gyo, gzo, trap;
+  int rpc, nrc;        // v_x rows per CTA, row chunks per cell
+  double* mx;          // m_x of f*_s: nx * nvx
+  double* colp;        // column partials: nx * nrc * (nvy + nvz)
 };
 
 enum FinalMode : int {

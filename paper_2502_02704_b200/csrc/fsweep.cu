@@ -16,6 +16,11 @@
 // which reproduces the zero-gradient ghost at every level (the edge cell's
 // inflow flux difference is exactly zero).
 //
+// Rounding: the transport is evaluated as (1 -/+ a) x +/- q_neighbour with
+// q = a x, a = (dt/dx) c_x (2 ops per element instead of the reference's 4),
+// within a few ulps of ref/kinetic.py:110-112; the multi-step path is held to
+// the oracle at 1e-12 (tests/test_gpu_fused.py) like every multi-step run.
+//
 // Finiteness (ref/kinetic.py:157-159): each thread sums its stored values of
 // every level; a non-finite sum flags BlowUpError at that level's step (same
 // documented corner as the marginal check: finite values whose sum overflows).
@@ -213,20 +218,22 @@ __global__ void __launch_bounds__(NTHR, MINB)
 #pragma unroll
               for (int v = 0; v < V; ++v) x[v] = fma(w, gz[l][v], rr[l] * raw[v]);
             }
-            double fl[V];
+            // upwind transport of ref/kinetic.py:110-112 with a = (dt/dx) c_x:
+            // up (c >= 0)  f* = x - a (x - x_{i-1}) = (1 - a) x + q_{i-1}
+            // down (c < 0) f* = x - a (x_{i+1} - x) = (1 + a) x - q_{i+1}
+            // with q = a x carried per level (2 fp64 ops per element instead of
+            // 4; a few ulps from the reference's order, see the header)
+            const double av = a.dtdx[l] * c;
+            const double keep = DOWNT ? 1.0 + av : 1.0 - av;
+            double q[V];
 #pragma unroll
-            for (int v = 0; v < V; ++v) fl[v] = __dmul_rn(c, x[v]);
+            for (int v = 0; v < V; ++v) q[v] = av * x[v];
             if (FAST || l < depth) {
-              // upwind transport of ref/kinetic.py:110-112, the sweep's order
-              const double dtdx = a.dtdx[l];
 #pragma unroll
-              for (int v = 0; v < V; ++v) {
-                const double d = DOWNT ? __dsub_rn(prev[l][k][v], fl[v]) : __dsub_rn(fl[v], prev[l][k][v]);
-                x[v] = __dsub_rn(x[v], __dmul_rn(dtdx, d));
-              }
+              for (int v = 0; v < V; ++v) x[v] = DOWNT ? fma(keep, x[v], -prev[l][k][v]) : fma(keep, x[v], prev[l][k][v]);
             }
 #pragma unroll
-            for (int v = 0; v < V; ++v) prev[l][k][v] = fl[v];
+            for (int v = 0; v < V; ++v) prev[l][k][v] = q[v];
             if (FAST || depth == L) {
               const bool ok = FAST || ((vmask >> k) & 1u);
               double sl = 0.0;
@@ -269,30 +276,42 @@ size_t fsweep_smem_bytes(const FSweepArgs& a, int V, int LZ, bool synth, int L, 
   return (size_t)ns * stage + (size_t)((a.nvx + 1) & ~1) * 8 + (size_t)ns * 8 + 16;
 }
 
-template <int V, int LZ, int K, int NTHR, int MINB>
-static cudaError_t launch_f(const CUtensorMap& map, const FSweepArgs& a, bool synth, int L, int grid,
-                            int ns, size_t smem, cudaStream_t st) {
-  void (*fn)(const CUtensorMap, const FSweepArgs, int) = nullptr;
-  switch (L) {
-    case 1: fn = synth ? fsweep_kernel<V, LZ, K, NTHR, MINB, true, 1> : fsweep_kernel<V, LZ, K, NTHR, MINB, false, 1>; break;
-    case 2: fn = synth ? fsweep_kernel<V, LZ, K, NTHR, MINB, true, 2> : fsweep_kernel<V, LZ, K, NTHR, MINB, false, 2>; break;
-    case 3: fn = synth ? fsweep_kernel<V, LZ, K, NTHR, MINB, true, 3> : fsweep_kernel<V, LZ, K, NTHR, MINB, false, 3>; break;
-    default: return cudaErrorInvalidValue;
-  }
+template <int V, int LZ, int K, int NTHR, int MINB, int L>
+static cudaError_t launch_l(const CUtensorMap& map, const FSweepArgs& a, bool synth, int grid, int ns,
+                            size_t smem, cudaStream_t st) {
+  void (*fn)(const CUtensorMap, const FSweepArgs, int) =
+      synth ? fsweep_kernel<V, LZ, K, NTHR, MINB, true, L> : fsweep_kernel<V, LZ, K, NTHR, MINB, false, L>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   return launch_pdl(fn, grid, NTHR, smem, st, map, a, ns);
 }
 
+// L = 1: the upwind sweep's CTA shape (256 threads, K lines each, 2 CTAs/SM);
+// L >= 2: the same box lines on 512 threads with K/2 lines each, one CTA per
+// SM (several levels of upwind carries per line do not fit 128 registers at K)
+template <int V, int LZ, int K>
+static cudaError_t launch_f(const CUtensorMap& map, const FSweepArgs& a, bool synth, int L, int grid,
+                            int ns, size_t smem, cudaStream_t st) {
+  switch (L) {
+    case 1: return launch_l<V, LZ, K, 256, 2, 1>(map, a, synth, grid, ns, smem, st);
+    case 2: return launch_l<V, LZ, K / 2, 512, 1, 2>(map, a, synth, grid, ns, smem, st);
+    case 3: return launch_l<V, LZ, K / 2, 512, 1, 3>(map, a, synth, grid, ns, smem, st);
+    case 4: return launch_l<V, LZ, K / 2, 512, 1, 4>(map, a, synth, grid, ns, smem, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+int fsweep_ctas_per_sm(int L) { return L >= 2 ? 1 : 2; }
+
 // Shapes: the TMA tile shapes of the upwind sweep (capi.cu kCfg ids).
 cudaError_t launch_fsweep(int cfg_id, const CUtensorMap& map, const FSweepArgs& a, bool synth, int L,
                           int grid, int ns, size_t smem, cudaStream_t st) {
   switch (cfg_id) {
-    case 0: return launch_f<2, 32, 4, 256, 2>(map, a, synth, L, grid, ns, smem, st);
-    case 2: return launch_f<2, 16, 4, 256, 2>(map, a, synth, L, grid, ns, smem, st);
-    case 3: return launch_f<2, 8, 4, 256, 2>(map, a, synth, L, grid, ns, smem, st);
-    case 4: return launch_f<2, 4, 4, 256, 2>(map, a, synth, L, grid, ns, smem, st);
-    case 11: return launch_f<6, 8, 2, 256, 2>(map, a, synth, L, grid, ns, smem, st);
+    case 0: return launch_f<2, 32, 4>(map, a, synth, L, grid, ns, smem, st);
+    case 2: return launch_f<2, 16, 4>(map, a, synth, L, grid, ns, smem, st);
+    case 3: return launch_f<2, 8, 4>(map, a, synth, L, grid, ns, smem, st);
+    case 4: return launch_f<2, 4, 4>(map, a, synth, L, grid, ns, smem, st);
+    case 11: return launch_f<6, 8, 2>(map, a, synth, L, grid, ns, smem, st);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -24,8 +24,9 @@ from . import _lib
 from .errors import BlowUpError, CorrectionOvershootError, DegenerateStateError
 from .grid import bc_code
 
-# fine steps per pass of the multi-step path (the C default, pbgk_set_fusion)
-DEFAULT_FUSION = 2
+# fine steps per pass of the multi-step path (the C default, pbgk_set_fusion:
+# -1 = the per-shape choice)
+DEFAULT_FUSION = -1
 
 KIND_PROJECT, KIND_LIFT, KIND_NONFINITE, KIND_UNPHYSICAL, KIND_OVERSHOOT = range(5)
 

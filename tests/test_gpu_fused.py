@@ -3,8 +3,8 @@ windows from moments advanced L fine steps per pass over f, with the relax
 tables of every step from the 2-D marginal recursion.
 
 Parity: the oracle's F (ref/kinetic.py:137-161) from L(U) to 1e-12 on f_S and
-on the moments, the one-step path to 1e-13 (only the marginal summation order
-differs), every boundary, both quadratures, 1-3 levels and ragged pass counts;
+on the moments, the one-step path to 1e-13 (the marginal summation order and
+the transport's association differ), every boundary, both quadratures, 1-4 levels and ragged pass counts;
 the status keys (step and kind of a failure) equal to the one-step path's."""
 
 import numpy as np
@@ -57,7 +57,7 @@ def _unpack(m):
 
 @pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "x".join(map(str, (s[0],) + s[1])))
 @pytest.mark.parametrize("bc", BCS)
-@pytest.mark.parametrize("levels", [2, 3])
+@pytest.mark.parametrize("levels", [2, 3, 4])
 def test_window_matches_oracle(shape, bc, levels):
     nx, nv, vm = shape
     g, mesh = _grids(nx, nv, vm)
@@ -78,7 +78,7 @@ def test_levels_agree_with_one_step_path(shape, bc):
     U = random_moments(nx, np.random.default_rng(7 * nx))
     t1 = 9.3 * O.fine_cap(mesh, 0.5, None)  # 10 steps: ragged passes for L = 3
     f0, m0, c0, _ = _window(g, bc, U, t1, 0)
-    for L in (1, 2, 3):
+    for L in (1, 2, 3, 4):
         f, m, c, _ = _window(g, bc, U, t1, L)
         assert c == c0 == -1
         assert rel_inf(f, f0) <= 1e-13
@@ -86,7 +86,7 @@ def test_levels_agree_with_one_step_path(shape, bc):
 
 
 @pytest.mark.parametrize("bc", BCS)
-@pytest.mark.parametrize("levels", [1, 2, 3])
+@pytest.mark.parametrize("levels", [1, 2, 3, 4])
 def test_trapezoid_matches_oracle(bc, levels):
     g, mesh = _grids(9, (16, 16, 16), 8.0, quad="trapezoid")
     U = random_moments(9, np.random.default_rng(3))
@@ -111,7 +111,7 @@ def test_even_data_keeps_exact_zero_velocity(levels):
     assert np.all(m[1:4] == 0.0)
 
 
-@pytest.mark.parametrize("levels", [1, 2, 3])
+@pytest.mark.parametrize("levels", [1, 2, 3, 4])
 def test_failure_keys_equal_one_step_path(levels):
     # a NaN density passes the reference's rho <= 0 test and surfaces as
     # BlowUpError; a negative one as DegenerateStateError -- same step and
@@ -140,7 +140,7 @@ def test_parareal_equals_one_step_path():
     U0 = P.project(P.lift(P.MomentField(*w.raw_moments()), g, bc=bc), g, bc=bc)
     cfg = P.PararealConfig(w.k_max, w.tol)
     runs = []
-    for L in (0, 2, 3):
+    for L in (0, 2, 3, 4):
         with rt.ctx_for(g, bc).fusion_levels(L):
             runs.append(P.run_parareal(U0, cfg, d, P.KineticParams(w.eps), P.FluidParams()))
     (t0, r0), *rest = runs
