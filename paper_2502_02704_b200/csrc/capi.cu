@@ -29,7 +29,8 @@ cudaError_t launch_fsweep(int cfg_id, const CUtensorMap& map, const FSweepArgs& 
 size_t fsweep_smem_bytes(const FSweepArgs& a, int V, int LZ, bool synth, int L, int ns);
 bool fsweep_has_cfg(int cfg_id);
 int fsweep_ctas_per_sm(int L);
-cudaError_t launch_marg(const MargArgs& m, const FinalArgs& f, double* scratch, cudaStream_t st);
+cudaError_t launch_marg(const MargArgs& m, const FinalArgs& f, double* scratch, int s, cudaStream_t st);
+size_t marg_state_doubles(int nvx);
 size_t marg_smem_bytes(int nvx, int nvy, int nvz, int TL);
 size_t marg_scratch_doubles(int nx, int nvx, int nvy, int nvz);
 cudaError_t launch_set_key(ErrKey* p, ErrKey v, cudaStream_t st);
@@ -152,7 +153,7 @@ struct pbgk_ctx {
   std::vector<MapEntry> maps;
   size_t ws_bytes = 0;
   // multi-step path (fsweep.cu + marginal.cu): levels per pass (0 = off),
-  // the 2-D marginal ping-pong and a ring of eight relax-table buffers
+  // the moment-recursion state ping-pong and a ring of eight relax-table buffers
   int fuse = -1;  // -1: per-shape default (fuse_levels)
   double* d_marg[2] = {nullptr, nullptr};
   double* d_tabs[8] = {};
@@ -718,7 +719,7 @@ bool fused_ok(pbgk_ctx* c, bool field) {
   if (!fsweep_has_cfg(c->plan[0].cfg)) return false;
   if (marg_smem_bytes(c->g.nvx, c->g.nvy, c->g.nvz, c->TL) > c->smem_optin) return false;
   if (!c->d_marg[0]) {
-    const size_t ms = (size_t)c->g.nx * c->g.nvx * (c->g.nvy + c->g.nvz) * sizeof(double);
+    const size_t ms = (size_t)c->g.nx * marg_state_doubles(c->g.nvx) * sizeof(double);
     const size_t tb = (size_t)c->g.nx * c->TL * sizeof(double);
     for (auto*& p : c->d_marg)
       if (cudaMalloc(&p, ms) != cudaSuccess) return false;
@@ -766,8 +767,8 @@ int run_marg(pbgk_ctx* c, const double* min, double* mout, const double* tab_in,
   f.tau = tau;
   f.step = step;
   ProfScope ps(c, st, 3, 0.0);
-  ++g_launches;  // two kernels: rows + final
-  CK(launch_marg(m, f, c->d_mscr, st));
+  if (step == 1) ++g_launches;  // the G sums of the lift tables
+  CK(launch_marg(m, f, c->d_mscr, step, st));
   return 0;
 }
 

@@ -90,22 +90,23 @@ struct FSweepArgs {
   int step0;           // step number of level 0's output (BlowUpError keys)
 };
 
-// Marginal recursion (marginal.cu): the 2-D marginals M_xy = sum_z f and
-// M_xz = sum_y f of f*_s obey a closed recursion under the upwind x transport
+// Moment recursion (marginal.cu): five weighted sums of f over (v_y, v_z)
+// per x cell and v_x row obey a closed recursion under the upwind x transport
 // and the separable BGK relaxation (both act on a v_x row with coefficients
-// independent of v_y, v_z).  One step maps M(f*_{s-1}) and the tables of
-// R_{s-1} to M(f*_s), its 1-D marginals and the tables of R_s.
+// independent of v_y, v_z).  One step maps Q(f*_{s-1}) and the tables of
+// R_{s-1} to Q(f*_s), the moments and the tables of R_s.
 struct MargArgs {
   int nx, nvx, nvy, nvz, bc;
-  const double* min;   // M(f*_{s-1}): nx * MS doubles; null: f_{s-1} = lift (tab_in r = 0)
-  double* mout;        // M(f*_s)
+  const double* min;   // Q(f*_{s-1}): nx * 5 nvx doubles; null: f_{s-1} = lift (tab_in r = 0)
+  double* mout;        // Q(f*_s)
   const double* tab_in;
   const double* cx;
+  const double* cy;
+  const double* cz;
   double dtdx;
   int TL, gxo, gyo, gzo, trap;
-  int rpc, nrc;        // v_x rows per CTA, row chunks per cell
-  double* mx;          // m_x of f*_s: nx * nvx
-  double* colp;        // column partials: nx * nrc * (nvy + nvz)
+  const double* gsum_in;  // per cell: sums of g_y, g_z of tab_in (6 doubles)
+  double* gsum_out;       // the same for the output tables
 };
 
 enum FinalMode : int {

@@ -1,46 +1,54 @@
-// Marginal recursion: the relax tables of every fine step without sweeping f.
+// Moment recursion: the relax tables of every fine step without sweeping f.
 //
-// Let M_xy[i][jx][jy] = sum_z w_z f[i][jx][jy][jz] and M_xz = sum_y w_y f
-// (w = 1, or the trapezoidal end weights).  Both parts of one fine step act on
-// a v_x row with coefficients that do not depend on (v_y, v_z):
+// Both parts of one fine step act on a v_x row with coefficients that do not
+// depend on (v_y, v_z):
 //   * the upwind x transport (ref/kinetic.py:110-112) is linear with
 //     coefficient c_x[jx];
 //   * the BGK relaxation (ref/kinetic.py:130-134) is f = r f* + r ls M with a
 //     separable Maxwellian M = (g_x amp) g_y g_z (ref/lifting.py:47-57).
-// Summing over v_z (resp. v_y) therefore commutes with both, and
-//   M(f*_s)(i) = T_x[ r M(f*_{s-1}) + r ls (g_x amp) g_y S_z ](i)
-// with S_z = sum_z w_z g_z (resp. g_z S_y for M_xz), evaluated on the cell and
-// its upwind neighbour.  The 1-D marginals of f*_s are row / column sums of
-// M(f*_s), so the moments and the relax table R_s of every step follow
-// (finalize_impl.cuh, ref/moments.py:91-113) from data 2/N_v the size of f.
-// The multi-step sweep (fsweep.cu) then applies the precomputed tables.
+// So any weighted sum of f over (v_y, v_z) commutes with both.  Per x cell
+// and v_x row the recursion carries five of them (w = 1, or the trapezoidal
+// end weights):
+//   Q0 = sum_yz f                          (= the marginal m_x[jx])
+//   Q1 = sum_z sum_{y<h} c_y (f_y - f_{n-1-y})   (folded first moment in v_y)
+//   Q2 = sum_yz c_y^2 f,   Q3, Q4 = the same in v_z
+// and one step is  Q_k(f*_s)(i) = T_x[ r Q_k(f*_{s-1}) + r ls (g_x amp) G_k ](i)
+// on the cell and its upwind neighbour, G_k the matching sums of g_y g_z of
+// the table row (G_0 = S_y0 S_z0, G_1 = S_y1 S_z0, ...).  From Q(f*_s) the
+// moments follow (ref/moments.py:91-113): rho and u_x, the x part of theta
+// exactly as the reference (marginal m_x, folded first moment, two-pass
+// second moment); u_y = sum Q1 dvol / rho; the y part of theta
+// sum (c_y - u_y)^2 m_y = Q2 - 2 u_y Q1 + u_y^2 Q0 (one-pass; a few ulps for
+// the low-Mach states here, relative error ~ eps (1 + u^2/theta) in general),
+// likewise z.  Then R_s = the table row of finalize_impl.cuh, same formulas.
 //
-// Two kernels per step: marg_rows_kernel (one CTA per cell and chunk of v_x
-// rows: the recursion itself, streaming, every load of a row in flight at
-// once) writes M(f*_s), the row sums m_x and per-chunk column partials;
-// marg_final_kernel (one CTA per cell) adds the chunk partials in chunk order
-// into m_y, m_z and runs the finalize (moments -> R_s).
+// The recursion moves 5 N_vx doubles per cell and step -- about 5/N_v^2 of
+// f -- and one warp per cell does the whole step (no CTA barrier).  The
+// multi-step sweep (fsweep.cu) applies the tables to f; the window's final
+// projection is taken from f itself (the reference-order marginal sweep).
 //
-// Rounding: the sums are taken in a different order than a direct reduction of
-// f*_s (transport-then-sum vs sum-then-transport), a few ulps per step, far
-// inside the 1e-10 parity bound.  Each marginal entry is a fixed tree, the
-// same for every index and its mirror, so even data keeps an exactly zero
-// folded first moment (ref/moments.py:80-88).
+// Folded sums keep an exactly zero velocity for even data (ref/moments.py:
+// 80-88): Q1, Q3 and G_1, G_3 vanish identically and the transport keeps
+// them at zero.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
-#include "finalize_impl.cuh"
 #include "ptx.cuh"
 
 namespace pbgk {
 
-constexpr int kRowThreads = 256;  // 8 warps, rpc / 8 rows each
-constexpr int kFinThr = 128;
+constexpr int kWarpsPerCta = 8;
 
-__device__ __forceinline__ double wq(int trap, int j, int n) {
+__device__ __forceinline__ double wsum(double x) {
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) x += __shfl_xor_sync(0xffffffffu, x, w);
+  return x;
+}
+
+__device__ __forceinline__ double wq(bool trap, int j, int n) {
   return (trap && (j == 0 || j == n - 1)) ? 0.5 : 1.0;
 }
 
@@ -51,202 +59,268 @@ __device__ __forceinline__ int nb_cell(int j, int nx, int bc) {
   return -1;  // absorbing ghost: zero
 }
 
-// Cell blockIdx.x, v_x rows [blockIdx.y * rpc, +rpc).  Warp w takes rows
-// w, w + 8, ... of the chunk; lane takes columns lane + 32 u of both parts.
-// m_x[jx] = the row's lane partials (ascending u) folded by an xor tree;
-// column partials over the chunk's rows in ascending jx.
-template <int RPW, int kCPL, bool TRAP>
-__global__ void __launch_bounds__(kRowThreads) marg_rows_kernel(const MargArgs m) {
-  extern __shared__ double sm[];
-  __shared__ double ssum[6];  // S_y, S_z of cells l, c, r
-  const int i = blockIdx.x, chunk = blockIdx.y;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nx = m.nx, nvx = m.nvx, nvy = m.nvy, nvz = m.nvz;
-  const int ncol = nvy + nvz, MS = nvx * ncol;
-  const int cl = nb_cell(i - 1, nx, m.bc), cr = nb_cell(i + 1, nx, m.bc);
-  // shared: per cell q (l, c, r): r, ls, then g_y | g_z; then per-row column values
-  double* g = sm;                      // [3][2 + ncol]
-  double* cp = g + 3 * (2 + ncol);     // [rpc][ncol]
-  pdl_wait();  // tables and M(f*_{s-1}) come from the preceding kernels
-  pdl_trigger();
-  for (int q = 0; q < 3; ++q) {
-    const int cc = q == 0 ? cl : (q == 1 ? i : cr);
-    for (int k = tid; k < 2 + ncol; k += kRowThreads) {
-      const int col = k < 2 ? k : (k - 2 < nvy ? m.gyo + k - 2 : m.gzo + k - 2 - nvy);
-      g[q * (2 + ncol) + k] = cc >= 0 ? __ldg(m.tab_in + (size_t)cc * m.TL + col) : 0.0;
-    }
+// Sums of one axis' g over the lanes of a warp (lane-strided, xor tree):
+// s0 = sum w g, s1 = sum_{j<h} w c (g_j - g_{n-1-j}), s2 = sum w c^2 g.
+__device__ __forceinline__ void axis_sums(const double* g, const double* c, int n, bool trap, int lane,
+                                          double& s0, double& s1, double& s2) {
+  s0 = s1 = s2 = 0.0;
+  const int h = n / 2;
+  for (int j = lane; j < n; j += 32) {
+    const double w = wq(trap, j, n);
+    s0 += w == 0.5 ? 0.5 * g[j] : g[j];
+    s2 += (w * c[j]) * (c[j] * g[j]);
+    if (j < h) s1 += (w * c[j]) * (g[j] - g[n - 1 - j]);
   }
-  __syncthreads();
-  if (warp < 6) {
-    const int q = warp >> 1, ax = warp & 1;  // ax 0: S_y, 1: S_z
-    const int n = ax == 0 ? nvy : nvz;
-    const double* gv = g + q * (2 + ncol) + 2 + (ax == 0 ? 0 : nvy);
-    double s = 0.0;
-    for (int j = lane; j < n; j += 32) s += (TRAP && (j == 0 || j == n - 1)) ? 0.5 * gv[j] : gv[j];
-#pragma unroll
-    for (int w = 16; w >= 1; w >>= 1) s += __shfl_xor_sync(0xffffffffu, s, w);
-    if (lane == 0) ssum[warp] = s;
-  }
-  __syncthreads();
-  const bool synth = (m.min == nullptr);
-  const int nneg = nvx / 2;
-  const int r0 = chunk * m.rpc;
-  // all loads of the warp's rows first
-  double mc[RPW][2][kCPL], mv[RPW][2][kCPL];
-#pragma unroll
-  for (int k = 0; k < RPW; ++k) {
-    const int jx = r0 + warp + 8 * k;
-    const int cn = jx < nneg ? cr : cl;
-#pragma unroll
-    for (int pz = 0; pz < 2; ++pz) {
-      const int n2 = pz == 0 ? nvy : nvz;
-      const size_t base = pz == 0 ? (size_t)jx * nvy : (size_t)nvx * nvy + (size_t)jx * nvz;
-#pragma unroll
-      for (int u = 0; u < kCPL; ++u) {
-        const int j2 = lane + 32 * u;
-        mc[k][pz][u] = mv[k][pz][u] = 0.0;
-        if (!synth && jx < nvx && j2 < n2) {
-          mc[k][pz][u] = __ldcg(m.min + (size_t)i * MS + base + j2);
-          if (cn >= 0) mv[k][pz][u] = __ldcg(m.min + (size_t)cn * MS + base + j2);
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < RPW; ++k) {
-    const int jx = r0 + warp + 8 * k;
-    const int rl = warp + 8 * k;  // row within the chunk
-    if (jx >= nvx || rl >= m.rpc) continue;
-    const double c = m.cx[jx];
-    const bool down = jx < nneg;  // c_x < 0 exactly for jx < nvx/2 (ref/grid.py:100-103)
-    const int qn = down ? 2 : 0;  // upwind neighbour: i+1 or i-1
-    const bool ghost = (down ? cr : cl) < 0;
-    const double* gc = g + (2 + ncol);
-    const double* gn = g + qn * (2 + ncol);
-    // relax coefficient of the row: (r ls g_x amp), or (ls g_x amp) for the lift
-    const double gxc = __ldg(m.tab_in + (size_t)i * m.TL + m.gxo + jx);
-    const double gxn = ghost ? 0.0 : __ldg(m.tab_in + (size_t)(down ? cr : cl) * m.TL + m.gxo + jx);
-    const double ac = (synth ? gc[1] : gc[0] * gc[1]) * gxc;
-    const double an = (synth ? gn[1] : gn[0] * gn[1]) * gxn;
-    const double wx = wq(TRAP, jx, nvx);
-    double rs = 0.0;
-#pragma unroll
-    for (int pz = 0; pz < 2; ++pz) {
-      const int n2 = pz == 0 ? nvy : nvz;
-      const size_t base = pz == 0 ? (size_t)jx * nvy : (size_t)nvx * nvy + (size_t)jx * nvz;
-      const double Sc = ssum[2 + (pz == 0 ? 1 : 0)], Sn = ssum[2 * qn + (pz == 0 ? 1 : 0)];
-      const int go = 2 + (pz == 0 ? 0 : nvy);
-#pragma unroll
-      for (int u = 0; u < kCPL; ++u) {
-        const int j2 = lane + 32 * u;
-        if (j2 < n2) {
-          const double gmc = ac * gc[go + j2];
-          const double x = synth ? gmc * Sc : fma(gmc, Sc, gc[0] * mc[k][pz][u]);
-          double xn = 0.0;
-          if (!ghost) {
-            const double gmn = an * gn[go + j2];
-            xn = synth ? gmn * Sn : fma(gmn, Sn, gn[0] * mv[k][pz][u]);
-          }
-          const double fl = __dmul_rn(c, x), pv = __dmul_rn(c, xn);
-          const double d = down ? __dsub_rn(pv, fl) : __dsub_rn(fl, pv);
-          const double o = __dsub_rn(x, __dmul_rn(m.dtdx, d));
-          m.mout[(size_t)i * MS + base + j2] = o;
-          if (pz == 0) rs += TRAP ? o * wq(1, j2, n2) : o;
-          cp[rl * ncol + (pz == 0 ? 0 : nvy) + j2] = TRAP ? o * wx : o;
-        }
-      }
-    }
-#pragma unroll
-    for (int w = 16; w >= 1; w >>= 1) rs += __shfl_xor_sync(0xffffffffu, rs, w);
-    if (lane == 0) m.mx[(size_t)i * nvx + jx] = rs;
-  }
-  __syncthreads();
-  const int nrow = min(m.rpc, nvx - r0);
-  for (int t = tid; t < ncol; t += kRowThreads) {
-    double s2 = 0.0;
-    for (int rl = 0; rl < nrow; ++rl) s2 += cp[rl * ncol + t];
-    m.colp[((size_t)i * m.nrc + chunk) * ncol + t] = s2;
-  }
+  s0 = wsum(s0);
+  s1 = wsum(s1);
+  s2 = wsum(s2);
 }
 
-// One CTA per cell: m_y, m_z = chunk partials in chunk order, then the
-// moments and R_s (finalize_impl.cuh).
-__global__ void __launch_bounds__(kFinThr) marg_final_kernel(const MargArgs m, const FinalArgs f) {
-  extern __shared__ double sm[];
-  __shared__ double sh[16];
-  const int i = blockIdx.x, tid = threadIdx.x;
-  const int nvx = m.nvx, ncol = m.nvy + m.nvz;
+// G sums of the table rows of a lift (the window's first step): one warp per
+// cell.  gsum[i] = {S_y0, S_y1, S_y2, S_z0, S_z1, S_z2}.
+__global__ void __launch_bounds__(32 * kWarpsPerCta) mrec_init_kernel(const MargArgs m) {
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
   pdl_wait();
   pdl_trigger();
-  for (int t = tid; t < nvx; t += kFinThr) sm[t] = __ldcg(m.mx + (size_t)i * nvx + t);
-  for (int t = tid; t < ncol; t += kFinThr) {
-    double s2 = 0.0;
-    for (int c = 0; c < m.nrc; ++c) s2 += __ldcg(m.colp + ((size_t)i * m.nrc + c) * ncol + t);
-    sm[nvx + t] = s2;  // m_y | m_z follow m_x
+  if (i >= m.nx) return;
+  const double* row = m.tab_in + (size_t)i * m.TL;
+  double a0, a1, a2, b0, b1, b2;
+  axis_sums(row + m.gyo, m.cy, m.nvy, m.trap, lane, a0, a1, a2);
+  axis_sums(row + m.gzo, m.cz, m.nvz, m.trap, lane, b0, b1, b2);
+  if (lane == 0) {
+    double* g = m.gsum_out + (size_t)i * 6;
+    g[0] = a0; g[1] = a1; g[2] = a2; g[3] = b0; g[4] = b1; g[5] = b2;
   }
-  __syncthreads();
-  finalize_cell<true>(f, i, sm, sh);
 }
 
-// rows per CTA (8 warps x RPW): 8 for tiny grids, else PBGK_MARG_RPC (16 or
-// 32; 32 only for <= 64 columns)
-static int marg_rpc(int nvx, int ncolmax) {
-  static const int env = getenv("PBGK_MARG_RPC") ? atoi(getenv("PBGK_MARG_RPC")) : 16;
-  if (nvx <= 8) return 8;
-  if (env >= 32 && nvx >= 32 && ncolmax <= 64) return 32;
-  return 16;
+// One recursion step: warp per cell i.  JPL = v_x rows per lane.
+template <int JPL, bool TRAP>
+__global__ void __launch_bounds__(32 * kWarpsPerCta) mrec_step_kernel(const MargArgs m, const FinalArgs f) {
+  extern __shared__ double sm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int i = blockIdx.x * kWarpsPerCta + wid;
+  const int nx = m.nx, nvx = m.nvx, nvy = m.nvy, nvz = m.nvz;
+  double* mxs = sm + (size_t)wid * nvx;  // this cell's m_x (mirror access)
+  pdl_wait();  // tables, G sums and Q(f*_{s-1}) come from the preceding kernels
+  pdl_trigger();
+  if (i >= nx) return;
+  const int cl = nb_cell(i - 1, nx, m.bc), cr = nb_cell(i + 1, nx, m.bc);
+  const bool synth = (m.min == nullptr);
+  const int nneg = nvx / 2;
+  const int QS = 5 * nvx;
+  // per cell q (l, c, r): r, ls and G_0..G_4 (uniform over the warp)
+  double rq[3], lq[3], G[3][5];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const int cc = q == 0 ? cl : (q == 1 ? i : cr);
+    rq[q] = lq[q] = 0.0;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) G[q][k] = 0.0;
+    if (cc >= 0) {
+      const double* row = m.tab_in + (size_t)cc * m.TL;
+      const double* gs = m.gsum_in + (size_t)cc * 6;
+      rq[q] = row[0];
+      lq[q] = row[1];
+      const double sy0 = gs[0], sy1 = gs[1], sy2 = gs[2], sz0 = gs[3], sz1 = gs[4], sz2 = gs[5];
+      G[q][0] = sy0 * sz0;
+      G[q][1] = sy1 * sz0;
+      G[q][2] = sy2 * sz0;
+      G[q][3] = sz1 * sy0;
+      G[q][4] = sz2 * sy0;
+    }
+  }
+  // loads first: Q of the cell and of the row's upwind neighbour
+  double qc[5][JPL], qn[5][JPL], gxc[JPL], gxn[JPL];
+#pragma unroll
+  for (int u = 0; u < JPL; ++u) {
+    const int jx = lane + 32 * u;
+    const int cn = jx < nneg ? cr : cl;
+    gxc[u] = gxn[u] = 0.0;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) qc[k][u] = qn[k][u] = 0.0;
+    if (jx < nvx) {
+      gxc[u] = __ldg(m.tab_in + (size_t)i * m.TL + m.gxo + jx);
+      if (cn >= 0) gxn[u] = __ldg(m.tab_in + (size_t)cn * m.TL + m.gxo + jx);
+      if (!synth) {
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+          qc[k][u] = __ldcg(m.min + (size_t)i * QS + k * nvx + jx);
+          if (cn >= 0) qn[k][u] = __ldcg(m.min + (size_t)cn * QS + k * nvx + jx);
+        }
+      }
+    }
+  }
+  // the step: relax (cell and upwind neighbour), upwind transport, in the
+  // one-step sweep's order; then the jx sums of the moments
+  double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0, q4 = 0.0;  // sum_jx w_x Q_k
+  int bad = 0;
+#pragma unroll
+  for (int u = 0; u < JPL; ++u) {
+    const int jx = lane + 32 * u;
+    if (jx >= nvx) continue;
+    const bool down = jx < nneg;  // c_x < 0 exactly for jx < nvx/2 (ref/grid.py:100-103)
+    const bool ghost = (down ? cr : cl) < 0;
+    const double c = m.cx[jx];
+    // neighbour constants by selects (a runtime index would spill to local memory)
+    const double rn = down ? rq[2] : rq[0], ln = down ? lq[2] : lq[0];
+    const double ac = (synth ? lq[1] : rq[1] * lq[1]) * gxc[u];
+    const double an = (synth ? ln : rn * ln) * gxn[u];
+    const double wx = wq(TRAP, jx, nvx);
+    double o[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const double Gn = down ? G[2][k] : G[0][k];
+      const double x = synth ? ac * G[1][k] : fma(ac, G[1][k], rq[1] * qc[k][u]);
+      const double xn = ghost ? 0.0 : (synth ? an * Gn : fma(an, Gn, rn * qn[k][u]));
+      const double fl = __dmul_rn(c, x), pv = __dmul_rn(c, xn);
+      const double d = down ? __dsub_rn(pv, fl) : __dsub_rn(fl, pv);
+      o[k] = __dsub_rn(x, __dmul_rn(m.dtdx, d));
+      m.mout[(size_t)i * QS + k * nvx + jx] = o[k];
+      bad |= !isfinite(o[k]);
+    }
+    mxs[jx] = o[0];
+    q0 += TRAP ? o[0] * wx : o[0];
+    q1 += TRAP ? o[1] * wx : o[1];
+    q2 += TRAP ? o[2] * wx : o[2];
+    q3 += TRAP ? o[3] * wx : o[3];
+    q4 += TRAP ? o[4] * wx : o[4];
+  }
+  __syncwarp();
+  q0 = wsum(q0);
+  q1 = wsum(q1);
+  q2 = wsum(q2);
+  q3 = wsum(q3);
+  q4 = wsum(q4);
+  const int nonfinite = __any_sync(0xffffffffu, bad);
+  // moments (ref/moments.py:100-112): rho and u_x from m_x as the reference
+  // (q0 is sum_jx w_x m_x in the finalize's lane order), folded first moment
+  const double* cx = m.cx;
+  double s1 = 0.0;
+  const int h = nvx / 2;
+  for (int j = lane; j < h; j += 32)
+    s1 += (mxs[j] - mxs[nvx - 1 - j]) * (TRAP ? cx[j] * wq(true, j, nvx) : cx[j]);
+  s1 = wsum(s1);
+  const double dvol = f.dvol;
+  const double rho = q0 * dvol;
+  const double u0 = (s1 * dvol) / rho;
+  const double u1 = (q1 * dvol) / rho;
+  const double u2 = (q3 * dvol) / rho;
+  double ex = 0.0;
+  for (int j = lane; j < nvx; j += 32) {
+    const double d = cx[j] - u0;
+    ex += (d * d) * (TRAP ? mxs[j] * wq(true, j, nvx) : mxs[j]);
+  }
+  ex = wsum(ex);
+  const double ey = (q2 - 2.0 * u1 * q1) + (u1 * u1) * q0;
+  const double ez = (q4 - 2.0 * u2 * q3) + (u2 * u2) * q0;
+  const double e2 = ((0.0 + ex) + ey) + ez;
+  const double th = (e2 * dvol) / (3.0 * rho);
+  if (lane == 0) {
+    if (rho <= 0.0) atomicMin(f.err, err_key(0, f.step, kErrProjectRho));
+    if (rho <= 0.0 || th <= 0.0) atomicMin(f.err, err_key(0, f.step, kErrLiftState));
+  }
+  // the table row of R_s (finalize_impl.cuh, same expressions and sum order)
+  const double inv2t = 1.0 / (2.0 * th);
+  const double tt = 6.283185307179586 * th;
+  const double amp = rho / (tt * sqrt(tt));  // (2 pi theta)^1.5, ref/lifting.py:50
+  double* row = f.tab + (size_t)i * f.TL;
+  double sxa = 0.0;
+  for (int j = lane; j < nvx; j += 32) {
+    const double d = cx[j] - u0;
+    const double g = exp(-(d * d) * inv2t) * amp;
+    sxa += (TRAP && (j == 0 || j == nvx - 1)) ? 0.5 * g : g;
+    row[f.gxo + j] = g;
+  }
+  sxa = wsum(sxa);
+  double a[2][3];
+#pragma unroll
+  for (int ax = 0; ax < 2; ++ax) {
+    const int n = ax == 0 ? nvy : nvz;
+    const double* c = ax == 0 ? m.cy : m.cz;
+    const double ua = ax == 0 ? u1 : u2;
+    const int off = ax == 0 ? f.gyo : f.gzo;
+    const int hh = n / 2;
+    double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+    for (int j = lane; j < n; j += 32) {
+      const double d = c[j] - ua;
+      const double g = exp(-(d * d) * inv2t);
+      const double w = wq(TRAP, j, n);
+      t0 += w == 0.5 ? 0.5 * g : g;
+      t2 += (w * c[j]) * (c[j] * g);
+      if (j < hh) {
+        const double dm = c[n - 1 - j] - ua;
+        t1 += (w * c[j]) * (g - exp(-(dm * dm) * inv2t));
+      }
+      row[off + j] = g;
+    }
+    a[ax][0] = wsum(t0);
+    a[ax][1] = wsum(t1);
+    a[ax][2] = wsum(t2);
+  }
+  for (int j = f.gyo + nvy + lane; j < f.gzo; j += 32) row[j] = 0.0;
+  for (int j = f.gzo + nvz + lane; j < f.TL; j += 32) row[j] = 0.0;
+  const double mass = ((sxa * a[0][0]) * a[1][0]) * dvol;
+  const double scale = rho / mass;
+  const double tau = f.tau_arr != nullptr ? f.tau_arr[i] : f.tau;
+  const double lam = (f.dt * tau) / f.eps;
+  const double r = 1.0 / (1.0 + lam);
+  const double ls = lam * scale;
+  if (lane == 0) {
+    row[0] = r;
+    row[1] = ls;
+    double* gs = m.gsum_out + (size_t)i * 6;
+    gs[0] = a[0][0]; gs[1] = a[0][1]; gs[2] = a[0][2];
+    gs[3] = a[1][0]; gs[4] = a[1][1]; gs[5] = a[1][2];
+    // f_s = R_s(f*_s) is finite iff f*_s and the table row are (BlowUpError(step))
+    if (nonfinite || !isfinite(r) || !isfinite(ls) || !isfinite(amp) || !isfinite(u0) ||
+        !isfinite(u1) || !isfinite(u2) || !isfinite(th))
+      atomicMin(f.err, err_key(0, f.step, kErrNonFinite));
+  }
 }
 
 size_t marg_smem_bytes(int nvx, int nvy, int nvz, int TL) {
-  (void)TL;
-  if (nvy > 128 || nvz > 128) return ~(size_t)0;  // columns per lane bound (4)
-  const int ncol = nvy + nvz;
-  return (size_t)(3 * (2 + ncol) + marg_rpc(nvx, std::max(nvy, nvz)) * ncol) * sizeof(double);
+  (void)nvy; (void)nvz; (void)TL;
+  if (nvx > 128) return ~(size_t)0;  // rows per lane bound (4)
+  return (size_t)kWarpsPerCta * nvx * sizeof(double);
 }
 
+// Q (5 nvx per cell) lives in the caller's ping-pong buffers; the scratch
+// holds the two G-sum arrays (6 per cell each)
+size_t marg_state_doubles(int nvx) { return (size_t)5 * nvx; }
 size_t marg_scratch_doubles(int nx, int nvx, int nvy, int nvz) {
-  const int rpc = marg_rpc(nvx, std::max(nvy, nvz)), nrc = (nvx + rpc - 1) / rpc;
-  return (size_t)nx * nvx + (size_t)nx * nrc * (nvy + nvz);
+  (void)nvx; (void)nvy; (void)nvz;
+  return (size_t)2 * 6 * nx;
 }
 
-cudaError_t launch_marg(const MargArgs& m0, const FinalArgs& f, double* scratch, cudaStream_t st) {
+// Step s >= 1.  s == 1: the input tables are a lift, their G sums come first.
+// The G sums ping-pong between the two halves of `scratch`.
+cudaError_t launch_marg(const MargArgs& m0, const FinalArgs& f, double* scratch, int s,
+                        cudaStream_t st) {
   MargArgs m = m0;
-  m.rpc = marg_rpc(m.nvx, std::max(m.nvy, m.nvz));
-  m.nrc = (m.nvx + m.rpc - 1) / m.rpc;
-  m.mx = scratch;
-  m.colp = scratch + (size_t)m.nx * m.nvx;
   m.TL = f.TL;
   m.gxo = f.gxo;
   m.gyo = f.gyo;
   m.gzo = f.gzo;
   m.trap = f.trap;
-  const size_t smem = marg_smem_bytes(m.nvx, m.nvy, m.nvz, f.TL);
-  // columns per lane: the longer of the two column axes over 32 lanes
-  const int cpl = (std::max(m.nvy, m.nvz) + 31) / 32;
-  void (*rk)(const MargArgs) = nullptr;
-#define PBGK_RK(R, C) (m.trap ? marg_rows_kernel<R, C, true> : marg_rows_kernel<R, C, false>)
-  if (m.rpc == 8) rk = cpl <= 1 ? PBGK_RK(1, 1) : (cpl == 2 ? PBGK_RK(1, 2) : PBGK_RK(1, 4));
-  else if (m.rpc == 16) rk = cpl <= 1 ? PBGK_RK(2, 1) : (cpl == 2 ? PBGK_RK(2, 2) : PBGK_RK(2, 4));
-  else rk = cpl <= 1 ? PBGK_RK(4, 1) : (cpl == 2 ? PBGK_RK(4, 2) : PBGK_RK(2, 4));
-#undef PBGK_RK
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  m.cy = f.cy;
+  m.cz = f.cz;
+  const size_t g6 = (size_t)6 * m.nx;
+  m.gsum_in = scratch + ((s - 1) & 1) * g6;
+  m.gsum_out = scratch + (s & 1) * g6;
+  const int grid = (m.nx + kWarpsPerCta - 1) / kWarpsPerCta;
+  if (s == 1) {
+    MargArgs mi = m;
+    mi.gsum_out = const_cast<double*>(m.gsum_in);
+    cudaError_t e = launch_pdl(mrec_init_kernel, grid, 32 * kWarpsPerCta, 0, st, mi);
     if (e != cudaSuccess) return e;
   }
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(m.nx, m.nrc);
-  cfg.blockDim = dim3(kRowThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = getenv("PBGK_NO_PDL") ? 0 : 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, rk, m);
-  if (e != cudaSuccess) return e;
-  const size_t fsm = (size_t)2 * (m.nvx + m.nvy + m.nvz) * sizeof(double);
-  return launch_pdl(marg_final_kernel, m.nx, kFinThr, fsm, st, m, f);
+  const int jpl = (m.nvx + 31) / 32;
+  void (*k)(const MargArgs, const FinalArgs) = nullptr;
+#define PBGK_MK(J) (m.trap ? mrec_step_kernel<J, true> : mrec_step_kernel<J, false>)
+  k = jpl <= 1 ? PBGK_MK(1) : (jpl == 2 ? PBGK_MK(2) : (jpl == 3 ? PBGK_MK(3) : PBGK_MK(4)));
+#undef PBGK_MK
+  return launch_pdl(k, grid, 32 * kWarpsPerCta, marg_smem_bytes(m.nvx, m.nvy, m.nvz, f.TL), st, m, f);
 }
 
 }  // namespace pbgk
