@@ -806,8 +806,12 @@ int run_fsweep(pbgk_ctx* c, int n, const double* in, double* out, const double* 
   // fit the plan's CTAs per SM
   const int per_sm = std::min(p.per_sm, fsweep_ctas_per_sm(n));
   const size_t budget = (per_sm == 2) ? (c->smem_per_sm / 2) - 2048 : c->smem_optin;
-  int ns = per_sm == 2 ? p.ns : std::max(p.ns, 4);
-  while (ns > 2 && fsweep_smem_bytes(a, s.V, s.LZ, synth, n, ns) > budget) --ns;
+  // (L >= 2 consumes two planes per round: at least 4 stages)
+  static const int pr = getenv("PBGK_FS_NS") ? atoi(getenv("PBGK_FS_NS")) : 6;  // dev knob
+  int ns = per_sm == 2 ? p.ns : std::max(p.ns, pr);
+  const int ns_min = per_sm == 2 ? 2 : 4;
+  while (ns > ns_min && fsweep_smem_bytes(a, s.V, s.LZ, synth, n, ns) > budget) --ns;
+  if (fsweep_smem_bytes(a, s.V, s.LZ, synth, n, ns) > budget) return fail("multi-step sweep: ring does not fit");
   const size_t smem = fsweep_smem_bytes(a, s.V, s.LZ, synth, n, ns);
   const double fbytes = 8.0 * (double)a.plane * a.nx;
   ProfScope ps(c, st, 2, (synth ? 0.0 : fbytes) + fbytes, n);

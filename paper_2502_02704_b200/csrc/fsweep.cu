@@ -40,6 +40,10 @@ __global__ void __launch_bounds__(NTHR, MINB)
     fsweep_kernel(const __grid_constant__ CUtensorMap fmap, const FSweepArgs a, int ns) {
   constexpr int NL = NTHR / LZ;
   constexpr int BZ = LZ * V;
+#ifndef PBGK_FS_PR
+#define PBGK_FS_PR 2
+#endif
+  constexpr int PR = PBGK_FS_PR;  // planes per round of the steady path (needs ns >= 2 PR)
   extern __shared__ __align__(128) unsigned char smem[];
 
   const Tiling& T = a.t;
@@ -113,7 +117,6 @@ __global__ void __launch_bounds__(NTHR, MINB)
   double cvx[K];
   unsigned vmask = 0, zmask = 0;
   bool full = false;
-  int cur_tile = -1;
   TileGeom tg{};
 
   double prev[L][K][V];
@@ -127,142 +130,155 @@ __global__ void __launch_bounds__(NTHR, MINB)
 #pragma unroll
   for (int l = 0; l < L; ++l) acc[l] = 0.0;
 
-  ItemIter<L, 0> it;
-  it.init(g0, g1, nx);
+  // consumer: the producer's item order (ItemIter<L, 0>), walked as runs of
+  // one tile: L lead items (depth 0..L-1, generic path), then the run's
+  // planes (depth L) on a lean path with no per-item bookkeeping beyond the
+  // stage ring
   int stg = 0;
   uint32_t ph = 0;
-  while (!it.done()) {
-    int t, p, kind;
-    it.next(nx, t, p, kind);
-    // depth: levels this item completes (lead item k of a run: k; a plane of
-    // the run: L, stored)
-    const int depth = (kind == kLead) ? L - (it.p - p) : L;
-    if (t != cur_tile) {
-      cur_tile = t;
-      tg = tile_geom(T, a.nvx, t);
-      vmask = 0;
+  int g = g0;
+  while (g < g1) {
+    const int t = g / nx;
+    const int p0 = g - t * nx;
+    const int p1 = min(nx, p0 + (g1 - g));
+    g += p1 - p0;
+    tg = tile_geom(T, a.nvx, t);
+    vmask = 0;
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const int l = lg + k * NL;
-        int jx = tg.r0 + (lab[k] >> 16), jy = tg.y0 + (lab[k] & 0xffff);
-        if (l < lines && jx < tg.r1 && jy < a.nvy) vmask |= 1u << k;
-        jx = min(jx, a.nvx - 1);
-        jy = min(jy, a.nvy - 1);
-        gxi[k] = a.gxo + jx;
-        gyi[k] = a.gyo + jy;
-        goff[k] = (jx * a.nvy + jy) * a.nvz + tg.z0 + zpos<V, LZ>(lz, 0);
-        cvx[k] = SCX[jx];
-      }
-      zmask = 0;
-#pragma unroll
-      for (int v = 0; v < V; ++v)
-        if (tg.z0 + zpos<V, LZ>(lz, v) < a.nvz) zmask |= 1u << v;
-      full = (vmask == (1u << K) - 1) && (zmask == (1u << V) - 1);
+    for (int k = 0; k < K; ++k) {
+      const int l = lg + k * NL;
+      int jx = tg.r0 + (lab[k] >> 16), jy = tg.y0 + (lab[k] & 0xffff);
+      if (l < lines && jx < tg.r1 && jy < a.nvy) vmask |= 1u << k;
+      jx = min(jx, a.nvx - 1);
+      jy = min(jy, a.nvy - 1);
+      gxi[k] = a.gxo + jx;
+      gyi[k] = a.gyo + jy;
+      goff[k] = (jx * a.nvy + jy) * a.nvz + tg.z0 + zpos<V, LZ>(lz, 0);
+      cvx[k] = SCX[jx];
     }
-    const int i = item_plane(nx, a.bc, tg, p);
-    const double* SF = reinterpret_cast<const double*>(smem + (size_t)stg * stage_bytes);
-    mbar_wait(&bars[stg], ph);
-
-    if (i < 0) {
-      // absorbing ghost plane: zero flux at every level
+    zmask = 0;
 #pragma unroll
-      for (int l = 0; l < L; ++l)
+    for (int v = 0; v < V; ++v)
+      if (tg.z0 + zpos<V, LZ>(lz, v) < a.nvz) zmask |= 1u << v;
+    full = (vmask == (1u << K) - 1) && (zmask == (1u << V) - 1);
+    // one item: plane i (-1 = absorbing ghost), `depth` levels completed;
+    // `sync`: end a round (CTA barrier, the producer refills the `nfree`
+    // stages the round consumed)
+    auto item = [&](int i, int depth, bool sync, int nfree) {
+      const double* SF = reinterpret_cast<const double*>(smem + (size_t)stg * stage_bytes);
+      mbar_wait(&bars[stg], ph);
+      if (i < 0) {
+        // absorbing ghost plane: zero flux at every level
 #pragma unroll
-        for (int k = 0; k < K; ++k)
+        for (int l = 0; l < L; ++l)
 #pragma unroll
-          for (int v = 0; v < V; ++v) prev[l][k][v] = 0.0;
-    } else {
-      double* gdst = (depth == L) ? a.fout + (size_t)i * a.plane : nullptr;
+          for (int k = 0; k < K; ++k)
+#pragma unroll
+            for (int v = 0; v < V; ++v) prev[l][k][v] = 0.0;
+      } else {
+        double* gdst = (depth == L) ? a.fout + (size_t)i * a.plane : nullptr;
       // per level: relax factors and this lane's g_z values of the plane's row
-      double rr[L], lss[L], gz[L][V];
+        double rr[L], lss[L], gz[L][V];
 #pragma unroll
-      for (int l = 0; l < L; ++l) {
-        const double* ST = reinterpret_cast<const double*>(
-            reinterpret_cast<const unsigned char*>(SF) + box_bytes + l * tab_bytes);
-        rr[l] = ST[0];
-        lss[l] = ST[1];
-        if (zmask == (1u << V) - 1) {
-          lds_lane<V, LZ>(ST + a.gzo + tg.z0 + zpos<V, LZ>(lz, 0), gz[l]);
-        } else {
+        for (int l = 0; l < L; ++l) {
+          const double* ST = reinterpret_cast<const double*>(
+              reinterpret_cast<const unsigned char*>(SF) + box_bytes + l * tab_bytes);
+          rr[l] = ST[0];
+          lss[l] = ST[1];
+          if (zmask == (1u << V) - 1) {
+            lds_lane<V, LZ>(ST + a.gzo + tg.z0 + zpos<V, LZ>(lz, 0), gz[l]);
+          } else {
 #pragma unroll
-          for (int v = 0; v < V; ++v)
-            gz[l][v] = ((zmask >> v) & 1u) ? ST[a.gzo + tg.z0 + zpos<V, LZ>(lz, v)] : 0.0;
-        }
-      }
-      auto body = [&](auto fast_c, auto down_c) {
-        constexpr bool FAST = decltype(fast_c)::value;
-        constexpr bool DOWNT = decltype(down_c)::value;
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          const double c = cvx[k];
-          double x[V];
-#pragma unroll
-          for (int l = 0; l < L; ++l) {
-            if (!FAST && l > depth) break;
-            const double* ST = reinterpret_cast<const double*>(
-                reinterpret_cast<const unsigned char*>(SF) + box_bytes + l * tab_bytes);
-            const double gxy = ST[gxi[k]] * ST[gyi[k]];
-            // relax R of this level (level 0 of a synthesising pass: f_0 = L(U))
-            if (l == 0 && SYNTH) {
-#pragma unroll
-              for (int v = 0; v < V; ++v) x[v] = (gxy * gz[0][v]) * lss[0];
-            } else {
-              double raw[V];
-              if (l == 0) {
-                lds_lane<V, LZ>(SF + soff[k], raw);
-              } else {
-#pragma unroll
-                for (int v = 0; v < V; ++v) raw[v] = x[v];
-              }
-              const double w = rr[l] * (lss[l] * gxy);
-#pragma unroll
-              for (int v = 0; v < V; ++v) x[v] = fma(w, gz[l][v], rr[l] * raw[v]);
-            }
-            // upwind transport of ref/kinetic.py:110-112 with a = (dt/dx) c_x:
-            // up (c >= 0)  f* = x - a (x - x_{i-1}) = (1 - a) x + q_{i-1}
-            // down (c < 0) f* = x - a (x_{i+1} - x) = (1 + a) x - q_{i+1}
-            // with q = a x carried per level (2 fp64 ops per element instead of
-            // 4; a few ulps from the reference's order, see the header)
-            const double av = a.dtdx[l] * c;
-            const double keep = DOWNT ? 1.0 + av : 1.0 - av;
-            double q[V];
-#pragma unroll
-            for (int v = 0; v < V; ++v) q[v] = av * x[v];
-            if (FAST || l < depth) {
-#pragma unroll
-              for (int v = 0; v < V; ++v) x[v] = DOWNT ? fma(keep, x[v], -prev[l][k][v]) : fma(keep, x[v], prev[l][k][v]);
-            }
-#pragma unroll
-            for (int v = 0; v < V; ++v) prev[l][k][v] = q[v];
-            if (FAST || depth == L) {
-              const bool ok = FAST || ((vmask >> k) & 1u);
-              double sl = 0.0;
-#pragma unroll
-              for (int v = 0; v < V; ++v) sl += (FAST || (ok && ((zmask >> v) & 1u))) ? x[v] : 0.0;
-              acc[l] += sl;
-              if (l == L - 1 && (FAST || ok)) store_line<V, LZ, FAST>(gdst + goff[k], x, zmask);
-            }
+            for (int v = 0; v < V; ++v)
+              gz[l][v] = ((zmask >> v) & 1u) ? ST[a.gzo + tg.z0 + zpos<V, LZ>(lz, v)] : 0.0;
           }
         }
-      };
-      using T1 = std::integral_constant<bool, true>;
-      using F1 = std::integral_constant<bool, false>;
-      if (full && depth == L) {
-        if (tg.down) body(T1{}, T1{}); else body(T1{}, F1{});
-      } else {
-        if (tg.down) body(F1{}, T1{}); else body(F1{}, F1{});
+        auto body = [&](auto fast_c, auto down_c) {
+          constexpr bool FAST = decltype(fast_c)::value;
+          constexpr bool DOWNT = decltype(down_c)::value;
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const double c = cvx[k];
+            double x[V];
+#pragma unroll
+            for (int l = 0; l < L; ++l) {
+              if (!FAST && l > depth) break;
+              const double* ST = reinterpret_cast<const double*>(
+                  reinterpret_cast<const unsigned char*>(SF) + box_bytes + l * tab_bytes);
+              const double gxy = ST[gxi[k]] * ST[gyi[k]];
+              // relax R of this level (level 0 of a synthesising pass: f_0 = L(U))
+              if (l == 0 && SYNTH) {
+#pragma unroll
+                for (int v = 0; v < V; ++v) x[v] = (gxy * gz[0][v]) * lss[0];
+              } else {
+                double raw[V];
+                if (l == 0) {
+                  lds_lane<V, LZ>(SF + soff[k], raw);
+                } else {
+#pragma unroll
+                  for (int v = 0; v < V; ++v) raw[v] = x[v];
+                }
+                const double w = rr[l] * (lss[l] * gxy);
+#pragma unroll
+                for (int v = 0; v < V; ++v) x[v] = fma(w, gz[l][v], rr[l] * raw[v]);
+              }
+              // upwind transport of ref/kinetic.py:110-112 with a = (dt/dx) c_x:
+              // up (c >= 0)  f* = x - a (x - x_{i-1}) = (1 - a) x + q_{i-1}
+              // down (c < 0) f* = x - a (x_{i+1} - x) = (1 + a) x - q_{i+1}
+              // with q = a x carried per level (2 fp64 ops per element instead of
+              // 4; a few ulps from the reference's order, see the header)
+              const double av = a.dtdx[l] * c;
+              const double keep = DOWNT ? 1.0 + av : 1.0 - av;
+              double q[V];
+#pragma unroll
+              for (int v = 0; v < V; ++v) q[v] = av * x[v];
+              if (FAST || l < depth) {
+#pragma unroll
+                for (int v = 0; v < V; ++v) x[v] = DOWNT ? fma(keep, x[v], -prev[l][k][v]) : fma(keep, x[v], prev[l][k][v]);
+              }
+#pragma unroll
+              for (int v = 0; v < V; ++v) prev[l][k][v] = q[v];
+              if (FAST || depth == L) {
+                const bool ok = FAST || ((vmask >> k) & 1u);
+                double sl = 0.0;
+#pragma unroll
+                for (int v = 0; v < V; ++v) sl += (FAST || (ok && ((zmask >> v) & 1u))) ? x[v] : 0.0;
+                acc[l] += sl;
+                if (l == L - 1 && (FAST || ok)) store_line<V, LZ, FAST>(gdst + goff[k], x, zmask);
+              }
+            }
+          }
+        };
+        using T1 = std::integral_constant<bool, true>;
+        using F1 = std::integral_constant<bool, false>;
+        if (full && depth == L) {
+          if (tg.down) body(T1{}, T1{}); else body(T1{}, F1{});
+        } else {
+          if (tg.down) body(F1{}, T1{}); else body(F1{}, F1{});
+        }
       }
+      if (sync) {
+        __syncthreads();  // the round's stages are consumed: the producer may refill them
+        if (tid == ptid) {
+          fence_proxy_async();
+          for (int q = 0; q < nfree && !prod.done(); ++q) issue_next();
+        }
+      }
+      if (++stg == ns) {
+        stg = 0;
+        ph ^= 1u;
+      }
+    };
+    for (int k = 0; k < L; ++k) item(item_plane(nx, a.bc, tg, p0 - L + k), k, true, 1);
+    // the run's planes PR per round (one barrier per round; the upwind carry
+    // goes from plane to plane in registers)
+    int p = p0;
+    for (; p + PR <= p1; p += PR) {
+#pragma unroll 1
+      for (int q = 0; q < PR - 1; ++q) item(tg.down ? nx - 1 - p - q : p + q, L, false, 0);
+      item(tg.down ? nx - PR - p : p + PR - 1, L, true, PR);
     }
-
-    __syncthreads();  // the stage is consumed: the producer may refill it
-    if (tid == ptid && !prod.done()) {
-      fence_proxy_async();
-      issue_next();
-    }
-    if (++stg == ns) {
-      stg = 0;
-      ph ^= 1u;
-    }
+    for (; p < p1; ++p) item(tg.down ? nx - 1 - p : p, L, true, 1);
   }
 #pragma unroll
   for (int l = 0; l < L; ++l)
