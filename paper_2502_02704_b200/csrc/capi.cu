@@ -31,6 +31,7 @@ bool fsweep_has_cfg(int cfg_id);
 int fsweep_ctas_per_sm(int L);
 cudaError_t launch_marg(const MargArgs& m, const FinalArgs& f, double* scratch, int s, cudaStream_t st);
 size_t marg_state_doubles(int nvx);
+cudaError_t launch_q_from_f(const MargArgs& m, const double* f, cudaStream_t st);
 size_t marg_smem_bytes(int nvx, int nvy, int nvz, int TL);
 size_t marg_scratch_doubles(int nx, int nvx, int nvy, int nvz);
 cudaError_t launch_set_key(ErrKey* p, ErrKey v, cudaStream_t st);
@@ -666,9 +667,9 @@ int pbgk_check_finite(pbgk_ctx* c, const double* f, int step, void* stream, long
 
 namespace {
 bool fused_ok(pbgk_ctx* c, bool field);
-int propagate_body_fused(pbgk_ctx* c, const double* mom0, double* f_out, double* f_tmp,
-                         int write_final, double* mom_out, int S, const double* h_dts, double eps,
-                         double tau, cudaStream_t st);
+int propagate_body_fused(pbgk_ctx* c, const double* f0, const double* mom0, double* f_out,
+                         double* f_tmp, int write_final, double* mom_out, int S, const double* h_dts,
+                         double eps, double tau, cudaStream_t st);
 
 // One propagation on the stream, failures atomicMin-ed into the current
 // error slot; no reset, no host synchronisation.
@@ -676,8 +677,9 @@ int propagate_body(pbgk_ctx* c, const double* f0, const double* mom0, double* f_
                    int write_final, double* mom_out, int S, const double* h_dts, double eps,
                    double tau, const double* E, double e_max, cudaStream_t st) {
   const bool field = (E != nullptr && e_max > 0.0);
-  if (!f0 && S > 0 && fused_ok(c, field))
-    return propagate_body_fused(c, mom0, f_out, f_tmp, write_final, mom_out, S, h_dts, eps, tau, st);
+  if (S > 0 && fused_ok(c, field))
+    return propagate_body_fused(c, f0, mom0, f_out, f_tmp, write_final, mom_out, S, h_dts, eps, tau,
+                                st);
   const int pid = field ? 1 : (c->x_scheme == 1 ? 2 : 0);
   const int W = S + (write_final ? 1 : 0);
   auto buf = [&](int w) { return ((W - w) % 2 == 0) ? f_out : f_tmp; };
@@ -825,21 +827,38 @@ int run_fsweep(pbgk_ctx* c, int n, const double* in, double* out, const double* 
 // marginal recursion produces R_1..R_S one step ahead of the passes; the
 // passes take up to L steps each; the last relax + projection is the
 // reference-order marginal sweep of f_S (P(f_S) comes from f itself).
-int propagate_body_fused(pbgk_ctx* c, const double* mom0, double* f_out, double* f_tmp,
-                         int write_final, double* mom_out, int S, const double* h_dts, double eps,
-                         double tau, cudaStream_t st) {
+int propagate_body_fused(pbgk_ctx* c, const double* f0, const double* mom0, double* f_out,
+                         double* f_tmp, int write_final, double* mom_out, int S, const double* h_dts,
+                         double eps, double tau, cudaStream_t st) {
   const int L = fuse_levels(c);
   const int P = (S + L - 1) / L;  // passes
   const int W = P + (write_final ? 1 : 0);
   auto buf = [&](int w) { return ((W - w) % 2 == 0) ? f_out : f_tmp; };
   double** T8 = c->d_tabs;  // ring: a pass reads R_s0..R_s0+L-1 while R_s0+L is written
-  if (run_final(c, 0, kFinSynthRaw, mom0, nullptr, T8[0], 0, 1, 1, nullptr, 0, st)) return -1;
+  // f_0: the lift of mom0 (synthesised by the first pass), or the given f0
+  // with identity tables (r = 1, ls = 0) and the recursion started from Q(f0)
+  if (f0) {
+    if (run_final(c, 0, kFinIdentity, nullptr, nullptr, T8[0], 0, 1, 1, nullptr, 0, st)) return -1;
+    MargArgs m{};
+    m.nx = c->g.nx;
+    m.nvx = c->g.nvx;
+    m.nvy = c->g.nvy;
+    m.nvz = c->g.nvz;
+    m.cy = c->d_c[1];
+    m.cz = c->d_c[2];
+    m.trap = c->quad;
+    m.mout = c->d_marg[0];
+    ++g_launches;
+    CK(launch_q_from_f(m, f0, st));
+  } else {
+    if (run_final(c, 0, kFinSynthRaw, mom0, nullptr, T8[0], 0, 1, 1, nullptr, 0, st)) return -1;
+  }
   int s0 = 0, w = 0;
-  const double* in = nullptr;
+  const double* in = f0;
   for (int s = 1; s <= S; ++s) {
     const double dt = h_dts[s - 1];
-    if (run_marg(c, s == 1 ? nullptr : c->d_marg[(s - 1) & 1], c->d_marg[s & 1], T8[(s - 1) & 7],
-                 T8[s & 7], dt, eps, tau, s, st))
+    const double* qin = (s == 1) ? (f0 ? c->d_marg[0] : nullptr) : c->d_marg[(s - 1) & 1];
+    if (run_marg(c, qin, c->d_marg[s & 1], T8[(s - 1) & 7], T8[s & 7], dt, eps, tau, s, st))
       return -1;
     if (s - s0 == L || s == S) {
       const int n = s - s0;

@@ -279,6 +279,58 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) mrec_step_kernel(const Marg
   }
 }
 
+// Q of a given distribution (the recursion's start for a window that begins
+// from f0): one warp per (cell, v_x row); lanes over v_z, sequential over v_y;
+// fixed trees, mirror-symmetric (folded sums are exactly 0 for even data).
+template <bool TRAP>
+__global__ void __launch_bounds__(32 * kWarpsPerCta) mrec_from_f_kernel(const MargArgs m, const double* f) {
+  const int lane = threadIdx.x & 31;
+  const long long w = (long long)blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
+  const int nvx = m.nvx, nvy = m.nvy, nvz = m.nvz;
+  pdl_wait();
+  pdl_trigger();
+  if (w >= (long long)m.nx * nvx) return;
+  const int i = (int)(w / nvx), jx = (int)(w - (long long)i * nvx);
+  const double* row = f + ((size_t)i * nvx + jx) * nvy * nvz;
+  const int hy = nvy / 2, hz = nvz / 2;
+  double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0, q4 = 0.0;
+  for (int jy = 0; jy < nvy; ++jy) {
+    const double wy = wq(TRAP, jy, nvy), cy = m.cy[jy];
+    const double* fy = row + (size_t)jy * nvz;
+    const double* fm = row + (size_t)(nvy - 1 - jy) * nvz;
+    for (int jz = lane; jz < nvz; jz += 32) {
+      const double wz = wq(TRAP, jz, nvz), cz = m.cz[jz];
+      const double v = fy[jz];
+      const double ww = wy * wz;
+      q0 += ww * v;
+      q2 += (ww * cy) * (cy * v);
+      q4 += (ww * cz) * (cz * v);
+      if (jy < hy) q1 += (ww * cy) * (v - fm[jz]);
+      if (jz < hz) q3 += (ww * cz) * (v - fy[nvz - 1 - jz]);
+    }
+  }
+  q0 = wsum(q0);
+  q1 = wsum(q1);
+  q2 = wsum(q2);
+  q3 = wsum(q3);
+  q4 = wsum(q4);
+  if (lane == 0) {
+    double* o = m.mout + (size_t)i * 5 * nvx;
+    o[jx] = q0;
+    o[nvx + jx] = q1;
+    o[2 * nvx + jx] = q2;
+    o[3 * nvx + jx] = q3;
+    o[4 * nvx + jx] = q4;
+  }
+}
+
+cudaError_t launch_q_from_f(const MargArgs& m, const double* f, cudaStream_t st) {
+  const long long warps = (long long)m.nx * m.nvx;
+  const int grid = (int)((warps + kWarpsPerCta - 1) / kWarpsPerCta);
+  auto k = m.trap ? mrec_from_f_kernel<true> : mrec_from_f_kernel<false>;
+  return launch_pdl(k, grid, 32 * kWarpsPerCta, 0, st, m, f);
+}
+
 size_t marg_smem_bytes(int nvx, int nvy, int nvz, int TL) {
   (void)nvy; (void)nvz; (void)TL;
   if (nvx > 128) return ~(size_t)0;  // rows per lane bound (4)

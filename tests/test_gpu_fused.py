@@ -148,3 +148,49 @@ def test_parareal_equals_one_step_path():
         assert len(r) == len(r0)
         for a, b in zip(t.snapshots, t0.snapshots):
             assert moment_gap((a.rho, a.u, a.theta), (b.rho, b.u, b.theta)) <= 1e-12
+
+
+def _from_f0(g, bc, f0, t1, levels):
+    """F over [0, t1] of a given f0 (propagate_kinetic's path) on `levels` steps per pass."""
+    kp = P.KineticParams(1e-2)
+    ctx = rt.ctx_for(g, P.BoundaryKind(bc))
+    fd = torch.from_numpy(np.ascontiguousarray(f0)).to(ctx.device)
+    dts = fine_schedule(t1, stable_dt_kinetic(g, kp))
+    out = ctx.empty_f()
+    with ctx.fusion_levels(levels):
+        code = _run_schedule(ctx, fd, None, dts, kp, out)
+    torch.cuda.synchronize()
+    return out.cpu().numpy(), code
+
+
+@pytest.mark.parametrize("shape", SHAPES[:6], ids=lambda s: "x".join(map(str, (s[0],) + s[1])))
+@pytest.mark.parametrize("bc", BCS)
+def test_given_f0_matches_oracle_and_one_step(shape, bc):
+    # propagate_kinetic from a non-Maxwellian f0: the recursion starts from the
+    # weighted sums of f0 itself (identity tables for step 0)
+    nx, nv, vm = shape
+    g, mesh = _grids(nx, nv, vm)
+    rng = np.random.default_rng(11 * nx)
+    f0 = O.lift(*random_moments(nx, rng), mesh) * rng.uniform(0.8, 1.2, (nx,) + nv)
+    t1 = 6.5 * O.fine_cap(mesh, 0.5, None)
+    want = O.fine_propagate(f0, 0.0, t1, mesh, 1e-2, bc)
+    one, c0 = _from_f0(g, bc, f0, t1, 0)
+    for L in (2, 3):
+        got, c = _from_f0(g, bc, f0, t1, L)
+        assert c == c0 == -1
+        assert rel_inf(got, want) <= 1e-12
+        assert rel_inf(got, one) <= 1e-13
+
+
+@pytest.mark.parametrize("levels", [2, 3])
+def test_given_f0_non_finite_reports_step_one(levels):
+    g, mesh = _grids(8, (16, 16, 16), 8.0)
+    f0 = O.lift(*random_moments(8, np.random.default_rng(2)), mesh)
+    f0[2, 3, 4, 5] = np.nan
+    t1 = 3.5 * O.fine_cap(mesh, 0.5, None)
+    _, c0 = _from_f0(g, "periodic", f0, t1, 0)
+    _, c = _from_f0(g, "periodic", f0, t1, levels)
+    assert c0 != -1 and c == c0
+    with pytest.raises(P.BlowUpError) as info:
+        rt.raise_kinetic(c)
+    assert info.value.step == 1
