@@ -29,7 +29,8 @@ cudaError_t launch_fsweep(int cfg_id, const CUtensorMap& map, const FSweepArgs& 
 size_t fsweep_smem_bytes(const FSweepArgs& a, int V, int LZ, bool synth, int L, int ns);
 bool fsweep_has_cfg(int cfg_id);
 int fsweep_ctas_per_sm(int L);
-cudaError_t launch_marg(const MargArgs& m, const FinalArgs& f, double* scratch, int s, cudaStream_t st);
+cudaError_t launch_marg(const MargArgs& m, const FinalArgs& f, double* gsum, int s, int nwin,
+                        cudaStream_t st);
 size_t marg_state_doubles(int nvx);
 cudaError_t launch_q_from_f(const MargArgs& m, const double* f, cudaStream_t st);
 size_t marg_smem_bytes(int nvx, int nvy, int nvz, int TL);
@@ -158,7 +159,15 @@ struct pbgk_ctx {
   int fuse = -1;  // -1: per-shape default (fuse_levels)
   double* d_marg[2] = {nullptr, nullptr};
   double* d_tabs[8] = {};
-  double* d_mscr = nullptr;  // recursion scratch: m_x and column partials of one step
+  double* d_mscr = nullptr;  // recursion scratch: the G sums of one window
+  // batched recursion of pbgk_propagate_windows: per-(window, step) tables,
+  // per-window state ping-pong, G sums, per-step dt and step counts
+  double* d_bt = nullptr;
+  double* d_bq = nullptr;
+  double* d_bg = nullptr;
+  double* d_bdts = nullptr;
+  int* d_bnst = nullptr;
+  size_t bt_cap = 0, bq_cap = 0, bg_cap = 0, bdts_cap = 0, bnst_cap = 0;
 };
 
 namespace {
@@ -537,6 +546,11 @@ void pbgk_ctx_destroy(pbgk_ctx* c) {
   for (auto* p : c->d_marg) cudaFree(p);
   for (auto* p : c->d_tabs) cudaFree(p);
   cudaFree(c->d_mscr);
+  cudaFree(c->d_bt);
+  cudaFree(c->d_bq);
+  cudaFree(c->d_bg);
+  cudaFree(c->d_bdts);
+  cudaFree(c->d_bnst);
   cudaFree(c->d_scratch);
   cudaFree(c->d_err);
   cudaFree(c->d_keys);
@@ -770,7 +784,7 @@ int run_marg(pbgk_ctx* c, const double* min, double* mout, const double* tab_in,
   f.step = step;
   ProfScope ps(c, st, 3, 0.0);
   if (step == 1) ++g_launches;  // the G sums of the lift tables
-  CK(launch_marg(m, f, c->d_mscr, step, st));
+  CK(launch_marg(m, f, c->d_mscr, step, 1, st));
   return 0;
 }
 
@@ -883,6 +897,143 @@ int propagate_body_fused(pbgk_ctx* c, const double* f0, const double* mom0, doub
 }
 }  // namespace
 
+}  // extern "C"
+
+namespace {
+template <typename T>
+int ensure_dev(T*& p, size_t& cap, size_t n, cudaStream_t st) {
+  if (n <= cap) return 0;
+  if (p) {
+    CK(cudaStreamSynchronize(st));
+    CK(cudaFree(p));
+    p = nullptr;
+    cap = 0;
+  }
+  CK(cudaMalloc(&p, n * sizeof(T)));
+  cap = n;
+  return 0;
+}
+
+// pbgk_propagate_windows on the multi-step path: the moment recursion of a
+// group of windows runs batched (one launch per step for the whole group,
+// grid.y = window), then each window's passes read its own per-step tables.
+// Groups bound the table memory (PBGK_BATCH_BYTES, default 2 GiB).
+int windows_fused(pbgk_ctx* c, int nwin, const double* mom_in, double* mom_out, double* f_a,
+                  double* f_b, const int* h_nsteps, const double* h_dts, double eps, double tau,
+                  cudaStream_t st) {
+  const int nx = c->g.nx;
+  const size_t m5 = (size_t)5 * nx;
+  const size_t tstep = (size_t)nx * c->TL;  // one table set
+  const size_t qw = (size_t)nx * marg_state_doubles(c->g.nvx);
+  int Smax = 0;
+  std::vector<size_t> off(nwin + 1, 0);
+  for (int w = 0; w < nwin; ++w) {
+    Smax = std::max(Smax, h_nsteps[w]);
+    off[w + 1] = off[w] + h_nsteps[w];
+  }
+  static const double budget = getenv("PBGK_BATCH_BYTES") ? atof(getenv("PBGK_BATCH_BYTES")) : 2147483648.0;
+  const double per_w = 8.0 * ((double)(Smax + 1) * tstep + 2.0 * qw + 12.0 * nx);
+  const int G = std::max(1, std::min(nwin, (int)(budget / per_w)));
+  const size_t t_ws = (size_t)(Smax + 1) * tstep;
+  if (ensure_dev(c->d_bt, c->bt_cap, (size_t)G * t_ws, st) ||
+      ensure_dev(c->d_bq, c->bq_cap, (size_t)2 * G * qw, st) ||
+      ensure_dev(c->d_bg, c->bg_cap, (size_t)G * 12 * nx, st) ||
+      ensure_dev(c->d_bdts, c->bdts_cap, (size_t)std::max(Smax, 1) * G, st) ||
+      ensure_dev(c->d_bnst, c->bnst_cap, (size_t)G, st))
+    return -1;
+  const int L = fuse_levels(c);
+  std::vector<double> hd((size_t)std::max(Smax, 1) * G);
+  std::vector<int> hn(G);
+  for (int w0 = 0; w0 < nwin; w0 += G) {
+    const int g = std::min(G, nwin - w0);
+    for (int k = 0; k < g; ++k) {
+      const int w = w0 + k;
+      hn[k] = h_nsteps[w];
+      for (int s = 0; s < Smax; ++s) hd[(size_t)s * g + k] = s < h_nsteps[w] ? h_dts[off[w] + s] : 0.0;
+    }
+    // pageable sources: the copies complete before the calls return
+    CK(cudaMemcpyAsync(c->d_bnst, hn.data(), g * sizeof(int), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(c->d_bdts, hd.data(), (size_t)std::max(Smax, 1) * g * sizeof(double),
+                       cudaMemcpyHostToDevice, st));
+    for (int k = 0; k < g; ++k) {
+      const int w = w0 + k;
+      if (h_nsteps[w] == 0) {  // empty window: the moments themselves
+        CK(cudaMemcpyAsync(mom_out + w * m5, mom_in + w * m5, m5 * sizeof(double),
+                           cudaMemcpyDeviceToDevice, st));
+        continue;
+      }
+      c->err_slot = c->d_keys + w;
+      const int rc = run_final(c, 0, kFinSynthRaw, mom_in + w * m5, nullptr, c->d_bt + k * t_ws, 0, 1,
+                               1, nullptr, 0, st);
+      c->err_slot = nullptr;
+      if (rc) return -1;
+    }
+    // the batched recursion: steps 1..Smax for the group's windows
+    for (int s = 1; s <= Smax; ++s) {
+      MargArgs mg{};
+      mg.nx = nx;
+      mg.nvx = c->g.nvx;
+      mg.nvy = c->g.nvy;
+      mg.nvz = c->g.nvz;
+      mg.bc = c->g.bc;
+      mg.min = s == 1 ? nullptr : c->d_bq + ((s - 1) & 1) * G * qw;
+      mg.mout = c->d_bq + (s & 1) * G * qw;
+      mg.tab_in = c->d_bt + (size_t)(s - 1) * tstep;
+      mg.cx = c->d_c[0];
+      mg.q_ws = (long long)qw;
+      mg.t_ws = (long long)t_ws;
+      mg.g_ws = 12LL * nx;
+      mg.dts = c->d_bdts + (size_t)(s - 1) * g;
+      mg.nst = c->d_bnst;
+      mg.errw = c->d_keys + w0;
+      mg.dx = c->dx;
+      FinalArgs f = fin_args(c, c->plan[0]);
+      f.mode = kFinRelax;
+      f.tab = c->d_bt + (size_t)s * tstep;
+      f.eps = eps;
+      f.tau = tau;
+      f.step = s;
+      ProfScope ps(c, st, 3, 0.0);
+      if (s == 1) ++g_launches;
+      CK(launch_marg(mg, f, c->d_bg, s, g, st));
+    }
+    // each window's passes and its final projection from f
+    for (int k = 0; k < g; ++k) {
+      const int w = w0 + k, S = h_nsteps[w];
+      if (S == 0) continue;
+      const double* T = c->d_bt + k * t_ws;
+      const int P = (S + L - 1) / L;
+      auto buf = [&](int i) { return ((P - i) % 2 == 0) ? f_a : f_b; };
+      c->err_slot = c->d_keys + w;
+      const double* in = nullptr;
+      int s0 = 0, wcount = 0;
+      while (s0 < S) {
+        const int n = std::min(L, S - s0);
+        const double* tabs[kMaxLevels];
+        double dtdx[kMaxLevels];
+        for (int l = 0; l < n; ++l) {
+          tabs[l] = T + (size_t)(s0 + l) * tstep;
+          dtdx[l] = h_dts[off[w] + s0 + l] / c->dx;
+        }
+        double* out = buf(++wcount);
+        if (run_fsweep(c, n, in, out, tabs, dtdx, s0 + 1, st)) { c->err_slot = nullptr; return -1; }
+        in = out;
+        s0 += n;
+      }
+      const int rc1 = run_sweep(c, 0, false, in, T + (size_t)S * tstep, nullptr, 0.0, nullptr, 0.0, 0.0,
+                                S, st);
+      const int rc2 = rc1 ? rc1 : run_final(c, 0, kFinProject, nullptr, mom_out + w * m5, nullptr, 0, 1, 1,
+                                           nullptr, S + 1, st);
+      c->err_slot = nullptr;
+      if (rc2) return -1;
+    }
+  }
+  return 0;
+}
+}  // namespace
+
+extern "C" {
+
 int pbgk_propagate(pbgk_ctx* c, const double* f0, const double* mom0, double* f_out, double* f_tmp,
                    int write_final, double* mom_out, int nsteps, const double* h_dts, double eps,
                    double tau, const double* E, double e_max, void* stream, long long* h_code) {
@@ -923,6 +1074,15 @@ int pbgk_propagate_windows(pbgk_ctx* c, int nwin, const double* mom_in, double* 
   }
   CK(cudaMemsetAsync(c->d_keys, 0xFF, (size_t)nwin * sizeof(ErrKey), st));  // kNoError = ~0
   const size_t m = (size_t)5 * c->g.nx;
+  const bool field = (E != nullptr && e_max > 0.0);
+  if (fused_ok(c, field)) {
+    if (windows_fused(c, nwin, mom_in, mom_out, f_a, f_b, h_nsteps, h_dts, eps, tau, st)) return -1;
+    CK(cudaMemcpyAsync(c->h_keys, c->d_keys, (size_t)nwin * sizeof(ErrKey), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int w = 0; w < nwin; ++w)
+      h_codes[w] = (c->h_keys[w] == kNoError) ? -1 : (long long)c->h_keys[w];
+    return 0;
+  }
   size_t off = 0;
   for (int w = 0; w < nwin; ++w) {
     const int S = h_nsteps[w];

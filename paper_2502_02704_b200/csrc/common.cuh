@@ -107,6 +107,14 @@ struct MargArgs {
   int TL, gxo, gyo, gzo, trap;
   const double* gsum_in;  // per cell: sums of g_y, g_z of tab_in (6 doubles)
   double* gsum_out;       // the same for the output tables
+  // batch of windows (grid.y = window): per-window strides (doubles) of the
+  // state, the tables and the G sums; per-window dt of this step, step counts
+  // and failure keys (null: a single window, dtdx / FinalArgs dt and err)
+  long long q_ws, t_ws, g_ws;
+  const double* dts;
+  const int* nst;
+  ErrKey* errw;
+  double dx;
 };
 
 enum FinalMode : int {
@@ -157,10 +165,10 @@ struct FluidArgs {
 // launching while the preceding kernel of the stream finishes; it must call
 // pdl_wait() (ptx.cuh) before consuming that kernel's results.
 template <typename... KArgs, typename... Args>
-static inline cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, size_t smem,
-                                     cudaStream_t st, Args&&... args) {
+static inline cudaError_t launch_pdl_grid(void (*kernel)(KArgs...), dim3 grid, int block, size_t smem,
+                                          cudaStream_t st, Args&&... args) {
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid);
+  cfg.gridDim = grid;
   cfg.blockDim = dim3(block);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
@@ -171,6 +179,12 @@ static inline cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int blo
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, size_t smem,
+                                     cudaStream_t st, Args&&... args) {
+  return launch_pdl_grid(kernel, dim3(grid), block, smem, st, std::forward<Args>(args)...);
 }
 
 }  // namespace pbgk

@@ -81,15 +81,16 @@ __device__ __forceinline__ void axis_sums(const double* g, const double* c, int 
 __global__ void __launch_bounds__(32 * kWarpsPerCta) mrec_init_kernel(const MargArgs m) {
   const int lane = threadIdx.x & 31;
   const int i = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
+  const int w = blockIdx.y;
   pdl_wait();
   pdl_trigger();
   if (i >= m.nx) return;
-  const double* row = m.tab_in + (size_t)i * m.TL;
+  const double* row = m.tab_in + w * m.t_ws + (size_t)i * m.TL;
   double a0, a1, a2, b0, b1, b2;
   axis_sums(row + m.gyo, m.cy, m.nvy, m.trap, lane, a0, a1, a2);
   axis_sums(row + m.gzo, m.cz, m.nvz, m.trap, lane, b0, b1, b2);
   if (lane == 0) {
-    double* g = m.gsum_out + (size_t)i * 6;
+    double* g = m.gsum_out + w * m.g_ws + (size_t)i * 6;
     g[0] = a0; g[1] = a1; g[2] = a2; g[3] = b0; g[4] = b1; g[5] = b2;
   }
 }
@@ -105,8 +106,20 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) mrec_step_kernel(const Marg
   pdl_wait();  // tables, G sums and Q(f*_{s-1}) come from the preceding kernels
   pdl_trigger();
   if (i >= nx) return;
+  // window of a batch (grid.y): its state, tables, G sums, dt and key
+  const int w = blockIdx.y;
+  if (m.nst != nullptr && f.step > m.nst[w]) return;  // this window has fewer steps
+  const double* qmin = m.min ? m.min + w * m.q_ws : nullptr;
+  double* qout = m.mout + w * m.q_ws;
+  const double* tab_in = m.tab_in + w * m.t_ws;
+  double* tab_out = f.tab + w * m.t_ws;
+  const double* gsum_in = m.gsum_in + w * m.g_ws;
+  double* gsum_out = m.gsum_out + w * m.g_ws;
+  const double dt = m.dts ? m.dts[w] : f.dt;
+  const double dtdx = m.dts ? dt / m.dx : m.dtdx;  // the host's dt / dx
+  ErrKey* err = m.errw ? m.errw + w : f.err;
   const int cl = nb_cell(i - 1, nx, m.bc), cr = nb_cell(i + 1, nx, m.bc);
-  const bool synth = (m.min == nullptr);
+  const bool synth = (qmin == nullptr);
   const int nneg = nvx / 2;
   const int QS = 5 * nvx;
   // per cell q (l, c, r): r, ls and G_0..G_4 (uniform over the warp)
@@ -118,8 +131,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) mrec_step_kernel(const Marg
 #pragma unroll
     for (int k = 0; k < 5; ++k) G[q][k] = 0.0;
     if (cc >= 0) {
-      const double* row = m.tab_in + (size_t)cc * m.TL;
-      const double* gs = m.gsum_in + (size_t)cc * 6;
+      const double* row = tab_in + (size_t)cc * m.TL;
+      const double* gs = gsum_in + (size_t)cc * 6;
       rq[q] = row[0];
       lq[q] = row[1];
       const double sy0 = gs[0], sy1 = gs[1], sy2 = gs[2], sz0 = gs[3], sz1 = gs[4], sz2 = gs[5];
@@ -140,13 +153,13 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) mrec_step_kernel(const Marg
 #pragma unroll
     for (int k = 0; k < 5; ++k) qc[k][u] = qn[k][u] = 0.0;
     if (jx < nvx) {
-      gxc[u] = __ldg(m.tab_in + (size_t)i * m.TL + m.gxo + jx);
-      if (cn >= 0) gxn[u] = __ldg(m.tab_in + (size_t)cn * m.TL + m.gxo + jx);
+      gxc[u] = __ldg(tab_in + (size_t)i * m.TL + m.gxo + jx);
+      if (cn >= 0) gxn[u] = __ldg(tab_in + (size_t)cn * m.TL + m.gxo + jx);
       if (!synth) {
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
-          qc[k][u] = __ldcg(m.min + (size_t)i * QS + k * nvx + jx);
-          if (cn >= 0) qn[k][u] = __ldcg(m.min + (size_t)cn * QS + k * nvx + jx);
+          qc[k][u] = __ldcg(qmin + (size_t)i * QS + k * nvx + jx);
+          if (cn >= 0) qn[k][u] = __ldcg(qmin + (size_t)cn * QS + k * nvx + jx);
         }
       }
     }
@@ -175,8 +188,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) mrec_step_kernel(const Marg
       const double xn = ghost ? 0.0 : (synth ? an * Gn : fma(an, Gn, rn * qn[k][u]));
       const double fl = __dmul_rn(c, x), pv = __dmul_rn(c, xn);
       const double d = down ? __dsub_rn(pv, fl) : __dsub_rn(fl, pv);
-      o[k] = __dsub_rn(x, __dmul_rn(m.dtdx, d));
-      m.mout[(size_t)i * QS + k * nvx + jx] = o[k];
+      o[k] = __dsub_rn(x, __dmul_rn(dtdx, d));
+      qout[(size_t)i * QS + k * nvx + jx] = o[k];
       bad |= !isfinite(o[k]);
     }
     mxs[jx] = o[0];
@@ -217,14 +230,14 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) mrec_step_kernel(const Marg
   const double e2 = ((0.0 + ex) + ey) + ez;
   const double th = (e2 * dvol) / (3.0 * rho);
   if (lane == 0) {
-    if (rho <= 0.0) atomicMin(f.err, err_key(0, f.step, kErrProjectRho));
-    if (rho <= 0.0 || th <= 0.0) atomicMin(f.err, err_key(0, f.step, kErrLiftState));
+    if (rho <= 0.0) atomicMin(err, err_key(0, f.step, kErrProjectRho));
+    if (rho <= 0.0 || th <= 0.0) atomicMin(err, err_key(0, f.step, kErrLiftState));
   }
   // the table row of R_s (finalize_impl.cuh, same expressions and sum order)
   const double inv2t = 1.0 / (2.0 * th);
   const double tt = 6.283185307179586 * th;
   const double amp = rho / (tt * sqrt(tt));  // (2 pi theta)^1.5, ref/lifting.py:50
-  double* row = f.tab + (size_t)i * f.TL;
+  double* row = tab_out + (size_t)i * f.TL;
   double sxa = 0.0;
   for (int j = lane; j < nvx; j += 32) {
     const double d = cx[j] - u0;
@@ -263,19 +276,19 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) mrec_step_kernel(const Marg
   const double mass = ((sxa * a[0][0]) * a[1][0]) * dvol;
   const double scale = rho / mass;
   const double tau = f.tau_arr != nullptr ? f.tau_arr[i] : f.tau;
-  const double lam = (f.dt * tau) / f.eps;
+  const double lam = (dt * tau) / f.eps;
   const double r = 1.0 / (1.0 + lam);
   const double ls = lam * scale;
   if (lane == 0) {
     row[0] = r;
     row[1] = ls;
-    double* gs = m.gsum_out + (size_t)i * 6;
+    double* gs = gsum_out + (size_t)i * 6;
     gs[0] = a[0][0]; gs[1] = a[0][1]; gs[2] = a[0][2];
     gs[3] = a[1][0]; gs[4] = a[1][1]; gs[5] = a[1][2];
     // f_s = R_s(f*_s) is finite iff f*_s and the table row are (BlowUpError(step))
     if (nonfinite || !isfinite(r) || !isfinite(ls) || !isfinite(amp) || !isfinite(u0) ||
         !isfinite(u1) || !isfinite(u2) || !isfinite(th))
-      atomicMin(f.err, err_key(0, f.step, kErrNonFinite));
+      atomicMin(err, err_key(0, f.step, kErrNonFinite));
   }
 }
 
@@ -345,9 +358,11 @@ size_t marg_scratch_doubles(int nx, int nvx, int nvy, int nvz) {
   return (size_t)2 * 6 * nx;
 }
 
-// Step s >= 1.  s == 1: the input tables are a lift, their G sums come first.
-// The G sums ping-pong between the two halves of `scratch`.
-cudaError_t launch_marg(const MargArgs& m0, const FinalArgs& f, double* scratch, int s,
+// Step s >= 1 for `nwin` windows (grid.y; the caller sets the per-window
+// strides, 0 for one window).  s == 1: the input tables are a lift or
+// identity rows, their G sums come first.  The G sums ping-pong between the
+// two halves (6 nx doubles each) of each window's `gsum` block (stride g_ws).
+cudaError_t launch_marg(const MargArgs& m0, const FinalArgs& f, double* gsum, int s, int nwin,
                         cudaStream_t st) {
   MargArgs m = m0;
   m.TL = f.TL;
@@ -358,13 +373,13 @@ cudaError_t launch_marg(const MargArgs& m0, const FinalArgs& f, double* scratch,
   m.cy = f.cy;
   m.cz = f.cz;
   const size_t g6 = (size_t)6 * m.nx;
-  m.gsum_in = scratch + ((s - 1) & 1) * g6;
-  m.gsum_out = scratch + (s & 1) * g6;
-  const int grid = (m.nx + kWarpsPerCta - 1) / kWarpsPerCta;
+  m.gsum_in = gsum + ((s - 1) & 1) * g6;
+  m.gsum_out = gsum + (s & 1) * g6;
+  const dim3 grid((m.nx + kWarpsPerCta - 1) / kWarpsPerCta, nwin);
   if (s == 1) {
     MargArgs mi = m;
     mi.gsum_out = const_cast<double*>(m.gsum_in);
-    cudaError_t e = launch_pdl(mrec_init_kernel, grid, 32 * kWarpsPerCta, 0, st, mi);
+    cudaError_t e = launch_pdl_grid(mrec_init_kernel, grid, 32 * kWarpsPerCta, 0, st, mi);
     if (e != cudaSuccess) return e;
   }
   const int jpl = (m.nvx + 31) / 32;
@@ -372,7 +387,7 @@ cudaError_t launch_marg(const MargArgs& m0, const FinalArgs& f, double* scratch,
 #define PBGK_MK(J) (m.trap ? mrec_step_kernel<J, true> : mrec_step_kernel<J, false>)
   k = jpl <= 1 ? PBGK_MK(1) : (jpl == 2 ? PBGK_MK(2) : (jpl == 3 ? PBGK_MK(3) : PBGK_MK(4)));
 #undef PBGK_MK
-  return launch_pdl(k, grid, 32 * kWarpsPerCta, marg_smem_bytes(m.nvx, m.nvy, m.nvz, f.TL), st, m, f);
+  return launch_pdl_grid(k, grid, 32 * kWarpsPerCta, marg_smem_bytes(m.nvx, m.nvy, m.nvz, f.TL), st, m, f);
 }
 
 }  // namespace pbgk

@@ -194,3 +194,32 @@ def test_given_f0_non_finite_reports_step_one(levels):
     with pytest.raises(P.BlowUpError) as info:
         rt.raise_kinetic(c)
     assert info.value.step == 1
+
+
+@pytest.mark.parametrize("levels", [2, 3])
+@pytest.mark.parametrize("bc", ["outflow", "periodic"])
+def test_batched_windows_equal_one_step_path(levels, bc, monkeypatch):
+    # pbgk_propagate_windows runs the recursion of all windows batched (one
+    # launch per step, windows of different lengths, an empty one, a failing
+    # one) -- per-window moments and keys as on the one-step path; also with
+    # window groups smaller than the batch (PBGK_BATCH_BYTES)
+    from paper_2502_02704_b200.kinetic import propagate_windows
+    g, mesh = _grids(10, (16, 16, 16), 8.0)
+    kp = P.KineticParams(1e-2)
+    ctx = rt.ctx_for(g, P.BoundaryKind(bc))
+    cap = stable_dt_kinetic(g, kp)
+    spans = [7.5 * cap, 4.0 * cap, 0.0, 9.2 * cap, 2.5 * cap]
+    rng = np.random.default_rng(9)
+    Us = [random_moments(10, rng) for _ in spans]
+    Us[3][0][4] = np.nan  # window 3 fails (BlowUpError at some step)
+    mom_in = torch.stack([rt.to_device_moments(P.MomentField(*U), ctx.device) for U in Us])
+    res = {}
+    for L in (0, levels):
+        out = ctx.empty_moments(len(spans))
+        with ctx.fusion_levels(L):
+            codes = propagate_windows(ctx, mom_in, spans, g, kp, None, out)
+        res[L] = (out.cpu().numpy(), codes)
+    (m0, c0), (m1, c1) = res[0], res[levels]
+    assert c1 == c0 and c0[3] != -1 and c0[2] == -1
+    for w in (0, 1, 2, 4):
+        assert moment_gap(_unpack(m1[w]), _unpack(m0[w])) <= 1e-13
