@@ -33,8 +33,10 @@ cudaError_t launch_marg(const MargArgs& m, const FinalArgs& f, double* gsum, int
                         cudaStream_t st);
 size_t marg_state_doubles(int nvx);
 cudaError_t launch_q_from_f(const MargArgs& m, const double* f, cudaStream_t st);
+cudaError_t launch_marg_all(const MargArgs& m0, const FinalArgs& f, const double* q0, double* qa,
+                            double* qb, double* gsum, long long t_step, int S, int nwin,
+                            unsigned* bar, cudaStream_t st);
 size_t marg_smem_bytes(int nvx, int nvy, int nvz, int TL);
-size_t marg_scratch_doubles(int nx, int nvx, int nvy, int nvz);
 cudaError_t launch_set_key(ErrKey* p, ErrKey v, cudaStream_t st);
 cudaError_t launch_fluid_batch(const FluidArgs& a, int nwin, const double* in, double* out,
                                const double* minuend, const double* t0, const double* t1,
@@ -61,6 +63,21 @@ int fail(const std::string& msg) {
     if (e_ != cudaSuccess)                                                         \
       return fail(std::string(#expr) + ": " + cudaGetErrorString(e_));            \
   } while (0)
+
+// device buffer of at least n elements (grown, never shrunk)
+template <typename T>
+int ensure_dev(T*& p, size_t& cap, size_t n, cudaStream_t st) {
+  if (n <= cap) return 0;
+  if (p) {
+    CK(cudaStreamSynchronize(st));
+    CK(cudaFree(p));
+    p = nullptr;
+    cap = 0;
+  }
+  CK(cudaMalloc(&p, n * sizeof(T)));
+  cap = n;
+  return 0;
+}
 
 // compile-time tile shapes of sweep.cu (index = cfg id)
 struct CfgShape {
@@ -154,20 +171,19 @@ struct pbgk_ctx {
   size_t times_cap = 0;
   std::vector<MapEntry> maps;
   size_t ws_bytes = 0;
-  // multi-step path (fsweep.cu + marginal.cu): levels per pass (0 = off),
-  // the moment-recursion state ping-pong and a ring of eight relax-table buffers
-  int fuse = -1;  // -1: per-shape default (fuse_levels)
-  double* d_marg[2] = {nullptr, nullptr};
-  double* d_tabs[8] = {};
-  double* d_mscr = nullptr;  // recursion scratch: the G sums of one window
-  // batched recursion of pbgk_propagate_windows: per-(window, step) tables,
-  // per-window state ping-pong, G sums, per-step dt and step counts
+  // multi-step path (fsweep.cu + marginal.cu): levels per pass (0 = off,
+  // -1 = the per-shape default of fuse_levels); Q of a given f0
+  int fuse = -1;
+  double* d_q0 = nullptr;
+  // the recursion's per-(window, step) tables, per-window state ping-pong,
+  // G sums, per-step dt and step counts (multi-step path)
   double* d_bt = nullptr;
   double* d_bq = nullptr;
   double* d_bg = nullptr;
   double* d_bdts = nullptr;
   int* d_bnst = nullptr;
   size_t bt_cap = 0, bq_cap = 0, bg_cap = 0, bdts_cap = 0, bnst_cap = 0;
+  unsigned* d_gbar = nullptr;  // grid barrier of the one-launch recursion
 };
 
 namespace {
@@ -543,14 +559,13 @@ void pbgk_ctx_destroy(pbgk_ctx* c) {
   cudaFree(c->d_part);
   cudaFree(c->d_tab[0]);
   cudaFree(c->d_tab[1]);
-  for (auto* p : c->d_marg) cudaFree(p);
-  for (auto* p : c->d_tabs) cudaFree(p);
-  cudaFree(c->d_mscr);
+  cudaFree(c->d_q0);
   cudaFree(c->d_bt);
   cudaFree(c->d_bq);
   cudaFree(c->d_bg);
   cudaFree(c->d_bdts);
   cudaFree(c->d_bnst);
+  cudaFree(c->d_gbar);
   cudaFree(c->d_scratch);
   cudaFree(c->d_err);
   cudaFree(c->d_keys);
@@ -680,7 +695,7 @@ int pbgk_check_finite(pbgk_ctx* c, const double* f, int step, void* stream, long
 }
 
 namespace {
-bool fused_ok(pbgk_ctx* c, bool field);
+bool fused_ok(pbgk_ctx* c, bool field, bool batched);
 int propagate_body_fused(pbgk_ctx* c, const double* f0, const double* mom0, double* f_out,
                          double* f_tmp, int write_final, double* mom_out, int S, const double* h_dts,
                          double eps, double tau, cudaStream_t st);
@@ -691,7 +706,7 @@ int propagate_body(pbgk_ctx* c, const double* f0, const double* mom0, double* f_
                    int write_final, double* mom_out, int S, const double* h_dts, double eps,
                    double tau, const double* E, double e_max, cudaStream_t st) {
   const bool field = (E != nullptr && e_max > 0.0);
-  if (S > 0 && fused_ok(c, field))
+  if (S > 0 && fused_ok(c, field, false))
     return propagate_body_fused(c, f0, mom0, f_out, f_tmp, write_final, mom_out, S, h_dts, eps, tau,
                                 st);
   const int pid = field ? 1 : (c->x_scheme == 1 ? 2 : 0);
@@ -728,64 +743,34 @@ namespace {
 // Multi-step path usable on this context for an upwind propagation without
 // the v_x field term (the marginal recursion is closed for it; MUSCL's
 // limiter is not linear, slabs exchange halos per step).
-int fuse_levels(pbgk_ctx* c);
+int fuse_levels(pbgk_ctx* c, bool batched);
 
-bool fused_ok(pbgk_ctx* c, bool field) {
-  if (fuse_levels(c) < 1 || field || c->x_scheme != 0 || c->g.bc == 3) return false;
+bool fused_ok(pbgk_ctx* c, bool field, bool batched = false) {
+  if (fuse_levels(c, batched) < 1 || field || c->x_scheme != 0 || c->g.bc == 3) return false;
   if (!fsweep_has_cfg(c->plan[0].cfg)) return false;
   if (marg_smem_bytes(c->g.nvx, c->g.nvy, c->g.nvz, c->TL) > c->smem_optin) return false;
-  if (!c->d_marg[0]) {
+  if (!c->d_q0) {
     const size_t ms = (size_t)c->g.nx * marg_state_doubles(c->g.nvx) * sizeof(double);
-    const size_t tb = (size_t)c->g.nx * c->TL * sizeof(double);
-    for (auto*& p : c->d_marg)
-      if (cudaMalloc(&p, ms) != cudaSuccess) return false;
-    for (auto*& p : c->d_tabs)
-      if (cudaMalloc(&p, tb) != cudaSuccess) return false;
-    const size_t sc = marg_scratch_doubles(c->g.nx, c->g.nvx, c->g.nvy, c->g.nvz) * sizeof(double);
-    if (cudaMalloc(&c->d_mscr, sc) != cudaSuccess) return false;
-    c->ws_bytes += 2 * ms + 8 * tb + sc;
+    if (cudaMalloc(&c->d_q0, ms) != cudaSuccess) return false;
+    c->ws_bytes += ms;
   }
   return true;
 }
 
 // Levels per pass: the context's setting, or (auto, -1) the measured best
 // per shape (round 1, one B200): 3 for the 2-wide lane layouts, 2 for the
-// 48-wide V = 6 one (its third level spills), one-step below ~4M cells where
-// the recursion's launches outweigh the saved traffic.
-int fuse_levels(pbgk_ctx* c) {
+// 48-wide V = 6 one (its third level spills); a single propagation below ~4M
+// cells stays one-step (its recursion steps are latency-bound launches),
+// batched windows (pbgk_propagate_windows: one recursion launch per step for
+// the whole batch) always take the multi-step path (config 0: 1.7x).
+int fuse_levels(pbgk_ctx* c, bool batched) {
   static const int env = getenv("PBGK_FUSE") ? atoi(getenv("PBGK_FUSE")) : -2;
   int L = env >= -1 ? env : c->fuse;
   if (L < 0) {
     const double cells = (double)c->g.nx * c->g.nvx * c->g.nvy * c->g.nvz;
-    L = cells < 4.0e6 ? 0 : (kCfg[c->plan[0].cfg].V == 6 ? 2 : 3);
+    L = (!batched && cells < 4.0e6) ? 0 : (kCfg[c->plan[0].cfg].V == 6 ? 2 : 3);
   }
   return std::min(L, 4);
-}
-
-int run_marg(pbgk_ctx* c, const double* min, double* mout, const double* tab_in, double* tab_out,
-             double dt, double eps, double tau, int step, cudaStream_t st) {
-  MargArgs m{};
-  m.nx = c->g.nx;
-  m.nvx = c->g.nvx;
-  m.nvy = c->g.nvy;
-  m.nvz = c->g.nvz;
-  m.bc = c->g.bc;
-  m.min = min;
-  m.mout = mout;
-  m.tab_in = tab_in;
-  m.cx = c->d_c[0];
-  m.dtdx = dt / c->dx;
-  FinalArgs f = fin_args(c, c->plan[0]);
-  f.mode = kFinRelax;
-  f.tab = tab_out;
-  f.dt = dt;
-  f.eps = eps;
-  f.tau = tau;
-  f.step = step;
-  ProfScope ps(c, st, 3, 0.0);
-  if (step == 1) ++g_launches;  // the G sums of the lift tables
-  CK(launch_marg(m, f, c->d_mscr, step, 1, st));
-  return 0;
 }
 
 // One pass of n <= 4 fine steps (steps s0+1 .. s0+n) over f.
@@ -837,22 +822,36 @@ int run_fsweep(pbgk_ctx* c, int n, const double* in, double* out, const double* 
   return 0;
 }
 
-// propagate_body for a window from moments on the multi-step path: the
-// marginal recursion produces R_1..R_S one step ahead of the passes; the
-// passes take up to L steps each; the last relax + projection is the
-// reference-order marginal sweep of f_S (P(f_S) comes from f itself).
+// propagate_body on the multi-step path (one window, from moments or a given
+// f0): the moment recursion for all S steps first (one launch when the grid
+// is co-resident), per-step tables; then the passes of up to L steps; the
+// last relax + projection is the reference-order marginal sweep of f*_S.
+int run_recursion(pbgk_ctx* c, int g, const double* q0, double* T, long long t_ws, int S,
+                  const double* dts, const int* nst, ErrKey* errw, double eps, double tau,
+                  cudaStream_t st);
+
 int propagate_body_fused(pbgk_ctx* c, const double* f0, const double* mom0, double* f_out,
                          double* f_tmp, int write_final, double* mom_out, int S, const double* h_dts,
                          double eps, double tau, cudaStream_t st) {
-  const int L = fuse_levels(c);
+  const int L = fuse_levels(c, false);
   const int P = (S + L - 1) / L;  // passes
   const int W = P + (write_final ? 1 : 0);
   auto buf = [&](int w) { return ((W - w) % 2 == 0) ? f_out : f_tmp; };
-  double** T8 = c->d_tabs;  // ring: a pass reads R_s0..R_s0+L-1 while R_s0+L is written
+  const size_t tstep = (size_t)c->g.nx * c->TL;
+  const size_t qw = (size_t)c->g.nx * marg_state_doubles(c->g.nvx);
+  if (ensure_dev(c->d_bt, c->bt_cap, (size_t)(S + 1) * tstep, st) ||
+      ensure_dev(c->d_bq, c->bq_cap, 2 * qw, st) ||
+      ensure_dev(c->d_bg, c->bg_cap, (size_t)12 * c->g.nx, st) ||
+      ensure_dev(c->d_bdts, c->bdts_cap, (size_t)S, st))
+    return -1;
+  double* T = c->d_bt;
+  // (pageable source: the copy completes before the call returns)
+  CK(cudaMemcpyAsync(c->d_bdts, h_dts, (size_t)S * sizeof(double), cudaMemcpyHostToDevice, st));
   // f_0: the lift of mom0 (synthesised by the first pass), or the given f0
   // with identity tables (r = 1, ls = 0) and the recursion started from Q(f0)
+  const double* q0 = nullptr;
   if (f0) {
-    if (run_final(c, 0, kFinIdentity, nullptr, nullptr, T8[0], 0, 1, 1, nullptr, 0, st)) return -1;
+    if (run_final(c, 0, kFinIdentity, nullptr, nullptr, T, 0, 1, 1, nullptr, 0, st)) return -1;
     MargArgs m{};
     m.nx = c->g.nx;
     m.nvx = c->g.nvx;
@@ -861,35 +860,31 @@ int propagate_body_fused(pbgk_ctx* c, const double* f0, const double* mom0, doub
     m.cy = c->d_c[1];
     m.cz = c->d_c[2];
     m.trap = c->quad;
-    m.mout = c->d_marg[0];
+    m.mout = c->d_q0;
     ++g_launches;
     CK(launch_q_from_f(m, f0, st));
+    q0 = c->d_q0;
   } else {
-    if (run_final(c, 0, kFinSynthRaw, mom0, nullptr, T8[0], 0, 1, 1, nullptr, 0, st)) return -1;
+    if (run_final(c, 0, kFinSynthRaw, mom0, nullptr, T, 0, 1, 1, nullptr, 0, st)) return -1;
   }
-  int s0 = 0, w = 0;
+  if (run_recursion(c, 1, q0, T, 0, S, c->d_bdts, nullptr, nullptr, eps, tau, st)) return -1;
+  int w = 0;
   const double* in = f0;
-  for (int s = 1; s <= S; ++s) {
-    const double dt = h_dts[s - 1];
-    const double* qin = (s == 1) ? (f0 ? c->d_marg[0] : nullptr) : c->d_marg[(s - 1) & 1];
-    if (run_marg(c, qin, c->d_marg[s & 1], T8[(s - 1) & 7], T8[s & 7], dt, eps, tau, s, st))
-      return -1;
-    if (s - s0 == L || s == S) {
-      const int n = s - s0;
-      const double* tabs[kMaxLevels];
-      double dtdx[kMaxLevels];
-      for (int l = 0; l < n; ++l) {
-        tabs[l] = T8[(s0 + l) & 7];
-        dtdx[l] = h_dts[s0 + l] / c->dx;
-      }
-      double* out = buf(++w);
-      if (run_fsweep(c, n, in, out, tabs, dtdx, s0 + 1, st)) return -1;
-      in = out;
-      s0 = s;
+  for (int s0 = 0; s0 < S;) {
+    const int n = std::min(L, S - s0);
+    const double* tabs[kMaxLevels];
+    double dtdx[kMaxLevels];
+    for (int l = 0; l < n; ++l) {
+      tabs[l] = T + (size_t)(s0 + l) * tstep;
+      dtdx[l] = h_dts[s0 + l] / c->dx;
     }
+    double* out = buf(++w);
+    if (run_fsweep(c, n, in, out, tabs, dtdx, s0 + 1, st)) return -1;
+    in = out;
+    s0 += n;
   }
-  if (run_sweep(c, 0, false, in, T8[S & 7], write_final ? f_out : nullptr, 0.0, nullptr, 0.0, 0.0, S,
-                st))
+  if (run_sweep(c, 0, false, in, T + (size_t)S * tstep, write_final ? f_out : nullptr, 0.0, nullptr,
+                0.0, 0.0, S, st))
     return -1;
   if (mom_out && run_final(c, 0, kFinProject, nullptr, mom_out, nullptr, 0, 1, 1, nullptr, S + 1, st))
     return -1;
@@ -900,17 +895,62 @@ int propagate_body_fused(pbgk_ctx* c, const double* f0, const double* mom0, doub
 }  // extern "C"
 
 namespace {
-template <typename T>
-int ensure_dev(T*& p, size_t& cap, size_t n, cudaStream_t st) {
-  if (n <= cap) return 0;
-  if (p) {
-    CK(cudaStreamSynchronize(st));
-    CK(cudaFree(p));
-    p = nullptr;
-    cap = 0;
+
+// The moment recursion for steps 1..S of `g` windows: per-(window, step)
+// tables at T + w t_ws + s (nx TL) (the step-0 tables already there), state
+// ping-pong in d_bq, G sums in d_bg, dts[s-1][w] and per-window step counts
+// on the device (nst may be null for one window), keys per window (errw, or
+// the context's error slot).  One cooperative launch for all steps when the
+// grid is co-resident, else one launch per step.
+int run_recursion(pbgk_ctx* c, int g, const double* q0, double* T, long long t_ws, int S,
+                  const double* dts, const int* nst, ErrKey* errw, double eps, double tau,
+                  cudaStream_t st) {
+  const int nx = c->g.nx;
+  const size_t tstep = (size_t)nx * c->TL;
+  const size_t qw = (size_t)nx * marg_state_doubles(c->g.nvx);
+  MargArgs mg{};
+  mg.nx = nx;
+  mg.nvx = c->g.nvx;
+  mg.nvy = c->g.nvy;
+  mg.nvz = c->g.nvz;
+  mg.bc = c->g.bc;
+  mg.cx = c->d_c[0];
+  mg.q_ws = (long long)qw;
+  mg.t_ws = t_ws;
+  mg.g_ws = 12LL * nx;
+  mg.nst = nst;
+  mg.errw = errw;
+  mg.dx = c->dx;
+  FinalArgs f = fin_args(c, c->plan[0]);
+  f.mode = kFinRelax;
+  f.eps = eps;
+  f.tau = tau;
+  static const bool no_multi = getenv("PBGK_REC_STEPWISE") != nullptr;  // dev A/B knob
+  if (!no_multi) {
+    if (!c->d_gbar) CK(cudaMalloc(&c->d_gbar, 2 * sizeof(unsigned)));
+    mg.tab_in = T;
+    mg.dts = dts;
+    ProfScope ps(c, st, 3, 0.0);
+    ++g_launches;  // + the barrier reset
+    const cudaError_t e = launch_marg_all(mg, f, q0, c->d_bq + (size_t)g * qw, c->d_bq, c->d_bg,
+                                          (long long)tstep, S, g, c->d_gbar, st);
+    if (e == cudaSuccess) return 0;
+    if (e != cudaErrorCooperativeLaunchTooLarge) return fail(std::string("recursion: ") + cudaGetErrorString(e));
+    cudaGetLastError();
   }
-  CK(cudaMalloc(&p, n * sizeof(T)));
-  cap = n;
+  for (int s = 1; s <= S; ++s) {
+    MargArgs m = mg;
+    m.min = s == 1 ? q0 : c->d_bq + ((s - 1) & 1) * g * qw;
+    m.mout = c->d_bq + (s & 1) * g * qw;
+    m.tab_in = T + (size_t)(s - 1) * tstep;
+    m.dts = dts + (size_t)(s - 1) * g;
+    FinalArgs fs = f;
+    fs.tab = T + (size_t)s * tstep;
+    fs.step = s;
+    ProfScope ps(c, st, 3, 0.0);
+    if (s == 1) ++g_launches;
+    CK(launch_marg(m, fs, c->d_bg, s, g, st));
+  }
   return 0;
 }
 
@@ -941,7 +981,7 @@ int windows_fused(pbgk_ctx* c, int nwin, const double* mom_in, double* mom_out, 
       ensure_dev(c->d_bdts, c->bdts_cap, (size_t)std::max(Smax, 1) * G, st) ||
       ensure_dev(c->d_bnst, c->bnst_cap, (size_t)G, st))
     return -1;
-  const int L = fuse_levels(c);
+  const int L = fuse_levels(c, true);
   std::vector<double> hd((size_t)std::max(Smax, 1) * G);
   std::vector<int> hn(G);
   for (int w0 = 0; w0 < nwin; w0 += G) {
@@ -969,34 +1009,9 @@ int windows_fused(pbgk_ctx* c, int nwin, const double* mom_in, double* mom_out, 
       if (rc) return -1;
     }
     // the batched recursion: steps 1..Smax for the group's windows
-    for (int s = 1; s <= Smax; ++s) {
-      MargArgs mg{};
-      mg.nx = nx;
-      mg.nvx = c->g.nvx;
-      mg.nvy = c->g.nvy;
-      mg.nvz = c->g.nvz;
-      mg.bc = c->g.bc;
-      mg.min = s == 1 ? nullptr : c->d_bq + ((s - 1) & 1) * G * qw;
-      mg.mout = c->d_bq + (s & 1) * G * qw;
-      mg.tab_in = c->d_bt + (size_t)(s - 1) * tstep;
-      mg.cx = c->d_c[0];
-      mg.q_ws = (long long)qw;
-      mg.t_ws = (long long)t_ws;
-      mg.g_ws = 12LL * nx;
-      mg.dts = c->d_bdts + (size_t)(s - 1) * g;
-      mg.nst = c->d_bnst;
-      mg.errw = c->d_keys + w0;
-      mg.dx = c->dx;
-      FinalArgs f = fin_args(c, c->plan[0]);
-      f.mode = kFinRelax;
-      f.tab = c->d_bt + (size_t)s * tstep;
-      f.eps = eps;
-      f.tau = tau;
-      f.step = s;
-      ProfScope ps(c, st, 3, 0.0);
-      if (s == 1) ++g_launches;
-      CK(launch_marg(mg, f, c->d_bg, s, g, st));
-    }
+    if (run_recursion(c, g, nullptr, c->d_bt, (long long)t_ws, Smax, c->d_bdts, c->d_bnst,
+                      c->d_keys + w0, eps, tau, st))
+      return -1;
     // each window's passes and its final projection from f
     for (int k = 0; k < g; ++k) {
       const int w = w0 + k, S = h_nsteps[w];
@@ -1075,7 +1090,7 @@ int pbgk_propagate_windows(pbgk_ctx* c, int nwin, const double* mom_in, double* 
   CK(cudaMemsetAsync(c->d_keys, 0xFF, (size_t)nwin * sizeof(ErrKey), st));  // kNoError = ~0
   const size_t m = (size_t)5 * c->g.nx;
   const bool field = (E != nullptr && e_max > 0.0);
-  if (fused_ok(c, field)) {
+  if (fused_ok(c, field, true)) {
     if (windows_fused(c, nwin, mom_in, mom_out, f_a, f_b, h_nsteps, h_dts, eps, tau, st)) return -1;
     CK(cudaMemcpyAsync(c->h_keys, c->d_keys, (size_t)nwin * sizeof(ErrKey), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));

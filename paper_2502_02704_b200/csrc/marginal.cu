@@ -95,20 +95,16 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) mrec_init_kernel(const Marg
   }
 }
 
-// One recursion step: warp per cell i.  JPL = v_x rows per lane.
+// One recursion step of cell i of window w by the calling warp (step `step`;
+// JPL = v_x rows per lane; mxs: nvx doubles of warp-private shared memory).
+// Every global read of data written by earlier steps goes through L2
+// (ld.global.cg): the persistent kernel below runs several steps per launch.
 template <int JPL, bool TRAP>
-__global__ void __launch_bounds__(32 * kWarpsPerCta) mrec_step_kernel(const MargArgs m, const FinalArgs f) {
-  extern __shared__ double sm[];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int i = blockIdx.x * kWarpsPerCta + wid;
+__device__ __forceinline__ void mrec_cell(const MargArgs& m, const FinalArgs& f, int step, int i, int w,
+                                          double* mxs) {
+  const int lane = threadIdx.x & 31;
   const int nx = m.nx, nvx = m.nvx, nvy = m.nvy, nvz = m.nvz;
-  double* mxs = sm + (size_t)wid * nvx;  // this cell's m_x (mirror access)
-  pdl_wait();  // tables, G sums and Q(f*_{s-1}) come from the preceding kernels
-  pdl_trigger();
-  if (i >= nx) return;
-  // window of a batch (grid.y): its state, tables, G sums, dt and key
-  const int w = blockIdx.y;
-  if (m.nst != nullptr && f.step > m.nst[w]) return;  // this window has fewer steps
+  if (m.nst != nullptr && step > m.nst[w]) return;  // this window has fewer steps
   const double* qmin = m.min ? m.min + w * m.q_ws : nullptr;
   double* qout = m.mout + w * m.q_ws;
   const double* tab_in = m.tab_in + w * m.t_ws;
@@ -133,9 +129,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) mrec_step_kernel(const Marg
     if (cc >= 0) {
       const double* row = tab_in + (size_t)cc * m.TL;
       const double* gs = gsum_in + (size_t)cc * 6;
-      rq[q] = row[0];
-      lq[q] = row[1];
-      const double sy0 = gs[0], sy1 = gs[1], sy2 = gs[2], sz0 = gs[3], sz1 = gs[4], sz2 = gs[5];
+      rq[q] = __ldcg(row);
+      lq[q] = __ldcg(row + 1);
+      const double sy0 = __ldcg(gs), sy1 = __ldcg(gs + 1), sy2 = __ldcg(gs + 2);
+      const double sz0 = __ldcg(gs + 3), sz1 = __ldcg(gs + 4), sz2 = __ldcg(gs + 5);
       G[q][0] = sy0 * sz0;
       G[q][1] = sy1 * sz0;
       G[q][2] = sy2 * sz0;
@@ -153,8 +150,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) mrec_step_kernel(const Marg
 #pragma unroll
     for (int k = 0; k < 5; ++k) qc[k][u] = qn[k][u] = 0.0;
     if (jx < nvx) {
-      gxc[u] = __ldg(tab_in + (size_t)i * m.TL + m.gxo + jx);
-      if (cn >= 0) gxn[u] = __ldg(tab_in + (size_t)cn * m.TL + m.gxo + jx);
+      gxc[u] = __ldcg(tab_in + (size_t)i * m.TL + m.gxo + jx);
+      if (cn >= 0) gxn[u] = __ldcg(tab_in + (size_t)cn * m.TL + m.gxo + jx);
       if (!synth) {
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
@@ -230,8 +227,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) mrec_step_kernel(const Marg
   const double e2 = ((0.0 + ex) + ey) + ez;
   const double th = (e2 * dvol) / (3.0 * rho);
   if (lane == 0) {
-    if (rho <= 0.0) atomicMin(err, err_key(0, f.step, kErrProjectRho));
-    if (rho <= 0.0 || th <= 0.0) atomicMin(err, err_key(0, f.step, kErrLiftState));
+    if (rho <= 0.0) atomicMin(err, err_key(0, step, kErrProjectRho));
+    if (rho <= 0.0 || th <= 0.0) atomicMin(err, err_key(0, step, kErrLiftState));
   }
   // the table row of R_s (finalize_impl.cuh, same expressions and sum order)
   const double inv2t = 1.0 / (2.0 * th);
@@ -288,7 +285,85 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) mrec_step_kernel(const Marg
     // f_s = R_s(f*_s) is finite iff f*_s and the table row are (BlowUpError(step))
     if (nonfinite || !isfinite(r) || !isfinite(ls) || !isfinite(amp) || !isfinite(u0) ||
         !isfinite(u1) || !isfinite(u2) || !isfinite(th))
-      atomicMin(err, err_key(0, f.step, kErrNonFinite));
+      atomicMin(err, err_key(0, step, kErrNonFinite));
+  }
+}
+
+template <int JPL, bool TRAP>
+__global__ void __launch_bounds__(32 * kWarpsPerCta) mrec_step_kernel(const MargArgs m, const FinalArgs f) {
+  extern __shared__ double sm[];
+  const int wid = threadIdx.x >> 5;
+  const int i = blockIdx.x * kWarpsPerCta + wid;
+  pdl_wait();  // tables, G sums and Q(f*_{s-1}) come from the preceding kernels
+  pdl_trigger();
+  if (i >= m.nx) return;
+  mrec_cell<JPL, TRAP>(m, f, f.step, i, blockIdx.y, sm + (size_t)wid * m.nvx);
+}
+
+// Device-wide barrier of a co-resident (cooperatively launched) grid:
+// generation counter, the last arriver resets the count and bumps it.
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = bar + 1;
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == nblocks - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// All steps 1..S of the recursion in one launch (small grids: the per-step
+// launches are latency-bound).  Per-step tables at tab_in + s * t_step (tab_in
+// = the step-0 tables), state ping-pong q[2] (q0: Q of a given f0, or null:
+// a lift), G sums ping-pong in gsum; one grid barrier per step.  Windows of a
+// batch: grid.y as in mrec_step_kernel.
+template <int JPL, bool TRAP>
+__global__ void __launch_bounds__(32 * kWarpsPerCta) mrec_multi_kernel(MargArgs m, FinalArgs f,
+                                                                        const double* q0, double* qa,
+                                                                        double* qb, double* gsum,
+                                                                        long long t_step, int S,
+                                                                        unsigned* bar) {
+  extern __shared__ double sm[];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x * kWarpsPerCta + wid;
+  const int w = blockIdx.y;
+  const unsigned nblocks = gridDim.x * gridDim.y;
+  pdl_wait();
+  pdl_trigger();
+  const size_t g6 = (size_t)6 * m.nx;
+  const double* tab0 = m.tab_in;
+  // G sums of the step-0 tables
+  if (i < m.nx) {
+    const double* row = tab0 + w * m.t_ws + (size_t)i * m.TL;
+    double a0, a1, a2, b0, b1, b2;
+    axis_sums(row + m.gyo, m.cy, m.nvy, m.trap, lane, a0, a1, a2);
+    axis_sums(row + m.gzo, m.cz, m.nvz, m.trap, lane, b0, b1, b2);
+    if (lane == 0) {
+      double* g = gsum + w * m.g_ws + (size_t)i * 6;
+      g[0] = a0; g[1] = a1; g[2] = a2; g[3] = b0; g[4] = b1; g[5] = b2;
+    }
+  }
+  for (int s = 1; s <= S; ++s) {
+    grid_barrier(bar, nblocks);
+    MargArgs ms = m;
+    ms.min = s == 1 ? q0 : ((s - 1) & 1 ? qa : qb);
+    ms.mout = (s & 1) ? qa : qb;
+    ms.tab_in = tab0 + (size_t)(s - 1) * t_step;
+    ms.gsum_in = gsum + ((s - 1) & 1) * g6;
+    ms.gsum_out = gsum + (s & 1) * g6;
+    ms.dts = m.dts + (size_t)(s - 1) * gridDim.y;
+    FinalArgs fs = f;
+    fs.tab = const_cast<double*>(tab0) + (size_t)s * t_step;
+    if (i < m.nx) mrec_cell<JPL, TRAP>(ms, fs, s, i, w, sm + (size_t)wid * m.nvx);
   }
 }
 
@@ -350,13 +425,8 @@ size_t marg_smem_bytes(int nvx, int nvy, int nvz, int TL) {
   return (size_t)kWarpsPerCta * nvx * sizeof(double);
 }
 
-// Q (5 nvx per cell) lives in the caller's ping-pong buffers; the scratch
-// holds the two G-sum arrays (6 per cell each)
+// Q (5 nvx per cell) lives in the caller's ping-pong buffers
 size_t marg_state_doubles(int nvx) { return (size_t)5 * nvx; }
-size_t marg_scratch_doubles(int nx, int nvx, int nvy, int nvz) {
-  (void)nvx; (void)nvy; (void)nvz;
-  return (size_t)2 * 6 * nx;
-}
 
 // Step s >= 1 for `nwin` windows (grid.y; the caller sets the per-window
 // strides, 0 for one window).  s == 1: the input tables are a lift or
@@ -388,6 +458,47 @@ cudaError_t launch_marg(const MargArgs& m0, const FinalArgs& f, double* gsum, in
   k = jpl <= 1 ? PBGK_MK(1) : (jpl == 2 ? PBGK_MK(2) : (jpl == 3 ? PBGK_MK(3) : PBGK_MK(4)));
 #undef PBGK_MK
   return launch_pdl_grid(k, grid, 32 * kWarpsPerCta, marg_smem_bytes(m.nvx, m.nvy, m.nvz, f.TL), st, m, f);
+}
+
+// All S steps in one cooperative launch when the grid is co-resident (see
+// mrec_multi_kernel); returns cudaErrorCooperativeLaunchTooLarge otherwise.
+cudaError_t launch_marg_all(const MargArgs& m0, const FinalArgs& f, const double* q0, double* qa,
+                            double* qb, double* gsum, long long t_step, int S, int nwin,
+                            unsigned* bar, cudaStream_t st) {
+  MargArgs m = m0;
+  m.TL = f.TL;
+  m.gxo = f.gxo;
+  m.gyo = f.gyo;
+  m.gzo = f.gzo;
+  m.trap = f.trap;
+  m.cy = f.cy;
+  m.cz = f.cz;
+  const int jpl = (m.nvx + 31) / 32;
+  void (*k)(MargArgs, FinalArgs, const double*, double*, double*, double*, long long, int, unsigned*) = nullptr;
+#define PBGK_MK(J) (m.trap ? mrec_multi_kernel<J, true> : mrec_multi_kernel<J, false>)
+  k = jpl <= 1 ? PBGK_MK(1) : (jpl == 2 ? PBGK_MK(2) : (jpl == 3 ? PBGK_MK(3) : PBGK_MK(4)));
+#undef PBGK_MK
+  const size_t smem = marg_smem_bytes(m.nvx, m.nvy, m.nvz, f.TL);
+  const dim3 grid((m.nx + kWarpsPerCta - 1) / kWarpsPerCta, nwin);
+  int dev = 0, nsm = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, 32 * kWarpsPerCta, smem);
+  if (e != cudaSuccess) return e;
+  if ((long long)grid.x * grid.y > (long long)per * nsm) return cudaErrorCooperativeLaunchTooLarge;
+  e = cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), st);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(32 * kWarpsPerCta);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, m, f, q0, qa, qb, gsum, t_step, S, bar);
 }
 
 }  // namespace pbgk
