@@ -305,8 +305,8 @@ def run_ours(args, w, world, rank, local):
             "recursion_share_of_step": share(prof.marg_ms),
             "fine_steps_per_multistep_pass": prof.msweep_steps / prof.msweeps,
             "multistep_sweeps_timed": prof.msweeps,
-            "note": "multi-step path: L fine steps per pass over f (relax tables from the 2-D "
-                    "marginal recursion), so one cell-update moves 16/L algorithmic bytes; "
+            "note": "multi-step path: L fine steps per pass over f (relax tables from the moment "
+                    "recursion), so one cell-update moves 16/L algorithmic bytes; "
                     "'achieved' is the pass's own f read + write over its time, and the "
                     "cell-update rate can exceed the one-step 16 B roofline"})
 

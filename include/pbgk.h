@@ -28,6 +28,8 @@
  *      kind 2  non-finite state after `step`    -> BlowUpError(step)
  *      kind 3  rho or p <= 0 in G after `step`  -> BlowUpError(step)
  *      kind 4  correction overshoot             -> CorrectionOvershootError(unit)
+ *      kind 5  internal: a multi-step pass timed out waiting for the
+ *              concurrent relax-table recursion  -> RuntimeError
  *    Keys are min-reduced: lowest unit, then earliest step, then the
  *    reference's raise order within a step (ref/moments.py:102-104,
  *    ref/lifting.py:44-45, ref/kinetic.py:157-159, ref/fluid.py:117-122).

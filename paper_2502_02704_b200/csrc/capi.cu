@@ -35,7 +35,10 @@ size_t marg_state_doubles(int nvx);
 cudaError_t launch_q_from_f(const MargArgs& m, const double* f, cudaStream_t st);
 cudaError_t launch_marg_all(const MargArgs& m0, const FinalArgs& f, const double* q0, double* qa,
                             double* qb, double* gsum, long long t_step, int S, int nwin,
-                            unsigned* bar, cudaStream_t st);
+                            unsigned* bar, cudaStream_t st, unsigned* prog, unsigned prog_base,
+                            int max_ctas);
+void marg_all_shape(int nx, int nvx, int nvy, int nvz, int TL, bool trap, int nwin, int* ctas,
+                    int* per_sm);
 size_t marg_smem_bytes(int nvx, int nvy, int nvz, int TL);
 cudaError_t launch_set_key(ErrKey* p, ErrKey v, cudaStream_t st);
 cudaError_t launch_fluid_batch(const FluidArgs& a, int nwin, const double* in, double* out,
@@ -184,6 +187,13 @@ struct pbgk_ctx {
   int* d_bnst = nullptr;
   size_t bt_cap = 0, bq_cap = 0, bg_cap = 0, bdts_cap = 0, bnst_cap = 0;
   unsigned* d_gbar = nullptr;  // grid barrier of the one-launch recursion
+  // concurrent recursion of single propagations: side stream, events, the
+  // device progress word (monotonic: each propagation takes a fresh base)
+  cudaStream_t st_side = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_done = nullptr;
+  unsigned* d_prog = nullptr;
+  unsigned prog_next = 1;
+  int rec_reserve = 0;  // SMs the passes leave to a concurrent recursion (0: serial)
 };
 
 namespace {
@@ -566,6 +576,10 @@ void pbgk_ctx_destroy(pbgk_ctx* c) {
   cudaFree(c->d_bdts);
   cudaFree(c->d_bnst);
   cudaFree(c->d_gbar);
+  cudaFree(c->d_prog);
+  if (c->ev_start) cudaEventDestroy(c->ev_start);
+  if (c->ev_done) cudaEventDestroy(c->ev_done);
+  if (c->st_side) cudaStreamDestroy(c->st_side);
   cudaFree(c->d_scratch);
   cudaFree(c->d_err);
   cudaFree(c->d_keys);
@@ -776,7 +790,8 @@ int fuse_levels(pbgk_ctx* c, bool batched) {
 
 // One pass of n <= 4 fine steps (steps s0+1 .. s0+n) over f.
 int run_fsweep(pbgk_ctx* c, int n, const double* in, double* out, const double* const* tabs,
-               const double* dtdx, int step0, cudaStream_t st) {
+               const double* dtdx, int step0, cudaStream_t st, const unsigned* prog = nullptr,
+               unsigned need = 0) {
   const Plan& p = c->plan[0];
   const CfgShape& s = kCfg[p.cfg];
   FSweepArgs a{};
@@ -801,6 +816,8 @@ int run_fsweep(pbgk_ctx* c, int n, const double* in, double* out, const double* 
   a.bc = c->g.bc;
   a.err = c->err_slot ? c->err_slot : c->d_err;
   a.step0 = step0;
+  a.prog = prog;
+  a.need = need;
   const bool synth = (in == nullptr);
   const CUtensorMap* map = tensor_map(c, synth ? nullptr : in, p.t, p.cfg);
   if (!map) return fail("tensor map: " + g_last_error);
@@ -819,6 +836,7 @@ int run_fsweep(pbgk_ctx* c, int n, const double* in, double* out, const double* 
   ProfScope ps(c, st, 2, (synth ? 0.0 : fbytes) + fbytes, n);
   int grid = (int)std::min<long long>(a.total, (long long)c->nsm * per_sm);
   if (c->slot_reserve > 0) grid = std::max(1, std::min(grid, c->nsm * per_sm - c->slot_reserve));
+  if (prog != nullptr) grid = std::max(1, std::min(grid, (c->nsm - c->rec_reserve) * per_sm));
   CK(launch_fsweep(p.cfg, *map, a, synth, n, grid, ns, smem, st));
   return 0;
 }
@@ -829,7 +847,34 @@ int run_fsweep(pbgk_ctx* c, int n, const double* in, double* out, const double* 
 // last relax + projection is the reference-order marginal sweep of f*_S.
 int run_recursion(pbgk_ctx* c, int g, const double* q0, double* T, long long t_ws, int S,
                   const double* dts, const int* nst, ErrKey* errw, double eps, double tau,
-                  cudaStream_t st);
+                  cudaStream_t st, unsigned* prog = nullptr, unsigned prog_base = 0,
+                  int max_ctas = 0);
+
+// A single propagation runs its recursion concurrently when its one-launch
+// grid fits <= 16 SMs (the passes lose at most 11 % of their SMs) and it has
+// enough steps to matter (PBGK_REC_CONCURRENT=0 disables: dev A/B knob).
+bool concurrent_ok(pbgk_ctx* c, int S, int L) {
+  static const int env = getenv("PBGK_REC_CONCURRENT") ? atoi(getenv("PBGK_REC_CONCURRENT")) : 1;
+  if (!env || S < 8 * L || getenv("PBGK_REC_STEPWISE")) return false;
+  int ctas = 0, per = 0;
+  marg_all_shape(c->g.nx, c->g.nvx, c->g.nvy, c->g.nvz, c->TL, c->quad != 0, 1, &ctas, &per);
+  if (per < 1) return false;
+  const int need = (ctas + per - 1) / per;
+  if (need > 16) return false;
+  if (!c->st_side) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&c->st_side, cudaStreamNonBlocking, hi) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming) != cudaSuccess ||
+        cudaMalloc(&c->d_prog, sizeof(unsigned)) != cudaSuccess ||
+        cudaMemset(c->d_prog, 0, sizeof(unsigned)) != cudaSuccess ||
+        (!c->d_gbar && cudaMalloc(&c->d_gbar, 2 * sizeof(unsigned)) != cudaSuccess))
+      return false;
+  }
+  c->rec_reserve = need;
+  return true;
+}
 
 int propagate_body_fused(pbgk_ctx* c, const double* f0, const double* mom0, double* f_out,
                          double* f_tmp, int write_final, double* mom_out, int S, const double* h_dts,
@@ -868,7 +913,27 @@ int propagate_body_fused(pbgk_ctx* c, const double* f0, const double* mom0, doub
   } else {
     if (run_final(c, 0, kFinSynthRaw, mom0, nullptr, T, 0, 1, 1, nullptr, 0, st)) return -1;
   }
-  if (run_recursion(c, 1, q0, T, 0, S, c->d_bdts, nullptr, nullptr, eps, tau, st)) return -1;
+  // concurrent recursion (long propagations on small grids, where its serial
+  // chain of S dependent steps is a large share): the one-launch recursion
+  // runs on a side stream on `rec_reserve` SMs, the passes on the others wait
+  // per pass on its device progress word
+  unsigned* prog = nullptr;
+  unsigned base = 0;
+  if (concurrent_ok(c, S, L)) {
+    prog = c->d_prog;
+    base = c->prog_next;
+    c->prog_next += (unsigned)S + 1;
+    CK(cudaEventRecord(c->ev_start, st));
+    CK(cudaStreamWaitEvent(c->st_side, c->ev_start, 0));
+    int ctas = 0, per = 0;
+    marg_all_shape(c->g.nx, c->g.nvx, c->g.nvy, c->g.nvz, c->TL, c->quad != 0, 1, &ctas, &per);
+    if (run_recursion(c, 1, q0, T, 0, S, c->d_bdts, nullptr, nullptr, eps, tau, c->st_side, prog, base,
+                      c->rec_reserve * per))
+      return -1;
+    CK(cudaEventRecord(c->ev_done, c->st_side));
+  } else if (run_recursion(c, 1, q0, T, 0, S, c->d_bdts, nullptr, nullptr, eps, tau, st)) {
+    return -1;
+  }
   int w = 0;
   const double* in = f0;
   for (int s0 = 0; s0 < S;) {
@@ -880,10 +945,12 @@ int propagate_body_fused(pbgk_ctx* c, const double* f0, const double* mom0, doub
       dtdx[l] = h_dts[s0 + l] / c->dx;
     }
     double* out = buf(++w);
-    if (run_fsweep(c, n, in, out, tabs, dtdx, s0 + 1, st)) return -1;
+    if (run_fsweep(c, n, in, out, tabs, dtdx, s0 + 1, st, prog, base + (unsigned)(s0 + n - 1)))
+      return -1;
     in = out;
     s0 += n;
   }
+  if (prog) CK(cudaStreamWaitEvent(st, c->ev_done, 0));  // R_S for the final relax
   if (run_sweep(c, 0, false, in, T + (size_t)S * tstep, write_final ? f_out : nullptr, 0.0, nullptr,
                 0.0, 0.0, S, st))
     return -1;
@@ -905,7 +972,7 @@ namespace {
 // grid is co-resident, else one launch per step.
 int run_recursion(pbgk_ctx* c, int g, const double* q0, double* T, long long t_ws, int S,
                   const double* dts, const int* nst, ErrKey* errw, double eps, double tau,
-                  cudaStream_t st) {
+                  cudaStream_t st, unsigned* prog, unsigned prog_base, int max_ctas) {
   const int nx = c->g.nx;
   const size_t tstep = (size_t)nx * c->TL;
   const size_t qw = (size_t)nx * marg_state_doubles(c->g.nvx);
@@ -934,8 +1001,10 @@ int run_recursion(pbgk_ctx* c, int g, const double* q0, double* T, long long t_w
     ProfScope ps(c, st, 3, 0.0);
     ++g_launches;  // + the barrier reset
     const cudaError_t e = launch_marg_all(mg, f, q0, c->d_bq + (size_t)g * qw, c->d_bq, c->d_bg,
-                                          (long long)tstep, S, g, c->d_gbar, st);
+                                          (long long)tstep, S, g, c->d_gbar, st, prog, prog_base,
+                                          max_ctas);
     if (e == cudaSuccess) return 0;
+    if (prog != nullptr) return fail("concurrent recursion: launch refused");
     if (e != cudaErrorCooperativeLaunchTooLarge) return fail(std::string("recursion: ") + cudaGetErrorString(e));
     cudaGetLastError();
   }

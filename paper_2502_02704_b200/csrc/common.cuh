@@ -29,6 +29,7 @@ enum ErrKind : int {
   kErrNonFinite = 2,    // BlowUpError(step)
   kErrUnphysical = 3,   // BlowUpError(step) from G's positivity guard
   kErrOvershoot = 4,    // CorrectionOvershootError(slice_index)
+  kErrSync = 5,         // internal: a pass gave up waiting for the concurrent recursion
 };
 constexpr ErrKey kNoError = ~0ull;
 __host__ __device__ constexpr ErrKey err_key(unsigned long long unit, unsigned long long step,
@@ -88,6 +89,10 @@ struct FSweepArgs {
   int bc;
   ErrKey* err;
   int step0;           // step number of level 0's output (BlowUpError keys)
+  // concurrent recursion (single propagations): wait until *prog >= need
+  // before the first table load (null: the tables are already complete)
+  const unsigned* prog;
+  unsigned need;
 };
 
 // Moment recursion (marginal.cu): five weighted sums of f over (v_y, v_z)

@@ -101,6 +101,20 @@ __global__ void __launch_bounds__(NTHR, MINB)
   };
   if (tid == ptid) {
     prefetch_tensormap(&fmap);
+    if (a.prog != nullptr) {
+      // the recursion runs concurrently (other SMs): wait for this pass's
+      // tables, then order the async-proxy (bulk copy) reads after them.
+      // Bounded (~5 s): a stalled recursion becomes an error, not a hang.
+      long long spins = 0;
+      while (ld_acquire_gpu(a.prog) < a.need) {
+        __nanosleep(256);
+        if (++spins > 20000000LL) {
+          atomicMin(a.err, err_key(0, a.step0, kErrSync));
+          break;
+        }
+      }
+      fence_proxy_async();
+    }
     for (int s = 0; s < ns && !prod.done(); ++s) issue_next();
   }
 
@@ -299,6 +313,12 @@ static cudaError_t launch_l(const CUtensorMap& map, const FSweepArgs& a, bool sy
       synth ? fsweep_kernel<V, LZ, K, NTHR, MINB, true, L> : fsweep_kernel<V, LZ, K, NTHR, MINB, false, L>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  if (a.prog != nullptr) {
+    // concurrent recursion: no programmatic early launch -- a second pass's
+    // CTAs waiting on the first would take the SMs reserved for the recursion
+    fn<<<grid, NTHR, smem, st>>>(map, a, ns);
+    return cudaGetLastError();
+  }
   return launch_pdl(fn, grid, NTHR, smem, st, map, a, ns);
 }
 

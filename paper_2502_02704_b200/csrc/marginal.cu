@@ -331,7 +331,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) mrec_multi_kernel(MargArgs 
                                                                         const double* q0, double* qa,
                                                                         double* qb, double* gsum,
                                                                         long long t_step, int S,
-                                                                        unsigned* bar) {
+                                                                        unsigned* bar, unsigned* prog,
+                                                                        unsigned prog_base) {
   extern __shared__ double sm[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x * kWarpsPerCta + wid;
@@ -354,6 +355,11 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) mrec_multi_kernel(MargArgs 
   }
   for (int s = 1; s <= S; ++s) {
     grid_barrier(bar, nblocks);
+    // steps < s are complete everywhere: publish for concurrent passes
+    if (prog != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+      __threadfence();
+      st_release_gpu(prog, prog_base + (unsigned)(s - 1));
+    }
     MargArgs ms = m;
     ms.min = s == 1 ? q0 : ((s - 1) & 1 ? qa : qb);
     ms.mout = (s & 1) ? qa : qb;
@@ -364,6 +370,13 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) mrec_multi_kernel(MargArgs 
     FinalArgs fs = f;
     fs.tab = const_cast<double*>(tab0) + (size_t)s * t_step;
     if (i < m.nx) mrec_cell<JPL, TRAP>(ms, fs, s, i, w, sm + (size_t)wid * m.nvx);
+  }
+  if (prog != nullptr) {
+    grid_barrier(bar, nblocks);
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+      __threadfence();
+      st_release_gpu(prog, prog_base + (unsigned)S);
+    }
   }
 }
 
@@ -460,11 +473,28 @@ cudaError_t launch_marg(const MargArgs& m0, const FinalArgs& f, double* gsum, in
   return launch_pdl_grid(k, grid, 32 * kWarpsPerCta, marg_smem_bytes(m.nvx, m.nvy, m.nvz, f.TL), st, m, f);
 }
 
+// CTAs of the one-launch recursion for nx cells and nwin windows, and how
+// many fit one SM (registers / shared memory).
+void marg_all_shape(int nx, int nvx, int nvy, int nvz, int TL, bool trap, int nwin, int* ctas,
+                    int* per_sm) {
+  const int jpl = (nvx + 31) / 32;
+  void (*k)(MargArgs, FinalArgs, const double*, double*, double*, double*, long long, int, unsigned*,
+            unsigned*, unsigned) = nullptr;
+#define PBGK_MK(J) (trap ? mrec_multi_kernel<J, true> : mrec_multi_kernel<J, false>)
+  k = jpl <= 1 ? PBGK_MK(1) : (jpl == 2 ? PBGK_MK(2) : (jpl == 3 ? PBGK_MK(3) : PBGK_MK(4)));
+#undef PBGK_MK
+  *ctas = ((nx + kWarpsPerCta - 1) / kWarpsPerCta) * nwin;
+  *per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k, 32 * kWarpsPerCta,
+                                                marg_smem_bytes(nvx, nvy, nvz, TL));
+}
+
 // All S steps in one cooperative launch when the grid is co-resident (see
 // mrec_multi_kernel); returns cudaErrorCooperativeLaunchTooLarge otherwise.
 cudaError_t launch_marg_all(const MargArgs& m0, const FinalArgs& f, const double* q0, double* qa,
                             double* qb, double* gsum, long long t_step, int S, int nwin,
-                            unsigned* bar, cudaStream_t st) {
+                            unsigned* bar, cudaStream_t st, unsigned* prog, unsigned prog_base,
+                            int max_ctas) {
   MargArgs m = m0;
   m.TL = f.TL;
   m.gxo = f.gxo;
@@ -474,7 +504,8 @@ cudaError_t launch_marg_all(const MargArgs& m0, const FinalArgs& f, const double
   m.cy = f.cy;
   m.cz = f.cz;
   const int jpl = (m.nvx + 31) / 32;
-  void (*k)(MargArgs, FinalArgs, const double*, double*, double*, double*, long long, int, unsigned*) = nullptr;
+  void (*k)(MargArgs, FinalArgs, const double*, double*, double*, double*, long long, int, unsigned*,
+            unsigned*, unsigned) = nullptr;
 #define PBGK_MK(J) (m.trap ? mrec_multi_kernel<J, true> : mrec_multi_kernel<J, false>)
   k = jpl <= 1 ? PBGK_MK(1) : (jpl == 2 ? PBGK_MK(2) : (jpl == 3 ? PBGK_MK(3) : PBGK_MK(4)));
 #undef PBGK_MK
@@ -486,6 +517,7 @@ cudaError_t launch_marg_all(const MargArgs& m0, const FinalArgs& f, const double
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, 32 * kWarpsPerCta, smem);
   if (e != cudaSuccess) return e;
   if ((long long)grid.x * grid.y > (long long)per * nsm) return cudaErrorCooperativeLaunchTooLarge;
+  if (max_ctas > 0 && (long long)grid.x * grid.y > max_ctas) return cudaErrorCooperativeLaunchTooLarge;
   e = cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), st);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
@@ -498,7 +530,7 @@ cudaError_t launch_marg_all(const MargArgs& m0, const FinalArgs& f, const double
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k, m, f, q0, qa, qb, gsum, t_step, S, bar);
+  return cudaLaunchKernelEx(&cfg, k, m, f, q0, qa, qb, gsum, t_step, S, bar, prog, prog_base);
 }
 
 }  // namespace pbgk

@@ -28,7 +28,7 @@ from .grid import bc_code
 # -1 = the per-shape choice)
 DEFAULT_FUSION = -1
 
-KIND_PROJECT, KIND_LIFT, KIND_NONFINITE, KIND_UNPHYSICAL, KIND_OVERSHOOT = range(5)
+KIND_PROJECT, KIND_LIFT, KIND_NONFINITE, KIND_UNPHYSICAL, KIND_OVERSHOOT, KIND_SYNC = range(6)
 
 _lock = threading.Lock()
 _ctx_cache: dict = {}
@@ -197,6 +197,9 @@ def raise_kinetic(code: int) -> None:
         raise DegenerateStateError("lift requires rho > 0 and theta > 0 in every cell")
     if kind == KIND_NONFINITE:
         raise BlowUpError("kinetic propagation lost finiteness at step %d" % step, step=step)
+    if kind == KIND_SYNC:
+        raise RuntimeError("internal: a multi-step pass timed out waiting for the concurrent "
+                           "recursion (step %d)" % step)
     raise RuntimeError("unexpected kinetic status key %#x" % code)
 
 

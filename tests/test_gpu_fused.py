@@ -223,3 +223,23 @@ def test_batched_windows_equal_one_step_path(levels, bc, monkeypatch):
     assert c1 == c0 and c0[3] != -1 and c0[2] == -1
     for w in (0, 1, 2, 4):
         assert moment_gap(_unpack(m1[w]), _unpack(m0[w])) <= 1e-13
+
+
+@pytest.mark.parametrize("bc", BCS)
+@pytest.mark.parametrize("levels", [2, 4])
+def test_long_propagation_concurrent_recursion(bc, levels):
+    # >= 8 L steps on a small grid: the recursion runs on a side stream on
+    # reserved SMs while the passes wait on its device progress word
+    g, mesh = _grids(24, (32, 32, 32), 8.0)
+    rng = np.random.default_rng(17)
+    f0 = O.lift(*random_moments(24, rng), mesh) * rng.uniform(0.9, 1.1, (24, 32, 32, 32))
+    t1 = 59.5 * O.fine_cap(mesh, 0.5, None)  # 60 steps
+    one, c0 = _from_f0(g, bc, f0, t1, 0)
+    got, c = _from_f0(g, bc, f0, t1, levels)
+    assert c == c0 == -1
+    assert rel_inf(got, one) <= 1e-12
+    U = random_moments(24, rng)
+    _, m0, k0, _ = _window(g, bc, U, t1, 0)
+    _, m1, k1, S = _window(g, bc, U, t1, levels)
+    assert S == 60 and k0 == k1 == -1
+    assert moment_gap(_unpack(m1), _unpack(m0)) <= 1e-12
