@@ -774,16 +774,15 @@ bool fused_ok(pbgk_ctx* c, bool field, bool batched = false) {
 // Levels per pass: the context's setting, or (auto, -1) the measured best
 // per shape (round 1, one B200): 4 for the 2-wide lane layouts (run as
 // 4-wide lanes, 255 registers), 3 for the 48-wide V = 6 one (its fourth level
-// spills heavily); a single propagation below ~4M
-// cells stays one-step (its recursion steps are latency-bound launches),
-// batched windows (pbgk_propagate_windows: one recursion launch per step for
-// the whole batch) always take the multi-step path (config 0: 1.7x).
+// spills heavily).  The same for single propagations and batched windows,
+// so a window gives bitwise the same moments either way (the pipelined
+// parareal schedule propagates windows one by one, the phased one batched).
 int fuse_levels(pbgk_ctx* c, bool batched) {
   static const int env = getenv("PBGK_FUSE") ? atoi(getenv("PBGK_FUSE")) : -2;
   int L = env >= -1 ? env : c->fuse;
   if (L < 0) {
-    const double cells = (double)c->g.nx * c->g.nvx * c->g.nvy * c->g.nvz;
-    L = (!batched && cells < 4.0e6) ? 0 : (kCfg[c->plan[0].cfg].V == 6 ? 3 : 4);
+    (void)batched;
+    L = kCfg[c->plan[0].cfg].V == 6 ? 3 : 4;
   }
   return std::min(L, 4);
 }

@@ -1,5 +1,7 @@
 """x-sharded fine propagator: slabs of x cells on
-ranks with per-step halo exchange must give BITWISE the single-GPU F.
+ranks with per-step halo exchange must give BITWISE the single-GPU F of the
+one-step path (the slabs' path; the multi-step path agrees with it to 1e-13,
+tests/test_gpu_fused.py).
 
 Multi-rank cases run 2-3 processes on cuda:0 over gloo: the halo exchange is
 host-staged and synchronous between steps, so no kernel waits on another
@@ -34,10 +36,10 @@ def _setup(nx=13, nv=(16, 8, 8), field=False, bc="periodic"):
 def _reference(g, kp, U, f0, bc, t1):
     from paper_2502_02704_b200 import runtime as rt
     from paper_2502_02704_b200.kinetic import propagate_window
-    f = P.propagate_kinetic(P.Distribution(f0), 0.0, t1, g, kp, bc).values
     ctx = rt.ctx_for(g, bc)
     mo = ctx.empty_moments()
     with ctx.fusion_levels(0):  # slabs run the one-step path; compare like with like
+        f = P.propagate_kinetic(P.Distribution(f0), 0.0, t1, g, kp, bc).values
         code = propagate_window(ctx, rt.to_device_moments(U, ctx.device), 0.0, t1, g, kp, None, mo)
     assert code == -1
     return np.asarray(f), mo.cpu().numpy()
@@ -148,7 +150,9 @@ def test_run_fine_mode_x_sharded_bitwise(tmp_path):
     path.write_text(CFG)
     cfg = P.parse_config(path)
     disc, kin, _, _ = prepare(cfg)
-    want = [np.stack([s.rho, s.theta]) for s in run_fine_mode(cfg, disc, kin)]
+    from paper_2502_02704_b200 import runtime as rt
+    with rt.ctx_for(disc.phase, disc.bc).fusion_levels(0):  # the slab path is one-step
+        want = [np.stack([s.rho, s.theta]) for s in run_fine_mode(cfg, disc, kin)]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
