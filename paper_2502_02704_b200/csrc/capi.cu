@@ -433,7 +433,7 @@ FinalArgs fin_args(pbgk_ctx* c, const Plan& p) {
 // One sweep over f (see sweep.cu).  `in` null => SYNTH from `tab`.
 int run_sweep(pbgk_ctx* c, int pid, bool field, const double* in, const double* tab, double* out,
               double dtdx, const double* E, double half_emax, double dtdv, int check_step,
-              cudaStream_t st) {
+              cudaStream_t st, int noreduce = 0) {
   const Plan& p = c->plan[pid];
   const CfgShape& s = kCfg[p.cfg];
   SweepArgs a = base_args(c, p);
@@ -448,6 +448,8 @@ int run_sweep(pbgk_ctx* c, int pid, bool field, const double* in, const double* 
   a.muscl = (c->x_scheme == 1 && dtdx != 0.0) ? 1 : 0;
   a.l2_keep = c->l2_keep;
   a.trap = c->quad;
+  a.noreduce = noreduce;
+  a.out_step = check_step;
   if (a.muscl && field) return fail("MUSCL x transport has no v_x field term (use the upwind scheme)");
   const bool synth = (in == nullptr);
   const CUtensorMap* map = tensor_map(c, synth ? nullptr : in, p.t, p.cfg);
@@ -712,7 +714,7 @@ namespace {
 bool fused_ok(pbgk_ctx* c, bool field, bool batched);
 int propagate_body_fused(pbgk_ctx* c, const double* f0, const double* mom0, double* f_out,
                          double* f_tmp, int write_final, double* mom_out, int S, const double* h_dts,
-                         double eps, double tau, cudaStream_t st);
+                         double eps, double tau, const double* E, double e_max, cudaStream_t st);
 
 // One propagation on the stream, failures atomicMin-ed into the current
 // error slot; no reset, no host synchronisation.
@@ -722,7 +724,7 @@ int propagate_body(pbgk_ctx* c, const double* f0, const double* mom0, double* f_
   const bool field = (E != nullptr && e_max > 0.0);
   if (S > 0 && fused_ok(c, field, false))
     return propagate_body_fused(c, f0, mom0, f_out, f_tmp, write_final, mom_out, S, h_dts, eps, tau,
-                                st);
+                                E, e_max, st);
   const int pid = field ? 1 : (c->x_scheme == 1 ? 2 : 0);
   const int W = S + (write_final ? 1 : 0);
   auto buf = [&](int w) { return ((W - w) % 2 == 0) ? f_out : f_tmp; };
@@ -760,7 +762,8 @@ namespace {
 int fuse_levels(pbgk_ctx* c, bool batched);
 
 bool fused_ok(pbgk_ctx* c, bool field, bool batched = false) {
-  if (fuse_levels(c, batched) < 1 || field || c->x_scheme != 0 || c->g.bc == 3) return false;
+  if (fuse_levels(c, batched) < 1 || c->x_scheme != 0 || c->g.bc == 3) return false;
+  (void)field;  // with the field term: one step per pass (see propagate_body_fused)
   if (!fsweep_has_cfg(c->plan[0].cfg)) return false;
   if (marg_smem_bytes(c->g.nvx, c->g.nvy, c->g.nvz, c->TL) > c->smem_optin) return false;
   if (!c->d_q0) {
@@ -846,8 +849,8 @@ int run_fsweep(pbgk_ctx* c, int n, const double* in, double* out, const double* 
 // last relax + projection is the reference-order marginal sweep of f*_S.
 int run_recursion(pbgk_ctx* c, int g, const double* q0, double* T, long long t_ws, int S,
                   const double* dts, const int* nst, ErrKey* errw, double eps, double tau,
-                  cudaStream_t st, unsigned* prog = nullptr, unsigned prog_base = 0,
-                  int max_ctas = 0);
+                  const double* E, double e_max, cudaStream_t st, unsigned* prog = nullptr,
+                  unsigned prog_base = 0, int max_ctas = 0);
 
 // A single propagation runs its recursion concurrently when its one-launch
 // grid fits <= 16 SMs (the passes lose at most 11 % of their SMs) and it has
@@ -877,8 +880,9 @@ bool concurrent_ok(pbgk_ctx* c, int S, int L) {
 
 int propagate_body_fused(pbgk_ctx* c, const double* f0, const double* mom0, double* f_out,
                          double* f_tmp, int write_final, double* mom_out, int S, const double* h_dts,
-                         double eps, double tau, cudaStream_t st) {
-  const int L = fuse_levels(c, false);
+                         double eps, double tau, const double* E, double e_max, cudaStream_t st) {
+  const bool field = (E != nullptr && e_max > 0.0);
+  const int L = field ? 1 : fuse_levels(c, false);
   const int P = (S + L - 1) / L;  // passes
   const int W = P + (write_final ? 1 : 0);
   auto buf = [&](int w) { return ((W - w) % 2 == 0) ? f_out : f_tmp; };
@@ -918,7 +922,7 @@ int propagate_body_fused(pbgk_ctx* c, const double* f0, const double* mom0, doub
   // per pass on its device progress word
   unsigned* prog = nullptr;
   unsigned base = 0;
-  if (concurrent_ok(c, S, L)) {
+  if (!field && concurrent_ok(c, S, L)) {
     prog = c->d_prog;
     base = c->prog_next;
     c->prog_next += (unsigned)S + 1;
@@ -926,11 +930,12 @@ int propagate_body_fused(pbgk_ctx* c, const double* f0, const double* mom0, doub
     CK(cudaStreamWaitEvent(c->st_side, c->ev_start, 0));
     int ctas = 0, per = 0;
     marg_all_shape(c->g.nx, c->g.nvx, c->g.nvy, c->g.nvz, c->TL, c->quad != 0, 1, &ctas, &per);
-    if (run_recursion(c, 1, q0, T, 0, S, c->d_bdts, nullptr, nullptr, eps, tau, c->st_side, prog, base,
+    if (run_recursion(c, 1, q0, T, 0, S, c->d_bdts, nullptr, nullptr, eps, tau, nullptr, 0.0, c->st_side,
+                      prog, base,
                       c->rec_reserve * per))
       return -1;
     CK(cudaEventRecord(c->ev_done, c->st_side));
-  } else if (run_recursion(c, 1, q0, T, 0, S, c->d_bdts, nullptr, nullptr, eps, tau, st)) {
+  } else if (run_recursion(c, 1, q0, T, 0, S, c->d_bdts, nullptr, nullptr, eps, tau, E, e_max, st)) {
     return -1;
   }
   int w = 0;
@@ -944,8 +949,15 @@ int propagate_body_fused(pbgk_ctx* c, const double* f0, const double* mom0, doub
       dtdx[l] = h_dts[s0 + l] / c->dx;
     }
     double* out = buf(++w);
-    if (run_fsweep(c, n, in, out, tabs, dtdx, s0 + 1, st, prog, base + (unsigned)(s0 + n - 1)))
+    if (field) {
+      // the v_x field term: the one-step sweep (its neighbour-row flux) on
+      // the recursion's tables, without the marginal partials
+      if (run_sweep(c, 1, true, in, tabs[0], out, dtdx[0], E, 0.5 * e_max, h_dts[s0] / c->dv[0], s0 + 1,
+                    st, 1))
+        return -1;
+    } else if (run_fsweep(c, n, in, out, tabs, dtdx, s0 + 1, st, prog, base + (unsigned)(s0 + n - 1))) {
       return -1;
+    }
     in = out;
     s0 += n;
   }
@@ -971,7 +983,8 @@ namespace {
 // grid is co-resident, else one launch per step.
 int run_recursion(pbgk_ctx* c, int g, const double* q0, double* T, long long t_ws, int S,
                   const double* dts, const int* nst, ErrKey* errw, double eps, double tau,
-                  cudaStream_t st, unsigned* prog, unsigned prog_base, int max_ctas) {
+                  const double* E, double e_max, cudaStream_t st, unsigned* prog, unsigned prog_base,
+                  int max_ctas) {
   const int nx = c->g.nx;
   const size_t tstep = (size_t)nx * c->TL;
   const size_t qw = (size_t)nx * marg_state_doubles(c->g.nvx);
@@ -988,6 +1001,9 @@ int run_recursion(pbgk_ctx* c, int g, const double* q0, double* T, long long t_w
   mg.nst = nst;
   mg.errw = errw;
   mg.dx = c->dx;
+  mg.E = (E != nullptr && e_max > 0.0) ? E : nullptr;
+  mg.half_emax = 0.5 * e_max;
+  mg.dvx = c->dv[0];
   FinalArgs f = fin_args(c, c->plan[0]);
   f.mode = kFinRelax;
   f.eps = eps;
@@ -1029,7 +1045,8 @@ int run_recursion(pbgk_ctx* c, int g, const double* q0, double* T, long long t_w
 // Groups bound the table memory (PBGK_BATCH_BYTES, default 2 GiB).
 int windows_fused(pbgk_ctx* c, int nwin, const double* mom_in, double* mom_out, double* f_a,
                   double* f_b, const int* h_nsteps, const double* h_dts, double eps, double tau,
-                  cudaStream_t st) {
+                  const double* E, double e_max, cudaStream_t st) {
+  const bool field = (E != nullptr && e_max > 0.0);
   const int nx = c->g.nx;
   const size_t m5 = (size_t)5 * nx;
   const size_t tstep = (size_t)nx * c->TL;  // one table set
@@ -1050,7 +1067,7 @@ int windows_fused(pbgk_ctx* c, int nwin, const double* mom_in, double* mom_out, 
       ensure_dev(c->d_bdts, c->bdts_cap, (size_t)std::max(Smax, 1) * G, st) ||
       ensure_dev(c->d_bnst, c->bnst_cap, (size_t)G, st))
     return -1;
-  const int L = fuse_levels(c, true);
+  const int L = field ? 1 : fuse_levels(c, true);
   std::vector<double> hd((size_t)std::max(Smax, 1) * G);
   std::vector<int> hn(G);
   for (int w0 = 0; w0 < nwin; w0 += G) {
@@ -1079,7 +1096,7 @@ int windows_fused(pbgk_ctx* c, int nwin, const double* mom_in, double* mom_out, 
     }
     // the batched recursion: steps 1..Smax for the group's windows
     if (run_recursion(c, g, nullptr, c->d_bt, (long long)t_ws, Smax, c->d_bdts, c->d_bnst,
-                      c->d_keys + w0, eps, tau, st))
+                      c->d_keys + w0, eps, tau, E, e_max, st))
       return -1;
     // each window's passes and its final projection from f
     for (int k = 0; k < g; ++k) {
@@ -1100,7 +1117,10 @@ int windows_fused(pbgk_ctx* c, int nwin, const double* mom_in, double* mom_out, 
           dtdx[l] = h_dts[off[w] + s0 + l] / c->dx;
         }
         double* out = buf(++wcount);
-        if (run_fsweep(c, n, in, out, tabs, dtdx, s0 + 1, st)) { c->err_slot = nullptr; return -1; }
+        const int rc = field ? run_sweep(c, 1, true, in, tabs[0], out, dtdx[0], E, 0.5 * e_max,
+                                         h_dts[off[w] + s0] / c->dv[0], s0 + 1, st, 1)
+                             : run_fsweep(c, n, in, out, tabs, dtdx, s0 + 1, st);
+        if (rc) { c->err_slot = nullptr; return -1; }
         in = out;
         s0 += n;
       }
@@ -1160,7 +1180,8 @@ int pbgk_propagate_windows(pbgk_ctx* c, int nwin, const double* mom_in, double* 
   const size_t m = (size_t)5 * c->g.nx;
   const bool field = (E != nullptr && e_max > 0.0);
   if (fused_ok(c, field, true)) {
-    if (windows_fused(c, nwin, mom_in, mom_out, f_a, f_b, h_nsteps, h_dts, eps, tau, st)) return -1;
+    if (windows_fused(c, nwin, mom_in, mom_out, f_a, f_b, h_nsteps, h_dts, eps, tau, E, e_max, st))
+      return -1;
     CK(cudaMemcpyAsync(c->h_keys, c->d_keys, (size_t)nwin * sizeof(ErrKey), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     for (int w = 0; w < nwin; ++w)

@@ -68,6 +68,9 @@ struct SweepArgs {
   int l2_keep;       // 1: f stores evict_last / loads evict_first (f ping-pong fits in L2)
   int trap;          // 1: trapezoidal velocity quadrature (end nodes weigh 1/2)
   int debug;         // development ablations (PBGK_DEBUG): 1 no reductions, 4 copy-through
+  int noreduce;      // multi-step path with the field term: no marginal partials (the
+                     // recursion gives the tables); f*'s finiteness flagged as step out_step
+  int out_step;
 };
 
 // Multi-step sweep (fsweep.cu): L consecutive fine steps per pass over f,
@@ -120,6 +123,8 @@ struct MargArgs {
   const int* nst;
   ErrKey* errw;
   double dx;
+  const double* E;     // v_x field per cell (null: none); half_emax = max|E| / 2
+  double half_emax, dvx;
 };
 
 enum FinalMode : int {

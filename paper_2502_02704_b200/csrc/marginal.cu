@@ -161,6 +161,26 @@ __device__ __forceinline__ void mrec_cell(const MargArgs& m, const FinalArgs& f,
       }
     }
   }
+  // v_x field term (ref/kinetic.py:114-123, linear in the v_x rows): the
+  // cell's relaxed rows go through warp-private shared memory first
+  const bool field = m.E != nullptr;
+  double cpf = 0.0, cmf = 0.0;
+  double* xs = mxs + nvx;  // [5][nvx]
+  if (field) {
+    const double hE = __dmul_rn(0.5, m.E[i]);
+    cpf = hE + m.half_emax;
+    cmf = hE - m.half_emax;
+#pragma unroll
+    for (int u = 0; u < JPL; ++u) {
+      const int jx = lane + 32 * u;
+      if (jx >= nvx) continue;
+      const double ac = (synth ? lq[1] : rq[1] * lq[1]) * gxc[u];
+#pragma unroll
+      for (int k = 0; k < 5; ++k)
+        xs[k * nvx + jx] = synth ? ac * G[1][k] : fma(ac, G[1][k], rq[1] * qc[k][u]);
+    }
+    __syncwarp();
+  }
   // the step: relax (cell and upwind neighbour), upwind transport, in the
   // one-step sweep's order; then the jx sums of the moments
   double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0, q4 = 0.0;  // sum_jx w_x Q_k
@@ -186,6 +206,13 @@ __device__ __forceinline__ void mrec_cell(const MargArgs& m, const FinalArgs& f,
       const double fl = __dmul_rn(c, x), pv = __dmul_rn(c, xn);
       const double d = down ? __dsub_rn(pv, fl) : __dsub_rn(fl, pv);
       o[k] = __dsub_rn(x, __dmul_rn(dtdx, d));
+      if (field) {
+        // Rusanov flux on interior v_x faces of the relaxed rows, zero at the
+        // cube faces: G(lo, hi) = cp lo + cm hi (the sweep's reassociation)
+        const double ghi = jx + 1 < nvx ? fma(cpf, x, cmf * xs[k * nvx + jx + 1]) : 0.0;
+        const double glo = jx > 0 ? fma(cpf, xs[k * nvx + jx - 1], cmf * x) : 0.0;
+        o[k] = fma(-(dt / m.dvx), ghi - glo, o[k]);  // the host's dt / dv_x
+      }
       qout[(size_t)i * QS + k * nvx + jx] = o[k];
       bad |= !isfinite(o[k]);
     }
@@ -297,7 +324,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) mrec_step_kernel(const Marg
   pdl_wait();  // tables, G sums and Q(f*_{s-1}) come from the preceding kernels
   pdl_trigger();
   if (i >= m.nx) return;
-  mrec_cell<JPL, TRAP>(m, f, f.step, i, blockIdx.y, sm + (size_t)wid * m.nvx);
+  mrec_cell<JPL, TRAP>(m, f, f.step, i, blockIdx.y, sm + (size_t)wid * 6 * m.nvx);
 }
 
 // Device-wide barrier of a co-resident (cooperatively launched) grid:
@@ -369,7 +396,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) mrec_multi_kernel(MargArgs 
     ms.dts = m.dts + (size_t)(s - 1) * gridDim.y;
     FinalArgs fs = f;
     fs.tab = const_cast<double*>(tab0) + (size_t)s * t_step;
-    if (i < m.nx) mrec_cell<JPL, TRAP>(ms, fs, s, i, w, sm + (size_t)wid * m.nvx);
+    if (i < m.nx) mrec_cell<JPL, TRAP>(ms, fs, s, i, w, sm + (size_t)wid * 6 * m.nvx);
   }
   if (prog != nullptr) {
     grid_barrier(bar, nblocks);
@@ -435,7 +462,7 @@ cudaError_t launch_q_from_f(const MargArgs& m, const double* f, cudaStream_t st)
 size_t marg_smem_bytes(int nvx, int nvy, int nvz, int TL) {
   (void)nvy; (void)nvz; (void)TL;
   if (nvx > 128) return ~(size_t)0;  // rows per lane bound (4)
-  return (size_t)kWarpsPerCta * nvx * sizeof(double);
+  return (size_t)kWarpsPerCta * 6 * nvx * sizeof(double);  // m_x + the field's relaxed rows
 }
 
 // Q (5 nvx per cell) lives in the caller's ping-pong buffers

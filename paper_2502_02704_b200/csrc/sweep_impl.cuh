@@ -392,6 +392,7 @@ __global__ void __launch_bounds__(NTHR, MINB)
   // MUSCL: the relaxed values of the two previous planes in march order
   double xm1[MUSCL ? K : 1][V], xm2[MUSCL ? K : 1][V];
 
+  double facc = 0.0;  // noreduce: sum of this thread's outputs (finiteness)
   ItemIter<LEAD, TRAIL> it;
   it.init(g0, g1, nx);
   int j = 0;        // item counter (LT/PZ parity)
@@ -730,7 +731,11 @@ __global__ void __launch_bounds__(NTHR, MINB)
         if (tg.down) body(F1{}, T1{}); else body(F1{}, F1{});
       }
 
-      if (out_plane && !(a.debug & 1)) {
+      if (out_plane && a.noreduce) {
+        // no partials: sum the plane's outputs for the finiteness flag
+#pragma unroll
+        for (int k = 0; k < K; ++k) facc += lp[k];
+      } else if (out_plane && !(a.debug & 1)) {
         // line totals -> LT, z partials -> PZ (double-buffered by item parity)
         double* LTb = LT + (j & 1) * lines;
         double* PZb = PZ + (j & 1) * NW * BZ;
@@ -762,7 +767,7 @@ __global__ void __launch_bounds__(NTHR, MINB)
       fence_proxy_async();
       issue_next();
     }
-    if (out_plane && i_out >= 0 && !(a.debug & 1)) {
+    if (out_plane && i_out >= 0 && !(a.debug & 1) && !a.noreduce) {
       // one output per thread, in equal contiguous chunks per warp so no warp
       // carries the serial sums alone (contiguous lanes keep smem reads
       // conflict-free)
@@ -833,6 +838,7 @@ __global__ void __launch_bounds__(NTHR, MINB)
       ph ^= 1u;
     }
   }
+  if (a.noreduce && !isfinite(facc)) atomicMin(a.err, err_key(0, a.out_step, kErrNonFinite));
 }
 
 // ---------------------------------------------------------------------------

@@ -243,3 +243,54 @@ def test_long_propagation_concurrent_recursion(bc, levels):
     _, m1, k1, S = _window(g, bc, U, t1, levels)
     assert S == 60 and k0 == k1 == -1
     assert moment_gap(_unpack(m1), _unpack(m0)) <= 1e-12
+
+
+def _window_field(g, bc, U, t1, levels, E):
+    kp = P.KineticParams(1e-2, force=E)
+    return _window(g, bc, U, t1, levels, kp=kp)
+
+
+@pytest.mark.parametrize("shape", [(9, (32, 32, 32), 8.0), (7, (48, 48, 48), 10.0), (5, (64, 64, 64), 8.0),
+                                   (10, (16, 8, 8), 6.0)],
+                         ids=lambda s: "x".join(map(str, (s[0],) + s[1])))
+@pytest.mark.parametrize("bc", BCS)
+def test_field_window_matches_oracle_and_one_step(shape, bc):
+    # the v_x field term: the recursion carries it, the passes are one-step
+    # sweeps on its tables without the marginal partials
+    nx, nv, vm = shape
+    g, mesh = _grids(nx, nv, vm)
+    E = 0.5 * np.sin(2 * np.pi * mesh.xc)
+    U = random_moments(nx, np.random.default_rng(nx + 5))
+    t1 = 6.5 * O.fine_cap(mesh, 0.5, E)
+    f, m, code, S = _window_field(g, bc, U, t1, -1, E)
+    f0, m0, c0, _ = _window_field(g, bc, U, t1, 0, E)
+    assert code == c0 == -1 and S == 7
+    want_f = O.fine_propagate(O.lift(*U, mesh), 0.0, t1, mesh, 1e-2, bc, E)
+    assert rel_inf(f, want_f) <= 1e-12
+    assert moment_gap(_unpack(m), O.project(want_f, mesh)) <= 1e-12
+    assert rel_inf(f, f0) <= 1e-13
+    assert moment_gap(_unpack(m), _unpack(m0)) <= 1e-13
+
+
+def test_field_batched_windows_and_nan_key():
+    from paper_2502_02704_b200.kinetic import propagate_windows
+    g, mesh = _grids(12, (32, 32, 32), 8.0)
+    E = 0.5 * np.sin(2 * np.pi * mesh.xc)
+    kp = P.KineticParams(1e-2, force=E)
+    ctx = rt.ctx_for(g, P.BoundaryKind.PERIODIC)
+    cap = stable_dt_kinetic(g, kp)
+    spans = [5.5 * cap, 3.0 * cap, 7.2 * cap]
+    rng = np.random.default_rng(21)
+    Us = [random_moments(12, rng) for _ in spans]
+    Us[1][0][7] = np.nan
+    mom_in = torch.stack([rt.to_device_moments(P.MomentField(*U), ctx.device) for U in Us])
+    res = {}
+    for L in (0, -1):
+        out = ctx.empty_moments(len(spans))
+        with ctx.fusion_levels(L):
+            codes = propagate_windows(ctx, mom_in, spans, g, kp, None, out)
+        res[L] = (out.cpu().numpy(), codes)
+    (m0, c0), (m1, c1) = res[0], res[-1]
+    assert c1 == c0 and c0[1] != -1
+    for w in (0, 2):
+        assert moment_gap(_unpack(m1[w]), _unpack(m0[w])) <= 1e-13
