@@ -299,6 +299,8 @@ def run_ours(args, w, world, rank, local):
                 "sweeps_timed": prof.sweeps,
                 "timed_in": "a second pass of %d step(s) with per-launch CUDA events on the "
                             "launching stream (kept out of the headline pass)" % prof_steps}
+    # the one-step design's bound: one f read + one f write per cell-update
+    roofline["one_step_roofline_cell_updates_per_s"] = hbm * 1e9 / 16.0
     if prof.msweeps > 0:
         roofline.update({
             "multistep_share_of_step": share(prof.msweep_ms),
@@ -314,6 +316,7 @@ def run_ours(args, w, world, rank, local):
     if not args.no_e2e:
         e2e = e2e_ours(args, w, P, phase, bc, disc, kinetic, fluid, U0, f_init, world, dev,
                        cell_updates, job_updates)
+    roofline["value_over_one_step_roofline"] = value / roofline["one_step_roofline_cell_updates_per_s"]
     return {"value": value, "ms_per_step": ms_per_step, "roofline": roofline, "clocks": clk,
             "gpu_launches": int(launches), "e2e": e2e}
 
