@@ -157,7 +157,7 @@ struct pbgk_ctx {
   int dev, nsm;
   size_t smem_optin, smem_per_sm;
   double* d_c[3] = {nullptr, nullptr, nullptr};
-  Plan plan[3];  // [0] upwind, [1] upwind + v_x field term, [2] MUSCL
+  Plan plan[4];  // [0] upwind, [1] upwind + v_x field term, [2] MUSCL, [3] multi-step sweep
   int TL, gxo, gyo, gzo;
   double* d_part = nullptr;
   size_t part_elems = 0;
@@ -228,7 +228,7 @@ struct ProfScope {
 };
 
 // Tile choice for one configuration of the sweep.
-bool make_plan(pbgk_ctx* c, bool field, bool muscl, Plan& out) {
+bool make_plan(pbgk_ctx* c, bool field, bool muscl, Plan& out, int only = -1) {
   const int nvx = c->g.nvx, nvy = c->g.nvy, nvz = c->g.nvz;
   const int nneg = nvx / 2;  // centres (j - (n-1)/2) dv are < 0 exactly for j < n/2
   const int npos = nvx - nneg;
@@ -251,6 +251,7 @@ bool make_plan(pbgk_ctx* c, bool field, bool muscl, Plan& out) {
   if (const char* force = getenv("PBGK_FORCE_CFG")) {  // development knob
     cands.assign(1, atoi(force));
   }
+  if (only >= 0) cands.assign(1, only);
   if (const char* force = getenv("PBGK_FORCE_FIELD_CFG"))  // development knob
     if (field) cands.assign(1, atoi(force));
   double best = 1e300;
@@ -533,8 +534,14 @@ int pbgk_ctx_create(const pbgk_grid_desc* g, pbgk_ctx** out) {
   c->gyo = c->gxo + g->nvx;
   c->gzo = (c->gyo + g->nvy + 1) & ~1;  // 16-byte aligned for vector reads
   c->TL = (c->gzo + g->nvz + 1) & ~1;
+  // the multi-step sweep: the upwind tiling, except 48-wide rows, which run
+  // as 16-wide boxes (its 2-wide lanes take four levels without spilling;
+  // the 48-wide V = 6 lanes spill at three)
   if (!make_plan(c, false, false, c->plan[0]) || !make_plan(c, true, false, c->plan[1]) ||
-      !make_plan(c, false, true, c->plan[2]))
+      !make_plan(c, false, true, c->plan[2]) ||
+      !make_plan(c, false, false, c->plan[3],
+                 getenv("PBGK_FPLAN_CFG") ? atoi(getenv("PBGK_FPLAN_CFG"))  // dev knob
+                                          : (kCfg[c->plan[0].cfg].V == 6 ? 3 : c->plan[0].cfg)))
     return bail(fail("no tiling fits this velocity grid"));
   for (int a = 0; a < 3; ++a) {
     std::vector<double> h(nv[a]);
@@ -764,7 +771,7 @@ int fuse_levels(pbgk_ctx* c, bool batched);
 bool fused_ok(pbgk_ctx* c, bool field, bool batched = false) {
   if (fuse_levels(c, batched) < 1 || c->x_scheme != 0 || c->g.bc == 3) return false;
   (void)field;  // with the field term: one step per pass (see propagate_body_fused)
-  if (!fsweep_has_cfg(c->plan[0].cfg)) return false;
+  if (!fsweep_has_cfg(c->plan[3].cfg)) return false;
   if (marg_smem_bytes(c->g.nvx, c->g.nvy, c->g.nvz, c->TL) > c->smem_optin) return false;
   if (!c->d_q0) {
     const size_t ms = (size_t)c->g.nx * marg_state_doubles(c->g.nvx) * sizeof(double);
@@ -785,7 +792,7 @@ int fuse_levels(pbgk_ctx* c, bool batched) {
   int L = env >= -1 ? env : c->fuse;
   if (L < 0) {
     (void)batched;
-    L = kCfg[c->plan[0].cfg].V == 6 ? 3 : 4;
+    L = kCfg[c->plan[3].cfg].V == 6 ? 3 : 4;
   }
   return std::min(L, 4);
 }
@@ -794,7 +801,7 @@ int fuse_levels(pbgk_ctx* c, bool batched) {
 int run_fsweep(pbgk_ctx* c, int n, const double* in, double* out, const double* const* tabs,
                const double* dtdx, int step0, cudaStream_t st, const unsigned* prog = nullptr,
                unsigned need = 0) {
-  const Plan& p = c->plan[0];
+  const Plan& p = c->plan[3];
   const CfgShape& s = kCfg[p.cfg];
   FSweepArgs a{};
   a.nx = c->g.nx;
