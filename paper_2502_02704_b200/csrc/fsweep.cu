@@ -43,6 +43,12 @@ __global__ void __launch_bounds__(NTHR, MINB)
 #ifndef PBGK_FS_PR
 #define PBGK_FS_PR 2
 #endif
+#ifndef PBGK_FS_LK
+#define PBGK_FS_LK 0
+#endif
+#ifndef PBGK_FS_DECOUPLE
+#define PBGK_FS_DECOUPLE 0
+#endif
   constexpr int PR = PBGK_FS_PR;  // planes per round of the steady path (needs ns >= 2 PR)
   extern __shared__ __align__(128) unsigned char smem[];
 
@@ -66,6 +72,9 @@ __global__ void __launch_bounds__(NTHR, MINB)
   for (int j = tid; j < a.nvx; j += NTHR) SCX[j] = a.cx[j];
   if (tid == 0) {
     for (int s = 0; s < ns; ++s) mbar_init(&bars[s], 1);
+#if PBGK_FS_DECOUPLE
+    for (int s = 0; s < ns; ++s) mbar_init(&bars[ns + s], NTHR / 32);  // stage empty: one arrive per warp
+#endif
     fence_mbar_init();
   }
   pdl_wait();
@@ -210,58 +219,73 @@ __global__ void __launch_bounds__(NTHR, MINB)
         auto body = [&](auto fast_c, auto down_c) {
           constexpr bool FAST = decltype(fast_c)::value;
           constexpr bool DOWNT = decltype(down_c)::value;
+          // level l of line k: relax, transport, carry, store at the last level
+          auto step = [&](int k, int l, double (&x)[V]) {
+            const double c = cvx[k];
+            const double* ST = reinterpret_cast<const double*>(
+                reinterpret_cast<const unsigned char*>(SF) + box_bytes + l * tab_bytes);
+            const double gxy = ST[gxi[k]] * ST[gyi[k]];
+            // relax R of this level (level 0 of a synthesising pass: f_0 = L(U))
+            if (l == 0 && SYNTH) {
+#pragma unroll
+              for (int v = 0; v < V; ++v) x[v] = (gxy * gz[0][v]) * lss[0];
+            } else {
+              double raw[V];
+              if (l == 0) {
+                lds_lane<V, LZ>(SF + soff[k], raw);
+              } else {
+#pragma unroll
+                for (int v = 0; v < V; ++v) raw[v] = x[v];
+              }
+              const double w = rr[l] * (lss[l] * gxy);
+#pragma unroll
+              for (int v = 0; v < V; ++v) x[v] = fma(w, gz[l][v], rr[l] * raw[v]);
+            }
+            // upwind transport of ref/kinetic.py:110-112 with a = (dt/dx) c_x:
+            // up (c >= 0)  f* = x - a (x - x_{i-1}) = (1 - a) x + q_{i-1}
+            // down (c < 0) f* = x - a (x_{i+1} - x) = (1 + a) x - q_{i+1}
+            // with q = a x carried per level (2 fp64 ops per element instead of
+            // 4; a few ulps from the reference's order, see the header)
+            const double av = a.dtdx[l] * c;
+            const double keep = DOWNT ? 1.0 + av : 1.0 - av;
+            double q[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) q[v] = av * x[v];
+            if (FAST || l < depth) {
+#pragma unroll
+              for (int v = 0; v < V; ++v) x[v] = DOWNT ? fma(keep, x[v], -prev[l][k][v]) : fma(keep, x[v], prev[l][k][v]);
+            }
+#pragma unroll
+            for (int v = 0; v < V; ++v) prev[l][k][v] = q[v];
+            if (FAST || depth == L) {
+              const bool ok = FAST || ((vmask >> k) & 1u);
+              double sl = 0.0;
+#pragma unroll
+              for (int v = 0; v < V; ++v) sl += (FAST || (ok && ((zmask >> v) & 1u))) ? x[v] : 0.0;
+              acc[l] += sl;
+              if (l == L - 1 && (FAST || ok)) store_line<V, LZ, FAST>(gdst + goff[k], x, zmask);
+            }
+          };
+#if PBGK_FS_LK
+          // levels outer, lines inner: the K lines' chains interleave per level
+          double x[K][V];
+#pragma unroll
+          for (int l = 0; l < L; ++l) {
+            if (!FAST && l > depth) break;
+#pragma unroll
+            for (int k = 0; k < K; ++k) step(k, l, x[k]);
+          }
+#else
 #pragma unroll
           for (int k = 0; k < K; ++k) {
-            const double c = cvx[k];
             double x[V];
 #pragma unroll
             for (int l = 0; l < L; ++l) {
               if (!FAST && l > depth) break;
-              const double* ST = reinterpret_cast<const double*>(
-                  reinterpret_cast<const unsigned char*>(SF) + box_bytes + l * tab_bytes);
-              const double gxy = ST[gxi[k]] * ST[gyi[k]];
-              // relax R of this level (level 0 of a synthesising pass: f_0 = L(U))
-              if (l == 0 && SYNTH) {
-#pragma unroll
-                for (int v = 0; v < V; ++v) x[v] = (gxy * gz[0][v]) * lss[0];
-              } else {
-                double raw[V];
-                if (l == 0) {
-                  lds_lane<V, LZ>(SF + soff[k], raw);
-                } else {
-#pragma unroll
-                  for (int v = 0; v < V; ++v) raw[v] = x[v];
-                }
-                const double w = rr[l] * (lss[l] * gxy);
-#pragma unroll
-                for (int v = 0; v < V; ++v) x[v] = fma(w, gz[l][v], rr[l] * raw[v]);
-              }
-              // upwind transport of ref/kinetic.py:110-112 with a = (dt/dx) c_x:
-              // up (c >= 0)  f* = x - a (x - x_{i-1}) = (1 - a) x + q_{i-1}
-              // down (c < 0) f* = x - a (x_{i+1} - x) = (1 + a) x - q_{i+1}
-              // with q = a x carried per level (2 fp64 ops per element instead of
-              // 4; a few ulps from the reference's order, see the header)
-              const double av = a.dtdx[l] * c;
-              const double keep = DOWNT ? 1.0 + av : 1.0 - av;
-              double q[V];
-#pragma unroll
-              for (int v = 0; v < V; ++v) q[v] = av * x[v];
-              if (FAST || l < depth) {
-#pragma unroll
-                for (int v = 0; v < V; ++v) x[v] = DOWNT ? fma(keep, x[v], -prev[l][k][v]) : fma(keep, x[v], prev[l][k][v]);
-              }
-#pragma unroll
-              for (int v = 0; v < V; ++v) prev[l][k][v] = q[v];
-              if (FAST || depth == L) {
-                const bool ok = FAST || ((vmask >> k) & 1u);
-                double sl = 0.0;
-#pragma unroll
-                for (int v = 0; v < V; ++v) sl += (FAST || (ok && ((zmask >> v) & 1u))) ? x[v] : 0.0;
-                acc[l] += sl;
-                if (l == L - 1 && (FAST || ok)) store_line<V, LZ, FAST>(gdst + goff[k], x, zmask);
-              }
+              step(k, l, x);
             }
           }
+#endif
         };
         using T1 = std::integral_constant<bool, true>;
         using F1 = std::integral_constant<bool, false>;
@@ -271,6 +295,19 @@ __global__ void __launch_bounds__(NTHR, MINB)
           if (tg.down) body(F1{}, T1{}); else body(F1{}, F1{});
         }
       }
+#if PBGK_FS_DECOUPLE
+      // no CTA barrier: every warp marks the stage consumed; the producer
+      // refills it once all warps have (warps run up to ns items apart)
+      (void)sync;
+      (void)nfree;
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&bars[ns + stg]);
+      if (tid == ptid && !prod.done()) {
+        mbar_wait(&bars[ns + stg], ph);
+        fence_proxy_async();
+        issue_next();
+      }
+#else
       if (sync) {
         __syncthreads();  // the round's stages are consumed: the producer may refill them
         if (tid == ptid) {
@@ -278,6 +315,7 @@ __global__ void __launch_bounds__(NTHR, MINB)
           for (int q = 0; q < nfree && !prod.done(); ++q) issue_next();
         }
       }
+#endif
       if (++stg == ns) {
         stg = 0;
         ph ^= 1u;
@@ -303,7 +341,7 @@ size_t fsweep_smem_bytes(const FSweepArgs& a, int V, int LZ, bool synth, int L, 
   const int BZ = LZ * V;
   const size_t box = synth ? 0 : (size_t)a.t.A * a.t.By * BZ * 8;
   const size_t stage = (box + (size_t)L * a.TL * 8 + 127) & ~(size_t)127;
-  return (size_t)ns * stage + (size_t)((a.nvx + 1) & ~1) * 8 + (size_t)ns * 8 + 16;
+  return (size_t)ns * stage + (size_t)((a.nvx + 1) & ~1) * 8 + (size_t)2 * ns * 8 + 16;
 }
 
 template <int V, int LZ, int K, int NTHR, int MINB, int L>
