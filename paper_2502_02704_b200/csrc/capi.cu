@@ -82,6 +82,13 @@ int ensure_dev(T*& p, size_t& cap, size_t n, cudaStream_t st) {
   return 0;
 }
 
+// bytes of per-step relax tables the multi-step path may hold (a group of
+// batched windows, or one long propagation)
+double batch_budget() {
+  static const double b = getenv("PBGK_BATCH_BYTES") ? atof(getenv("PBGK_BATCH_BYTES")) : 2147483648.0;
+  return b;
+}
+
 // compile-time tile shapes of sweep.cu (index = cfg id)
 struct CfgShape {
   int V, LZ, K, NTHR;
@@ -730,7 +737,10 @@ int propagate_body(pbgk_ctx* c, const double* f0, const double* mom0, double* f_
                    int write_final, double* mom_out, int S, const double* h_dts, double eps,
                    double tau, const double* E, double e_max, cudaStream_t st) {
   const bool field = (E != nullptr && e_max > 0.0);
-  if (S > 0 && fused_ok(c, field, false))
+  // (the multi-step path keeps the tables of every step: a very long single
+  // propagation whose tables exceed PBGK_BATCH_BYTES stays one-step)
+  if (S > 0 && fused_ok(c, field, false) &&
+      8.0 * (S + 1) * (double)c->g.nx * c->TL <= batch_budget())
     return propagate_body_fused(c, f0, mom0, f_out, f_tmp, write_final, mom_out, S, h_dts, eps, tau,
                                 E, e_max, st);
   const int pid = field ? 1 : (c->x_scheme == 1 ? 2 : 0);
@@ -1065,7 +1075,7 @@ int windows_fused(pbgk_ctx* c, int nwin, const double* mom_in, double* mom_out, 
     Smax = std::max(Smax, h_nsteps[w]);
     off[w + 1] = off[w] + h_nsteps[w];
   }
-  static const double budget = getenv("PBGK_BATCH_BYTES") ? atof(getenv("PBGK_BATCH_BYTES")) : 2147483648.0;
+  const double budget = batch_budget();
   const double per_w = 8.0 * ((double)(Smax + 1) * tstep + 2.0 * qw + 12.0 * nx);
   const int G = std::max(1, std::min(nwin, (int)(budget / per_w)));
   const size_t t_ws = (size_t)(Smax + 1) * tstep;
@@ -1187,7 +1197,9 @@ int pbgk_propagate_windows(pbgk_ctx* c, int nwin, const double* mom_in, double* 
   CK(cudaMemsetAsync(c->d_keys, 0xFF, (size_t)nwin * sizeof(ErrKey), st));  // kNoError = ~0
   const size_t m = (size_t)5 * c->g.nx;
   const bool field = (E != nullptr && e_max > 0.0);
-  if (fused_ok(c, field, true)) {
+  int smax = 0;
+  for (int w = 0; w < nwin; ++w) smax = std::max(smax, h_nsteps[w]);
+  if (fused_ok(c, field, true) && 8.0 * (smax + 1) * (double)c->g.nx * c->TL <= batch_budget()) {
     if (windows_fused(c, nwin, mom_in, mom_out, f_a, f_b, h_nsteps, h_dts, eps, tau, E, e_max, st))
       return -1;
     CK(cudaMemcpyAsync(c->h_keys, c->d_keys, (size_t)nwin * sizeof(ErrKey), cudaMemcpyDeviceToHost, st));
