@@ -33,7 +33,8 @@
 // fallback for odd shapes), and three extensions: MUSCL (minmod x transport,
 // output one plane behind the loads, 2 lead / 1 trail halo items per run),
 // TRAP (trapezoidal velocity quadrature: end nodes weigh 1/2 in the
-// reductions).  bc 3 (runtime) is a slab of an x-sharded domain whose halo
+// reductions), NORED (the multi-step path's field passes: no marginal
+// partials, a finiteness sum instead; field variants only).  bc 3 (runtime) is a slab of an x-sharded domain whose halo
 // planes sit in the padded buffers.
 #pragma once
 #include <cuda.h>
@@ -255,7 +256,7 @@ __device__ __forceinline__ void store_line(double* d, const double (&o)[V], unsi
 }
 
 template <int V, int LZ, int K, int NTHR, int MINB, bool SYNTH, bool FIELD, bool TMA, bool MUSCL,
-          bool TRAP>
+          bool TRAP, bool NORED = false>
 __global__ void __launch_bounds__(NTHR, MINB)
     sweep_kernel(const __grid_constant__ CUtensorMap fmap, const SweepArgs a, int ns) {
   static_assert(!(TRAP && FIELD), "the field term is defined on midpoint velocity cells only");
@@ -731,7 +732,7 @@ __global__ void __launch_bounds__(NTHR, MINB)
         if (tg.down) body(F1{}, T1{}); else body(F1{}, F1{});
       }
 
-      if (out_plane && a.noreduce) {
+      if (NORED && out_plane) {
         // no partials: sum the plane's outputs for the finiteness flag
 #pragma unroll
         for (int k = 0; k < K; ++k) facc += lp[k];
@@ -767,7 +768,7 @@ __global__ void __launch_bounds__(NTHR, MINB)
       fence_proxy_async();
       issue_next();
     }
-    if (out_plane && i_out >= 0 && !(a.debug & 1) && !a.noreduce) {
+    if (!NORED && out_plane && i_out >= 0 && !(a.debug & 1)) {
       // one output per thread, in equal contiguous chunks per warp so no warp
       // carries the serial sums alone (contiguous lanes keep smem reads
       // conflict-free)
@@ -838,7 +839,7 @@ __global__ void __launch_bounds__(NTHR, MINB)
       ph ^= 1u;
     }
   }
-  if (a.noreduce && !isfinite(facc)) atomicMin(a.err, err_key(0, a.out_step, kErrNonFinite));
+  if (NORED && !isfinite(facc)) atomicMin(a.err, err_key(0, a.out_step, kErrNonFinite));
 }
 
 // ---------------------------------------------------------------------------
@@ -871,9 +872,14 @@ static cudaError_t launch_cfg(const CUtensorMap& map, const SweepArgs& a, bool s
                  : sweep_kernel<V, LZ, K, NTHR, MINB, false, false, TMA, true, false>;
   } else {
     if (field) {
-      if constexpr ((MODES & 4) != 0)
-        fn = synth ? sweep_kernel<V, LZ, K, NTHR, MINB, true, true, TMA, false, false>
-                   : sweep_kernel<V, LZ, K, NTHR, MINB, false, true, TMA, false, false>;
+      if constexpr ((MODES & 4) != 0) {
+        if (a.noreduce)
+          fn = synth ? sweep_kernel<V, LZ, K, NTHR, MINB, true, true, TMA, false, false, true>
+                     : sweep_kernel<V, LZ, K, NTHR, MINB, false, true, TMA, false, false, true>;
+        else
+          fn = synth ? sweep_kernel<V, LZ, K, NTHR, MINB, true, true, TMA, false, false>
+                     : sweep_kernel<V, LZ, K, NTHR, MINB, false, true, TMA, false, false>;
+      }
     } else {
       if constexpr ((MODES & 1) != 0)
         fn = synth ? sweep_kernel<V, LZ, K, NTHR, MINB, true, false, TMA, false, false>
