@@ -726,7 +726,7 @@ int pbgk_check_finite(pbgk_ctx* c, const double* f, int step, void* stream, long
 }
 
 namespace {
-bool fused_ok(pbgk_ctx* c, bool field, bool batched);
+bool fused_ok(pbgk_ctx* c, bool field);
 int propagate_body_fused(pbgk_ctx* c, const double* f0, const double* mom0, double* f_out,
                          double* f_tmp, int write_final, double* mom_out, int S, const double* h_dts,
                          double eps, double tau, const double* E, double e_max, cudaStream_t st);
@@ -739,7 +739,7 @@ int propagate_body(pbgk_ctx* c, const double* f0, const double* mom0, double* f_
   const bool field = (E != nullptr && e_max > 0.0);
   // (the multi-step path keeps the tables of every step: a very long single
   // propagation whose tables exceed PBGK_BATCH_BYTES stays one-step)
-  if (S > 0 && fused_ok(c, field, false) &&
+  if (S > 0 && fused_ok(c, field) &&
       8.0 * (S + 1) * (double)c->g.nx * c->TL <= batch_budget())
     return propagate_body_fused(c, f0, mom0, f_out, f_tmp, write_final, mom_out, S, h_dts, eps, tau,
                                 E, e_max, st);
@@ -774,14 +774,15 @@ int propagate_body(pbgk_ctx* c, const double* f0, const double* mom0, double* f_
 }  // namespace
 
 namespace {
-// Multi-step path usable on this context for an upwind propagation without
-// the v_x field term (the marginal recursion is closed for it; MUSCL's
-// limiter is not linear, slabs exchange halos per step).
-int fuse_levels(pbgk_ctx* c, bool batched);
+// Multi-step path usable on this context: the upwind scheme (the moment
+// recursion is closed for it, with or without the v_x field term -- the field
+// runs one step per pass, see propagate_body_fused; MUSCL's limiter is not
+// linear), bc 0..2 (slabs exchange halos per step).
+int fuse_levels(pbgk_ctx* c);
 
-bool fused_ok(pbgk_ctx* c, bool field, bool batched = false) {
-  if (fuse_levels(c, batched) < 1 || c->x_scheme != 0 || c->g.bc == 3) return false;
-  (void)field;  // with the field term: one step per pass (see propagate_body_fused)
+bool fused_ok(pbgk_ctx* c, bool field) {
+  (void)field;
+  if (fuse_levels(c) < 1 || c->x_scheme != 0 || c->g.bc == 3) return false;
   if (!fsweep_has_cfg(c->plan[3].cfg)) return false;
   if (marg_smem_bytes(c->g.nvx, c->g.nvy, c->g.nvz, c->TL) > c->smem_optin) return false;
   if (!c->d_q0) {
@@ -798,11 +799,10 @@ bool fused_ok(pbgk_ctx* c, bool field, bool batched = false) {
 // spills heavily).  The same for single propagations and batched windows,
 // so a window gives bitwise the same moments either way (the pipelined
 // parareal schedule propagates windows one by one, the phased one batched).
-int fuse_levels(pbgk_ctx* c, bool batched) {
+int fuse_levels(pbgk_ctx* c) {
   static const int env = getenv("PBGK_FUSE") ? atoi(getenv("PBGK_FUSE")) : -2;
   int L = env >= -1 ? env : c->fuse;
   if (L < 0) {
-    (void)batched;
     L = kCfg[c->plan[3].cfg].V == 6 ? 3 : 4;
   }
   return std::min(L, 4);
@@ -900,7 +900,7 @@ int propagate_body_fused(pbgk_ctx* c, const double* f0, const double* mom0, doub
                          double* f_tmp, int write_final, double* mom_out, int S, const double* h_dts,
                          double eps, double tau, const double* E, double e_max, cudaStream_t st) {
   const bool field = (E != nullptr && e_max > 0.0);
-  const int L = field ? 1 : fuse_levels(c, false);
+  const int L = field ? 1 : fuse_levels(c);
   const int P = (S + L - 1) / L;  // passes
   const int W = P + (write_final ? 1 : 0);
   auto buf = [&](int w) { return ((W - w) % 2 == 0) ? f_out : f_tmp; };
@@ -1085,7 +1085,7 @@ int windows_fused(pbgk_ctx* c, int nwin, const double* mom_in, double* mom_out, 
       ensure_dev(c->d_bdts, c->bdts_cap, (size_t)std::max(Smax, 1) * G, st) ||
       ensure_dev(c->d_bnst, c->bnst_cap, (size_t)G, st))
     return -1;
-  const int L = field ? 1 : fuse_levels(c, true);
+  const int L = field ? 1 : fuse_levels(c);
   std::vector<double> hd((size_t)std::max(Smax, 1) * G);
   std::vector<int> hn(G);
   for (int w0 = 0; w0 < nwin; w0 += G) {
@@ -1199,7 +1199,7 @@ int pbgk_propagate_windows(pbgk_ctx* c, int nwin, const double* mom_in, double* 
   const bool field = (E != nullptr && e_max > 0.0);
   int smax = 0;
   for (int w = 0; w < nwin; ++w) smax = std::max(smax, h_nsteps[w]);
-  if (fused_ok(c, field, true) && 8.0 * (smax + 1) * (double)c->g.nx * c->TL <= batch_budget()) {
+  if (fused_ok(c, field) && 8.0 * (smax + 1) * (double)c->g.nx * c->TL <= batch_budget()) {
     if (windows_fused(c, nwin, mom_in, mom_out, f_a, f_b, h_nsteps, h_dts, eps, tau, E, e_max, st))
       return -1;
     CK(cudaMemcpyAsync(c->h_keys, c->d_keys, (size_t)nwin * sizeof(ErrKey), cudaMemcpyDeviceToHost, st));
