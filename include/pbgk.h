@@ -30,6 +30,9 @@
  *      kind 4  correction overshoot             -> CorrectionOvershootError(unit)
  *      kind 5  internal: a multi-step pass timed out waiting for the
  *              concurrent relax-table recursion  -> RuntimeError
+ *      (kind 6 is internal to the library: "non-finite within a multi-step
+ *      pass"; pbgk_propagate / pbgk_propagate_windows re-run that
+ *      propagation on the one-step path and return its exact key)
  *    Keys are min-reduced: lowest unit, then earliest step, then the
  *    reference's raise order within a step (ref/moments.py:102-104,
  *    ref/lifting.py:44-45, ref/kinetic.py:157-159, ref/fluid.py:117-122).

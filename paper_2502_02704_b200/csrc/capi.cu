@@ -184,6 +184,7 @@ struct pbgk_ctx {
   // multi-step path (fsweep.cu + marginal.cu): levels per pass (0 = off,
   // -1 = the per-shape default of fuse_levels); Q of a given f0
   int fuse = -1;
+  int one_step = 0;  // force the one-step path (exact re-run after a kind-6 status)
   double* d_q0 = nullptr;
   // the recursion's per-(window, step) tables, per-window state ping-pong,
   // G sums, per-step dt and step counts (multi-step path)
@@ -739,7 +740,7 @@ int propagate_body(pbgk_ctx* c, const double* f0, const double* mom0, double* f_
   const bool field = (E != nullptr && e_max > 0.0);
   // (the multi-step path keeps the tables of every step: a very long single
   // propagation whose tables exceed PBGK_BATCH_BYTES stays one-step)
-  if (S > 0 && fused_ok(c, field) &&
+  if (S > 0 && !c->one_step && fused_ok(c, field) &&
       8.0 * (S + 1) * (double)c->g.nx * c->TL <= batch_budget())
     return propagate_body_fused(c, f0, mom0, f_out, f_tmp, write_final, mom_out, S, h_dts, eps, tau,
                                 E, e_max, st);
@@ -1170,7 +1171,20 @@ int pbgk_propagate(pbgk_ctx* c, const double* f0, const double* mom0, double* f_
   if (propagate_body(c, f0, mom0, f_out, f_tmp, write_final, mom_out, nsteps, h_dts, eps, tau, E,
                      e_max, st))
     return -1;
-  return fetch_err(c, st, h_code);
+  long long code = -1;
+  if (fetch_err(c, st, &code)) return -1;
+  if (code >= 0 && (int)(code & 0xFF) == kErrNonFiniteMulti) {
+    // non-finite somewhere in a multi-step pass: the one-step path finds the step
+    if (reset_err(c, st)) return -1;
+    c->one_step = 1;
+    const int rc = propagate_body(c, f0, mom0, f_out, f_tmp, write_final, mom_out, nsteps, h_dts, eps,
+                                  tau, E, e_max, st);
+    c->one_step = 0;
+    if (rc) return -1;
+    if (fetch_err(c, st, &code)) return -1;
+  }
+  if (h_code) *h_code = code;
+  return 0;
 }
 
 int pbgk_propagate_windows(pbgk_ctx* c, int nwin, const double* mom_in, double* mom_out,
@@ -1204,6 +1218,23 @@ int pbgk_propagate_windows(pbgk_ctx* c, int nwin, const double* mom_in, double* 
       return -1;
     CK(cudaMemcpyAsync(c->h_keys, c->d_keys, (size_t)nwin * sizeof(ErrKey), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    // a window whose first failure is "non-finite somewhere in a multi-step
+    // pass" is re-run on the one-step path for its exact key
+    std::vector<size_t> offs(nwin + 1, 0);
+    for (int w = 0; w < nwin; ++w) offs[w + 1] = offs[w] + h_nsteps[w];
+    for (int w = 0; w < nwin; ++w) {
+      if (c->h_keys[w] == kNoError || (int)(c->h_keys[w] & 0xFF) != kErrNonFiniteMulti) continue;
+      CK(cudaMemsetAsync(c->d_keys + w, 0xFF, sizeof(ErrKey), st));
+      c->err_slot = c->d_keys + w;
+      c->one_step = 1;
+      const int rc = propagate_body(c, nullptr, mom_in + w * m, f_a, f_b, 0, mom_out + w * m,
+                                    h_nsteps[w], h_dts + offs[w], eps, tau, E, e_max, st);
+      c->one_step = 0;
+      c->err_slot = nullptr;
+      if (rc) return -1;
+      CK(cudaMemcpyAsync(c->h_keys + w, c->d_keys + w, sizeof(ErrKey), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    }
     for (int w = 0; w < nwin; ++w)
       h_codes[w] = (c->h_keys[w] == kNoError) ? -1 : (long long)c->h_keys[w];
     return 0;

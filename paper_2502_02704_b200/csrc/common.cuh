@@ -30,6 +30,8 @@ enum ErrKind : int {
   kErrUnphysical = 3,   // BlowUpError(step) from G's positivity guard
   kErrOvershoot = 4,    // CorrectionOvershootError(slice_index)
   kErrSync = 5,         // internal: a pass gave up waiting for the concurrent recursion
+  kErrNonFiniteMulti = 6,  // internal: non-finite f somewhere in a multi-step pass that starts at
+                           // `step`; the host re-runs that propagation on the one-step path
 };
 constexpr ErrKey kNoError = ~0ull;
 __host__ __device__ constexpr ErrKey err_key(unsigned long long unit, unsigned long long step,

@@ -21,9 +21,13 @@
 // within a few ulps of ref/kinetic.py:110-112; the multi-step path is held to
 // the oracle at 1e-12 (tests/test_gpu_fused.py) like every multi-step run.
 //
-// Finiteness (ref/kinetic.py:157-159): each thread sums its stored values of
-// every level; a non-finite sum flags BlowUpError at that level's step (same
-// documented corner as the marginal check: finite values whose sum overflows).
+// Finiteness (ref/kinetic.py:157-159): each thread sums its stored (last
+// level) values; a non-finite value at any level stays non-finite in the same
+// element through the later levels, so a non-finite sum means "some step of
+// this pass" -- status kind 6, on which the host re-runs the propagation on
+// the one-step path to report the exact BlowUpError(step) (same documented
+// corner as the marginal check: finite values whose sum overflows).  Per-level
+// sums (PBGK_FS_LASTACC=0) cost 9 % on config 4.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -48,6 +52,9 @@ __global__ void __launch_bounds__(NTHR, MINB)
 #endif
 #ifndef PBGK_FS_DECOUPLE
 #define PBGK_FS_DECOUPLE 0
+#endif
+#ifndef PBGK_FS_LASTACC
+#define PBGK_FS_LASTACC 1
 #endif
   constexpr int PR = PBGK_FS_PR;  // planes per round of the steady path (needs ns >= 2 PR)
   extern __shared__ __align__(128) unsigned char smem[];
@@ -257,7 +264,7 @@ __global__ void __launch_bounds__(NTHR, MINB)
             }
 #pragma unroll
             for (int v = 0; v < V; ++v) prev[l][k][v] = q[v];
-            if (FAST || depth == L) {
+            if ((FAST || depth == L) && (!PBGK_FS_LASTACC || l == L - 1)) {
               const bool ok = FAST || ((vmask >> k) & 1u);
               double sl = 0.0;
 #pragma unroll
@@ -332,9 +339,17 @@ __global__ void __launch_bounds__(NTHR, MINB)
     }
     for (; p < p1; ++p) item(tg.down ? nx - 1 - p : p, L, true, 1);
   }
+#if PBGK_FS_LASTACC
+  // only the stored level is summed (a non-finite value at any level stays
+  // non-finite in the same element through the later ones): the failing step
+  // is one of this pass's, and the host finds it on the one-step path
+  if (!isfinite(acc[L - 1]))
+    atomicMin(a.err, err_key(0, a.step0, L == 1 ? kErrNonFinite : kErrNonFiniteMulti));
+#else
 #pragma unroll
   for (int l = 0; l < L; ++l)
     if (!isfinite(acc[l])) atomicMin(a.err, err_key(0, a.step0 + l, kErrNonFinite));
+#endif
 }
 
 size_t fsweep_smem_bytes(const FSweepArgs& a, int V, int LZ, bool synth, int L, int ns) {

@@ -28,7 +28,7 @@ from .grid import bc_code
 # -1 = the per-shape choice)
 DEFAULT_FUSION = -1
 
-KIND_PROJECT, KIND_LIFT, KIND_NONFINITE, KIND_UNPHYSICAL, KIND_OVERSHOOT, KIND_SYNC = range(6)
+KIND_PROJECT, KIND_LIFT, KIND_NONFINITE, KIND_UNPHYSICAL, KIND_OVERSHOOT, KIND_SYNC, KIND_NONFINITE_MULTI = range(7)
 
 _lock = threading.Lock()
 _ctx_cache: dict = {}
