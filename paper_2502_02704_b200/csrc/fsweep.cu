@@ -56,6 +56,9 @@ __global__ void __launch_bounds__(NTHR, MINB)
 #ifndef PBGK_FS_LASTACC
 #define PBGK_FS_LASTACC 1
 #endif
+#ifndef PBGK_FS_LATE
+#define PBGK_FS_LATE 1
+#endif
   constexpr int PR = PBGK_FS_PR;  // planes per round of the steady path (needs ns >= 2 PR)
   extern __shared__ __align__(128) unsigned char smem[];
 
@@ -208,9 +211,15 @@ __global__ void __launch_bounds__(NTHR, MINB)
       } else {
         double* gdst = (depth == L) ? a.fout + (size_t)i * a.plane : nullptr;
       // per level: relax factors and this lane's g_z values of the plane's row
-        double rr[L], lss[L], gz[L][V];
+#if PBGK_FS_LATE
+        // (late variant: each (line, level) step reads its table factors)
+        constexpr int LP = 1;
+#else
+        constexpr int LP = L;
+#endif
+        double rr[LP], lss[LP], gz[LP][V];
 #pragma unroll
-        for (int l = 0; l < L; ++l) {
+        for (int l = 0; l < LP && !PBGK_FS_LATE; ++l) {
           const double* ST = reinterpret_cast<const double*>(
               reinterpret_cast<const unsigned char*>(SF) + box_bytes + l * tab_bytes);
           rr[l] = ST[0];
@@ -232,10 +241,27 @@ __global__ void __launch_bounds__(NTHR, MINB)
             const double* ST = reinterpret_cast<const double*>(
                 reinterpret_cast<const unsigned char*>(SF) + box_bytes + l * tab_bytes);
             const double gxy = ST[gxi[k]] * ST[gyi[k]];
+#if PBGK_FS_LATE
+            double rl = ST[0], lsl = ST[1], gzl[V];
+            if (FAST || zmask == (1u << V) - 1) {
+              lds_lane<V, LZ>(ST + a.gzo + tg.z0 + zpos<V, LZ>(lz, 0), gzl);
+            } else {
+#pragma unroll
+              for (int v = 0; v < V; ++v)
+                gzl[v] = ((zmask >> v) & 1u) ? ST[a.gzo + tg.z0 + zpos<V, LZ>(lz, v)] : 0.0;
+            }
+#define PBGK_RR rl
+#define PBGK_LS lsl
+#define PBGK_GZ(v) gzl[v]
+#else
+#define PBGK_RR rr[l]
+#define PBGK_LS lss[l]
+#define PBGK_GZ(v) gz[l][v]
+#endif
             // relax R of this level (level 0 of a synthesising pass: f_0 = L(U))
             if (l == 0 && SYNTH) {
 #pragma unroll
-              for (int v = 0; v < V; ++v) x[v] = (gxy * gz[0][v]) * lss[0];
+              for (int v = 0; v < V; ++v) x[v] = (gxy * PBGK_GZ(v)) * PBGK_LS;
             } else {
               double raw[V];
               if (l == 0) {
@@ -244,10 +270,13 @@ __global__ void __launch_bounds__(NTHR, MINB)
 #pragma unroll
                 for (int v = 0; v < V; ++v) raw[v] = x[v];
               }
-              const double w = rr[l] * (lss[l] * gxy);
+              const double w = PBGK_RR * (PBGK_LS * gxy);
 #pragma unroll
-              for (int v = 0; v < V; ++v) x[v] = fma(w, gz[l][v], rr[l] * raw[v]);
+              for (int v = 0; v < V; ++v) x[v] = fma(w, PBGK_GZ(v), PBGK_RR * raw[v]);
             }
+#undef PBGK_RR
+#undef PBGK_LS
+#undef PBGK_GZ
             // upwind transport of ref/kinetic.py:110-112 with a = (dt/dx) c_x:
             // up (c >= 0)  f* = x - a (x - x_{i-1}) = (1 - a) x + q_{i-1}
             // down (c < 0) f* = x - a (x_{i+1} - x) = (1 + a) x - q_{i+1}
