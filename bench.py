@@ -427,8 +427,9 @@ def main():
         line = {"metric": metric, "value": v, "unit": "cell-updates/s", "impl": "reference",
                 "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": float(np.mean([s["seconds"] for s in samples])) * 1e3,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic", "config": cfg_json,
+                "higher_is_better": True,
+                "scaling": "strong" if (w.mode == "parareal" or args.xshard) else "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg_json,
                 "cpu_baseline": {"value": v, "unit": "cell-updates/s", "cores": samples[0]["cores"],
                                  "kind": "port", "sample": samples[0]["sample"]},
                 "e2e": {"value": v, "unit": "cell-updates/s", "h2d_bytes_per_step": 0,
