@@ -533,13 +533,17 @@ __global__ void __launch_bounds__(NTHR, MINB)
       // marginal partials.  FAST: full tile, transport on, output plane
       // written (every step but the first/last of a window) -- no masks and no
       // per-line tests; otherwise the general masked path.  DOWNT: c_x < 0
-      // (the upwind neighbour is plane i+1, already in `prev`).
-      auto body = [&](auto fast_c, auto down_c) {
-        constexpr bool FAST = decltype(fast_c)::value;
+      // (the upwind neighbour is plane i+1, already in `prev`).  RO: full
+      // tile, no transport and no store (a window's final relax + projection
+      // of f*_S, read-only): FAST's unmasked partials without the update.
+      auto body = [&](auto fast_c, auto down_c, auto ro_c) {
+        constexpr bool RO = decltype(ro_c)::value;
+        constexpr bool FAST = decltype(fast_c)::value && !RO;
+        constexpr bool FULL = FAST || RO;
         constexpr bool DOWNT = decltype(down_c)::value;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-          const bool ok = FAST || ((vmask >> k) & 1u);
+          const bool ok = FULL || ((vmask >> k) & 1u);
           const double gxy = ST[gxi[k]] * ST[gyi[k]];
           const double c = cvx[k];
           double x[V];
@@ -555,11 +559,13 @@ __global__ void __launch_bounds__(NTHR, MINB)
             for (int v = 0; v < V; ++v) x[v] = fma(w, gz[v], r * raw[v]);
           }
           double fl[V];  // this plane's upwind flux c f_pre
+          if constexpr (!RO) {
 #pragma unroll
-          for (int v = 0; v < V; ++v) fl[v] = __dmul_rn(c, x[v]);
-          if (FAST || out_plane) {
+            for (int v = 0; v < V; ++v) fl[v] = __dmul_rn(c, x[v]);
+          }
+          if (FULL || out_plane) {
             double o[V];
-            if (FAST || transport) {
+            if (!RO && (FAST || transport)) {
 #pragma unroll
               for (int v = 0; v < V; ++v) {
                 // f* = f - (dt/dx)(F_{i+1/2} - F_{i-1/2}); upward: F_{i+1/2} = c f_i,
@@ -629,16 +635,18 @@ __global__ void __launch_bounds__(NTHR, MINB)
             double sl = 0.0;
 #pragma unroll
             for (int v = 0; v < V; ++v) {
-              const double m = FAST ? o[v] : ((ok && ((zmask >> v) & 1u)) ? o[v] : 0.0);
+              const double m = FULL ? o[v] : ((ok && ((zmask >> v) & 1u)) ? o[v] : 0.0);
               accum(m, k, v, sl);
             }
             lp[k] = sl;
-            if (FAST || (gdst != nullptr && ok)) {
+            if (!RO && (FAST || (gdst != nullptr && ok))) {
               store_line<V, LZ, FAST>(gdst + goff[k], o, zmask, a.l2_keep != 0, pol_keep);
             }
           }
+          if constexpr (!RO) {
 #pragma unroll
-          for (int v = 0; v < V; ++v) prev[k][v] = fl[v];
+            for (int v = 0; v < V; ++v) prev[k][v] = fl[v];
+          }
         }
       };
       // MUSCL (minmod) x transport, one plane behind the loads: item q
@@ -727,9 +735,18 @@ __global__ void __launch_bounds__(NTHR, MINB)
           }
         }
       } else if (full && out_plane && transport && gdst != nullptr) {
-        if (tg.down) body(T1{}, T1{}); else body(T1{}, F1{});
+        if (tg.down) body(T1{}, T1{}, F1{}); else body(T1{}, F1{}, F1{});
       } else {
-        if (tg.down) body(F1{}, T1{}); else body(F1{}, F1{});
+        bool ro = false;
+        if constexpr (!FIELD && !SYNTH && !MUSCL) {
+          if (full && out_plane && !transport && gdst == nullptr) {
+            body(F1{}, F1{}, T1{});
+            ro = true;
+          }
+        }
+        if (!ro) {
+          if (tg.down) body(F1{}, T1{}, F1{}); else body(F1{}, F1{}, F1{});
+        }
       }
 
       if (NORED && out_plane) {
