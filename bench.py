@@ -321,6 +321,12 @@ def run_ours(args, w, world, rank, local):
             "gpu_launches": int(launches), "e2e": e2e}
 
 
+# untimed end-to-end calls before the timed ones: the first two reach the
+# pinned host allocator's steady state (a returned f stays alive while the
+# next call allocates its own, so two blocks get cudaHostAlloc'd)
+E2E_WARM = 2
+
+
 def e2e_ours(args, w, P, phase, bc, disc, kinetic, fluid, U0, f_init, world, dev, cell_updates,
              job_updates):
     """Same metric through the public API with host buffers (copies timed)."""
@@ -334,7 +340,7 @@ def e2e_ours(args, w, P, phase, bc, disc, kinetic, fluid, U0, f_init, world, dev
         h2d = 5 * nx * 8 + (nx * 8 if w.force() is not None else 0)
         d2h = (3 * w.n_g + 2) * 5 * nx * 8
         times = []
-        for _ in range(reps + 1):
+        for _ in range(E2E_WARM + reps):
             if world > 1:
                 dist.barrier()
             torch.cuda.synchronize(dev)
@@ -342,7 +348,7 @@ def e2e_ours(args, w, P, phase, bc, disc, kinetic, fluid, U0, f_init, world, dev
             traj, rec = P.run_parareal(U0h, cfg, disc, kinetic, fluid)
             torch.cuda.synchronize(dev)
             times.append(time.perf_counter() - tic)
-        sec = float(np.mean(times[1:]))
+        sec = float(np.mean(times[E2E_WARM:]))
     elif args.xshard:
         # the sharded public path: each rank uploads its slab, propagates with
         # the halo exchange, downloads its slab
@@ -353,7 +359,7 @@ def e2e_ours(args, w, P, phase, bc, disc, kinetic, fluid, U0, f_init, world, dev
         out_h = torch.empty_like(pinned).pin_memory()
         h2d = d2h = host.nbytes
         times = []
-        for _ in range(reps + 1):
+        for _ in range(E2E_WARM + reps):
             if world > 1:
                 dist.barrier()
             torch.cuda.synchronize(dev)
@@ -363,20 +369,20 @@ def e2e_ours(args, w, P, phase, bc, disc, kinetic, fluid, U0, f_init, world, dev
             out_h.copy_(fl)
             torch.cuda.synchronize(dev)
             times.append(time.perf_counter() - tic)
-        sec = float(np.mean(times[1:]))
+        sec = float(np.mean(times[E2E_WARM:]))
     else:
         host = f_init.values.copy()
         pinned = torch.from_numpy(host).pin_memory()
         h2d = d2h = host.nbytes
         times = []
-        for _ in range(reps + 1):
+        for _ in range(E2E_WARM + reps):
             torch.cuda.synchronize(dev)
             tic = time.perf_counter()
             f = P.Distribution(pinned)
             g = P.propagate_kinetic(f, 0.0, w.t_final, phase, kinetic, bc)
             out = g.values
             times.append(time.perf_counter() - tic)
-        sec = float(np.mean(times[1:]))
+        sec = float(np.mean(times[E2E_WARM:]))
     t = torch.tensor([sec], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
