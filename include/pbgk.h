@@ -164,16 +164,31 @@ int pbgk_ctx_set_quadrature(pbgk_ctx* ctx, int quadrature);
  * MUSCL has no v_x field term: sweeps with E != 0 fail on a MUSCL context. */
 int pbgk_set_x_scheme(pbgk_ctx* ctx, int scheme);
 
-/* Multi-step path of pbgk_propagate / pbgk_propagate_windows for windows
- * that start from moments (mom0, f0 == NULL) with the upwind scheme, no v_x
- * field term and bc 0..2: `levels` (1..4) fine steps per pass over f, their
- * relax tables from the 2-D marginal recursion (the marginals of f over v_z
- * and over v_y evolve in closed form under the upwind x transport and the
- * separable BGK relaxation), so f is read and written once per `levels`
- * steps.  Same results as the one-step path to rounding (the marginal sums
- * and the transport are associated differently); 0 = always the one-step
- * path; -1 (default) = the measured best per shape. */
+/* Multi-step path of pbgk_propagate / pbgk_propagate_windows (upwind
+ * scheme, bc 0..2): the relax tables R_s of every step come first from the
+ * moment recursion -- per x cell and v_x row five weighted sums of f over
+ * (v_y, v_z) (the marginal m_x, the folded first moments and the second
+ * moments in v_y and v_z) evolve in closed form under the upwind x transport,
+ * the v_x field flux and the separable BGK relaxation -- then f is read and
+ * written once per `levels` fine steps.  With the v_x field term a pass is
+ * one step (the one-step field sweep on the recursion's tables).  Same
+ * results as the one-step path to rounding (sums and transport associated
+ * differently); 0 = always the one-step path; -1 (default) = the measured
+ * best.  `levels` (1..4) applies to the round-1 pass kernel (fsweep.cu);
+ * pbgk_set_msweep selects the round-2 kernel and its level count. */
 int pbgk_set_fusion(pbgk_ctx* ctx, int levels);
+
+/* Round-2 pass kernel of the multi-step path (msweep.cu, default on): up to
+ * 8 fine steps per pass over f, warp-specialised (one warp issues the TMA box
+ * and the table-row slices), 3 fp64 instructions per element and level, and
+ * the window's final relax + projection folded into its last pass (partial
+ * records of P(f_S), no store of f_S unless the caller wants it).  Needs
+ * v_x / v_y / v_z counts divisible by 16 / 8 / 16 (else the round-1 kernel
+ * runs).  on = 0 selects the round-1 kernel; levels = 0 (auto: 8), 4 or 8.
+ * Replaces the numpy loop of ref/kinetic.py:152-160 like pbgk_propagate. */
+int pbgk_set_msweep(pbgk_ctx* ctx, int on, int levels);
+/* Levels per pass the round-2 kernel runs on this context (0: not used). */
+int pbgk_msweep_levels(pbgk_ctx* ctx);
 
 /* ---- x-sharded fine propagation (slabs) --------------------------------- */
 /* A context created with bc = 3 is one x-slab of a larger domain (one rank

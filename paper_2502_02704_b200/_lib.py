@@ -48,6 +48,8 @@ PROTOTYPES = {
     "pbgk_set_grid_reserve": (c_int, [_P, _I]),
     "pbgk_set_x_scheme": (c_int, [_P, _I]),
     "pbgk_set_fusion": (c_int, [_P, _I]),
+    "pbgk_set_msweep": (c_int, [_P, _I, _I]),
+    "pbgk_msweep_levels": (c_int, [_P]),
     "pbgk_table_len": (c_int, [_P]),
     "pbgk_propagate_windows": (c_int, [_P, _I, _P, _P, _P, _P, POINTER(c_int), POINTER(c_double),
                                        _D, _D, _P, _D, _P, POINTER(c_longlong)]),

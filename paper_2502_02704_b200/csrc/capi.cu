@@ -29,6 +29,10 @@ cudaError_t launch_fsweep(int cfg_id, const CUtensorMap& map, const FSweepArgs& 
 size_t fsweep_smem_bytes(const FSweepArgs& a, int V, int LZ, bool synth, int L, int ns);
 bool fsweep_has_cfg(int cfg_id);
 int fsweep_ctas_per_sm(int L);
+cudaError_t launch_msweep(int K, int L, int mode, const CUtensorMap& map, const MSweepArgs& a, int grid,
+                          int ns, size_t smem, cudaStream_t st);
+size_t msweep_smem_bytes(int K, int L, int mode, int nvx, int ns);
+int msweep_tiling(int nvx, int nvy, int nvz, int K, Tiling* t);
 cudaError_t launch_marg(const MargArgs& m, const FinalArgs& f, double* gsum, int s, int nwin,
                         cudaStream_t st);
 size_t marg_state_doubles(int nvx);
@@ -202,6 +206,16 @@ struct pbgk_ctx {
   unsigned* d_prog = nullptr;
   unsigned prog_next = 1;
   int rec_reserve = 0;  // SMs the passes leave to a concurrent recursion (0: serial)
+  int no_concurrent = 0;  // serial recursion (re-run after a pass gave up waiting, status kind 5)
+  // round-2 multi-step sweep (msweep.cu): on/off (pbgk_set_msweep), levels
+  // per pass (0 = auto: 8), its tilings for K = 1 / 2 lines per thread (NT =
+  // 0: the velocity grid does not tile) and its partial records (the
+  // window's final projection)
+  int ms = 1;
+  int ms_levels = 0;
+  Tiling ms_t[2] = {};
+  double* d_mpart = nullptr;
+  size_t mpart_cap = 0;
 };
 
 namespace {
@@ -552,6 +566,8 @@ int pbgk_ctx_create(const pbgk_grid_desc* g, pbgk_ctx** out) {
                  getenv("PBGK_FPLAN_CFG") ? atoi(getenv("PBGK_FPLAN_CFG"))  // dev knob
                                           : (g->nvz % 16 == 0 ? 3 : c->plan[0].cfg)))
     return bail(fail("no tiling fits this velocity grid"));
+  for (int k = 1; k <= 2; ++k)
+    if (!msweep_tiling(g->nvx, g->nvy, g->nvz, k, &c->ms_t[k - 1])) c->ms_t[k - 1].NT = 0;
   for (int a = 0; a < 3; ++a) {
     std::vector<double> h(nv[a]);
     for (int j = 0; j < nv[a]; ++j) h[j] = ((double)j - (nv[a] - 1) / 2.0) * c->dv[a];  // ref/grid.py:100-103
@@ -595,6 +611,7 @@ void pbgk_ctx_destroy(pbgk_ctx* c) {
   cudaFree(c->d_bnst);
   cudaFree(c->d_gbar);
   cudaFree(c->d_prog);
+  cudaFree(c->d_mpart);
   if (c->ev_start) cudaEventDestroy(c->ev_start);
   if (c->ev_done) cudaEventDestroy(c->ev_done);
   if (c->st_side) cudaStreamDestroy(c->st_side);
@@ -855,10 +872,127 @@ int run_fsweep(pbgk_ctx* c, int n, const double* in, double* out, const double* 
   const size_t smem = fsweep_smem_bytes(a, s.V, s.LZ, synth, n, ns);
   const double fbytes = 8.0 * (double)a.plane * a.nx;
   ProfScope ps(c, st, 2, (synth ? 0.0 : fbytes) + fbytes, n);
+  // persistent grid minus the CTA slots left to side-stream work AND the SMs
+  // of a concurrent recursion (both can be active at once)
   int grid = (int)std::min<long long>(a.total, (long long)c->nsm * per_sm);
-  if (c->slot_reserve > 0) grid = std::max(1, std::min(grid, c->nsm * per_sm - c->slot_reserve));
-  if (prog != nullptr) grid = std::max(1, std::min(grid, (c->nsm - c->rec_reserve) * per_sm));
+  const int reserve = c->slot_reserve + (prog != nullptr ? c->rec_reserve * per_sm : 0);
+  grid = std::max(1, std::min(grid, c->nsm * per_sm - reserve));
   CK(launch_fsweep(p.cfg, *map, a, synth, n, grid, ns, smem, st));
+  return 0;
+}
+
+// Round-2 multi-step sweep (msweep.cu): levels per pass and lines per thread
+// (8 levels on 1 line x 4 v_z per thread, 4 levels on 2 lines), or 0 when the
+// context's velocity grid / quadrature / scheme does not run on it.
+int ms_levels(pbgk_ctx* c) {
+  static const int env = getenv("PBGK_MS") ? atoi(getenv("PBGK_MS")) : -1;  // dev A/B knob
+  if (!(env >= 0 ? env : c->ms) || c->quad != 0 || c->x_scheme != 0 || c->g.bc == 3) return 0;
+  if (c->fuse > 0) return 0;  // an explicit pbgk_set_fusion level count selects the round-1 kernel
+  static const int envl = getenv("PBGK_MS_L") ? atoi(getenv("PBGK_MS_L")) : 0;  // dev A/B knob
+  const int L = envl ? envl : (c->ms_levels ? c->ms_levels : 8);
+  const int K = L > 4 ? 1 : 2;
+  if (c->ms_t[K - 1].NT == 0) return 0;
+  return L;
+}
+
+// One msweep pass: n <= L fine steps (steps step0 .. step0+n-1) from `in`
+// (null: SYNTH, level 0 lifts tabs[0]), writing the last level to `out`
+// (may be null); FINAL (`tabR` non-null): R_S applied, partial records of
+// P(f_S) into d_mpart.
+int run_msweep(pbgk_ctx* c, int L, const double* in, double* out, const double* const* tabs,
+               const double* tabR, const double* dtdx, int n, int step0, cudaStream_t st,
+               const unsigned* prog = nullptr, unsigned need = 0) {
+  const int K = L > 4 ? 1 : 2;
+  const Tiling& t = c->ms_t[K - 1];
+  MSweepArgs a{};
+  a.nx = c->g.nx;
+  a.nvx = c->g.nvx;
+  a.nvy = c->g.nvy;
+  a.nvz = c->g.nvz;
+  a.plane = (long long)c->g.nvx * c->g.nvy * c->g.nvz;
+  a.t = t;
+  a.total = (long long)t.NT * c->g.nx;
+  a.fout = out;
+  for (int l = 0; l < kMaxL; ++l) {
+    a.tab[l] = tabs[std::min(l, n - 1)];  // levels >= n are skipped (their copies land unused)
+    a.dtdx[l] = l < n ? dtdx[l] : 0.0;
+  }
+  a.tabR = tabR;
+  a.nlev = n;
+  a.TL = c->TL;
+  a.gxo = c->gxo;
+  a.gyo = c->gyo;
+  a.gzo = c->gzo;
+  a.cx = c->d_c[0];
+  a.bc = c->g.bc;
+  a.err = c->err_slot ? c->err_slot : c->d_err;
+  a.step0 = step0;
+  a.prog = prog;
+  a.need = need;
+  static const int dbg = getenv("PBGK_MS_DBG") ? atoi(getenv("PBGK_MS_DBG")) : 0;  // dev ablations
+  a.dbg = dbg;
+  const int mode = (in == nullptr ? 1 : 0) | (tabR != nullptr ? 2 : 0);
+  if (tabR) {
+    if (ensure_dev(c->d_mpart, c->mpart_cap, (size_t)c->g.nx * t.NT * t.PS, st)) return -1;
+    a.part = c->d_mpart;
+  }
+  const CUtensorMap* map = tensor_map(c, in, t, 3);
+  if (!map) return fail("tensor map: " + g_last_error);
+  static const int ns_env = getenv("PBGK_MS_NS") ? atoi(getenv("PBGK_MS_NS")) : 0;  // dev knob
+  int ns = ns_env > 0 ? ns_env : 12;
+  while (ns > 2 && msweep_smem_bytes(K, L, mode, c->g.nvx, ns) > c->smem_optin) --ns;
+  const size_t smem = msweep_smem_bytes(K, L, mode, c->g.nvx, ns);
+  if (smem > c->smem_optin) return fail("msweep: ring does not fit");
+  const double fbytes = 8.0 * (double)a.plane * a.nx;
+  ProfScope ps(c, st, 2, (in ? fbytes : 0.0) + (out ? fbytes : 0.0), n);
+  // one CTA per SM, minus the slots left to side-stream work and the SMs of a
+  // concurrent recursion
+  int grid = (int)std::min<long long>(a.total, (long long)c->nsm);
+  int reserve = c->slot_reserve + (prog != nullptr ? c->rec_reserve : 0);
+  grid = std::max(1, std::min(grid, c->nsm - reserve));
+  CK(launch_msweep(K, L, mode, *map, a, grid, ns, smem, st));
+  return 0;
+}
+
+// The passes of one window on the msweep path, then its projection: tables
+// T[s] (R_s; T[0] the lift or identity rows), S steps with h_dts; f0 null:
+// the first pass synthesises L(mom); f_S = R_S(f*_S) is stored to f_out only
+// when write_final; mom_out (may be null) gets P(f_S).
+int ms_window(pbgk_ctx* c, int L, const double* f0, double* f_out, double* f_tmp, int write_final,
+              double* mom_out, const double* T, int S, const double* h_dts, cudaStream_t st,
+              const unsigned* prog = nullptr, unsigned base = 0) {
+  const size_t tstep = (size_t)c->g.nx * c->TL;
+  const int P = (S + L - 1) / L;
+  const int W = P - 1 + (write_final ? 1 : 0);
+  auto buf = [&](int w) { return ((W - w) % 2 == 0) ? f_out : f_tmp; };
+  const double* in = f0;
+  int wcount = 0;
+  for (int s0 = 0; s0 < S;) {
+    const int n = std::min(L, S - s0);
+    const bool last = s0 + n == S;
+    const double* tabs[kMaxL];
+    double dtdx[kMaxL];
+    for (int l = 0; l < n; ++l) {
+      tabs[l] = T + (size_t)(s0 + l) * tstep;
+      dtdx[l] = h_dts[s0 + l] / c->dx;
+    }
+    double* out = (!last || write_final) ? buf(++wcount) : nullptr;
+    if (run_msweep(c, L, in, out, tabs, last ? T + (size_t)S * tstep : nullptr, dtdx, n, s0 + 1, st, prog,
+                   base + (unsigned)(last ? S : s0 + n - 1)))
+      return -1;
+    in = out;
+    s0 += n;
+  }
+  if (mom_out) {
+    FinalArgs f = fin_args(c, c->plan[0]);
+    f.t = c->ms_t[L > 4 ? 0 : 1];
+    f.part = c->d_mpart;
+    f.mode = kFinProject;
+    f.mom_out = mom_out;
+    f.step = S + 1;
+    ProfScope ps(c, st, 1, 0.0);
+    CK(launch_finalize(f, st));
+  }
   return 0;
 }
 
@@ -941,7 +1075,7 @@ int propagate_body_fused(pbgk_ctx* c, const double* f0, const double* mom0, doub
   // per pass on its device progress word
   unsigned* prog = nullptr;
   unsigned base = 0;
-  if (!field && concurrent_ok(c, S, L)) {
+  if (!field && !c->no_concurrent && concurrent_ok(c, S, L)) {
     prog = c->d_prog;
     base = c->prog_next;
     c->prog_next += (unsigned)S + 1;
@@ -957,36 +1091,44 @@ int propagate_body_fused(pbgk_ctx* c, const double* f0, const double* mom0, doub
   } else if (run_recursion(c, 1, q0, T, 0, S, c->d_bdts, nullptr, nullptr, eps, tau, E, e_max, st)) {
     return -1;
   }
-  int w = 0;
-  const double* in = f0;
-  for (int s0 = 0; s0 < S;) {
-    const int n = std::min(L, S - s0);
-    const double* tabs[kMaxLevels];
-    double dtdx[kMaxLevels];
-    for (int l = 0; l < n; ++l) {
-      tabs[l] = T + (size_t)(s0 + l) * tstep;
-      dtdx[l] = h_dts[s0 + l] / c->dx;
+  int rc = 0;
+  const int LM = field ? 0 : ms_levels(c);
+  if (LM > 0) {
+    rc = ms_window(c, LM, f0, f_out, f_tmp, write_final, mom_out, T, S, h_dts, st, prog, base);
+  } else {
+    int w = 0;
+    const double* in = f0;
+    for (int s0 = 0; s0 < S && rc == 0;) {
+      const int n = std::min(L, S - s0);
+      const double* tabs[kMaxLevels];
+      double dtdx[kMaxLevels];
+      for (int l = 0; l < n; ++l) {
+        tabs[l] = T + (size_t)(s0 + l) * tstep;
+        dtdx[l] = h_dts[s0 + l] / c->dx;
+      }
+      double* out = buf(++w);
+      if (field) {
+        // the v_x field term: the one-step sweep (its neighbour-row flux) on
+        // the recursion's tables, without the marginal partials
+        rc = run_sweep(c, 1, true, in, tabs[0], out, dtdx[0], E, 0.5 * e_max, h_dts[s0] / c->dv[0], s0 + 1,
+                       st, 1);
+      } else {
+        rc = run_fsweep(c, n, in, out, tabs, dtdx, s0 + 1, st, prog, base + (unsigned)(s0 + n - 1));
+      }
+      in = out;
+      s0 += n;
     }
-    double* out = buf(++w);
-    if (field) {
-      // the v_x field term: the one-step sweep (its neighbour-row flux) on
-      // the recursion's tables, without the marginal partials
-      if (run_sweep(c, 1, true, in, tabs[0], out, dtdx[0], E, 0.5 * e_max, h_dts[s0] / c->dv[0], s0 + 1,
-                    st, 1))
-        return -1;
-    } else if (run_fsweep(c, n, in, out, tabs, dtdx, s0 + 1, st, prog, base + (unsigned)(s0 + n - 1))) {
-      return -1;
-    }
-    in = out;
-    s0 += n;
+    if (prog && rc == 0) rc = cudaStreamWaitEvent(st, c->ev_done, 0) == cudaSuccess ? 0 : fail("event");
+    if (rc == 0)
+      rc = run_sweep(c, 0, false, in, T + (size_t)S * tstep, write_final ? f_out : nullptr, 0.0, nullptr,
+                     0.0, 0.0, S, st);
+    if (rc == 0 && mom_out)
+      rc = run_final(c, 0, kFinProject, nullptr, mom_out, nullptr, 0, 1, 1, nullptr, S + 1, st);
   }
-  if (prog) CK(cudaStreamWaitEvent(st, c->ev_done, 0));  // R_S for the final relax
-  if (run_sweep(c, 0, false, in, T + (size_t)S * tstep, write_final ? f_out : nullptr, 0.0, nullptr,
-                0.0, 0.0, S, st))
-    return -1;
-  if (mom_out && run_final(c, 0, kFinProject, nullptr, mom_out, nullptr, 0, 1, 1, nullptr, S + 1, st))
-    return -1;
-  return 0;
+  // the side-stream recursion joins the stream on every exit path (its
+  // tables and state buffers are reused by the next call)
+  if (prog) cudaStreamWaitEvent(st, c->ev_done, 0);
+  return rc;
 }
 }  // namespace
 
@@ -1087,6 +1229,7 @@ int windows_fused(pbgk_ctx* c, int nwin, const double* mom_in, double* mom_out, 
       ensure_dev(c->d_bnst, c->bnst_cap, (size_t)G, st))
     return -1;
   const int L = field ? 1 : fuse_levels(c);
+  const int LM = field ? 0 : ms_levels(c);
   std::vector<double> hd((size_t)std::max(Smax, 1) * G);
   std::vector<int> hn(G);
   for (int w0 = 0; w0 < nwin; w0 += G) {
@@ -1122,9 +1265,15 @@ int windows_fused(pbgk_ctx* c, int nwin, const double* mom_in, double* mom_out, 
       const int w = w0 + k, S = h_nsteps[w];
       if (S == 0) continue;
       const double* T = c->d_bt + k * t_ws;
+      c->err_slot = c->d_keys + w;
+      if (LM > 0) {
+        const int rc = ms_window(c, LM, nullptr, f_a, f_b, 0, mom_out + w * m5, T, S, h_dts + off[w], st);
+        c->err_slot = nullptr;
+        if (rc) return -1;
+        continue;
+      }
       const int P = (S + L - 1) / L;
       auto buf = [&](int i) { return ((P - i) % 2 == 0) ? f_a : f_b; };
-      c->err_slot = c->d_keys + w;
       const double* in = nullptr;
       int s0 = 0, wcount = 0;
       while (s0 < S) {
@@ -1173,6 +1322,17 @@ int pbgk_propagate(pbgk_ctx* c, const double* f0, const double* mom0, double* f_
     return -1;
   long long code = -1;
   if (fetch_err(c, st, &code)) return -1;
+  if (code >= 0 && (int)(code & 0xFF) == kErrSync) {
+    // a pass gave up waiting for the concurrent recursion (its SMs were taken
+    // by other work): the same propagation with the recursion run serially
+    if (reset_err(c, st)) return -1;
+    c->no_concurrent = 1;
+    const int rc = propagate_body(c, f0, mom0, f_out, f_tmp, write_final, mom_out, nsteps, h_dts, eps,
+                                  tau, E, e_max, st);
+    c->no_concurrent = 0;
+    if (rc) return -1;
+    if (fetch_err(c, st, &code)) return -1;
+  }
   if (code >= 0 && (int)(code & 0xFF) == kErrNonFiniteMulti) {
     // non-finite somewhere in a multi-step pass: the one-step path finds the step
     if (reset_err(c, st)) return -1;
@@ -1415,6 +1575,16 @@ int pbgk_set_fusion(pbgk_ctx* c, int levels) {
   c->fuse = levels;
   return 0;
 }
+
+int pbgk_set_msweep(pbgk_ctx* c, int on, int levels) {
+  if (!c) return fail("null context");
+  if (levels != 0 && levels != 4 && levels != 8) return fail("msweep levels must be 0 (auto), 4 or 8");
+  c->ms = on != 0;
+  c->ms_levels = levels;
+  return 0;
+}
+
+int pbgk_msweep_levels(pbgk_ctx* c) { return c ? ms_levels(c) : -1; }
 
 int pbgk_set_grid_reserve(pbgk_ctx* c, int slots) {
   if (!c) return fail("pbgk_set_grid_reserve: null context");

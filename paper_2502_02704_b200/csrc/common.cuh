@@ -100,6 +100,32 @@ struct FSweepArgs {
   unsigned need;
 };
 
+// Multi-step sweep, round 2 (msweep.cu): up to kMaxL levels per pass,
+// warp-specialised; tab[l] the relax table applied before level l's
+// transport, tabR (FINAL mode) R_S of the window's last step, part the
+// partial records of P(f_S) on the kernel's own tiling.
+constexpr int kMaxL = 8;
+struct MSweepArgs {
+  int nx, nvx, nvy, nvz;
+  long long plane;
+  Tiling t;
+  long long total;       // NT * nx plane items (halos excluded)
+  double* fout;          // null: nothing stored (FINAL: partials only)
+  const double* tab[kMaxL];
+  const double* tabR;
+  int nlev;              // levels of this pass (<= the compiled L)
+  int TL, gxo, gyo, gzo;
+  const double* cx;
+  double dtdx[kMaxL];
+  int bc;
+  ErrKey* err;
+  int step0;
+  double* part;
+  const unsigned* prog;
+  unsigned need;
+  int dbg;               // development ablations (PBGK_MS_DBG): 1 no table copies, 2 no box load
+};
+
 // Moment recursion (marginal.cu): five weighted sums of f over (v_y, v_z)
 // per x cell and v_x row obey a closed recursion under the upwind x transport
 // and the separable BGK relaxation (both act on a v_x row with coefficients

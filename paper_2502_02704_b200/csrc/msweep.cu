@@ -1,0 +1,585 @@
+// Multi-step sweep, round 2: up to 8 fine steps of f per pass.
+//
+// Same algorithm as fsweep.cu (the relax tables R_s of every step come from
+// the moment recursion, marginal.cu; a velocity tile marches in x and every
+// level keeps the upwind flux of the previous plane in registers; only the
+// last level is stored: 16/L bytes of HBM per cell-update), re-laid out for
+// latency hiding and a lean per-element instruction stream:
+//
+//   * box A = 8 v_x rows x BY = 8K v_y x BZ = 16 v_z (16 KB at K = 2); a warp
+//     owns one box row, so the per-row scalars (relax factor, transport
+//     coefficients) are warp-uniform; a thread owns K lines (adjacent v_y) x
+//     4 consecutive v_z.
+//   * two warp groups split the levels: group 0 runs levels [0, L/2) of plane
+//     p and hands its output to group 1 through the stage's box area (each
+//     thread rewrites exactly the elements it read), group 1 runs levels
+//     [L/2, L) of plane p while group 0 moves on to plane p+1.  16 warps per
+//     SM, half the carries per thread, half the dependent chain per item.
+//   * relax + transport of level l, per element (ref/kinetic.py:110-112,
+//     130-134):  z = x + (ls gxa gy) gz,  out = (keep r) z + q_prev,
+//     q = (a r) z,  with a = (dt/dx)|c_x| and keep = 1 - a: the reference's
+//     f* = f - (dt/dx)(F_i+1 - F_i) after f = r (f* + ls M), re-associated (a
+//     few ulps; the multi-step path is held to the oracle at 1e-12).  (keep,
+//     a) per (v_x row, level) sit in a shared table computed once per launch.
+//   * loads: thread 0 of group 0 issues the TMA box of a plane, every group-0
+//     thread one 16-byte cp.async chunk of the table-row slices the tile needs
+//     (r, ls | gxa of its rows | gy | gz per level: 0.3 KB instead of whole
+//     rows); full / mid / empty mbarriers per ring stage, no CTA barrier on
+//     the steady path.
+//   * FINAL (the window's last pass): R_S applied to the last level's output
+//     and the per-(plane, tile) marginal partial records [m_x rows | m_y |
+//     m_z] written for finalize.cu (kFinProject) -- the projection P(f_S)
+//     without storing f_S and reading it back.  Fixed trees, the same for
+//     every marginal index and its mirror (even data keeps an exactly zero
+//     folded first moment, ref/moments.py:80-88).
+//   * SYNTH (the window's first pass from moments): level 0 input is the lift
+//     f_0 = ls gxa gy gz of tab[0] (ref/lifting.py:47-57), no f read.
+//
+// Finiteness (ref/kinetic.py:157-159): the stored level's values (or, FINAL,
+// the m_x partials) are summed per thread; non-finite -> status kind 6 at the
+// pass's first step, on which the host re-runs the propagation on the
+// one-step path for the exact BlowUpError(step).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <type_traits>
+
+#include "common.cuh"
+#include "ptx.cuh"
+#include "sweep_impl.cuh"
+
+namespace pbgk {
+
+namespace ms {
+constexpr int A = 8;      // v_x rows per box = warps per group
+constexpr int BZ = 16;    // v_z per box line (128 B)
+constexpr int NW = A;     // warps per group
+constexpr int NTG = 32 * NW;
+constexpr int NTHR = 2 * NTG;
+__host__ __device__ constexpr int by(int K) { return 8 * K; }
+__host__ __device__ constexpr int ts(int K) { return 2 + A + by(K) + BZ; }  // table slice (doubles)
+}  // namespace ms
+
+enum MsMode : int { kMsSynth = 1, kMsFinal = 2 };
+
+// The item sequence of a CTA's segment [g0, g1) of the (tile, plane)
+// items: every run of consecutive planes of one tile is preceded by `nlev`
+// lead items (its upwind halo planes; lead item k completes k levels).
+struct MsSeq {
+  long long g, g1;
+  int nx, nlev;
+  int t, p, p1, lead;  // current run: tile, next position, end; lead items left
+  __device__ __forceinline__ void init(long long g0_, long long g1_, int nx_, int nlev_) {
+    g = g0_;
+    g1 = g1_;
+    nx = nx_;
+    nlev = nlev_;
+    p = p1 = 0;
+    lead = 0;
+    t = -1;
+  }
+  // next item: tile (changes only at a run start), position; false at the end
+  __device__ __forceinline__ bool next(int& tile, int& pos, bool& new_run) {
+    new_run = false;
+    if (lead == 0 && p == p1) {
+      if (g >= g1) return false;
+      t = (int)(g / nx);
+      p = (int)(g - (long long)t * nx);
+      p1 = (int)min((long long)nx, p + (g1 - g));
+      g += p1 - p;
+      lead = nlev;
+      new_run = true;
+    }
+    tile = t;
+    if (lead > 0) {
+      pos = p - lead;
+      --lead;
+    } else {
+      pos = p++;
+    }
+    return true;
+  }
+};
+
+template <int NT_>
+__device__ __forceinline__ void named_sync(int id) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(NT_) : "memory");
+}
+
+template <int K, int L, int MODE>
+__global__ void __launch_bounds__(ms::NTHR, 1)
+    msweep_kernel(const __grid_constant__ CUtensorMap fmap, const MSweepArgs a, int ns) {
+  using namespace ms;
+  constexpr bool SYNTH = (MODE & kMsSynth) != 0;
+  constexpr bool FINAL = (MODE & kMsFinal) != 0;
+  constexpr int LH = L / 2;  // levels per group
+  constexpr int BY = by(K);
+  constexpr int TS = ts(K);
+  constexpr int NTAB = L + (FINAL ? 1 : 0);
+  constexpr uint32_t BOXB = (uint32_t)(A * BY * BZ * 8);  // also the group hand-off area
+  constexpr uint32_t STAGEB = (BOXB + NTAB * TS * 8 + 127u) & ~127u;
+  constexpr int REC = A + BY + BZ;
+  constexpr int RS = 1 + BY + BZ;             // per-warp partial block (FINAL)
+  constexpr int NCH = (2 + A + BY + BZ) / 2;  // 16-byte chunks of one table slice
+  static_assert(NTAB * NCH <= 2 * NTG, "table chunks: two per loader thread at most");
+  extern __shared__ __align__(128) unsigned char smem[];
+
+  const Tiling& T = a.t;
+  const int tid = threadIdx.x;
+  const int nx = a.nx, nvx = a.nvx;
+  const int nlev = a.nlev;
+  double2* AK = reinterpret_cast<double2*>(smem + (size_t)ns * STAGEB);   // [nvx][L] (keep, a)
+  double* RB = reinterpret_cast<double*>(AK + L * nvx);                    // FINAL: [2][NW][RS]
+  uint64_t* full = reinterpret_cast<uint64_t*>(RB + (FINAL ? 2 * NW * RS : 0));
+  uint64_t* mid = full + ns;
+  uint64_t* empty = mid + ns;
+
+  const long long g0 = (a.total * blockIdx.x) / gridDim.x;
+  const long long g1 = (a.total * (blockIdx.x + 1)) / gridDim.x;
+
+  // transport coefficients per (row, level): a = (dt/dx) |c_x|, keep = 1 - a
+  // (up rows: f* = (1-a) f + a f_{i-1}; down rows: (1-a) f + a f_{i+1})
+  for (int j = tid; j < L * nvx; j += NTHR) {
+    const int jx = j / L, l = j - jx * L;
+    const double c = a.cx[jx];
+    const double av = a.dtdx[l] * (c < 0.0 ? -c : c);
+    AK[j] = make_double2(1.0 - av, av);
+  }
+  if (tid == 0) {
+    for (int s = 0; s < ns; ++s) {
+      mbar_init(&full[s], 1 + NTG);  // the box's expect-tx arrive + one cp.async arrive per loader
+      mbar_init(&mid[s], NW);
+      mbar_init(&empty[s], NW);
+    }
+    fence_mbar_init();
+  }
+  pdl_wait();
+  pdl_trigger();
+  __syncthreads();
+
+  const int grp = tid / NTG;        // 0: levels [0, LH) + loads; 1: levels [LH, L) + output
+  const int gt = tid - grp * NTG;
+  const int w = gt >> 5;            // box row
+  const int lane = tid & 31;
+  const int lg = lane >> 2;         // line group: lines y = K lg .. K lg + K-1
+  const int lz = lane & 3;          // v_z 4 lz .. 4 lz + 3
+  const int yl = K * lg;
+  const int boff = (w * BY + yl) * BZ + 4 * lz;  // box offset of line 0 (doubles)
+
+  double prev[LH][K][4];
+#pragma unroll
+  for (int l = 0; l < LH; ++l)
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) prev[l][k][v] = 0.0;
+  double acc = 0.0;
+  int stg = 0;
+  uint32_t ph = 0;
+  TileGeom tg{};
+  const double2* AKr = AK;
+  long long goff = 0;
+  int t = 0;
+
+  // levels [BASE, BASE + LH) of one item: relax with the level's table, then
+  // (levels < depth) transport; level == depth (a lead item) only relaxes and
+  // passes its flux on.  FULLC: a run plane of a full pass (no runtime
+  // conditions -- the steady path)
+  auto levels = [&](double (&x)[K][4], const double* tabs, int depth, auto fullc, auto basec) {
+    constexpr bool FULLC = decltype(fullc)::value;
+    constexpr int BASE = decltype(basec)::value;
+#pragma unroll
+    for (int ll = 0; ll < LH; ++ll) {
+      const int l = BASE + ll;
+      if (!FULLC && (l >= nlev || l > depth)) break;
+#ifndef PBGK_MS_FENCE
+#define PBGK_MS_FENCE 0
+#endif
+      // (optional) keep the level's shared loads from being hoisted into the
+      // previous level: register pressure vs. latency hiding
+      if (PBGK_MS_FENCE && ll > 0) asm volatile("" ::: "memory");
+      const double* S = tabs + l * TS;
+      const double2 rl = *reinterpret_cast<const double2*>(S);  // r, ls
+      const double gxa = S[2 + w];
+      double gy[K];
+      if constexpr (K == 1) {
+        gy[0] = S[2 + A + yl];
+      } else {
+#pragma unroll
+        for (int k = 0; k < K; k += 2) {
+          const double2 q = *reinterpret_cast<const double2*>(S + 2 + A + yl + k);
+          gy[k] = q.x;
+          gy[k + 1] = q.y;
+        }
+      }
+      const double2 z01 = *reinterpret_cast<const double2*>(S + 2 + A + BY + 4 * lz);
+      const double2 z23 = *reinterpret_cast<const double2*>(S + 2 + A + BY + 4 * lz + 2);
+      const double gz[4] = {z01.x, z01.y, z23.x, z23.y};
+      const double2 ak = AKr[l];  // (keep, a)
+      const double W = rl.y * gxa;  // ls gxa
+      const bool lift0 = SYNTH && l == 0;
+      const double kr = lift0 ? ak.x : ak.x * rl.x;
+      const double ar = lift0 ? ak.y : ak.y * rl.x;
+      if (FULLC || l < depth) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const double wk = W * gy[k];
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const double z = lift0 ? wk * gz[v] : fma(wk, gz[v], x[k][v]);
+            x[k][v] = fma(kr, z, prev[ll][k][v]);
+            prev[ll][k][v] = ar * z;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const double wk = W * gy[k];
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const double z = lift0 ? wk * gz[v] : fma(wk, gz[v], x[k][v]);
+            prev[ll][k][v] = ar * z;
+          }
+        }
+      }
+    }
+  };
+  auto load_x = [&](double (&x)[K][4], const double* box) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const double2 u0 = *reinterpret_cast<const double2*>(box + boff + k * BZ);
+      const double2 u1 = *reinterpret_cast<const double2*>(box + boff + k * BZ + 2);
+      x[k][0] = u0.x; x[k][1] = u0.y; x[k][2] = u1.x; x[k][3] = u1.y;
+    }
+  };
+  auto zero_prev = [&]() {
+#pragma unroll
+    for (int l = 0; l < LH; ++l)
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) prev[l][k][v] = 0.0;
+  };
+  using TRUE_ = std::integral_constant<bool, true>;
+  using FALSE_ = std::integral_constant<bool, false>;
+  // the run walk of the segment, the same for both groups
+  auto walk = [&](auto&& item) {
+    for (long long g = g0; g < g1;) {
+      t = (int)(g / nx);
+      const int p0 = (int)(g - (long long)t * nx);
+      const int p1 = (int)min((long long)nx, p0 + (g1 - g));
+      g += p1 - p0;
+      tg = tile_geom(T, nvx, t);
+      const int jx = tg.r0 + w;
+      AKr = AK + jx * L;
+      goff = ((long long)jx * a.nvy + tg.y0 + yl) * a.nvz + tg.z0 + 4 * lz;
+#pragma unroll 1
+      for (int k = 0; k < nlev; ++k) item(p0 - nlev + k, k, FALSE_{});
+      if (nlev == L) {
+#pragma unroll 1
+        for (int p = p0; p < p1; ++p) item(p, L, TRUE_{});
+      } else {
+#pragma unroll 1
+        for (int p = p0; p < p1; ++p) item(p, nlev, FALSE_{});
+      }
+    }
+  };
+
+  if (grp == 0) {
+    // ---------------- group 0: loads, levels [0, LH) ----------------
+    MsSeq pseq;
+    pseq.init(g0, g1, nx, nlev);
+    int pstg = 0;
+    uint32_t pph = 0;
+    const int dist = ns - 2;  // items loaded ahead (group 1 trails by about one item)
+    TileGeom ptg{};
+    // this thread's (at most two) 16-byte table chunks of an item: level,
+    // slice kind and offsets fixed for the launch, the tile offset per run
+    const double* csrc[2];
+    int cdst[2], coff[2], ckind[2];
+    bool cval[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int j = gt + r * NTG;
+      cval[r] = j < NTAB * NCH;
+      const int l = cval[r] ? j / NCH : 0, c = j - l * NCH;
+      csrc[r] = (FINAL && l == L) ? a.tabR : a.tab[l < L ? l : 0];
+      if (c == 0) {
+        ckind[r] = 0; coff[r] = 0; cdst[r] = 0;
+      } else if (c <= A / 2) {
+        ckind[r] = 1; coff[r] = a.gxo + 2 * (c - 1); cdst[r] = 2 + 2 * (c - 1);
+      } else if (c <= A / 2 + BY / 2) {
+        const int q = c - 1 - A / 2;
+        ckind[r] = 2; coff[r] = a.gyo + 2 * q; cdst[r] = 2 + A + 2 * q;
+      } else {
+        const int q = c - 1 - A / 2 - BY / 2;
+        ckind[r] = 3; coff[r] = a.gzo + 2 * q; cdst[r] = 2 + A + BY + 2 * q;
+      }
+      cdst[r] += l * TS;
+    }
+    int crun[2] = {0, 0};  // coff + the current run's tile offset
+    const bool dbox = !(a.dbg & 2);
+    auto issue_next = [&]() {
+      int pt, pp;
+      bool nr;
+      if (!pseq.next(pt, pp, nr)) return;
+      if (nr) {
+        ptg = tile_geom(T, nvx, pt);
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+          crun[r] = coff[r] + (ckind[r] == 1 ? ptg.r0 : ckind[r] == 2 ? ptg.y0 : ckind[r] == 3 ? ptg.z0 : 0);
+      }
+      int i = ptg.down ? nx - 1 - pp : pp;
+      if ((unsigned)i >= (unsigned)nx) i = item_plane(nx, a.bc, ptg, pp);  // halo positions
+      const int s = pstg;
+      // the stage's previous item must be released by group 1
+      mbar_wait(&empty[s], pph ^ 1u);
+      unsigned char* st = smem + (size_t)s * STAGEB;
+      if (gt == 0) {
+        mbar_arrive_expect_tx(&full[s], (i < 0 || SYNTH || !dbox) ? 0u : BOXB);
+        if (i >= 0 && !SYNTH && dbox) tma_load_4d(st, &fmap, ptg.z0, ptg.y0, ptg.r0, i, &full[s]);
+      }
+      if (i >= 0 && !(a.dbg & 1)) {
+        // the table-row slices of every level: 16-byte cp.async chunks (L2 hits)
+        double* dst0 = reinterpret_cast<double*>(st + BOXB);
+        const size_t ro = (size_t)i * a.TL;
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+          if (cval[r]) cp_async_16(dst0 + cdst[r], csrc[r] + ro + crun[r]);
+      }
+      cp_async_mbar_arrive(&full[s]);
+      if (++pstg == ns) {
+        pstg = 0;
+        pph ^= 1u;
+      }
+    };
+    if (gt == 0) prefetch_tensormap(&fmap);
+    if (a.prog != nullptr) {
+      // the recursion runs concurrently on other SMs: wait for this pass's
+      // tables (bounded: a stalled recursion becomes status kind 5)
+      if (gt == 0) {
+        long long spins = 0;
+        while (ld_acquire_gpu(a.prog) < a.need) {
+          __nanosleep(256);
+          if (++spins > 20000000LL) {
+            atomicMin(a.err, err_key(0, a.step0, kErrSync));
+            break;
+          }
+        }
+        fence_proxy_async();
+      }
+      named_sync<NTG>(2);
+    }
+    for (int q = 0; q < dist; ++q) issue_next();
+    walk([&](int p, int depth, auto fullc) {
+      constexpr bool FULLC = decltype(fullc)::value;
+      const int i = FULLC ? (tg.down ? nx - 1 - p : p) : item_plane(nx, a.bc, tg, p);
+      mbar_wait(&full[stg], ph);
+      double* box = reinterpret_cast<double*>(smem + (size_t)stg * STAGEB);
+      if (!FULLC && i < 0) {
+        zero_prev();  // absorbing ghost plane (lead items only): zero flux at every level
+      } else {
+        const double* tabs = box + BOXB / 8;
+        double x[K][4];
+        if (!SYNTH) load_x(x, box);
+        levels(x, tabs, depth, fullc, std::integral_constant<int, 0>{});
+        // hand-off to group 1: every item it continues (a run plane, or a
+        // lead item deep enough to reach its levels)
+        if (FULLC || depth == nlev || depth >= LH) {
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            *reinterpret_cast<double2*>(box + boff + k * BZ) = make_double2(x[k][0], x[k][1]);
+            *reinterpret_cast<double2*>(box + boff + k * BZ + 2) = make_double2(x[k][2], x[k][3]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&mid[stg]);
+      if (++stg == ns) {
+        stg = 0;
+        ph ^= 1u;
+      }
+      issue_next();
+    });
+    return;
+  }
+
+  // ---------------- group 1: levels [LH, L), output ----------------
+  int rbuf = 0;
+  walk([&](int p, int depth, auto fullc) {
+    constexpr bool FULLC = decltype(fullc)::value;
+    const int i = FULLC ? (tg.down ? nx - 1 - p : p) : item_plane(nx, a.bc, tg, p);
+    mbar_wait(&mid[stg], ph);
+    const double* box = reinterpret_cast<const double*>(smem + (size_t)stg * STAGEB);
+    if (!FULLC && i < 0) {
+      zero_prev();
+    } else if (FULLC || depth == nlev || depth >= LH) {
+      const double* tabs = box + BOXB / 8;
+      double x[K][4];
+      load_x(x, box);
+      levels(x, tabs, depth, fullc, std::integral_constant<int, LH>{});
+      if (FULLC || depth == nlev) {
+        if constexpr (FINAL) {
+          // R_S (ref/kinetic.py:130-134) of the last level's output
+          const double* S = tabs + L * TS;
+          const double2 rl = *reinterpret_cast<const double2*>(S);
+          const double W = rl.y * S[2 + w];
+          const double2 z01 = *reinterpret_cast<const double2*>(S + 2 + A + BY + 4 * lz);
+          const double2 z23 = *reinterpret_cast<const double2*>(S + 2 + A + BY + 4 * lz + 2);
+          const double gz[4] = {z01.x, z01.y, z23.x, z23.y};
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const double wk = W * S[2 + A + yl + k];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) x[k][v] = rl.x * fma(wk, gz[v], x[k][v]);
+          }
+        }
+        if (a.fout != nullptr) {
+          double* d = a.fout + (size_t)i * a.plane + goff;
+#pragma unroll
+          for (int k = 0; k < K; ++k)
+            st_global_v4(d + (size_t)k * a.nvz, x[k][0], x[k][1], x[k][2], x[k][3]);
+        }
+        if constexpr (FINAL) {
+          // per-warp partials: line totals (lanes of a line), the row total,
+          // the v_z partials over the warp's lines; fixed trees
+          double lt[K], zs[4];
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            lt[k] = (x[k][0] + x[k][1]) + (x[k][2] + x[k][3]);
+            lt[k] += __shfl_xor_sync(0xffffffffu, lt[k], 1);
+            lt[k] += __shfl_xor_sync(0xffffffffu, lt[k], 2);
+          }
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            double s = x[0][v];
+#pragma unroll
+            for (int k = 1; k < K; ++k) s += x[k][v];
+            zs[v] = s;
+          }
+          double rt = lt[0];
+#pragma unroll
+          for (int k = 1; k < K; ++k) rt += lt[k];
+#pragma unroll
+          for (int m = 4; m <= 16; m <<= 1) {
+            rt += __shfl_xor_sync(0xffffffffu, rt, m);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) zs[v] += __shfl_xor_sync(0xffffffffu, zs[v], m);
+          }
+          double* R = RB + (size_t)(rbuf * NW + w) * RS;
+          if (lane == 0) R[0] = rt;
+          if (lz == 0) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) R[1 + yl + k] = lt[k];
+          }
+          if (lg == 0) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) R[1 + BY + 4 * lz + v] = zs[v];
+          }
+          named_sync<NTG>(1);
+          // the record [m_x rows | m_y | m_z] of (plane i, tile t): rows from
+          // the warps, m_y / m_z summed over the warps in order
+          if (gt < REC) {
+            const double* R0 = RB + (size_t)rbuf * NW * RS;
+            double s;
+            if (gt < A) {
+              s = R0[(size_t)gt * RS];
+              acc += s;
+            } else {
+              const int off = gt < A + BY ? 1 + (gt - A) : 1 + BY + (gt - A - BY);
+              s = R0[off];
+#pragma unroll
+              for (int q = 1; q < NW; ++q) s += R0[(size_t)q * RS + off];
+            }
+            a.part[((size_t)i * T.NT + t) * T.PS + gt] = s;
+          }
+          rbuf ^= 1;
+        } else {
+#pragma unroll
+          for (int k = 0; k < K; ++k) acc += (x[k][0] + x[k][1]) + (x[k][2] + x[k][3]);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stg]);
+    if (++stg == ns) {
+      stg = 0;
+      ph ^= 1u;
+    }
+  });
+  if (!isfinite(acc)) atomicMin(a.err, err_key(0, a.step0, kErrNonFiniteMulti));
+}
+
+size_t msweep_smem_bytes(int K, int L, int mode, int nvx, int ns) {
+  const bool fin = mode & kMsFinal;
+  const int BY = ms::by(K), TS = ms::ts(K);
+  const size_t box = (size_t)ms::A * BY * ms::BZ * 8;
+  const size_t stage = (box + (size_t)(L + (fin ? 1 : 0)) * TS * 8 + 127) & ~(size_t)127;
+  return (size_t)ns * stage + (size_t)L * nvx * 16 + (fin ? 2 * ms::NW * (1 + BY + ms::BZ) * 8 : 0) +
+         (size_t)3 * ns * 8;
+}
+
+int msweep_threads() { return ms::NTHR; }
+
+// Box shape of the kernel for a velocity grid (0 if it does not tile):
+// 8 rows of each c_x sign, 8K v_y, 16 v_z, no partial boxes.
+int msweep_tiling(int nvx, int nvy, int nvz, int K, Tiling* t) {
+  const int BY = ms::by(K);
+  if (nvx % (2 * ms::A) != 0 || nvy % BY != 0 || nvz % ms::BZ != 0) return 0;
+  t->A = ms::A;
+  t->By = BY;
+  t->Bz = ms::BZ;
+  t->rows_load = ms::A;
+  t->nneg = nvx / 2;
+  t->ntn = t->nneg / ms::A;
+  t->ntp = (nvx - t->nneg) / ms::A;
+  t->nty = nvy / BY;
+  t->ntz = nvz / ms::BZ;
+  t->NT = (t->ntn + t->ntp) * t->nty * t->ntz;
+  t->PS = (ms::A + BY + ms::BZ + 1) & ~1;
+  return 1;
+}
+
+template <int K, int L, int MODE>
+static cudaError_t launch_ms(const CUtensorMap& map, const MSweepArgs& a, int grid, int ns, size_t smem,
+                             cudaStream_t st) {
+  auto fn = msweep_kernel<K, L, MODE>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (a.prog != nullptr) {
+    fn<<<grid, ms::NTHR, smem, st>>>(map, a, ns);
+    return cudaGetLastError();
+  }
+  return launch_pdl(fn, grid, ms::NTHR, smem, st, map, a, ns);
+}
+
+template <int K, int L>
+static cudaError_t launch_ms_mode(int mode, const CUtensorMap& map, const MSweepArgs& a, int grid, int ns,
+                                  size_t smem, cudaStream_t st) {
+  switch (mode) {
+    case 0: return launch_ms<K, L, 0>(map, a, grid, ns, smem, st);
+    case kMsSynth: return launch_ms<K, L, kMsSynth>(map, a, grid, ns, smem, st);
+    case kMsFinal: return launch_ms<K, L, kMsFinal>(map, a, grid, ns, smem, st);
+    case kMsSynth | kMsFinal: return launch_ms<K, L, kMsSynth | kMsFinal>(map, a, grid, ns, smem, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// L: compiled level counts (a pass may run fewer, a.nlev <= L)
+cudaError_t launch_msweep(int K, int L, int mode, const CUtensorMap& map, const MSweepArgs& a, int grid,
+                          int ns, size_t smem, cudaStream_t st) {
+  if (K == 2) {
+    switch (L) {
+      case 4: return launch_ms_mode<2, 4>(mode, map, a, grid, ns, smem, st);
+      case 8: return launch_ms_mode<2, 8>(mode, map, a, grid, ns, smem, st);
+    }
+  } else if (K == 1) {
+    switch (L) {
+      case 4: return launch_ms_mode<1, 4>(mode, map, a, grid, ns, smem, st);
+      case 8: return launch_ms_mode<1, 8>(mode, map, a, grid, ns, smem, st);
+    }
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace pbgk

@@ -101,6 +101,25 @@ class Ctx:
             else:
                 self.set_fusion(old)
 
+    def set_msweep(self, on: bool, levels: int = 0) -> None:
+        """Pass kernel of the multi-step path (include/pbgk.h pbgk_set_msweep):
+        the round-2 msweep kernel (default) or the round-1 fsweep kernel."""
+        _lib.check(self.lib.pbgk_set_msweep(self.h, int(bool(on)), int(levels)), "pbgk_set_msweep")
+        self.msweep = (bool(on), int(levels))
+
+    @contextlib.contextmanager
+    def msweep_mode(self, on: bool, levels: int = 0):
+        """Temporarily select the multi-step pass kernel (tests / A-B)."""
+        old = getattr(self, "msweep", (True, 0))
+        self.set_msweep(on, levels)
+        try:
+            yield self
+        finally:
+            self.set_msweep(*old)
+
+    def msweep_levels(self) -> int:
+        return int(self.lib.pbgk_msweep_levels(self.h))
+
     def describe(self) -> str:
         buf = ctypes.create_string_buffer(1024)
         _lib.check(self.lib.pbgk_ctx_describe(self.h, buf, 1024), "pbgk_ctx_describe")
