@@ -890,6 +890,7 @@ int ms_levels(pbgk_ctx* c) {
   if (c->fuse > 0) return 0;  // an explicit pbgk_set_fusion level count selects the round-1 kernel
   static const int envl = getenv("PBGK_MS_L") ? atoi(getenv("PBGK_MS_L")) : 0;  // dev A/B knob
   const int L = envl ? envl : (c->ms_levels ? c->ms_levels : 8);
+  if (L != 4 && L != 8) return 0;
   const int K = L > 4 ? 1 : 2;
   if (c->ms_t[K - 1].NT == 0) return 0;
   return L;
@@ -940,7 +941,7 @@ int run_msweep(pbgk_ctx* c, int L, const double* in, double* out, const double* 
   if (!map) return fail("tensor map: " + g_last_error);
   static const int ns_env = getenv("PBGK_MS_NS") ? atoi(getenv("PBGK_MS_NS")) : 0;  // dev knob
   int ns = ns_env > 0 ? ns_env : 12;
-  while (ns > 2 && msweep_smem_bytes(K, L, mode, c->g.nvx, ns) > c->smem_optin) --ns;
+  while (ns > 3 && msweep_smem_bytes(K, L, mode, c->g.nvx, ns) > c->smem_optin) --ns;
   const size_t smem = msweep_smem_bytes(K, L, mode, c->g.nvx, ns);
   if (smem > c->smem_optin) return fail("msweep: ring does not fit");
   const double fbytes = 8.0 * (double)a.plane * a.nx;

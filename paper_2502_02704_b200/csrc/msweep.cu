@@ -62,41 +62,36 @@ __host__ __device__ constexpr int ts(int K) { return 2 + A + by(K) + BZ; }  // t
 
 enum MsMode : int { kMsSynth = 1, kMsFinal = 2 };
 
-// The item sequence of a CTA's segment [g0, g1) of the (tile, plane)
-// items: every run of consecutive planes of one tile is preceded by `nlev`
-// lead items (its upwind halo planes; lead item k completes k levels).
-struct MsSeq {
+#ifndef PBGK_MS_SLEEP
+#define PBGK_MS_SLEEP 0
+#endif
+#if PBGK_MS_SLEEP
+#define PBGK_MS_WAIT mbar_wait_sleep
+#else
+#define PBGK_MS_WAIT mbar_wait
+#endif
+
+// The item sequence of a CTA's segment [g0, g1) of (tile, plane) positions:
+// every run of consecutive planes of one tile is preceded by `nlev` lead
+// positions (its upwind halo planes; lead position k completes k levels);
+// the run's positions (lead + planes) are grouped P per item, the last item
+// of a run possibly short.
+struct MsRuns {
   long long g, g1;
   int nx, nlev;
-  int t, p, p1, lead;  // current run: tile, next position, end; lead items left
   __device__ __forceinline__ void init(long long g0_, long long g1_, int nx_, int nlev_) {
     g = g0_;
     g1 = g1_;
     nx = nx_;
     nlev = nlev_;
-    p = p1 = 0;
-    lead = 0;
-    t = -1;
   }
-  // next item: tile (changes only at a run start), position; false at the end
-  __device__ __forceinline__ bool next(int& tile, int& pos, bool& new_run) {
-    new_run = false;
-    if (lead == 0 && p == p1) {
-      if (g >= g1) return false;
-      t = (int)(g / nx);
-      p = (int)(g - (long long)t * nx);
-      p1 = (int)min((long long)nx, p + (g1 - g));
-      g += p1 - p;
-      lead = nlev;
-      new_run = true;
-    }
-    tile = t;
-    if (lead > 0) {
-      pos = p - lead;
-      --lead;
-    } else {
-      pos = p++;
-    }
+  // next run: tile, first plane position p0, end p1; false at the end
+  __device__ __forceinline__ bool next(int& t, int& p0, int& p1) {
+    if (g >= g1) return false;
+    t = (int)(g / nx);
+    p0 = (int)(g - (long long)t * nx);
+    p1 = (int)min((long long)nx, p0 + (g1 - g));
+    g += p1 - p0;
     return true;
   }
 };
@@ -106,22 +101,29 @@ __device__ __forceinline__ void named_sync(int id) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(NT_) : "memory");
 }
 
-template <int K, int L, int MODE>
+template <int K, int L, int MODE, int P>
 __global__ void __launch_bounds__(ms::NTHR, 1)
     msweep_kernel(const __grid_constant__ CUtensorMap fmap, const MSweepArgs a, int ns) {
   using namespace ms;
   constexpr bool SYNTH = (MODE & kMsSynth) != 0;
   constexpr bool FINAL = (MODE & kMsFinal) != 0;
-  constexpr int LH = L / 2;  // levels per group
+#ifndef PBGK_MS_LA
+#define PBGK_MS_LA 0
+#endif
+  // levels [0, LA) run in group 0 (which also issues the loads), [LA, L) in
+  // group 1; LH = the larger share (carry registers)
+  constexpr int LA = PBGK_MS_LA > 0 && PBGK_MS_LA < L ? PBGK_MS_LA : L / 2;
+  constexpr int LH = LA > L - LA ? LA : L - LA;
   constexpr int BY = by(K);
   constexpr int TS = ts(K);
   constexpr int NTAB = L + (FINAL ? 1 : 0);
   constexpr uint32_t BOXB = (uint32_t)(A * BY * BZ * 8);  // also the group hand-off area
-  constexpr uint32_t STAGEB = (BOXB + NTAB * TS * 8 + 127u) & ~127u;
+  constexpr uint32_t PLB = (BOXB + NTAB * TS * 8 + 127u) & ~127u;  // one plane of a stage
+  constexpr uint32_t STAGEB = P * PLB;
   constexpr int REC = A + BY + BZ;
   constexpr int RS = 1 + BY + BZ;             // per-warp partial block (FINAL)
   constexpr int NCH = (2 + A + BY + BZ) / 2;  // 16-byte chunks of one table slice
-  static_assert(NTAB * NCH <= 2 * NTG, "table chunks: two per loader thread at most");
+  constexpr int CPT = (P * NTAB * NCH + NTG - 1) / NTG;  // chunks per loader thread
   extern __shared__ __align__(128) unsigned char smem[];
 
   const Tiling& T = a.t;
@@ -147,7 +149,7 @@ __global__ void __launch_bounds__(ms::NTHR, 1)
   }
   if (tid == 0) {
     for (int s = 0; s < ns; ++s) {
-      mbar_init(&full[s], 1 + NTG);  // the box's expect-tx arrive + one cp.async arrive per loader
+      mbar_init(&full[s], 1 + NTG);  // the boxes' expect-tx arrive + one cp.async arrive per loader
       mbar_init(&mid[s], NW);
       mbar_init(&empty[s], NW);
     }
@@ -157,7 +159,7 @@ __global__ void __launch_bounds__(ms::NTHR, 1)
   pdl_trigger();
   __syncthreads();
 
-  const int grp = tid / NTG;        // 0: levels [0, LH) + loads; 1: levels [LH, L) + output
+  const int grp = tid / NTG;        // 0: loads + levels [0, LH); 1: levels [LH, L) + output
   const int gt = tid - grp * NTG;
   const int w = gt >> 5;            // box row
   const int lane = tid & 31;
@@ -176,28 +178,20 @@ __global__ void __launch_bounds__(ms::NTHR, 1)
   double acc = 0.0;
   int stg = 0;
   uint32_t ph = 0;
-  TileGeom tg{};
-  const double2* AKr = AK;
-  long long goff = 0;
-  int t = 0;
 
-  // levels [BASE, BASE + LH) of one item: relax with the level's table, then
-  // (levels < depth) transport; level == depth (a lead item) only relaxes and
-  // passes its flux on.  FULLC: a run plane of a full pass (no runtime
-  // conditions -- the steady path)
-  auto levels = [&](double (&x)[K][4], const double* tabs, int depth, auto fullc, auto basec) {
+  // levels [BASE, BASE + LH) of one plane: relax with the level's table, then
+  // (levels < depth) transport; level == depth (a lead position) only
+  // relaxes and passes its flux on.  FULLC: a run plane of a full pass (no
+  // runtime conditions -- the steady path)
+  auto levels = [&](double (&x)[K][4], const double* tabs, int depth, const double2* AKr, auto fullc,
+                    auto basec) {
     constexpr bool FULLC = decltype(fullc)::value;
     constexpr int BASE = decltype(basec)::value;
+    constexpr int CNT = BASE == 0 ? LA : L - LA;
 #pragma unroll
-    for (int ll = 0; ll < LH; ++ll) {
+    for (int ll = 0; ll < CNT; ++ll) {
       const int l = BASE + ll;
       if (!FULLC && (l >= nlev || l > depth)) break;
-#ifndef PBGK_MS_FENCE
-#define PBGK_MS_FENCE 0
-#endif
-      // (optional) keep the level's shared loads from being hoisted into the
-      // previous level: register pressure vs. latency hiding
-      if (PBGK_MS_FENCE && ll > 0) asm volatile("" ::: "memory");
       const double* S = tabs + l * TS;
       const double2 rl = *reinterpret_cast<const double2*>(S);  // r, ls
       const double gxa = S[2 + w];
@@ -215,11 +209,22 @@ __global__ void __launch_bounds__(ms::NTHR, 1)
       const double2 z01 = *reinterpret_cast<const double2*>(S + 2 + A + BY + 4 * lz);
       const double2 z23 = *reinterpret_cast<const double2*>(S + 2 + A + BY + 4 * lz + 2);
       const double gz[4] = {z01.x, z01.y, z23.x, z23.y};
+#ifndef PBGK_MS_EXP
+#define PBGK_MS_EXP 0
+#endif
+#if PBGK_MS_EXP
+      // timing experiment only (wrong results): per-row factors as if
+      // precomputed in the table
+      const double W = gxa;
+      const bool lift0 = SYNTH && l == 0;
+      const double kr = rl.x, ar = rl.y;
+#else
       const double2 ak = AKr[l];  // (keep, a)
       const double W = rl.y * gxa;  // ls gxa
       const bool lift0 = SYNTH && l == 0;
       const double kr = lift0 ? ak.x : ak.x * rl.x;
       const double ar = lift0 ? ak.y : ak.y * rl.x;
+#endif
       if (FULLC || l < depth) {
 #pragma unroll
         for (int k = 0; k < K; ++k) {
@@ -262,90 +267,129 @@ __global__ void __launch_bounds__(ms::NTHR, 1)
   };
   using TRUE_ = std::integral_constant<bool, true>;
   using FALSE_ = std::integral_constant<bool, false>;
-  // the run walk of the segment, the same for both groups
+  // the walk over the segment's runs and their items, the same for both
+  // groups; item(tg, p0, u0, n, fullc): positions p0 - nlev + u0 .. + n - 1
   auto walk = [&](auto&& item) {
-    for (long long g = g0; g < g1;) {
-      t = (int)(g / nx);
-      const int p0 = (int)(g - (long long)t * nx);
-      const int p1 = (int)min((long long)nx, p0 + (g1 - g));
-      g += p1 - p0;
-      tg = tile_geom(T, nvx, t);
-      const int jx = tg.r0 + w;
-      AKr = AK + jx * L;
-      goff = ((long long)jx * a.nvy + tg.y0 + yl) * a.nvz + tg.z0 + 4 * lz;
+    MsRuns runs;
+    runs.init(g0, g1, nx, nlev);
+    int t, p0, p1;
+    while (runs.next(t, p0, p1)) {
+      const TileGeom tg = tile_geom(T, nvx, t);
+      const int nitems = (p1 - p0) + nlev;
+      // FULLC items: every position a run plane (u >= nlev), P of them, all levels
+      int f0 = (nlev + P - 1) / P, f1 = nitems / P;
+      if (nlev != L || f1 < f0) f0 = f1 = (nitems + P - 1) / P;
 #pragma unroll 1
-      for (int k = 0; k < nlev; ++k) item(p0 - nlev + k, k, FALSE_{});
-      if (nlev == L) {
+      for (int j = 0; j < f0; ++j) item(tg, t, p0, j * P, min(P, nitems - j * P), FALSE_{});
 #pragma unroll 1
-        for (int p = p0; p < p1; ++p) item(p, L, TRUE_{});
-      } else {
+      for (int j = f0; j < f1; ++j) item(tg, t, p0, j * P, P, TRUE_{});
 #pragma unroll 1
-        for (int p = p0; p < p1; ++p) item(p, nlev, FALSE_{});
-      }
+      for (int j = f1; j * P < nitems; ++j) item(tg, t, p0, j * P, min(P, nitems - j * P), FALSE_{});
     }
+  };
+  // plane of position p0 - nlev + u of a run
+  auto plane_of = [&](const TileGeom& tg, int p0, int u, bool interior) {
+    const int p = p0 - nlev + u;
+    if (interior) return tg.down ? nx - 1 - p : p;
+    return item_plane(nx, a.bc, tg, p);
   };
 
   if (grp == 0) {
     // ---------------- group 0: loads, levels [0, LH) ----------------
-    MsSeq pseq;
-    pseq.init(g0, g1, nx, nlev);
+    // this thread's table chunks of an item: (plane, level, slice) fixed for
+    // the launch; source pointer with the run's tile offset set per run, the
+    // plane row added per item
+    const double* cptr[CPT];
+    int cdst[CPT], cpl[CPT];
+    auto decode = [&](const TileGeom& tg) {
+#pragma unroll
+      for (int r = 0; r < CPT; ++r) {
+        const int j = gt + r * NTG;
+        const bool ok = j < P * NTAB * NCH;
+        const int pl = ok ? j / (NTAB * NCH) : 0;
+        const int jj = ok ? j - pl * NTAB * NCH : 0;
+        const int l = jj / NCH, c = jj - l * NCH;
+        int so, dof;
+        if (c == 0) {
+          so = 0; dof = 0;
+        } else if (c <= A / 2) {
+          so = a.gxo + tg.r0 + 2 * (c - 1); dof = 2 + 2 * (c - 1);
+        } else if (c <= A / 2 + BY / 2) {
+          const int q = c - 1 - A / 2;
+          so = a.gyo + tg.y0 + 2 * q; dof = 2 + A + 2 * q;
+        } else {
+          const int q = c - 1 - A / 2 - BY / 2;
+          so = a.gzo + tg.z0 + 2 * q; dof = 2 + A + BY + 2 * q;
+        }
+        cpl[r] = ok ? pl : -1;
+        cptr[r] = ((FINAL && l == L) ? a.tabR : a.tab[l < L ? l : 0]) + so;
+        cdst[r] = (int)(pl * (PLB / 8) + BOXB / 8) + l * TS + dof;
+      }
+    };
+    // loader state: its own walk over the runs (one item per issue)
+    MsRuns lruns;
+    lruns.init(g0, g1, nx, nlev);
+    int lt = 0, lp0 = 0, lnit = 0, lu = 0;
+    bool lmore = true;
+    TileGeom ltg{};
     int pstg = 0;
     uint32_t pph = 0;
-    const int dist = ns - 2;  // items loaded ahead (group 1 trails by about one item)
-    TileGeom ptg{};
-    // this thread's (at most two) 16-byte table chunks of an item: level,
-    // slice kind and offsets fixed for the launch, the tile offset per run
-    const double* csrc[2];
-    int cdst[2], coff[2], ckind[2];
-    bool cval[2];
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const int j = gt + r * NTG;
-      cval[r] = j < NTAB * NCH;
-      const int l = cval[r] ? j / NCH : 0, c = j - l * NCH;
-      csrc[r] = (FINAL && l == L) ? a.tabR : a.tab[l < L ? l : 0];
-      if (c == 0) {
-        ckind[r] = 0; coff[r] = 0; cdst[r] = 0;
-      } else if (c <= A / 2) {
-        ckind[r] = 1; coff[r] = a.gxo + 2 * (c - 1); cdst[r] = 2 + 2 * (c - 1);
-      } else if (c <= A / 2 + BY / 2) {
-        const int q = c - 1 - A / 2;
-        ckind[r] = 2; coff[r] = a.gyo + 2 * q; cdst[r] = 2 + A + 2 * q;
-      } else {
-        const int q = c - 1 - A / 2 - BY / 2;
-        ckind[r] = 3; coff[r] = a.gzo + 2 * q; cdst[r] = 2 + A + BY + 2 * q;
-      }
-      cdst[r] += l * TS;
-    }
-    int crun[2] = {0, 0};  // coff + the current run's tile offset
     const bool dbox = !(a.dbg & 2);
+    const int dist = ns - 2;  // items loaded ahead (group 1 trails by about one item)
     auto issue_next = [&]() {
-      int pt, pp;
-      bool nr;
-      if (!pseq.next(pt, pp, nr)) return;
-      if (nr) {
-        ptg = tile_geom(T, nvx, pt);
-#pragma unroll
-        for (int r = 0; r < 2; ++r)
-          crun[r] = coff[r] + (ckind[r] == 1 ? ptg.r0 : ckind[r] == 2 ? ptg.y0 : ckind[r] == 3 ? ptg.z0 : 0);
+      if (!lmore) return;
+      if (lu >= lnit) {
+        int lp1;
+        if (!lruns.next(lt, lp0, lp1)) {
+          lmore = false;
+          return;
+        }
+        lnit = (lp1 - lp0) + nlev;
+        lu = 0;
+        ltg = tile_geom(T, nvx, lt);
+        decode(ltg);
       }
-      int i = ptg.down ? nx - 1 - pp : pp;
-      if ((unsigned)i >= (unsigned)nx) i = item_plane(nx, a.bc, ptg, pp);  // halo positions
+      const int n = min(P, lnit - lu);
+      int ip[P];
+#pragma unroll
+      for (int pl = 0; pl < P; ++pl) {
+        const int u = lu + pl;
+        int i = -1;
+        if (pl < n) {
+          const int pp = lp0 - nlev + u;
+          i = ltg.down ? nx - 1 - pp : pp;
+          if ((unsigned)i >= (unsigned)nx) i = item_plane(nx, a.bc, ltg, pp);  // halo positions
+        }
+        ip[pl] = i;
+      }
+      lu += n;
       const int s = pstg;
       // the stage's previous item must be released by group 1
       mbar_wait(&empty[s], pph ^ 1u);
       unsigned char* st = smem + (size_t)s * STAGEB;
       if (gt == 0) {
-        mbar_arrive_expect_tx(&full[s], (i < 0 || SYNTH || !dbox) ? 0u : BOXB);
-        if (i >= 0 && !SYNTH && dbox) tma_load_4d(st, &fmap, ptg.z0, ptg.y0, ptg.r0, i, &full[s]);
-      }
-      if (i >= 0 && !(a.dbg & 1)) {
-        // the table-row slices of every level: 16-byte cp.async chunks (L2 hits)
-        double* dst0 = reinterpret_cast<double*>(st + BOXB);
-        const size_t ro = (size_t)i * a.TL;
+        uint32_t bytes = 0;
 #pragma unroll
-        for (int r = 0; r < 2; ++r)
-          if (cval[r]) cp_async_16(dst0 + cdst[r], csrc[r] + ro + crun[r]);
+        for (int pl = 0; pl < P; ++pl)
+          if (ip[pl] >= 0 && !SYNTH && dbox) bytes += BOXB;
+        mbar_arrive_expect_tx(&full[s], bytes);
+#pragma unroll
+        for (int pl = 0; pl < P; ++pl)
+          if (ip[pl] >= 0 && !SYNTH && dbox)
+            tma_load_4d(st + pl * PLB, &fmap, ltg.z0, ltg.y0, ltg.r0, ip[pl], &full[s]);
+      }
+      if (!(a.dbg & 1)) {
+        // the table-row slices of every level of the item's planes: 16-byte
+        // cp.async chunks (L2 hits)
+#pragma unroll
+        for (int r = 0; r < CPT; ++r) {
+          const int pl = cpl[r];
+          int i = -1;
+#pragma unroll
+          for (int q = 0; q < P; ++q)
+            if (pl == q) i = ip[q];
+          if (i >= 0) cp_async_16(reinterpret_cast<double*>(st) + cdst[r], cptr[r] + (size_t)i * a.TL);
+        }
       }
       cp_async_mbar_arrive(&full[s]);
       if (++pstg == ns) {
@@ -371,21 +415,27 @@ __global__ void __launch_bounds__(ms::NTHR, 1)
       named_sync<NTG>(2);
     }
     for (int q = 0; q < dist; ++q) issue_next();
-    walk([&](int p, int depth, auto fullc) {
+    walk([&](const TileGeom& tg, int t, int p0, int u0, int n, auto fullc) {
       constexpr bool FULLC = decltype(fullc)::value;
-      const int i = FULLC ? (tg.down ? nx - 1 - p : p) : item_plane(nx, a.bc, tg, p);
-      mbar_wait(&full[stg], ph);
-      double* box = reinterpret_cast<double*>(smem + (size_t)stg * STAGEB);
-      if (!FULLC && i < 0) {
-        zero_prev();  // absorbing ghost plane (lead items only): zero flux at every level
-      } else {
+      PBGK_MS_WAIT(&full[stg], ph);
+      const double2* AKr = AK + (tg.r0 + w) * L;
+#pragma unroll 1
+      for (int pl = 0; pl < (FULLC ? P : n); ++pl) {
+        const int u = u0 + pl;
+        const int depth = u < nlev ? u : nlev;
+        const int i = plane_of(tg, p0, u, FULLC);
+        double* box = reinterpret_cast<double*>(smem + (size_t)stg * STAGEB + pl * PLB);
+        if (!FULLC && i < 0) {
+          zero_prev();  // absorbing ghost plane (lead positions only): zero flux at every level
+          continue;
+        }
         const double* tabs = box + BOXB / 8;
         double x[K][4];
         if (!SYNTH) load_x(x, box);
-        levels(x, tabs, depth, fullc, std::integral_constant<int, 0>{});
-        // hand-off to group 1: every item it continues (a run plane, or a
-        // lead item deep enough to reach its levels)
-        if (FULLC || depth == nlev || depth >= LH) {
+        levels(x, tabs, depth, AKr, fullc, std::integral_constant<int, 0>{});
+        // hand-off to group 1: every plane it continues (a run plane, or a
+        // lead position deep enough to reach its levels)
+        if (FULLC || depth == nlev || depth >= LA) {
 #pragma unroll
           for (int k = 0; k < K; ++k) {
             *reinterpret_cast<double2*>(box + boff + k * BZ) = make_double2(x[k][0], x[k][1]);
@@ -406,98 +456,105 @@ __global__ void __launch_bounds__(ms::NTHR, 1)
 
   // ---------------- group 1: levels [LH, L), output ----------------
   int rbuf = 0;
-  walk([&](int p, int depth, auto fullc) {
+  walk([&](const TileGeom& tg, int t, int p0, int u0, int n, auto fullc) {
     constexpr bool FULLC = decltype(fullc)::value;
-    const int i = FULLC ? (tg.down ? nx - 1 - p : p) : item_plane(nx, a.bc, tg, p);
-    mbar_wait(&mid[stg], ph);
-    const double* box = reinterpret_cast<const double*>(smem + (size_t)stg * STAGEB);
-    if (!FULLC && i < 0) {
-      zero_prev();
-    } else if (FULLC || depth == nlev || depth >= LH) {
+    PBGK_MS_WAIT(&mid[stg], ph);
+    const double2* AKr = AK + (tg.r0 + w) * L;
+    const long long goff = ((long long)(tg.r0 + w) * a.nvy + tg.y0 + yl) * a.nvz + tg.z0 + 4 * lz;
+#pragma unroll 1
+    for (int pl = 0; pl < (FULLC ? P : n); ++pl) {
+      const int u = u0 + pl;
+      const int depth = u < nlev ? u : nlev;
+      const int i = plane_of(tg, p0, u, FULLC);
+      const double* box = reinterpret_cast<const double*>(smem + (size_t)stg * STAGEB + pl * PLB);
+      if (!FULLC && i < 0) {
+        zero_prev();
+        continue;
+      }
+      if (!(FULLC || depth == nlev || depth >= LA)) continue;
       const double* tabs = box + BOXB / 8;
       double x[K][4];
       load_x(x, box);
-      levels(x, tabs, depth, fullc, std::integral_constant<int, LH>{});
-      if (FULLC || depth == nlev) {
-        if constexpr (FINAL) {
-          // R_S (ref/kinetic.py:130-134) of the last level's output
-          const double* S = tabs + L * TS;
-          const double2 rl = *reinterpret_cast<const double2*>(S);
-          const double W = rl.y * S[2 + w];
-          const double2 z01 = *reinterpret_cast<const double2*>(S + 2 + A + BY + 4 * lz);
-          const double2 z23 = *reinterpret_cast<const double2*>(S + 2 + A + BY + 4 * lz + 2);
-          const double gz[4] = {z01.x, z01.y, z23.x, z23.y};
+      levels(x, tabs, depth, AKr, fullc, std::integral_constant<int, LA>{});
+      if (!(FULLC || depth == nlev)) continue;
+      if constexpr (FINAL) {
+        // R_S (ref/kinetic.py:130-134) of the last level's output
+        const double* S = tabs + L * TS;
+        const double2 rl = *reinterpret_cast<const double2*>(S);
+        const double W = rl.y * S[2 + w];
+        const double2 z01 = *reinterpret_cast<const double2*>(S + 2 + A + BY + 4 * lz);
+        const double2 z23 = *reinterpret_cast<const double2*>(S + 2 + A + BY + 4 * lz + 2);
+        const double gz[4] = {z01.x, z01.y, z23.x, z23.y};
 #pragma unroll
-          for (int k = 0; k < K; ++k) {
-            const double wk = W * S[2 + A + yl + k];
+        for (int k = 0; k < K; ++k) {
+          const double wk = W * S[2 + A + yl + k];
 #pragma unroll
-            for (int v = 0; v < 4; ++v) x[k][v] = rl.x * fma(wk, gz[v], x[k][v]);
-          }
+          for (int v = 0; v < 4; ++v) x[k][v] = rl.x * fma(wk, gz[v], x[k][v]);
         }
-        if (a.fout != nullptr) {
-          double* d = a.fout + (size_t)i * a.plane + goff;
+      }
+      if (a.fout != nullptr) {
+        double* d = a.fout + (size_t)i * a.plane + goff;
 #pragma unroll
-          for (int k = 0; k < K; ++k)
-            st_global_v4(d + (size_t)k * a.nvz, x[k][0], x[k][1], x[k][2], x[k][3]);
+        for (int k = 0; k < K; ++k)
+          st_global_v4(d + (size_t)k * a.nvz, x[k][0], x[k][1], x[k][2], x[k][3]);
+      }
+      if constexpr (FINAL) {
+        // per-warp partials: line totals (lanes of a line), the row total,
+        // the v_z partials over the warp's lines; fixed trees
+        double lt[K], zs[4];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          lt[k] = (x[k][0] + x[k][1]) + (x[k][2] + x[k][3]);
+          lt[k] += __shfl_xor_sync(0xffffffffu, lt[k], 1);
+          lt[k] += __shfl_xor_sync(0xffffffffu, lt[k], 2);
         }
-        if constexpr (FINAL) {
-          // per-warp partials: line totals (lanes of a line), the row total,
-          // the v_z partials over the warp's lines; fixed trees
-          double lt[K], zs[4];
 #pragma unroll
-          for (int k = 0; k < K; ++k) {
-            lt[k] = (x[k][0] + x[k][1]) + (x[k][2] + x[k][3]);
-            lt[k] += __shfl_xor_sync(0xffffffffu, lt[k], 1);
-            lt[k] += __shfl_xor_sync(0xffffffffu, lt[k], 2);
-          }
+        for (int v = 0; v < 4; ++v) {
+          double s = x[0][v];
 #pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            double s = x[0][v];
-#pragma unroll
-            for (int k = 1; k < K; ++k) s += x[k][v];
-            zs[v] = s;
-          }
-          double rt = lt[0];
-#pragma unroll
-          for (int k = 1; k < K; ++k) rt += lt[k];
-#pragma unroll
-          for (int m = 4; m <= 16; m <<= 1) {
-            rt += __shfl_xor_sync(0xffffffffu, rt, m);
-#pragma unroll
-            for (int v = 0; v < 4; ++v) zs[v] += __shfl_xor_sync(0xffffffffu, zs[v], m);
-          }
-          double* R = RB + (size_t)(rbuf * NW + w) * RS;
-          if (lane == 0) R[0] = rt;
-          if (lz == 0) {
-#pragma unroll
-            for (int k = 0; k < K; ++k) R[1 + yl + k] = lt[k];
-          }
-          if (lg == 0) {
-#pragma unroll
-            for (int v = 0; v < 4; ++v) R[1 + BY + 4 * lz + v] = zs[v];
-          }
-          named_sync<NTG>(1);
-          // the record [m_x rows | m_y | m_z] of (plane i, tile t): rows from
-          // the warps, m_y / m_z summed over the warps in order
-          if (gt < REC) {
-            const double* R0 = RB + (size_t)rbuf * NW * RS;
-            double s;
-            if (gt < A) {
-              s = R0[(size_t)gt * RS];
-              acc += s;
-            } else {
-              const int off = gt < A + BY ? 1 + (gt - A) : 1 + BY + (gt - A - BY);
-              s = R0[off];
-#pragma unroll
-              for (int q = 1; q < NW; ++q) s += R0[(size_t)q * RS + off];
-            }
-            a.part[((size_t)i * T.NT + t) * T.PS + gt] = s;
-          }
-          rbuf ^= 1;
-        } else {
-#pragma unroll
-          for (int k = 0; k < K; ++k) acc += (x[k][0] + x[k][1]) + (x[k][2] + x[k][3]);
+          for (int k = 1; k < K; ++k) s += x[k][v];
+          zs[v] = s;
         }
+        double rt = lt[0];
+#pragma unroll
+        for (int k = 1; k < K; ++k) rt += lt[k];
+#pragma unroll
+        for (int m = 4; m <= 16; m <<= 1) {
+          rt += __shfl_xor_sync(0xffffffffu, rt, m);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) zs[v] += __shfl_xor_sync(0xffffffffu, zs[v], m);
+        }
+        double* R = RB + (size_t)(rbuf * NW + w) * RS;
+        if (lane == 0) R[0] = rt;
+        if (lz == 0) {
+#pragma unroll
+          for (int k = 0; k < K; ++k) R[1 + yl + k] = lt[k];
+        }
+        if (lg == 0) {
+#pragma unroll
+          for (int v = 0; v < 4; ++v) R[1 + BY + 4 * lz + v] = zs[v];
+        }
+        named_sync<NTG>(1);
+        // the record [m_x rows | m_y | m_z] of (plane i, tile t): rows from
+        // the warps, m_y / m_z summed over the warps in order
+        if (gt < REC) {
+          const double* R0 = RB + (size_t)rbuf * NW * RS;
+          double s;
+          if (gt < A) {
+            s = R0[(size_t)gt * RS];
+            acc += s;
+          } else {
+            const int off = gt < A + BY ? 1 + (gt - A) : 1 + BY + (gt - A - BY);
+            s = R0[off];
+#pragma unroll
+            for (int q = 1; q < NW; ++q) s += R0[(size_t)q * RS + off];
+          }
+          a.part[((size_t)i * T.NT + t) * T.PS + gt] = s;
+        }
+        rbuf ^= 1;
+      } else {
+#pragma unroll
+        for (int k = 0; k < K; ++k) acc += (x[k][0] + x[k][1]) + (x[k][2] + x[k][3]);
       }
     }
     __syncwarp();
@@ -510,11 +567,15 @@ __global__ void __launch_bounds__(ms::NTHR, 1)
   if (!isfinite(acc)) atomicMin(a.err, err_key(0, a.step0, kErrNonFiniteMulti));
 }
 
+#ifndef PBGK_MS_P
+#define PBGK_MS_P 1
+#endif
+
 size_t msweep_smem_bytes(int K, int L, int mode, int nvx, int ns) {
   const bool fin = mode & kMsFinal;
   const int BY = ms::by(K), TS = ms::ts(K);
   const size_t box = (size_t)ms::A * BY * ms::BZ * 8;
-  const size_t stage = (box + (size_t)(L + (fin ? 1 : 0)) * TS * 8 + 127) & ~(size_t)127;
+  const size_t stage = PBGK_MS_P * ((box + (size_t)(L + (fin ? 1 : 0)) * TS * 8 + 127) & ~(size_t)127);
   return (size_t)ns * stage + (size_t)L * nvx * 16 + (fin ? 2 * ms::NW * (1 + BY + ms::BZ) * 8 : 0) +
          (size_t)3 * ns * 8;
 }
@@ -543,7 +604,7 @@ int msweep_tiling(int nvx, int nvy, int nvz, int K, Tiling* t) {
 template <int K, int L, int MODE>
 static cudaError_t launch_ms(const CUtensorMap& map, const MSweepArgs& a, int grid, int ns, size_t smem,
                              cudaStream_t st) {
-  auto fn = msweep_kernel<K, L, MODE>;
+  auto fn = msweep_kernel<K, L, MODE, PBGK_MS_P>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (a.prog != nullptr) {
@@ -571,11 +632,9 @@ cudaError_t launch_msweep(int K, int L, int mode, const CUtensorMap& map, const 
   if (K == 2) {
     switch (L) {
       case 4: return launch_ms_mode<2, 4>(mode, map, a, grid, ns, smem, st);
-      case 8: return launch_ms_mode<2, 8>(mode, map, a, grid, ns, smem, st);
     }
   } else if (K == 1) {
     switch (L) {
-      case 4: return launch_ms_mode<1, 4>(mode, map, a, grid, ns, smem, st);
       case 8: return launch_ms_mode<1, 8>(mode, map, a, grid, ns, smem, st);
     }
   }

@@ -92,14 +92,36 @@ def job_cfg1(workers):
          planes_i=np.array([64, 191]), planes=f[[64, 191]], seconds=sec)
 
 
-def job_cfg3a(workers):
+def job_cfg3a(workers, perturb=0.0):
     w = config(3)
     R, g, bc, d, kin, flu = ref_setup(w)
     U0 = R.project(R.lift(R.MomentField(*w.raw_moments()), g), g)
+    if perturb:
+        # the reference's sensitivity to rounding-level differences in its
+        # fine solves: every window jump gets a seeded absolute perturbation
+        # of size `perturb` (what another correct fp64 implementation of F
+        # differs by), the rest of the run unmodified
+        import parabgk.parareal as RP
+        orig = RP._window_jump
+
+        def jump(n, U, *args, **kw):
+            n_, delta, st = orig(n, U, *args, **kw)
+            seed = int(np.frombuffer(np.float64(U.rho[0] + 7 * U.theta[-1]).tobytes(), np.uint64)[0] % 2**32)
+            rng = np.random.default_rng([n, seed])
+            delta = R.MomentField(delta.rho + perturb * rng.uniform(-1, 1, delta.rho.shape),
+                                  delta.u + perturb * rng.uniform(-1, 1, delta.u.shape),
+                                  delta.theta + perturb * rng.uniform(-1, 1, delta.theta.shape))
+            return n_, delta, st
+        RP._window_jump = jump
     tic = time.time()
     traj, rec = R.run_parareal(U0, R.PararealConfig(w.k_max, w.tol, workers=workers), d, kin, flu)
     sec = time.time() - tic
     S = traj.snapshots
+    if perturb:
+        save("cfg3a_pert", perturb=perturb, snap_rho=np.stack([s.rho for s in S]),
+             snap_u=np.stack([s.u for s in S]), snap_theta=np.stack([s.theta for s in S]),
+             errors=np.array([r.error for r in rec]), k=np.array([r.k for r in rec]), seconds=sec)
+        return
     t = d.time.coarse_times
     f = R.lift(S[w.n_g - 1], g)
     f = R.propagate_kinetic(f, float(t[w.n_g - 1]), float(t[w.n_g]), g, kin, bc,
@@ -209,7 +231,9 @@ def job_abs_cfg4x8(workers):
 if __name__ == "__main__":
     job = sys.argv[1]
     nw = int(sys.argv[2]) if len(sys.argv) > 2 else 1
-    if job.startswith("cfg2_e"):
+    if job == "cfg3a_pert":
+        job_cfg3a(nw, perturb=1e-13)
+    elif job.startswith("cfg2_e"):
         job_cfg2(float(job[6:]), nw)
     else:
         globals()["job_" + job](nw)
