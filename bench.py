@@ -49,6 +49,8 @@ def parse():
                     help="override the workload's x boundary")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-parareal", action="store_true",
+                    help="skip the full-run parareal wall time (k_max iterations)")
     ap.add_argument("--xshard", action="store_true",
                     help="fine-only configs: shard the x cells over the ranks (halo exchange per "
                          "step, strong scaling) instead of replicas")
@@ -66,6 +68,37 @@ def peaks():
     return PEAKS_FALLBACK, "fallback"
 
 
+def free_port() -> int:
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    return port
+
+
+def relaunch_if_needed(args):
+    """`--gpus N` without a torchrun environment: re-exec this script under
+    torch.distributed.run with one process per GPU (the reference fans its
+    windows out to worker processes the same way, ref/parareal.py:161-170);
+    a torchrun environment whose WORLD_SIZE disagrees with --gpus is an
+    error, never a silent 1-GPU measurement."""
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is None:
+        if args.gpus > 1:
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                   "--nproc-per-node=%d" % args.gpus, "--master-addr=127.0.0.1",
+                   "--master-port=%d" % free_port(), str(Path(__file__).resolve())] + sys.argv[1:]
+            env = dict(os.environ)
+            env.setdefault("NCCL_DEBUG", "INFO")  # communicator lines: rank count visible in the log
+            env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            raise SystemExit(subprocess.call(cmd, env=env))
+        return
+    if int(world_env) != args.gpus:
+        raise SystemExit("bench.py: --gpus %d but WORLD_SIZE=%s (launch with --nproc-per-node %d)"
+                         % (args.gpus, world_env, args.gpus))
+
+
 def dist_setup(args):
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -76,6 +109,9 @@ def dist_setup(args):
     shared = os.environ.get("PBGK_SHARED_GPU") == "1"
     if shared:
         local = 0
+    elif world > 1 and torch.cuda.device_count() < world:
+        raise SystemExit("bench.py: %d ranks but %d visible GPUs (PBGK_SHARED_GPU=1 shares cuda:0 "
+                         "for development only)" % (world, torch.cuda.device_count()))
     if world > 1:
         torch.cuda.set_device(local)
         if shared:
@@ -84,7 +120,7 @@ def dist_setup(args):
             torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
-    return world, rank, local
+    return world, rank, local, shared
 
 
 class ClockSampler:
@@ -275,8 +311,10 @@ def run_ours(args, w, world, rank, local):
     # dominant kernel: the multi-step sweep (fsweep.cu) when the window ran on
     # the multi-step path, else the one-step sweep (sweep_impl.cuh)
     multi = prof.msweeps > 0 and prof.msweep_ms >= prof.sweep_ms
+    ms_levels = ctx.msweep_levels() if hasattr(ctx, "msweep_levels") else 0
     if multi:
-        kern, kms, kbytes, kn = "fsweep_kernel", prof.msweep_ms, prof.msweep_bytes, prof.msweeps
+        kern = "msweep_kernel" if ms_levels > 0 else "fsweep_kernel"
+        kms, kbytes, kn = prof.msweep_ms, prof.msweep_bytes, prof.msweeps
         bpu = prof.msweep_bytes / (prof.msweep_steps * w.cells)
     else:
         kern, kms, kbytes, kn = "sweep_kernel", prof.sweep_ms, prof.sweep_bytes, prof.sweeps
@@ -307,18 +345,64 @@ def run_ours(args, w, world, rank, local):
             "recursion_share_of_step": share(prof.marg_ms),
             "fine_steps_per_multistep_pass": prof.msweep_steps / prof.msweeps,
             "multistep_sweeps_timed": prof.msweeps,
-            "note": "multi-step path: L fine steps per pass over f (relax tables from the moment "
-                    "recursion), so one cell-update moves 16/L algorithmic bytes; "
-                    "'achieved' is the pass's own f read + write over its time, and the "
-                    "cell-update rate can exceed the one-step 16 B roofline"})
+            "byte_model": "a window of S fine steps runs P = ceil(S/L) passes over f: the first "
+                          "synthesises L(U) and writes f (8 B/cell), passes 2..P-1 read and write "
+                          "f (16 B/cell), the last reads f and writes only the partial records of "
+                          "P(f_S) (8 B/cell): 16 (P-1) B per cell per window, i.e. 16 (P-1)/S "
+                          "B per cell-update (ref: 16 B, one read + one write per step)",
+            "levels_per_pass": ms_levels if ms_levels > 0 else None,
+            "note": "'achieved' / 'frac' are the pass kernel's own algorithmic f bytes over its "
+                    "CUDA-event time; at 8 levels per pass the kernel is bound by its fp64 + "
+                    "shared-memory instruction stream, not by HBM (profiles/), so frac is the "
+                    "HBM share it leaves unused; value_over_one_step_roofline compares the "
+                    "cell-update rate with the one-step design's 16 B/update HBM bound"})
 
     e2e = None
     if not args.no_e2e:
         e2e = e2e_ours(args, w, P, phase, bc, disc, kinetic, fluid, U0, f_init, world, dev,
                        cell_updates, job_updates)
+    par = None
+    if w.mode == "parareal" and not args.no_parareal:
+        par = parareal_full(args, w, P, disc, kinetic, fluid, U0, world, dev)
     roofline["value_over_one_step_roofline"] = value / roofline["one_step_roofline_cell_updates_per_s"]
     return {"value": value, "ms_per_step": ms_per_step, "roofline": roofline, "clocks": clk,
-            "gpu_launches": int(launches), "e2e": e2e}
+            "gpu_launches": int(launches), "e2e": e2e, "parareal": par}
+
+
+def parareal_full(args, w, P, disc, kinetic, fluid, U0, world, dev):
+    """BASELINE's 'parareal wall time': the whole run_parareal (K = the
+    workload's k_max, its tol) through the public API, host moments in and
+    the host trajectory out, wall clock around it (the reference's
+    parareal_seconds, ref/runner.py:76-117), max over ranks."""
+    import torch
+    import torch.distributed as dist
+    U0h = P.MomentField(U0.rho.copy(), U0.u.copy(), U0.theta.copy())
+    cfg = P.PararealConfig(k_max=w.k_max, tol=w.tol, pipelined=args.schedule == "pipelined")
+    seen = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    tic = time.perf_counter()
+    stopped = None
+    try:
+        _, rec = P.run_parareal(U0h, cfg, disc, kinetic, fluid, sink=seen.append)
+        stopped = "tol" if rec and rec[-1].error < w.tol else "k_max"
+    except P.CorrectionOvershootError as e:
+        rec = seen
+        stopped = "CorrectionOvershootError(slice_index=%d) in iteration %d" % (e.slice_index, len(seen) + 1)
+    torch.cuda.synchronize(dev)
+    sec = time.perf_counter() - tic
+    t = torch.tensor([sec], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    sec = float(t.item())
+    iters = len(rec) + (1 if stopped.startswith("Correction") else 0)  # the failing iteration's
+    windows = sum(w.n_g - k + 1 for k in range(1, iters + 1))        # fine stage did run
+    cu = windows * w.cells * w.window_steps()
+    return {"k_max": w.k_max, "tol": w.tol, "iterations_completed": len(rec),
+            "errors": [r.error for r in rec], "stopped": stopped, "wall_s": sec,
+            "windows_propagated": windows, "cell_updates": cu, "cell_updates_per_s": cu / sec,
+            "api": "run_parareal(k_max=%d) host moments in / host trajectory out" % w.k_max}
 
 
 # untimed end-to-end calls before the timed ones: the first two reach the
@@ -393,13 +477,15 @@ def e2e_ours(args, w, P, phase, bc, disc, kinetic, fluid, U0, f_init, world, dev
                    ("SlabFine.propagate (x-sharded)" if args.xshard else "propagate_kinetic")}
 
 
-def cpu_baseline(w, steps=6, cells=4.0e6):
-    from oracle.cpu_bench import slab_rate
-    plane = int(np.prod(w.nv))
-    nx_slab = max(4, int(cells // plane))
-    r = slab_rate(w.nx, w.nv, w.v_max, w.eps, nx_slab, steps, alpha=w.alpha)
+def cpu_baseline(w, budget_cells=1.0e8):
+    """The reference algorithm (the bit-identical oracle port) on this host's
+    cores, run the way the reference runs the workload (oracle/cpu_bench.py):
+    parareal configs as a window pool of whole window jumps, fine-only
+    configs on one core."""
+    from oracle.cpu_bench import workload_rate
+    r = workload_rate(w, budget_cells)
     return {"value": r["value"], "unit": "cell-updates/s", "cores": r["cores"], "kind": "port",
-            "sample": r["sample"], "seconds": r["per_core_s"]}
+            "sample": r["sample"], "seconds": r["seconds"]}
 
 
 def main():
@@ -424,14 +510,13 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        samples = []
         for _ in range(args.warmup):
-            pass  # the CPU port has no warm-up effects beyond process start
-        for _ in range(args.steps):
-            samples.append(cpu_baseline(w, steps=3, cells=2.0e6))
+            cpu_baseline(w)  # warm-up: process pool start-up, page cache, numpy paths
+        samples = [cpu_baseline(w) for _ in range(args.steps)]
         v = float(np.mean([s["value"] for s in samples]))
         line = {"metric": metric, "value": v, "unit": "cell-updates/s", "impl": "reference",
-                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "n_gpus": world if "WORLD_SIZE" in os.environ else args.gpus,
+                "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": float(np.mean([s["seconds"] for s in samples])) * 1e3,
                 "higher_is_better": True,
                 "scaling": "strong" if (w.mode == "parareal" or args.xshard) else "weak",
@@ -443,7 +528,8 @@ def main():
         print(json.dumps(line))
         return
 
-    world, rank, local = dist_setup(args)
+    relaunch_if_needed(args)
+    world, rank, local, shared = dist_setup(args)
     res = run_ours(args, w, world, rank, local)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -455,7 +541,10 @@ def main():
                 "scaling": "strong" if (w.mode == "parareal" or args.xshard) else "weak", "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic (seeded BASELINE.json configs; no dataset)",
                 "config": cfg_json, "roofline": res["roofline"], "cpu_baseline": cpu,
-                "e2e": res["e2e"], "gpu_launches": res["gpu_launches"], "clocks": res["clocks"]}
+                "e2e": res["e2e"], "gpu_launches": res["gpu_launches"], "clocks": res["clocks"],
+                "parareal": res["parareal"]}
+        if shared:
+            line["config"]["shared_gpu"] = "all ranks on cuda:0 with gloo collectives (development only)"
         print(json.dumps(line))
     if world > 1:
         import torch.distributed as dist

@@ -189,6 +189,11 @@ int pbgk_set_fusion(pbgk_ctx* ctx, int levels);
 int pbgk_set_msweep(pbgk_ctx* ctx, int on, int levels);
 /* Levels per pass the round-2 kernel runs on this context (0: not used). */
 int pbgk_msweep_levels(pbgk_ctx* ctx);
+/* Device bytes the multi-step path may spend on per-step relax tables: the
+ * batched windows of pbgk_propagate_windows run in groups that fit (a single
+ * propagation whose tables do not fit runs one-step).  0 = the default
+ * (PBGK_BATCH_BYTES, else 2 GiB).  Results do not depend on the grouping. */
+int pbgk_set_batch_bytes(pbgk_ctx* ctx, double bytes);
 
 /* ---- x-sharded fine propagation (slabs) --------------------------------- */
 /* A context created with bc = 3 is one x-slab of a larger domain (one rank

@@ -50,6 +50,7 @@ PROTOTYPES = {
     "pbgk_set_fusion": (c_int, [_P, _I]),
     "pbgk_set_msweep": (c_int, [_P, _I, _I]),
     "pbgk_msweep_levels": (c_int, [_P]),
+    "pbgk_set_batch_bytes": (c_int, [_P, _D]),
     "pbgk_table_len": (c_int, [_P]),
     "pbgk_propagate_windows": (c_int, [_P, _I, _P, _P, _P, _P, POINTER(c_int), POINTER(c_double),
                                        _D, _D, _P, _D, _P, POINTER(c_longlong)]),

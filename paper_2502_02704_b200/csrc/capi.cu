@@ -88,7 +88,7 @@ int ensure_dev(T*& p, size_t& cap, size_t n, cudaStream_t st) {
 
 // bytes of per-step relax tables the multi-step path may hold (a group of
 // batched windows, or one long propagation)
-double batch_budget() {
+double default_batch_budget() {
   static const double b = getenv("PBGK_BATCH_BYTES") ? atof(getenv("PBGK_BATCH_BYTES")) : 2147483648.0;
   return b;
 }
@@ -213,6 +213,7 @@ struct pbgk_ctx {
   // window's final projection)
   int ms = 1;
   int ms_levels = 0;
+  double batch_bytes = 0.0;  // table budget of the multi-step path (0: the default)
   Tiling ms_t[2] = {};
   double* d_mpart = nullptr;
   size_t mpart_cap = 0;
@@ -221,6 +222,11 @@ struct pbgk_ctx {
 namespace {
 
 std::atomic<long long> g_launches{0};
+
+// bytes of per-step relax tables the multi-step path may hold (a group of
+// batched windows, or one long propagation): the context's setting, else
+// PBGK_BATCH_BYTES, else 2 GiB
+double batch_budget(const pbgk_ctx* c) { return c->batch_bytes > 0.0 ? c->batch_bytes : default_batch_budget(); }
 
 // CUDA-event bracket around one launch when profiling is on.
 struct ProfScope {
@@ -758,7 +764,7 @@ int propagate_body(pbgk_ctx* c, const double* f0, const double* mom0, double* f_
   // (the multi-step path keeps the tables of every step: a very long single
   // propagation whose tables exceed PBGK_BATCH_BYTES stays one-step)
   if (S > 0 && !c->one_step && fused_ok(c, field) &&
-      8.0 * (S + 1) * (double)c->g.nx * c->TL <= batch_budget())
+      8.0 * (S + 1) * (double)c->g.nx * c->TL <= batch_budget(c))
     return propagate_body_fused(c, f0, mom0, f_out, f_tmp, write_final, mom_out, S, h_dts, eps, tau,
                                 E, e_max, st);
   const int pid = field ? 1 : (c->x_scheme == 1 ? 2 : 0);
@@ -1219,7 +1225,7 @@ int windows_fused(pbgk_ctx* c, int nwin, const double* mom_in, double* mom_out, 
     Smax = std::max(Smax, h_nsteps[w]);
     off[w + 1] = off[w] + h_nsteps[w];
   }
-  const double budget = batch_budget();
+  const double budget = batch_budget(c);
   const double per_w = 8.0 * ((double)(Smax + 1) * tstep + 2.0 * qw + 12.0 * nx);
   const int G = std::max(1, std::min(nwin, (int)(budget / per_w)));
   const size_t t_ws = (size_t)(Smax + 1) * tstep;
@@ -1374,7 +1380,7 @@ int pbgk_propagate_windows(pbgk_ctx* c, int nwin, const double* mom_in, double* 
   const bool field = (E != nullptr && e_max > 0.0);
   int smax = 0;
   for (int w = 0; w < nwin; ++w) smax = std::max(smax, h_nsteps[w]);
-  if (fused_ok(c, field) && 8.0 * (smax + 1) * (double)c->g.nx * c->TL <= batch_budget()) {
+  if (fused_ok(c, field) && 8.0 * (smax + 1) * (double)c->g.nx * c->TL <= batch_budget(c)) {
     if (windows_fused(c, nwin, mom_in, mom_out, f_a, f_b, h_nsteps, h_dts, eps, tau, E, e_max, st))
       return -1;
     CK(cudaMemcpyAsync(c->h_keys, c->d_keys, (size_t)nwin * sizeof(ErrKey), cudaMemcpyDeviceToHost, st));
@@ -1586,6 +1592,13 @@ int pbgk_set_msweep(pbgk_ctx* c, int on, int levels) {
 }
 
 int pbgk_msweep_levels(pbgk_ctx* c) { return c ? ms_levels(c) : -1; }
+
+int pbgk_set_batch_bytes(pbgk_ctx* c, double bytes) {
+  if (!c) return fail("null context");
+  if (!(bytes >= 0.0)) return fail("batch bytes must be >= 0");
+  c->batch_bytes = bytes;
+  return 0;
+}
 
 int pbgk_set_grid_reserve(pbgk_ctx* c, int slots) {
   if (!c) return fail("pbgk_set_grid_reserve: null context");

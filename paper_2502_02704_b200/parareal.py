@@ -48,8 +48,9 @@ __all__ = ["PararealConfig", "ConvergenceRecord", "ParTrajectory", "WorkRange",
 class PararealConfig:
     """k_max, tol, frozen-prefix switch, workers (ref/parareal.py:49-65).
 
-    ``workers`` is accepted for compatibility; parallelism here is the GPU
-    itself, plus ranks when torch.distributed is initialised.
+    ``workers`` = parallel fine solvers, here GPU ranks: under
+    torch.distributed it must equal the world size (or be 1); without it, a
+    value > 1 runs on this process's GPU with a RuntimeWarning.
     """
 
     k_max: int
@@ -120,15 +121,53 @@ def estimate_k_opt(t_kin, t_fluid, t_lift, t_proj, n_g, n_p) -> int:
 
 
 class _DeviceExecutor:
-    """Stand-in for the reference's process pool: the GPU is the parallel stage."""
+    """What ``make_executor`` returns: the reference's process pool
+    (ref/parareal.py:161-170) becomes the device itself -- the fine stage of
+    an iteration is one batched launch sequence on this rank's GPU, and the
+    windows are dealt to ranks (one per GPU) when torch.distributed is
+    initialised."""
+
+    def __init__(self, workers: int = 1):
+        self.workers = workers
 
     def shutdown(self, wait: bool = True):
         return None
 
 
 def make_executor(workers, disc, kinetic, fluid):
-    """Compatibility shim for ref/parareal.py:161-170 (no process pool needed)."""
-    return _DeviceExecutor()
+    """ref/parareal.py:161-170: the parallel stage of this implementation (see
+    _DeviceExecutor); `workers` is checked against the rank count."""
+    _check_workers(workers)
+    return _DeviceExecutor(workers)
+
+
+def _world() -> int:
+    dist = torch.distributed
+    return dist.get_world_size() if (dist.is_available() and dist.is_initialized()) else 1
+
+
+def _check_workers(workers: int) -> None:
+    """``workers`` (ref PararealConfig.workers) means parallel fine solvers:
+    here GPU ranks.  Under torch.distributed it must match the world size;
+    without it, a request for several workers runs on this process's GPU and
+    says so (never silently)."""
+    world = _world()
+    if world > 1 and workers not in (1, world):
+        raise ConfigurationError("workers=%d but torch.distributed runs %d ranks (one GPU each)"
+                                 % (workers, world))
+    if world == 1 and workers > 1:
+        import warnings
+        warnings.warn("workers=%d: the fine stage of every iteration runs batched on this "
+                      "process's GPU; launch %d ranks with torchrun (one per GPU) to shard the "
+                      "windows over GPUs" % (workers, workers), RuntimeWarning, stacklevel=3)
+
+
+def _check_executor(executor) -> None:
+    if executor is not None and not isinstance(executor, _DeviceExecutor):
+        raise ConfigurationError(
+            "compute_jumps: the fine stage runs on the GPU (windows dealt to torch.distributed "
+            "ranks, one per GPU); a host executor (%s) cannot run it -- pass executor=None or "
+            "the object make_executor() returns" % type(executor).__name__)
 
 
 # ---------------------------------------------------------------------------
@@ -449,6 +488,7 @@ def initial_coarse_sweep(U0: MomentField, disc, fluid: FluidParams) -> ParTrajec
 def compute_jumps(traj: ParTrajectory, k: int, disc, kinetic, fluid,
                   use_frozen_prefix: bool = True, executor=None, timing=None) -> None:
     """Fill traj.jumps[k-1:] (or all) in place (ref/parareal.py:179-214)."""
+    _check_executor(executor)
     start = k if use_frozen_prefix else 1
     n_g = disc.time.n_g
     if start > n_g:
@@ -504,6 +544,8 @@ def run_parareal(U0: MomentField, config: PararealConfig, disc, kinetic: Kinetic
     every rank must call it with the same arguments; all ranks return the same
     (bitwise) trajectory.
     """
+    if group is None:
+        _check_workers(config.workers)
     b = backend or GpuBackend(disc, kinetic, fluid)
     run = (PipelinedRun if config.pipelined else ShardedRun)(b, group)
     n_g = disc.time.n_g

@@ -120,6 +120,10 @@ class Ctx:
     def msweep_levels(self) -> int:
         return int(self.lib.pbgk_msweep_levels(self.h))
 
+    def set_batch_bytes(self, nbytes: float) -> None:
+        """Table budget of the multi-step path (include/pbgk.h pbgk_set_batch_bytes)."""
+        _lib.check(self.lib.pbgk_set_batch_bytes(self.h, float(nbytes)), "pbgk_set_batch_bytes")
+
     def describe(self) -> str:
         buf = ctypes.create_string_buffer(1024)
         _lib.check(self.lib.pbgk_ctx_describe(self.h, buf, 1024), "pbgk_ctx_describe")
@@ -165,6 +169,26 @@ def ctx_for(grid, bc, device: torch.device | None = None) -> Ctx:
                 c.set_quadrature(1)
             _ctx_cache[key] = c
         return c
+
+
+def release_contexts(device: torch.device | None = None) -> int:
+    """Destroy the cached contexts (all, or those of one device): their device
+    workspace -- the multi-step path's per-step tables, partial records and
+    the f-sized scratch buffers (8.6 GB at config 4) -- goes back to the
+    allocator.  Returns how many were released; later calls create new ones."""
+    with _lock:
+        keys = [k for k, c in _ctx_cache.items() if device is None or c.device == device]
+        for k in keys:
+            c = _ctx_cache.pop(k)
+            c._f_tmp = [None, None]
+            try:
+                torch.cuda.synchronize(c.device)
+                c.lib.pbgk_ctx_destroy(c.h)
+            finally:
+                c.h = None
+    if keys:
+        torch.cuda.empty_cache()
+    return len(keys)
 
 
 # ---------------------------------------------------------------------------

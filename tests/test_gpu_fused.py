@@ -198,11 +198,11 @@ def test_given_f0_non_finite_reports_step_one(levels):
 
 @pytest.mark.parametrize("levels", [2, 3])
 @pytest.mark.parametrize("bc", ["outflow", "periodic"])
-def test_batched_windows_equal_one_step_path(levels, bc, monkeypatch):
+def test_batched_windows_equal_one_step_path(levels, bc):
     # pbgk_propagate_windows runs the recursion of all windows batched (one
     # launch per step, windows of different lengths, an empty one, a failing
-    # one) -- per-window moments and keys as on the one-step path; also with
-    # window groups smaller than the batch (PBGK_BATCH_BYTES)
+    # one) -- per-window moments and keys as on the one-step path (window
+    # groups smaller than the batch: test_gpu_msweep.py)
     from paper_2502_02704_b200.kinetic import propagate_windows
     g, mesh = _grids(10, (16, 16, 16), 8.0)
     kp = P.KineticParams(1e-2)

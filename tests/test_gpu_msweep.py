@@ -230,3 +230,77 @@ def test_parareal_equals_one_step_path():
         assert len(r) == len(r0)
         for a, b in zip(t.snapshots, t0.snapshots):
             assert moment_gap((a.rho, a.u, a.theta), (b.rho, b.u, b.theta)) <= 1e-12
+
+
+@pytest.mark.parametrize("levels", LEVELS)
+def test_batched_windows_in_groups(levels):
+    # a table budget of about two windows (pbgk_set_batch_bytes): the batched
+    # recursion runs in groups of two, the empty and the failing window in the
+    # second group; results as on one group and as on the one-step path
+    from paper_2502_02704_b200.kinetic import propagate_windows
+    g, mesh = _grids(10, (16, 16, 16), 8.0)
+    kp = P.KineticParams(1e-2)
+    ctx = rt.ctx_for(g, P.BoundaryKind.OUTFLOW)
+    cap = stable_dt_kinetic(g, kp)
+    spans = [17.5 * cap, 4.0 * cap, 0.0, 9.2 * cap, 8.0 * cap]
+    rng = np.random.default_rng(13)
+    Us = [random_moments(10, rng) for _ in spans]
+    Us[3][0][4] = np.nan
+    mom_in = torch.stack([rt.to_device_moments(P.MomentField(*U), ctx.device) for U in Us])
+    smax = 18
+    per_window = 8.0 * ((smax + 1) * 10 * P_table_len(ctx) + 2 * 10 * 5 * 16 + 12 * 10)
+    res = []
+    for budget in (0.0, 2.2 * per_window):
+        ctx.set_batch_bytes(budget)
+        out = ctx.empty_moments(len(spans))
+        with ctx.msweep_mode(True, levels):
+            codes = propagate_windows(ctx, mom_in, spans, g, kp, None, out)
+        res.append((out.cpu().numpy(), codes))
+    ctx.set_batch_bytes(0.0)
+    with ctx.fusion_levels(0):
+        out = ctx.empty_moments(len(spans))
+        c0 = propagate_windows(ctx, mom_in, spans, g, kp, None, out)
+        m0 = out.cpu().numpy()
+    (ma, ca), (mb, cb) = res
+    assert ca == cb == c0 and c0[3] != -1 and c0[2] == -1
+    for w in (0, 1, 2, 4):
+        assert np.array_equal(ma[w], mb[w])  # grouping does not change a window's arithmetic
+        assert moment_gap(_unpack(mb[w]), _unpack(m0[w])) <= 1e-13
+
+
+def P_table_len(ctx):
+    return int(ctx.lib.pbgk_table_len(ctx.h))
+
+
+@pytest.mark.parametrize("levels", LEVELS)
+def test_high_transverse_mach_matches_oracle(levels):
+    # the recursion's one-pass transverse variance Q2 - 2 u Q1 + u^2 Q0 loses
+    # about log10(u^2 / theta) digits: a drifting cold state (|u_y| / sqrt
+    # theta = 10, |u_z| / sqrt theta = 8) must still match the oracle's
+    # two-pass projection (ref/moments.py:108-112)
+    nx = 8
+    g, mesh = _grids(nx, (32, 32, 32), 8.0)
+    rng = np.random.default_rng(23)
+    rho = rng.uniform(0.8, 1.2, nx)
+    th = rng.uniform(0.36, 0.44, nx)
+    u = np.zeros((nx, 3))
+    u[:, 0] = rng.uniform(-0.3, 0.3, nx)
+    u[:, 1] = 10.0 * np.sqrt(th) * rng.choice([-1.0, 1.0], nx)
+    u[:, 2] = 8.0 * np.sqrt(th)
+    t1 = 19.5 * O.fine_cap(mesh, 0.5, None)
+    for bc in ("periodic", "outflow"):
+        f, m, code, _ = _window(g, bc, (rho, u, th), t1, levels)
+        assert code == -1
+        want_f = O.fine_propagate(O.lift(rho, u, th, mesh), 0.0, t1, mesh, 1e-2, bc)
+        assert rel_inf(f, want_f) <= 1e-12
+        assert moment_gap(_unpack(m), O.project(want_f, mesh)) <= 1e-12
+
+
+def test_release_contexts_frees_and_recreates():
+    g, mesh = _grids(6, (16, 16, 16), 8.0)
+    U = random_moments(6, np.random.default_rng(3))
+    t1 = 9.5 * O.fine_cap(mesh, 0.5, None)
+    _, m1, c1, _ = _window(g, "periodic", U, t1, 8)
+    assert P.release_contexts() >= 1
+    _, m2, c2, _ = _window(g, "periodic", U, t1, 8)  # a fresh context
+    assert c1 == c2 == -1 and np.array_equal(m1, m2)
