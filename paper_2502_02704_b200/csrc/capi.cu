@@ -32,6 +32,7 @@ int fsweep_ctas_per_sm(int L);
 cudaError_t launch_msweep(int K, int L, int mode, const CUtensorMap& map, const MSweepArgs& a, int grid,
                           int ns, size_t smem, cudaStream_t st);
 size_t msweep_smem_bytes(int K, int L, int mode, int nvx, int ns);
+int msweep_ctas_per_sm();
 int msweep_tiling(int nvx, int nvy, int nvz, int K, Tiling* t);
 cudaError_t launch_marg(const MargArgs& m, const FinalArgs& f, double* gsum, int s, int nwin,
                         cudaStream_t st);
@@ -897,7 +898,7 @@ int ms_levels(pbgk_ctx* c) {
   static const int envl = getenv("PBGK_MS_L") ? atoi(getenv("PBGK_MS_L")) : 0;  // dev A/B knob
   const int L = envl ? envl : (c->ms_levels ? c->ms_levels : 8);
   if (L != 4 && L != 8) return 0;
-  const int K = L > 4 ? 1 : 2;
+  const int K = L > 6 ? 1 : 2;
   if (c->ms_t[K - 1].NT == 0) return 0;
   return L;
 }
@@ -909,7 +910,7 @@ int ms_levels(pbgk_ctx* c) {
 int run_msweep(pbgk_ctx* c, int L, const double* in, double* out, const double* const* tabs,
                const double* tabR, const double* dtdx, int n, int step0, cudaStream_t st,
                const unsigned* prog = nullptr, unsigned need = 0) {
-  const int K = L > 4 ? 1 : 2;
+  const int K = L > 6 ? 1 : 2;
   const Tiling& t = c->ms_t[K - 1];
   MSweepArgs a{};
   a.nx = c->g.nx;
@@ -936,8 +937,6 @@ int run_msweep(pbgk_ctx* c, int L, const double* in, double* out, const double* 
   a.step0 = step0;
   a.prog = prog;
   a.need = need;
-  static const int dbg = getenv("PBGK_MS_DBG") ? atoi(getenv("PBGK_MS_DBG")) : 0;  // dev ablations
-  a.dbg = dbg;
   const int mode = (in == nullptr ? 1 : 0) | (tabR != nullptr ? 2 : 0);
   if (tabR) {
     if (ensure_dev(c->d_mpart, c->mpart_cap, (size_t)c->g.nx * t.NT * t.PS, st)) return -1;
@@ -946,17 +945,19 @@ int run_msweep(pbgk_ctx* c, int L, const double* in, double* out, const double* 
   const CUtensorMap* map = tensor_map(c, in, t, 3);
   if (!map) return fail("tensor map: " + g_last_error);
   static const int ns_env = getenv("PBGK_MS_NS") ? atoi(getenv("PBGK_MS_NS")) : 0;  // dev knob
+  const int per_sm = msweep_ctas_per_sm();
+  const size_t budget = per_sm == 1 ? c->smem_optin : c->smem_per_sm / per_sm - 1024;
   int ns = ns_env > 0 ? ns_env : 12;
-  while (ns > 3 && msweep_smem_bytes(K, L, mode, c->g.nvx, ns) > c->smem_optin) --ns;
+  while (ns > 3 && msweep_smem_bytes(K, L, mode, c->g.nvx, ns) > budget) --ns;
   const size_t smem = msweep_smem_bytes(K, L, mode, c->g.nvx, ns);
-  if (smem > c->smem_optin) return fail("msweep: ring does not fit");
+  if (smem > budget) return fail("msweep: ring does not fit");
   const double fbytes = 8.0 * (double)a.plane * a.nx;
   ProfScope ps(c, st, 2, (in ? fbytes : 0.0) + (out ? fbytes : 0.0), n);
   // one CTA per SM, minus the slots left to side-stream work and the SMs of a
   // concurrent recursion
-  int grid = (int)std::min<long long>(a.total, (long long)c->nsm);
-  int reserve = c->slot_reserve + (prog != nullptr ? c->rec_reserve : 0);
-  grid = std::max(1, std::min(grid, c->nsm - reserve));
+  int grid = (int)std::min<long long>(a.total, (long long)c->nsm * per_sm);
+  int reserve = c->slot_reserve + (prog != nullptr ? c->rec_reserve * per_sm : 0);
+  grid = std::max(1, std::min(grid, c->nsm * per_sm - reserve));
   CK(launch_msweep(K, L, mode, *map, a, grid, ns, smem, st));
   return 0;
 }
@@ -992,7 +993,7 @@ int ms_window(pbgk_ctx* c, int L, const double* f0, double* f_out, double* f_tmp
   }
   if (mom_out) {
     FinalArgs f = fin_args(c, c->plan[0]);
-    f.t = c->ms_t[L > 4 ? 0 : 1];
+    f.t = c->ms_t[L > 6 ? 0 : 1];
     f.part = c->d_mpart;
     f.mode = kFinProject;
     f.mom_out = mom_out;

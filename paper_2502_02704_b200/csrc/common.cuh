@@ -123,7 +123,6 @@ struct MSweepArgs {
   double* part;
   const unsigned* prog;
   unsigned need;
-  int dbg;               // development ablations (PBGK_MS_DBG): 1 no table copies, 2 no box load
 };
 
 // Moment recursion (marginal.cu): five weighted sums of f over (v_y, v_z)

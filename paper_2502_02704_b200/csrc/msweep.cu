@@ -62,14 +62,6 @@ __host__ __device__ constexpr int ts(int K) { return 2 + A + by(K) + BZ; }  // t
 
 enum MsMode : int { kMsSynth = 1, kMsFinal = 2 };
 
-#ifndef PBGK_MS_SLEEP
-#define PBGK_MS_SLEEP 0
-#endif
-#if PBGK_MS_SLEEP
-#define PBGK_MS_WAIT mbar_wait_sleep
-#else
-#define PBGK_MS_WAIT mbar_wait
-#endif
 
 // The item sequence of a CTA's segment [g0, g1) of (tile, plane) positions:
 // every run of consecutive planes of one tile is preceded by `nlev` lead
@@ -101,8 +93,14 @@ __device__ __forceinline__ void named_sync(int id) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(NT_) : "memory");
 }
 
-template <int K, int L, int MODE, int P>
-__global__ void __launch_bounds__(ms::NTHR, 1)
+#ifndef PBGK_MS_NG
+#define PBGK_MS_NG 2
+#endif
+
+// NG = 2: two warp groups split the levels (16 warps, one CTA per SM);
+// NG = 1: one group runs every level (8 warps, two CTAs per SM)
+template <int K, int L, int MODE, int P, int NG>
+__global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
     msweep_kernel(const __grid_constant__ CUtensorMap fmap, const MSweepArgs a, int ns) {
   using namespace ms;
   constexpr bool SYNTH = (MODE & kMsSynth) != 0;
@@ -112,13 +110,18 @@ __global__ void __launch_bounds__(ms::NTHR, 1)
 #endif
   // levels [0, LA) run in group 0 (which also issues the loads), [LA, L) in
   // group 1; LH = the larger share (carry registers)
-  constexpr int LA = PBGK_MS_LA > 0 && PBGK_MS_LA < L ? PBGK_MS_LA : L / 2;
+  constexpr int LA = NG == 1 ? L : (PBGK_MS_LA > 0 && PBGK_MS_LA < L ? PBGK_MS_LA : L / 2);
   constexpr int LH = LA > L - LA ? LA : L - LA;
+  constexpr int NTHR_K = NG * NTG;
   constexpr int BY = by(K);
   constexpr int TS = ts(K);
   constexpr int NTAB = L + (FINAL ? 1 : 0);
-  constexpr uint32_t BOXB = (uint32_t)(A * BY * BZ * 8);  // also the group hand-off area
-  constexpr uint32_t PLB = (BOXB + NTAB * TS * 8 + 127u) & ~127u;  // one plane of a stage
+  constexpr uint32_t BOXB = (uint32_t)(A * BY * BZ * 8);
+  // the group hand-off area of a plane: after its box and tables, not in the
+  // TMA destination (shared stores into the box the async proxy fills cost
+  // ~35 % of the pass, measured)
+  constexpr uint32_t HOFF = (BOXB + NTAB * TS * 8 + 127u) & ~127u;
+  constexpr uint32_t PLB = NG == 2 ? HOFF + BOXB : HOFF;  // one plane of a stage
   constexpr uint32_t STAGEB = P * PLB;
   constexpr int REC = A + BY + BZ;
   constexpr int RS = 1 + BY + BZ;             // per-warp partial block (FINAL)
@@ -141,7 +144,7 @@ __global__ void __launch_bounds__(ms::NTHR, 1)
 
   // transport coefficients per (row, level): a = (dt/dx) |c_x|, keep = 1 - a
   // (up rows: f* = (1-a) f + a f_{i-1}; down rows: (1-a) f + a f_{i+1})
-  for (int j = tid; j < L * nvx; j += NTHR) {
+  for (int j = tid; j < L * nvx; j += NTHR_K) {
     const int jx = j / L, l = j - jx * L;
     const double c = a.cx[jx];
     const double av = a.dtdx[l] * (c < 0.0 ? -c : c);
@@ -167,6 +170,10 @@ __global__ void __launch_bounds__(ms::NTHR, 1)
   const int lz = lane & 3;          // v_z 4 lz .. 4 lz + 3
   const int yl = K * lg;
   const int boff = (w * BY + yl) * BZ + 4 * lz;  // box offset of line 0 (doubles)
+  // a thread's four v_z are held as two pairs, the pair at +2 first for odd
+  // line groups: the two line groups of a quarter warp then hit disjoint
+  // shared-memory banks (box lines are 128 B apart, i.e. bank-aligned)
+  const int h0 = 2 * (lg & 1), h1 = 2 - h0;
 
   double prev[LH][K][4];
 #pragma unroll
@@ -206,25 +213,14 @@ __global__ void __launch_bounds__(ms::NTHR, 1)
           gy[k + 1] = q.y;
         }
       }
-      const double2 z01 = *reinterpret_cast<const double2*>(S + 2 + A + BY + 4 * lz);
-      const double2 z23 = *reinterpret_cast<const double2*>(S + 2 + A + BY + 4 * lz + 2);
+      const double2 z01 = *reinterpret_cast<const double2*>(S + 2 + A + BY + 4 * lz + h0);
+      const double2 z23 = *reinterpret_cast<const double2*>(S + 2 + A + BY + 4 * lz + h1);
       const double gz[4] = {z01.x, z01.y, z23.x, z23.y};
-#ifndef PBGK_MS_EXP
-#define PBGK_MS_EXP 0
-#endif
-#if PBGK_MS_EXP
-      // timing experiment only (wrong results): per-row factors as if
-      // precomputed in the table
-      const double W = gxa;
-      const bool lift0 = SYNTH && l == 0;
-      const double kr = rl.x, ar = rl.y;
-#else
       const double2 ak = AKr[l];  // (keep, a)
       const double W = rl.y * gxa;  // ls gxa
       const bool lift0 = SYNTH && l == 0;
       const double kr = lift0 ? ak.x : ak.x * rl.x;
       const double ar = lift0 ? ak.y : ak.y * rl.x;
-#endif
       if (FULLC || l < depth) {
 #pragma unroll
         for (int k = 0; k < K; ++k) {
@@ -252,8 +248,8 @@ __global__ void __launch_bounds__(ms::NTHR, 1)
   auto load_x = [&](double (&x)[K][4], const double* box) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      const double2 u0 = *reinterpret_cast<const double2*>(box + boff + k * BZ);
-      const double2 u1 = *reinterpret_cast<const double2*>(box + boff + k * BZ + 2);
+      const double2 u0 = *reinterpret_cast<const double2*>(box + boff + k * BZ + h0);
+      const double2 u1 = *reinterpret_cast<const double2*>(box + boff + k * BZ + h1);
       x[k][0] = u0.x; x[k][1] = u0.y; x[k][2] = u1.x; x[k][3] = u1.y;
     }
   };
@@ -292,6 +288,94 @@ __global__ void __launch_bounds__(ms::NTHR, 1)
     const int p = p0 - nlev + u;
     if (interior) return tg.down ? nx - 1 - p : p;
     return item_plane(nx, a.bc, tg, p);
+  };
+
+  // the pass's last level of a run plane: R_S (FINAL), the store, the
+  // partial records (FINAL) or the finiteness sum
+  int rbuf = 0;
+  auto emit = [&](double (&x)[K][4], const double* tabs, int i, int t, long long goff) {
+    if constexpr (FINAL) {
+      // R_S (ref/kinetic.py:130-134) of the last level's output
+      const double* S = tabs + L * TS;
+      const double2 rl = *reinterpret_cast<const double2*>(S);
+      const double W = rl.y * S[2 + w];
+      const double2 z01 = *reinterpret_cast<const double2*>(S + 2 + A + BY + 4 * lz + h0);
+      const double2 z23 = *reinterpret_cast<const double2*>(S + 2 + A + BY + 4 * lz + h1);
+      const double gz[4] = {z01.x, z01.y, z23.x, z23.y};
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const double wk = W * S[2 + A + yl + k];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) x[k][v] = rl.x * fma(wk, gz[v], x[k][v]);
+      }
+    }
+    const bool sw = h0 != 0;  // the thread's pairs in v_z order
+    if (a.fout != nullptr) {
+      double* d = a.fout + (size_t)i * a.plane + goff;
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        st_global_v4(d + (size_t)k * a.nvz, sw ? x[k][2] : x[k][0], sw ? x[k][3] : x[k][1],
+                     sw ? x[k][0] : x[k][2], sw ? x[k][1] : x[k][3]);
+    }
+    if constexpr (FINAL) {
+      // per-warp partials: line totals (lanes of a line), the row total,
+      // the v_z partials over the warp's lines; fixed trees
+      double lt[K], zs[4];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        lt[k] = (x[k][0] + x[k][1]) + (x[k][2] + x[k][3]);
+        lt[k] += __shfl_xor_sync(0xffffffffu, lt[k], 1);
+        lt[k] += __shfl_xor_sync(0xffffffffu, lt[k], 2);
+      }
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int e = sw ? (v ^ 2) : v;  // v_z order
+        double s = x[0][e];
+#pragma unroll
+        for (int k = 1; k < K; ++k) s += x[k][e];
+        zs[v] = s;
+      }
+      double rt = lt[0];
+#pragma unroll
+      for (int k = 1; k < K; ++k) rt += lt[k];
+#pragma unroll
+      for (int m = 4; m <= 16; m <<= 1) {
+        rt += __shfl_xor_sync(0xffffffffu, rt, m);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) zs[v] += __shfl_xor_sync(0xffffffffu, zs[v], m);
+      }
+      double* R = RB + (size_t)(rbuf * NW + w) * RS;
+      if (lane == 0) R[0] = rt;
+      if (lz == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) R[1 + yl + k] = lt[k];
+      }
+      if (lg == 0) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) R[1 + BY + 4 * lz + v] = zs[v];
+      }
+      named_sync<NTG>(1);
+      // the record [m_x rows | m_y | m_z] of (plane i, tile t): rows from
+      // the warps, m_y / m_z summed over the warps in order
+      if (gt < REC) {
+        const double* R0 = RB + (size_t)rbuf * NW * RS;
+        double s;
+        if (gt < A) {
+          s = R0[(size_t)gt * RS];
+          acc += s;
+        } else {
+          const int off = gt < A + BY ? 1 + (gt - A) : 1 + BY + (gt - A - BY);
+          s = R0[off];
+#pragma unroll
+          for (int q = 1; q < NW; ++q) s += R0[(size_t)q * RS + off];
+        }
+        a.part[((size_t)i * T.NT + t) * T.PS + gt] = s;
+      }
+      rbuf ^= 1;
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k) acc += (x[k][0] + x[k][1]) + (x[k][2] + x[k][3]);
+    }
   };
 
   if (grp == 0) {
@@ -334,7 +418,6 @@ __global__ void __launch_bounds__(ms::NTHR, 1)
     TileGeom ltg{};
     int pstg = 0;
     uint32_t pph = 0;
-    const bool dbox = !(a.dbg & 2);
     const int dist = ns - 2;  // items loaded ahead (group 1 trails by about one item)
     auto issue_next = [&]() {
       if (!lmore) return;
@@ -371,14 +454,14 @@ __global__ void __launch_bounds__(ms::NTHR, 1)
         uint32_t bytes = 0;
 #pragma unroll
         for (int pl = 0; pl < P; ++pl)
-          if (ip[pl] >= 0 && !SYNTH && dbox) bytes += BOXB;
+          if (ip[pl] >= 0 && !SYNTH) bytes += BOXB;
         mbar_arrive_expect_tx(&full[s], bytes);
 #pragma unroll
         for (int pl = 0; pl < P; ++pl)
-          if (ip[pl] >= 0 && !SYNTH && dbox)
+          if (ip[pl] >= 0 && !SYNTH)
             tma_load_4d(st + pl * PLB, &fmap, ltg.z0, ltg.y0, ltg.r0, ip[pl], &full[s]);
       }
-      if (!(a.dbg & 1)) {
+      {
         // the table-row slices of every level of the item's planes: 16-byte
         // cp.async chunks (L2 hits)
 #pragma unroll
@@ -417,7 +500,7 @@ __global__ void __launch_bounds__(ms::NTHR, 1)
     for (int q = 0; q < dist; ++q) issue_next();
     walk([&](const TileGeom& tg, int t, int p0, int u0, int n, auto fullc) {
       constexpr bool FULLC = decltype(fullc)::value;
-      PBGK_MS_WAIT(&full[stg], ph);
+      mbar_wait(&full[stg], ph);
       const double2* AKr = AK + (tg.r0 + w) * L;
 #pragma unroll 1
       for (int pl = 0; pl < (FULLC ? P : n); ++pl) {
@@ -433,32 +516,41 @@ __global__ void __launch_bounds__(ms::NTHR, 1)
         double x[K][4];
         if (!SYNTH) load_x(x, box);
         levels(x, tabs, depth, AKr, fullc, std::integral_constant<int, 0>{});
+        if constexpr (NG == 1) {
+          if (FULLC || depth == nlev) {
+            const long long goff =
+                ((long long)(tg.r0 + w) * a.nvy + tg.y0 + yl) * a.nvz + tg.z0 + 4 * lz;
+            emit(x, tabs, i, t, goff);
+          }
+          continue;
+        }
         // hand-off to group 1: every plane it continues (a run plane, or a
         // lead position deep enough to reach its levels)
         if (FULLC || depth == nlev || depth >= LA) {
 #pragma unroll
           for (int k = 0; k < K; ++k) {
-            *reinterpret_cast<double2*>(box + boff + k * BZ) = make_double2(x[k][0], x[k][1]);
-            *reinterpret_cast<double2*>(box + boff + k * BZ + 2) = make_double2(x[k][2], x[k][3]);
+            double* ho = box + HOFF / 8;
+            *reinterpret_cast<double2*>(ho + boff + k * BZ + h0) = make_double2(x[k][0], x[k][1]);
+            *reinterpret_cast<double2*>(ho + boff + k * BZ + h1) = make_double2(x[k][2], x[k][3]);
           }
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&mid[stg]);
+      if (lane == 0) mbar_arrive(NG == 1 ? &empty[stg] : &mid[stg]);
       if (++stg == ns) {
         stg = 0;
         ph ^= 1u;
       }
       issue_next();
     });
+    if (NG == 1 && !isfinite(acc)) atomicMin(a.err, err_key(0, a.step0, kErrNonFiniteMulti));
     return;
   }
 
   // ---------------- group 1: levels [LH, L), output ----------------
-  int rbuf = 0;
   walk([&](const TileGeom& tg, int t, int p0, int u0, int n, auto fullc) {
     constexpr bool FULLC = decltype(fullc)::value;
-    PBGK_MS_WAIT(&mid[stg], ph);
+    mbar_wait(&mid[stg], ph);
     const double2* AKr = AK + (tg.r0 + w) * L;
     const long long goff = ((long long)(tg.r0 + w) * a.nvy + tg.y0 + yl) * a.nvz + tg.z0 + 4 * lz;
 #pragma unroll 1
@@ -474,91 +566,15 @@ __global__ void __launch_bounds__(ms::NTHR, 1)
       if (!(FULLC || depth == nlev || depth >= LA)) continue;
       const double* tabs = box + BOXB / 8;
       double x[K][4];
-      load_x(x, box);
+      load_x(x, box + HOFF / 8);
       levels(x, tabs, depth, AKr, fullc, std::integral_constant<int, LA>{});
       if (!(FULLC || depth == nlev)) continue;
-      if constexpr (FINAL) {
-        // R_S (ref/kinetic.py:130-134) of the last level's output
-        const double* S = tabs + L * TS;
-        const double2 rl = *reinterpret_cast<const double2*>(S);
-        const double W = rl.y * S[2 + w];
-        const double2 z01 = *reinterpret_cast<const double2*>(S + 2 + A + BY + 4 * lz);
-        const double2 z23 = *reinterpret_cast<const double2*>(S + 2 + A + BY + 4 * lz + 2);
-        const double gz[4] = {z01.x, z01.y, z23.x, z23.y};
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          const double wk = W * S[2 + A + yl + k];
-#pragma unroll
-          for (int v = 0; v < 4; ++v) x[k][v] = rl.x * fma(wk, gz[v], x[k][v]);
-        }
-      }
-      if (a.fout != nullptr) {
-        double* d = a.fout + (size_t)i * a.plane + goff;
-#pragma unroll
-        for (int k = 0; k < K; ++k)
-          st_global_v4(d + (size_t)k * a.nvz, x[k][0], x[k][1], x[k][2], x[k][3]);
-      }
-      if constexpr (FINAL) {
-        // per-warp partials: line totals (lanes of a line), the row total,
-        // the v_z partials over the warp's lines; fixed trees
-        double lt[K], zs[4];
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          lt[k] = (x[k][0] + x[k][1]) + (x[k][2] + x[k][3]);
-          lt[k] += __shfl_xor_sync(0xffffffffu, lt[k], 1);
-          lt[k] += __shfl_xor_sync(0xffffffffu, lt[k], 2);
-        }
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          double s = x[0][v];
-#pragma unroll
-          for (int k = 1; k < K; ++k) s += x[k][v];
-          zs[v] = s;
-        }
-        double rt = lt[0];
-#pragma unroll
-        for (int k = 1; k < K; ++k) rt += lt[k];
-#pragma unroll
-        for (int m = 4; m <= 16; m <<= 1) {
-          rt += __shfl_xor_sync(0xffffffffu, rt, m);
-#pragma unroll
-          for (int v = 0; v < 4; ++v) zs[v] += __shfl_xor_sync(0xffffffffu, zs[v], m);
-        }
-        double* R = RB + (size_t)(rbuf * NW + w) * RS;
-        if (lane == 0) R[0] = rt;
-        if (lz == 0) {
-#pragma unroll
-          for (int k = 0; k < K; ++k) R[1 + yl + k] = lt[k];
-        }
-        if (lg == 0) {
-#pragma unroll
-          for (int v = 0; v < 4; ++v) R[1 + BY + 4 * lz + v] = zs[v];
-        }
-        named_sync<NTG>(1);
-        // the record [m_x rows | m_y | m_z] of (plane i, tile t): rows from
-        // the warps, m_y / m_z summed over the warps in order
-        if (gt < REC) {
-          const double* R0 = RB + (size_t)rbuf * NW * RS;
-          double s;
-          if (gt < A) {
-            s = R0[(size_t)gt * RS];
-            acc += s;
-          } else {
-            const int off = gt < A + BY ? 1 + (gt - A) : 1 + BY + (gt - A - BY);
-            s = R0[off];
-#pragma unroll
-            for (int q = 1; q < NW; ++q) s += R0[(size_t)q * RS + off];
-          }
-          a.part[((size_t)i * T.NT + t) * T.PS + gt] = s;
-        }
-        rbuf ^= 1;
-      } else {
-#pragma unroll
-        for (int k = 0; k < K; ++k) acc += (x[k][0] + x[k][1]) + (x[k][2] + x[k][3]);
-      }
+      emit(x, tabs, i, t, goff);
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[stg]);
+    // the stage's shared-memory reads are in registers: a relaxed arrive, so
+    // the warp does not wait for its global stores to complete
+    if (lane == 0) mbar_arrive_relaxed(&empty[stg]);
     if (++stg == ns) {
       stg = 0;
       ph ^= 1u;
@@ -575,12 +591,16 @@ size_t msweep_smem_bytes(int K, int L, int mode, int nvx, int ns) {
   const bool fin = mode & kMsFinal;
   const int BY = ms::by(K), TS = ms::ts(K);
   const size_t box = (size_t)ms::A * BY * ms::BZ * 8;
-  const size_t stage = PBGK_MS_P * ((box + (size_t)(L + (fin ? 1 : 0)) * TS * 8 + 127) & ~(size_t)127);
+  const size_t stage = PBGK_MS_P * (((box + (size_t)(L + (fin ? 1 : 0)) * TS * 8 + 127) & ~(size_t)127) +
+                                    (PBGK_MS_NG == 2 ? box : 0));
   return (size_t)ns * stage + (size_t)L * nvx * 16 + (fin ? 2 * ms::NW * (1 + BY + ms::BZ) * 8 : 0) +
          (size_t)3 * ns * 8;
 }
 
-int msweep_threads() { return ms::NTHR; }
+int msweep_threads() { return PBGK_MS_NG * ms::NTG; }
+
+// CTAs per SM the pass kernel is built for
+int msweep_ctas_per_sm() { return PBGK_MS_NG == 1 ? 2 : 1; }
 
 // Box shape of the kernel for a velocity grid (0 if it does not tile):
 // 8 rows of each c_x sign, 8K v_y, 16 v_z, no partial boxes.
@@ -604,14 +624,14 @@ int msweep_tiling(int nvx, int nvy, int nvz, int K, Tiling* t) {
 template <int K, int L, int MODE>
 static cudaError_t launch_ms(const CUtensorMap& map, const MSweepArgs& a, int grid, int ns, size_t smem,
                              cudaStream_t st) {
-  auto fn = msweep_kernel<K, L, MODE, PBGK_MS_P>;
+  auto fn = msweep_kernel<K, L, MODE, PBGK_MS_P, PBGK_MS_NG>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (a.prog != nullptr) {
-    fn<<<grid, ms::NTHR, smem, st>>>(map, a, ns);
+    fn<<<grid, PBGK_MS_NG * ms::NTG, smem, st>>>(map, a, ns);
     return cudaGetLastError();
   }
-  return launch_pdl(fn, grid, ms::NTHR, smem, st, map, a, ns);
+  return launch_pdl(fn, grid, PBGK_MS_NG * ms::NTG, smem, st, map, a, ns);
 }
 
 template <int K, int L>

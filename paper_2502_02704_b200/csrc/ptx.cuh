@@ -41,21 +41,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-// The same wait with a suspend-time hint: a warp whose phase is not complete
-// sleeps in the barrier instead of spinning through issue slots.
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  uint32_t addr = smem_u32(bar);
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(addr),
-      "r"(parity), "r"(0x10000)
-      : "memory");
-}
-
 // Non-blocking probe of a phase (true once the phase with `parity` completed).
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
@@ -74,6 +59,14 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
 // Plain arrive (release semantics at CTA scope).
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Arrive without release semantics: the arriving thread's earlier memory
+// operations are not ordered before it (for a consumer freeing a stage whose
+// reads are already in registers -- a release would wait for its global
+// stores too).
+__device__ __forceinline__ void mbar_arrive_relaxed(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 // 1-D bulk copy global -> shared, completing on an mbarrier (16-byte granules).
