@@ -125,6 +125,7 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
   constexpr uint32_t STAGEB = P * PLB;
   constexpr int REC = A + BY + BZ;
   constexpr int RS = 1 + BY + BZ;             // per-warp partial block (FINAL)
+  constexpr int FR = 8;                       // FINAL records reduced per barrier
   constexpr int NCH = (2 + A + BY + BZ) / 2;  // 16-byte chunks of one table slice
   constexpr int CPT = (P * NTAB * NCH + NTG - 1) / NTG;  // chunks per loader thread
   extern __shared__ __align__(128) unsigned char smem[];
@@ -134,8 +135,9 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
   const int nx = a.nx, nvx = a.nvx;
   const int nlev = a.nlev;
   double2* AK = reinterpret_cast<double2*>(smem + (size_t)ns * STAGEB);   // [nvx][L] (keep, a)
-  double* RB = reinterpret_cast<double*>(AK + L * nvx);                    // FINAL: [2][NW][RS]
-  uint64_t* full = reinterpret_cast<uint64_t*>(RB + (FINAL ? 2 * NW * RS : 0));
+  double* RB = reinterpret_cast<double*>(AK + L * nvx);                    // FINAL: [2][FR][NW][RS]
+  long long* RI = reinterpret_cast<long long*>(RB + (FINAL ? 2 * FR * NW * RS : 0));  // [2][FR]
+  uint64_t* full = reinterpret_cast<uint64_t*>(RI + (FINAL ? 2 * FR : 0));
   uint64_t* mid = full + ns;
   uint64_t* empty = mid + ns;
 
@@ -290,9 +292,30 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
     return item_plane(nx, a.bc, tg, p);
   };
 
+  // FINAL: the records [m_x rows | m_y | m_z] of a batch of (plane, tile)
+  // items from the per-warp partials -- rows from the warps, m_y / m_z summed
+  // over the warps in order (the same tree for every entry and its mirror)
+  int nfin = 0;
+  auto flush = [&](int set, int cnt) {
+    named_sync<NTG>(1);
+    for (int e = gt; e < cnt * REC; e += NTG) {
+      const int q = e / REC, ent = e - q * REC;
+      const double* R0 = RB + (size_t)(set * FR + q) * NW * RS;
+      double s;
+      if (ent < A) {
+        s = R0[(size_t)ent * RS];
+        acc += s;
+      } else {
+        const int off = ent < A + BY ? 1 + (ent - A) : 1 + BY + (ent - A - BY);
+        s = R0[off];
+#pragma unroll
+        for (int qq = 1; qq < NW; ++qq) s += R0[(size_t)qq * RS + off];
+      }
+      a.part[(size_t)RI[set * FR + q] * T.PS + ent] = s;
+    }
+  };
   // the pass's last level of a run plane: R_S (FINAL), the store, the
   // partial records (FINAL) or the finiteness sum
-  int rbuf = 0;
   auto emit = [&](double (&x)[K][4], const double* tabs, int i, int t, long long goff) {
     if constexpr (FINAL) {
       // R_S (ref/kinetic.py:130-134) of the last level's output
@@ -344,7 +367,10 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
 #pragma unroll
         for (int v = 0; v < 4; ++v) zs[v] += __shfl_xor_sync(0xffffffffu, zs[v], m);
       }
-      double* R = RB + (size_t)(rbuf * NW + w) * RS;
+      // into the batch slot of this record; the records of a batch are
+      // reduced after one barrier (FR records per barrier)
+      const int slot = nfin % FR, set = (nfin / FR) & 1;
+      double* R = RB + ((size_t)(set * FR + slot) * NW + w) * RS;
       if (lane == 0) R[0] = rt;
       if (lz == 0) {
 #pragma unroll
@@ -354,24 +380,8 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
 #pragma unroll
         for (int v = 0; v < 4; ++v) R[1 + BY + 4 * lz + v] = zs[v];
       }
-      named_sync<NTG>(1);
-      // the record [m_x rows | m_y | m_z] of (plane i, tile t): rows from
-      // the warps, m_y / m_z summed over the warps in order
-      if (gt < REC) {
-        const double* R0 = RB + (size_t)rbuf * NW * RS;
-        double s;
-        if (gt < A) {
-          s = R0[(size_t)gt * RS];
-          acc += s;
-        } else {
-          const int off = gt < A + BY ? 1 + (gt - A) : 1 + BY + (gt - A - BY);
-          s = R0[off];
-#pragma unroll
-          for (int q = 1; q < NW; ++q) s += R0[(size_t)q * RS + off];
-        }
-        a.part[((size_t)i * T.NT + t) * T.PS + gt] = s;
-      }
-      rbuf ^= 1;
+      if (gt == 0) RI[set * FR + slot] = (long long)i * T.NT + t;
+      if (++nfin % FR == 0) flush(set, FR);
     } else {
 #pragma unroll
       for (int k = 0; k < K; ++k) acc += (x[k][0] + x[k][1]) + (x[k][2] + x[k][3]);
@@ -543,6 +553,7 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
       }
       issue_next();
     });
+    if (NG == 1 && FINAL && nfin % FR) flush((nfin / FR) & 1, nfin % FR);
     if (NG == 1 && !isfinite(acc)) atomicMin(a.err, err_key(0, a.step0, kErrNonFiniteMulti));
     return;
   }
@@ -580,6 +591,7 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
       ph ^= 1u;
     }
   });
+  if (FINAL && nfin % FR) flush((nfin / FR) & 1, nfin % FR);
   if (!isfinite(acc)) atomicMin(a.err, err_key(0, a.step0, kErrNonFiniteMulti));
 }
 
@@ -593,7 +605,7 @@ size_t msweep_smem_bytes(int K, int L, int mode, int nvx, int ns) {
   const size_t box = (size_t)ms::A * BY * ms::BZ * 8;
   const size_t stage = PBGK_MS_P * (((box + (size_t)(L + (fin ? 1 : 0)) * TS * 8 + 127) & ~(size_t)127) +
                                     (PBGK_MS_NG == 2 ? box : 0));
-  return (size_t)ns * stage + (size_t)L * nvx * 16 + (fin ? 2 * ms::NW * (1 + BY + ms::BZ) * 8 : 0) +
+  return (size_t)ns * stage + (size_t)L * nvx * 16 + (fin ? 2 * 8 * ms::NW * (1 + BY + ms::BZ) * 8 + 2 * 8 * 8 : 0) +
          (size_t)3 * ns * 8;
 }
 
