@@ -170,8 +170,9 @@ int pbgk_set_x_scheme(pbgk_ctx* ctx, int scheme);
  * (v_y, v_z) (the marginal m_x, the folded first moments and the second
  * moments in v_y and v_z) evolve in closed form under the upwind x transport,
  * the v_x field flux and the separable BGK relaxation -- then f is read and
- * written once per `levels` fine steps.  With the v_x field term a pass is
- * one step (the one-step field sweep on the recursion's tables).  Same
+ * written once per `levels` fine steps.  With the v_x field term the passes
+ * are the field-term kernel's (pbgk_set_esweep), else one step each (the
+ * one-step field sweep on the recursion's tables).  Same
  * results as the one-step path to rounding (sums and transport associated
  * differently); 0 = always the one-step path; -1 (default) = the measured
  * best.  `levels` (1..4) applies to the round-1 pass kernel (fsweep.cu);
@@ -189,6 +190,16 @@ int pbgk_set_fusion(pbgk_ctx* ctx, int levels);
 int pbgk_set_msweep(pbgk_ctx* ctx, int on, int levels);
 /* Levels per pass the round-2 kernel runs on this context (0: not used). */
 int pbgk_msweep_levels(pbgk_ctx* ctx);
+/* Multi-step passes WITH the v_x field term (esweep.cu, default on): a warp
+ * owns whole v_x columns and marches an x segment, up to 4 fine steps per
+ * pass (3 at nvx = 32) with the field flux's v_x neighbours in registers /
+ * shuffles.  Needs nvx = 16, 32 or 48 and nvz % 8 == 0 (else, and with
+ * on = 0, the field runs one step per pass).  An explicit pbgk_set_fusion
+ * level count caps its levels.  Replaces ref/kinetic.py:152-160 with a force
+ * (ref/kinetic.py:114-123) like pbgk_propagate. */
+int pbgk_set_esweep(pbgk_ctx* ctx, int on);
+/* Levels per pass of the field-term kernel on this context (0: not used). */
+int pbgk_esweep_levels(pbgk_ctx* ctx);
 /* Device bytes the multi-step path may spend on per-step relax tables: the
  * batched windows of pbgk_propagate_windows run in groups that fit (a single
  * propagation whose tables do not fit runs one-step).  0 = the default

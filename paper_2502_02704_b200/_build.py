@@ -18,7 +18,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIBDIR = PKG / "lib"
 LIB = LIBDIR / "libpbgk.so"
-SOURCES = ["sweep.cu", "sweep_a.cu", "sweep_b.cu", "sweep_c.cu", "finalize.cu", "fluid.cu", "fsweep.cu", "msweep.cu", "marginal.cu", "capi.cu"]
+SOURCES = ["sweep.cu", "sweep_a.cu", "sweep_b.cu", "sweep_c.cu", "finalize.cu", "fluid.cu", "fsweep.cu", "msweep.cu", "esweep.cu", "marginal.cu", "capi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "-I", str(ROOT / "include")]

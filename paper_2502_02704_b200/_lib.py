@@ -49,6 +49,8 @@ PROTOTYPES = {
     "pbgk_set_x_scheme": (c_int, [_P, _I]),
     "pbgk_set_fusion": (c_int, [_P, _I]),
     "pbgk_set_msweep": (c_int, [_P, _I, _I]),
+    "pbgk_set_esweep": (c_int, [_P, _I]),
+    "pbgk_esweep_levels": (c_int, [_P]),
     "pbgk_msweep_levels": (c_int, [_P]),
     "pbgk_set_batch_bytes": (c_int, [_P, _D]),
     "pbgk_table_len": (c_int, [_P]),

@@ -34,6 +34,10 @@ cudaError_t launch_msweep(int K, int L, int mode, const CUtensorMap& map, const 
 size_t msweep_smem_bytes(int K, int L, int mode, int nvx, int ns);
 int msweep_ctas_per_sm();
 int msweep_tiling(int nvx, int nvy, int nvz, int K, Tiling* t);
+int esweep_levels(int nvx, int nvz);
+size_t esweep_smem_bytes(int nvx);
+int esweep_ctas_per_sm(int nvx);
+cudaError_t launch_esweep(const ESweepArgs& a, bool synth, int grid, size_t smem, cudaStream_t st);
 cudaError_t launch_marg(const MargArgs& m, const FinalArgs& f, double* gsum, int s, int nwin,
                         cudaStream_t st);
 size_t marg_state_doubles(int nvx);
@@ -218,6 +222,10 @@ struct pbgk_ctx {
   Tiling ms_t[2] = {};
   double* d_mpart = nullptr;
   size_t mpart_cap = 0;
+  // multi-step passes with the v_x field term (esweep.cu): on/off
+  // (pbgk_set_esweep), CTAs per SM of its build for this nvx (0: unknown yet)
+  int es = 1;
+  int es_per_sm = 0;
 };
 
 namespace {
@@ -1004,6 +1012,77 @@ int ms_window(pbgk_ctx* c, int L, const double* f0, double* f_out, double* f_tmp
   return 0;
 }
 
+// Levels per pass of the field-term passes (esweep.cu): its compiled maximum
+// for this nvx, or fewer under an explicit pbgk_set_fusion; 0 when the shape,
+// scheme or boundary does not run on it (the field then runs one step per
+// pass on the recursion's tables).
+int es_levels(pbgk_ctx* c) {
+  static const int env = getenv("PBGK_ES") ? atoi(getenv("PBGK_ES")) : -1;  // dev A/B knob
+  if (!(env >= 0 ? env : c->es) || c->x_scheme != 0 || c->g.bc > 2) return 0;
+  const int Lmax = esweep_levels(c->g.nvx, c->g.nvz);
+  if (Lmax < 1 || esweep_smem_bytes(c->g.nvx) > c->smem_optin) return 0;
+  if (c->es_per_sm == 0) c->es_per_sm = std::max(0, esweep_ctas_per_sm(c->g.nvx));
+  if (c->es_per_sm < 1) return 0;
+  return c->fuse > 0 ? std::min(c->fuse, Lmax) : Lmax;
+}
+
+// One field-term pass: n levels (steps step0 .. step0+n-1) from `in` (null:
+// SYNTH, level 0 lifts tabs[0]) to `out`.
+int run_esweep(pbgk_ctx* c, int n, const double* in, double* out, const double* const* tabs,
+               const double* dts, const double* E, double e_max, int step0, cudaStream_t st) {
+  ESweepArgs a{};
+  a.nx = c->g.nx;
+  a.nvx = c->g.nvx;
+  a.nvy = c->g.nvy;
+  a.nvz = c->g.nvz;
+  a.fin = in;
+  a.fout = out;
+  for (int l = 0; l < kMaxLevels; ++l) {
+    a.tab[l] = tabs[std::min(l, n - 1)];
+    a.dtdx[l] = l < n ? dts[l] / c->dx : 0.0;
+    a.dtdv[l] = l < n ? dts[l] / c->dv[0] : 0.0;
+  }
+  a.TL = c->TL;
+  a.gyo = c->gyo;
+  a.gzo = c->gzo;
+  a.cx = c->d_c[0];
+  a.E = E;
+  a.half_emax = 0.5 * e_max;
+  a.nlev = n;
+  a.bc = c->g.bc;
+  a.err = c->err_slot ? c->err_slot : c->d_err;
+  a.step0 = step0;
+  const int per_sm = c->es_per_sm;
+  int grid = c->nsm * per_sm;
+  if (c->slot_reserve > 0) grid = std::max(1, grid - (c->slot_reserve + 3) / 4);
+  // items: warp columns x x-segments; the segment count minimising the
+  // busiest warp's positions (its segments plus their 2n halo positions)
+  const int warps = grid * 4;
+  a.ncol = a.nvy * (a.nvz / 8);
+  int best = 1;
+  double best_cost = 1e300;
+  const int smax = std::max(1, std::min(a.nx, 256));
+  for (int ns = 1; ns <= smax; ++ns) {
+    const int len = (a.nx + ns - 1) / ns;
+    const long long items = (long long)a.ncol * ns;
+    const double rounds = (double)((items + warps - 1) / warps);
+    const double cost = rounds * (len + 2 * n);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = ns;
+    }
+  }
+  a.seglen = (a.nx + best - 1) / best;
+  a.nseg = (a.nx + a.seglen - 1) / a.seglen;
+  const long long items = (long long)a.ncol * a.nseg;
+  grid = (int)std::max(1LL, std::min<long long>(grid, (items + 3) / 4));
+  const size_t smem = esweep_smem_bytes(c->g.nvx);
+  const double fbytes = 8.0 * (double)a.nx * a.nvx * a.nvy * a.nvz;
+  ProfScope ps(c, st, 2, (in ? fbytes : 0.0) + fbytes, n);
+  CK(launch_esweep(a, in == nullptr, grid, smem, st));
+  return 0;
+}
+
 // propagate_body on the multi-step path (one window, from moments or a given
 // f0): the moment recursion for all S steps first (one launch when the grid
 // is co-resident), per-step tables; then the passes of up to L steps; the
@@ -1043,7 +1122,8 @@ int propagate_body_fused(pbgk_ctx* c, const double* f0, const double* mom0, doub
                          double* f_tmp, int write_final, double* mom_out, int S, const double* h_dts,
                          double eps, double tau, const double* E, double e_max, cudaStream_t st) {
   const bool field = (E != nullptr && e_max > 0.0);
-  const int L = field ? 1 : fuse_levels(c);
+  const int LE = field ? es_levels(c) : 0;
+  const int L = field ? std::max(LE, 1) : fuse_levels(c);
   const int P = (S + L - 1) / L;  // passes
   const int W = P + (write_final ? 1 : 0);
   auto buf = [&](int w) { return ((W - w) % 2 == 0) ? f_out : f_tmp; };
@@ -1115,7 +1195,10 @@ int propagate_body_fused(pbgk_ctx* c, const double* f0, const double* mom0, doub
         dtdx[l] = h_dts[s0 + l] / c->dx;
       }
       double* out = buf(++w);
-      if (field) {
+      if (field && LE > 0) {
+        // the v_x field term, n levels per pass on the recursion's tables
+        rc = run_esweep(c, n, in, out, tabs, h_dts + s0, E, e_max, s0 + 1, st);
+      } else if (field) {
         // the v_x field term: the one-step sweep (its neighbour-row flux) on
         // the recursion's tables, without the marginal partials
         rc = run_sweep(c, 1, true, in, tabs[0], out, dtdx[0], E, 0.5 * e_max, h_dts[s0] / c->dv[0], s0 + 1,
@@ -1236,7 +1319,8 @@ int windows_fused(pbgk_ctx* c, int nwin, const double* mom_in, double* mom_out, 
       ensure_dev(c->d_bdts, c->bdts_cap, (size_t)std::max(Smax, 1) * G, st) ||
       ensure_dev(c->d_bnst, c->bnst_cap, (size_t)G, st))
     return -1;
-  const int L = field ? 1 : fuse_levels(c);
+  const int LE = field ? es_levels(c) : 0;
+  const int L = field ? std::max(LE, 1) : fuse_levels(c);
   const int LM = field ? 0 : ms_levels(c);
   std::vector<double> hd((size_t)std::max(Smax, 1) * G);
   std::vector<int> hn(G);
@@ -1293,9 +1377,11 @@ int windows_fused(pbgk_ctx* c, int nwin, const double* mom_in, double* mom_out, 
           dtdx[l] = h_dts[off[w] + s0 + l] / c->dx;
         }
         double* out = buf(++wcount);
-        const int rc = field ? run_sweep(c, 1, true, in, tabs[0], out, dtdx[0], E, 0.5 * e_max,
-                                         h_dts[off[w] + s0] / c->dv[0], s0 + 1, st, 1)
-                             : run_fsweep(c, n, in, out, tabs, dtdx, s0 + 1, st);
+        const int rc = (field && LE > 0)
+                           ? run_esweep(c, n, in, out, tabs, h_dts + off[w] + s0, E, e_max, s0 + 1, st)
+                       : field ? run_sweep(c, 1, true, in, tabs[0], out, dtdx[0], E, 0.5 * e_max,
+                                           h_dts[off[w] + s0] / c->dv[0], s0 + 1, st, 1)
+                               : run_fsweep(c, n, in, out, tabs, dtdx, s0 + 1, st);
         if (rc) { c->err_slot = nullptr; return -1; }
         in = out;
         s0 += n;
@@ -1583,6 +1669,14 @@ int pbgk_set_fusion(pbgk_ctx* c, int levels) {
   c->fuse = levels;
   return 0;
 }
+
+int pbgk_set_esweep(pbgk_ctx* c, int on) {
+  if (!c) return fail("null context");
+  c->es = on != 0;
+  return 0;
+}
+
+int pbgk_esweep_levels(pbgk_ctx* c) { return c ? es_levels(c) : 0; }
 
 int pbgk_set_msweep(pbgk_ctx* c, int on, int levels) {
   if (!c) return fail("null context");

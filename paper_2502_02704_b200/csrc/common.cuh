@@ -125,6 +125,28 @@ struct MSweepArgs {
   unsigned need;
 };
 
+// Multi-step sweep with the v_x field term (esweep.cu): up to kMaxLevels
+// levels per pass, a warp per (whole v_x column, x segment) item; tab[l] the
+// relax table applied before level l's transport (SYNTH: fin null, tab[0]
+// the lift tables), dtdx / dtdv per level, E per x cell.
+struct ESweepArgs {
+  int nx, nvx, nvy, nvz;
+  const double* fin;   // null: level 0 synthesises f_0 from tab[0]
+  double* fout;
+  const double* tab[kMaxLevels];
+  int TL, gyo, gzo;
+  const double* cx;
+  const double* E;
+  double half_emax;
+  double dtdx[kMaxLevels], dtdv[kMaxLevels];
+  int nlev;
+  int bc;              // 0 absorbing, 1 periodic, 2 outflow
+  int ncol;            // warp columns: nvy * nvz / 8
+  int nseg, seglen;    // x segments per column and their length (planes)
+  ErrKey* err;
+  int step0;
+};
+
 // Moment recursion (marginal.cu): five weighted sums of f over (v_y, v_z)
 // per x cell and v_x row obey a closed recursion under the upwind x transport
 // and the separable BGK relaxation (both act on a v_x row with coefficients

@@ -120,6 +120,25 @@ class Ctx:
     def msweep_levels(self) -> int:
         return int(self.lib.pbgk_msweep_levels(self.h))
 
+    def set_esweep(self, on: bool) -> None:
+        """Field-term pass kernel of the multi-step path (include/pbgk.h
+        pbgk_set_esweep): several steps per pass (default) or one."""
+        _lib.check(self.lib.pbgk_set_esweep(self.h, int(bool(on))), "pbgk_set_esweep")
+        self.esweep = bool(on)
+
+    @contextlib.contextmanager
+    def esweep_mode(self, on: bool):
+        """Temporarily select the field-term pass kernel (tests / A-B)."""
+        old = getattr(self, "esweep", True)
+        self.set_esweep(on)
+        try:
+            yield self
+        finally:
+            self.set_esweep(old)
+
+    def esweep_levels(self) -> int:
+        return int(self.lib.pbgk_esweep_levels(self.h))
+
     def set_batch_bytes(self, nbytes: float) -> None:
         """Table budget of the multi-step path (include/pbgk.h pbgk_set_batch_bytes)."""
         _lib.check(self.lib.pbgk_set_batch_bytes(self.h, float(nbytes)), "pbgk_set_batch_bytes")
