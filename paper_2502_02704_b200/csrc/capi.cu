@@ -29,11 +29,11 @@ cudaError_t launch_fsweep(int cfg_id, const CUtensorMap& map, const FSweepArgs& 
 size_t fsweep_smem_bytes(const FSweepArgs& a, int V, int LZ, bool synth, int L, int ns);
 bool fsweep_has_cfg(int cfg_id);
 int fsweep_ctas_per_sm(int L);
-cudaError_t launch_msweep(int K, int L, int mode, const CUtensorMap& map, const MSweepArgs& a, int grid,
+cudaError_t launch_msweep(int L, int mode, const CUtensorMap& map, const MSweepArgs& a, int grid,
                           int ns, size_t smem, cudaStream_t st);
-size_t msweep_smem_bytes(int K, int L, int mode, int nvx, int ns);
+size_t msweep_smem_bytes(int L, int mode, int nvx, int ns);
 int msweep_ctas_per_sm();
-int msweep_tiling(int nvx, int nvy, int nvz, int K, Tiling* t);
+int msweep_tiling(int nvx, int nvy, int nvz, Tiling* t);
 int esweep_levels(int nvx, int nvz);
 size_t esweep_smem_bytes(int nvx);
 int esweep_ctas_per_sm(int nvx);
@@ -219,7 +219,7 @@ struct pbgk_ctx {
   int ms = 1;
   int ms_levels = 0;
   double batch_bytes = 0.0;  // table budget of the multi-step path (0: the default)
-  Tiling ms_t[2] = {};
+  Tiling ms_t = {};
   double* d_mpart = nullptr;
   size_t mpart_cap = 0;
   // multi-step passes with the v_x field term (esweep.cu): on/off
@@ -581,8 +581,7 @@ int pbgk_ctx_create(const pbgk_grid_desc* g, pbgk_ctx** out) {
                  getenv("PBGK_FPLAN_CFG") ? atoi(getenv("PBGK_FPLAN_CFG"))  // dev knob
                                           : (g->nvz % 16 == 0 ? 3 : c->plan[0].cfg)))
     return bail(fail("no tiling fits this velocity grid"));
-  for (int k = 1; k <= 2; ++k)
-    if (!msweep_tiling(g->nvx, g->nvy, g->nvz, k, &c->ms_t[k - 1])) c->ms_t[k - 1].NT = 0;
+  if (!msweep_tiling(g->nvx, g->nvy, g->nvz, &c->ms_t)) c->ms_t.NT = 0;
   for (int a = 0; a < 3; ++a) {
     std::vector<double> h(nv[a]);
     for (int j = 0; j < nv[a]; ++j) h[j] = ((double)j - (nv[a] - 1) / 2.0) * c->dv[a];  // ref/grid.py:100-103
@@ -896,8 +895,7 @@ int run_fsweep(pbgk_ctx* c, int n, const double* in, double* out, const double* 
   return 0;
 }
 
-// Round-2 multi-step sweep (msweep.cu): levels per pass and lines per thread
-// (8 levels on 1 line x 4 v_z per thread, 4 levels on 2 lines), or 0 when the
+// Round-2 multi-step sweep (msweep.cu): levels per pass (8, or 4 on request), or 0 when the
 // context's velocity grid / quadrature / scheme does not run on it.
 int ms_levels(pbgk_ctx* c) {
   static const int env = getenv("PBGK_MS") ? atoi(getenv("PBGK_MS")) : -1;  // dev A/B knob
@@ -906,8 +904,7 @@ int ms_levels(pbgk_ctx* c) {
   static const int envl = getenv("PBGK_MS_L") ? atoi(getenv("PBGK_MS_L")) : 0;  // dev A/B knob
   const int L = envl ? envl : (c->ms_levels ? c->ms_levels : 8);
   if (L != 4 && L != 8) return 0;
-  const int K = L > 6 ? 1 : 2;
-  if (c->ms_t[K - 1].NT == 0) return 0;
+  if (c->ms_t.NT == 0) return 0;
   return L;
 }
 
@@ -918,8 +915,7 @@ int ms_levels(pbgk_ctx* c) {
 int run_msweep(pbgk_ctx* c, int L, const double* in, double* out, const double* const* tabs,
                const double* tabR, const double* dtdx, int n, int step0, cudaStream_t st,
                const unsigned* prog = nullptr, unsigned need = 0) {
-  const int K = L > 6 ? 1 : 2;
-  const Tiling& t = c->ms_t[K - 1];
+  const Tiling& t = c->ms_t;
   MSweepArgs a{};
   a.nx = c->g.nx;
   a.nvx = c->g.nvx;
@@ -956,8 +952,8 @@ int run_msweep(pbgk_ctx* c, int L, const double* in, double* out, const double* 
   const int per_sm = msweep_ctas_per_sm();
   const size_t budget = per_sm == 1 ? c->smem_optin : c->smem_per_sm / per_sm - 1024;
   int ns = ns_env > 0 ? ns_env : 12;
-  while (ns > 3 && msweep_smem_bytes(K, L, mode, c->g.nvx, ns) > budget) --ns;
-  const size_t smem = msweep_smem_bytes(K, L, mode, c->g.nvx, ns);
+  while (ns > 3 && msweep_smem_bytes(L, mode, c->g.nvx, ns) > budget) --ns;
+  const size_t smem = msweep_smem_bytes(L, mode, c->g.nvx, ns);
   if (smem > budget) return fail("msweep: ring does not fit");
   const double fbytes = 8.0 * (double)a.plane * a.nx;
   ProfScope ps(c, st, 2, (in ? fbytes : 0.0) + (out ? fbytes : 0.0), n);
@@ -966,7 +962,7 @@ int run_msweep(pbgk_ctx* c, int L, const double* in, double* out, const double* 
   int grid = (int)std::min<long long>(a.total, (long long)c->nsm * per_sm);
   int reserve = c->slot_reserve + (prog != nullptr ? c->rec_reserve * per_sm : 0);
   grid = std::max(1, std::min(grid, c->nsm * per_sm - reserve));
-  CK(launch_msweep(K, L, mode, *map, a, grid, ns, smem, st));
+  CK(launch_msweep(L, mode, *map, a, grid, ns, smem, st));
   return 0;
 }
 
@@ -1001,7 +997,7 @@ int ms_window(pbgk_ctx* c, int L, const double* f0, double* f_out, double* f_tmp
   }
   if (mom_out) {
     FinalArgs f = fin_args(c, c->plan[0]);
-    f.t = c->ms_t[L > 6 ? 0 : 1];
+    f.t = c->ms_t;
     f.part = c->d_mpart;
     f.mode = kFinProject;
     f.mom_out = mom_out;

@@ -6,10 +6,13 @@
 // last level is stored: 16/L bytes of HBM per cell-update), re-laid out for
 // latency hiding and a lean per-element instruction stream:
 //
-//   * box A = 8 v_x rows x BY = 8K v_y x BZ = 16 v_z (16 KB at K = 2); a warp
-//     owns one box row, so the per-row scalars (relax factor, transport
-//     coefficients) are warp-uniform; a thread owns K lines (adjacent v_y) x
-//     4 consecutive v_z.
+//   * box A = 8 v_x rows x BY = 8 v_y x BZ = 16 v_z (8 KB); a warp owns one
+//     box row, so the per-row scalars (relax factor, transport coefficients)
+//     are warp-uniform; a thread owns a 2 x 2 patch (two adjacent v_y lines x
+//     two adjacent v_z): its table factors are two g_y and two g_z, each one
+//     8-byte shared load whose warp-wide footprint is <= 128 B (one data-pipe
+//     cycle; measured with tools/ubench/lds_bench.cu: a 16-byte load whose
+//     lanes differ inside a quarter warp costs four).
 //   * two warp groups split the levels: group 0 runs levels [0, L/2) of plane
 //     p and hands its output to group 1 through the stage's box area (each
 //     thread rewrites exactly the elements it read), group 1 runs levels
@@ -56,8 +59,8 @@ constexpr int BZ = 16;    // v_z per box line (128 B)
 constexpr int NW = A;     // warps per group
 constexpr int NTG = 32 * NW;
 constexpr int NTHR = 2 * NTG;
-__host__ __device__ constexpr int by(int K) { return 8 * K; }
-__host__ __device__ constexpr int ts(int K) { return 2 + A + by(K) + BZ; }  // table slice (doubles)
+constexpr int BY = 8;     // v_y lines per box row
+constexpr int TS = 2 + A + BY + BZ;  // table slice (doubles): r, ls | gxa rows | g_y | g_z
 }  // namespace ms
 
 enum MsMode : int { kMsSynth = 1, kMsFinal = 2 };
@@ -99,7 +102,7 @@ __device__ __forceinline__ void named_sync(int id) {
 
 // NG = 2: two warp groups split the levels (16 warps, one CTA per SM);
 // NG = 1: one group runs every level (8 warps, two CTAs per SM)
-template <int K, int L, int MODE, int P, int NG>
+template <int L, int MODE, int P, int NG>
 __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
     msweep_kernel(const __grid_constant__ CUtensorMap fmap, const MSweepArgs a, int ns) {
   using namespace ms;
@@ -113,8 +116,6 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
   constexpr int LA = NG == 1 ? L : (PBGK_MS_LA > 0 && PBGK_MS_LA < L ? PBGK_MS_LA : L / 2);
   constexpr int LH = LA > L - LA ? LA : L - LA;
   constexpr int NTHR_K = NG * NTG;
-  constexpr int BY = by(K);
-  constexpr int TS = ts(K);
   constexpr int NTAB = L + (FINAL ? 1 : 0);
   constexpr uint32_t BOXB = (uint32_t)(A * BY * BZ * 8);
   // the group hand-off area of a plane: after its box and tables, not in the
@@ -168,22 +169,20 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
   const int gt = tid - grp * NTG;
   const int w = gt >> 5;            // box row
   const int lane = tid & 31;
-  const int lg = lane >> 2;         // line group: lines y = K lg .. K lg + K-1
-  const int lz = lane & 3;          // v_z 4 lz .. 4 lz + 3
-  const int yl = K * lg;
-  const int boff = (w * BY + yl) * BZ + 4 * lz;  // box offset of line 0 (doubles)
-  // a thread's four v_z are held as two pairs, the pair at +2 first for odd
-  // line groups: the two line groups of a quarter warp then hit disjoint
-  // shared-memory banks (box lines are 128 B apart, i.e. bank-aligned)
-  const int h0 = 2 * (lg & 1), h1 = 2 - h0;
+  const int yp = lane >> 3;         // lines y = 2 yp, 2 yp + 1
+  const int zp = lane & 7;          // v_z 2 zp, 2 zp + 1
+  const int yl = 2 * yp;
+  // box offset of the patch (doubles); a quarter warp (one yp) reads one whole
+  // 128-byte box line per 16-byte access: no bank conflicts
+  const int boff = (w * BY + yl) * BZ + 2 * zp;
 
-  double prev[LH][K][4];
+  double prev[LH][2][2];
 #pragma unroll
   for (int l = 0; l < LH; ++l)
 #pragma unroll
-    for (int k = 0; k < K; ++k)
+    for (int k = 0; k < 2; ++k)
 #pragma unroll
-      for (int v = 0; v < 4; ++v) prev[l][k][v] = 0.0;
+      for (int v = 0; v < 2; ++v) prev[l][k][v] = 0.0;
   double acc = 0.0;
   int stg = 0;
   uint32_t ph = 0;
@@ -192,7 +191,7 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
   // (levels < depth) transport; level == depth (a lead position) only
   // relaxes and passes its flux on.  FULLC: a run plane of a full pass (no
   // runtime conditions -- the steady path)
-  auto levels = [&](double (&x)[K][4], const double* tabs, int depth, const double2* AKr, auto fullc,
+  auto levels = [&](double (&x)[2][2], const double* tabs, int depth, const double2* AKr, auto fullc,
                     auto basec) {
     constexpr bool FULLC = decltype(fullc)::value;
     constexpr int BASE = decltype(basec)::value;
@@ -204,20 +203,10 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
       const double* S = tabs + l * TS;
       const double2 rl = *reinterpret_cast<const double2*>(S);  // r, ls
       const double gxa = S[2 + w];
-      double gy[K];
-      if constexpr (K == 1) {
-        gy[0] = S[2 + A + yl];
-      } else {
-#pragma unroll
-        for (int k = 0; k < K; k += 2) {
-          const double2 q = *reinterpret_cast<const double2*>(S + 2 + A + yl + k);
-          gy[k] = q.x;
-          gy[k + 1] = q.y;
-        }
-      }
-      const double2 z01 = *reinterpret_cast<const double2*>(S + 2 + A + BY + 4 * lz + h0);
-      const double2 z23 = *reinterpret_cast<const double2*>(S + 2 + A + BY + 4 * lz + h1);
-      const double gz[4] = {z01.x, z01.y, z23.x, z23.y};
+      // 8-byte loads on purpose (see the header): four / eight distinct
+      // addresses per warp, one data-pipe cycle each
+      const double gy[2] = {lds_f64(S + 2 + A + yl), lds_f64(S + 2 + A + yl + 1)};
+      const double gz[2] = {lds_f64(S + 2 + A + BY + 2 * zp), lds_f64(S + 2 + A + BY + 2 * zp + 1)};
       const double2 ak = AKr[l];  // (keep, a)
       const double W = rl.y * gxa;  // ls gxa
       const bool lift0 = SYNTH && l == 0;
@@ -225,10 +214,10 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
       const double ar = lift0 ? ak.y : ak.y * rl.x;
       if (FULLC || l < depth) {
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
+        for (int k = 0; k < 2; ++k) {
           const double wk = W * gy[k];
 #pragma unroll
-          for (int v = 0; v < 4; ++v) {
+          for (int v = 0; v < 2; ++v) {
             const double z = lift0 ? wk * gz[v] : fma(wk, gz[v], x[k][v]);
             x[k][v] = fma(kr, z, prev[ll][k][v]);
             prev[ll][k][v] = ar * z;
@@ -236,10 +225,10 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
         }
       } else {
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
+        for (int k = 0; k < 2; ++k) {
           const double wk = W * gy[k];
 #pragma unroll
-          for (int v = 0; v < 4; ++v) {
+          for (int v = 0; v < 2; ++v) {
             const double z = lift0 ? wk * gz[v] : fma(wk, gz[v], x[k][v]);
             prev[ll][k][v] = ar * z;
           }
@@ -247,21 +236,21 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
       }
     }
   };
-  auto load_x = [&](double (&x)[K][4], const double* box) {
+  auto load_x = [&](double (&x)[2][2], const double* box) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const double2 u0 = *reinterpret_cast<const double2*>(box + boff + k * BZ + h0);
-      const double2 u1 = *reinterpret_cast<const double2*>(box + boff + k * BZ + h1);
-      x[k][0] = u0.x; x[k][1] = u0.y; x[k][2] = u1.x; x[k][3] = u1.y;
+    for (int k = 0; k < 2; ++k) {
+      const double2 u = *reinterpret_cast<const double2*>(box + boff + k * BZ);
+      x[k][0] = u.x;
+      x[k][1] = u.y;
     }
   };
   auto zero_prev = [&]() {
 #pragma unroll
     for (int l = 0; l < LH; ++l)
 #pragma unroll
-      for (int k = 0; k < K; ++k)
+      for (int k = 0; k < 2; ++k)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) prev[l][k][v] = 0.0;
+        for (int v = 0; v < 2; ++v) prev[l][k][v] = 0.0;
   };
   using TRUE_ = std::integral_constant<bool, true>;
   using FALSE_ = std::integral_constant<bool, false>;
@@ -316,75 +305,62 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
   };
   // the pass's last level of a run plane: R_S (FINAL), the store, the
   // partial records (FINAL) or the finiteness sum
-  auto emit = [&](double (&x)[K][4], const double* tabs, int i, int t, long long goff) {
+  auto emit = [&](double (&x)[2][2], const double* tabs, int i, int t, long long goff) {
     if constexpr (FINAL) {
       // R_S (ref/kinetic.py:130-134) of the last level's output
       const double* S = tabs + L * TS;
       const double2 rl = *reinterpret_cast<const double2*>(S);
       const double W = rl.y * S[2 + w];
-      const double2 z01 = *reinterpret_cast<const double2*>(S + 2 + A + BY + 4 * lz + h0);
-      const double2 z23 = *reinterpret_cast<const double2*>(S + 2 + A + BY + 4 * lz + h1);
-      const double gz[4] = {z01.x, z01.y, z23.x, z23.y};
+      const double gz[2] = {lds_f64(S + 2 + A + BY + 2 * zp), lds_f64(S + 2 + A + BY + 2 * zp + 1)};
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const double wk = W * S[2 + A + yl + k];
+      for (int k = 0; k < 2; ++k) {
+        const double wk = W * lds_f64(S + 2 + A + yl + k);
 #pragma unroll
-        for (int v = 0; v < 4; ++v) x[k][v] = rl.x * fma(wk, gz[v], x[k][v]);
+        for (int v = 0; v < 2; ++v) x[k][v] = rl.x * fma(wk, gz[v], x[k][v]);
       }
     }
-    const bool sw = h0 != 0;  // the thread's pairs in v_z order
     if (a.fout != nullptr) {
       double* d = a.fout + (size_t)i * a.plane + goff;
 #pragma unroll
-      for (int k = 0; k < K; ++k)
-        st_global_v4(d + (size_t)k * a.nvz, sw ? x[k][2] : x[k][0], sw ? x[k][3] : x[k][1],
-                     sw ? x[k][0] : x[k][2], sw ? x[k][1] : x[k][3]);
+      for (int k = 0; k < 2; ++k) st_global_v2(d + (size_t)k * a.nvz, x[k][0], x[k][1]);
     }
     if constexpr (FINAL) {
-      // per-warp partials: line totals (lanes of a line), the row total,
-      // the v_z partials over the warp's lines; fixed trees
-      double lt[K], zs[4];
+      // per-warp partials: line totals (the 8 lanes of a line pair), the row
+      // total, the v_z partials over the warp's lines; fixed butterfly trees
+      // (symmetric under index reversal)
+      double lt[2], zs[2];
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        lt[k] = (x[k][0] + x[k][1]) + (x[k][2] + x[k][3]);
-        lt[k] += __shfl_xor_sync(0xffffffffu, lt[k], 1);
-        lt[k] += __shfl_xor_sync(0xffffffffu, lt[k], 2);
+      for (int k = 0; k < 2; ++k) {
+        lt[k] = x[k][0] + x[k][1];
+#pragma unroll
+        for (int m = 1; m <= 4; m <<= 1) lt[k] += __shfl_xor_sync(0xffffffffu, lt[k], m);
       }
+      double rt = lt[0] + lt[1];
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const int e = sw ? (v ^ 2) : v;  // v_z order
-        double s = x[0][e];
+      for (int v = 0; v < 2; ++v) zs[v] = x[0][v] + x[1][v];
 #pragma unroll
-        for (int k = 1; k < K; ++k) s += x[k][e];
-        zs[v] = s;
-      }
-      double rt = lt[0];
-#pragma unroll
-      for (int k = 1; k < K; ++k) rt += lt[k];
-#pragma unroll
-      for (int m = 4; m <= 16; m <<= 1) {
+      for (int m = 8; m <= 16; m <<= 1) {
         rt += __shfl_xor_sync(0xffffffffu, rt, m);
 #pragma unroll
-        for (int v = 0; v < 4; ++v) zs[v] += __shfl_xor_sync(0xffffffffu, zs[v], m);
+        for (int v = 0; v < 2; ++v) zs[v] += __shfl_xor_sync(0xffffffffu, zs[v], m);
       }
       // into the batch slot of this record; the records of a batch are
       // reduced after one barrier (FR records per barrier)
       const int slot = nfin % FR, set = (nfin / FR) & 1;
       double* R = RB + ((size_t)(set * FR + slot) * NW + w) * RS;
       if (lane == 0) R[0] = rt;
-      if (lz == 0) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) R[1 + yl + k] = lt[k];
+      if (zp == 0) {
+        R[1 + yl] = lt[0];
+        R[1 + yl + 1] = lt[1];
       }
-      if (lg == 0) {
-#pragma unroll
-        for (int v = 0; v < 4; ++v) R[1 + BY + 4 * lz + v] = zs[v];
+      if (yp == 0) {
+        R[1 + BY + 2 * zp] = zs[0];
+        R[1 + BY + 2 * zp + 1] = zs[1];
       }
       if (gt == 0) RI[set * FR + slot] = (long long)i * T.NT + t;
       if (++nfin % FR == 0) flush(set, FR);
     } else {
-#pragma unroll
-      for (int k = 0; k < K; ++k) acc += (x[k][0] + x[k][1]) + (x[k][2] + x[k][3]);
+      acc += (x[0][0] + x[0][1]) + (x[1][0] + x[1][1]);
     }
   };
 
@@ -523,13 +499,13 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
           continue;
         }
         const double* tabs = box + BOXB / 8;
-        double x[K][4];
+        double x[2][2];
         if (!SYNTH) load_x(x, box);
         levels(x, tabs, depth, AKr, fullc, std::integral_constant<int, 0>{});
         if constexpr (NG == 1) {
           if (FULLC || depth == nlev) {
             const long long goff =
-                ((long long)(tg.r0 + w) * a.nvy + tg.y0 + yl) * a.nvz + tg.z0 + 4 * lz;
+                ((long long)(tg.r0 + w) * a.nvy + tg.y0 + yl) * a.nvz + tg.z0 + 2 * zp;
             emit(x, tabs, i, t, goff);
           }
           continue;
@@ -538,10 +514,9 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
         // lead position deep enough to reach its levels)
         if (FULLC || depth == nlev || depth >= LA) {
 #pragma unroll
-          for (int k = 0; k < K; ++k) {
+          for (int k = 0; k < 2; ++k) {
             double* ho = box + HOFF / 8;
-            *reinterpret_cast<double2*>(ho + boff + k * BZ + h0) = make_double2(x[k][0], x[k][1]);
-            *reinterpret_cast<double2*>(ho + boff + k * BZ + h1) = make_double2(x[k][2], x[k][3]);
+            *reinterpret_cast<double2*>(ho + boff + k * BZ) = make_double2(x[k][0], x[k][1]);
           }
         }
       }
@@ -563,7 +538,7 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
     constexpr bool FULLC = decltype(fullc)::value;
     mbar_wait(&mid[stg], ph);
     const double2* AKr = AK + (tg.r0 + w) * L;
-    const long long goff = ((long long)(tg.r0 + w) * a.nvy + tg.y0 + yl) * a.nvz + tg.z0 + 4 * lz;
+    const long long goff = ((long long)(tg.r0 + w) * a.nvy + tg.y0 + yl) * a.nvz + tg.z0 + 2 * zp;
 #pragma unroll 1
     for (int pl = 0; pl < (FULLC ? P : n); ++pl) {
       const int u = u0 + pl;
@@ -576,7 +551,7 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
       }
       if (!(FULLC || depth == nlev || depth >= LA)) continue;
       const double* tabs = box + BOXB / 8;
-      double x[K][4];
+      double x[2][2];
       load_x(x, box + HOFF / 8);
       levels(x, tabs, depth, AKr, fullc, std::integral_constant<int, LA>{});
       if (!(FULLC || depth == nlev)) continue;
@@ -599,14 +574,13 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
 #define PBGK_MS_P 1
 #endif
 
-size_t msweep_smem_bytes(int K, int L, int mode, int nvx, int ns) {
+size_t msweep_smem_bytes(int L, int mode, int nvx, int ns) {
   const bool fin = mode & kMsFinal;
-  const int BY = ms::by(K), TS = ms::ts(K);
-  const size_t box = (size_t)ms::A * BY * ms::BZ * 8;
-  const size_t stage = PBGK_MS_P * (((box + (size_t)(L + (fin ? 1 : 0)) * TS * 8 + 127) & ~(size_t)127) +
+  const size_t box = (size_t)ms::A * ms::BY * ms::BZ * 8;
+  const size_t stage = PBGK_MS_P * (((box + (size_t)(L + (fin ? 1 : 0)) * ms::TS * 8 + 127) & ~(size_t)127) +
                                     (PBGK_MS_NG == 2 ? box : 0));
-  return (size_t)ns * stage + (size_t)L * nvx * 16 + (fin ? 2 * 8 * ms::NW * (1 + BY + ms::BZ) * 8 + 2 * 8 * 8 : 0) +
-         (size_t)3 * ns * 8;
+  return (size_t)ns * stage + (size_t)L * nvx * 16 +
+         (fin ? 2 * 8 * ms::NW * (1 + ms::BY + ms::BZ) * 8 + 2 * 8 * 8 : 0) + (size_t)3 * ns * 8;
 }
 
 int msweep_threads() { return PBGK_MS_NG * ms::NTG; }
@@ -615,28 +589,27 @@ int msweep_threads() { return PBGK_MS_NG * ms::NTG; }
 int msweep_ctas_per_sm() { return PBGK_MS_NG == 1 ? 2 : 1; }
 
 // Box shape of the kernel for a velocity grid (0 if it does not tile):
-// 8 rows of each c_x sign, 8K v_y, 16 v_z, no partial boxes.
-int msweep_tiling(int nvx, int nvy, int nvz, int K, Tiling* t) {
-  const int BY = ms::by(K);
-  if (nvx % (2 * ms::A) != 0 || nvy % BY != 0 || nvz % ms::BZ != 0) return 0;
+// 8 rows of each c_x sign, 8 v_y, 16 v_z, no partial boxes.
+int msweep_tiling(int nvx, int nvy, int nvz, Tiling* t) {
+  if (nvx % (2 * ms::A) != 0 || nvy % ms::BY != 0 || nvz % ms::BZ != 0) return 0;
   t->A = ms::A;
-  t->By = BY;
+  t->By = ms::BY;
   t->Bz = ms::BZ;
   t->rows_load = ms::A;
   t->nneg = nvx / 2;
   t->ntn = t->nneg / ms::A;
   t->ntp = (nvx - t->nneg) / ms::A;
-  t->nty = nvy / BY;
+  t->nty = nvy / ms::BY;
   t->ntz = nvz / ms::BZ;
   t->NT = (t->ntn + t->ntp) * t->nty * t->ntz;
-  t->PS = (ms::A + BY + ms::BZ + 1) & ~1;
+  t->PS = (ms::A + ms::BY + ms::BZ + 1) & ~1;
   return 1;
 }
 
-template <int K, int L, int MODE>
+template <int L, int MODE>
 static cudaError_t launch_ms(const CUtensorMap& map, const MSweepArgs& a, int grid, int ns, size_t smem,
                              cudaStream_t st) {
-  auto fn = msweep_kernel<K, L, MODE, PBGK_MS_P, PBGK_MS_NG>;
+  auto fn = msweep_kernel<L, MODE, PBGK_MS_P, PBGK_MS_NG>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (a.prog != nullptr) {
@@ -646,29 +619,24 @@ static cudaError_t launch_ms(const CUtensorMap& map, const MSweepArgs& a, int gr
   return launch_pdl(fn, grid, PBGK_MS_NG * ms::NTG, smem, st, map, a, ns);
 }
 
-template <int K, int L>
+template <int L>
 static cudaError_t launch_ms_mode(int mode, const CUtensorMap& map, const MSweepArgs& a, int grid, int ns,
                                   size_t smem, cudaStream_t st) {
   switch (mode) {
-    case 0: return launch_ms<K, L, 0>(map, a, grid, ns, smem, st);
-    case kMsSynth: return launch_ms<K, L, kMsSynth>(map, a, grid, ns, smem, st);
-    case kMsFinal: return launch_ms<K, L, kMsFinal>(map, a, grid, ns, smem, st);
-    case kMsSynth | kMsFinal: return launch_ms<K, L, kMsSynth | kMsFinal>(map, a, grid, ns, smem, st);
+    case 0: return launch_ms<L, 0>(map, a, grid, ns, smem, st);
+    case kMsSynth: return launch_ms<L, kMsSynth>(map, a, grid, ns, smem, st);
+    case kMsFinal: return launch_ms<L, kMsFinal>(map, a, grid, ns, smem, st);
+    case kMsSynth | kMsFinal: return launch_ms<L, kMsSynth | kMsFinal>(map, a, grid, ns, smem, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
 // L: compiled level counts (a pass may run fewer, a.nlev <= L)
-cudaError_t launch_msweep(int K, int L, int mode, const CUtensorMap& map, const MSweepArgs& a, int grid,
-                          int ns, size_t smem, cudaStream_t st) {
-  if (K == 2) {
-    switch (L) {
-      case 4: return launch_ms_mode<2, 4>(mode, map, a, grid, ns, smem, st);
-    }
-  } else if (K == 1) {
-    switch (L) {
-      case 8: return launch_ms_mode<1, 8>(mode, map, a, grid, ns, smem, st);
-    }
+cudaError_t launch_msweep(int L, int mode, const CUtensorMap& map, const MSweepArgs& a, int grid, int ns,
+                          size_t smem, cudaStream_t st) {
+  switch (L) {
+    case 4: return launch_ms_mode<4>(mode, map, a, grid, ns, smem, st);
+    case 8: return launch_ms_mode<8>(mode, map, a, grid, ns, smem, st);
   }
   return cudaErrorInvalidValue;
 }

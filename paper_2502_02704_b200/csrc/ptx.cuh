@@ -154,6 +154,15 @@ __device__ __forceinline__ void prefetch_tensormap(const CUtensorMap* map) {
 }
 
 // Streaming 128-bit store (f is written once per sweep and re-read next sweep).
+// one 8-byte shared load that stays 8 bytes wide (the compiler would fuse two
+// adjacent ones into a 16-byte load, which costs more data-pipe cycles when
+// lanes of a quarter warp read different addresses)
+__device__ __forceinline__ double lds_f64(const double* p) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(smem_u32(p)));
+  return v;
+}
+
 __device__ __forceinline__ void st_global_v2(double* p, double a, double b) {
   asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
 }
