@@ -22,8 +22,9 @@
 //     130-134):  z = x + (ls gxa gy) gz,  out = (keep r) z + q_prev,
 //     q = (a r) z,  with a = (dt/dx)|c_x| and keep = 1 - a: the reference's
 //     f* = f - (dt/dx)(F_i+1 - F_i) after f = r (f* + ls M), re-associated (a
-//     few ulps; the multi-step path is held to the oracle at 1e-12).  (keep,
-//     a) per (v_x row, level) sit in a shared table computed once per launch.
+//     few ulps; the multi-step path is held to the oracle at 1e-12).  a per
+//     (v_x row, level) sits in a shared table computed once per launch;
+//     a r and keep r = r - a r per warp and level.
 //   * loads: thread 0 of group 0 issues the TMA box of a plane, every group-0
 //     thread one 16-byte cp.async chunk of the table-row slices the tile needs
 //     (r, ls | gxa of its rows | gy | gz per level: 0.3 KB instead of whole
@@ -50,6 +51,17 @@
 #include "common.cuh"
 #include "ptx.cuh"
 #include "sweep_impl.cuh"
+
+// development A/B knobs (tools/ab_ms.sh)
+#ifndef PBGK_MS_ZSPLIT
+#define PBGK_MS_ZSPLIT 0
+#endif
+#ifndef PBGK_MS_GYASM
+#define PBGK_MS_GYASM 1
+#endif
+#ifndef PBGK_MS_AONLY
+#define PBGK_MS_AONLY 1
+#endif
 
 namespace pbgk {
 
@@ -113,7 +125,9 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
 #endif
   // levels [0, LA) run in group 0 (which also issues the loads), [LA, L) in
   // group 1; LH = the larger share (carry registers)
-  constexpr int LA = NG == 1 ? L : (PBGK_MS_LA > 0 && PBGK_MS_LA < L ? PBGK_MS_LA : L / 2);
+  // (measured on config 4, 8 levels: 3 + 5 is 6 % faster than 4 + 4 -- group 0
+  // also walks the loader; 2 + 6 spills)
+  constexpr int LA = NG == 1 ? L : (PBGK_MS_LA > 0 && PBGK_MS_LA < L ? PBGK_MS_LA : (L == 8 ? 3 : L / 2));
   constexpr int LH = LA > L - LA ? LA : L - LA;
   constexpr int NTHR_K = NG * NTG;
   constexpr int NTAB = L + (FINAL ? 1 : 0);
@@ -135,8 +149,8 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
   const int tid = threadIdx.x;
   const int nx = a.nx, nvx = a.nvx;
   const int nlev = a.nlev;
-  double2* AK = reinterpret_cast<double2*>(smem + (size_t)ns * STAGEB);   // [nvx][L] (keep, a)
-  double* RB = reinterpret_cast<double*>(AK + L * nvx);                    // FINAL: [2][FR][NW][RS]
+  double* AK = reinterpret_cast<double*>(smem + (size_t)ns * STAGEB);     // [nvx][L] a = (dt/dx)|c_x|
+  double* RB = reinterpret_cast<double*>(AK + L * nvx * (PBGK_MS_AONLY ? 1 : 2));                    // FINAL: [2][FR][NW][RS]
   long long* RI = reinterpret_cast<long long*>(RB + (FINAL ? 2 * FR * NW * RS : 0));  // [2][FR]
   uint64_t* full = reinterpret_cast<uint64_t*>(RI + (FINAL ? 2 * FR : 0));
   uint64_t* mid = full + ns;
@@ -151,7 +165,11 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
     const int jx = j / L, l = j - jx * L;
     const double c = a.cx[jx];
     const double av = a.dtdx[l] * (c < 0.0 ? -c : c);
-    AK[j] = make_double2(1.0 - av, av);
+#if PBGK_MS_AONLY
+    AK[j] = av;
+#else
+    reinterpret_cast<double2*>(AK)[j] = make_double2(1.0 - av, av);
+#endif
   }
   if (tid == 0) {
     for (int s = 0; s < ns; ++s) {
@@ -170,11 +188,14 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
   const int w = gt >> 5;            // box row
   const int lane = tid & 31;
   const int yp = lane >> 3;         // lines y = 2 yp, 2 yp + 1
-  const int zp = lane & 7;          // v_z 2 zp, 2 zp + 1
+  const int zp = lane & 7;          // v_z zp and zp + 8: not adjacent, so the two g_z loads of a
+                                    // level stay 8 bytes wide (ptxas fuses adjacent ones)
   const int yl = 2 * yp;
-  // box offset of the patch (doubles); a quarter warp (one yp) reads one whole
-  // 128-byte box line per 16-byte access: no bank conflicts
-  const int boff = (w * BY + yl) * BZ + 2 * zp;
+  // box offset of the patch (doubles); a quarter warp (one yp) reads half a
+  // 128-byte box line per 8-byte access: no bank conflicts
+  constexpr int ZM = PBGK_MS_ZSPLIT ? 1 : 2, ZS = PBGK_MS_ZSPLIT ? 8 : 1;  // v_z of element v: ZM zp + ZS v
+  const int zo = ZM * zp;
+  const int boff = (w * BY + yl) * BZ + zo;
 
   double prev[LH][2][2];
 #pragma unroll
@@ -191,7 +212,7 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
   // (levels < depth) transport; level == depth (a lead position) only
   // relaxes and passes its flux on.  FULLC: a run plane of a full pass (no
   // runtime conditions -- the steady path)
-  auto levels = [&](double (&x)[2][2], const double* tabs, int depth, const double2* AKr, auto fullc,
+  auto levels = [&](double (&x)[2][2], const double* tabs, int depth, const double* AKr, auto fullc,
                     auto basec) {
     constexpr bool FULLC = decltype(fullc)::value;
     constexpr int BASE = decltype(basec)::value;
@@ -203,15 +224,29 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
       const double* S = tabs + l * TS;
       const double2 rl = *reinterpret_cast<const double2*>(S);  // r, ls
       const double gxa = S[2 + w];
-      // 8-byte loads on purpose (see the header): four / eight distinct
-      // addresses per warp, one data-pipe cycle each
+#if PBGK_MS_GYASM
       const double gy[2] = {lds_f64(S + 2 + A + yl), lds_f64(S + 2 + A + yl + 1)};
-      const double gz[2] = {lds_f64(S + 2 + A + BY + 2 * zp), lds_f64(S + 2 + A + BY + 2 * zp + 1)};
-      const double2 ak = AKr[l];  // (keep, a)
+      const double gz[2] = {lds_f64(S + 2 + A + BY + zo), lds_f64(S + 2 + A + BY + zo + ZS)};
+#else
+      const double2 gyp = *reinterpret_cast<const double2*>(S + 2 + A + yl);  // uniform per quarter warp
+      const double gy[2] = {gyp.x, gyp.y};
+      const double gz[2] = {S[2 + A + BY + zo], S[2 + A + BY + zo + ZS]};
+#endif
+#if PBGK_MS_AONLY
+      const double av = AKr[l];
+#else
+      const double2 ak = reinterpret_cast<const double2*>(AKr)[l];
+#endif
       const double W = rl.y * gxa;  // ls gxa
       const bool lift0 = SYNTH && l == 0;
+      // (a r, (1 - a) r) as a r and r - a r
+#if PBGK_MS_AONLY
+      const double ar = lift0 ? av : av * rl.x;
+      const double kr = (lift0 ? 1.0 : rl.x) - ar;
+#else
       const double kr = lift0 ? ak.x : ak.x * rl.x;
       const double ar = lift0 ? ak.y : ak.y * rl.x;
+#endif
       if (FULLC || l < depth) {
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
@@ -239,9 +274,8 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
   auto load_x = [&](double (&x)[2][2], const double* box) {
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-      const double2 u = *reinterpret_cast<const double2*>(box + boff + k * BZ);
-      x[k][0] = u.x;
-      x[k][1] = u.y;
+      x[k][0] = box[boff + k * BZ];
+      x[k][1] = box[boff + k * BZ + ZS];
     }
   };
   auto zero_prev = [&]() {
@@ -311,10 +345,10 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
       const double* S = tabs + L * TS;
       const double2 rl = *reinterpret_cast<const double2*>(S);
       const double W = rl.y * S[2 + w];
-      const double gz[2] = {lds_f64(S + 2 + A + BY + 2 * zp), lds_f64(S + 2 + A + BY + 2 * zp + 1)};
+      const double gz[2] = {S[2 + A + BY + zo], S[2 + A + BY + zo + ZS]};
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
-        const double wk = W * lds_f64(S + 2 + A + yl + k);
+        const double wk = W * S[2 + A + yl + k];
 #pragma unroll
         for (int v = 0; v < 2; ++v) x[k][v] = rl.x * fma(wk, gz[v], x[k][v]);
       }
@@ -322,7 +356,10 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
     if (a.fout != nullptr) {
       double* d = a.fout + (size_t)i * a.plane + goff;
 #pragma unroll
-      for (int k = 0; k < 2; ++k) st_global_v2(d + (size_t)k * a.nvz, x[k][0], x[k][1]);
+      for (int k = 0; k < 2; ++k) {
+        d[(size_t)k * a.nvz] = x[k][0];
+        d[(size_t)k * a.nvz + ZS] = x[k][1];
+      }
     }
     if constexpr (FINAL) {
       // per-warp partials: line totals (the 8 lanes of a line pair), the row
@@ -354,8 +391,8 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
         R[1 + yl + 1] = lt[1];
       }
       if (yp == 0) {
-        R[1 + BY + 2 * zp] = zs[0];
-        R[1 + BY + 2 * zp + 1] = zs[1];
+        R[1 + BY + zo] = zs[0];
+        R[1 + BY + zo + ZS] = zs[1];
       }
       if (gt == 0) RI[set * FR + slot] = (long long)i * T.NT + t;
       if (++nfin % FR == 0) flush(set, FR);
@@ -487,7 +524,7 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
     walk([&](const TileGeom& tg, int t, int p0, int u0, int n, auto fullc) {
       constexpr bool FULLC = decltype(fullc)::value;
       mbar_wait(&full[stg], ph);
-      const double2* AKr = AK + (tg.r0 + w) * L;
+      const double* AKr = AK + (tg.r0 + w) * L * (PBGK_MS_AONLY ? 1 : 2);
 #pragma unroll 1
       for (int pl = 0; pl < (FULLC ? P : n); ++pl) {
         const int u = u0 + pl;
@@ -505,7 +542,7 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
         if constexpr (NG == 1) {
           if (FULLC || depth == nlev) {
             const long long goff =
-                ((long long)(tg.r0 + w) * a.nvy + tg.y0 + yl) * a.nvz + tg.z0 + 2 * zp;
+                ((long long)(tg.r0 + w) * a.nvy + tg.y0 + yl) * a.nvz + tg.z0 + zo;
             emit(x, tabs, i, t, goff);
           }
           continue;
@@ -516,7 +553,8 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
 #pragma unroll
           for (int k = 0; k < 2; ++k) {
             double* ho = box + HOFF / 8;
-            *reinterpret_cast<double2*>(ho + boff + k * BZ) = make_double2(x[k][0], x[k][1]);
+            ho[boff + k * BZ] = x[k][0];
+            ho[boff + k * BZ + ZS] = x[k][1];
           }
         }
       }
@@ -537,8 +575,8 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
   walk([&](const TileGeom& tg, int t, int p0, int u0, int n, auto fullc) {
     constexpr bool FULLC = decltype(fullc)::value;
     mbar_wait(&mid[stg], ph);
-    const double2* AKr = AK + (tg.r0 + w) * L;
-    const long long goff = ((long long)(tg.r0 + w) * a.nvy + tg.y0 + yl) * a.nvz + tg.z0 + 2 * zp;
+    const double* AKr = AK + (tg.r0 + w) * L * (PBGK_MS_AONLY ? 1 : 2);
+    const long long goff = ((long long)(tg.r0 + w) * a.nvy + tg.y0 + yl) * a.nvz + tg.z0 + zo;
 #pragma unroll 1
     for (int pl = 0; pl < (FULLC ? P : n); ++pl) {
       const int u = u0 + pl;
