@@ -115,13 +115,12 @@ template <int V, int L, bool SYNTH, int D>
 __global__ void __launch_bounds__(es::NTHR, 2)
     esweep_kernel(const __grid_constant__ ESweepArgs a) {
   using namespace es;
+  constexpr int H = V / 2;    // rows of each c_x sign per lane
   constexpr int SL = slice(V);
   constexpr int NX8 = 8 * V;  // nvx
   constexpr uint32_t STB = (uint32_t)stage_bytes(V, L);
   constexpr uint32_t FB = 32u * V * 16u;  // f area of a stage
   extern __shared__ __align__(128) unsigned char smem[];
-  double2* AK = reinterpret_cast<double2*>(smem);  // [L][nvx] (kappa_interior, a)
-  unsigned char* ring0 = smem + (size_t)L * NX8 * sizeof(double2);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -131,49 +130,55 @@ __global__ void __launch_bounds__(es::NTHR, 2)
   const bool periodic = a.bc == 1;
   const bool outflow = a.bc == 2;
 
-  for (int j = tid; j < L * NX8; j += NTHR) {
-    const int l = j / NX8, jx = j - l * NX8;
-    const double cv = a.cx[jx];
-    const double av = a.dtdx[l] * (cv < 0.0 ? -cv : cv);
-    AK[j] = make_double2(1.0 - av - a.dtdv[l] * (2.0 * a.half_emax), av);
-  }
   pdl_wait();
   pdl_trigger();
-  __syncthreads();
 
-  unsigned char* ring = ring0 + (size_t)warp * D * STB;
+  unsigned char* ring = smem + (size_t)warp * D * STB;
   const int gw = blockIdx.x * NW + warp;
   const int nwarps = gridDim.x * NW;
-  const bool up = a.cx[s * V] > 0.0;  // the segment's rows share the sign of c_x
-  const bool row_lo = s == 0, row_hi = s == 7;
+  // this lane's rows: v < H the c_x < 0 rows s H + v (their upwind plane is
+  // q + 1), v >= H the c_x > 0 rows nvx/2 + s H + (v - H) (upwind plane q - 1)
+  const int rd0 = s * H, ru0 = NX8 / 2 + s * H;
+  double ac[V];  // |c_x| of the rows
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const double cv = a.cx[v < H ? rd0 + v : ru0 + (v - H)];
+    ac[v] = cv < 0.0 ? -cv : cv;
+  }
+  const bool row_lo = s == 0, row_hi = s == 7;  // the lane holds row 0 / row nvx - 1
+  const int lane_up = (lane + 4) & 31, lane_dn = (lane + 28) & 31;  // lanes s + 1 / s - 1 (mod 8)
+
+  // the loader role of this lane for the level slices (16-byte chunks: r, ls,
+  // g_x | g_z of the warp's 8 v_z; 8-byte: g_y, E)
+  constexpr int NC = 4 * V + 7;
+  constexpr int NR = (NC + 31) / 32;
 
   // issue the loads of one position into stage `st`
   auto issue = [&](const EsIt& it, int st) {
     unsigned char* S = ring + (size_t)st * STB;
     if (!it.done) {
       if (!SYNTH) {
-        const int q = periodic ? es_wrap(it.p, nx) : it.p;
+        int q = it.p;
+        if (periodic) q = q < 0 ? q + nx : (q >= nx ? q - nx : q);
         if (q >= 0 && q < nx) {
-          const double* src = a.fin + (((size_t)q * NX8 + s * V) * a.nvy + it.y) * a.nvz + it.z0 + 2 * c;
+          const double* src = a.fin + (((size_t)q * NX8 + rd0) * a.nvy + it.y) * a.nvz + it.z0 + 2 * c;
+          const size_t rs = (size_t)a.nvy * a.nvz;
 #pragma unroll
           for (int v = 0; v < V; ++v)
-            cp_async_16(S + (v * 32 + lane) * 16, src + (size_t)v * a.nvy * a.nvz);
+            cp_async_16(S + (v * 32 + lane) * 16, src + (size_t)(v < H ? v : NX8 / 2 - H + v) * rs);
         }
       }
-      // level slices: lanes [0, 4V+1) r, ls, g_x (16-byte chunks), 4V+1..4V+4
-      // g_z chunks, 4V+5 g_y, 4V+6 E_q
-      constexpr int NC = 4 * V + 7;
 #pragma unroll
       for (int l = 0; l < L; ++l) {
         if (l >= n) break;
         int q = it.p - l;
-        if (periodic) q = es_wrap(q, nx);
+        if (periodic) q = q < 0 ? q + nx : (q >= nx ? q - nx : q);
         if (q < 0 || q >= nx) continue;
         const double* row = a.tab[l] + (size_t)q * a.TL;
         double* dst = reinterpret_cast<double*>(S + FB) + l * SL;
 #pragma unroll
-        for (int k0 = 0; k0 < NC; k0 += 32) {
-          const int k = k0 + lane;
+        for (int r = 0; r < NR; ++r) {
+          const int k = r * 32 + lane;
           if (k <= 4 * V) {
             cp_async_16(dst + 2 * k, row + 2 * k);
           } else if (k < 4 * V + 5) {
@@ -190,14 +195,27 @@ __global__ void __launch_bounds__(es::NTHR, 2)
     cp_async_commit();
   };
 
-  // level carries: relaxed input planes p-l-1 (yh) and p-l-2 (yp), E of p-l-1
-  double yh[L][V][2], yp[L][V][2], eh[L];
+  // Level carries, double-buffered by the parity of the position (no register
+  // moves: slot ph holds the plane relaxed at the previous position, slot
+  // ph ^ 1 receives this position's):
+  //   yh: the relaxed input plane, all rows
+  //   xd: the c_x > 0 rows' output, which a level computes one position
+  //       earlier than its c_x < 0 rows' (see `level`) and hands on with them
+  //   eh: E of the held plane
+  double yh[L][2][V][2], xd[L][2][H][2], eh[L][2];
+  auto zero_carries = [&]() {
 #pragma unroll
-  for (int l = 0; l < L; ++l) {
-    eh[l] = 0.0;
+    for (int l = 0; l < L; ++l)
 #pragma unroll
-    for (int v = 0; v < V; ++v) yh[l][v][0] = yh[l][v][1] = yp[l][v][0] = yp[l][v][1] = 0.0;
-  }
+      for (int b = 0; b < 2; ++b) {
+        eh[l][b] = 0.0;
+#pragma unroll
+        for (int v = 0; v < V; ++v) yh[l][b][v][0] = yh[l][b][v][1] = 0.0;
+#pragma unroll
+        for (int v = 0; v < H; ++v) xd[l][b][v][0] = xd[l][b][v][1] = 0.0;
+      }
+  };
+  zero_carries();
   double acc = 0.0;
 
   EsIt pf, cu;
@@ -212,38 +230,49 @@ __global__ void __launch_bounds__(es::NTHR, 2)
   int ist = D - 1;
   int item = -1;
 
-  // one level on the stage's slice: relax the incoming plane (x, plane p-l)
-  // into ynew, transport + field of the held plane (p-l-1) into x.  FAST: all
-  // planes interior (no ghosts, no skipped levels)
-  auto level = [&](auto lc, auto fastc, double (&x)[V][2], const double* S, int p) {
+  // One level at one position.  In: x = plane m = p - l of the level's input
+  // (all rows).  The level relaxes it (y_m), then transports
+  //   * its c_x < 0 rows on plane m - 1 (held y_{m-1}, upwind neighbour y_m,
+  //     v_x neighbours from y_{m-1}, E_{m-1}), and
+  //   * its c_x > 0 rows on plane m itself (y_m, upwind neighbour y_{m-1},
+  //     v_x neighbours from y_m, E_m), kept for one position,
+  // and hands plane m - 1 on: the c_x < 0 rows just computed with the c_x > 0
+  // rows computed at the previous position.  One carry per element either
+  // way.  Out: x = plane m - 1 of the level's output.  FAST: every plane
+  // interior (no ghosts, no skipped levels).
+  auto level = [&](auto lc, auto phc, auto fastc, double (&x)[V][2], const double* S, int p) {
     constexpr int l = decltype(lc)::value;
+    constexpr int PH = decltype(phc)::value;
     constexpr bool FAST = decltype(fastc)::value;
     const double* T = S + l * SL;
-    const int qn = p - l;  // plane of the incoming input (non-periodic: may be a ghost)
+    const int m = p - l;
     bool ghost = false;
+    double(&yn)[V][2] = yh[l][PH ^ 1];
+    double(&yo)[V][2] = yh[l][PH];
     if (!FAST && !periodic) {
-      if (qn < 0 || qn > nx) return false;  // nothing of this level (or later) at this position
-      ghost = qn == nx;
+      if (m < 0 || m > nx) {
+        // nothing of this level (or a later one) at this position; its (unused)
+        // carries change slots, so that only one slot is live between positions
+#pragma unroll
+        for (int v = 0; v < V; ++v) yn[v][0] = yo[v][0], yn[v][1] = yo[v][1];
+#pragma unroll
+        for (int v = 0; v < H; ++v) xd[l][PH ^ 1][v][0] = xd[l][PH][v][0], xd[l][PH ^ 1][v][1] = xd[l][PH][v][1];
+        eh[l][PH ^ 1] = eh[l][PH];
+        return;
+      }
+      ghost = m == nx;
     }
-    double yn[V][2];
     double en = 0.0;
     if (!ghost) {
-      const double2 rl = *reinterpret_cast<const double2*>(T);           // r, ls
+      const double2 rl = *reinterpret_cast<const double2*>(T);            // r, ls
       const double2 ge = *reinterpret_cast<const double2*>(T + NX8 + 2);  // g_y, E
       const double2 gz = *reinterpret_cast<const double2*>(T + NX8 + 4 + 2 * c);
       en = ge.y;
       constexpr bool LIFT = SYNTH && l == 0;
       const double rlg = LIFT ? rl.y * ge.x : (rl.x * rl.y) * ge.x;
-      double gx[V];
-#pragma unroll
-      for (int v = 0; v < V; v += 2) {
-        const double2 g2 = *reinterpret_cast<const double2*>(T + 2 + s * V + v);
-        gx[v] = g2.x;
-        gx[v + 1] = g2.y;
-      }
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        const double w = rlg * gx[v];
+        const double w = rlg * T[2 + (v < H ? rd0 + v : ru0 + (v - H))];
         if (LIFT) {
           yn[v][0] = w * gz.x;
           yn[v][1] = w * gz.y;
@@ -253,83 +282,86 @@ __global__ void __launch_bounds__(es::NTHR, 2)
         }
       }
     } else {
-      // right ghost plane nx of this level: 0 (absorbing) or plane nx-1 (outflow)
+      // right ghost plane nx of this level: 0 (absorbing) or plane nx - 1 (outflow)
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        yn[v][0] = outflow ? yh[l][v][0] : 0.0;
-        yn[v][1] = outflow ? yh[l][v][1] : 0.0;
+        yn[v][0] = outflow ? yo[v][0] : 0.0;
+        yn[v][1] = outflow ? yo[v][1] : 0.0;
       }
     }
-    const int qh = qn - 1;
-    const bool work = FAST || periodic || qh >= 0;
-    if (work) {
-      // left ghost plane -1 of this level when the held plane is 0
-      if (!FAST && !periodic && qh == 0) {
+    eh[l][PH ^ 1] = en;
+    // left ghost plane -1 when the incoming plane is 0
+    if (!FAST && !periodic && m == 0) {
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-          yp[l][v][0] = outflow ? yh[l][v][0] : 0.0;
-          yp[l][v][1] = outflow ? yh[l][v][1] : 0.0;
-        }
+      for (int v = 0; v < V; ++v) {
+        yo[v][0] = outflow ? yn[v][0] : 0.0;
+        yo[v][1] = outflow ? yn[v][1] : 0.0;
       }
-      const double hE = 0.5 * eh[l];
-      const double DCP = a.dtdv[l] * (hE + a.half_emax);
-      const double DCM = a.dtdv[l] * (hE - a.half_emax);
+    }
+    const double dv = a.dtdv[l], dxl = a.dtdx[l];
+    const double k0 = 1.0 - dv * (2.0 * a.half_emax);  // interior rows: 1 - a_j - (dt/dv) e_max
+    // c_x < 0 rows, plane m - 1: v_x neighbours from the held plane
+    {
+      const double hE = 0.5 * eh[l][PH];
+      const double DCP = dv * (hE + a.half_emax), DCM = dv * (hE - a.half_emax);
       double lo[2], hi[2];
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
-        lo[k] = __shfl_up_sync(0xffffffffu, yh[l][V - 1][k], 4);
-        hi[k] = __shfl_down_sync(0xffffffffu, yh[l][0][k], 4);
+        // below: row s H - 1 (lane s - 1's last c_x < 0 row; none for row 0);
+        // above: row (s + 1) H (lane s + 1's first c_x < 0 row; for s = 7 row
+        // nvx / 2, lane s = 0's first c_x > 0 row)
+        lo[k] = __shfl_sync(0xffffffffu, yo[H - 1][k], lane_dn);
+        hi[k] = __shfl_sync(0xffffffffu, row_lo ? yo[H][k] : yo[0][k], lane_up);
         if (row_lo) lo[k] = 0.0;
-        if (row_hi) hi[k] = 0.0;
       }
-      const double2* AKl = AK + l * NX8 + s * V;
 #pragma unroll
-      for (int v = 0; v < V; ++v) {
-        const double2 ka = AKl[v];
-        double kap = ka.x;
-        if (v == 0 && row_lo) kap = ka.x + 2.0 * a.dtdv[l] * a.half_emax - DCP;
-        if (v == V - 1 && row_hi) kap = ka.x + 2.0 * a.dtdv[l] * a.half_emax + DCM;
+      for (int v = 0; v < H; ++v) {
+        const double av = dxl * ac[v];
+        double kap = k0 - av;
+        if (v == 0 && row_lo) kap = (1.0 - av) - DCP;  // row 0: no flux through the cube face
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-          const double ym = v > 0 ? yh[l][v - 1][k] : lo[k];
-          const double yq = v < V - 1 ? yh[l][v + 1][k] : hi[k];
-          const double nb = up ? yp[l][v][k] : yn[v][k];
-          x[v][k] = fma(kap, yh[l][v][k], fma(ka.y, nb, fma(DCP, ym, -(DCM * yq))));
+          const double ym = v > 0 ? yo[v - 1][k] : lo[k];
+          const double yq = v < H - 1 ? yo[v + 1][k] : hi[k];
+          x[v][k] = fma(kap, yo[v][k], fma(av, yn[v][k], fma(DCP, ym, -(DCM * yq))));
         }
       }
     }
+    // c_x > 0 rows, plane m: v_x neighbours from the incoming plane; handed
+    // on at the next position
+    {
+      const double hE = 0.5 * en;
+      const double DCP = dv * (hE + a.half_emax), DCM = dv * (hE - a.half_emax);
+      double lo[2], hi[2];
 #pragma unroll
-    for (int v = 0; v < V; ++v) {
-      yp[l][v][0] = yh[l][v][0];
-      yp[l][v][1] = yh[l][v][1];
-      yh[l][v][0] = yn[v][0];
-      yh[l][v][1] = yn[v][1];
-    }
-    eh[l] = en;
-    return work;
-  };
-
-#pragma unroll 1
-  while (!cu.done) {
-    __syncwarp();
-    issue(pf, ist);
-    pf.next(a, n, nwarps);
-    if (++ist == D) ist = 0;
-    cp_async_wait<D - 1>();
-    __syncwarp();
-    if (cu.item != item) {
-      // a new item: its carries restart (the halo positions refill them)
-      item = cu.item;
+      for (int k = 0; k < 2; ++k) {
+        // below: row nvx/2 + s H - 1 (lane s - 1's last c_x > 0 row; for s = 0
+        // row nvx/2 - 1, lane s = 7's last c_x < 0 row); above: lane s + 1's
+        // first c_x > 0 row (none for row nvx - 1)
+        lo[k] = __shfl_sync(0xffffffffu, row_hi ? yn[H - 1][k] : yn[V - 1][k], lane_dn);
+        hi[k] = __shfl_sync(0xffffffffu, yn[H][k], lane_up);
+        if (row_hi) hi[k] = 0.0;
+      }
 #pragma unroll
-      for (int l = 0; l < L; ++l) {
-        eh[l] = 0.0;
+      for (int v = H; v < V; ++v) {
+        const double av = dxl * ac[v];
+        double kap = k0 - av;
+        if (v == V - 1 && row_hi) kap = (1.0 - av) + DCM;  // row nvx - 1
 #pragma unroll
-        for (int v = 0; v < V; ++v) yh[l][v][0] = yh[l][v][1] = yp[l][v][0] = yp[l][v][1] = 0.0;
+        for (int k = 0; k < 2; ++k) {
+          const double ym = v > H ? yn[v - 1][k] : lo[k];
+          const double yq = v < V - 1 ? yn[v + 1][k] : hi[k];
+          x[v][k] = xd[l][PH][v - H][k];
+          xd[l][PH ^ 1][v - H][k] = fma(kap, yn[v][k], fma(av, yo[v][k], fma(DCP, ym, -(DCM * yq))));
+        }
       }
     }
-    const unsigned char* S = ring + (size_t)stg * STB;
+  };
+
+  auto position = [&](auto phc, auto fastc, const unsigned char* S, int p, const EsIt& it) {
+    constexpr bool FAST = decltype(fastc)::value;
+    constexpr int PHV = decltype(phc)::value;
     const double* ST = reinterpret_cast<const double*>(S + FB);
-    const int p = cu.p;
     double x[V][2];
     if (!SYNTH) {
 #pragma unroll
@@ -342,59 +374,100 @@ __global__ void __launch_bounds__(es::NTHR, 2)
 #pragma unroll
       for (int v = 0; v < V; ++v) x[v][0] = x[v][1] = 0.0;
     }
-    const bool fast = periodic || (p >= n + 1 && p <= nx - 1);
-    // (each level decides from its own planes whether it runs: a skipped
-    // level's successors either skip too or only see a ghost input)
-    if (fast && n == L) {
-      level(std::integral_constant<int, 0>{}, std::true_type{}, x, ST, p);
-      if constexpr (L > 1) level(std::integral_constant<int, 1>{}, std::true_type{}, x, ST, p);
-      if constexpr (L > 2) level(std::integral_constant<int, 2>{}, std::true_type{}, x, ST, p);
-      if constexpr (L > 3) level(std::integral_constant<int, 3>{}, std::true_type{}, x, ST, p);
-    } else {
-      level(std::integral_constant<int, 0>{}, std::false_type{}, x, ST, p);
-      if constexpr (L > 1) if (n > 1) level(std::integral_constant<int, 1>{}, std::false_type{}, x, ST, p);
-      if constexpr (L > 2) if (n > 2) level(std::integral_constant<int, 2>{}, std::false_type{}, x, ST, p);
-      if constexpr (L > 3) if (n > 3) level(std::integral_constant<int, 3>{}, std::false_type{}, x, ST, p);
-    }
-    // output plane p - n of the last level (inside the segment, the last
-    // level's held plane is a real plane, so it ran)
+    level(std::integral_constant<int, 0>{}, phc, fastc, x, ST, p);
+    if constexpr (L > 1) if (FAST || n > 1) level(std::integral_constant<int, 1>{}, phc, fastc, x, ST, p);
+    if constexpr (L > 2) if (FAST || n > 2) level(std::integral_constant<int, 2>{}, phc, fastc, x, ST, p);
+    if constexpr (L > 3) if (FAST || n > 3) level(std::integral_constant<int, 3>{}, phc, fastc, x, ST, p);
+    (void)PHV;
+    // output plane p - n of the last level
     const int qo = p - n;
-    if (qo >= cu.x0 && qo < cu.x1) {
-      double* dst = a.fout + (((size_t)qo * NX8 + s * V) * a.nvy + cu.y) * a.nvz + cu.z0 + 2 * c;
+    if (qo >= it.x0 && qo < it.x1) {
+      double* dst = a.fout + (((size_t)qo * NX8 + rd0) * a.nvy + it.y) * a.nvz + it.z0 + 2 * c;
+      const size_t rs = (size_t)a.nvy * a.nvz;
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        st_global_v2(dst + (size_t)v * a.nvy * a.nvz, x[v][0], x[v][1]);
+        st_global_v2(dst + (size_t)(v < H ? v : NX8 / 2 - H + v) * rs, x[v][0], x[v][1]);
         acc += x[v][0] + x[v][1];
       }
     }
+  };
+
+  // one position (parity PH of the carries' slots); false at the end
+  auto step = [&](auto phc) {
+    constexpr int PH = decltype(phc)::value;
+    if (cu.done) return false;
+    __syncwarp();
+    issue(pf, ist);
+    pf.next(a, n, nwarps);
+    if (++ist == D) ist = 0;
+    cp_async_wait<D - 1>();
+    __syncwarp();
+    if (cu.item != item) {
+      // a new item: its carries restart (the halo positions refill them)
+      item = cu.item;
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        eh[l][PH] = 0.0;
+#pragma unroll
+        for (int v = 0; v < V; ++v) yh[l][PH][v][0] = yh[l][PH][v][1] = 0.0;
+#pragma unroll
+        for (int v = 0; v < H; ++v) xd[l][PH][v][0] = xd[l][PH][v][1] = 0.0;
+      }
+    }
+    const unsigned char* S = ring + (size_t)stg * STB;
+    const int p = cu.p;
+    // FAST: every level's planes p - l and p - l - 1 are interior, all levels run
+    const bool fast = n == L && (periodic || (p >= n + 1 && p <= nx - 1));
+    if (fast) position(phc, std::true_type{}, S, p, cu);
+    else position(phc, std::false_type{}, S, p, cu);
     if (++stg == D) stg = 0;
     cu.next(a, n, nwarps);
+    return true;
+  };
+#pragma unroll 1
+  while (true) {
+    if (!step(std::integral_constant<int, 0>{})) break;
+    if (!step(std::integral_constant<int, 1>{})) break;
   }
   cp_async_wait<0>();
   if (!isfinite(acc)) atomicMin(a.err, err_key(0, a.step0, kErrNonFiniteMulti));
 }
 
-// shapes the kernel runs: nvx = 8 V (V = 2, 4, 6, 8), nvz % 8 == 0, the
-// table layout of capi.cu (g_x at 2, g_z 16-byte aligned)
+// shapes the kernel runs: nvx = 8 V (V = 2, 4, 6, 8: a lane holds V / 2 rows
+// of each c_x sign), nvz % 8 == 0, the table layout of capi.cu (g_x at 2, g_z
+// 16-byte aligned)
+#ifndef PBGK_ES_L2
+#define PBGK_ES_L2 4  // levels of the nvx = 16 build (dev A/B knobs)
+#endif
 #ifndef PBGK_ES_L4
-#define PBGK_ES_L4 3  // levels of the nvx = 32 build (dev A/B knob: 2, 3 or 4)
+#define PBGK_ES_L4 3  // nvx = 32 (4: 150 B of spills, 13 % slower)
+#endif
+#ifndef PBGK_ES_L6
+#define PBGK_ES_L6 2  // nvx = 48 (3 spills)
+#endif
+#ifndef PBGK_ES_L8
+#define PBGK_ES_L8 0  // nvx = 64: off (2 levels spill; one-step field passes)
 #endif
 int esweep_levels(int nvx, int nvz) {
-  if (nvx % 8 != 0 || nvz % es::ZW != 0) return 0;
+  if (nvx % 16 != 0 || nvz % es::ZW != 0) return 0;
   switch (nvx / 8) {
-    case 2: return 4;
+    case 2: return PBGK_ES_L2;
     case 4: return PBGK_ES_L4;
-    case 6: return 2;
+    case 6: return PBGK_ES_L6;
+    case 8: return PBGK_ES_L8;
   }
-  return 0;  // (nvx = 64: two levels need 768 B of spills; one-step passes)
+  return 0;
 }
 
-constexpr int kEsD = 4;  // ring stages per warp
+#ifndef PBGK_ES_D
+#define PBGK_ES_D 4
+#endif
+constexpr int kEsD = PBGK_ES_D;  // ring stages per warp
 
 size_t esweep_smem_bytes(int nvx) {
   const int V = nvx / 8;
   const int L = esweep_levels(nvx, 8);
-  return (size_t)L * nvx * 16 + (size_t)es::NW * kEsD * es::stage_bytes(V, L);
+  return (size_t)es::NW * kEsD * es::stage_bytes(V, L);
 }
 
 int esweep_ctas_per_sm(int nvx);
@@ -419,20 +492,23 @@ static int occ(size_t smem) {
 int esweep_ctas_per_sm(int nvx) {
   const size_t smem = esweep_smem_bytes(nvx);
   switch (nvx / 8) {
-    case 2: return occ<2, 4>(smem);
+    case 2: return occ<2, PBGK_ES_L2>(smem);
     case 4: return occ<4, PBGK_ES_L4>(smem);
-    case 6: return occ<6, 2>(smem);
+    case 6: return occ<6, PBGK_ES_L6>(smem);
   }
   return 0;
 }
 
+template <int V, int L>
+static cudaError_t launch_es_v(const ESweepArgs& a, bool synth, int grid, size_t smem, cudaStream_t st) {
+  return synth ? launch_es<V, L, true>(a, grid, smem, st) : launch_es<V, L, false>(a, grid, smem, st);
+}
+
 cudaError_t launch_esweep(const ESweepArgs& a, bool synth, int grid, size_t smem, cudaStream_t st) {
   switch (a.nvx / 8) {
-    case 2: return synth ? launch_es<2, 4, true>(a, grid, smem, st) : launch_es<2, 4, false>(a, grid, smem, st);
-    case 4:
-      return synth ? launch_es<4, PBGK_ES_L4, true>(a, grid, smem, st)
-                   : launch_es<4, PBGK_ES_L4, false>(a, grid, smem, st);
-    case 6: return synth ? launch_es<6, 2, true>(a, grid, smem, st) : launch_es<6, 2, false>(a, grid, smem, st);
+    case 2: return launch_es_v<2, PBGK_ES_L2>(a, synth, grid, smem, st);
+    case 4: return launch_es_v<4, PBGK_ES_L4>(a, synth, grid, smem, st);
+    case 6: return launch_es_v<6, PBGK_ES_L6>(a, synth, grid, smem, st);
   }
   return cudaErrorInvalidValue;
 }
