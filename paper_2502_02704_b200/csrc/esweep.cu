@@ -63,6 +63,20 @@ __host__ __device__ constexpr int stage_bytes(int V, int L) { return 32 * V * 16
 __device__ __forceinline__ void cp_async_8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+// predicated copies: every lane runs the same instructions (no divergent
+// branches on the loader roles)
+__device__ __forceinline__ void cp_async_16_if(uint32_t dst, const void* src, bool on) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.b32 p, %2, 0; @p cp.async.cg.shared.global [%0], [%1], 16; }" ::"r"(dst),
+      "l"(src), "r"((int)on)
+      : "memory");
+}
+__device__ __forceinline__ void cp_async_8_if(uint32_t dst, const void* src, bool on) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.b32 p, %2, 0; @p cp.async.ca.shared.global [%0], [%1], 8; }" ::"r"(dst),
+      "l"(src), "r"((int)on)
+      : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -73,6 +87,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // an item's input positions p = ps .. pe (inclusive), see the header.
 struct EsIt {
   int item, p, pe, x0, x1, y, z0;
+  long long foff;  // (y nvz + z0): the column's offset inside a v_x row of a plane (doubles)
   bool done;
   __device__ __forceinline__ void setup(const ESweepArgs& a, int n) {
     const int nitems = a.ncol * a.nseg;
@@ -85,6 +100,7 @@ struct EsIt {
     const int nzb = a.nvz / es::ZW;
     y = col / nzb;
     z0 = (col - y * nzb) * es::ZW;
+    foff = (long long)y * a.nvz + z0;
     x0 = seg * a.seglen;
     x1 = min(a.nx, x0 + a.seglen);
     if (a.bc == 1) {
@@ -108,8 +124,6 @@ struct EsIt {
     }
   }
 };
-
-__device__ __forceinline__ int es_wrap(int q, int nx) { return ((q % nx) + nx) % nx; }
 
 template <int V, int L, bool SYNTH, int D>
 __global__ void __launch_bounds__(es::NTHR, 2)
@@ -148,48 +162,46 @@ __global__ void __launch_bounds__(es::NTHR, 2)
   const bool row_lo = s == 0, row_hi = s == 7;  // the lane holds row 0 / row nvx - 1
   const int lane_up = (lane + 4) & 31, lane_dn = (lane + 28) & 31;  // lanes s + 1 / s - 1 (mod 8)
 
-  // the loader role of this lane for the level slices (16-byte chunks: r, ls,
-  // g_x | g_z of the warp's 8 v_z; 8-byte: g_y, E)
+  // the loader role of this lane for a level slice [r, ls, g_x | g_y, E | g_z
+  // of the warp's 8 v_z]: lanes 0 .. 4V the 16-byte chunks of r, ls, g_x, the
+  // next four those of g_z, then one 8-byte copy each of g_y and E; per-lane
+  // source offset (from the table row, or from E) and destination offset,
+  // the column's part of the source added per item
   constexpr int NC = 4 * V + 7;
-  constexpr int NR = (NC + 31) / 32;
+  static_assert(NC <= 32, "one loader round per level");
+  const bool r16 = lane <= 4 * V + 4, r8 = lane == 4 * V + 5 || lane == 4 * V + 6;
+  const bool rz = lane > 4 * V && lane <= 4 * V + 4, ry = lane == 4 * V + 5, rE = lane == 4 * V + 6;
+  const int soff0 = lane <= 4 * V ? 2 * lane : (rz ? a.gzo + 2 * (lane - (4 * V + 1)) : (ry ? a.gyo : 0));
+  const int doff = lane <= 4 * V ? 2 * lane : (rz ? NX8 + 4 + 2 * (lane - (4 * V + 1)) : (ry ? NX8 + 2 : NX8 + 3));
+  const long long rs = (long long)a.nvy * a.nvz;      // one v_x row of a plane
+  const long long plane = (long long)NX8 * rs;
+  const long long lane_f = (long long)rd0 * rs + 2 * c;  // this lane's first row + v_z pair
+  const uint32_t ring_u = smem_u32(ring);
 
   // issue the loads of one position into stage `st`
   auto issue = [&](const EsIt& it, int st) {
-    unsigned char* S = ring + (size_t)st * STB;
+    const uint32_t S = ring_u + (uint32_t)st * STB;
     if (!it.done) {
+      int q0 = it.p;
+      if (periodic) q0 = q0 < 0 ? q0 + nx : (q0 >= nx ? q0 - nx : q0);
       if (!SYNTH) {
-        int q = it.p;
-        if (periodic) q = q < 0 ? q + nx : (q >= nx ? q - nx : q);
-        if (q >= 0 && q < nx) {
-          const double* src = a.fin + (((size_t)q * NX8 + rd0) * a.nvy + it.y) * a.nvz + it.z0 + 2 * c;
-          const size_t rs = (size_t)a.nvy * a.nvz;
+        const bool on = q0 >= 0 && q0 < nx;
+        const double* src = a.fin + ((long long)q0 * plane + lane_f + it.foff);
 #pragma unroll
-          for (int v = 0; v < V; ++v)
-            cp_async_16(S + (v * 32 + lane) * 16, src + (size_t)(v < H ? v : NX8 / 2 - H + v) * rs);
-        }
+        for (int v = 0; v < V; ++v)
+          cp_async_16_if(S + (v * 32 + lane) * 16, src + (long long)(v < H ? v : NX8 / 2 - H + v) * rs, on);
       }
+      const int so = soff0 + (rz ? it.z0 : (ry ? it.y : 0));
 #pragma unroll
       for (int l = 0; l < L; ++l) {
         if (l >= n) break;
-        int q = it.p - l;
-        if (periodic) q = q < 0 ? q + nx : (q >= nx ? q - nx : q);
-        if (q < 0 || q >= nx) continue;
-        const double* row = a.tab[l] + (size_t)q * a.TL;
-        double* dst = reinterpret_cast<double*>(S + FB) + l * SL;
-#pragma unroll
-        for (int r = 0; r < NR; ++r) {
-          const int k = r * 32 + lane;
-          if (k <= 4 * V) {
-            cp_async_16(dst + 2 * k, row + 2 * k);
-          } else if (k < 4 * V + 5) {
-            const int m = k - (4 * V + 1);
-            cp_async_16(dst + NX8 + 4 + 2 * m, row + a.gzo + it.z0 + 2 * m);
-          } else if (k == 4 * V + 5) {
-            cp_async_8(dst + NX8 + 2, row + a.gyo + it.y);
-          } else if (k == 4 * V + 6) {
-            cp_async_8(dst + NX8 + 3, a.E + q);
-          }
-        }
+        int q = q0 - l;
+        if (periodic && q < 0) q += nx;
+        const bool on = q >= 0 && q < nx;
+        const double* src = rE ? a.E + q : a.tab[l] + ((long long)q * a.TL + so);
+        const uint32_t dst = S + FB + (uint32_t)(l * SL + doff) * 8u;
+        cp_async_16_if(dst, src, on && r16);
+        cp_async_8_if(dst, src, on && r8);
       }
     }
     cp_async_commit();
@@ -382,11 +394,10 @@ __global__ void __launch_bounds__(es::NTHR, 2)
     // output plane p - n of the last level
     const int qo = p - n;
     if (qo >= it.x0 && qo < it.x1) {
-      double* dst = a.fout + (((size_t)qo * NX8 + rd0) * a.nvy + it.y) * a.nvz + it.z0 + 2 * c;
-      const size_t rs = (size_t)a.nvy * a.nvz;
+      double* dst = a.fout + ((long long)qo * plane + lane_f + it.foff);
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        st_global_v2(dst + (size_t)(v < H ? v : NX8 / 2 - H + v) * rs, x[v][0], x[v][1]);
+        st_global_v2(dst + (long long)(v < H ? v : NX8 / 2 - H + v) * rs, x[v][0], x[v][1]);
         acc += x[v][0] + x[v][1];
       }
     }
