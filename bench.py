@@ -285,6 +285,12 @@ def run_ours(args, w, world, rank, local):
     launches0 = lib.pbgk_launch_count()
     total_ms = timed(args.steps)
     launches = lib.pbgk_launch_count() - launches0
+    # a timed region shorter than the sampler's period (config 0: ~10 ms): the
+    # same steps keep the GPU under the same load until two samples arrived
+    t_end = time.time() + 3.0
+    while clocks.proc is not None and len(clocks.lines) < 2 and time.time() < t_end:
+        step()
+        torch.cuda.synchronize(dev)
     clk = clocks.stop()
     # roofline: a second timed pass with per-launch CUDA events on the
     # launching stream (sweep / finalize durations and algorithmic bytes)

@@ -29,8 +29,9 @@ cudaError_t launch_fsweep(int cfg_id, const CUtensorMap& map, const FSweepArgs& 
 size_t fsweep_smem_bytes(const FSweepArgs& a, int V, int LZ, bool synth, int L, int ns);
 bool fsweep_has_cfg(int cfg_id);
 int fsweep_ctas_per_sm(int L);
-cudaError_t launch_msweep(int L, int mode, const CUtensorMap& map, const MSweepArgs& a, int grid,
+cudaError_t launch_msweep(int L, int mode, const CUtensorMap& map, const MSweepArgs& a, int grid_x, int nwin,
                           int ns, size_t smem, cudaStream_t st);
+cudaError_t launch_finalize_batch(const FinalArgs& a, const FinalBatch& b, int nwin, cudaStream_t st);
 size_t msweep_smem_bytes(int L, int mode, int nvx, int ns);
 int msweep_ctas_per_sm();
 int msweep_tiling(int nvx, int nvy, int nvz, Tiling* t);
@@ -132,7 +133,7 @@ struct Plan {
 
 struct MapEntry {
   const void* ptr;
-  int rows_load, By, Bz;
+  int rows_load, By, Bz, planes;
   CUtensorMap map;
 };
 
@@ -220,6 +221,8 @@ struct pbgk_ctx {
   int ms_levels = 0;
   double batch_bytes = 0.0;  // table budget of the multi-step path (0: the default)
   Tiling ms_t = {};
+  double* d_fb[2] = {nullptr, nullptr};  // f of a batch of windows (ms_windows_batched)
+  size_t fb_cap[2] = {0, 0};
   double* d_mpart = nullptr;
   size_t mpart_cap = 0;
   // multi-step passes with the v_x field term (esweep.cu): on/off
@@ -379,11 +382,14 @@ bool make_plan(pbgk_ctx* c, bool field, bool muscl, Plan& out, int only = -1) {
   return true;
 }
 
-const CUtensorMap* tensor_map(pbgk_ctx* c, const double* ptr, const Tiling& t, int cfg) {
+// nplanes > 0: a batch of windows stacked along x (nx * windows planes)
+const CUtensorMap* tensor_map(pbgk_ctx* c, const double* ptr, const Tiling& t, int cfg, int nplanes = 0) {
   static CUtensorMap dummy;
   if (!kCfg[cfg].tma || ptr == nullptr) return &dummy;
+  const int planes = nplanes > 0 ? nplanes : c->g.nx + (c->g.bc == 3 ? 2 : 0);
   for (auto& m : c->maps)
-    if (m.ptr == ptr && m.rows_load == t.rows_load && m.By == t.By && m.Bz == t.Bz) return &m.map;
+    if (m.ptr == ptr && m.rows_load == t.rows_load && m.By == t.By && m.Bz == t.Bz && m.planes == planes)
+      return &m.map;
   auto enc = get_encode();
   if (!enc) return nullptr;
   MapEntry e;
@@ -391,9 +397,10 @@ const CUtensorMap* tensor_map(pbgk_ctx* c, const double* ptr, const Tiling& t, i
   e.rows_load = t.rows_load;
   e.By = t.By;
   e.Bz = t.Bz;
+  e.planes = planes;
   // slab contexts (bc 3) address padded buffers: one halo plane per side
   const cuuint64_t dims[4] = {(cuuint64_t)c->g.nvz, (cuuint64_t)c->g.nvy, (cuuint64_t)c->g.nvx,
-                              (cuuint64_t)c->g.nx + (c->g.bc == 3 ? 2 : 0)};
+                              (cuuint64_t)planes};
   const cuuint64_t strides[3] = {(cuuint64_t)c->g.nvz * 8, (cuuint64_t)c->g.nvy * c->g.nvz * 8,
                                  (cuuint64_t)c->g.nvx * c->g.nvy * c->g.nvz * 8};
   const cuuint32_t box[4] = {(cuuint32_t)t.Bz, (cuuint32_t)t.By, (cuuint32_t)t.rows_load, 1};
@@ -626,6 +633,8 @@ void pbgk_ctx_destroy(pbgk_ctx* c) {
   cudaFree(c->d_gbar);
   cudaFree(c->d_prog);
   cudaFree(c->d_mpart);
+  cudaFree(c->d_fb[0]);
+  cudaFree(c->d_fb[1]);
   if (c->ev_start) cudaEventDestroy(c->ev_start);
   if (c->ev_done) cudaEventDestroy(c->ev_done);
   if (c->st_side) cudaStreamDestroy(c->st_side);
@@ -912,10 +921,23 @@ int ms_levels(pbgk_ctx* c) {
 // (null: SYNTH, level 0 lifts tabs[0]), writing the last level to `out`
 // (may be null); FINAL (`tabR` non-null): R_S applied, partial records of
 // P(f_S) into d_mpart.
+// A batch of windows in one msweep launch (grid.y = window): `in` / `out` hold
+// the windows' f back to back, tabs / tabR / d_mpart are window 0's with
+// stride t_ws / the record block, keys at errw[window], dt of step s0 + l of
+// window k on the device at dts[(s0 + l) * nwin + k].
+struct MsBatch {
+  int nwin;
+  long long t_ws;
+  ErrKey* errw;
+  const double* dts;
+  int s0;
+};
+
 int run_msweep(pbgk_ctx* c, int L, const double* in, double* out, const double* const* tabs,
                const double* tabR, const double* dtdx, int n, int step0, cudaStream_t st,
-               const unsigned* prog = nullptr, unsigned need = 0) {
+               const unsigned* prog = nullptr, unsigned need = 0, const MsBatch* mb = nullptr) {
   const Tiling& t = c->ms_t;
+  const int nwin = mb ? mb->nwin : 1;
   MSweepArgs a{};
   a.nx = c->g.nx;
   a.nvx = c->g.nvx;
@@ -943,10 +965,20 @@ int run_msweep(pbgk_ctx* c, int L, const double* in, double* out, const double* 
   a.need = need;
   const int mode = (in == nullptr ? 1 : 0) | (tabR != nullptr ? 2 : 0);
   if (tabR) {
-    if (ensure_dev(c->d_mpart, c->mpart_cap, (size_t)c->g.nx * t.NT * t.PS, st)) return -1;
+    if (ensure_dev(c->d_mpart, c->mpart_cap, (size_t)nwin * c->g.nx * t.NT * t.PS, st)) return -1;
     a.part = c->d_mpart;
   }
-  const CUtensorMap* map = tensor_map(c, in, t, 3);
+  if (mb) {
+    a.f_ws = a.plane * a.nx;
+    a.t_ws = mb->t_ws;
+    a.p_ws = (long long)c->g.nx * t.NT * t.PS;
+    a.errw = mb->errw;
+    a.dts = mb->dts;
+    a.dts_g = nwin;
+    a.s0 = mb->s0;
+    a.dx = c->dx;
+  }
+  const CUtensorMap* map = tensor_map(c, in, t, 3, mb ? nwin * c->g.nx : 0);
   if (!map) return fail("tensor map: " + g_last_error);
   static const int ns_env = getenv("PBGK_MS_NS") ? atoi(getenv("PBGK_MS_NS")) : 0;  // dev knob
   const int per_sm = msweep_ctas_per_sm();
@@ -955,14 +987,54 @@ int run_msweep(pbgk_ctx* c, int L, const double* in, double* out, const double* 
   while (ns > 3 && msweep_smem_bytes(L, mode, c->g.nvx, ns) > budget) --ns;
   const size_t smem = msweep_smem_bytes(L, mode, c->g.nvx, ns);
   if (smem > budget) return fail("msweep: ring does not fit");
-  const double fbytes = 8.0 * (double)a.plane * a.nx;
+  const double fbytes = 8.0 * (double)a.plane * a.nx * nwin;
   ProfScope ps(c, st, 2, (in ? fbytes : 0.0) + (out ? fbytes : 0.0), n);
   // one CTA per SM, minus the slots left to side-stream work and the SMs of a
-  // concurrent recursion
+  // concurrent recursion; a batch splits them between its windows
   int grid = (int)std::min<long long>(a.total, (long long)c->nsm * per_sm);
   int reserve = c->slot_reserve + (prog != nullptr ? c->rec_reserve * per_sm : 0);
   grid = std::max(1, std::min(grid, c->nsm * per_sm - reserve));
-  CK(launch_msweep(L, mode, *map, a, grid, ns, smem, st));
+  if (nwin > 1) grid = std::max(1, grid / nwin);
+  CK(launch_msweep(L, mode, *map, a, grid, nwin, ns, smem, st));
+  return 0;
+}
+
+// The passes and the projection of a batch of g windows with S steps each
+// (small grids: one window cannot fill the GPU, its tile runs are shorter than
+// their lead-in): every pass is one launch over all windows, f in the
+// context's batch buffers; tables at T + k t_ws, moments to mom_out + k * 5 nx.
+int ms_windows_batched(pbgk_ctx* c, int L, int g, const double* T, long long t_ws, int S,
+                       const double* d_dts, ErrKey* errw, double* mom_out, cudaStream_t st) {
+  const size_t tstep = (size_t)c->g.nx * c->TL;
+  const size_t fw = (size_t)c->g.nx * c->g.nvx * c->g.nvy * c->g.nvz;
+  const int P = (S + L - 1) / L;
+  if (P > 1 && ensure_dev(c->d_fb[0], c->fb_cap[0], (size_t)g * fw, st)) return -1;
+  if (P > 2 && ensure_dev(c->d_fb[1], c->fb_cap[1], (size_t)g * fw, st)) return -1;
+  const double* in = nullptr;
+  int wcount = 0;
+  for (int s0 = 0; s0 < S;) {
+    const int n = std::min(L, S - s0);
+    const bool last = s0 + n == S;
+    const double* tabs[kMaxL];
+    double dtdx[kMaxL] = {};
+    for (int l = 0; l < n; ++l) tabs[l] = T + (size_t)(s0 + l) * tstep;
+    double* out = last ? nullptr : c->d_fb[(wcount++) & 1];
+    MsBatch mb{g, t_ws, errw, d_dts, s0};
+    if (run_msweep(c, L, in, out, tabs, last ? T + (size_t)S * tstep : nullptr, dtdx, n, s0 + 1, st, nullptr, 0,
+                   &mb))
+      return -1;
+    in = out;
+    s0 += n;
+  }
+  FinalArgs f = fin_args(c, c->plan[0]);
+  f.t = c->ms_t;
+  f.part = c->d_mpart;
+  f.mode = kFinProject;
+  f.mom_out = mom_out;
+  f.step = S + 1;
+  FinalBatch fb{(long long)c->g.nx * c->ms_t.NT * c->ms_t.PS, 0, (long long)5 * c->g.nx, 0, errw};
+  ProfScope ps(c, st, 1, 0.0);
+  CK(launch_finalize_batch(f, fb, g, st));
   return 0;
 }
 
@@ -1331,6 +1403,29 @@ int windows_fused(pbgk_ctx* c, int nwin, const double* mom_in, double* mom_out, 
     CK(cudaMemcpyAsync(c->d_bnst, hn.data(), g * sizeof(int), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(c->d_bdts, hd.data(), (size_t)std::max(Smax, 1) * g * sizeof(double),
                        cudaMemcpyHostToDevice, st));
+    // small grids: the group's windows as one batch per launch (equal step
+    // counts; f of the batch in the context's own buffers)
+    bool batched = LM > 0 && g >= 2 && g <= c->nsm && h_nsteps[w0] > 0 && !getenv("PBGK_NO_WBATCH") &&
+                   8.0 * (double)g * nx * c->g.nvx * c->g.nvy * c->g.nvz <= 256.0 * 1048576.0;
+    for (int k = 1; k < g && batched; ++k) batched = h_nsteps[w0 + k] == h_nsteps[w0];
+    if (batched) {
+      FinalArgs f = fin_args(c, c->plan[0]);
+      f.mode = kFinSynthRaw;
+      f.mom_in = mom_in + w0 * m5;
+      f.tab = c->d_bt;
+      FinalBatch fb{0, (long long)m5, 0, (long long)t_ws, c->d_keys + w0};
+      {
+        ProfScope ps(c, st, 1, 0.0);
+        CK(launch_finalize_batch(f, fb, g, st));
+      }
+      if (run_recursion(c, g, nullptr, c->d_bt, (long long)t_ws, Smax, c->d_bdts, c->d_bnst,
+                        c->d_keys + w0, eps, tau, E, e_max, st))
+        return -1;
+      if (ms_windows_batched(c, LM, g, c->d_bt, (long long)t_ws, h_nsteps[w0], c->d_bdts, c->d_keys + w0,
+                             mom_out + w0 * m5, st))
+        return -1;
+      continue;
+    }
     for (int k = 0; k < g; ++k) {
       const int w = w0 + k;
       if (h_nsteps[w] == 0) {  // empty window: the moments themselves

@@ -123,6 +123,16 @@ struct MSweepArgs {
   double* part;
   const unsigned* prog;
   unsigned need;
+  // a batch of windows in one launch (grid.y = window; small grids, where one
+  // window cannot fill the GPU): per-window strides (doubles) of f in / out
+  // (the tensor map spans nx * windows planes), of the tables and of the
+  // partial records; per-window failure keys; per-window dt of step s on the
+  // device at dts[(s0 + l) * dts_g + window] (null: dtdx[l] for every window)
+  long long f_ws, t_ws, p_ws;
+  ErrKey* errw;
+  const double* dts;
+  int dts_g, s0;
+  double dx;
 };
 
 // Multi-step sweep with the v_x field term (esweep.cu): up to kMaxLevels
@@ -203,6 +213,14 @@ struct FinalArgs {
   int step;
   int check_finite;      // kFinProject: flag non-finite marginals as BlowUpError(step)
   int trap;              // trapezoidal velocity quadrature (end nodes weigh 1/2)
+};
+
+// finalize over a batch of windows (grid.y = window): per-window strides
+// (doubles) of the partial records, the moments in / out and the tables, and
+// per-window failure keys (null: FinalArgs err)
+struct FinalBatch {
+  long long part_ws, mom_in_ws, mom_out_ws, tab_ws;
+  ErrKey* errw;
 };
 
 // Coarse propagator arguments (fluid.cu).  model 0: the reference's Rusanov

@@ -38,6 +38,24 @@ __global__ void __launch_bounds__(kFinThreads, MINB) finalize_kernel(const Final
   finalize_cell(a, blockIdx.x, sm, sh);
 }
 
+// the same per-cell work for window blockIdx.y of a batch
+template <int MINB>
+__global__ void __launch_bounds__(kFinThreads, MINB)
+    finalize_batch_kernel(const FinalArgs a0, const FinalBatch b) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ double sm[];
+  __shared__ double sh[16];
+  FinalArgs a = a0;
+  const long long w = blockIdx.y;
+  if (a.part != nullptr) a.part += w * b.part_ws;
+  if (a.mom_in != nullptr) a.mom_in += w * b.mom_in_ws;
+  if (a.mom_out != nullptr) a.mom_out += w * b.mom_out_ws;
+  if (a.tab != nullptr) a.tab += w * b.tab_ws;
+  if (b.errw != nullptr) a.err = b.errw + w;
+  finalize_cell(a, blockIdx.x, sm, sh);
+}
+
 __global__ void set_key_kernel(ErrKey* p, ErrKey v) { *p = v; }
 
 cudaError_t launch_finalize(const FinalArgs& a, cudaStream_t st) {
@@ -61,6 +79,18 @@ cudaError_t launch_finalize(const FinalArgs& a, cudaStream_t st) {
     if (e != cudaSuccess) return e;
   }
   return launch_pdl(k, a.nx, kFinThreads, smem, st, a);
+}
+
+cudaError_t launch_finalize_batch(const FinalArgs& a, const FinalBatch& b, int nwin, cudaStream_t st) {
+  size_t smem = (size_t)2 * (a.nvx + a.nvy + a.nvz) * sizeof(double);
+  if (a.mom_in == nullptr && a.mode != kFinIdentity)
+    smem += (size_t)chunk_scratch(a.t, a.nvx, a.nvy, a.nvz) * sizeof(double);
+  auto k = finalize_batch_kernel<4>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  return launch_pdl_grid(k, dim3(a.nx, nwin), kFinThreads, smem, st, a, b);
 }
 
 cudaError_t launch_set_key(ErrKey* p, ErrKey v, cudaStream_t st) {

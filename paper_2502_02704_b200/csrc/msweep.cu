@@ -148,6 +148,11 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
   const Tiling& T = a.t;
   const int tid = threadIdx.x;
   const int nx = a.nx, nvx = a.nvx;
+  // window of a batched launch (grid.y; 0 otherwise) and its buffers
+  const int win = blockIdx.y;
+  double* const fout = a.fout != nullptr ? a.fout + (size_t)win * a.f_ws : nullptr;
+  double* const part = a.part != nullptr ? a.part + (size_t)win * a.p_ws : nullptr;
+  ErrKey* const errp = a.errw != nullptr ? a.errw + win : a.err;
   const int nlev = a.nlev;
   double* AK = reinterpret_cast<double*>(smem + (size_t)ns * STAGEB);     // [nvx][L] a = (dt/dx)|c_x|
   double* RB = reinterpret_cast<double*>(AK + L * nvx * (PBGK_MS_AONLY ? 1 : 2));                    // FINAL: [2][FR][NW][RS]
@@ -164,7 +169,8 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
   for (int j = tid; j < L * nvx; j += NTHR_K) {
     const int jx = j / L, l = j - jx * L;
     const double c = a.cx[jx];
-    const double av = a.dtdx[l] * (c < 0.0 ? -c : c);
+    const double dtl = a.dts == nullptr ? a.dtdx[l] : (l < nlev ? a.dts[(size_t)(a.s0 + l) * a.dts_g + win] / a.dx : 0.0);
+    const double av = dtl * (c < 0.0 ? -c : c);
 #if PBGK_MS_AONLY
     AK[j] = av;
 #else
@@ -334,7 +340,7 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
 #pragma unroll
         for (int qq = 1; qq < NW; ++qq) s += R0[(size_t)qq * RS + off];
       }
-      a.part[(size_t)RI[set * FR + q] * T.PS + ent] = s;
+      part[(size_t)RI[set * FR + q] * T.PS + ent] = s;
     }
   };
   // the pass's last level of a run plane: R_S (FINAL), the store, the
@@ -353,8 +359,8 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
         for (int v = 0; v < 2; ++v) x[k][v] = rl.x * fma(wk, gz[v], x[k][v]);
       }
     }
-    if (a.fout != nullptr) {
-      double* d = a.fout + (size_t)i * a.plane + goff;
+    if (fout != nullptr) {
+      double* d = fout + (size_t)i * a.plane + goff;
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
         d[(size_t)k * a.nvz] = x[k][0];
@@ -429,7 +435,7 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
           so = a.gzo + tg.z0 + 2 * q; dof = 2 + A + BY + 2 * q;
         }
         cpl[r] = ok ? pl : -1;
-        cptr[r] = ((FINAL && l == L) ? a.tabR : a.tab[l < L ? l : 0]) + so;
+        cptr[r] = ((FINAL && l == L) ? a.tabR : a.tab[l < L ? l : 0]) + (size_t)win * a.t_ws + so;
         cdst[r] = (int)(pl * (PLB / 8) + BOXB / 8) + l * TS + dof;
       }
     };
@@ -482,7 +488,7 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
 #pragma unroll
         for (int pl = 0; pl < P; ++pl)
           if (ip[pl] >= 0 && !SYNTH)
-            tma_load_4d(st + pl * PLB, &fmap, ltg.z0, ltg.y0, ltg.r0, ip[pl], &full[s]);
+            tma_load_4d(st + pl * PLB, &fmap, ltg.z0, ltg.y0, ltg.r0, ip[pl] + win * nx, &full[s]);
       }
       {
         // the table-row slices of every level of the item's planes: 16-byte
@@ -512,7 +518,7 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
         while (ld_acquire_gpu(a.prog) < a.need) {
           __nanosleep(256);
           if (++spins > 20000000LL) {
-            atomicMin(a.err, err_key(0, a.step0, kErrSync));
+            atomicMin(errp, err_key(0, a.step0, kErrSync));
             break;
           }
         }
@@ -567,7 +573,7 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
       issue_next();
     });
     if (NG == 1 && FINAL && nfin % FR) flush((nfin / FR) & 1, nfin % FR);
-    if (NG == 1 && !isfinite(acc)) atomicMin(a.err, err_key(0, a.step0, kErrNonFiniteMulti));
+    if (NG == 1 && !isfinite(acc)) atomicMin(errp, err_key(0, a.step0, kErrNonFiniteMulti));
     return;
   }
 
@@ -605,7 +611,7 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
     }
   });
   if (FINAL && nfin % FR) flush((nfin / FR) & 1, nfin % FR);
-  if (!isfinite(acc)) atomicMin(a.err, err_key(0, a.step0, kErrNonFiniteMulti));
+  if (!isfinite(acc)) atomicMin(errp, err_key(0, a.step0, kErrNonFiniteMulti));
 }
 
 #ifndef PBGK_MS_P
@@ -645,7 +651,7 @@ int msweep_tiling(int nvx, int nvy, int nvz, Tiling* t) {
 }
 
 template <int L, int MODE>
-static cudaError_t launch_ms(const CUtensorMap& map, const MSweepArgs& a, int grid, int ns, size_t smem,
+static cudaError_t launch_ms(const CUtensorMap& map, const MSweepArgs& a, dim3 grid, int ns, size_t smem,
                              cudaStream_t st) {
   auto fn = msweep_kernel<L, MODE, PBGK_MS_P, PBGK_MS_NG>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -654,11 +660,11 @@ static cudaError_t launch_ms(const CUtensorMap& map, const MSweepArgs& a, int gr
     fn<<<grid, PBGK_MS_NG * ms::NTG, smem, st>>>(map, a, ns);
     return cudaGetLastError();
   }
-  return launch_pdl(fn, grid, PBGK_MS_NG * ms::NTG, smem, st, map, a, ns);
+  return launch_pdl_grid(fn, grid, PBGK_MS_NG * ms::NTG, smem, st, map, a, ns);
 }
 
 template <int L>
-static cudaError_t launch_ms_mode(int mode, const CUtensorMap& map, const MSweepArgs& a, int grid, int ns,
+static cudaError_t launch_ms_mode(int mode, const CUtensorMap& map, const MSweepArgs& a, dim3 grid, int ns,
                                   size_t smem, cudaStream_t st) {
   switch (mode) {
     case 0: return launch_ms<L, 0>(map, a, grid, ns, smem, st);
@@ -669,9 +675,11 @@ static cudaError_t launch_ms_mode(int mode, const CUtensorMap& map, const MSweep
   }
 }
 
-// L: compiled level counts (a pass may run fewer, a.nlev <= L)
-cudaError_t launch_msweep(int L, int mode, const CUtensorMap& map, const MSweepArgs& a, int grid, int ns,
-                          size_t smem, cudaStream_t st) {
+// L: compiled level counts (a pass may run fewer, a.nlev <= L); nwin > 1: a
+// batch of windows (grid.y)
+cudaError_t launch_msweep(int L, int mode, const CUtensorMap& map, const MSweepArgs& a, int grid_x, int nwin,
+                          int ns, size_t smem, cudaStream_t st) {
+  const dim3 grid(grid_x, nwin);
   switch (L) {
     case 4: return launch_ms_mode<4>(mode, map, a, grid, ns, smem, st);
     case 8: return launch_ms_mode<8>(mode, map, a, grid, ns, smem, st);

@@ -268,6 +268,45 @@ def test_batched_windows_in_groups(levels):
         assert moment_gap(_unpack(mb[w]), _unpack(m0[w])) <= 1e-13
 
 
+@pytest.mark.parametrize("levels", LEVELS)
+@pytest.mark.parametrize("bc", BCS)
+@pytest.mark.parametrize("nsteps", [3.5, 8.0, 21.3])
+def test_equal_windows_run_as_one_batch(levels, bc, nsteps, monkeypatch):
+    # windows of equal step counts on a small grid: every pass is ONE launch
+    # over all windows (grid.y = window, capi.cu ms_windows_batched).  Same
+    # arithmetic per window as the window-by-window passes (bitwise), the
+    # oracle's P(F(L(U))) (ref/parareal.py:123-142) to 1e-12, a failing window
+    # keeps its one-step key and does not disturb its neighbours
+    from paper_2502_02704_b200.kinetic import propagate_windows
+    g, mesh = _grids(10, (16, 16, 16), 8.0)
+    kp = P.KineticParams(1e-2)
+    ctx = rt.ctx_for(g, P.BoundaryKind(bc))
+    cap = stable_dt_kinetic(g, kp)
+    spans = [nsteps * cap] * 5
+    rng = np.random.default_rng(31)
+    Us = [random_moments(10, rng) for _ in spans]
+    Us[2][0][7] = np.nan
+    mom_in = torch.stack([rt.to_device_moments(P.MomentField(*U), ctx.device) for U in Us])
+    res = []
+    for nobatch in (False, True):
+        if nobatch:
+            monkeypatch.setenv("PBGK_NO_WBATCH", "1")
+        out = ctx.empty_moments(len(spans))
+        with ctx.msweep_mode(True, levels):
+            codes = propagate_windows(ctx, mom_in, spans, g, kp, None, out)
+        res.append((out.cpu().numpy(), codes))
+    monkeypatch.delenv("PBGK_NO_WBATCH")
+    with ctx.fusion_levels(0):
+        out = ctx.empty_moments(len(spans))
+        c0 = propagate_windows(ctx, mom_in, spans, g, kp, None, out)
+    (ma, ca), (mb, cb) = res
+    assert ca == cb == c0 and c0[2] != -1 and all(c0[w] == -1 for w in (0, 1, 3, 4))
+    for w in (0, 1, 3, 4):
+        assert np.array_equal(ma[w], mb[w])
+        want = O.project(O.fine_propagate(O.lift(*Us[w], mesh), 0.0, spans[w], mesh, 1e-2, bc), mesh)
+        assert moment_gap(_unpack(ma[w]), want) <= 1e-12
+
+
 def P_table_len(ctx):
     return int(ctx.lib.pbgk_table_len(ctx.h))
 
