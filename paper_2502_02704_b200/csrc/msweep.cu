@@ -127,7 +127,14 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
   // group 1; LH = the larger share (carry registers)
   // (measured on config 4, 8 levels: 3 + 5 is 6 % faster than 4 + 4 -- group 0
   // also walks the loader; 2 + 6 spills)
-  constexpr int LA = NG == 1 ? L : (PBGK_MS_LA > 0 && PBGK_MS_LA < L ? PBGK_MS_LA : (L == 8 ? 3 : L / 2));
+#ifndef PBGK_MS_LAF
+#define PBGK_MS_LAF 4
+#endif
+  // FINAL: group 1 also applies R_S and reduces the partial records, so it
+  // takes one level fewer (4 + 4)
+  constexpr int LA = NG == 1 ? L
+                             : (PBGK_MS_LA > 0 && PBGK_MS_LA < L ? PBGK_MS_LA
+                                                                 : (L == 8 ? (FINAL ? PBGK_MS_LAF : 3) : L / 2));
   constexpr int LH = LA > L - LA ? LA : L - LA;
   constexpr int NTHR_K = NG * NTG;
   constexpr int NTAB = L + (FINAL ? 1 : 0);
@@ -332,7 +339,10 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
       const double* R0 = RB + (size_t)(set * FR + q) * NW * RS;
       double s;
       if (ent < A) {
-        s = R0[(size_t)ent * RS];
+        // the row total of warp `ent` from its line totals (a fixed tree)
+        const double* Lt = R0 + (size_t)ent * RS + 1;
+        static_assert(BY == 8, "row total tree");
+        s = ((Lt[0] + Lt[1]) + (Lt[2] + Lt[3])) + ((Lt[4] + Lt[5]) + (Lt[6] + Lt[7]));
         acc += s;
       } else {
         const int off = ent < A + BY ? 1 + (ent - A) : 1 + BY + (ent - A - BY);
@@ -371,35 +381,32 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
       // per-warp partials: line totals (the 8 lanes of a line pair), the row
       // total, the v_z partials over the warp's lines; fixed butterfly trees
       // (symmetric under index reversal)
+      // Two values reduced over 2^k lanes in k shuffles: in the first round a
+      // lane keeps one value and sends the other (the partner keeps that one),
+      // the later rounds are a butterfly of the kept value.  Every total is
+      // the tree ((a0 + a1) + (a2 + a3)) + ... of a plain butterfly.
       double lt[2], zs[2];
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        lt[k] = x[k][0] + x[k][1];
-#pragma unroll
-        for (int m = 1; m <= 4; m <<= 1) lt[k] += __shfl_xor_sync(0xffffffffu, lt[k], m);
-      }
-      double rt = lt[0] + lt[1];
+      for (int k = 0; k < 2; ++k) lt[k] = x[k][0] + x[k][1];
 #pragma unroll
       for (int v = 0; v < 2; ++v) zs[v] = x[0][v] + x[1][v];
-#pragma unroll
-      for (int m = 8; m <= 16; m <<= 1) {
-        rt += __shfl_xor_sync(0xffffffffu, rt, m);
-#pragma unroll
-        for (int v = 0; v < 2; ++v) zs[v] += __shfl_xor_sync(0xffffffffu, zs[v], m);
-      }
+      const bool zodd = zp & 1, yodd = yp & 1;
+      // line totals over the 8 lanes of a line pair: even zp ends with line
+      // yl, odd zp with line yl + 1
+      double ltot = (zodd ? lt[1] : lt[0]) + __shfl_xor_sync(0xffffffffu, zodd ? lt[0] : lt[1], 1);
+      ltot += __shfl_xor_sync(0xffffffffu, ltot, 2);
+      ltot += __shfl_xor_sync(0xffffffffu, ltot, 4);
+      // v_z partials over the warp's lines: even yp ends with element 0, odd
+      // yp with element 1
+      double ztot = (yodd ? zs[1] : zs[0]) + __shfl_xor_sync(0xffffffffu, yodd ? zs[0] : zs[1], 8);
+      ztot += __shfl_xor_sync(0xffffffffu, ztot, 16);
       // into the batch slot of this record; the records of a batch are
-      // reduced after one barrier (FR records per barrier)
+      // reduced after one barrier (FR records per barrier); the row total is
+      // summed from the line totals there
       const int slot = nfin % FR, set = (nfin / FR) & 1;
       double* R = RB + ((size_t)(set * FR + slot) * NW + w) * RS;
-      if (lane == 0) R[0] = rt;
-      if (zp == 0) {
-        R[1 + yl] = lt[0];
-        R[1 + yl + 1] = lt[1];
-      }
-      if (yp == 0) {
-        R[1 + BY + zo] = zs[0];
-        R[1 + BY + zo + ZS] = zs[1];
-      }
+      if (zp < 2) R[1 + yl + zp] = ltot;
+      if (yp < 2) R[1 + BY + zo + ZS * yp] = ztot;
       if (gt == 0) RI[set * FR + slot] = (long long)i * T.NT + t;
       if (++nfin % FR == 0) flush(set, FR);
     } else {
