@@ -36,7 +36,8 @@ size_t msweep_smem_bytes(int L, int mode, int nvx, int ns);
 int msweep_ctas_per_sm();
 int msweep_tiling(int nvx, int nvy, int nvz, Tiling* t);
 int esweep_levels(int nvx, int nvz);
-size_t esweep_smem_bytes(int nvx);
+size_t esweep_smem_bytes(int nvx, bool fin);
+void esweep_tiling(int nvx, int nvy, int nvz, Tiling* t);
 int esweep_ctas_per_sm(int nvx);
 cudaError_t launch_esweep(const ESweepArgs& a, bool synth, int grid, size_t smem, cudaStream_t st);
 cudaError_t launch_marg(const MargArgs& m, const FinalArgs& f, double* gsum, int s, int nwin,
@@ -1088,17 +1089,33 @@ int es_levels(pbgk_ctx* c) {
   static const int env = getenv("PBGK_ES") ? atoi(getenv("PBGK_ES")) : -1;  // dev A/B knob
   if (!(env >= 0 ? env : c->es) || c->x_scheme != 0 || c->g.bc > 2) return 0;
   const int Lmax = esweep_levels(c->g.nvx, c->g.nvz);
-  if (Lmax < 1 || esweep_smem_bytes(c->g.nvx) > c->smem_optin) return 0;
+  if (Lmax < 1 || esweep_smem_bytes(c->g.nvx, true) > c->smem_optin) return 0;
   if (c->es_per_sm == 0) c->es_per_sm = std::max(0, esweep_ctas_per_sm(c->g.nvx));
   if (c->es_per_sm < 1) return 0;
   return c->fuse > 0 ? std::min(c->fuse, Lmax) : Lmax;
 }
 
+// The window's last field-term pass can project (FINAL): midpoint quadrature
+// (the partial records carry no quadrature weights).
+bool es_final_ok(pbgk_ctx* c) {
+  return getenv("PBGK_ES_NOFINAL") == nullptr && c->quad == 0;  // (env: A/B and test knob, read per call)
+}
+
 // One field-term pass: n levels (steps step0 .. step0+n-1) from `in` (null:
-// SYNTH, level 0 lifts tabs[0]) to `out`.
+// SYNTH, level 0 lifts tabs[0]) to `out`; FINAL (`tabR` non-null, out null):
+// R_S applied and the partial records of P(f_S) written to d_mpart.
 int run_esweep(pbgk_ctx* c, int n, const double* in, double* out, const double* const* tabs,
-               const double* dts, const double* E, double e_max, int step0, cudaStream_t st) {
+               const double* dts, const double* E, double e_max, int step0, cudaStream_t st,
+               const double* tabR = nullptr) {
   ESweepArgs a{};
+  if (tabR) {
+    Tiling t;
+    esweep_tiling(c->g.nvx, c->g.nvy, c->g.nvz, &t);
+    if (ensure_dev(c->d_mpart, c->mpart_cap, (size_t)c->g.nx * t.NT * t.PS, st)) return -1;
+    a.tabR = tabR;
+    a.part = c->d_mpart;
+    a.PS = t.PS;
+  }
   a.nx = c->g.nx;
   a.nvx = c->g.nvx;
   a.nvy = c->g.nvy;
@@ -1144,10 +1161,23 @@ int run_esweep(pbgk_ctx* c, int n, const double* in, double* out, const double* 
   a.nseg = (a.nx + a.seglen - 1) / a.seglen;
   const long long items = (long long)a.ncol * a.nseg;
   grid = (int)std::max(1LL, std::min<long long>(grid, (items + 3) / 4));
-  const size_t smem = esweep_smem_bytes(c->g.nvx);
+  const size_t smem = esweep_smem_bytes(c->g.nvx, tabR != nullptr);
   const double fbytes = 8.0 * (double)a.nx * a.nvx * a.nvy * a.nvz;
-  ProfScope ps(c, st, 2, (in ? fbytes : 0.0) + fbytes, n);
+  ProfScope ps(c, st, 2, (in ? fbytes : 0.0) + (out ? fbytes : 0.0), n);
   CK(launch_esweep(a, in == nullptr, grid, smem, st));
+  return 0;
+}
+
+// P(f_S) from the partial records of a FINAL field-term pass
+int es_project(pbgk_ctx* c, double* mom_out, int step, cudaStream_t st) {
+  FinalArgs f = fin_args(c, c->plan[0]);
+  esweep_tiling(c->g.nvx, c->g.nvy, c->g.nvz, &f.t);
+  f.part = c->d_mpart;
+  f.mode = kFinProject;
+  f.mom_out = mom_out;
+  f.step = step;
+  ProfScope ps(c, st, 1, 0.0);
+  CK(launch_finalize(f, st));
   return 0;
 }
 
@@ -1253,6 +1283,7 @@ int propagate_body_fused(pbgk_ctx* c, const double* f0, const double* mom0, doub
     rc = ms_window(c, LM, f0, f_out, f_tmp, write_final, mom_out, T, S, h_dts, st, prog, base);
   } else {
     int w = 0;
+    bool projected = false;
     const double* in = f0;
     for (int s0 = 0; s0 < S && rc == 0;) {
       const int n = std::min(L, S - s0);
@@ -1261,6 +1292,13 @@ int propagate_body_fused(pbgk_ctx* c, const double* f0, const double* mom0, doub
       for (int l = 0; l < n; ++l) {
         tabs[l] = T + (size_t)(s0 + l) * tstep;
         dtdx[l] = h_dts[s0 + l] / c->dx;
+      }
+      if (field && LE > 0 && s0 + n == S && !write_final && mom_out && es_final_ok(c)) {
+        // the window's last pass: R_S and the projection folded in (no f_S)
+        rc = run_esweep(c, n, in, nullptr, tabs, h_dts + s0, E, e_max, s0 + 1, st, T + (size_t)S * tstep);
+        if (rc == 0) rc = es_project(c, mom_out, S + 1, st);
+        projected = true;
+        break;
       }
       double* out = buf(++w);
       if (field && LE > 0) {
@@ -1278,10 +1316,10 @@ int propagate_body_fused(pbgk_ctx* c, const double* f0, const double* mom0, doub
       s0 += n;
     }
     if (prog && rc == 0) rc = cudaStreamWaitEvent(st, c->ev_done, 0) == cudaSuccess ? 0 : fail("event");
-    if (rc == 0)
+    if (rc == 0 && !projected)
       rc = run_sweep(c, 0, false, in, T + (size_t)S * tstep, write_final ? f_out : nullptr, 0.0, nullptr,
                      0.0, 0.0, S, st);
-    if (rc == 0 && mom_out)
+    if (rc == 0 && mom_out && !projected)
       rc = run_final(c, 0, kFinProject, nullptr, mom_out, nullptr, 0, 1, 1, nullptr, S + 1, st);
   }
   // the side-stream recursion joins the stream on every exit path (its
@@ -1459,6 +1497,7 @@ int windows_fused(pbgk_ctx* c, int nwin, const double* mom_in, double* mom_out, 
       auto buf = [&](int i) { return ((P - i) % 2 == 0) ? f_a : f_b; };
       const double* in = nullptr;
       int s0 = 0, wcount = 0;
+      bool projected = false;
       while (s0 < S) {
         const int n = std::min(L, S - s0);
         const double* tabs[kMaxLevels];
@@ -1466,6 +1505,15 @@ int windows_fused(pbgk_ctx* c, int nwin, const double* mom_in, double* mom_out, 
         for (int l = 0; l < n; ++l) {
           tabs[l] = T + (size_t)(s0 + l) * tstep;
           dtdx[l] = h_dts[off[w] + s0 + l] / c->dx;
+        }
+        if (field && LE > 0 && s0 + n == S && es_final_ok(c)) {
+          // the window's last pass: R_S and the projection folded in (no f_S)
+          int rcf = run_esweep(c, n, in, nullptr, tabs, h_dts + off[w] + s0, E, e_max, s0 + 1, st,
+                               T + (size_t)S * tstep);
+          if (rcf == 0) rcf = es_project(c, mom_out + w * m5, S + 1, st);
+          if (rcf) { c->err_slot = nullptr; return -1; }
+          projected = true;
+          break;
         }
         double* out = buf(++wcount);
         const int rc = (field && LE > 0)
@@ -1476,6 +1524,10 @@ int windows_fused(pbgk_ctx* c, int nwin, const double* mom_in, double* mom_out, 
         if (rc) { c->err_slot = nullptr; return -1; }
         in = out;
         s0 += n;
+      }
+      if (projected) {
+        c->err_slot = nullptr;
+        continue;
       }
       const int rc1 = run_sweep(c, 0, false, in, T + (size_t)S * tstep, nullptr, 0.0, nullptr, 0.0, 0.0,
                                 S, st);

@@ -155,6 +155,14 @@ struct ESweepArgs {
   int nseg, seglen;    // x segments per column and their length (planes)
   ErrKey* err;
   int step0;
+  // FINAL (the window's last pass, tabR non-null): R_S (tabR) applied to the
+  // last level's output and, instead of the store, the partial records
+  // [m_x rows | m_y | m_z of the column's 8 v_z] of every (plane, warp column)
+  // written to part (stride PS doubles, NT = ncol records per plane) for
+  // finalize.cu (kFinProject)
+  const double* tabR;
+  double* part;
+  int PS;
 };
 
 // Moment recursion (marginal.cu): five weighted sums of f over (v_y, v_z)

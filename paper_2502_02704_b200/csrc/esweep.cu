@@ -35,6 +35,12 @@
 //     pipeline of D positions.
 //   * SYNTH (the window's first pass from moments): level 0 input is the lift
 //     f_0 = ls g_x g_y g_z of tab[0] (ref/lifting.py:47-57), no f read.
+//   * FINAL (the window's last pass): R_S (ref/kinetic.py:130-134) applied to
+//     the last level's output and the column's marginal partial record
+//     [m_x rows | m_y | m_z] written per plane for finalize.cu (kFinProject,
+//     the projection P(f_S) of ref/moments.py:60-112) instead of f_S: no
+//     store and no read-back of f_S.  Fixed trees, the same for every entry
+//     and its mirror (even data keeps an exactly zero folded first moment).
 //
 // Ghost planes (bc 0 absorbing: 0; bc 2 outflow: the edge plane of the same
 // level) are substituted where level l's neighbour plane falls outside the
@@ -86,7 +92,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // The position stream of one warp: items (column, x segment) gw, gw + W, ...;
 // an item's input positions p = ps .. pe (inclusive), see the header.
 struct EsIt {
-  int item, p, pe, x0, x1, y, z0;
+  int item, p, pe, x0, x1, y, z0, col;
   long long foff;  // (y nvz + z0): the column's offset inside a v_x row of a plane (doubles)
   bool done;
   __device__ __forceinline__ void setup(const ESweepArgs& a, int n) {
@@ -95,7 +101,7 @@ struct EsIt {
       done = true;
       return;
     }
-    const int col = item / a.nseg;
+    col = item / a.nseg;
     const int seg = item - col * a.nseg;
     const int nzb = a.nvz / es::ZW;
     y = col / nzb;
@@ -125,14 +131,15 @@ struct EsIt {
   }
 };
 
-template <int V, int L, bool SYNTH, int D>
+template <int V, int L, bool SYNTH, int D, bool FINAL>
 __global__ void __launch_bounds__(es::NTHR, 2)
     esweep_kernel(const __grid_constant__ ESweepArgs a) {
   using namespace es;
   constexpr int H = V / 2;    // rows of each c_x sign per lane
   constexpr int SL = slice(V);
   constexpr int NX8 = 8 * V;  // nvx
-  constexpr uint32_t STB = (uint32_t)stage_bytes(V, L);
+  constexpr int NS = L + (FINAL ? 1 : 0);  // table slices per stage (FINAL: R_S after the levels)
+  constexpr uint32_t STB = (uint32_t)stage_bytes(V, NS);
   constexpr uint32_t FB = 32u * V * 16u;  // f area of a stage
   extern __shared__ __align__(128) unsigned char smem[];
 
@@ -193,12 +200,13 @@ __global__ void __launch_bounds__(es::NTHR, 2)
       }
       const int so = soff0 + (rz ? it.z0 : (ry ? it.y : 0));
 #pragma unroll
-      for (int l = 0; l < L; ++l) {
-        if (l >= n) break;
+      for (int l = 0; l < NS; ++l) {
+        if (l >= n + (FINAL ? 1 : 0)) break;
         int q = q0 - l;
         if (periodic && q < 0) q += nx;
         const bool on = q >= 0 && q < nx;
-        const double* src = rE ? a.E + q : a.tab[l] + ((long long)q * a.TL + so);
+        const double* tb = (FINAL && l == n) ? a.tabR : a.tab[l < L ? l : 0];  // slot n: R_S of plane p - n
+        const double* src = rE ? a.E + q : tb + ((long long)q * a.TL + so);
         const uint32_t dst = S + FB + (uint32_t)(l * SL + doff) * 8u;
         cp_async_16_if(dst, src, on && r16);
         cp_async_8_if(dst, src, on && r8);
@@ -394,11 +402,58 @@ __global__ void __launch_bounds__(es::NTHR, 2)
     // output plane p - n of the last level
     const int qo = p - n;
     if (qo >= it.x0 && qo < it.x1) {
-      double* dst = a.fout + ((long long)qo * plane + lane_f + it.foff);
+      if constexpr (FINAL) {
+        // f_S = R_S(f*_S) of plane qo (slice n of the stage), then the
+        // column's partial record.  Trees: a row total = the lane's two v_z,
+        // then a butterfly over the 4 v_z pairs; an m_z entry = the lane's
+        // rows in order, then a butterfly over the 8 row groups; m_y = the
+        // lane's row totals in order, then the butterfly over the row groups.
+        const double* T = ST + n * SL;
+        const double2 rl = *reinterpret_cast<const double2*>(T);
+        const double2 ge = *reinterpret_cast<const double2*>(T + NX8 + 2);
+        const double2 gz = *reinterpret_cast<const double2*>(T + NX8 + 4 + 2 * c);
+        const double rlg = (rl.x * rl.y) * ge.x;
+        double t[V], zs[2] = {0.0, 0.0};
 #pragma unroll
-      for (int v = 0; v < V; ++v) {
-        st_global_v2(dst + (long long)(v < H ? v : NX8 / 2 - H + v) * rs, x[v][0], x[v][1]);
-        acc += x[v][0] + x[v][1];
+        for (int v = 0; v < V; ++v) {
+          const double w = rlg * T[2 + (v < H ? rd0 + v : ru0 + (v - H))];
+          const double y0 = fma(w, gz.x, rl.x * x[v][0]);
+          const double y1 = fma(w, gz.y, rl.x * x[v][1]);
+          t[v] = y0 + y1;
+          zs[0] = v == 0 ? y0 : zs[0] + y0;
+          zs[1] = v == 0 ? y1 : zs[1] + y1;
+        }
+#pragma unroll
+        for (int m = 1; m <= 2; m <<= 1)
+#pragma unroll
+          for (int v = 0; v < V; ++v) t[v] += __shfl_xor_sync(0xffffffffu, t[v], m);
+        double tot = t[0];
+#pragma unroll
+        for (int v = 1; v < V; ++v) tot += t[v];
+#pragma unroll
+        for (int m = 4; m <= 16; m <<= 1) {
+          tot += __shfl_xor_sync(0xffffffffu, tot, m);
+          zs[0] += __shfl_xor_sync(0xffffffffu, zs[0], m);
+          zs[1] += __shfl_xor_sync(0xffffffffu, zs[1], m);
+        }
+        acc += tot;
+        double* R = a.part + ((long long)qo * a.ncol + it.col) * a.PS;
+        if (c == 0) {
+#pragma unroll
+          for (int v = 0; v < V; ++v) R[v < H ? rd0 + v : ru0 + (v - H)] = t[v];
+        }
+        if (s == 0) {
+          R[NX8 + 1 + 2 * c] = zs[0];
+          R[NX8 + 2 + 2 * c] = zs[1];
+        }
+        if (lane == 0) R[NX8] = tot;
+      } else {
+        double* dst = a.fout + ((long long)qo * plane + lane_f + it.foff);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          st_global_v2(dst + (long long)(v < H ? v : NX8 / 2 - H + v) * rs, x[v][0], x[v][1]);
+          acc += x[v][0] + x[v][1];
+        }
       }
     }
   };
@@ -475,17 +530,33 @@ int esweep_levels(int nvx, int nvz) {
 #endif
 constexpr int kEsD = PBGK_ES_D;  // ring stages per warp
 
-size_t esweep_smem_bytes(int nvx) {
+size_t esweep_smem_bytes(int nvx, bool fin) {
   const int V = nvx / 8;
   const int L = esweep_levels(nvx, 8);
-  return (size_t)es::NW * kEsD * es::stage_bytes(V, L);
+  return (size_t)es::NW * kEsD * es::stage_bytes(V, L + (fin ? 1 : 0));
+}
+
+// the tiling of the FINAL pass's partial records for finalize.cu: one tile per
+// warp column (all v_x rows x 1 v_y x 8 v_z)
+void esweep_tiling(int nvx, int nvy, int nvz, Tiling* t) {
+  t->A = nvx;
+  t->By = 1;
+  t->Bz = es::ZW;
+  t->rows_load = nvx;
+  t->nneg = 0;
+  t->ntn = 0;
+  t->ntp = 1;
+  t->nty = nvy;
+  t->ntz = nvz / es::ZW;
+  t->NT = t->nty * t->ntz;
+  t->PS = nvx + 10;
 }
 
 int esweep_ctas_per_sm(int nvx);
 
-template <int V, int L, bool SYNTH>
+template <int V, int L, bool SYNTH, bool FINAL>
 static cudaError_t launch_es(const ESweepArgs& a, int grid, size_t smem, cudaStream_t st) {
-  auto fn = esweep_kernel<V, L, SYNTH, kEsD>;
+  auto fn = esweep_kernel<V, L, SYNTH, kEsD, FINAL>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   return launch_pdl(fn, grid, es::NTHR, smem, st, a);
@@ -494,14 +565,15 @@ static cudaError_t launch_es(const ESweepArgs& a, int grid, size_t smem, cudaStr
 template <int V, int L>
 static int occ(size_t smem) {
   int n = 0;
-  auto fn = esweep_kernel<V, L, false, kEsD>;
+  auto fn = esweep_kernel<V, L, false, kEsD, true>;
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, es::NTHR, smem) != cudaSuccess) return 0;
   return n;
 }
 
+// resident CTAs per SM (of the FINAL build: the larger stage)
 int esweep_ctas_per_sm(int nvx) {
-  const size_t smem = esweep_smem_bytes(nvx);
+  const size_t smem = esweep_smem_bytes(nvx, true);
   switch (nvx / 8) {
     case 2: return occ<2, PBGK_ES_L2>(smem);
     case 4: return occ<4, PBGK_ES_L4>(smem);
@@ -512,7 +584,9 @@ int esweep_ctas_per_sm(int nvx) {
 
 template <int V, int L>
 static cudaError_t launch_es_v(const ESweepArgs& a, bool synth, int grid, size_t smem, cudaStream_t st) {
-  return synth ? launch_es<V, L, true>(a, grid, smem, st) : launch_es<V, L, false>(a, grid, smem, st);
+  const bool fin = a.tabR != nullptr;
+  if (synth) return fin ? launch_es<V, L, true, true>(a, grid, smem, st) : launch_es<V, L, true, false>(a, grid, smem, st);
+  return fin ? launch_es<V, L, false, true>(a, grid, smem, st) : launch_es<V, L, false, false>(a, grid, smem, st);
 }
 
 cudaError_t launch_esweep(const ESweepArgs& a, bool synth, int grid, size_t smem, cudaStream_t st) {

@@ -147,3 +147,84 @@ def test_non_finite_start_key_equals_one_step_path(levels):
     with pytest.raises(P.BlowUpError) as info:
         rt.raise_kinetic(c)
     assert info.value.step == 1
+
+
+def _window_moments(g, bc, E, t1, levels, U):
+    """P(f_S) of one window from moments, no f_S wanted: the last field pass
+    projects (FINAL) unless PBGK_ES_NOFINAL is set."""
+    kp = P.KineticParams(1e-2, force=E)
+    ctx = rt.ctx_for(g, P.BoundaryKind(bc))
+    m0 = rt.to_device_moments(P.MomentField(*U), ctx.device)
+    dts = fine_schedule(t1, stable_dt_kinetic(g, kp))
+    out, mo = ctx.empty_f(), ctx.empty_moments()
+    with ctx.fusion_levels(levels), ctx.esweep_mode(True):
+        code = _run_schedule(ctx, None, m0, dts, kp, out, want_f=False, mom_out=mo)
+    torch.cuda.synchronize()
+    return mo.cpu().numpy(), code, len(dts)
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "x".join(map(str, (s[0],) + s[1])))
+@pytest.mark.parametrize("bc", BCS)
+@pytest.mark.parametrize("levels", [1, 2, 3, 4])
+def test_final_pass_projects_like_the_oracle(shape, bc, levels, monkeypatch):
+    # the window's last field pass applies R_S and writes the partial records
+    # of P(f_S) (ref/kinetic.py:130-134, ref/moments.py:60-112) instead of f_S;
+    # 5.5 / 8 steps: ragged and full last passes, a single SYNTH + FINAL pass
+    nx, nv, vm = shape
+    g, mesh = _grids(nx, nv, vm)
+    E = _field(mesh)
+    U = random_moments(nx, np.random.default_rng(11 * nx + levels))
+    for steps in (2.5, 7.5):
+        t1 = steps * O.fine_cap(mesh, 0.5, E)
+        m, code, S = _window_moments(g, bc, E, t1, levels, U)
+        monkeypatch.setenv("PBGK_ES_NOFINAL", "1")
+        m1, c1, _ = _window_moments(g, bc, E, t1, levels, U)
+        monkeypatch.delenv("PBGK_ES_NOFINAL")
+        assert code == c1 == -1
+        want = O.project(O.fine_propagate(O.lift(*U, mesh), 0.0, t1, mesh, 1e-2, bc, E), mesh)
+        assert moment_gap(_unpack(m), want) <= 1e-12
+        assert moment_gap(_unpack(m), _unpack(m1)) <= 1e-13
+
+
+def test_final_pass_even_data_keeps_zero_transverse_velocity():
+    # u_y = u_z = 0 data stays even in v_y, v_z under F with a v_x force: the
+    # folded first moments (ref/moments.py:80-88) of the FINAL pass's records
+    # are exactly zero (the same tree for an entry and its mirror)
+    g, mesh = _grids(12, (32, 16, 16), 8.0)
+    E = _field(mesh)
+    rho, u, th = random_moments(12, np.random.default_rng(2))
+    u[:, 1:] = 0.0
+    for bc in BCS:
+        m, code, _ = _window_moments(g, bc, E, 9.5 * O.fine_cap(mesh, 0.5, E), -1, (rho, u, th))
+        assert code == -1
+        assert np.all(m[2] == 0.0) and np.all(m[3] == 0.0)
+
+
+def test_final_pass_windows_keys_and_groups(monkeypatch):
+    # pbgk_propagate_windows with a force: windows of different lengths, an
+    # empty and a failing one; FINAL passes vs the separate final sweep
+    from paper_2502_02704_b200.kinetic import propagate_windows
+    g, mesh = _grids(10, (32, 8, 8), 8.0)
+    E = _field(mesh)
+    kp = P.KineticParams(1e-2, force=E)
+    ctx = rt.ctx_for(g, P.BoundaryKind.PERIODIC)
+    cap = stable_dt_kinetic(g, kp)
+    spans = [9.5 * cap, 3.0 * cap, 0.0, 6.2 * cap, 6.0 * cap]
+    rng = np.random.default_rng(19)
+    Us = [random_moments(10, rng) for _ in spans]
+    Us[3][0][4] = np.nan
+    mom_in = torch.stack([rt.to_device_moments(P.MomentField(*U), ctx.device) for U in Us])
+    res = []
+    for nofinal in (False, True):
+        if nofinal:
+            monkeypatch.setenv("PBGK_ES_NOFINAL", "1")
+        out = ctx.empty_moments(len(spans))
+        codes = propagate_windows(ctx, mom_in, spans, g, kp, None, out)
+        res.append((out.cpu().numpy(), codes))
+    monkeypatch.delenv("PBGK_ES_NOFINAL")
+    (ma, ca), (mb, cb) = res
+    assert ca == cb and ca[3] != -1 and ca[2] == -1
+    for w in (0, 1, 2, 4):
+        assert moment_gap(_unpack(ma[w]), _unpack(mb[w])) <= 1e-13
+    want = O.project(O.fine_propagate(O.lift(*Us[0], mesh), 0.0, spans[0], mesh, 1e-2, "periodic", E), mesh)
+    assert moment_gap(_unpack(ma[0]), want) <= 1e-12
