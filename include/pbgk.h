@@ -124,7 +124,8 @@ int pbgk_propagate_windows(pbgk_ctx* ctx, int nwin, const double* mom_in, double
 /* Coarse Euler propagator G (ref/fluid.py:91-125) on one GPU: advance
  * `nwin` independent primitive states mom_in[w] (double[nwin][5][nx]) over
  * [h_t0[w], h_t1[w]] into mom_out[w]; when `minuend` is non-NULL the output
- * is minuend[w] - G(mom_in[w]) (the parareal jump, ref/parareal.py:142).
+ * is minuend[w] - G(mom_in[w]) (the parareal jump, ref/parareal.py:142);
+ * `minuend` may alias `mom_out` (each entry is read, then written, by one thread).
  * dt_max <= 0 means no cap.  force: per-cell E or NULL.  Failure keys carry
  * the window index (0-based) as unit. */
 int pbgk_fluid_propagate(pbgk_ctx* ctx, int nwin, const double* mom_in, double* mom_out,

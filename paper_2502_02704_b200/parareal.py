@@ -198,9 +198,16 @@ class GpuBackend:
         """out[w] = P F L(snaps[n-1]) - G(snaps[n-1]) for n = windows[w]; status per window."""
         codes = []
         t = self.times
+        src = None
+        if windows:
+            # a rank's windows are consecutive (work_distribution): their start
+            # states are a view of the snapshots, no gather
+            if windows == list(range(windows[0], windows[0] + len(windows))):
+                src = snaps[windows[0] - 1:windows[0] - 1 + len(windows)]
+            else:
+                src = snaps[torch.tensor([n - 1 for n in windows], device=self.device)]
         if windows and tau_constant(self.kinetic.tau) is not None:
             # the whole fine stage in one library call (one host sync)
-            src = snaps[torch.tensor([n - 1 for n in windows], device=self.device)]
             tic = time.perf_counter()
             codes = propagate_windows(self.ctx, src, [t[n] - t[n - 1] for n in windows],
                                       self.disc.phase, self.kinetic, self.disc.time.dt_f,
@@ -214,11 +221,10 @@ class GpuBackend:
                 self.t_kin = max(self.t_kin, time.perf_counter() - tic)
                 codes.append(c)
         if windows:
-            src = snaps[torch.tensor([n - 1 for n in windows], device=self.device)]
             tic = time.perf_counter()
             gc = fluid_batch(self.ctx, src, out[:len(windows)], [t[n - 1] for n in windows],
                              [t[n] for n in windows], self.fluid, self.disc.time.dt_g,
-                             minuend=out[:len(windows)].clone(), force_dev=self.force_dev)
+                             minuend=out[:len(windows)], force_dev=self.force_dev)  # in place: each entry is read, then written, by one thread
             self.t_fluid = max(self.t_fluid, (time.perf_counter() - tic) / len(windows))
             if gc >= 0:
                 # the failing window of the batch (unit = batch index)
