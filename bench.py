@@ -318,8 +318,10 @@ def run_ours(args, w, world, rank, local):
     # the multi-step path, else the one-step sweep (sweep_impl.cuh)
     multi = prof.msweeps > 0 and prof.msweep_ms >= prof.sweep_ms
     ms_levels = ctx.msweep_levels() if hasattr(ctx, "msweep_levels") else 0
+    field = w.force_kind is not None
+    es_levels = ctx.esweep_levels() if (field and hasattr(ctx, "esweep_levels")) else 0
     if multi:
-        kern = "msweep_kernel" if ms_levels > 0 else "fsweep_kernel"
+        kern = "esweep_kernel" if es_levels > 0 else ("msweep_kernel" if ms_levels > 0 else "fsweep_kernel")
         kms, kbytes, kn = prof.msweep_ms, prof.msweep_bytes, prof.msweeps
         bpu = prof.msweep_bytes / (prof.msweep_steps * w.cells)
     else:
@@ -356,11 +358,12 @@ def run_ours(args, w, world, rank, local):
                           "f (16 B/cell), the last reads f and writes only the partial records of "
                           "P(f_S) (8 B/cell): 16 (P-1) B per cell per window, i.e. 16 (P-1)/S "
                           "B per cell-update (ref: 16 B, one read + one write per step)",
-            "levels_per_pass": ms_levels if ms_levels > 0 else None,
-            "note": "'achieved' / 'frac' are the pass kernel's own algorithmic f bytes over its "
-                    "CUDA-event time; at 8 levels per pass the kernel is bound by its fp64 + "
-                    "shared-memory instruction stream, not by HBM (profiles/), so frac is the "
-                    "HBM share it leaves unused; value_over_one_step_roofline compares the "
+            "levels_per_pass": es_levels if es_levels > 0 else (ms_levels if ms_levels > 0 else None),
+            "note": "'achieved' / 'frac' are the pass kernel's own algorithmic f bytes (averaged "
+                    "over the window's first / steady / last passes, like 'traffic') over its "
+                    "CUDA-event time; with several levels per pass the kernel is bound by its "
+                    "fp64 + shared-memory instruction stream, not by HBM (profiles/), so frac is "
+                    "the HBM share it leaves unused; value_over_one_step_roofline compares the "
                     "cell-update rate with the one-step design's 16 B/update HBM bound"})
 
     e2e = None

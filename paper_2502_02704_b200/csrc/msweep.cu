@@ -56,6 +56,9 @@
 #ifndef PBGK_MS_ZSPLIT
 #define PBGK_MS_ZSPLIT 0
 #endif
+#ifndef PBGK_MS_HINT
+#define PBGK_MS_HINT 1
+#endif
 #ifndef PBGK_MS_GYASM
 #define PBGK_MS_GYASM 1
 #endif
@@ -455,6 +458,10 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
     int pstg = 0;
     uint32_t pph = 0;
     const int dist = ns - 2;  // items loaded ahead (group 1 trails by about one item)
+    // L2 policies: the table slices of a plane are re-read by every tile
+    // (keep), f streams through once per pass
+    const uint64_t pol_keep = PBGK_MS_HINT >= 1 ? make_policy_evict_last() : 0;
+    const uint64_t pol_stream = PBGK_MS_HINT >= 2 ? make_policy_evict_first() : 0;
     auto issue_next = [&]() {
       if (!lmore) return;
       if (lu >= lnit) {
@@ -495,7 +502,13 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
 #pragma unroll
         for (int pl = 0; pl < P; ++pl)
           if (ip[pl] >= 0 && !SYNTH)
-            tma_load_4d(st + pl * PLB, &fmap, ltg.z0, ltg.y0, ltg.r0, ip[pl] + win * nx, &full[s]);
+          {
+            if (PBGK_MS_HINT >= 2)
+              tma_load_4d_hint(st + pl * PLB, &fmap, ltg.z0, ltg.y0, ltg.r0, ip[pl] + win * nx, &full[s],
+                               pol_stream);
+            else
+              tma_load_4d(st + pl * PLB, &fmap, ltg.z0, ltg.y0, ltg.r0, ip[pl] + win * nx, &full[s]);
+          }
       }
       {
         // the table-row slices of every level of the item's planes: 16-byte
@@ -507,7 +520,12 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
 #pragma unroll
           for (int q = 0; q < P; ++q)
             if (pl == q) i = ip[q];
-          if (i >= 0) cp_async_16(reinterpret_cast<double*>(st) + cdst[r], cptr[r] + (size_t)i * a.TL);
+          if (i >= 0) {
+            if (PBGK_MS_HINT >= 1)
+              cp_async_16_hint(reinterpret_cast<double*>(st) + cdst[r], cptr[r] + (size_t)i * a.TL, pol_keep);
+            else
+              cp_async_16(reinterpret_cast<double*>(st) + cdst[r], cptr[r] + (size_t)i * a.TL);
+          }
         }
       }
       cp_async_mbar_arrive(&full[s]);
