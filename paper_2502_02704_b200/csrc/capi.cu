@@ -1033,7 +1033,8 @@ int ms_windows_batched(pbgk_ctx* c, int L, int g, const double* T, long long t_w
   f.mode = kFinProject;
   f.mom_out = mom_out;
   f.step = S + 1;
-  FinalBatch fb{(long long)c->g.nx * c->ms_t.NT * c->ms_t.PS, 0, (long long)5 * c->g.nx, 0, errw};
+  f.relax_tab = T + (size_t)S * tstep;  // the records are those of f*_S
+  FinalBatch fb{(long long)c->g.nx * c->ms_t.NT * c->ms_t.PS, 0, (long long)5 * c->g.nx, t_ws, errw};
   ProfScope ps(c, st, 1, 0.0);
   CK(launch_finalize_batch(f, fb, g, st));
   return 0;
@@ -1075,6 +1076,8 @@ int ms_window(pbgk_ctx* c, int L, const double* f0, double* f_out, double* f_tmp
     f.mode = kFinProject;
     f.mom_out = mom_out;
     f.step = S + 1;
+    // f_S not stored: the last pass's records are those of f*_S
+    f.relax_tab = write_final ? nullptr : T + (size_t)S * tstep;
     ProfScope ps(c, st, 1, 0.0);
     CK(launch_finalize(f, st));
   }

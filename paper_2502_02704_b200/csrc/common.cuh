@@ -221,6 +221,11 @@ struct FinalArgs {
   int step;
   int check_finite;      // kFinProject: flag non-finite marginals as BlowUpError(step)
   int trap;              // trapezoidal velocity quadrature (end nodes weigh 1/2)
+  // non-null (midpoint quadrature): the partials are those of f*; the
+  // marginals of f = R(f*) = r (f* + ls g_x g_y g_z) (ref/kinetic.py:130-134,
+  // linear and separable) are formed from them with this table before the
+  // projection: m_x[j] = r (m*_x[j] + ls g_x[j] (sum g_y) (sum g_z)), ...
+  const double* relax_tab;
 };
 
 // finalize over a batch of windows (grid.y = window): per-window strides

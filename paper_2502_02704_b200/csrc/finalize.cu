@@ -52,6 +52,7 @@ __global__ void __launch_bounds__(kFinThreads, MINB)
   if (a.mom_in != nullptr) a.mom_in += w * b.mom_in_ws;
   if (a.mom_out != nullptr) a.mom_out += w * b.mom_out_ws;
   if (a.tab != nullptr) a.tab += w * b.tab_ws;
+  if (a.relax_tab != nullptr) a.relax_tab += w * b.tab_ws;
   if (b.errw != nullptr) a.err = b.errw + w;
   finalize_cell(a, blockIdx.x, sm, sh);
 }

@@ -168,6 +168,30 @@ static __device__ __forceinline__ void finalize_cell(const FinalArgs& a, int i, 
     th = a.mom_in[4 * a.nx + i];
   } else {
     if (!HAVE_MARG) gather_marginals(a, i, sm);
+    if (a.relax_tab != nullptr) {
+      // the marginals of R(f*) from those of f*: warp ax sums the factors of
+      // axis ax (lane-strided, then the butterfly: a fixed tree), then every
+      // entry adds its axis factor times the other two sums
+      const double* row = a.relax_tab + (size_t)i * a.TL;
+      if (warp < 3) {
+        const int n = nv(warp);
+        const int off = warp == 0 ? a.gxo : (warp == 1 ? a.gyo : a.gzo);
+        double s = 0.0;
+        for (int j = lane; j < n; j += 32) s += row[off + j];
+        s = warp_allsum(s);
+        if (lane == 0) sh[8 + warp] = s;
+      }
+      __syncthreads();
+      const double r = row[0], ls = row[1];
+      for (int j = tid; j < nvx + nvy + nvz; j += blockDim.x) {
+        const int ax = j < nvx ? 0 : (j < nvx + nvy ? 1 : 2);
+        const int jj = j - (ax == 0 ? 0 : (ax == 1 ? nvx : nvx + nvy));
+        const int off = ax == 0 ? a.gxo : (ax == 1 ? a.gyo : a.gzo);
+        const double other = ax == 0 ? sh[9] * sh[10] : (ax == 1 ? sh[8] * sh[10] : sh[8] * sh[9]);
+        sm[j] = r * fma(ls * row[off + jj], other, sm[j]);  // mx | my | mz are contiguous
+      }
+      __syncthreads();
+    }
     // finiteness of f* (all its values feed these sums; a NaN/Inf anywhere
     // leaves a non-finite marginal) -- the guard of ref/kinetic.py:157-159;
     // warps 1..3 test their axis while reducing the folded first moment

@@ -359,8 +359,10 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
   // the pass's last level of a run plane: R_S (FINAL), the store, the
   // partial records (FINAL) or the finiteness sum
   auto emit = [&](double (&x)[2][2], const double* tabs, int i, int t, long long goff) {
-    if constexpr (FINAL) {
-      // R_S (ref/kinetic.py:130-134) of the last level's output
+    if (FINAL && fout != nullptr) {
+      // R_S (ref/kinetic.py:130-134) of the last level's output, when f_S is
+      // stored; otherwise the records are those of f*_S and finalize forms
+      // the marginals of R_S(f*_S) from them (FinalArgs relax_tab)
       const double* S = tabs + L * TS;
       const double2 rl = *reinterpret_cast<const double2*>(S);
       const double W = rl.y * S[2 + w];
@@ -428,7 +430,8 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
 #pragma unroll
       for (int r = 0; r < CPT; ++r) {
         const int j = gt + r * NTG;
-        const bool ok = j < P * NTAB * NCH;
+        // (the R_S slice is loaded only when f_S is stored)
+        const bool ok = j < P * NTAB * NCH && !(FINAL && fout == nullptr && (j % (NTAB * NCH)) / NCH == L);
         const int pl = ok ? j / (NTAB * NCH) : 0;
         const int jj = ok ? j - pl * NTAB * NCH : 0;
         const int l = jj / NCH, c = jj - l * NCH;
