@@ -194,7 +194,9 @@ int pbgk_msweep_levels(pbgk_ctx* ctx);
 /* Multi-step passes WITH the v_x field term (esweep.cu, default on): a warp
  * owns whole v_x columns and marches an x segment, up to 4 fine steps per
  * pass (3 at nvx = 32) with the field flux's v_x neighbours in registers /
- * shuffles.  Needs nvx = 16, 32 or 48 and nvz % 8 == 0 (else, and with
+ * shuffles; the window's last pass applies R_S and writes the partial
+ * records of P(f_S) instead of f_S when only the moments are wanted (midpoint
+ * quadrature).  Needs nvx = 16, 32 or 48 and nvz % 8 == 0 (else, and with
  * on = 0, the field runs one step per pass).  An explicit pbgk_set_fusion
  * level count caps its levels.  Replaces ref/kinetic.py:152-160 with a force
  * (ref/kinetic.py:114-123) like pbgk_propagate. */
