@@ -433,7 +433,9 @@ def e2e_ours(args, w, P, phase, bc, disc, kinetic, fluid, U0, f_init, world, dev
         h2d = 5 * nx * 8 + (nx * 8 if w.force() is not None else 0)
         d2h = (3 * w.n_g + 2) * 5 * nx * 8
         times = []
-        for _ in range(E2E_WARM + reps):
+        n_calls = E2E_WARM + reps
+        k = 0
+        while k < n_calls:
             if world > 1:
                 dist.barrier()
             torch.cuda.synchronize(dev)
@@ -441,6 +443,10 @@ def e2e_ours(args, w, P, phase, bc, disc, kinetic, fluid, U0, f_init, world, dev
             traj, rec = P.run_parareal(U0h, cfg, disc, kinetic, fluid)
             torch.cuda.synchronize(dev)
             times.append(time.perf_counter() - tic)
+            k += 1
+            # millisecond-sized calls (config 0): three samples are noise, take 30
+            if k == E2E_WARM + 1 and times[-1] < 5e-3:
+                n_calls = E2E_WARM + 30
         sec = float(np.mean(times[E2E_WARM:]))
     elif args.xshard:
         # the sharded public path: each rank uploads its slab, propagates with

@@ -189,6 +189,12 @@ struct pbgk_ctx {
   ErrKey* h_err = nullptr;  // pinned
   double* h_dbl = nullptr;  // pinned small
   double* d_times = nullptr;
+  double* d_times2 = nullptr;             // coarse times of the correction sweep
+  size_t times2_cap = 0;
+  // host copies of what the small per-call upload buffers hold: an unchanged
+  // upload (the same schedule / time grid in every parareal iteration) is skipped
+  std::vector<double> sh_times, sh_times2, sh_bdts;
+  std::vector<int> sh_bnst;
   size_t times_cap = 0;
   std::vector<MapEntry> maps;
   size_t ws_bytes = 0;
@@ -644,6 +650,7 @@ void pbgk_ctx_destroy(pbgk_ctx* c) {
   cudaFree(c->d_keys);
   cudaFreeHost(c->h_keys);
   cudaFree(c->d_times);
+  cudaFree(c->d_times2);
   if (c->h_err) cudaFreeHost(c->h_err);
   if (c->h_dbl) cudaFreeHost(c->h_dbl);
   delete c;
@@ -1237,6 +1244,7 @@ int propagate_body_fused(pbgk_ctx* c, const double* f0, const double* mom0, doub
     return -1;
   double* T = c->d_bt;
   // (pageable source: the copy completes before the call returns)
+  c->sh_bdts.clear();
   CK(cudaMemcpyAsync(c->d_bdts, h_dts, (size_t)S * sizeof(double), cudaMemcpyHostToDevice, st));
   // f_0: the lift of mom0 (synthesised by the first pass), or the given f0
   // with identity tables (r = 1, ls = 0) and the recursion started from Q(f0)
@@ -1422,6 +1430,8 @@ int windows_fused(pbgk_ctx* c, int nwin, const double* mom_in, double* mom_out, 
   const double per_w = 8.0 * ((double)(Smax + 1) * tstep + 2.0 * qw + 12.0 * nx);
   const int G = std::max(1, std::min(nwin, (int)(budget / per_w)));
   const size_t t_ws = (size_t)(Smax + 1) * tstep;
+  if ((size_t)std::max(Smax, 1) * G > c->bdts_cap) c->sh_bdts.clear();  // reallocated below
+  if ((size_t)G > c->bnst_cap) c->sh_bnst.clear();
   if (ensure_dev(c->d_bt, c->bt_cap, (size_t)G * t_ws, st) ||
       ensure_dev(c->d_bq, c->bq_cap, (size_t)2 * G * qw, st) ||
       ensure_dev(c->d_bg, c->bg_cap, (size_t)G * 12 * nx, st) ||
@@ -1440,10 +1450,18 @@ int windows_fused(pbgk_ctx* c, int nwin, const double* mom_in, double* mom_out, 
       hn[k] = h_nsteps[w];
       for (int s = 0; s < Smax; ++s) hd[(size_t)s * g + k] = s < h_nsteps[w] ? h_dts[off[w] + s] : 0.0;
     }
-    // pageable sources: the copies complete before the calls return
-    CK(cudaMemcpyAsync(c->d_bnst, hn.data(), g * sizeof(int), cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(c->d_bdts, hd.data(), (size_t)std::max(Smax, 1) * g * sizeof(double),
-                       cudaMemcpyHostToDevice, st));
+    // pageable sources: the copies complete before the calls return; an
+    // unchanged group (every parareal iteration repeats the schedule) is not
+    // uploaded again
+    const size_t nd = (size_t)std::max(Smax, 1) * g;
+    if (!(c->sh_bnst.size() == (size_t)g && std::memcmp(c->sh_bnst.data(), hn.data(), g * sizeof(int)) == 0)) {
+      c->sh_bnst.assign(hn.begin(), hn.begin() + g);
+      CK(cudaMemcpyAsync(c->d_bnst, hn.data(), g * sizeof(int), cudaMemcpyHostToDevice, st));
+    }
+    if (!(c->sh_bdts.size() == nd && std::memcmp(c->sh_bdts.data(), hd.data(), nd * sizeof(double)) == 0)) {
+      c->sh_bdts.assign(hd.begin(), hd.begin() + nd);
+      CK(cudaMemcpyAsync(c->d_bdts, hd.data(), nd * sizeof(double), cudaMemcpyHostToDevice, st));
+    }
     // small grids: the group's windows as one batch per launch (equal step
     // counts; f of the batch in the context's own buffers)
     bool batched = LM > 0 && g >= 2 && g <= c->nsm && h_nsteps[w0] > 0 && !getenv("PBGK_NO_WBATCH") &&
@@ -1661,19 +1679,27 @@ int pbgk_propagate_windows(pbgk_ctx* c, int nwin, const double* mom_in, double* 
 }
 
 namespace {
-int upload_times(pbgk_ctx* c, const double* h, size_t n, cudaStream_t st) {
-  if (n > c->times_cap) {
-    if (c->d_times) {
+// slot 0: window times of the batched G; slot 1: coarse times of the correction
+int upload_times(pbgk_ctx* c, int slot, const double* h, size_t n, cudaStream_t st) {
+  double*& d = slot == 0 ? c->d_times : c->d_times2;
+  size_t& dcap = slot == 0 ? c->times_cap : c->times2_cap;
+  std::vector<double>& sh = slot == 0 ? c->sh_times : c->sh_times2;
+  if (n > dcap) {
+    if (d) {
       CK(cudaStreamSynchronize(st));
-      CK(cudaFree(c->d_times));
-      c->d_times = nullptr;
+      CK(cudaFree(d));
+      d = nullptr;
     }
+    sh.clear();
     size_t cap = 256;
     while (cap < n) cap *= 2;
-    CK(cudaMalloc(&c->d_times, cap * sizeof(double)));
-    c->times_cap = cap;
+    CK(cudaMalloc(&d, cap * sizeof(double)));
+    dcap = cap;
   }
-  CK(cudaMemcpyAsync(c->d_times, h, n * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (sh.size() == n && std::memcmp(sh.data(), h, n * sizeof(double)) == 0) return 0;
+  sh.assign(h, h + n);
+  // from the context's own copy: it outlives the call
+  CK(cudaMemcpyAsync(d, sh.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
   return 0;
 }
 }  // namespace
@@ -1691,7 +1717,7 @@ int pbgk_fluid_propagate(pbgk_ctx* c, int nwin, const double* mom_in, double* mo
     t[w] = h_t0[w];
     t[nwin + w] = h_t1[w];
   }
-  if (upload_times(c, t.data(), t.size(), st)) return -1;
+  if (upload_times(c, 0, t.data(), t.size(), st)) return -1;
   if (reset_err(c, st)) return -1;
   FluidArgs a{c->g.nx, c->dx, c->g.bc == 1 ? 1 : 0, dt_max, cfl, force, c->d_err, c->g_model,
               c->g_diff};
@@ -1707,14 +1733,14 @@ int pbgk_parareal_correct(pbgk_ctx* c, int n_g, int start, double* snaps, const 
   if (cudaSetDevice(c->dev) != cudaSuccess) return fail("cudaSetDevice");
   if (start < 1) return fail("pbgk_parareal_correct: start < 1");
   cudaStream_t st = (cudaStream_t)stream;
-  if (upload_times(c, h_times, (size_t)n_g + 1, st)) return -1;
+  if (upload_times(c, 1, h_times, (size_t)n_g + 1, st)) return -1;
   if (reset_err(c, st)) return -1;
   FluidArgs a{c->g.nx, c->dx, c->g.bc == 1 ? 1 : 0, dt_max, cfl, force, c->d_err, c->g_model,
               c->g_diff};
   double* d_e = c->d_scratch;
   CK(cudaMemsetAsync(d_e, 0, sizeof(double), st));
   if (start <= n_g) ++g_launches;
-  if (start <= n_g) CK(launch_correct(a, n_g, start, snaps, old, jumps, c->d_times, d_e, st));
+  if (start <= n_g) CK(launch_correct(a, n_g, start, snaps, old, jumps, c->d_times2, d_e, st));
   CK(cudaMemcpyAsync(c->h_dbl, d_e, sizeof(double), cudaMemcpyDeviceToHost, st));
   long long code = -1;
   if (fetch_err(c, st, &code)) return -1;

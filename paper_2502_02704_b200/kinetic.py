@@ -275,16 +275,28 @@ def propagate_windows(ctx, mom_in: torch.Tensor, spans, grid, params, dt_max,
     cap = stable_dt_kinetic(grid, params)
     if dt_max is not None:
         cap = min(cap, dt_max)
-    counts, dts = [], []
-    for span in spans:
-        d = fine_schedule(span, cap) if span > 0.0 else []
-        counts.append(len(d))
-        dts += [_kdt(x, params) for x in d]
     nwin = len(spans)
+    # the batch's schedules are the same in every parareal iteration: keep the
+    # marshalled arrays of the last few (spans, cap, scaling) on the context
+    key = (tuple(float(x) for x in spans), float(cap), float(params.epsilon), getattr(params, "alpha", 0))
+    cache = ctx.__dict__.setdefault("_schedule_cache", {})
+    hit = cache.get(key)
+    if hit is None:
+        counts, dts, per_span = [], [], {}
+        for span in key[0]:
+            d = per_span.get(span)
+            if d is None:
+                d = [_kdt(x, params) for x in fine_schedule(span, cap)] if span > 0.0 else []
+                per_span[span] = d
+            counts.append(len(d))
+            dts += d
+        hit = ((ctypes.c_int * max(nwin, 1))(*counts), (ctypes.c_double * max(len(dts), 1))(*dts))
+        if len(cache) >= 8:
+            cache.clear()
+        cache[key] = hit
+    c_counts, c_dts = hit
     _scheme(ctx, params)
     E, e_max = rt.to_device_field(params.force, ctx.device, ctx.nx)
-    c_counts = (ctypes.c_int * max(nwin, 1))(*counts)
-    c_dts = (ctypes.c_double * max(len(dts), 1))(*dts)
     codes = (ctypes.c_longlong * max(nwin, 1))()
     rt._lib.check(ctx.lib.pbgk_propagate_windows(
         ctx.h, nwin, rt.ptr(mom_in), rt.ptr(mom_out), rt.ptr(ctx.f_scratch(0)),

@@ -361,10 +361,9 @@ class ShardedRun:
         work = self.n_g - start + 1
         if self.world == 1:
             windows = list(range(start, self.n_g + 1))
-            out = self.b.empty(len(windows))
-            status = self.b.jumps(snaps, windows, out)
+            # the jumps land in place; a failing window raises before anything reads them
+            status = self.b.jumps(snaps, windows, jumps[start - 1:])
             _raise_window_status(status)
-            jumps[start - 1:] = out
             return
         dist = torch.distributed
         chunk = -(-work // self.world)  # ceil
