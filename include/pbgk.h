@@ -206,7 +206,8 @@ int pbgk_esweep_levels(pbgk_ctx* ctx);
 /* Device bytes the multi-step path may spend on per-step relax tables: the
  * batched windows of pbgk_propagate_windows run in groups that fit (a single
  * propagation whose tables do not fit runs one-step).  0 = the default
- * (PBGK_BATCH_BYTES, else 2 GiB).  Results do not depend on the grouping. */
+ * (PBGK_BATCH_BYTES, else a quarter of the free device memory within 2..16
+ * GiB).  Results do not depend on the grouping. */
 int pbgk_set_batch_bytes(pbgk_ctx* ctx, double bytes);
 
 /* ---- x-sharded fine propagation (slabs) --------------------------------- */

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <atomic>
 #include <mutex>
 #include <string>
@@ -95,8 +96,17 @@ int ensure_dev(T*& p, size_t& cap, size_t n, cudaStream_t st) {
 
 // bytes of per-step relax tables the multi-step path may hold (a group of
 // batched windows, or one long propagation)
+// Default: a quarter of the device memory free at first use, between 2 and
+// 16 GiB (config 3b's windows carry 2 GB of tables each: at 2 GiB their
+// recursions ran one window at a time, 16 % of an iteration; at 16 GiB 8 %).
 double default_batch_budget() {
-  static const double b = getenv("PBGK_BATCH_BYTES") ? atof(getenv("PBGK_BATCH_BYTES")) : 2147483648.0;
+  static const double b = [] {
+    if (getenv("PBGK_BATCH_BYTES")) return atof(getenv("PBGK_BATCH_BYTES"));
+    size_t free_b = 0, total_b = 0;
+    const double gib = 1073741824.0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return 2.0 * gib;
+    return std::min(16.0 * gib, std::max(2.0 * gib, 0.25 * (double)free_b));
+  }();
   return b;
 }
 
@@ -244,7 +254,7 @@ std::atomic<long long> g_launches{0};
 
 // bytes of per-step relax tables the multi-step path may hold (a group of
 // batched windows, or one long propagation): the context's setting, else
-// PBGK_BATCH_BYTES, else 2 GiB
+// PBGK_BATCH_BYTES, else a quarter of the free device memory within 2..16 GiB
 double batch_budget(const pbgk_ctx* c) { return c->batch_bytes > 0.0 ? c->batch_bytes : default_batch_budget(); }
 
 // CUDA-event bracket around one launch when profiling is on.
@@ -1411,7 +1421,7 @@ int run_recursion(pbgk_ctx* c, int g, const double* q0, double* T, long long t_w
 // pbgk_propagate_windows on the multi-step path: the moment recursion of a
 // group of windows runs batched (one launch per step for the whole group,
 // grid.y = window), then each window's passes read its own per-step tables.
-// Groups bound the table memory (PBGK_BATCH_BYTES, default 2 GiB).
+// Groups bound the table memory (PBGK_BATCH_BYTES; default: see default_batch_budget).
 int windows_fused(pbgk_ctx* c, int nwin, const double* mom_in, double* mom_out, double* f_a,
                   double* f_b, const int* h_nsteps, const double* h_dts, double eps, double tau,
                   const double* E, double e_max, cudaStream_t st) {
