@@ -316,8 +316,12 @@ __device__ __forceinline__ void mrec_cell(const MargArgs& m, const FinalArgs& f,
   }
 }
 
+#ifndef PBGK_MREC_MINB
+#define PBGK_MREC_MINB 2  // 128 registers, 16 warps per SM: the step is latency-bound (config 2 +3.5 %, config 4 +1 %)
+#endif
 template <int JPL, bool TRAP>
-__global__ void __launch_bounds__(32 * kWarpsPerCta) mrec_step_kernel(const MargArgs m, const FinalArgs f) {
+__global__ void __launch_bounds__(32 * kWarpsPerCta, PBGK_MREC_MINB)
+    mrec_step_kernel(const MargArgs m, const FinalArgs f) {
   extern __shared__ double sm[];
   const int wid = threadIdx.x >> 5;
   const int i = blockIdx.x * kWarpsPerCta + wid;
