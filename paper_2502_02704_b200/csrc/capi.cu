@@ -1188,11 +1188,12 @@ int run_esweep(pbgk_ctx* c, int n, const double* in, double* out, const double* 
   return 0;
 }
 
-// P(f_S) from the partial records of a FINAL field-term pass
-int es_project(pbgk_ctx* c, double* mom_out, int step, cudaStream_t st) {
+// P(f_S) from the partial records (of f*_S) of a FINAL field-term pass
+int es_project(pbgk_ctx* c, double* mom_out, const double* tabR, int step, cudaStream_t st) {
   FinalArgs f = fin_args(c, c->plan[0]);
   esweep_tiling(c->g.nvx, c->g.nvy, c->g.nvz, &f.t);
   f.part = c->d_mpart;
+  f.relax_tab = tabR;  // the records are those of f*_S
   f.mode = kFinProject;
   f.mom_out = mom_out;
   f.step = step;
@@ -1317,7 +1318,7 @@ int propagate_body_fused(pbgk_ctx* c, const double* f0, const double* mom0, doub
       if (field && LE > 0 && s0 + n == S && !write_final && mom_out && es_final_ok(c)) {
         // the window's last pass: R_S and the projection folded in (no f_S)
         rc = run_esweep(c, n, in, nullptr, tabs, h_dts + s0, E, e_max, s0 + 1, st, T + (size_t)S * tstep);
-        if (rc == 0) rc = es_project(c, mom_out, S + 1, st);
+        if (rc == 0) rc = es_project(c, mom_out, T + (size_t)S * tstep, S + 1, st);
         projected = true;
         break;
       }
@@ -1541,7 +1542,7 @@ int windows_fused(pbgk_ctx* c, int nwin, const double* mom_in, double* mom_out, 
           // the window's last pass: R_S and the projection folded in (no f_S)
           int rcf = run_esweep(c, n, in, nullptr, tabs, h_dts + off[w] + s0, E, e_max, s0 + 1, st,
                                T + (size_t)S * tstep);
-          if (rcf == 0) rcf = es_project(c, mom_out + w * m5, S + 1, st);
+          if (rcf == 0) rcf = es_project(c, mom_out + w * m5, T + (size_t)S * tstep, S + 1, st);
           if (rcf) { c->err_slot = nullptr; return -1; }
           projected = true;
           break;

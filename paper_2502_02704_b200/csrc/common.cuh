@@ -155,11 +155,11 @@ struct ESweepArgs {
   int nseg, seglen;    // x segments per column and their length (planes)
   ErrKey* err;
   int step0;
-  // FINAL (the window's last pass, tabR non-null): R_S (tabR) applied to the
-  // last level's output and, instead of the store, the partial records
-  // [m_x rows | m_y | m_z of the column's 8 v_z] of every (plane, warp column)
-  // written to part (stride PS doubles, NT = ncol records per plane) for
-  // finalize.cu (kFinProject)
+  // FINAL (the window's last pass, tabR non-null): instead of the store, the
+  // partial records [m_x rows | m_y | m_z of the column's 8 v_z] of the last
+  // level's output f*_S for every (plane, warp column), written to part
+  // (stride PS doubles, NT = ncol records per plane) for finalize.cu
+  // (kFinProject with relax_tab = tabR: R_S applied to the marginals)
   const double* tabR;
   double* part;
   int PS;

@@ -35,12 +35,13 @@
 //     pipeline of D positions.
 //   * SYNTH (the window's first pass from moments): level 0 input is the lift
 //     f_0 = ls g_x g_y g_z of tab[0] (ref/lifting.py:47-57), no f read.
-//   * FINAL (the window's last pass): R_S (ref/kinetic.py:130-134) applied to
-//     the last level's output and the column's marginal partial record
-//     [m_x rows | m_y | m_z] written per plane for finalize.cu (kFinProject,
-//     the projection P(f_S) of ref/moments.py:60-112) instead of f_S: no
-//     store and no read-back of f_S.  Fixed trees, the same for every entry
-//     and its mirror (even data keeps an exactly zero folded first moment).
+//   * FINAL (the window's last pass): the column's marginal partial record
+//     [m_x rows | m_y | m_z] of the last level's output f*_S written per
+//     plane for finalize.cu (kFinProject, the projection P(f_S) of
+//     ref/moments.py:60-112; it applies the linear, separable R_S of
+//     ref/kinetic.py:130-134 to the marginals) instead of f_S: no store and
+//     no read-back of f_S.  Fixed trees, the same for every entry and its
+//     mirror (even data keeps an exactly zero folded first moment).
 //
 // Ghost planes (bc 0 absorbing: 0; bc 2 outflow: the edge plane of the same
 // level) are substituted where level l's neighbour plane falls outside the
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(es::NTHR, 2)
   constexpr int H = V / 2;    // rows of each c_x sign per lane
   constexpr int SL = slice(V);
   constexpr int NX8 = 8 * V;  // nvx
-  constexpr int NS = L + (FINAL ? 1 : 0);  // table slices per stage (FINAL: R_S after the levels)
+  constexpr int NS = L;  // table slices per stage
   constexpr uint32_t STB = (uint32_t)stage_bytes(V, NS);
   constexpr uint32_t FB = 32u * V * 16u;  // f area of a stage
   extern __shared__ __align__(128) unsigned char smem[];
@@ -201,12 +202,11 @@ __global__ void __launch_bounds__(es::NTHR, 2)
       const int so = soff0 + (rz ? it.z0 : (ry ? it.y : 0));
 #pragma unroll
       for (int l = 0; l < NS; ++l) {
-        if (l >= n + (FINAL ? 1 : 0)) break;
+        if (l >= n) break;
         int q = q0 - l;
         if (periodic && q < 0) q += nx;
         const bool on = q >= 0 && q < nx;
-        const double* tb = (FINAL && l == n) ? a.tabR : a.tab[l < L ? l : 0];  // slot n: R_S of plane p - n
-        const double* src = rE ? a.E + q : tb + ((long long)q * a.TL + so);
+        const double* src = rE ? a.E + q : a.tab[l] + ((long long)q * a.TL + so);
         const uint32_t dst = S + FB + (uint32_t)(l * SL + doff) * 8u;
         cp_async_16_if(dst, src, on && r16);
         cp_async_8_if(dst, src, on && r8);
@@ -403,49 +403,67 @@ __global__ void __launch_bounds__(es::NTHR, 2)
     const int qo = p - n;
     if (qo >= it.x0 && qo < it.x1) {
       if constexpr (FINAL) {
-        // f_S = R_S(f*_S) of plane qo (slice n of the stage), then the
-        // column's partial record.  Trees: a row total = the lane's two v_z,
-        // then a butterfly over the 4 v_z pairs; an m_z entry = the lane's
-        // rows in order, then a butterfly over the 8 row groups; m_y = the
-        // lane's row totals in order, then the butterfly over the row groups.
-        const double* T = ST + n * SL;
-        const double2 rl = *reinterpret_cast<const double2*>(T);
-        const double2 ge = *reinterpret_cast<const double2*>(T + NX8 + 2);
-        const double2 gz = *reinterpret_cast<const double2*>(T + NX8 + 4 + 2 * c);
-        const double rlg = (rl.x * rl.y) * ge.x;
+        // the column's partial record of plane qo of f*_S (finalize applies R_S
+        // to the marginals: FinalArgs relax_tab).  Two or four values are
+        // reduced per shuffle round -- a lane keeps some and sends the others,
+        // the partner keeps those -- so every total is the tree of a plain
+        // butterfly: a row total = the lane's two v_z, then the 4 v_z pairs;
+        // an m_z entry = the lane's rows in order, then the 8 row groups;
+        // m_y = the kept row totals over all lanes.
+        static_assert(V == 2 || V == 4 || V == 6, "row totals per lane");
         double t[V], zs[2] = {0.0, 0.0};
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-          const double w = rlg * T[2 + (v < H ? rd0 + v : ru0 + (v - H))];
-          const double y0 = fma(w, gz.x, rl.x * x[v][0]);
-          const double y1 = fma(w, gz.y, rl.x * x[v][1]);
-          t[v] = y0 + y1;
-          zs[0] = v == 0 ? y0 : zs[0] + y0;
-          zs[1] = v == 0 ? y1 : zs[1] + y1;
+          t[v] = x[v][0] + x[v][1];
+          zs[0] = v == 0 ? x[v][0] : zs[0] + x[v][0];
+          zs[1] = v == 0 ? x[v][1] : zs[1] + x[v][1];
         }
+        // row totals over c (lanes xor 1, xor 2): V values -> V / 2 -> ...
+        const bool c0 = c & 1, c1 = (c >> 1) & 1;
+        constexpr int V2 = V / 2;
+        double u[V2];
 #pragma unroll
-        for (int m = 1; m <= 2; m <<= 1)
-#pragma unroll
-          for (int v = 0; v < V; ++v) t[v] += __shfl_xor_sync(0xffffffffu, t[v], m);
-        double tot = t[0];
-#pragma unroll
-        for (int v = 1; v < V; ++v) tot += t[v];
-#pragma unroll
-        for (int m = 4; m <= 16; m <<= 1) {
-          tot += __shfl_xor_sync(0xffffffffu, tot, m);
-          zs[0] += __shfl_xor_sync(0xffffffffu, zs[0], m);
-          zs[1] += __shfl_xor_sync(0xffffffffu, zs[1], m);
+        for (int v = 0; v < V2; ++v) {
+          const double keep = c0 ? t[V2 + v] : t[v];
+          const double send = c0 ? t[v] : t[V2 + v];
+          u[v] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
         }
+        // u[v] = rows (c0 ? V2 + v : v) summed over the pair (c, c ^ 1)
+        double rowt;       // one finished row total per lane (V == 6: two on c1 == 0 lanes, one on the others)
+        double rowt2 = 0.0;
+        int rv, rv2 = -1;  // its row slot v
+        if constexpr (V2 == 1) {
+          rowt = u[0] + __shfl_xor_sync(0xffffffffu, u[0], 2);
+          rv = c0 ? 1 : 0;
+        } else if constexpr (V2 == 2) {
+          const double keep = c1 ? u[1] : u[0];
+          const double send = c1 ? u[0] : u[1];
+          rowt = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+          rv = (c0 ? V2 : 0) + (c1 ? 1 : 0);
+        } else {
+          // three values over two lanes: slot 0 / 1 exchanged, slot 2 a butterfly
+          const double keep = c1 ? u[1] : u[0];
+          const double send = c1 ? u[0] : u[1];
+          rowt = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+          rv = (c0 ? V2 : 0) + (c1 ? 1 : 0);
+          rowt2 = u[2] + __shfl_xor_sync(0xffffffffu, u[2], 2);
+          rv2 = c1 ? -1 : (c0 ? V2 : 0) + 2;
+        }
+        // m_z over the row groups s (lanes xor 4, 8, 16)
+        const bool s0b = s & 1;
+        double zt = (s0b ? zs[1] : zs[0]) + __shfl_xor_sync(0xffffffffu, s0b ? zs[0] : zs[1], 4);
+        zt += __shfl_xor_sync(0xffffffffu, zt, 8);
+        zt += __shfl_xor_sync(0xffffffffu, zt, 16);
+        // m_y: every finished row total once (rowt2 only where it is kept)
+        // (V == 2: both c1 lanes hold the same row total, one of them counts)
+        double tot = ((V2 == 1 && c1) ? 0.0 : rowt) + ((V2 == 3 && !c1) ? rowt2 : 0.0);
+#pragma unroll
+        for (int m = 1; m <= 16; m <<= 1) tot += __shfl_xor_sync(0xffffffffu, tot, m);
         acc += tot;
         double* R = a.part + ((long long)qo * a.ncol + it.col) * a.PS;
-        if (c == 0) {
-#pragma unroll
-          for (int v = 0; v < V; ++v) R[v < H ? rd0 + v : ru0 + (v - H)] = t[v];
-        }
-        if (s == 0) {
-          R[NX8 + 1 + 2 * c] = zs[0];
-          R[NX8 + 2 + 2 * c] = zs[1];
-        }
+        R[rv < H ? rd0 + rv : ru0 + (rv - H)] = rowt;
+        if (V2 == 3 && rv2 >= 0) R[rv2 < H ? rd0 + rv2 : ru0 + (rv2 - H)] = rowt2;
+        if (s < 2) R[NX8 + 1 + 2 * c + s] = zt;
         if (lane == 0) R[NX8] = tot;
       } else {
         double* dst = a.fout + ((long long)qo * plane + lane_f + it.foff);
@@ -531,9 +549,10 @@ int esweep_levels(int nvx, int nvz) {
 constexpr int kEsD = PBGK_ES_D;  // ring stages per warp
 
 size_t esweep_smem_bytes(int nvx, bool fin) {
+  (void)fin;  // (the FINAL pass loads the same slices)
   const int V = nvx / 8;
   const int L = esweep_levels(nvx, 8);
-  return (size_t)es::NW * kEsD * es::stage_bytes(V, L + (fin ? 1 : 0));
+  return (size_t)es::NW * kEsD * es::stage_bytes(V, L);
 }
 
 // the tiling of the FINAL pass's partial records for finalize.cu: one tile per
