@@ -117,19 +117,55 @@ __device__ __forceinline__ void named_sync(int id) {
 
 // NG = 2: two warp groups split the levels (16 warps, one CTA per SM);
 // NG = 1: one group runs every level (8 warps, two CTAs per SM)
+#ifndef PBGK_MS_LW
+#define PBGK_MS_LW 1
+#endif
+// LW (two groups only): a 17th warp issues every load (the TMA boxes and the
+// table chunks), so group 0 runs nothing but its levels; all warps then fit
+// 120 registers (65536 / 544 threads) with the levels split 4 + 4
+constexpr bool kMsLW = PBGK_MS_LW && PBGK_MS_NG == 2;
+constexpr int kMsLoaders = 128;  // a whole warpgroup, so that it can hand its registers to the others
+constexpr int kMsThreads = PBGK_MS_NG * ms::NTG + (kMsLW ? kMsLoaders : 0);
+// Registers after the role split.  The kernel starts at 96 per thread (640
+// threads); what the compute groups gain must come out of what the loader
+// warpgroup releases (the CTA's pool holds only released registers -- asking
+// for more never returns): 128 x (96 - 32) = 8192 >= 256 x (R0 - 96) + 256 x
+// (R1 - 96).
+#ifndef PBGK_MS_R0
+#define PBGK_MS_R0 104
+#endif
+#ifndef PBGK_MS_R1
+#define PBGK_MS_R1 120
+#endif
+#ifndef PBGK_MS_RL
+#define PBGK_MS_RL 32
+#endif
+static_assert(128 * (96 - PBGK_MS_RL) >= 256 * (PBGK_MS_R0 - 96) + 256 * (PBGK_MS_R1 - 96), "register pool");
+template <int N>
+__device__ __forceinline__ void reg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <int N>
+__device__ __forceinline__ void reg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+
 template <int L, int MODE, int P, int NG>
-__global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
+__global__ void __launch_bounds__(kMsThreads, NG == 1 ? 2 : 1)
     msweep_kernel(const __grid_constant__ CUtensorMap fmap, const MSweepArgs a, int ns) {
   using namespace ms;
   constexpr bool SYNTH = (MODE & kMsSynth) != 0;
   constexpr bool FINAL = (MODE & kMsFinal) != 0;
+  constexpr bool LW = kMsLW && NG == 2;
+  constexpr int NLD = LW ? kMsLoaders : NTG;  // loader threads
 #ifndef PBGK_MS_LA
 #define PBGK_MS_LA 0
 #endif
   // levels [0, LA) run in group 0 (which also issues the loads), [LA, L) in
   // group 1; LH = the larger share (carry registers)
-  // (measured on config 4, 8 levels: 3 + 5 is 6 % faster than 4 + 4 -- group 0
-  // also walks the loader; 2 + 6 spills)
+  // (measured on config 4, 8 levels: with the loads in group 0, 3 + 5 is 6 %
+  // faster than 4 + 4 -- group 0 also walks the loader; 2 + 6 spills.  With
+  // the loader warpgroup 4 + 4 is 1.5 % faster than 3 + 5)
 #ifndef PBGK_MS_LAF
 #define PBGK_MS_LAF 4
 #endif
@@ -137,9 +173,9 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
   // takes one level fewer (4 + 4)
   constexpr int LA = NG == 1 ? L
                              : (PBGK_MS_LA > 0 && PBGK_MS_LA < L ? PBGK_MS_LA
-                                                                 : (L == 8 ? (FINAL ? PBGK_MS_LAF : 3) : L / 2));
+                                                                 : (L == 8 ? ((FINAL || LW) ? PBGK_MS_LAF : 3) : L / 2));
   constexpr int LH = LA > L - LA ? LA : L - LA;
-  constexpr int NTHR_K = NG * NTG;
+  constexpr int NTHR_K = NG * NTG + (LW ? kMsLoaders : 0);
   constexpr int NTAB = L + (FINAL ? 1 : 0);
   constexpr uint32_t BOXB = (uint32_t)(A * BY * BZ * 8);
   // the group hand-off area of a plane: after its box and tables, not in the
@@ -152,7 +188,7 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
   constexpr int RS = 1 + BY + BZ;             // per-warp partial block (FINAL)
   constexpr int FR = 8;                       // FINAL records reduced per barrier
   constexpr int NCH = (2 + A + BY + BZ) / 2;  // 16-byte chunks of one table slice
-  constexpr int CPT = (P * NTAB * NCH + NTG - 1) / NTG;  // chunks per loader thread
+  constexpr int CPT = (P * NTAB * NCH + NLD - 1) / NLD;  // chunks per loader thread
   extern __shared__ __align__(128) unsigned char smem[];
 
   const Tiling& T = a.t;
@@ -189,7 +225,7 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
   }
   if (tid == 0) {
     for (int s = 0; s < ns; ++s) {
-      mbar_init(&full[s], 1 + NTG);  // the boxes' expect-tx arrive + one cp.async arrive per loader
+      mbar_init(&full[s], 1 + NLD);  // the boxes' expect-tx arrive + one cp.async arrive per loader
       mbar_init(&mid[s], NW);
       mbar_init(&empty[s], NW);
     }
@@ -199,8 +235,11 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
   pdl_trigger();
   __syncthreads();
 
-  const int grp = tid / NTG;        // 0: loads + levels [0, LH); 1: levels [LH, L) + output
+  const int grp = tid / NTG;        // 0: (loads +) levels [0, LA); 1: levels [LA, L) + output; 2: the loader warp (LW)
   const int gt = tid - grp * NTG;
+  const bool loader = LW ? grp == 2 : grp == 0;
+  const int lid = gt;               // loader thread index (LW: within the loader warpgroup)
+
   const int w = gt >> 5;            // box row
   const int lane = tid & 31;
   const int yp = lane >> 3;         // lines y = 2 yp, 2 yp + 1
@@ -419,8 +458,8 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
     }
   };
 
-  if (grp == 0) {
-    // ---------------- group 0: loads, levels [0, LH) ----------------
+  if (grp == 0 || (LW && grp == 2)) {
+    // ---------------- group 0: loads (or the loader warp's), levels [0, LA) ----------------
     // this thread's table chunks of an item: (plane, level, slice) fixed for
     // the launch; source pointer with the run's tile offset set per run, the
     // plane row added per item
@@ -429,7 +468,7 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
     auto decode = [&](const TileGeom& tg) {
 #pragma unroll
       for (int r = 0; r < CPT; ++r) {
-        const int j = gt + r * NTG;
+        const int j = lid + r * NLD;
         // (the R_S slice is loaded only when f_S is stored)
         const bool ok = j < P * NTAB * NCH && !(FINAL && fout == nullptr && (j % (NTAB * NCH)) / NCH == L);
         const int pl = ok ? j / (NTAB * NCH) : 0;
@@ -496,7 +535,7 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
       // the stage's previous item must be released by group 1
       mbar_wait(&empty[s], pph ^ 1u);
       unsigned char* st = smem + (size_t)s * STAGEB;
-      if (gt == 0) {
+      if (lid == 0) {
         uint32_t bytes = 0;
 #pragma unroll
         for (int pl = 0; pl < P; ++pl)
@@ -537,11 +576,11 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
         pph ^= 1u;
       }
     };
-    if (gt == 0) prefetch_tensormap(&fmap);
-    if (a.prog != nullptr) {
+    if (lid == 0 && loader) prefetch_tensormap(&fmap);
+    if (a.prog != nullptr && loader) {
       // the recursion runs concurrently on other SMs: wait for this pass's
       // tables (bounded: a stalled recursion becomes status kind 5)
-      if (gt == 0) {
+      if (lid == 0) {
         long long spins = 0;
         while (ld_acquire_gpu(a.prog) < a.need) {
           __nanosleep(256);
@@ -552,9 +591,20 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
         }
         fence_proxy_async();
       }
-      named_sync<NTG>(2);
+      if (LW) named_sync<kMsLoaders>(2);
+      else named_sync<NTG>(2);
     }
-    for (int q = 0; q < dist; ++q) issue_next();
+    if (LW && grp == 2) {
+      // the loader warpgroup: every item's loads, as far ahead as the ring
+      // allows; its registers go to the compute groups
+      reg_dec<PBGK_MS_RL>();
+      while (lmore) issue_next();
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      return;
+    }
+    if constexpr (LW && PBGK_MS_R0 > 96) reg_inc<PBGK_MS_R0>();
+    if (!LW)
+      for (int q = 0; q < dist; ++q) issue_next();
     walk([&](const TileGeom& tg, int t, int p0, int u0, int n, auto fullc) {
       constexpr bool FULLC = decltype(fullc)::value;
       mbar_wait(&full[stg], ph);
@@ -598,7 +648,7 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
         stg = 0;
         ph ^= 1u;
       }
-      issue_next();
+      if (!LW) issue_next();
     });
     if (NG == 1 && FINAL && nfin % FR) flush((nfin / FR) & 1, nfin % FR);
     if (NG == 1 && !isfinite(acc)) atomicMin(errp, err_key(0, a.step0, kErrNonFiniteMulti));
@@ -606,6 +656,7 @@ __global__ void __launch_bounds__(NG * ms::NTG, NG == 1 ? 2 : 1)
   }
 
   // ---------------- group 1: levels [LH, L), output ----------------
+  if constexpr (LW) reg_inc<PBGK_MS_R1>();
   walk([&](const TileGeom& tg, int t, int p0, int u0, int n, auto fullc) {
     constexpr bool FULLC = decltype(fullc)::value;
     mbar_wait(&mid[stg], ph);
@@ -655,7 +706,7 @@ size_t msweep_smem_bytes(int L, int mode, int nvx, int ns) {
          (fin ? 2 * 8 * ms::NW * (1 + ms::BY + ms::BZ) * 8 + 2 * 8 * 8 : 0) + (size_t)3 * ns * 8;
 }
 
-int msweep_threads() { return PBGK_MS_NG * ms::NTG; }
+int msweep_threads() { return kMsThreads; }
 
 // CTAs per SM the pass kernel is built for
 int msweep_ctas_per_sm() { return PBGK_MS_NG == 1 ? 2 : 1; }
@@ -685,10 +736,10 @@ static cudaError_t launch_ms(const CUtensorMap& map, const MSweepArgs& a, dim3 g
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (a.prog != nullptr) {
-    fn<<<grid, PBGK_MS_NG * ms::NTG, smem, st>>>(map, a, ns);
+    fn<<<grid, kMsThreads, smem, st>>>(map, a, ns);
     return cudaGetLastError();
   }
-  return launch_pdl_grid(fn, grid, PBGK_MS_NG * ms::NTG, smem, st, map, a, ns);
+  return launch_pdl_grid(fn, grid, kMsThreads, smem, st, map, a, ns);
 }
 
 template <int L>
