@@ -120,9 +120,9 @@ __device__ __forceinline__ void named_sync(int id) {
 #ifndef PBGK_MS_LW
 #define PBGK_MS_LW 1
 #endif
-// LW (two groups only): a 17th warp issues every load (the TMA boxes and the
-// table chunks), so group 0 runs nothing but its levels; all warps then fit
-// 120 registers (65536 / 544 threads) with the levels split 4 + 4
+// LW (two groups only): a loader warpgroup (warps 16-19) issues every load
+// (the TMA boxes and the table chunks), so group 0 runs nothing but its
+// levels, and hands most of its registers to the compute groups (setmaxnreg)
 constexpr bool kMsLW = PBGK_MS_LW && PBGK_MS_NG == 2;
 constexpr int kMsLoaders = 128;  // a whole warpgroup, so that it can hand its registers to the others
 constexpr int kMsThreads = PBGK_MS_NG * ms::NTG + (kMsLW ? kMsLoaders : 0);
@@ -132,15 +132,23 @@ constexpr int kMsThreads = PBGK_MS_NG * ms::NTG + (kMsLW ? kMsLoaders : 0);
 // for more never returns): 128 x (96 - 32) = 8192 >= 256 x (R0 - 96) + 256 x
 // (R1 - 96).
 #ifndef PBGK_MS_R0
-#define PBGK_MS_R0 104
+#define PBGK_MS_R0 120
 #endif
 #ifndef PBGK_MS_R1
-#define PBGK_MS_R1 120
+#define PBGK_MS_R1 104
 #endif
 #ifndef PBGK_MS_RL
 #define PBGK_MS_RL 32
 #endif
 static_assert(128 * (96 - PBGK_MS_RL) >= 256 * (PBGK_MS_R0 - 96) + 256 * (PBGK_MS_R1 - 96), "register pool");
+// the FINAL pass (group 1 also reduces the partial records) may split differently
+#ifndef PBGK_MS_R0F
+#define PBGK_MS_R0F PBGK_MS_R0
+#endif
+#ifndef PBGK_MS_R1F
+#define PBGK_MS_R1F PBGK_MS_R1
+#endif
+static_assert(128 * (96 - PBGK_MS_RL) >= 256 * (PBGK_MS_R0F - 96) + 256 * (PBGK_MS_R1F - 96), "register pool");
 template <int N>
 __device__ __forceinline__ void reg_inc() {
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
@@ -165,7 +173,9 @@ __global__ void __launch_bounds__(kMsThreads, NG == 1 ? 2 : 1)
   // group 1; LH = the larger share (carry registers)
   // (measured on config 4, 8 levels: with the loads in group 0, 3 + 5 is 6 %
   // faster than 4 + 4 -- group 0 also walks the loader; 2 + 6 spills.  With
-  // the loader warpgroup 4 + 4 is 1.5 % faster than 3 + 5)
+  // the loader warpgroup group 1 -- the output, the finiteness sums, FINAL's
+  // reductions -- is the heavier one: a config 4 window's passes take 8.79 ms
+  // at 3 + 5, 8.67 at 4 + 4, 8.30 at 5 + 3, 8.84 at 6 + 2)
 #ifndef PBGK_MS_LAF
 #define PBGK_MS_LAF 4
 #endif
@@ -173,7 +183,7 @@ __global__ void __launch_bounds__(kMsThreads, NG == 1 ? 2 : 1)
   // takes one level fewer (4 + 4)
   constexpr int LA = NG == 1 ? L
                              : (PBGK_MS_LA > 0 && PBGK_MS_LA < L ? PBGK_MS_LA
-                                                                 : (L == 8 ? ((FINAL || LW) ? PBGK_MS_LAF : 3) : L / 2));
+                                                                 : (L == 8 ? (LW ? 5 : (FINAL ? PBGK_MS_LAF : 3)) : L / 2));
   constexpr int LH = LA > L - LA ? LA : L - LA;
   constexpr int NTHR_K = NG * NTG + (LW ? kMsLoaders : 0);
   constexpr int NTAB = L + (FINAL ? 1 : 0);
@@ -602,7 +612,7 @@ __global__ void __launch_bounds__(kMsThreads, NG == 1 ? 2 : 1)
       asm volatile("cp.async.wait_all;" ::: "memory");
       return;
     }
-    if constexpr (LW && PBGK_MS_R0 > 96) reg_inc<PBGK_MS_R0>();
+    if constexpr (LW && (FINAL ? PBGK_MS_R0F : PBGK_MS_R0) > 96) reg_inc<(FINAL ? PBGK_MS_R0F : PBGK_MS_R0)>();
     if (!LW)
       for (int q = 0; q < dist; ++q) issue_next();
     walk([&](const TileGeom& tg, int t, int p0, int u0, int n, auto fullc) {
@@ -656,7 +666,7 @@ __global__ void __launch_bounds__(kMsThreads, NG == 1 ? 2 : 1)
   }
 
   // ---------------- group 1: levels [LH, L), output ----------------
-  if constexpr (LW) reg_inc<PBGK_MS_R1>();
+  if constexpr (LW && (FINAL ? PBGK_MS_R1F : PBGK_MS_R1) > 96) reg_inc<(FINAL ? PBGK_MS_R1F : PBGK_MS_R1)>();
   walk([&](const TileGeom& tg, int t, int p0, int u0, int n, auto fullc) {
     constexpr bool FULLC = decltype(fullc)::value;
     mbar_wait(&mid[stg], ph);
