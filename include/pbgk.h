@@ -181,8 +181,9 @@ int pbgk_set_x_scheme(pbgk_ctx* ctx, int scheme);
 int pbgk_set_fusion(pbgk_ctx* ctx, int levels);
 
 /* Round-2 pass kernel of the multi-step path (msweep.cu, default on): up to
- * 8 fine steps per pass over f, warp-specialised (one warp issues the TMA box
- * and the table-row slices), 3 fp64 instructions per element and level, and
+ * 8 fine steps per pass over f, warp-specialised (a loader warpgroup issues
+ * the TMA boxes and the table-row slices and hands its registers to the two
+ * compute groups), 3 fp64 instructions per element and level, and
  * the window's final relax + projection folded into its last pass (partial
  * records of P(f_S), no store of f_S unless the caller wants it).  Needs
  * v_x / v_y / v_z counts divisible by 16 / 8 / 16 (else the round-1 kernel
