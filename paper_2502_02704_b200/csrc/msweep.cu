@@ -13,11 +13,12 @@
 //     8-byte shared load whose warp-wide footprint is <= 128 B (one data-pipe
 //     cycle; measured with tools/ubench/lds_bench.cu: a 16-byte load whose
 //     lanes differ inside a quarter warp costs four).
-//   * two warp groups split the levels: group 0 runs levels [0, L/2) of plane
-//     p and hands its output to group 1 through the stage's box area (each
-//     thread rewrites exactly the elements it read), group 1 runs levels
-//     [L/2, L) of plane p while group 0 moves on to plane p+1.  16 warps per
-//     SM, half the carries per thread, half the dependent chain per item.
+//   * two warp groups split the levels: group 0 runs levels [0, LA) of plane
+//     p and hands its output to group 1 through a hand-off area of the stage,
+//     group 1 runs levels [LA, L) of plane p, the output and the reductions
+//     while group 0 moves on to plane p+1 (LA = 5 of 8).  A third warpgroup
+//     only issues the loads and hands its registers to the other two
+//     (setmaxnreg: 32 / 120 / 104 registers from a 96-register start).
 //   * relax + transport of level l, per element (ref/kinetic.py:110-112,
 //     130-134):  z = x + (ls gxa gy) gz,  out = (keep r) z + q_prev,
 //     q = (a r) z,  with a = (dt/dx)|c_x| and keep = 1 - a: the reference's
@@ -25,8 +26,8 @@
 //     few ulps; the multi-step path is held to the oracle at 1e-12).  a per
 //     (v_x row, level) sits in a shared table computed once per launch;
 //     a r and keep r = r - a r per warp and level.
-//   * loads: thread 0 of group 0 issues the TMA box of a plane, every group-0
-//     thread one 16-byte cp.async chunk of the table-row slices the tile needs
+//   * loads: loader thread 0 issues the TMA box of a plane, the loader
+//     threads the 16-byte cp.async chunks of the table-row slices the tile needs
 //     (r, ls | gxa of its rows | gy | gz per level: 0.3 KB instead of whole
 //     rows); full / mid / empty mbarriers per ring stage, no CTA barrier on
 //     the steady path.
