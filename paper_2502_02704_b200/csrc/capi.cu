@@ -33,7 +33,10 @@ int fsweep_ctas_per_sm(int L);
 cudaError_t launch_msweep(int L, int mode, const CUtensorMap& map, const MSweepArgs& a, int grid_x, int nwin,
                           int ns, size_t smem, cudaStream_t st);
 cudaError_t launch_finalize_batch(const FinalArgs& a, const FinalBatch& b, int nwin, cudaStream_t st);
-size_t msweep_smem_bytes(int L, int mode, int nvx, int ns);
+size_t msweep_smem_bytes(int L, int mode, int nvx, int ns, bool pre);
+cudaError_t launch_ms_prep(const double* T, long long t_ws, long long tstep, int TL, int gxo, const double* cx,
+                           const double* dts, int dts_g, double dx, int S, int nx, int nvx, int lift0,
+                           double* trip, long long trip_ws, int nwin, cudaStream_t st);
 int msweep_ctas_per_sm();
 int msweep_tiling(int nvx, int nvy, int nvz, Tiling* t);
 int esweep_levels(int nvx, int nvz);
@@ -242,6 +245,8 @@ struct pbgk_ctx {
   size_t fb_cap[2] = {0, 0};
   double* d_mpart = nullptr;
   size_t mpart_cap = 0;
+  double* d_trip = nullptr;  // per-row factors of a window's steps (ms_prep_kernel)
+  size_t trip_cap = 0;
   // multi-step passes with the v_x field term (esweep.cu): on/off
   // (pbgk_set_esweep), CTAs per SM of its build for this nvx (0: unknown yet)
   int es = 1;
@@ -650,6 +655,7 @@ void pbgk_ctx_destroy(pbgk_ctx* c) {
   cudaFree(c->d_gbar);
   cudaFree(c->d_prog);
   cudaFree(c->d_mpart);
+  cudaFree(c->d_trip);
   cudaFree(c->d_fb[0]);
   cudaFree(c->d_fb[1]);
   if (c->ev_start) cudaEventDestroy(c->ev_start);
@@ -953,10 +959,14 @@ struct MsBatch {
 
 int run_msweep(pbgk_ctx* c, int L, const double* in, double* out, const double* const* tabs,
                const double* tabR, const double* dtdx, int n, int step0, cudaStream_t st,
-               const unsigned* prog = nullptr, unsigned need = 0, const MsBatch* mb = nullptr) {
+               const unsigned* prog = nullptr, unsigned need = 0, const MsBatch* mb = nullptr,
+               const double* trip = nullptr, long long trip_ws = 0) {
   const Tiling& t = c->ms_t;
   const int nwin = mb ? mb->nwin : 1;
   MSweepArgs a{};
+  a.trip = trip;
+  a.trip_ls = (long long)c->g.nx * c->g.nvx * 4;
+  a.trip_ws = trip_ws;
   a.nx = c->g.nx;
   a.nvx = c->g.nvx;
   a.nvy = c->g.nvy;
@@ -1002,8 +1012,8 @@ int run_msweep(pbgk_ctx* c, int L, const double* in, double* out, const double* 
   const int per_sm = msweep_ctas_per_sm();
   const size_t budget = per_sm == 1 ? c->smem_optin : c->smem_per_sm / per_sm - 1024;
   int ns = ns_env > 0 ? ns_env : 12;
-  while (ns > 3 && msweep_smem_bytes(L, mode, c->g.nvx, ns) > budget) --ns;
-  const size_t smem = msweep_smem_bytes(L, mode, c->g.nvx, ns);
+  while (ns > 3 && msweep_smem_bytes(L, mode, c->g.nvx, ns, trip != nullptr) > budget) --ns;
+  const size_t smem = msweep_smem_bytes(L, mode, c->g.nvx, ns, trip != nullptr);
   if (smem > budget) return fail("msweep: ring does not fit");
   const double fbytes = 8.0 * (double)a.plane * a.nx * nwin;
   ProfScope ps(c, st, 2, (in ? fbytes : 0.0) + (out ? fbytes : 0.0), n);
@@ -1015,6 +1025,24 @@ int run_msweep(pbgk_ctx* c, int L, const double* in, double* out, const double* 
   if (nwin > 1) grid = std::max(1, grid / nwin);
   CK(launch_msweep(L, mode, *map, a, grid, nwin, ns, smem, st));
   return 0;
+}
+
+// The per-row factors of S steps of g windows into d_trip (see msweep.cu
+// ms_prep_kernel); dts[s * dts_g + window] on the device.  Returns the
+// window stride (doubles), 0 when switched off (PBGK_MS_NOPRE: A/B and test
+// knob, read per call), -1 on error.
+long long ms_prep(pbgk_ctx* c, int g, const double* T, long long t_ws, int S, const double* d_dts, int dts_g,
+                  bool lift0, cudaStream_t st) {
+  if (getenv("PBGK_MS_NOPRE") != nullptr || S <= 0) return 0;
+  const long long ws = (long long)S * c->g.nx * c->g.nvx * 4;
+  if (ensure_dev(c->d_trip, c->trip_cap, (size_t)g * ws, st)) return -1;
+  ProfScope ps(c, st, 3, 0.0);
+  if (launch_ms_prep(T, t_ws, (long long)c->g.nx * c->TL, c->TL, c->gxo, c->d_c[0], d_dts, dts_g, c->dx, S,
+                     c->g.nx, c->g.nvx, lift0 ? 1 : 0, c->d_trip, ws, g, st) != cudaSuccess) {
+    fail("ms_prep launch");
+    return -1;
+  }
+  return ws;
 }
 
 // The passes and the projection of a batch of g windows with S steps each
@@ -1030,6 +1058,9 @@ int ms_windows_batched(pbgk_ctx* c, int L, int g, const double* T, long long t_w
   if (P > 2 && ensure_dev(c->d_fb[1], c->fb_cap[1], (size_t)g * fw, st)) return -1;
   const double* in = nullptr;
   int wcount = 0;
+  const long long trip_ws = ms_prep(c, g, T, t_ws, S, d_dts, g, true, st);
+  if (trip_ws < 0) return -1;
+  const size_t lstride = (size_t)c->g.nx * c->g.nvx * 4;
   for (int s0 = 0; s0 < S;) {
     const int n = std::min(L, S - s0);
     const bool last = s0 + n == S;
@@ -1039,7 +1070,7 @@ int ms_windows_batched(pbgk_ctx* c, int L, int g, const double* T, long long t_w
     double* out = last ? nullptr : c->d_fb[(wcount++) & 1];
     MsBatch mb{g, t_ws, errw, d_dts, s0};
     if (run_msweep(c, L, in, out, tabs, last ? T + (size_t)S * tstep : nullptr, dtdx, n, s0 + 1, st, nullptr, 0,
-                   &mb))
+                   &mb, trip_ws > 0 ? c->d_trip + s0 * lstride : nullptr, trip_ws))
       return -1;
     in = out;
     s0 += n;
@@ -1063,8 +1094,17 @@ int ms_windows_batched(pbgk_ctx* c, int L, int g, const double* T, long long t_w
 // when write_final; mom_out (may be null) gets P(f_S).
 int ms_window(pbgk_ctx* c, int L, const double* f0, double* f_out, double* f_tmp, int write_final,
               double* mom_out, const double* T, int S, const double* h_dts, cudaStream_t st,
-              const unsigned* prog = nullptr, unsigned base = 0) {
+              const unsigned* prog = nullptr, unsigned base = 0, const double* d_dts = nullptr,
+              int dts_g = 1) {
   const size_t tstep = (size_t)c->g.nx * c->TL;
+  // the per-row factors of every step, once per window (not with a concurrent
+  // recursion: its tables arrive pass by pass)
+  long long trip_ws = 0;
+  if (prog == nullptr && d_dts != nullptr) {
+    trip_ws = ms_prep(c, 1, T, 0, S, d_dts, dts_g, f0 == nullptr, st);
+    if (trip_ws < 0) return -1;
+  }
+  const size_t lstride = (size_t)c->g.nx * c->g.nvx * 4;
   const int P = (S + L - 1) / L;
   const int W = P - 1 + (write_final ? 1 : 0);
   auto buf = [&](int w) { return ((W - w) % 2 == 0) ? f_out : f_tmp; };
@@ -1081,7 +1121,8 @@ int ms_window(pbgk_ctx* c, int L, const double* f0, double* f_out, double* f_tmp
     }
     double* out = (!last || write_final) ? buf(++wcount) : nullptr;
     if (run_msweep(c, L, in, out, tabs, last ? T + (size_t)S * tstep : nullptr, dtdx, n, s0 + 1, st, prog,
-                   base + (unsigned)(last ? S : s0 + n - 1)))
+                   base + (unsigned)(last ? S : s0 + n - 1), nullptr,
+                   trip_ws > 0 ? c->d_trip + s0 * lstride : nullptr, 0))
       return -1;
     in = out;
     s0 += n;
@@ -1302,7 +1343,7 @@ int propagate_body_fused(pbgk_ctx* c, const double* f0, const double* mom0, doub
   int rc = 0;
   const int LM = field ? 0 : ms_levels(c);
   if (LM > 0) {
-    rc = ms_window(c, LM, f0, f_out, f_tmp, write_final, mom_out, T, S, h_dts, st, prog, base);
+    rc = ms_window(c, LM, f0, f_out, f_tmp, write_final, mom_out, T, S, h_dts, st, prog, base, c->d_bdts, 1);
   } else {
     int w = 0;
     bool projected = false;
@@ -1520,7 +1561,8 @@ int windows_fused(pbgk_ctx* c, int nwin, const double* mom_in, double* mom_out, 
       const double* T = c->d_bt + k * t_ws;
       c->err_slot = c->d_keys + w;
       if (LM > 0) {
-        const int rc = ms_window(c, LM, nullptr, f_a, f_b, 0, mom_out + w * m5, T, S, h_dts + off[w], st);
+        const int rc = ms_window(c, LM, nullptr, f_a, f_b, 0, mom_out + w * m5, T, S, h_dts + off[w], st,
+                                 nullptr, 0, c->d_bdts + k, g);
         c->err_slot = nullptr;
         if (rc) return -1;
         continue;

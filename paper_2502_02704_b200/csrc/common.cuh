@@ -133,6 +133,11 @@ struct MSweepArgs {
   const double* dts;
   int dts_g, s0;
   double dx;
+  // per-row factors (ls gxa, keep r, a r, -) of level l and cell i at
+  // trip + l trip_ls + i 4 nvx (+ window trip_ws), precomputed once per window
+  // (ms_prep_kernel); null: the kernel forms them from the tables and dtdx
+  const double* trip;
+  long long trip_ls, trip_ws;
 };
 
 // Multi-step sweep with the v_x field term (esweep.cu): up to kMaxLevels

@@ -47,6 +47,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <type_traits>
 
 #include "common.cuh"
@@ -77,6 +78,10 @@ constexpr int NTG = 32 * NW;
 constexpr int NTHR = 2 * NTG;
 constexpr int BY = 8;     // v_y lines per box row
 constexpr int TS = 2 + A + BY + BZ;  // table slice (doubles): r, ls | gxa rows | g_y | g_z
+// PRE: (ls gxa, keep r, a r, -) per box row | g_y | g_z -- the per-row factors
+// of every (cell, step) precomputed once per window (ms_prep_kernel)
+constexpr int TSP = 4 * A + BY + BZ;
+__host__ __device__ constexpr int slice_doubles(bool pre) { return pre ? TSP : TS; }
 }  // namespace ms
 
 enum MsMode : int { kMsSynth = 1, kMsFinal = 2 };
@@ -159,10 +164,11 @@ __device__ __forceinline__ void reg_dec() {
   asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
 }
 
-template <int L, int MODE, int P, int NG>
+template <int L, int MODE, int P, int NG, bool PRE>
 __global__ void __launch_bounds__(kMsThreads, NG == 1 ? 2 : 1)
     msweep_kernel(const __grid_constant__ CUtensorMap fmap, const MSweepArgs a, int ns) {
   using namespace ms;
+  constexpr int TS = slice_doubles(PRE);  // (shadows ms::TS) doubles per level slice of a stage
   constexpr bool SYNTH = (MODE & kMsSynth) != 0;
   constexpr bool FINAL = (MODE & kMsFinal) != 0;
   constexpr bool LW = kMsLW && NG == 2;
@@ -198,8 +204,10 @@ __global__ void __launch_bounds__(kMsThreads, NG == 1 ? 2 : 1)
   constexpr int REC = A + BY + BZ;
   constexpr int RS = 1 + BY + BZ;             // per-warp partial block (FINAL)
   constexpr int FR = 8;                       // FINAL records reduced per barrier
-  constexpr int NCH = (2 + A + BY + BZ) / 2;  // 16-byte chunks of one table slice
-  constexpr int CPT = (P * NTAB * NCH + NLD - 1) / NLD;  // chunks per loader thread
+  constexpr int NCH = (2 + A + BY + BZ) / 2;  // 16-byte chunks of one plain table slice (R_S; every level without PRE)
+  constexpr int NCHP = PRE ? TSP / 2 : NCH;   // chunks of one level slice
+  constexpr int NCHT = L * NCHP + (FINAL ? NCH : 0);  // chunks of one plane
+  constexpr int CPT = (P * NCHT + NLD - 1) / NLD;  // chunks per loader thread
   extern __shared__ __align__(128) unsigned char smem[];
 
   const Tiling& T = a.t;
@@ -211,8 +219,8 @@ __global__ void __launch_bounds__(kMsThreads, NG == 1 ? 2 : 1)
   double* const part = a.part != nullptr ? a.part + (size_t)win * a.p_ws : nullptr;
   ErrKey* const errp = a.errw != nullptr ? a.errw + win : a.err;
   const int nlev = a.nlev;
-  double* AK = reinterpret_cast<double*>(smem + (size_t)ns * STAGEB);     // [nvx][L] a = (dt/dx)|c_x|
-  double* RB = reinterpret_cast<double*>(AK + L * nvx * (PBGK_MS_AONLY ? 1 : 2));                    // FINAL: [2][FR][NW][RS]
+  double* AK = reinterpret_cast<double*>(smem + (size_t)ns * STAGEB);     // [nvx][L] a = (dt/dx)|c_x| (not PRE)
+  double* RB = reinterpret_cast<double*>(AK + (PRE ? 0 : L * nvx * (PBGK_MS_AONLY ? 1 : 2)));  // FINAL: [2][FR][NW][RS]
   long long* RI = reinterpret_cast<long long*>(RB + (FINAL ? 2 * FR * NW * RS : 0));  // [2][FR]
   uint64_t* full = reinterpret_cast<uint64_t*>(RI + (FINAL ? 2 * FR : 0));
   uint64_t* mid = full + ns;
@@ -223,7 +231,7 @@ __global__ void __launch_bounds__(kMsThreads, NG == 1 ? 2 : 1)
 
   // transport coefficients per (row, level): a = (dt/dx) |c_x|, keep = 1 - a
   // (up rows: f* = (1-a) f + a f_{i-1}; down rows: (1-a) f + a f_{i+1})
-  for (int j = tid; j < L * nvx; j += NTHR_K) {
+  for (int j = tid; j < (PRE ? 0 : L * nvx); j += NTHR_K) {
     const int jx = j / L, l = j - jx * L;
     const double c = a.cx[jx];
     const double dtl = a.dts == nullptr ? a.dtdx[l] : (l < nlev ? a.dts[(size_t)(a.s0 + l) * a.dts_g + win] / a.dx : 0.0);
@@ -288,31 +296,38 @@ __global__ void __launch_bounds__(kMsThreads, NG == 1 ? 2 : 1)
       const int l = BASE + ll;
       if (!FULLC && (l >= nlev || l > depth)) break;
       const double* S = tabs + l * TS;
-      const double2 rl = *reinterpret_cast<const double2*>(S);  // r, ls
-      const double gxa = S[2 + w];
-#if PBGK_MS_GYASM
-      const double gy[2] = {lds_f64(S + 2 + A + yl), lds_f64(S + 2 + A + yl + 1)};
-      const double gz[2] = {lds_f64(S + 2 + A + BY + zo), lds_f64(S + 2 + A + BY + zo + ZS)};
-#else
-      const double2 gyp = *reinterpret_cast<const double2*>(S + 2 + A + yl);  // uniform per quarter warp
-      const double gy[2] = {gyp.x, gyp.y};
-      const double gz[2] = {S[2 + A + BY + zo], S[2 + A + BY + zo + ZS]};
-#endif
-#if PBGK_MS_AONLY
-      const double av = AKr[l];
-#else
-      const double2 ak = reinterpret_cast<const double2*>(AKr)[l];
-#endif
-      const double W = rl.y * gxa;  // ls gxa
       const bool lift0 = SYNTH && l == 0;
-      // (a r, (1 - a) r) as a r and r - a r
+      double W, kr, ar;
+      double gy[2], gz[2];
+      if constexpr (PRE) {
+        // (ls gxa, keep r, a r) of this row, cell and level from the window's table
+        const double2 wk2 = *reinterpret_cast<const double2*>(S + 4 * w);
+        W = wk2.x;
+        kr = wk2.y;
+        ar = S[4 * w + 2];
+        gy[0] = lds_f64(S + 4 * A + yl);
+        gy[1] = lds_f64(S + 4 * A + yl + 1);
+        gz[0] = lds_f64(S + 4 * A + BY + zo);
+        gz[1] = lds_f64(S + 4 * A + BY + zo + ZS);
+      } else {
+        const double2 rl = *reinterpret_cast<const double2*>(S);  // r, ls
+        const double gxa = S[2 + w];
+        gy[0] = lds_f64(S + 2 + A + yl);
+        gy[1] = lds_f64(S + 2 + A + yl + 1);
+        gz[0] = lds_f64(S + 2 + A + BY + zo);
+        gz[1] = lds_f64(S + 2 + A + BY + zo + ZS);
 #if PBGK_MS_AONLY
-      const double ar = lift0 ? av : av * rl.x;
-      const double kr = (lift0 ? 1.0 : rl.x) - ar;
+        const double av = AKr[l];
+        // (a r, (1 - a) r) as a r and r - a r
+        ar = lift0 ? av : av * rl.x;
+        kr = (lift0 ? 1.0 : rl.x) - ar;
 #else
-      const double kr = lift0 ? ak.x : ak.x * rl.x;
-      const double ar = lift0 ? ak.y : ak.y * rl.x;
+        const double2 ak = reinterpret_cast<const double2*>(AKr)[l];
+        kr = lift0 ? ak.x : ak.x * rl.x;
+        ar = lift0 ? ak.y : ak.y * rl.x;
 #endif
+        W = rl.y * gxa;  // ls gxa
+      }
       if (FULLC || l < depth) {
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
@@ -476,17 +491,40 @@ __global__ void __launch_bounds__(kMsThreads, NG == 1 ? 2 : 1)
     // plane row added per item
     const double* cptr[CPT];
     int cdst[CPT], cpl[CPT];
+    bool crow[CPT];  // a row chunk of the window's per-row table (cell stride 4 nvx, else TL)
     auto decode = [&](const TileGeom& tg) {
 #pragma unroll
       for (int r = 0; r < CPT; ++r) {
         const int j = lid + r * NLD;
+        const bool inr = j < P * NCHT;
+        const int pl = inr ? j / NCHT : 0;
+        const int jj = inr ? j - pl * NCHT : 0;
+        const bool rslot = FINAL && jj >= L * NCHP;  // the R_S slice (plain layout)
         // (the R_S slice is loaded only when f_S is stored)
-        const bool ok = j < P * NTAB * NCH && !(FINAL && fout == nullptr && (j % (NTAB * NCH)) / NCH == L);
-        const int pl = ok ? j / (NTAB * NCH) : 0;
-        const int jj = ok ? j - pl * NTAB * NCH : 0;
-        const int l = jj / NCH, c = jj - l * NCH;
+        const bool ok = inr && !(rslot && fout == nullptr);
+        const int l = rslot ? L : jj / NCHP;
+        const int c = rslot ? jj - L * NCHP : jj - l * NCHP;
+        const double* base = rslot ? a.tabR : a.tab[l < L ? l : 0];
+        size_t wso = (size_t)win * a.t_ws;  // the window's tables
         int so, dof;
-        if (c == 0) {
+        bool rowc = false;
+        if (PRE && !rslot) {
+          if (c < 2 * A) {
+            // a box row's (ls gxa, keep r | a r, -) from the window's row table;
+            // levels the pass does not run read the last one's rows (unused)
+            const int lc = l < nlev ? l : nlev - 1;
+            base = a.trip + (size_t)lc * a.trip_ls;
+            wso = (size_t)win * a.trip_ws;
+            so = (tg.r0 + (c >> 1)) * 4 + 2 * (c & 1); dof = 2 * c;
+            rowc = true;
+          } else if (c < 2 * A + BY / 2) {
+            const int q = c - 2 * A;
+            so = a.gyo + tg.y0 + 2 * q; dof = 4 * A + 2 * q;
+          } else {
+            const int q = c - 2 * A - BY / 2;
+            so = a.gzo + tg.z0 + 2 * q; dof = 4 * A + BY + 2 * q;
+          }
+        } else if (c == 0) {
           so = 0; dof = 0;
         } else if (c <= A / 2) {
           so = a.gxo + tg.r0 + 2 * (c - 1); dof = 2 + 2 * (c - 1);
@@ -498,7 +536,8 @@ __global__ void __launch_bounds__(kMsThreads, NG == 1 ? 2 : 1)
           so = a.gzo + tg.z0 + 2 * q; dof = 2 + A + BY + 2 * q;
         }
         cpl[r] = ok ? pl : -1;
-        cptr[r] = ((FINAL && l == L) ? a.tabR : a.tab[l < L ? l : 0]) + (size_t)win * a.t_ws + so;
+        cptr[r] = base + wso + so;
+        crow[r] = rowc;
         cdst[r] = (int)(pl * (PLB / 8) + BOXB / 8) + l * TS + dof;
       }
     };
@@ -574,10 +613,11 @@ __global__ void __launch_bounds__(kMsThreads, NG == 1 ? 2 : 1)
           for (int q = 0; q < P; ++q)
             if (pl == q) i = ip[q];
           if (i >= 0) {
+            const double* src = cptr[r] + ((PRE && crow[r]) ? (size_t)i * (4 * nvx) : (size_t)i * a.TL);
             if (PBGK_MS_HINT >= 1)
-              cp_async_16_hint(reinterpret_cast<double*>(st) + cdst[r], cptr[r] + (size_t)i * a.TL, pol_keep);
+              cp_async_16_hint(reinterpret_cast<double*>(st) + cdst[r], src, pol_keep);
             else
-              cp_async_16(reinterpret_cast<double*>(st) + cdst[r], cptr[r] + (size_t)i * a.TL);
+              cp_async_16(reinterpret_cast<double*>(st) + cdst[r], src);
           }
         }
       }
@@ -708,13 +748,54 @@ __global__ void __launch_bounds__(kMsThreads, NG == 1 ? 2 : 1)
 #define PBGK_MS_P 1
 #endif
 
-size_t msweep_smem_bytes(int L, int mode, int nvx, int ns) {
+size_t msweep_smem_bytes(int L, int mode, int nvx, int ns, bool pre) {
   const bool fin = mode & kMsFinal;
   const size_t box = (size_t)ms::A * ms::BY * ms::BZ * 8;
-  const size_t stage = PBGK_MS_P * (((box + (size_t)(L + (fin ? 1 : 0)) * ms::TS * 8 + 127) & ~(size_t)127) +
-                                    (PBGK_MS_NG == 2 ? box : 0));
-  return (size_t)ns * stage + (size_t)L * nvx * 16 +
+  const size_t stage =
+      PBGK_MS_P * (((box + (size_t)(L + (fin ? 1 : 0)) * ms::slice_doubles(pre) * 8 + 127) & ~(size_t)127) +
+                   (PBGK_MS_NG == 2 ? box : 0));
+  return (size_t)ns * stage + (pre ? 0 : (size_t)L * nvx * 16) +
          (fin ? 2 * 8 * ms::NW * (1 + ms::BY + ms::BZ) * 8 + 2 * 8 * 8 : 0) + (size_t)3 * ns * 8;
+}
+
+// The per-row factors of every (window, step, cell): W = ls gxa, keep r =
+// r - a r, a r with a = (dt_s / dx) |c_x| (ref/kinetic.py:110-112,130-134, the
+// pass kernel's re-association, the same rounded operations); step 0 of a
+// window from moments is the lift (keep = 1 - a, a; no r).  One thread per
+// (step, cell, row); grid.z = window.
+__global__ void __launch_bounds__(256)
+    ms_prep_kernel(const double* T, long long t_ws, long long tstep, int TL, int gxo, const double* cx,
+                   const double* dts, int dts_g, double dx, int S, int nx, int nvx, int lift0, double* trip,
+                   long long trip_ws) {
+  pdl_wait();
+  pdl_trigger();
+  const int win = blockIdx.z;
+  const long long n = (long long)S * nx * nvx;
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (long long)gridDim.x * blockDim.x) {
+    const int row = (int)(j % nvx);
+    const long long sc = j / nvx;
+    const int cell = (int)(sc % nx), s = (int)(sc / nx);
+    const double* t = T + (size_t)win * t_ws + (size_t)s * tstep + (size_t)cell * TL;
+    const double r = __ldg(t), ls = __ldg(t + 1), gxa = __ldg(t + gxo + row);
+    const double c = cx[row];
+    const double av = __dmul_rn(__ddiv_rn(dts[(size_t)s * dts_g + win], dx), c < 0.0 ? -c : c);
+    const bool lift = lift0 && s == 0;
+    const double ar = lift ? av : __dmul_rn(av, r);
+    const double kr = __dsub_rn(lift ? 1.0 : r, ar);
+    double* o = trip + (size_t)win * trip_ws + (size_t)j * 4;
+    reinterpret_cast<double2*>(o)[0] = make_double2(__dmul_rn(ls, gxa), kr);
+    reinterpret_cast<double2*>(o)[1] = make_double2(ar, 0.0);
+  }
+}
+
+cudaError_t launch_ms_prep(const double* T, long long t_ws, long long tstep, int TL, int gxo, const double* cx,
+                           const double* dts, int dts_g, double dx, int S, int nx, int nvx, int lift0,
+                           double* trip, long long trip_ws, int nwin, cudaStream_t st) {
+  const long long n = (long long)S * nx * nvx;
+  const int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 8);
+  return launch_pdl_grid(ms_prep_kernel, dim3(blocks, 1, nwin), 256, 0, st, T, t_ws, tstep, TL, gxo, cx, dts,
+                         dts_g, dx, S, nx, nvx, lift0, trip, trip_ws);
 }
 
 int msweep_threads() { return kMsThreads; }
@@ -740,10 +821,10 @@ int msweep_tiling(int nvx, int nvy, int nvz, Tiling* t) {
   return 1;
 }
 
-template <int L, int MODE>
+template <int L, int MODE, bool PRE>
 static cudaError_t launch_ms(const CUtensorMap& map, const MSweepArgs& a, dim3 grid, int ns, size_t smem,
                              cudaStream_t st) {
-  auto fn = msweep_kernel<L, MODE, PBGK_MS_P, PBGK_MS_NG>;
+  auto fn = msweep_kernel<L, MODE, PBGK_MS_P, PBGK_MS_NG, PRE>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (a.prog != nullptr) {
@@ -753,14 +834,14 @@ static cudaError_t launch_ms(const CUtensorMap& map, const MSweepArgs& a, dim3 g
   return launch_pdl_grid(fn, grid, kMsThreads, smem, st, map, a, ns);
 }
 
-template <int L>
+template <int L, bool PRE>
 static cudaError_t launch_ms_mode(int mode, const CUtensorMap& map, const MSweepArgs& a, dim3 grid, int ns,
                                   size_t smem, cudaStream_t st) {
   switch (mode) {
-    case 0: return launch_ms<L, 0>(map, a, grid, ns, smem, st);
-    case kMsSynth: return launch_ms<L, kMsSynth>(map, a, grid, ns, smem, st);
-    case kMsFinal: return launch_ms<L, kMsFinal>(map, a, grid, ns, smem, st);
-    case kMsSynth | kMsFinal: return launch_ms<L, kMsSynth | kMsFinal>(map, a, grid, ns, smem, st);
+    case 0: return launch_ms<L, 0, PRE>(map, a, grid, ns, smem, st);
+    case kMsSynth: return launch_ms<L, kMsSynth, PRE>(map, a, grid, ns, smem, st);
+    case kMsFinal: return launch_ms<L, kMsFinal, PRE>(map, a, grid, ns, smem, st);
+    case kMsSynth | kMsFinal: return launch_ms<L, kMsSynth | kMsFinal, PRE>(map, a, grid, ns, smem, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -770,9 +851,14 @@ static cudaError_t launch_ms_mode(int mode, const CUtensorMap& map, const MSweep
 cudaError_t launch_msweep(int L, int mode, const CUtensorMap& map, const MSweepArgs& a, int grid_x, int nwin,
                           int ns, size_t smem, cudaStream_t st) {
   const dim3 grid(grid_x, nwin);
+  // a.trip: the per-row factors precomputed (ms_prep_kernel), else from the
+  // tables in the kernel (passes that wait on a concurrent recursion)
+  const bool pre = a.trip != nullptr;
   switch (L) {
-    case 4: return launch_ms_mode<4>(mode, map, a, grid, ns, smem, st);
-    case 8: return launch_ms_mode<8>(mode, map, a, grid, ns, smem, st);
+    case 4: return pre ? launch_ms_mode<4, true>(mode, map, a, grid, ns, smem, st)
+                       : launch_ms_mode<4, false>(mode, map, a, grid, ns, smem, st);
+    case 8: return pre ? launch_ms_mode<8, true>(mode, map, a, grid, ns, smem, st)
+                       : launch_ms_mode<8, false>(mode, map, a, grid, ns, smem, st);
   }
   return cudaErrorInvalidValue;
 }

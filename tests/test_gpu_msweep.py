@@ -343,3 +343,24 @@ def test_release_contexts_frees_and_recreates():
     assert P.release_contexts() >= 1
     _, m2, c2, _ = _window(g, "periodic", U, t1, 8)  # a fresh context
     assert c1 == c2 == -1 and np.array_equal(m1, m2)
+
+
+@pytest.mark.parametrize("levels", LEVELS)
+@pytest.mark.parametrize("bc", BCS)
+def test_precomputed_row_factors_are_bitwise_the_in_kernel_ones(levels, bc, monkeypatch):
+    # the per-row factors (ls gxa, keep r, a r) of every step come from a small
+    # kernel once per window (msweep.cu ms_prep_kernel) or, with PBGK_MS_NOPRE
+    # and under a concurrent recursion, are formed in the pass kernel: the same
+    # rounded operations, so f_S and P(f_S) agree bit for bit (19 steps: a
+    # ragged last pass; from moments and from a given f0)
+    g, mesh = _grids(9, (32, 16, 48), 7.0)
+    U = random_moments(9, np.random.default_rng(77))
+    t1 = 18.5 * O.fine_cap(mesh, 0.5, None)
+    f_a, m_a, c_a, _ = _window(g, bc, U, t1, levels)
+    g0, _ = _from_f0(g, bc, f_a * 1.0, 6.5 * O.fine_cap(mesh, 0.5, None), levels)
+    monkeypatch.setenv("PBGK_MS_NOPRE", "1")
+    f_b, m_b, c_b, _ = _window(g, bc, U, t1, levels)
+    g1, _ = _from_f0(g, bc, f_a * 1.0, 6.5 * O.fine_cap(mesh, 0.5, None), levels)
+    monkeypatch.delenv("PBGK_MS_NOPRE")
+    assert c_a == c_b == -1
+    assert np.array_equal(f_a, f_b) and np.array_equal(m_a, m_b) and np.array_equal(g0, g1)
