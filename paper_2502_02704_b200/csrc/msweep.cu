@@ -58,8 +58,11 @@
 #ifndef PBGK_MS_ZSPLIT
 #define PBGK_MS_ZSPLIT 0
 #endif
+#ifndef PBGK_MS_STHINT
+#define PBGK_MS_STHINT 1
+#endif
 #ifndef PBGK_MS_HINT
-#define PBGK_MS_HINT 1
+#define PBGK_MS_HINT 2
 #endif
 #ifndef PBGK_MS_GYASM
 #define PBGK_MS_GYASM 1
@@ -423,6 +426,7 @@ __global__ void __launch_bounds__(kMsThreads, NG == 1 ? 2 : 1)
   };
   // the pass's last level of a run plane: R_S (FINAL), the store, the
   // partial records (FINAL) or the finiteness sum
+  const uint64_t pol_out = (PBGK_MS_STHINT && (NG == 1 || grp == 1)) ? make_policy_evict_first() : 0;
   auto emit = [&](double (&x)[2][2], const double* tabs, int i, int t, long long goff) {
     if (FINAL && fout != nullptr) {
       // R_S (ref/kinetic.py:130-134) of the last level's output, when f_S is
@@ -443,8 +447,13 @@ __global__ void __launch_bounds__(kMsThreads, NG == 1 ? 2 : 1)
       double* d = fout + (size_t)i * a.plane + goff;
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
-        d[(size_t)k * a.nvz] = x[k][0];
-        d[(size_t)k * a.nvz + ZS] = x[k][1];
+        if (PBGK_MS_STHINT) {
+          // f streams out: its lines leave L2 first (the table rows stay)
+          st_global_v2_hint(d + (size_t)k * a.nvz, x[k][0], x[k][1], pol_out);
+        } else {
+          d[(size_t)k * a.nvz] = x[k][0];
+          d[(size_t)k * a.nvz + ZS] = x[k][1];
+        }
       }
     }
     if constexpr (FINAL) {
