@@ -189,11 +189,14 @@ __global__ void __launch_bounds__(kMsThreads, NG == 1 ? 2 : 1)
 #ifndef PBGK_MS_LAF
 #define PBGK_MS_LAF 4
 #endif
+#ifndef PBGK_MS_LAFW
+#define PBGK_MS_LAFW 6  // FINAL with the loader warpgroup: group 1 also reduces (window passes 7.70 ms at 5 + 3, 7.61 at 6 + 2, 7.57 at 7 + 1 with spills)
+#endif
   // FINAL: group 1 also applies R_S and reduces the partial records, so it
   // takes one level fewer (4 + 4)
   constexpr int LA = NG == 1 ? L
                              : (PBGK_MS_LA > 0 && PBGK_MS_LA < L ? PBGK_MS_LA
-                                                                 : (L == 8 ? (LW ? 5 : (FINAL ? PBGK_MS_LAF : 3)) : L / 2));
+                                                                 : (L == 8 ? (LW ? (FINAL ? PBGK_MS_LAFW : 5) : (FINAL ? PBGK_MS_LAF : 3)) : L / 2));
   constexpr int LH = LA > L - LA ? LA : L - LA;
   constexpr int NTHR_K = NG * NTG + (LW ? kMsLoaders : 0);
   constexpr int NTAB = L + (FINAL ? 1 : 0);
